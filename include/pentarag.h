@@ -1,0 +1,149 @@
+/*
+ * pentarag.h — C ABI of the B200-native PentaRAG fast-routing hot path
+ * (libpentarag.so, built from paper_2506_21593_b200/csrc).
+ *
+ * Plain pointers and sizes only: no torch, no C++ types.  Every `d_` pointer
+ * is DEVICE memory owned by the caller; every call is ordered on the caller's
+ * `stream` (a cudaStream_t passed as void*, NULL = legacy default stream).
+ * Store buffers (the rows behind an index, the KV slot table) are owned by
+ * the library and released by the matching *_destroy call.
+ *
+ * Each entry point names the reference interface it replaces; reference
+ * paths are relative to /root/reference/pkg/src/ragcascade/.  The Python
+ * host layer (paper_2506_21593_b200/) binds these with ctypes and keeps the
+ * reference's duck-typed surface (FlatIndex, FixedKVCache, SemanticCache,
+ * MainKnowledgeBase, AdaptiveKnowledgeMemory, CascadeRouter).
+ *
+ * Errors: every int-returning function returns PR_OK (0) or a negative
+ * status; pr_last_error() gives a thread-local message.  The host layer maps
+ * statuses onto the reference exceptions (errors.py:10-130).  No C++
+ * exception crosses this boundary.  Handles are not thread-safe: the host
+ * layer serialises calls per handle, as the reference serialises per index
+ * (index.py:80 RLock).
+ */
+#ifndef PENTARAG_H
+#define PENTARAG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------ */
+#define PR_OK 0
+#define PR_ERR_BAD_ARG (-1)        /* ValueError (index.py:161-162, knowledge.py:77-80) */
+#define PR_ERR_INVALID_VECTOR (-2) /* InvalidVector (errors.py:34-37) */
+#define PR_ERR_EMPTY (-3)          /* EmptyKnowledgeBase (errors.py:46-49) */
+#define PR_ERR_CUDA (-4)           /* CUDA runtime/driver failure */
+#define PR_ERR_NOMEM (-5)          /* device allocation failed */
+#define PR_ERR_UNSUPPORTED (-6)    /* not built for / not running on sm_100a */
+
+/* ---- search modes ------------------------------------------------------ */
+#define PR_SEARCH_AUTO 0   /* tensor-core scan when eligible, else exact  */
+#define PR_SEARCH_EXACT 1  /* fp64 einsum-order scan of every row          */
+#define PR_SEARCH_TENSOR 2 /* tcgen05 fp16 scan + certified fp64 rescoring */
+
+typedef struct pr_index pr_index;
+typedef struct pr_kv pr_kv;
+
+/* Per-call counters of the last pr_index_search on a handle (host-side copy;
+ * reading them synchronises the handle's last search stream). */
+typedef struct pr_search_stats {
+    int64_t queries;        /* queries in the call                              */
+    int64_t tensor_queries; /* went through the tcgen05 scan                    */
+    int64_t fallback;       /* failed the certificate -> exact fp64 rescan      */
+    int64_t candidates;     /* rows rescored in fp64 after the tensor scan      */
+    int32_t nsplit;         /* row splits used by the scan grid                 */
+    int32_t path;           /* PR_SEARCH_EXACT or PR_SEARCH_TENSOR              */
+} pr_search_stats;
+
+/* ---- library ------------------------------------------------------------ */
+const char *pr_last_error(void);
+int pr_abi_version(void);
+/* Device properties of the current device; fails with PR_ERR_UNSUPPORTED if
+ * it is not compute capability 10.0 (the only target this library is built for). */
+int pr_device_info(int *sm_count, int *cc_major, int *cc_minor);
+
+/* ---- vector contract: index.py:58-70 (_coerce_vector), embedding.py:52-67 -
+ * d_bad[i] = 1 if row i has a NaN/Inf or | ||v||_2 - 1 | > tol (fp64 norm). */
+int pr_check_unit(const float *d_vecs, int64_t n, int dim, double tol, uint8_t *d_bad, void *stream);
+
+/* ---- flat index store: index.py:73-153 (FlatIndex storage, insert/extend) --
+ * Rows are kept twice: fp32 (the exact copy every score is computed from, as
+ * _vectors32/_vectors64 at index.py:82-83,144-145) and fp16 (the tensor-core
+ * scan copy).  Row i is the i-th inserted entry id, so row order is the
+ * reference's insertion (tie-break) order. */
+int pr_index_create(int dim, int64_t capacity, uint32_t flags, pr_index **out);
+int pr_index_destroy(pr_index *h);
+int64_t pr_index_count(const pr_index *h);
+int pr_index_dim(const pr_index *h);
+int pr_index_reserve(pr_index *h, int64_t capacity, void *stream);
+/* append n rows (d_vecs is [n, dim] fp32, row-major) — a new entry id (index.py:134-141) */
+int pr_index_append(pr_index *h, const float *d_vecs, int64_t n, void *stream);
+/* overwrite rows in place — an existing entry id keeps its row (index.py:142-145) */
+int pr_index_update_rows(pr_index *h, const int64_t *d_rows, const float *d_vecs, int64_t n, void *stream);
+/* FlatIndex.clear (index.py:191-196): forget every row, keep the buffers */
+int pr_index_clear(pr_index *h);
+/* keep only the first n rows (used by rebuild-style eviction, caches.py:166-181) */
+int pr_index_truncate(pr_index *h, int64_t n);
+/* copy rows [row0, row0+n) out as fp32 [n, dim] (FlatIndex.vector, index.py:111-114) */
+int pr_index_read_rows(const pr_index *h, int64_t row0, int64_t n, float *d_out, void *stream);
+/* append rows gathered from another index with the same dim (AKM settle from
+ * KB rows, knowledge.py:217-228) */
+int pr_index_append_from(pr_index *h, const pr_index *src, const int64_t *d_src_rows, int64_t n, void *stream);
+
+/* ---- search: index.py:155-189 (FlatIndex.search) ------------------------
+ * For each of nq queries (d_q is [nq, dim] fp32): top-min(k, count) rows by
+ * (score desc, row asc), score = np.einsum("ij,j->i") in fp64 bit-for-bit.
+ *   d_rows     int64 [nq, k]  row index, -1 past d_count
+ *   d_raw      fp64  [nq, k]  einsum score (may be NULL)
+ *   d_reported fp64  [nq, k]  SearchHit.score: self-snap + clamp (may be NULL)
+ *   d_count    int32 [nq]     min(k, count)
+ * k must be >= 1 (PR_ERR_BAD_ARG otherwise). An empty index gives count 0. */
+int pr_index_search(pr_index *h, const float *d_q, int64_t nq, int k, uint32_t mode, int64_t *d_rows,
+                    double *d_raw, double *d_reported, int32_t *d_count, void *stream);
+int pr_index_last_stats(pr_index *h, pr_search_stats *out);
+
+/* Merge per-shard top-k lists into the global top-k (the NCCL all-gather
+ * merge of a row-sharded store).  d_rows/d_raw are [nshard, nq, k] with
+ * global row ids; d_count is [nshard, nq].  Output as pr_index_search, with
+ * d_snap [nshard, nq, k] (1 where the shard saw a bit-identical row) used to
+ * produce d_reported. */
+int pr_merge_shards(const int64_t *d_rows, const double *d_raw, const uint8_t *d_snap, const int32_t *d_count,
+                    int nshard, int64_t nq, int k, int64_t *d_out_rows, double *d_out_raw,
+                    double *d_out_reported, int32_t *d_out_count, void *stream);
+/* d_snap[q, j] = 1 iff row d_rows[q, j] of h is element-wise equal to query q
+ * and d_raw > 1 - 1e-6 (the self-snap predicate, index.py:180). */
+int pr_index_snap_flags(const pr_index *h, const float *d_q, int64_t nq, int k, const int64_t *d_rows,
+                        const double *d_raw, const int32_t *d_count, int64_t row_offset, uint8_t *d_snap,
+                        void *stream);
+
+/* ---- fixed KV cache: caches.py:45-101 (FixedKVCache) --------------------
+ * Keys are the UTF-8 bytes of the query text (byte-exact, caches.py:57-58);
+ * the table stores their 128-bit fingerprint (pr_fingerprint) in an
+ * open-addressing table of 64-byte buckets probed by 4-lane groups with
+ * 16-byte loads.  Values are int64 write sequence numbers: a larger value is
+ * a later write, so concurrent puts resolve last-write-wins (caches.py:67-74). */
+int pr_kv_create(int64_t capacity, pr_kv **out);
+int pr_kv_destroy(pr_kv *h);
+/* fingerprint n keys: bytes d_bytes[d_off[i] .. d_off[i+1]) -> d_fp[2i], d_fp[2i+1] */
+int pr_fingerprint(const uint8_t *d_bytes, const int64_t *d_off, int64_t n, uint64_t *d_fp, void *stream);
+void pr_fingerprint_host(const uint8_t *bytes, int64_t len, uint64_t out[2]);
+int pr_kv_put(pr_kv *h, const uint64_t *d_fp, const int64_t *d_vals, int64_t n, void *stream);
+/* d_vals[i] = value or -1; d_hit[i] = 1/0 (hit/miss, caches.py:57-65) */
+int pr_kv_get(pr_kv *h, const uint64_t *d_fp, int64_t n, int64_t *d_vals, uint8_t *d_hit, void *stream);
+/* fused fingerprint + probe over a text arena (the L1 probe of a routed batch) */
+int pr_kv_get_text(pr_kv *h, const uint8_t *d_bytes, const int64_t *d_off, int64_t n, int64_t *d_vals,
+                   uint8_t *d_hit, void *stream);
+int pr_kv_erase(pr_kv *h, const uint64_t *d_fp, int64_t n, void *stream);
+int pr_kv_clear(pr_kv *h, void *stream);
+int64_t pr_kv_size(pr_kv *h);      /* live keys (synchronises) */
+int64_t pr_kv_capacity(pr_kv *h);  /* slots */
+/* dump live (fingerprint, value) pairs; returns count written (<= max) or <0 */
+int64_t pr_kv_export(pr_kv *h, uint64_t *d_fp, int64_t *d_vals, int64_t max, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PENTARAG_H */

@@ -1,0 +1,818 @@
+// FlatIndex store + search orchestration (reference: index.py:73-189).
+//
+// Data layout in HBM (per index handle):
+//   x32  fp32 [cap, dp8]     exact copy, rows zero-padded to a multiple of 8
+//                            (einsum-order tail reads the padding as zeros)
+//   x16  fp16 [cap256, dp64] tensor-core scan copy, zero-padded to 64 columns
+//                            (one 128-byte swizzle atom per K block)
+// Row i == the i-th inserted id, so row order is the tie-break order.
+#include <cuda.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstring>
+#include <mutex>
+
+#include "common.cuh"
+#include "select.cuh"
+#include "tc_scan.cuh"
+
+namespace pr {
+
+// ---------------------------------------------------------------------------
+// errors
+static thread_local char g_err[1024] = "";
+void set_error(const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+const char *last_error() { return g_err; }
+
+int sm_count() {
+    static int cached = -1;
+    if (cached < 0) {
+        int dev = 0, v = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        cached = v > 0 ? v : 148;
+    }
+    return cached;
+}
+
+// ---------------------------------------------------------------------------
+// store kernels
+
+// fp32 [n, d] -> x32 rows (stride dp8) and x16 rows (stride dp64), zero padded.
+// rows == nullptr: destination row = row0 + i; else destination row = rows[i].
+__global__ void write_rows_kernel(const float *__restrict__ src, int64_t n, int d, const int64_t *__restrict__ rows,
+                                  int64_t row0, float *__restrict__ x32, int dp8, __half *__restrict__ x16,
+                                  int dp64) {
+    int64_t total = n * (int64_t)dp64;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = t / dp64;
+        int j = (int)(t - i * dp64);
+        float v = (j < d) ? src[i * d + j] : 0.0f;
+        int64_t r = rows ? rows[i] : row0 + i;
+        if (j < dp8) x32[r * dp8 + j] = v;
+        x16[r * dp64 + j] = __float2half_rn(v);
+    }
+}
+
+__global__ void gather_rows_kernel(const float *__restrict__ sx32, const __half *__restrict__ sx16,
+                                   const int64_t *__restrict__ src_rows, int64_t n, int dp8, int dp64,
+                                   int64_t row0, float *__restrict__ x32, __half *__restrict__ x16) {
+    int64_t total = n * (int64_t)dp64;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = t / dp64;
+        int j = (int)(t - i * dp64);
+        int64_t s = src_rows[i];
+        if (j < dp8) x32[(row0 + i) * dp8 + j] = sx32[s * dp8 + j];
+        x16[(row0 + i) * dp64 + j] = sx16[s * dp64 + j];
+    }
+}
+
+__global__ void read_rows_kernel(const float *__restrict__ x32, int dp8, int d, int64_t row0, int64_t n,
+                                 float *__restrict__ out) {
+    int64_t total = n * (int64_t)d;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = t / d;
+        int j = (int)(t - i * d);
+        out[t] = x32[(row0 + i) * dp8 + j];
+    }
+}
+
+// unit-norm + finiteness check, one warp per vector (index.py:63-69)
+__global__ void check_unit_kernel(const float *__restrict__ v, int64_t n, int d, double tol, uint8_t *__restrict__ bad) {
+    int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32;
+    int lane = threadIdx.x & 31;
+    if (w >= n) return;
+    const float *x = v + w * d;
+    double ss = 0.0;
+    int nonfinite = 0;
+    for (int j = lane; j < d; j += 32) {
+        float f = x[j];
+        if (!isfinite(f)) nonfinite = 1;
+        ss = fma((double)f, (double)f, ss);
+    }
+    for (int o = 16; o; o >>= 1) {
+        ss += __shfl_xor_sync(0xffffffffu, ss, o);
+        nonfinite |= __shfl_xor_sync(0xffffffffu, nonfinite, o);
+    }
+    if (lane == 0) bad[w] = (nonfinite || fabs(sqrt(ss) - 1.0) > tol) ? 1 : 0;
+}
+
+// queries fp32 [nq, d] -> [nq, dp8] fp32 (zero padded)
+__global__ void pad_queries_kernel(const float *__restrict__ q, int64_t nq, int d, int dp8, float *__restrict__ out) {
+    int64_t total = nq * (int64_t)dp8;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = t / dp8;
+        int j = (int)(t - i * dp8);
+        out[t] = j < d ? q[i * d + j] : 0.0f;
+    }
+}
+
+static int grid_for(int64_t total, int block = 256) {
+    int64_t g = (total + block - 1) / block;
+    int64_t cap = (int64_t)sm_count() * 16;
+    return (int)std::max<int64_t>(1, std::min(g, cap));
+}
+
+// ---------------------------------------------------------------------------
+// exact fp64 scan (numpy einsum order) with per-(query, split) top-K lists.
+//
+// One CTA = 256 threads = 256 consecutive rows per step, QT queries held in
+// shared memory as fp64.  Each thread reduces its row against all QT queries
+// (2*QT independent fp64 accumulation chains), scores go to shared memory,
+// then warp w keeps the top-K of queries w, w+8, ... in shared memory with a
+// warp-parallel sorted insert.  Persistent: CTAs loop over (query tile,
+// row split) work items; the number of selected queries may live on the
+// device (fallback lists), so no host sync is needed.
+struct ScanArgs {
+    const float *X;
+    int64_t n;
+    int xstride;  // dp8
+    int d;
+    const float *Q;  // padded fp32 queries [*, xstride]
+    const int32_t *qsel;
+    const int32_t *nsel_dev;
+    int32_t nsel_host;
+    int nsplit;
+    int64_t rows_per_split;
+    int K;
+    double *part_s;
+    int64_t *part_r;
+    int32_t *part_c;
+};
+
+constexpr int SCAN_THREADS = 256;
+
+template <int QT>
+__global__ void __launch_bounds__(SCAN_THREADS) exact_scan_kernel(ScanArgs p) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int qs_stride = p.xstride;
+    double *qs = reinterpret_cast<double *>(smem);         // [QT][xstride]
+    double *sc = qs + QT * qs_stride;                       // [QT][256]
+    double *tks = sc + QT * SCAN_THREADS;                   // [QT][K]
+    int64_t *tkr = reinterpret_cast<int64_t *>(tks + QT * p.K);  // [QT][K]
+    int *tkc = reinterpret_cast<int *>(tkr + QT * p.K);     // [QT]
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int nsel = p.nsel_dev ? *p.nsel_dev : p.nsel_host;
+    const int qtiles = (nsel + QT - 1) / QT;
+    const int64_t work = (int64_t)qtiles * p.nsplit;
+    const int d = p.d, K = p.K;
+
+    for (int64_t w = blockIdx.x; w < work; w += gridDim.x) {
+        const int qt = (int)(w / p.nsplit);
+        const int split = (int)(w - (int64_t)qt * p.nsplit);
+        const int64_t row_begin = (int64_t)split * p.rows_per_split;
+        const int64_t row_end = min(p.n, row_begin + p.rows_per_split);
+        __syncthreads();
+        for (int i = tid; i < QT * qs_stride; i += SCAN_THREADS) {
+            int qi = i / qs_stride, j = i - qi * qs_stride;
+            int sel = qt * QT + qi;
+            double v = 0.0;
+            if (sel < nsel) {
+                int qidx = p.qsel ? p.qsel[sel] : sel;
+                v = (double)p.Q[(int64_t)qidx * qs_stride + j];
+            }
+            qs[i] = v;
+        }
+        if (tid < QT) tkc[tid] = 0;
+        __syncthreads();
+
+        for (int64_t r0 = row_begin; r0 < row_end; r0 += SCAN_THREADS) {
+            const int64_t r = r0 + tid;
+            double acc0[QT], acc1[QT];
+#pragma unroll
+            for (int qi = 0; qi < QT; ++qi) acc0[qi] = acc1[qi] = 0.0;
+            if (r < row_end) {
+                const float *x = p.X + r * (int64_t)p.xstride;
+                int j = 0;
+                for (; j + 8 <= d; j += 8) {
+                    float4 xa = __ldg(reinterpret_cast<const float4 *>(x + j));
+                    float4 xb = __ldg(reinterpret_cast<const float4 *>(x + j + 4));
+                    const double x0 = xa.x, x1 = xa.y, x2 = xa.z, x3 = xa.w;
+                    const double x4 = xb.x, x5 = xb.y, x6 = xb.z, x7 = xb.w;
+#pragma unroll
+                    for (int qi = 0; qi < QT; ++qi) {
+                        const double2 *qq = reinterpret_cast<const double2 *>(qs + qi * qs_stride + j);
+                        const double2 q67 = qq[3], q45 = qq[2], q23 = qq[1], q01 = qq[0];
+                        acc0[qi] = fma(x6, q67.x, acc0[qi]);
+                        acc1[qi] = fma(x7, q67.y, acc1[qi]);
+                        acc0[qi] = fma(x4, q45.x, acc0[qi]);
+                        acc1[qi] = fma(x5, q45.y, acc1[qi]);
+                        acc0[qi] = fma(x2, q23.x, acc0[qi]);
+                        acc1[qi] = fma(x3, q23.y, acc1[qi]);
+                        acc0[qi] = fma(x0, q01.x, acc0[qi]);
+                        acc1[qi] = fma(x1, q01.y, acc1[qi]);
+                    }
+                }
+                for (; j < d; j += 2) {
+                    const double x0 = x[j], x1 = x[j + 1];
+#pragma unroll
+                    for (int qi = 0; qi < QT; ++qi) {
+                        acc0[qi] = fma(x0, qs[qi * qs_stride + j], acc0[qi]);
+                        acc1[qi] = fma(x1, qs[qi * qs_stride + j + 1], acc1[qi]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int qi = 0; qi < QT; ++qi)
+                sc[qi * SCAN_THREADS + tid] = (r < row_end) ? 0.0 + (acc0[qi] + acc1[qi]) : -INFINITY;
+            __syncthreads();
+
+            for (int qi = warp; qi < QT; qi += SCAN_THREADS / 32) {
+                if (qt * QT + qi >= nsel) break;
+                double *ls = tks + qi * K;
+                int64_t *lr = tkr + qi * K;
+                int cnt = tkc[qi];
+                for (int c = 0; c < SCAN_THREADS / 32; ++c) {
+                    const int64_t rr = r0 + c * 32 + lane;
+                    const double s = sc[qi * SCAN_THREADS + c * 32 + lane];
+                    const bool valid = rr < row_end;
+                    double thr = (cnt == K) ? ls[K - 1] : -INFINITY;
+                    unsigned m = __ballot_sync(0xffffffffu, valid && (cnt < K || s > thr));
+                    while (m) {
+                        const int src = __ffs(m) - 1;
+                        m &= m - 1;
+                        const double sv = __shfl_sync(0xffffffffu, s, src);
+                        const int64_t rv = r0 + c * 32 + src;
+                        if (cnt == K && !(sv > ls[K - 1])) continue;
+                        // rows arrive in ascending order: equal scores already in the
+                        // list rank first, so the insert position counts entries >= sv
+                        int pos = 0;
+                        for (int base = 0; base < cnt; base += 32) {
+                            int j = base + lane;
+                            pos += __popc(__ballot_sync(0xffffffffu, j < cnt && ls[j] >= sv));
+                        }
+                        const int last = min(cnt, K - 1);
+                        const int j0 = lane, j1 = lane + 32;
+                        const bool mv0 = j0 > pos && j0 <= last;
+                        const bool mv1 = j1 > pos && j1 <= last;
+                        double s0 = 0, s1 = 0;
+                        int64_t q0 = 0, q1 = 0;
+                        if (mv0) { s0 = ls[j0 - 1]; q0 = lr[j0 - 1]; }
+                        if (mv1) { s1 = ls[j1 - 1]; q1 = lr[j1 - 1]; }
+                        __syncwarp();
+                        if (mv0) { ls[j0] = s0; lr[j0] = q0; }
+                        if (mv1) { ls[j1] = s1; lr[j1] = q1; }
+                        if (lane == 0) { ls[pos] = sv; lr[pos] = rv; }
+                        __syncwarp();
+                        cnt = min(cnt + 1, K);
+                    }
+                }
+                if (lane == 0) tkc[qi] = cnt;
+                __syncwarp();
+            }
+            __syncthreads();
+        }
+
+        for (int qi = warp; qi < QT; qi += SCAN_THREADS / 32) {
+            const int sel = qt * QT + qi;
+            if (sel >= nsel) break;
+            const int cnt = tkc[qi];
+            const int64_t base = ((int64_t)sel * p.nsplit + split) * K;
+            for (int j = lane; j < K; j += 32) {
+                p.part_s[base + j] = j < cnt ? tks[qi * K + j] : -INFINITY;
+                p.part_r[base + j] = j < cnt ? tkr[qi * K + j] : -1;
+            }
+            if (lane == 0) p.part_c[(int64_t)sel * p.nsplit + split] = cnt;
+        }
+    }
+}
+
+static size_t scan_smem_bytes(int QT, int xstride, int K) {
+    return sizeof(double) * ((size_t)QT * xstride + (size_t)QT * SCAN_THREADS + (size_t)QT * K) +
+           sizeof(int64_t) * (size_t)QT * K + sizeof(int) * QT;
+}
+
+// ---------------------------------------------------------------------------
+// merge per-split lists -> final top-k, self-snap, clamp (index.py:176-185)
+struct MergeArgs {
+    const double *part_s;
+    const int64_t *part_r;
+    int nsplit;
+    int Kp;  // entries per split list
+    int k;
+    int64_t take;  // min(k, n)
+    const int32_t *qsel;
+    const int32_t *nsel_dev;
+    int32_t nsel_host;
+    const float *X;
+    int xstride;
+    int d;
+    const float *Q;  // padded queries [*, xstride]
+    int64_t *out_rows;
+    double *out_raw;
+    double *out_rep;
+    int32_t *out_count;
+};
+
+__global__ void __launch_bounds__(128) merge_topk_kernel(MergeArgs a) {
+    __shared__ double red_s[4];
+    __shared__ int64_t red_r[4];
+    const int nsel = a.nsel_dev ? *a.nsel_dev : a.nsel_host;
+    const int M = a.nsplit * a.Kp;
+    for (int sel = blockIdx.x; sel < nsel; sel += gridDim.x) {
+        const int qidx = a.qsel ? a.qsel[sel] : sel;
+        const double *ps = a.part_s + (int64_t)sel * M;
+        const int64_t *pr_ = a.part_r + (int64_t)sel * M;
+        const float *q = a.Q + (int64_t)qidx * a.xstride;
+        double last_s = INFINITY;
+        int64_t last_r = -1;
+        for (int j = 0; j < a.k; ++j) {
+            double bs = -INFINITY;
+            int64_t br = -1;
+            if (j < a.take) {
+                for (int e = threadIdx.x; e < M; e += blockDim.x) {
+                    int64_t r = pr_[e];
+                    if (r < 0) continue;
+                    double s = ps[e];
+                    bool after_last = (last_r < 0) || ranks_before(last_s, last_r, s, r);
+                    if (after_last && (br < 0 || ranks_before(s, r, bs, br))) { bs = s; br = r; }
+                }
+            }
+            block_best(bs, br, red_s, red_r);
+            const int64_t o = (int64_t)qidx * a.k + j;
+            if (br < 0) {
+                if (threadIdx.x == 0) {
+                    a.out_rows[o] = -1;
+                    if (a.out_raw) a.out_raw[o] = 0.0;
+                    if (a.out_rep) a.out_rep[o] = 0.0;
+                }
+                continue;
+            }
+            double rep;
+            finalize_hit(a.X, a.xstride, a.d, q, br, bs, &rep);
+            if (threadIdx.x == 0) {
+                a.out_rows[o] = br;
+                if (a.out_raw) a.out_raw[o] = bs;
+                if (a.out_rep) a.out_rep[o] = rep;
+            }
+            last_s = bs;
+            last_r = br;
+        }
+        if (threadIdx.x == 0) a.out_count[qidx] = (int32_t)a.take;
+    }
+}
+
+__global__ void empty_result_kernel(int64_t nq, int k, int64_t *rows, double *raw, double *rep, int32_t *count) {
+    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t < nq * k) {
+        rows[t] = -1;
+        if (raw) raw[t] = 0.0;
+        if (rep) rep[t] = 0.0;
+    }
+    if (t < nq) count[t] = 0;
+}
+
+
+// ---------------------------------------------------------------------------
+// row-sharded stores: per-shard snap flags + the all-gather merge
+__global__ void snap_flags_kernel(const float *__restrict__ x32, int dp8, int d, const float *__restrict__ q,
+                                  int64_t nq, int k, const int64_t *__restrict__ rows, const double *__restrict__ raw,
+                                  const int32_t *__restrict__ count, int64_t row_offset, uint8_t *__restrict__ snap) {
+    const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32;
+    const int lane = threadIdx.x & 31;
+    if (w >= nq * k) return;
+    const int64_t qi = w / k;
+    const int j = (int)(w - qi * k);
+    int eq = 0;
+    if (j < count[qi] && raw[w] > 1.0 - 1e-6) {
+        const float *x = x32 + (rows[w] - row_offset) * (int64_t)dp8;
+        const float *qq = q + qi * d;
+        int bad = 0;
+        for (int t = lane; t < d; t += 32) bad |= !(x[t] == qq[t]);
+        eq = !__any_sync(0xffffffffu, bad);
+    } else {
+        __syncwarp();
+    }
+    if (lane == 0) snap[w] = (uint8_t)eq;
+}
+
+__global__ void merge_shards_kernel(const int64_t *__restrict__ rows, const double *__restrict__ raw,
+                                    const uint8_t *__restrict__ snap, const int32_t *__restrict__ count, int nshard,
+                                    int64_t nq, int k, int64_t *out_rows, double *out_raw, double *out_rep,
+                                    int32_t *out_count) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
+        int pos[64];
+        int total = 0;
+        for (int s = 0; s < nshard; ++s) {
+            pos[s] = 0;
+            total += count[(int64_t)s * nq + q];
+        }
+        const int take = total < k ? total : k;
+        for (int j = 0; j < k; ++j) {
+            const int64_t o = q * k + j;
+            if (j >= take) {
+                out_rows[o] = -1;
+                if (out_raw) out_raw[o] = 0.0;
+                if (out_rep) out_rep[o] = 0.0;
+                continue;
+            }
+            int bs = -1;
+            double best_s = 0;
+            int64_t best_r = 0;
+            for (int s = 0; s < nshard; ++s) {
+                if (pos[s] >= count[(int64_t)s * nq + q]) continue;
+                const int64_t e = ((int64_t)s * nq + q) * k + pos[s];
+                if (bs < 0 || ranks_before(raw[e], rows[e], best_s, best_r)) {
+                    bs = s;
+                    best_s = raw[e];
+                    best_r = rows[e];
+                }
+            }
+            const int64_t e = ((int64_t)bs * nq + q) * k + pos[bs];
+            pos[bs]++;
+            out_rows[o] = best_r;
+            if (out_raw) out_raw[o] = best_s;
+            if (out_rep) out_rep[o] = (snap && snap[e]) ? 1.0 : fmax(-1.0, fmin(1.0, best_s));
+        }
+        out_count[q] = take;
+    }
+}
+}  // namespace pr
+
+// ===========================================================================
+// handle
+struct pr_index {
+    int dim = 0, dp8 = 0, dp64 = 0;
+    int64_t count = 0, cap = 0, cap256 = 0;
+    float *x32 = nullptr;
+    __half *x16 = nullptr;
+    pr::TcStoreMap tmap;  // TMA descriptor of x16 (rebuilt on reallocation)
+    bool tmap_ok = false;
+    pr_search_stats stats{};
+    // device scratch (grown on demand, stream-ordered)
+    void *scratch = nullptr;
+    size_t scratch_bytes = 0;
+    int32_t *d_counters = nullptr;  // [4]: fallback count, candidate count, ...
+    cudaStream_t last_stream = nullptr;
+};
+
+namespace pr {
+
+static int ensure_scratch(pr_index *h, size_t bytes, cudaStream_t st) {
+    if (h->scratch_bytes >= bytes) return PR_OK;
+    if (h->scratch) PR_CUDA(cudaFreeAsync(h->scratch, st));
+    h->scratch = nullptr;
+    h->scratch_bytes = 0;
+    size_t b = std::max(bytes, (size_t)(1 << 20));
+    PR_CUDA(cudaMallocAsync(&h->scratch, b, st));
+    h->scratch_bytes = b;
+    return PR_OK;
+}
+
+static int reserve(pr_index *h, int64_t cap, cudaStream_t st) {
+    if (cap <= h->cap) return PR_OK;
+    int64_t c = std::max<int64_t>(h->cap ? h->cap : 1024, 1024);
+    while (c < cap) c *= 2;
+    int64_t c256 = round_up<int64_t>(c, 256);
+    float *nx32 = nullptr;
+    __half *nx16 = nullptr;
+    PR_CUDA(cudaMalloc(&nx32, (size_t)c * h->dp8 * sizeof(float)));
+    cudaError_t e = cudaMalloc(&nx16, (size_t)c256 * h->dp64 * sizeof(__half));
+    if (e != cudaSuccess) {
+        cudaFree(nx32);
+        PR_FAIL(PR_ERR_NOMEM, "index reserve(%lld rows): %s", (long long)c, cudaGetErrorString(e));
+    }
+    PR_CUDA(cudaMemsetAsync(nx16, 0, (size_t)c256 * h->dp64 * sizeof(__half), st));
+    if (h->count > 0) {
+        PR_CUDA(cudaMemcpyAsync(nx32, h->x32, (size_t)h->count * h->dp8 * sizeof(float), cudaMemcpyDeviceToDevice, st));
+        PR_CUDA(cudaMemcpyAsync(nx16, h->x16, (size_t)h->count * h->dp64 * sizeof(__half), cudaMemcpyDeviceToDevice, st));
+    }
+    PR_CUDA(cudaStreamSynchronize(st));
+    if (h->x32) cudaFree(h->x32);
+    if (h->x16) cudaFree(h->x16);
+    h->x32 = nx32;
+    h->x16 = nx16;
+    h->cap = c;
+    h->cap256 = c256;
+    h->tmap_ok = false;
+    return PR_OK;
+}
+
+// ---------------------------------------------------------------------------
+// search orchestration
+
+constexpr int KMAX_EXACT = 64;
+
+static int pick_qt(int nsel, int xstride, int K) {
+    const size_t limit = 200 * 1024;
+    int qts[5] = {16, 8, 4, 2, 1};
+    for (int i = 0; i < 5; ++i) {
+        int qt = qts[i];
+        if (qt > 1 && nsel <= qt / 2) continue;  // don't pay for empty query slots
+        if (scan_smem_bytes(qt, xstride, K) <= limit) return qt;
+    }
+    return 1;
+}
+
+template <int QT>
+static int launch_scan_t(const ScanArgs &a, int grid, cudaStream_t st) {
+    size_t smem = scan_smem_bytes(QT, a.xstride, a.K);
+    static bool attr_set = false;
+    if (!attr_set) {
+        PR_CUDA(cudaFuncSetAttribute(exact_scan_kernel<QT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        attr_set = true;
+    }
+    exact_scan_kernel<QT><<<grid, SCAN_THREADS, smem, st>>>(a);
+    PR_LAUNCH_CHECK();
+    return PR_OK;
+}
+
+static int launch_scan(int QT, const ScanArgs &a, int grid, cudaStream_t st) {
+    switch (QT) {
+        case 16: return launch_scan_t<16>(a, grid, st);
+        case 8: return launch_scan_t<8>(a, grid, st);
+        case 4: return launch_scan_t<4>(a, grid, st);
+        case 2: return launch_scan_t<2>(a, grid, st);
+        default: return launch_scan_t<1>(a, grid, st);
+    }
+}
+
+static void choose_splits(int64_t n, int qtiles_hint, int *nsplit, int64_t *rows_per_split) {
+    const int sms = sm_count();
+    int64_t target = std::max<int64_t>(1, (int64_t)2 * sms / std::max(1, qtiles_hint));
+    int64_t max_split = std::max<int64_t>(1, ceil_div<int64_t>(n, 1024));
+    int64_t ns = std::min(target, max_split);
+    ns = std::min<int64_t>(ns, 4 * sms);
+    int64_t rps = round_up<int64_t>(ceil_div<int64_t>(n, ns), SCAN_THREADS);
+    *rows_per_split = rps;
+    *nsplit = (int)ceil_div<int64_t>(n, rps);
+}
+
+// Exact path over a (possibly device-sized) selection of queries.  Results
+// are scattered to the output positions qsel[i] (or i).
+int exact_search(pr_index *h, const float *Qp, const int32_t *qsel, const int32_t *nsel_dev, int nsel_max, int k,
+                 int64_t *rows, double *raw, double *rep, int32_t *count, Carve &cv, cudaStream_t st) {
+    const int K = k;
+    int QT = pick_qt(nsel_max, h->dp8, K);
+    int nsplit;
+    int64_t rps;
+    choose_splits(h->count, ceil_div(nsel_max, QT), &nsplit, &rps);
+    double *ps = cv.take<double>((size_t)nsel_max * nsplit * K);
+    int64_t *prr = cv.take<int64_t>((size_t)nsel_max * nsplit * K);
+    int32_t *pc = cv.take<int32_t>((size_t)nsel_max * nsplit);
+    ScanArgs a{h->x32, h->count, h->dp8, h->dim, Qp, qsel, nsel_dev, nsel_max, nsplit, rps, K, ps, prr, pc};
+    int64_t work = (int64_t)ceil_div(nsel_max, QT) * nsplit;
+    int grid = (int)std::min<int64_t>(work, (int64_t)sm_count() * 2);
+    if (grid < 1) grid = 1;
+    int rc = launch_scan(QT, a, grid, st);
+    if (rc) return rc;
+    MergeArgs m{ps, prr, nsplit, K, k, std::min<int64_t>(k, h->count), qsel, nsel_dev, nsel_max,
+                h->x32, h->dp8, h->dim, Qp, rows, raw, rep, count};
+    int mgrid = std::max(1, std::min(nsel_max, sm_count() * 8));
+    merge_topk_kernel<<<mgrid, 128, 0, st>>>(m);
+    PR_LAUNCH_CHECK();
+    h->stats.nsplit = nsplit;
+    return PR_OK;
+}
+
+size_t exact_scratch_bytes(int nsel_max, int k, int64_t n) {
+    int QT = 1;
+    (void)QT;
+    const int sms = sm_count();
+    int64_t ns = std::min<int64_t>(4 * sms, std::max<int64_t>(1, ceil_div<int64_t>(n, 1024)));
+    return (size_t)nsel_max * ns * k * (8 + 8) + (size_t)nsel_max * ns * 4 + 4096;
+}
+
+}  // namespace pr
+
+// ===========================================================================
+// C ABI
+using namespace pr;
+
+extern "C" {
+
+const char *pr_last_error(void) { return pr::last_error(); }
+int pr_abi_version(void) { return 1; }
+
+int pr_device_info(int *sms, int *major, int *minor) {
+    int dev = 0;
+    PR_CUDA(cudaGetDevice(&dev));
+    cudaDeviceProp p;
+    PR_CUDA(cudaGetDeviceProperties(&p, dev));
+    if (sms) *sms = p.multiProcessorCount;
+    if (major) *major = p.major;
+    if (minor) *minor = p.minor;
+    if (p.major != 10 || p.minor != 0)
+        PR_FAIL(PR_ERR_UNSUPPORTED, "libpentarag is built for sm_100a only; device is sm_%d%d", p.major, p.minor);
+    return PR_OK;
+}
+
+int pr_check_unit(const float *d_vecs, int64_t n, int dim, double tol, uint8_t *d_bad, void *stream) {
+    if (n < 0 || dim < 1) PR_FAIL(PR_ERR_BAD_ARG, "pr_check_unit: bad shape");
+    if (n == 0) return PR_OK;
+    int64_t threads = n * 32;
+    check_unit_kernel<<<(unsigned)ceil_div<int64_t>(threads, 256), 256, 0, as_stream(stream)>>>(d_vecs, n, dim, tol, d_bad);
+    PR_LAUNCH_CHECK();
+    return PR_OK;
+}
+
+int pr_index_create(int dim, int64_t capacity, uint32_t flags, pr_index **out) {
+    (void)flags;
+    if (!out) PR_FAIL(PR_ERR_BAD_ARG, "out is NULL");
+    if (dim < 1) PR_FAIL(PR_ERR_BAD_ARG, "dim must be >= 1");  // index.py:77-78
+    pr_index *h = new pr_index();
+    h->dim = dim;
+    h->dp8 = round_up(dim, 8);
+    h->dp64 = round_up(dim, 64);
+    int rc = reserve(h, std::max<int64_t>(capacity, 1024), nullptr);
+    if (rc) {
+        delete h;
+        return rc;
+    }
+    PR_CUDA(cudaMalloc(&h->d_counters, 16 * sizeof(int32_t)));
+    *out = h;
+    return PR_OK;
+}
+
+int pr_index_destroy(pr_index *h) {
+    if (!h) return PR_OK;
+    cudaDeviceSynchronize();
+    if (h->x32) cudaFree(h->x32);
+    if (h->x16) cudaFree(h->x16);
+    if (h->scratch) cudaFree(h->scratch);
+    if (h->d_counters) cudaFree(h->d_counters);
+    delete h;
+    return PR_OK;
+}
+
+int64_t pr_index_count(const pr_index *h) { return h ? h->count : -1; }
+int pr_index_dim(const pr_index *h) { return h ? h->dim : -1; }
+
+int pr_index_reserve(pr_index *h, int64_t capacity, void *stream) {
+    if (!h || capacity < 0) PR_FAIL(PR_ERR_BAD_ARG, "bad reserve");
+    return reserve(h, capacity, as_stream(stream));
+}
+
+int pr_index_append(pr_index *h, const float *d_vecs, int64_t n, void *stream) {
+    if (!h || n < 0) PR_FAIL(PR_ERR_BAD_ARG, "bad append");
+    if (n == 0) return PR_OK;
+    cudaStream_t st = as_stream(stream);
+    int rc = reserve(h, h->count + n, st);
+    if (rc) return rc;
+    write_rows_kernel<<<grid_for(n * h->dp64), 256, 0, st>>>(d_vecs, n, h->dim, nullptr, h->count, h->x32, h->dp8,
+                                                              h->x16, h->dp64);
+    PR_LAUNCH_CHECK();
+    h->count += n;
+    return PR_OK;
+}
+
+int pr_index_update_rows(pr_index *h, const int64_t *d_rows, const float *d_vecs, int64_t n, void *stream) {
+    if (!h || n < 0) PR_FAIL(PR_ERR_BAD_ARG, "bad update");
+    if (n == 0) return PR_OK;
+    write_rows_kernel<<<grid_for(n * h->dp64), 256, 0, as_stream(stream)>>>(d_vecs, n, h->dim, d_rows, 0, h->x32,
+                                                                             h->dp8, h->x16, h->dp64);
+    PR_LAUNCH_CHECK();
+    return PR_OK;
+}
+
+int pr_index_clear(pr_index *h) {
+    if (!h) PR_FAIL(PR_ERR_BAD_ARG, "null handle");
+    h->count = 0;
+    return PR_OK;
+}
+
+int pr_index_truncate(pr_index *h, int64_t n) {
+    if (!h || n < 0 || n > h->count) PR_FAIL(PR_ERR_BAD_ARG, "bad truncate");
+    h->count = n;
+    return PR_OK;
+}
+
+int pr_index_read_rows(const pr_index *h, int64_t row0, int64_t n, float *d_out, void *stream) {
+    if (!h || row0 < 0 || n < 0 || row0 + n > h->count) PR_FAIL(PR_ERR_BAD_ARG, "read_rows out of range");
+    if (n == 0) return PR_OK;
+    read_rows_kernel<<<grid_for(n * h->dim), 256, 0, as_stream(stream)>>>(h->x32, h->dp8, h->dim, row0, n, d_out);
+    PR_LAUNCH_CHECK();
+    return PR_OK;
+}
+
+int pr_index_append_from(pr_index *h, const pr_index *src, const int64_t *d_src_rows, int64_t n, void *stream) {
+    if (!h || !src || n < 0 || src->dim != h->dim) PR_FAIL(PR_ERR_BAD_ARG, "bad append_from");
+    if (n == 0) return PR_OK;
+    cudaStream_t st = as_stream(stream);
+    int rc = reserve(h, h->count + n, st);
+    if (rc) return rc;
+    gather_rows_kernel<<<grid_for(n * h->dp64), 256, 0, st>>>(src->x32, src->x16, d_src_rows, n, h->dp8, h->dp64,
+                                                               h->count, h->x32, h->x16);
+    PR_LAUNCH_CHECK();
+    h->count += n;
+    return PR_OK;
+}
+
+int pr_index_search(pr_index *h, const float *d_q, int64_t nq, int k, uint32_t mode, int64_t *d_rows, double *d_raw,
+                    double *d_reported, int32_t *d_count, void *stream) {
+    if (!h) PR_FAIL(PR_ERR_BAD_ARG, "null handle");
+    if (k < 1) PR_FAIL(PR_ERR_BAD_ARG, "k must be >= 1");  // index.py:161-162
+    if (nq < 0 || nq > INT32_MAX / 2) PR_FAIL(PR_ERR_BAD_ARG, "bad query count");
+    if (mode > PR_SEARCH_TENSOR) PR_FAIL(PR_ERR_BAD_ARG, "bad mode");
+    cudaStream_t st = as_stream(stream);
+    h->last_stream = st;
+    h->stats = pr_search_stats{};
+    h->stats.queries = nq;
+    if (nq == 0) return PR_OK;
+    if (h->count == 0 || k > KMAX_EXACT) {
+        if (h->count == 0) {
+            empty_result_kernel<<<(unsigned)ceil_div<int64_t>(nq * k, 256), 256, 0, st>>>(nq, k, d_rows, d_raw,
+                                                                                         d_reported, d_count);
+            PR_LAUNCH_CHECK();
+            return PR_OK;
+        }
+    }
+    if (k > KMAX_EXACT) return pr::big_k_search(h->x32, h->count, h->dp8, h->dim, d_q, nq, k, d_rows, d_raw, d_reported, d_count, st);
+
+    const bool tensor_ok = pr::tc_eligible(h->dim, h->count, k);
+    bool use_tc = (mode == PR_SEARCH_TENSOR) || (mode == PR_SEARCH_AUTO && tensor_ok && pr::tc_worthwhile(h->count, nq));
+    if (use_tc && !tensor_ok) use_tc = false;
+
+    size_t need = (size_t)nq * h->dp8 * sizeof(float) + exact_scratch_bytes((int)nq, k, h->count) + 65536;
+    if (use_tc) need += pr::tc_scratch_bytes(nq, h->dp64, h->count, k);
+    int rc = ensure_scratch(h, need, st);
+    if (rc) return rc;
+    Carve cv{reinterpret_cast<char *>(h->scratch)};
+    float *Qp = cv.take<float>((size_t)nq * h->dp8);
+    pad_queries_kernel<<<grid_for(nq * h->dp8), 256, 0, st>>>(d_q, nq, h->dim, h->dp8, Qp);
+    PR_LAUNCH_CHECK();
+
+    if (!use_tc) {
+        h->stats.path = PR_SEARCH_EXACT;
+        return exact_search(h, Qp, nullptr, nullptr, (int)nq, k, d_rows, d_raw, d_reported, d_count, cv, st);
+    }
+    h->stats.path = PR_SEARCH_TENSOR;
+    if (!h->tmap_ok) {
+        rc = pr::tc_make_store_map(&h->tmap, h->x16, h->cap256, h->dp64);
+        if (rc) return rc;
+        h->tmap_ok = true;
+    }
+    pr::TcSearch ts{};
+    ts.x32 = h->x32;
+    ts.x16 = h->x16;
+    ts.store_map = &h->tmap;
+    ts.n = h->count;
+    ts.d = h->dim;
+    ts.dp8 = h->dp8;
+    ts.dp64 = h->dp64;
+    ts.q32 = d_q;
+    ts.qp = Qp;
+    ts.nq = nq;
+    ts.k = k;
+    ts.rows = d_rows;
+    ts.raw = d_raw;
+    ts.rep = d_reported;
+    ts.count = d_count;
+    ts.counters = h->d_counters;
+    rc = pr::tc_search(ts, cv, st, &h->stats);
+    if (rc) return rc;
+    // certificate failures -> exact rescan of just those queries (device-sized list)
+    return exact_search(h, Qp, ts.fallback_list, h->d_counters, (int)nq, k, d_rows, d_raw, d_reported, d_count, cv,
+                        st);
+}
+
+int pr_index_last_stats(pr_index *h, pr_search_stats *out) {
+    if (!h || !out) PR_FAIL(PR_ERR_BAD_ARG, "null");
+    if (h->stats.path == PR_SEARCH_TENSOR) {
+        int32_t c[4];
+        PR_CUDA(cudaMemcpyAsync(c, h->d_counters, sizeof(c), cudaMemcpyDeviceToHost, h->last_stream));
+        PR_CUDA(cudaStreamSynchronize(h->last_stream));
+        h->stats.fallback = c[0];
+        h->stats.candidates = c[1];
+        h->stats.tensor_queries = h->stats.queries;
+    }
+    *out = h->stats;
+    return PR_OK;
+}
+
+int pr_index_snap_flags(const pr_index *h, const float *d_q, int64_t nq, int k, const int64_t *d_rows,
+                        const double *d_raw, const int32_t *d_count, int64_t row_offset, uint8_t *d_snap,
+                        void *stream) {
+    if (!h || nq < 0 || k < 1) PR_FAIL(PR_ERR_BAD_ARG, "bad snap_flags");
+    if (nq == 0) return PR_OK;
+    int64_t threads = nq * k * 32;
+    snap_flags_kernel<<<(unsigned)ceil_div<int64_t>(threads, 256), 256, 0, as_stream(stream)>>>(
+        h->x32, h->dp8, h->dim, d_q, nq, k, d_rows, d_raw, d_count, row_offset, d_snap);
+    PR_LAUNCH_CHECK();
+    return PR_OK;
+}
+
+int pr_merge_shards(const int64_t *d_rows, const double *d_raw, const uint8_t *d_snap, const int32_t *d_count,
+                    int nshard, int64_t nq, int k, int64_t *d_out_rows, double *d_out_raw, double *d_out_reported,
+                    int32_t *d_out_count, void *stream) {
+    if (nshard < 1 || nshard > 64 || nq < 0 || k < 1) PR_FAIL(PR_ERR_BAD_ARG, "bad merge_shards");
+    if (nq == 0) return PR_OK;
+    merge_shards_kernel<<<(unsigned)ceil_div<int64_t>(nq, 128), 128, 0, as_stream(stream)>>>(
+        d_rows, d_raw, d_snap, d_count, nshard, nq, k, d_out_rows, d_out_raw, d_out_reported, d_out_count);
+    PR_LAUNCH_CHECK();
+    return PR_OK;
+}
+
+}  // extern "C"

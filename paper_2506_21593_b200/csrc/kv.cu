@@ -1,0 +1,401 @@
+// Fixed KV cache on the GPU (reference: caches.py:45-101, FixedKVCache).
+//
+// The reference keys a dict by the raw query text: any one-byte difference
+// is a different key (caches.py:1-5).  Here a key is the 128-bit
+// fingerprint of its UTF-8 bytes (Murmur3-x64-128 construction, seed below,
+// top bit of the first word forced to 1 so {0,0} can mean EMPTY and {0,1}
+// TOMBSTONE).  Two distinct keys collide with probability ~2^-127; for 1e8
+// live keys the chance of any collision is ~1e16 / 2^128 ≈ 3e-23.
+//
+// Table: nslots 16-byte slots {w0, w1} (power of two) grouped in 64-byte
+// buckets of 4 slots, plus an int64 value per slot.  A probe is done by a
+// 4-lane group: each lane issues one 16-byte load, the group covers one
+// bucket per step, matches/empties are found with a warp ballot, and probing
+// moves linearly to the next bucket.  Values are write sequence numbers
+// supplied by the host; puts resolve with atomicMax, so the largest (latest)
+// write wins even when one batch writes the same key twice (caches.py:67-74).
+#include <algorithm>
+
+#include "common.cuh"
+
+struct pr_kv {
+    uint64_t *slots = nullptr;   // [nslots][2]
+    int64_t *vals = nullptr;     // [nslots]
+    int64_t nslots = 0;
+    unsigned long long *d_count = nullptr;  // [0] live, [1] tombstones
+    int64_t upper = 0;  // host-side upper bound of live + tombstones (no sync needed)
+};
+
+namespace pr {
+
+constexpr uint64_t FP_SEED = 0x5EED1024CA5CADE5ull;  // same constant family as embedding.py:33
+constexpr int KV_BUCKET = 4;
+
+__host__ __device__ __forceinline__ uint64_t rotl64(uint64_t x, int r) { return (x << r) | (x >> (64 - r)); }
+__host__ __device__ __forceinline__ uint64_t fmix64(uint64_t k) {
+    k ^= k >> 33;
+    k *= 0xff51afd7ed558ccdull;
+    k ^= k >> 33;
+    k *= 0xc4ceb9fe1a85ec53ull;
+    k ^= k >> 33;
+    return k;
+}
+
+__host__ __device__ inline void fingerprint128(const uint8_t *data, int64_t len, uint64_t *h_out, uint64_t *l_out) {
+    const uint64_t c1 = 0x87c37b91114253d5ull, c2 = 0x4cf5ad432745937full;
+    uint64_t h1 = FP_SEED, h2 = FP_SEED ^ 0x9E3779B97F4A7C15ull;
+    const int64_t nblocks = len / 16;
+    for (int64_t i = 0; i < nblocks; ++i) {
+        uint64_t k1 = 0, k2 = 0;
+        for (int b = 7; b >= 0; --b) k1 = (k1 << 8) | data[16 * i + b];
+        for (int b = 7; b >= 0; --b) k2 = (k2 << 8) | data[16 * i + 8 + b];
+        k1 *= c1; k1 = rotl64(k1, 31); k1 *= c2; h1 ^= k1;
+        h1 = rotl64(h1, 27); h1 += h2; h1 = h1 * 5 + 0x52dce729;
+        k2 *= c2; k2 = rotl64(k2, 33); k2 *= c1; h2 ^= k2;
+        h2 = rotl64(h2, 31); h2 += h1; h2 = h2 * 5 + 0x38495ab5;
+    }
+    const uint8_t *tail = data + nblocks * 16;
+    const int rem = (int)(len & 15);
+    uint64_t k1 = 0, k2 = 0;
+    for (int b = rem - 1; b >= 8; --b) k2 = (k2 << 8) | tail[b];
+    for (int b = std::min(rem, 8) - 1; b >= 0; --b) k1 = (k1 << 8) | tail[b];
+    if (rem > 8) { k2 *= c2; k2 = rotl64(k2, 33); k2 *= c1; h2 ^= k2; }
+    if (rem > 0) { k1 *= c1; k1 = rotl64(k1, 31); k1 *= c2; h1 ^= k1; }
+    h1 ^= (uint64_t)len;
+    h2 ^= (uint64_t)len;
+    h1 += h2; h2 += h1;
+    h1 = fmix64(h1); h2 = fmix64(h2);
+    h1 += h2; h2 += h1;
+    *h_out = h1 | 0x8000000000000000ull;  // never EMPTY/TOMBSTONE
+    *l_out = h2;
+}
+
+__global__ void fingerprint_kernel(const uint8_t *__restrict__ bytes, const int64_t *__restrict__ off, int64_t n,
+                                   uint64_t *__restrict__ fp) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t h, l;
+        fingerprint128(bytes + off[i], off[i + 1] - off[i], &h, &l);
+        fp[2 * i] = h;
+        fp[2 * i + 1] = l;
+    }
+}
+
+__device__ __forceinline__ ulonglong2 ld_slot(const uint64_t *slots, int64_t s) {
+    return __ldcg(reinterpret_cast<const ulonglong2 *>(slots + 2 * s));
+}
+
+__device__ __forceinline__ bool cas_slot(uint64_t *slots, int64_t s, uint64_t e0, uint64_t e1, uint64_t n0, uint64_t n1,
+                                         uint64_t &o0, uint64_t &o1) {
+    asm volatile(
+        "{\n\t.reg .b128 d, c, v;\n\t"
+        "mov.b128 c, {%2, %3};\n\t"
+        "mov.b128 v, {%4, %5};\n\t"
+        "atom.global.cas.b128 d, [%6], c, v;\n\t"
+        "mov.b128 {%0, %1}, d;\n\t}"
+        : "=l"(o0), "=l"(o1)
+        : "l"(e0), "l"(e1), "l"(n0), "l"(n1), "l"(slots + 2 * s)
+        : "memory");
+    return o0 == e0 && o1 == e1;
+}
+
+// 4-lane groups; every lane of the warp runs the loop until all groups finish
+template <int OP>  // 0 get, 1 put, 2 erase
+__global__ void kv_probe_kernel(uint64_t *slots, int64_t *vals, int64_t nslots, unsigned long long *counts,
+                                const uint64_t *__restrict__ fp, const uint8_t *__restrict__ bytes,
+                                const int64_t *__restrict__ off, int64_t n, const int64_t *__restrict__ in_vals,
+                                int64_t *__restrict__ out_vals, uint8_t *__restrict__ out_hit) {
+    const int lane = threadIdx.x & 31;
+    const int sub = lane & (KV_BUCKET - 1);
+    const int gshift = lane & ~(KV_BUCKET - 1);
+    const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / KV_BUCKET;
+    const int64_t nb = nslots / KV_BUCKET;
+    bool active = i < n;
+    uint64_t k0 = 0, k1 = 0;
+    if (active) {
+        if (fp) {
+            k0 = fp[2 * i];
+            k1 = fp[2 * i + 1];
+        } else {
+            // fused fingerprint: each lane of the group hashes (cheap, keeps lanes converged)
+            fingerprint128(bytes + off[i], off[i + 1] - off[i], &k0, &k1);
+        }
+    }
+    int64_t b = (int64_t)(k1 & (uint64_t)(nb - 1));
+    int64_t probes = 0;
+    while (__any_sync(0xffffffffu, active)) {
+        bool match = false, empty = false;
+        ulonglong2 v = make_ulonglong2(0, 0);
+        const int64_t s = b * KV_BUCKET + sub;
+        if (active) {
+            v = ld_slot(slots, s);
+            match = (v.x == k0 && v.y == k1);
+            empty = (v.x == 0 && v.y == 0);
+        }
+        const unsigned mm = (__ballot_sync(0xffffffffu, match) >> gshift) & 0xFu;
+        const unsigned me = (__ballot_sync(0xffffffffu, empty) >> gshift) & 0xFu;
+        if (active) {
+            if (mm) {
+                const int who = __ffs(mm) - 1;
+                if (sub == who) {
+                    if (OP == 0) {
+                        out_vals[i] = vals[s];
+                        out_hit[i] = 1;
+                    } else if (OP == 1) {
+                        atomicMax(reinterpret_cast<long long *>(vals + s), (long long)in_vals[i]);
+                    } else {
+                        uint64_t o0, o1;
+                        if (cas_slot(slots, s, k0, k1, 0, 1, o0, o1)) {
+                            vals[s] = -1;
+                            atomicAdd(&counts[0], (unsigned long long)-1ll);
+                            atomicAdd(&counts[1], 1ull);
+                        }
+                    }
+                }
+                active = false;
+            } else if (me) {
+                if (OP == 1) {
+                    const int who = __ffs(me) - 1;
+                    int claimed = 0;  // 1 = inserted, 2 = found ours, 0 = lost to another key
+                    if (sub == who) {
+                        uint64_t o0, o1;
+                        if (cas_slot(slots, s, 0, 0, k0, k1, o0, o1)) {
+                            atomicMax(reinterpret_cast<long long *>(vals + s), (long long)in_vals[i]);
+                            atomicAdd(&counts[0], 1ull);
+                            claimed = 1;
+                        } else if (o0 == k0 && o1 == k1) {
+                            atomicMax(reinterpret_cast<long long *>(vals + s), (long long)in_vals[i]);
+                            claimed = 2;
+                        }
+                    }
+                    // broadcast the outcome inside the 4-lane group
+                    const unsigned got = (__ballot_sync(__activemask(), claimed != 0) >> gshift) & 0xFu;
+                    if (got) active = false;  // else: re-read the same bucket
+                } else {
+                    if (OP == 0) {
+                        out_vals[i] = -1;
+                        out_hit[i] = 0;
+                    }
+                    active = false;
+                }
+            } else {
+                b = (b + 1) & (nb - 1);
+                if (++probes > nb) {  // table full: cannot happen below load 1.0
+                    if (OP == 0 && sub == 0) {
+                        out_vals[i] = -1;
+                        out_hit[i] = 0;
+                    }
+                    active = false;
+                }
+            }
+        }
+    }
+}
+
+__global__ void kv_export_kernel(const uint64_t *slots, const int64_t *vals, int64_t nslots, uint64_t *fp_out,
+                                 int64_t *val_out, int64_t max, unsigned long long *cursor) {
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nslots; s += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t w0 = slots[2 * s];
+        if (w0 & 0x8000000000000000ull) {
+            unsigned long long p = atomicAdd(cursor, 1ull);
+            if ((int64_t)p < max) {
+                fp_out[2 * p] = w0;
+                fp_out[2 * p + 1] = slots[2 * s + 1];
+                val_out[p] = vals[s];
+            }
+        }
+    }
+}
+
+__global__ void kv_reinsert_kernel(const uint64_t *old_slots, const int64_t *old_vals, int64_t old_n, uint64_t *slots,
+                                   int64_t *vals, int64_t nslots, unsigned long long *counts) {
+    // one thread per old slot, single-lane linear probing (rebuild only)
+    const int64_t nb = nslots / KV_BUCKET;
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < old_n; s += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t w0 = old_slots[2 * s], w1 = old_slots[2 * s + 1];
+        if (!(w0 & 0x8000000000000000ull)) continue;
+        int64_t b = (int64_t)(w1 & (uint64_t)(nb - 1));
+        for (int64_t probe = 0; probe <= nb; ++probe) {
+            bool done = false;
+            for (int j = 0; j < KV_BUCKET; ++j) {
+                uint64_t o0, o1;
+                int64_t t = b * KV_BUCKET + j;
+                if (cas_slot(slots, t, 0, 0, w0, w1, o0, o1)) {
+                    vals[t] = old_vals[s];
+                    atomicAdd(&counts[0], 1ull);
+                    done = true;
+                    break;
+                }
+            }
+            if (done) break;
+            b = (b + 1) & (nb - 1);
+        }
+    }
+}
+
+static int64_t slots_for(int64_t keys) {
+    int64_t s = 1024;
+    while (s < 2 * keys) s *= 2;  // load factor <= 0.5
+    return s;
+}
+
+static int alloc_table(pr_kv *h, int64_t nslots, cudaStream_t st) {
+    PR_CUDA(cudaMalloc(&h->slots, (size_t)nslots * 16));
+    PR_CUDA(cudaMalloc(&h->vals, (size_t)nslots * 8));
+    PR_CUDA(cudaMemsetAsync(h->slots, 0, (size_t)nslots * 16, st));
+    PR_CUDA(cudaMemsetAsync(h->vals, 0xFF, (size_t)nslots * 8, st));
+    h->nslots = nslots;
+    return PR_OK;
+}
+
+static int grow(pr_kv *h, int64_t need_keys, cudaStream_t st) {
+    // rebuild into a table sized for need_keys (drops tombstones)
+    unsigned long long c[2];
+    PR_CUDA(cudaMemcpyAsync(c, h->d_count, sizeof(c), cudaMemcpyDeviceToHost, st));
+    PR_CUDA(cudaStreamSynchronize(st));
+    int64_t live = (int64_t)c[0];
+    int64_t want = slots_for(std::max<int64_t>(need_keys, live));
+    if (want == h->nslots && c[1] == 0) {
+        h->upper = live;
+        return PR_OK;
+    }
+    uint64_t *os = h->slots;
+    int64_t *ov = h->vals;
+    int64_t on = h->nslots;
+    int rc = alloc_table(h, want, st);
+    if (rc) return rc;
+    PR_CUDA(cudaMemsetAsync(h->d_count, 0, 2 * sizeof(unsigned long long), st));
+    int g = (int)std::min<int64_t>(ceil_div<int64_t>(on, 256), (int64_t)sm_count() * 16);
+    kv_reinsert_kernel<<<g, 256, 0, st>>>(os, ov, on, h->slots, h->vals, h->nslots, h->d_count);
+    PR_LAUNCH_CHECK();
+    PR_CUDA(cudaStreamSynchronize(st));
+    cudaFree(os);
+    cudaFree(ov);
+    h->upper = live;
+    return PR_OK;
+}
+
+static int probe_grid(int64_t n) { return (int)std::max<int64_t>(1, ceil_div<int64_t>(n * KV_BUCKET, 256)); }
+
+}  // namespace pr
+
+using namespace pr;
+
+extern "C" {
+
+void pr_fingerprint_host(const uint8_t *bytes, int64_t len, uint64_t out[2]) {
+    fingerprint128(bytes, len, &out[0], &out[1]);
+}
+
+int pr_fingerprint(const uint8_t *d_bytes, const int64_t *d_off, int64_t n, uint64_t *d_fp, void *stream) {
+    if (n < 0) PR_FAIL(PR_ERR_BAD_ARG, "n < 0");
+    if (n == 0) return PR_OK;
+    int g = (int)std::min<int64_t>(ceil_div<int64_t>(n, 256), (int64_t)sm_count() * 16);
+    fingerprint_kernel<<<g, 256, 0, as_stream(stream)>>>(d_bytes, d_off, n, d_fp);
+    PR_LAUNCH_CHECK();
+    return PR_OK;
+}
+
+int pr_kv_create(int64_t capacity, pr_kv **out) {
+    if (!out || capacity < 0) PR_FAIL(PR_ERR_BAD_ARG, "bad kv_create");
+    pr_kv *h = new pr_kv();
+    int rc = alloc_table(h, slots_for(capacity), nullptr);
+    if (rc) {
+        delete h;
+        return rc;
+    }
+    PR_CUDA(cudaMalloc(&h->d_count, 2 * sizeof(unsigned long long)));
+    PR_CUDA(cudaMemset(h->d_count, 0, 2 * sizeof(unsigned long long)));
+    PR_CUDA(cudaDeviceSynchronize());
+    *out = h;
+    return PR_OK;
+}
+
+int pr_kv_destroy(pr_kv *h) {
+    if (!h) return PR_OK;
+    cudaDeviceSynchronize();
+    cudaFree(h->slots);
+    cudaFree(h->vals);
+    cudaFree(h->d_count);
+    delete h;
+    return PR_OK;
+}
+
+int pr_kv_put(pr_kv *h, const uint64_t *d_fp, const int64_t *d_vals, int64_t n, void *stream) {
+    if (!h || n < 0) PR_FAIL(PR_ERR_BAD_ARG, "bad kv_put");
+    if (n == 0) return PR_OK;
+    cudaStream_t st = as_stream(stream);
+    if (2 * (h->upper + n) > h->nslots) {
+        int rc = grow(h, h->upper + n, st);
+        if (rc) return rc;
+    }
+    kv_probe_kernel<1><<<probe_grid(n), 256, 0, st>>>(h->slots, h->vals, h->nslots, h->d_count, d_fp, nullptr, nullptr,
+                                                      n, d_vals, nullptr, nullptr);
+    PR_LAUNCH_CHECK();
+    h->upper += n;
+    return PR_OK;
+}
+
+int pr_kv_get(pr_kv *h, const uint64_t *d_fp, int64_t n, int64_t *d_vals, uint8_t *d_hit, void *stream) {
+    if (!h || n < 0) PR_FAIL(PR_ERR_BAD_ARG, "bad kv_get");
+    if (n == 0) return PR_OK;
+    kv_probe_kernel<0><<<probe_grid(n), 256, 0, as_stream(stream)>>>(h->slots, h->vals, h->nslots, h->d_count, d_fp,
+                                                                     nullptr, nullptr, n, nullptr, d_vals, d_hit);
+    PR_LAUNCH_CHECK();
+    return PR_OK;
+}
+
+int pr_kv_get_text(pr_kv *h, const uint8_t *d_bytes, const int64_t *d_off, int64_t n, int64_t *d_vals, uint8_t *d_hit,
+                   void *stream) {
+    if (!h || n < 0) PR_FAIL(PR_ERR_BAD_ARG, "bad kv_get_text");
+    if (n == 0) return PR_OK;
+    kv_probe_kernel<0><<<probe_grid(n), 256, 0, as_stream(stream)>>>(h->slots, h->vals, h->nslots, h->d_count, nullptr,
+                                                                     d_bytes, d_off, n, nullptr, d_vals, d_hit);
+    PR_LAUNCH_CHECK();
+    return PR_OK;
+}
+
+int pr_kv_erase(pr_kv *h, const uint64_t *d_fp, int64_t n, void *stream) {
+    if (!h || n < 0) PR_FAIL(PR_ERR_BAD_ARG, "bad kv_erase");
+    if (n == 0) return PR_OK;
+    kv_probe_kernel<2><<<probe_grid(n), 256, 0, as_stream(stream)>>>(h->slots, h->vals, h->nslots, h->d_count, d_fp,
+                                                                     nullptr, nullptr, n, nullptr, nullptr, nullptr);
+    PR_LAUNCH_CHECK();
+    return PR_OK;
+}
+
+int pr_kv_clear(pr_kv *h, void *stream) {
+    if (!h) PR_FAIL(PR_ERR_BAD_ARG, "null kv");
+    cudaStream_t st = as_stream(stream);
+    PR_CUDA(cudaMemsetAsync(h->slots, 0, (size_t)h->nslots * 16, st));
+    PR_CUDA(cudaMemsetAsync(h->vals, 0xFF, (size_t)h->nslots * 8, st));
+    PR_CUDA(cudaMemsetAsync(h->d_count, 0, 2 * sizeof(unsigned long long), st));
+    h->upper = 0;
+    return PR_OK;
+}
+
+int64_t pr_kv_size(pr_kv *h) {
+    if (!h) return -1;
+    unsigned long long c[2];
+    if (cudaMemcpy(c, h->d_count, sizeof(c), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    return (int64_t)c[0];
+}
+
+int64_t pr_kv_capacity(pr_kv *h) { return h ? h->nslots : -1; }
+
+int64_t pr_kv_export(pr_kv *h, uint64_t *d_fp, int64_t *d_vals, int64_t max, void *stream) {
+    if (!h || max < 0) PR_FAIL(PR_ERR_BAD_ARG, "bad kv_export");
+    cudaStream_t st = as_stream(stream);
+    unsigned long long *cur = nullptr;
+    PR_CUDA(cudaMallocAsync(&cur, sizeof(unsigned long long), st));
+    PR_CUDA(cudaMemsetAsync(cur, 0, sizeof(unsigned long long), st));
+    int g = (int)std::min<int64_t>(ceil_div<int64_t>(h->nslots, 256), (int64_t)sm_count() * 16);
+    kv_export_kernel<<<g, 256, 0, st>>>(h->slots, h->vals, h->nslots, d_fp, d_vals, max, cur);
+    PR_LAUNCH_CHECK();
+    unsigned long long c = 0;
+    PR_CUDA(cudaMemcpyAsync(&c, cur, sizeof(c), cudaMemcpyDeviceToHost, st));
+    PR_CUDA(cudaStreamSynchronize(st));
+    cudaFree(cur);
+    return (int64_t)std::min<unsigned long long>(c, (unsigned long long)max);
+}
+
+}  // extern "C"

@@ -1,0 +1,595 @@
+// Tensor-core score+select for FlatIndex.search (index.py:155-189), sm_100a.
+//
+// Stage 1 (tc_scan_kernel): S = Q16 · X16ᵀ on tcgen05 (kind::f16, fp32
+//   accumulators in TMEM).  One CTA = 128 queries (TMEM lanes) × a split of
+//   256-row store tiles (TMEM columns).  Warp 0 issues TMA loads of 64-column
+//   (128 B, SWIZZLE_128B) K-slices into a 3-stage smem ring, warp 1 issues the
+//   MMAs from one elected lane into a double-buffered TMEM accumulator, warps
+//   4-7 drain TMEM with tcgen05.ld (thread i <-> query i) and keep, per query,
+//   the top TC_KP approximate scores of the split.  The score matrix never
+//   leaves the SM.
+// Stage 2 (tc_rescore_kernel): per query, rescore in fp64 numpy-einsum order
+//   (bit-exact) every candidate that can still reach the top-k, pick the exact
+//   top-k and certify it against the largest score any non-candidate could
+//   have (split floor + rigorous fp16 error bound).  Queries whose
+//   certificate fails are listed for an exact fp64 rescan (index.cu).
+#include <cuda.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "common.cuh"
+#include "select.cuh"
+#include "tc_scan.cuh"
+
+namespace pr {
+
+constexpr int TC_STAGES = 3;
+constexpr int TC_THREADS = 256;
+constexpr int TC_A_BYTES = TC_BLOCK_M * TC_BLOCK_K * 2;  // 16 KB
+constexpr int TC_B_BYTES = TC_BLOCK_N * TC_BLOCK_K * 2;  // 32 KB
+constexpr int TC_BUF = 16;                               // per-thread staging of new candidates
+constexpr int TC_EPI_THREADS = 128;
+constexpr int TC_TMEM_COLS = 512;
+
+constexpr size_t tc_smem_bytes() {
+    return 1024 /*alignment slack*/ + (size_t)TC_STAGES * (TC_A_BYTES + TC_B_BYTES) +
+           (size_t)(TC_KP + TC_BUF) * TC_EPI_THREADS * 8 + 256 /*barriers*/;
+}
+
+// ---------------------------------------------------------------------------
+// PTX wrappers
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap *map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// K-major operand tile in the canonical SWIZZLE_128B layout that TMA writes:
+// rows of 128 B, 8-row core-matrix groups 1024 B apart (SBO), version 1 (sm_100).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
+    d |= (uint64_t)1 << 16;            // LBO (unused for swizzled K-major)
+    d |= (uint64_t)(1024 >> 4) << 32;  // SBO
+    d |= (uint64_t)1 << 46;            // descriptor version (sm_100)
+    d |= (uint64_t)2 << 61;            // SWIZZLE_128B
+    return d;
+}
+
+// kind::f16 instruction descriptor: A,B = F16 K-major, D = F32, N = 256, M = 128
+constexpr uint32_t TC_IDESC = (1u << 4) | ((uint32_t)(TC_BLOCK_N >> 3) << 17) | ((uint32_t)(TC_BLOCK_M >> 4) << 24);
+
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(TC_IDESC), "r"(accum)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t *bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+#define TMEM_LD32(addr, v)                                                                                         \
+    asm volatile(                                                                                                  \
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18," \
+        "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                                            \
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),           \
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),     \
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),   \
+          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])    \
+        : "r"(addr))
+
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// (score desc, row asc) as one 64-bit key, larger = ranks first.  Key 0 is
+// below every real key and marks an empty slot.
+__device__ __forceinline__ uint64_t cand_key(float s, uint32_t row) {
+    uint32_t u = __float_as_uint(s);
+    u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+    return ((uint64_t)u << 32) | (uint64_t)(0xFFFFFFFFu - row);
+}
+__device__ __forceinline__ float key_score(uint64_t key) {
+    uint32_t u = (uint32_t)(key >> 32);
+    u = (u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u;
+    return __uint_as_float(u);
+}
+__device__ __forceinline__ uint32_t key_row(uint64_t key) { return 0xFFFFFFFFu - (uint32_t)key; }
+
+// merge the per-thread staging buffer into the per-thread sorted list.
+// lists are [slot][thread] in smem (conflict-free when threads move together).
+__device__ __noinline__ float flush_candidates(uint64_t *list, uint64_t *buf, int nb, int t) {
+    for (int b = 0; b < nb; ++b) {
+        uint64_t key = buf[b * TC_EPI_THREADS + t];
+        if (key <= list[(TC_KP - 1) * TC_EPI_THREADS + t]) continue;
+        int pos = TC_KP - 1;
+        while (pos > 0 && key > list[(pos - 1) * TC_EPI_THREADS + t]) {
+            list[pos * TC_EPI_THREADS + t] = list[(pos - 1) * TC_EPI_THREADS + t];
+            --pos;
+        }
+        list[pos * TC_EPI_THREADS + t] = key;
+    }
+    uint64_t last = list[(TC_KP - 1) * TC_EPI_THREADS + t];
+    return last ? key_score(last) : -INFINITY;
+}
+
+struct TcScanParams {
+    int64_t n;
+    int nkb;              // K blocks (dp64 / 64)
+    int nsplit;
+    int tiles_per_split;  // 256-row tiles per split
+    int ntiles;
+    uint64_t *cand;       // [nq_pad, nsplit, TC_KP] keys
+};
+
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    tc_scan_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tx, TcScanParams p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    uint8_t *sA = smem;
+    uint8_t *sB = sA + TC_STAGES * TC_A_BYTES;
+    uint64_t *list = reinterpret_cast<uint64_t *>(sB + TC_STAGES * TC_B_BYTES);  // [TC_KP][128]
+    uint64_t *buf = list + TC_KP * TC_EPI_THREADS;                                // [TC_BUF][128]
+    uint64_t *full = buf + TC_BUF * TC_EPI_THREADS;
+    uint64_t *empty = full + TC_STAGES;
+    uint64_t *tfull = empty + TC_STAGES;
+    uint64_t *tempty = tfull + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int qtile = blockIdx.x, split = blockIdx.y;
+    const int t0 = split * p.tiles_per_split;
+    const int t1 = min(p.ntiles, t0 + p.tiles_per_split);
+    const int nlocal = max(0, t1 - t0);
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tq);
+        tma_prefetch_desc(&tx);
+        for (int s = 0; s < TC_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], TC_EPI_THREADS / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(TC_TMEM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------- TMA producer ----------------
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int i = 0; i < nlocal; ++i) {
+                const int t = t0 + i;
+                for (int kb = 0; kb < p.nkb; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_expect_tx(&full[stage], TC_A_BYTES + TC_B_BYTES);
+                    tma_load_2d(sA + stage * TC_A_BYTES, &tq, &full[stage], kb * TC_BLOCK_K, qtile * TC_BLOCK_M);
+                    tma_load_2d(sB + stage * TC_B_BYTES, &tx, &full[stage], kb * TC_BLOCK_K, t * TC_BLOCK_N);
+                    if (++stage == TC_STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer (single thread) ----------------
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int i = 0; i < nlocal; ++i) {
+                const int acc = i & 1;
+                const uint32_t aphase = (i >> 1) & 1;
+                mbar_wait(&tempty[acc], aphase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem + acc * TC_BLOCK_N;
+                for (int kb = 0; kb < p.nkb; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint64_t ad = sw128_desc(smem_u32(sA + stage * TC_A_BYTES));
+                    const uint64_t bd = sw128_desc(smem_u32(sB + stage * TC_B_BYTES));
+#pragma unroll
+                    for (int k = 0; k < TC_BLOCK_K / 16; ++k)  // +32 B per K=16 step inside the swizzle atom
+                        mma_f16(d_tmem, ad + 2 * k, bd + 2 * k, (kb | k) != 0);
+                    mma_commit(&empty[stage]);
+                    if (++stage == TC_STAGES) { stage = 0; phase ^= 1; }
+                }
+                mma_commit(&tfull[acc]);
+            }
+        }
+    } else if (warp >= 4) {
+        // ---------------- epilogue: TMEM -> registers -> top-K' ----------------
+        const int et = threadIdx.x - 128;  // 0..127 == TMEM lane == query within tile
+        const int ew = warp - 4;
+        for (int s = 0; s < TC_KP; ++s) list[s * TC_EPI_THREADS + et] = 0;
+        float thr = -INFINITY;
+        int nb = 0;
+        for (int i = 0; i < nlocal; ++i) {
+            const int acc = i & 1;
+            const uint32_t aphase = (i >> 1) & 1;
+            mbar_wait(&tfull[acc], aphase);
+            tc_fence_after();
+            const int64_t rbase = (int64_t)(t0 + i) * TC_BLOCK_N;
+#pragma unroll 1
+            for (int c = 0; c < TC_BLOCK_N / 32; ++c) {
+                uint32_t v[32];
+                TMEM_LD32(tmem + ((uint32_t)(ew * 32) << 16) + acc * TC_BLOCK_N + c * 32, v);
+                tmem_wait_ld();
+                const int64_t rb = rbase + c * 32;
+                const int64_t rem_rows = p.n - rb;
+                const int lim = rem_rows < 32 ? (int)rem_rows : 32;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const float s = __uint_as_float(v[j]);
+                    if (j < lim && s > thr) {
+                        buf[nb * TC_EPI_THREADS + et] = cand_key(s, (uint32_t)(rb + j));
+                        if (++nb == TC_BUF) {
+                            thr = flush_candidates(list, buf, nb, et);
+                            nb = 0;
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
+        flush_candidates(list, buf, nb, et);
+        const int64_t q = (int64_t)qtile * TC_BLOCK_M + et;
+        uint64_t *out = p.cand + (q * p.nsplit + split) * TC_KP;
+        for (int s = 0; s < TC_KP; ++s) out[s] = list[s * TC_EPI_THREADS + et];
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TC_TMEM_COLS) : "memory");
+    }
+}
+
+// ---------------------------------------------------------------------------
+// queries fp32 (padded to dp8) -> fp16 [nq_pad, dp64], zero padding rows/cols
+__global__ void queries_to_f16_kernel(const float *__restrict__ qp, int64_t nq, int dp8, int d, int64_t nq_pad, int dp64,
+                                      __half *__restrict__ out) {
+    int64_t total = nq_pad * (int64_t)dp64;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = t / dp64;
+        int j = (int)(t - i * dp64);
+        float v = (i < nq && j < d) ? qp[i * dp8 + j] : 0.0f;
+        out[t] = __float2half_rn(v);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// stage 2: certified exact rescoring, one CTA per query
+constexpr int RS_THREADS = 128;
+constexpr int RS_MAX = 512;  // rescored candidates per query before giving up
+
+struct RescoreArgs {
+    const uint64_t *cand;
+    int nsplit;
+    int64_t nq;
+    int k;
+    int64_t take;
+    double err;  // E: |approx - exact| bound
+    const float *x32;
+    int dp8, d;
+    const float *qp;
+    int64_t *rows;
+    double *raw, *rep;
+    int32_t *count;
+    int32_t *counters;
+    int32_t *fallback;
+};
+
+__global__ void __launch_bounds__(RS_THREADS) tc_rescore_kernel(RescoreArgs a) {
+    __shared__ int64_t r_row[RS_MAX];
+    __shared__ double r_apx[RS_MAX];
+    __shared__ double r_ex[RS_MAX];
+    __shared__ double red_s[RS_THREADS / 32];
+    __shared__ int64_t red_r[RS_THREADS / 32];
+    __shared__ int r_n;
+    const int M = a.nsplit * TC_KP;
+    for (int64_t q = blockIdx.x; q < a.nq; q += gridDim.x) {
+        const uint64_t *cq = a.cand + q * (int64_t)M;
+        // F: the largest approximate score a non-candidate can have
+        double F = -INFINITY;
+        for (int sp = threadIdx.x; sp < a.nsplit; sp += RS_THREADS) {
+            uint64_t last = cq[sp * TC_KP + TC_KP - 1];
+            if (last) F = fmax(F, (double)key_score(last));
+        }
+        {
+            double tmp = F;
+            int64_t dummy = 0;
+            // max-reduce via block_best on (score, row=0)
+            int64_t rr = (tmp == -INFINITY) ? -1 : 0;
+            block_best(tmp, rr, red_s, red_r);
+            F = (rr < 0) ? -INFINITY : tmp;
+            (void)dummy;
+        }
+        // a_k: take-th best approximate candidate (keys are unique)
+        uint64_t last_key = ~0ull;
+        for (int64_t j = 0; j < a.take; ++j) {
+            uint64_t best = 0;
+            for (int e = threadIdx.x; e < M; e += RS_THREADS) {
+                uint64_t key = cq[e];
+                if (key && key < last_key && key > best) best = key;
+            }
+            for (int o = 16; o; o >>= 1) {
+                uint64_t ob = __shfl_xor_sync(0xffffffffu, best, o);
+                best = ob > best ? ob : best;
+            }
+            if ((threadIdx.x & 31) == 0) red_r[threadIdx.x >> 5] = (int64_t)best;
+            __syncthreads();
+            best = 0;
+            for (int w = 0; w < RS_THREADS / 32; ++w) best = ((uint64_t)red_r[w] > best) ? (uint64_t)red_r[w] : best;
+            __syncthreads();
+            last_key = best;
+        }
+        const double ak = (last_key && last_key != ~0ull) ? (double)key_score(last_key) : -INFINITY;
+        const double cut = ak - 2.0 * a.err;
+        if (threadIdx.x == 0) r_n = 0;
+        __syncthreads();
+        for (int e = threadIdx.x; e < M; e += RS_THREADS) {
+            uint64_t key = cq[e];
+            if (!key) continue;
+            double s = key_score(key);
+            if (s >= cut) {
+                int slot = atomicAdd(&r_n, 1);
+                if (slot < RS_MAX) {
+                    r_row[slot] = key_row(key);
+                    r_apx[slot] = s;
+                }
+            }
+        }
+        __syncthreads();
+        const int nr = r_n;
+        if (nr > RS_MAX) {
+            if (threadIdx.x == 0) {
+                int slot = atomicAdd(&a.counters[0], 1);
+                a.fallback[slot] = (int32_t)q;
+            }
+            __syncthreads();
+            continue;
+        }
+        const float *qv = a.qp + q * (int64_t)a.dp8;
+        for (int e = threadIdx.x; e < nr; e += RS_THREADS)
+            r_ex[e] = einsum_dot_f32(a.x32 + r_row[e] * (int64_t)a.dp8, qv, a.d);
+        if (threadIdx.x == 0) atomicAdd(&a.counters[1], nr);
+        __syncthreads();
+        // exact top-take of R, certificate, outputs
+        double last_s = INFINITY;
+        int64_t last_r = -1;
+        bool ok = true;
+        for (int64_t j = 0; j < a.take; ++j) {
+            double bs = -INFINITY;
+            int64_t br = -1;
+            for (int e = threadIdx.x; e < nr; e += RS_THREADS) {
+                double s = r_ex[e];
+                int64_t r = r_row[e];
+                bool after = (last_r < 0) || ranks_before(last_s, last_r, s, r);
+                if (after && (br < 0 || ranks_before(s, r, bs, br))) { bs = s; br = r; }
+            }
+            block_best(bs, br, red_s, red_r);
+            if (br < 0) { ok = false; break; }
+            last_s = bs;
+            last_r = br;
+        }
+        // every non-candidate scores <= F + E exactly; candidates outside R
+        // score < a_k - E <= e_k
+        if (ok && !(last_s > F + a.err)) ok = false;
+        if (!ok) {
+            if (threadIdx.x == 0) {
+                int slot = atomicAdd(&a.counters[0], 1);
+                a.fallback[slot] = (int32_t)q;
+            }
+            __syncthreads();
+            continue;
+        }
+        last_s = INFINITY;
+        last_r = -1;
+        for (int64_t j = 0; j < a.k; ++j) {
+            const int64_t o = q * a.k + j;
+            if (j >= a.take) {
+                if (threadIdx.x == 0) {
+                    a.rows[o] = -1;
+                    if (a.raw) a.raw[o] = 0.0;
+                    if (a.rep) a.rep[o] = 0.0;
+                }
+                continue;
+            }
+            double bs = -INFINITY;
+            int64_t br = -1;
+            for (int e = threadIdx.x; e < nr; e += RS_THREADS) {
+                double s = r_ex[e];
+                int64_t r = r_row[e];
+                bool after = (last_r < 0) || ranks_before(last_s, last_r, s, r);
+                if (after && (br < 0 || ranks_before(s, r, bs, br))) { bs = s; br = r; }
+            }
+            block_best(bs, br, red_s, red_r);
+            double rep;
+            finalize_hit(a.x32, a.dp8, a.d, qv, br, bs, &rep);
+            if (threadIdx.x == 0) {
+                a.rows[o] = br;
+                if (a.raw) a.raw[o] = bs;
+                if (a.rep) a.rep[o] = rep;
+            }
+            last_s = bs;
+            last_r = br;
+        }
+        if (threadIdx.x == 0) a.count[q] = (int32_t)a.take;
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+
+static int make_map(CUtensorMap *m, const void *base, int64_t rows, int cols, int box_rows) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) PR_FAIL(PR_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+    cuuint32_t box[2] = {(cuuint32_t)TC_BLOCK_K, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void *>(base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) PR_FAIL(PR_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return PR_OK;
+}
+
+bool tc_eligible(int d, int64_t n, int k) { return k <= TC_KP && n > 0 && n < (int64_t)0xFFFFFFF0ll && d <= 8192; }
+bool tc_worthwhile(int64_t n, int64_t nq) { return n >= 16384 && nq >= 1; }
+
+double tc_error_bound(int d, int dp64) {
+    // |fp16(x) - x| <= u|x| + eta  (u = 2^-11 round-to-nearest, eta = 2^-25 half the
+    // fp16 subnormal spacing).  For unit vectors within the 1e-4 norm tolerance
+    // (index.py:46) S = sum|q_i v_i| <= (1 + 1e-4)^2 and sum|x_i| <= sqrt(d)(1 + 1e-4):
+    //   product error   <= (2u + u^2) S + eta (2 + 2u) sqrt(d) (1 + 1e-4) + d eta^2
+    //   fp32 accumulate <= dp64 * 2^-23 * (sum of |fp16 products|)   (any order, truncation)
+    const double u = std::ldexp(1.0, -11), eta = std::ldexp(1.0, -25);
+    const double S = (1 + 1e-4) * (1 + 1e-4);
+    const double prod = (2 * u + u * u) * S + eta * (2 + 2 * u) * std::sqrt((double)d) * (1 + 1e-4) + d * eta * eta;
+    const double sum_abs = S * (1 + u) * (1 + u) + prod;
+    const double acc = dp64 * std::ldexp(1.0, -23) * sum_abs;
+    return (prod + acc) * 1.01 + 1e-9;
+}
+
+size_t tc_scratch_bytes(int64_t nq, int dp64, int64_t n, int k) {
+    (void)k;
+    int64_t nq_pad = round_up<int64_t>(nq, TC_BLOCK_M);
+    int64_t ntiles = ceil_div<int64_t>(n, TC_BLOCK_N);
+    int64_t maxsplit = std::min<int64_t>(ntiles, 4 * 148);
+    return (size_t)nq_pad * dp64 * 2 + (size_t)nq_pad * maxsplit * TC_KP * 8 + (size_t)nq * 4 + 4096;
+}
+
+int tc_make_store_map(TcStoreMap *m, const __half *x16, int64_t rows, int dp64) {
+    return make_map(&m->map, x16, rows, dp64, TC_BLOCK_N);
+}
+
+static int choose_nsplit(int64_t qtiles, int64_t ntiles) {
+    const int sms = sm_count();
+    int best = 1;
+    double best_eff = -1;
+    int64_t lo = std::max<int64_t>(1, ceil_div<int64_t>(sms, qtiles));
+    int64_t hi = std::min<int64_t>(ntiles, std::max<int64_t>(lo, 8 * sms / std::max<int64_t>(1, qtiles)));
+    hi = std::min<int64_t>(hi, 4 * 148);
+    for (int64_t ns = lo; ns <= std::max(lo, hi); ++ns) {
+        int64_t tps = ceil_div<int64_t>(ntiles, ns);
+        int64_t real_ns = ceil_div<int64_t>(ntiles, tps);
+        int64_t ctas = qtiles * real_ns;
+        int64_t waves = ceil_div<int64_t>(ctas, sms);
+        // time ~ waves * tps ; useful work ~ qtiles * ntiles
+        double eff = (double)(qtiles * ntiles) / (double)(waves * sms * tps);
+        if (eff > best_eff + 1e-3) {
+            best_eff = eff;
+            best = (int)real_ns;
+        }
+        if (ns > lo && eff > 0.97) break;
+    }
+    if (ntiles < 1) return 1;
+    return std::max(1, best);
+}
+
+int tc_search(TcSearch &s, Carve &cv, cudaStream_t st, pr_search_stats *stats) {
+    const int64_t nq_pad = round_up<int64_t>(s.nq, TC_BLOCK_M);
+    const int64_t qtiles = nq_pad / TC_BLOCK_M;
+    const int64_t ntiles = ceil_div<int64_t>(s.n, TC_BLOCK_N);
+    const int nsplit = choose_nsplit(qtiles, ntiles);
+    const int tps = (int)ceil_div<int64_t>(ntiles, nsplit);
+    __half *q16 = cv.take<__half>((size_t)nq_pad * s.dp64);
+    uint64_t *cand = cv.take<uint64_t>((size_t)nq_pad * nsplit * TC_KP);
+    s.fallback_list = cv.take<int32_t>((size_t)s.nq);
+
+    {
+        int64_t total = nq_pad * s.dp64;
+        int grid = (int)std::min<int64_t>(ceil_div<int64_t>(total, 256), (int64_t)sm_count() * 16);
+        queries_to_f16_kernel<<<grid, 256, 0, st>>>(s.qp, s.nq, s.dp8, s.d, nq_pad, s.dp64, q16);
+        PR_LAUNCH_CHECK();
+    }
+    TcStoreMap qmap;
+    int rc = make_map(&qmap.map, q16, nq_pad, s.dp64, TC_BLOCK_M);
+    if (rc) return rc;
+
+    static bool attr = false;
+    if (!attr) {
+        PR_CUDA(cudaFuncSetAttribute(tc_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc_smem_bytes()));
+        attr = true;
+    }
+    TcScanParams p{s.n, s.dp64 / TC_BLOCK_K, nsplit, tps, (int)ntiles, cand};
+    dim3 grid((unsigned)qtiles, (unsigned)nsplit);
+    tc_scan_kernel<<<grid, TC_THREADS, tc_smem_bytes(), st>>>(qmap.map, s.store_map->map, p);
+    PR_LAUNCH_CHECK();
+
+    PR_CUDA(cudaMemsetAsync(s.counters, 0, 4 * sizeof(int32_t), st));
+    RescoreArgs ra{cand, nsplit, s.nq, s.k, std::min<int64_t>(s.k, s.n), tc_error_bound(s.d, s.dp64), s.x32,
+                   s.dp8, s.d, s.qp, s.rows, s.raw, s.rep, s.count, s.counters, s.fallback_list};
+    int rgrid = (int)std::min<int64_t>(s.nq, (int64_t)sm_count() * 16);
+    tc_rescore_kernel<<<rgrid, RS_THREADS, 0, st>>>(ra);
+    PR_LAUNCH_CHECK();
+    stats->nsplit = nsplit;
+    return PR_OK;
+}
+
+}  // namespace pr

@@ -1,0 +1,51 @@
+// Internal interface between index.cu (orchestration) and the tensor-core
+// score+select path (tc_scan.cu) / the large-k path (bigk.cu).
+#pragma once
+
+#include <cuda.h>
+
+#include "common.cuh"
+
+namespace pr {
+
+struct alignas(64) TcStoreMap {
+    CUtensorMap map;
+};
+
+// Candidates kept per (query, row split) by the tcgen05 epilogue.
+constexpr int TC_KP = 32;
+constexpr int TC_BLOCK_M = 128;  // queries per CTA (TMEM lanes)
+constexpr int TC_BLOCK_N = 256;  // store rows per MMA tile (TMEM columns)
+constexpr int TC_BLOCK_K = 64;   // fp16 columns per stage = one 128B swizzle atom
+
+struct Carve;
+
+struct TcSearch {
+    const float *x32;
+    const __half *x16;
+    const TcStoreMap *store_map;
+    int64_t n;
+    int d, dp8, dp64;
+    const float *q32;  // caller queries [nq, d]
+    const float *qp;   // padded fp32 queries [nq, dp8]
+    int64_t nq;
+    int k;
+    int64_t *rows;
+    double *raw, *rep;
+    int32_t *count;
+    int32_t *counters;      // [0] fallback count, [1] rescored candidates
+    int32_t *fallback_list; // out: query ids failing the certificate
+};
+
+bool tc_eligible(int d, int64_t n, int k);
+bool tc_worthwhile(int64_t n, int64_t nq);
+size_t tc_scratch_bytes(int64_t nq, int dp64, int64_t n, int k);
+int tc_make_store_map(TcStoreMap *m, const __half *x16, int64_t rows, int dp64);
+int tc_search(TcSearch &s, Carve &cv, cudaStream_t st, pr_search_stats *stats);
+// fp16 rounding + tensor-core accumulation error bound for unit vectors of dim d
+double tc_error_bound(int d, int dp64);
+
+int big_k_search(const float *x32, int64_t n, int dp8, int d, const float *q, int64_t nq, int k, int64_t *rows,
+                 double *raw, double *rep, int32_t *count, cudaStream_t st);
+
+}  // namespace pr

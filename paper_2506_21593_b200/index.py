@@ -1,0 +1,360 @@
+"""Device-resident exact flat index — drop-in for ``FlatIndex``.
+
+Reference: ``ragcascade/index.py:73-261``.  Same method set (insert, extend,
+search, clear, payload, vector, entry_ids, __len__, __contains__, dim,
+search_count, snapshot/restore) and the same results bit-for-bit: scores are
+the reference's fp64 ``np.einsum`` values (index.py:173) reproduced on the
+GPU in numpy's reduction order, ranked by (score desc, row asc)
+(index.py:176), self-snapped and clamped (index.py:180-185).
+
+Ids and payloads stay in Python (they are opaque objects); vectors live in
+libpentarag's device store (fp32 exact copy + fp16 tensor-core copy).  The
+batch entry point ``search_batch`` takes a [B, dim] float32 tensor (device or
+host) and returns device tensors; it is what the cascade and the benches use.
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+import struct
+import threading
+import zlib
+from dataclasses import dataclass
+from typing import Any, Callable, Iterable
+
+import numpy as np
+
+from . import _lib
+from .errors import CorruptSnapshot, InvalidVector
+from .vectors import DIMENSION, INDEX_NORM_TOLERANCE, coerce_index_vector
+
+_MAGIC = b"RCFLATIX"
+_VERSION = 1
+_HEADER = struct.Struct("<8sIIQQI")  # magic, version, dim, count, payload_len, crc32 (index.py:40-42)
+
+MODE_AUTO = _lib.PR_SEARCH_AUTO
+MODE_EXACT = _lib.PR_SEARCH_EXACT
+MODE_TENSOR = _lib.PR_SEARCH_TENSOR
+
+
+@dataclass(frozen=True)
+class SearchHit:
+    entry_id: str
+    score: float
+    rank: int
+
+
+@dataclass
+class BatchResult:
+    """Device tensors of one batched search."""
+
+    rows: Any      # int64 [B, k], -1 past count
+    scores: Any    # float64 [B, k]  reported score (snap + clamp)
+    raw: Any       # float64 [B, k]  einsum score
+    count: Any     # int32 [B]
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+class FlatIndex:
+    """Exact cosine k-NN over unit vectors, stored and scanned on the GPU."""
+
+    def __init__(self, dim: int = DIMENSION, *, capacity: int = 0):
+        if dim < 1:
+            raise ValueError("dim must be >= 1")
+        _lib.require_device()
+        self._L = _lib.load()
+        self._dim = dim
+        self._lock = threading.RLock()
+        h = ctypes.c_void_p()
+        _lib.check(self._L.pr_index_create(dim, max(0, int(capacity)), 0, ctypes.byref(h)), "pr_index_create")
+        self._h = h
+        self._ids: list[str] = []
+        self._row_by_id: dict[str, int] = {}
+        self._payloads: list[Any] = []
+        self.search_count = 0
+        self.last_stats: _lib.SearchStats | None = None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                self._L.pr_index_destroy(h)
+            except Exception:  # noqa: BLE001 - interpreter shutdown
+                pass
+            self._h = None
+
+    # -- introspection -----------------------------------------------------
+    @property
+    def dim(self) -> int:
+        return self._dim
+
+    @property
+    def handle(self) -> ctypes.c_void_p:
+        return self._h
+
+    def __len__(self) -> int:
+        with self._lock:
+            return len(self._ids)
+
+    def __contains__(self, entry_id: str) -> bool:
+        with self._lock:
+            return entry_id in self._row_by_id
+
+    def entry_ids(self) -> tuple[str, ...]:
+        with self._lock:
+            return tuple(self._ids)
+
+    def row_of(self, entry_id: str) -> int:
+        with self._lock:
+            return self._row_by_id[entry_id]
+
+    def id_at(self, row: int) -> str:
+        return self._ids[row]
+
+    def payload(self, entry_id: str) -> Any:
+        with self._lock:
+            return self._payloads[self._row_by_id[entry_id]]
+
+    def payload_at(self, row: int) -> Any:
+        return self._payloads[row]
+
+    def vector(self, entry_id: str) -> np.ndarray:
+        with self._lock:
+            row = self._row_by_id[entry_id]
+            return self.read_rows(row, 1).cpu().numpy()[0]
+
+    def read_rows(self, row0: int, n: int):
+        torch = _torch()
+        out = torch.empty((n, self._dim), dtype=torch.float32, device="cuda")
+        _lib.check(self._L.pr_index_read_rows(self._h, row0, n, _lib.ptr(out), _lib.stream_ptr()), "read_rows")
+        return out
+
+    # -- writes --------------------------------------------------------------
+    def insert(self, entry_id: str, vector, payload: Any = None) -> None:
+        """Upsert: a new id appends a row, an existing id is overwritten in
+        place and keeps its tie-break slot (index.py:125-145)."""
+        arr = coerce_index_vector(vector, self._dim)
+        with self._lock:
+            row = self._row_by_id.get(entry_id)
+            if row is None:
+                self._append_rows(arr[None, :])
+                self._row_by_id[entry_id] = len(self._ids)
+                self._ids.append(entry_id)
+                self._payloads.append(payload)
+            else:
+                self._payloads[row] = payload
+                self._update_rows(np.array([row], dtype=np.int64), arr[None, :])
+
+    def extend(self, items: Iterable[tuple[str, Any, Any]]) -> int:
+        """Bulk upsert of (entry_id, vector, payload) with sequential semantics,
+        shipped to the device in one append + one in-place update."""
+        items = list(items)
+        arrs = [coerce_index_vector(v, self._dim) for _, v, _ in items]
+        with self._lock:
+            new_vecs: list[np.ndarray] = []
+            upd: dict[int, np.ndarray] = {}
+            base = len(self._ids)
+            for (eid, _, payload), arr in zip(items, arrs):
+                row = self._row_by_id.get(eid)
+                if row is None:
+                    row = len(self._ids)
+                    self._row_by_id[eid] = row
+                    self._ids.append(eid)
+                    self._payloads.append(payload)
+                    new_vecs.append(arr)
+                else:
+                    self._payloads[row] = payload
+                    if row >= base:
+                        new_vecs[row - base] = arr
+                    else:
+                        upd[row] = arr
+            if new_vecs:
+                self._append_rows(np.stack(new_vecs))
+            if upd:
+                rows = np.fromiter(upd.keys(), dtype=np.int64, count=len(upd))
+                self._update_rows(rows, np.stack(list(upd.values())))
+        return len(items)
+
+    def extend_arrays(self, ids: list[str], vectors, payloads: list[Any] | None = None,
+                      *, validate: bool = True) -> int:
+        """Bulk append of NEW ids from a [n, dim] float32 array/tensor (the
+        loader path: one H2D copy, device-side unit-norm validation)."""
+        torch = _torch()
+        t = torch.as_tensor(vectors, dtype=torch.float32)
+        if t.dim() != 2 or t.shape[1] != self._dim or t.shape[0] != len(ids):
+            raise InvalidVector(f"expected [{len(ids)}, {self._dim}] vectors, got {tuple(t.shape)}")
+        t = t.to("cuda", non_blocking=True).contiguous()
+        if validate:
+            check_unit(t, INDEX_NORM_TOLERANCE)
+        with self._lock:
+            for eid in ids:
+                if eid in self._row_by_id:
+                    raise ValueError(f"extend_arrays only appends new ids; {eid!r} exists")
+            base = len(self._ids)
+            _lib.check(self._L.pr_index_append(self._h, _lib.ptr(t), t.shape[0], _lib.stream_ptr()), "append")
+            for i, eid in enumerate(ids):
+                self._row_by_id[eid] = base + i
+            self._ids.extend(ids)
+            self._payloads.extend(payloads if payloads is not None else [None] * len(ids))
+        return len(ids)
+
+    def append_rows_from(self, src: "FlatIndex", src_rows, ids: list[str], payloads: list[Any]) -> None:
+        """Append rows copied device-to-device from another index (AKM settle
+        from knowledge-base rows)."""
+        torch = _torch()
+        r = torch.as_tensor(src_rows, dtype=torch.int64).to("cuda").contiguous()
+        with self._lock:
+            base = len(self._ids)
+            _lib.check(
+                self._L.pr_index_append_from(self._h, src.handle, _lib.ptr(r), r.numel(), _lib.stream_ptr()),
+                "append_from",
+            )
+            for i, eid in enumerate(ids):
+                self._row_by_id[eid] = base + i
+            self._ids.extend(ids)
+            self._payloads.extend(payloads)
+
+    def _append_rows(self, arr: np.ndarray) -> None:
+        torch = _torch()
+        t = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float32)).to("cuda", non_blocking=False)
+        _lib.check(self._L.pr_index_append(self._h, _lib.ptr(t), t.shape[0], _lib.stream_ptr()), "append")
+
+    def _update_rows(self, rows: np.ndarray, arr: np.ndarray) -> None:
+        torch = _torch()
+        r = torch.from_numpy(rows).to("cuda")
+        t = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float32)).to("cuda")
+        _lib.check(self._L.pr_index_update_rows(self._h, _lib.ptr(r), _lib.ptr(t), t.shape[0], _lib.stream_ptr()),
+                   "update")
+
+    def clear(self) -> None:
+        with self._lock:
+            self._ids.clear()
+            self._row_by_id.clear()
+            self._payloads.clear()
+            _lib.check(self._L.pr_index_clear(self._h), "clear")
+
+    def truncate(self, n: int) -> None:
+        with self._lock:
+            for eid in self._ids[n:]:
+                del self._row_by_id[eid]
+            del self._ids[n:]
+            del self._payloads[n:]
+            _lib.check(self._L.pr_index_truncate(self._h, n), "truncate")
+
+    # -- search ----------------------------------------------------------------
+    def search_batch(self, queries, k: int, *, mode: int = MODE_AUTO, validate: bool = True,
+                     out: BatchResult | None = None) -> BatchResult:
+        """Batched FlatIndex.search.  ``queries``: [B, dim] float32 (torch
+        tensor on any device, or numpy).  Returns device tensors; counts
+        ``search_count`` once per query like B sequential calls."""
+        if k < 1:
+            raise ValueError("k must be >= 1")
+        torch = _torch()
+        q = torch.as_tensor(queries, dtype=torch.float32)
+        if q.dim() != 2 or q.shape[1] != self._dim:
+            raise InvalidVector(f"expected [B, {self._dim}] queries, got {tuple(q.shape)}")
+        q = q.to("cuda", non_blocking=True).contiguous()
+        B = q.shape[0]
+        if validate and B:
+            check_unit(q, INDEX_NORM_TOLERANCE)
+        if out is None:
+            out = BatchResult(
+                rows=torch.empty((B, k), dtype=torch.int64, device="cuda"),
+                scores=torch.empty((B, k), dtype=torch.float64, device="cuda"),
+                raw=torch.empty((B, k), dtype=torch.float64, device="cuda"),
+                count=torch.empty((B,), dtype=torch.int32, device="cuda"),
+            )
+        with self._lock:
+            self.search_count += B
+            if B:
+                rc = self._L.pr_index_search(
+                    self._h, _lib.ptr(q), B, k, mode, _lib.ptr(out.rows), _lib.ptr(out.raw),
+                    _lib.ptr(out.scores), _lib.ptr(out.count), _lib.stream_ptr(),
+                )
+                _lib.check(rc, "pr_index_search")
+        return out
+
+    def stats(self) -> _lib.SearchStats:
+        st = _lib.SearchStats()
+        _lib.check(self._L.pr_index_last_stats(self._h, ctypes.byref(st)), "last_stats")
+        return st
+
+    def search(self, query_vector, k: int, *, mode: int = MODE_AUTO) -> list[SearchHit]:
+        """Exact top-k by cosine, ties by insertion order (index.py:155-189)."""
+        if k < 1:
+            raise ValueError("k must be >= 1")
+        q32 = coerce_index_vector(query_vector, self._dim)
+        with self._lock:
+            res = self.search_batch(q32[None, :], k, mode=mode, validate=False)
+            n = int(res.count[0].item())
+            rows = res.rows[0, :n].cpu().numpy()
+            scores = res.scores[0, :n].cpu().numpy()
+            return [SearchHit(self._ids[int(r)], float(s), i + 1) for i, (r, s) in enumerate(zip(rows, scores))]
+
+    def hits_from_batch(self, res: BatchResult) -> list[list[SearchHit]]:
+        counts = res.count.cpu().numpy()
+        rows = res.rows.cpu().numpy()
+        scores = res.scores.cpu().numpy()
+        out = []
+        for b in range(rows.shape[0]):
+            out.append([SearchHit(self._ids[int(rows[b, j])], float(scores[b, j]), j + 1) for j in range(counts[b])])
+        return out
+
+    # -- snapshot / restore (index.py:198-261) ----------------------------
+    def snapshot(self, payload_encoder: Callable[[Any], Any] | None = None) -> bytes:
+        enc = payload_encoder or (lambda p: p)
+        with self._lock:
+            n = len(self._ids)
+            vec_block = self.read_rows(0, n).cpu().numpy().tobytes() if n else b""
+            lines = [json.dumps({"id": self._ids[i], "payload": enc(self._payloads[i])}, ensure_ascii=False)
+                     for i in range(n)]
+            meta = ("\n".join(lines) + ("\n" if lines else "")).encode("utf-8")
+            body = vec_block + meta
+            return _HEADER.pack(_MAGIC, _VERSION, self._dim, n, len(meta), zlib.crc32(body)) + body
+
+    @classmethod
+    def restore(cls, data: bytes, payload_decoder: Callable[[Any], Any] | None = None) -> "FlatIndex":
+        dec = payload_decoder or (lambda p: p)
+        if len(data) < _HEADER.size:
+            raise CorruptSnapshot("snapshot shorter than header")
+        magic, version, dim, count, meta_len, crc = _HEADER.unpack_from(data)
+        if magic != _MAGIC:
+            raise CorruptSnapshot(f"bad magic {magic!r}")
+        if version != _VERSION:
+            raise CorruptSnapshot(f"unsupported snapshot version {version}")
+        body = data[_HEADER.size:]
+        vec_len = count * dim * 4
+        if len(body) != vec_len + meta_len:
+            raise CorruptSnapshot(f"body length {len(body)} != expected {vec_len + meta_len}")
+        if zlib.crc32(body) != crc:
+            raise CorruptSnapshot("checksum mismatch")
+        vecs = np.frombuffer(body[:vec_len], dtype=np.float32).reshape(count, dim)
+        meta = body[vec_len:].decode("utf-8").splitlines()
+        if len(meta) != count:
+            raise CorruptSnapshot(f"payload sidecar has {len(meta)} lines, expected {count}")
+        recs = []
+        for i, line in enumerate(meta):
+            try:
+                recs.append(json.loads(line))
+            except json.JSONDecodeError as exc:
+                raise CorruptSnapshot(f"payload line {i + 1}: {exc}") from exc
+        idx = cls(dim=dim, capacity=count)
+        idx.extend((r["id"], vecs[i], dec(r.get("payload"))) for i, r in enumerate(recs))
+        return idx
+
+
+def check_unit(t, tol: float) -> None:
+    """Device-side unit-norm/finiteness check of a [n, dim] float32 CUDA tensor."""
+    torch = _torch()
+    L = _lib.load()
+    bad = torch.empty((t.shape[0],), dtype=torch.uint8, device="cuda")
+    _lib.check(L.pr_check_unit(_lib.ptr(t), t.shape[0], t.shape[1], tol, _lib.ptr(bad), _lib.stream_ptr()),
+               "check_unit")
+    if bool(bad.any().item()):
+        i = int(torch.nonzero(bad)[0].item())
+        raise InvalidVector(f"vector {i} is not finite unit-norm within {tol}")

@@ -1,0 +1,141 @@
+"""FlatIndex on the GPU vs the CPU oracle (reference index.py:155-189).
+
+Bit-exact: row ids, raw fp64 scores (numpy einsum order) and reported
+scores (snap + clamp) must equal the oracle's, in both the exact fp64 scan
+and the tcgen05 fp16 scan + certified rescoring.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import random_unit_vectors
+
+pytestmark = pytest.mark.gpu
+
+
+def _oracle():
+    from oracle import flat_index
+
+    return flat_index
+
+
+def _check(idx, X, Q, k, mode):
+    import torch
+
+    F = _oracle()
+    res = idx.search_batch(torch.from_numpy(Q), k, mode=mode)
+    torch.cuda.synchronize()
+    want = F.c_search(X, Q, k)
+    got_rows = res.rows.cpu().numpy()
+    got_raw = res.raw.cpu().numpy()
+    got_rep = res.scores.cpu().numpy()
+    got_cnt = res.count.cpu().numpy()
+    np.testing.assert_array_equal(got_cnt, want.count)
+    for b in range(Q.shape[0]):
+        c = want.count[b]
+        np.testing.assert_array_equal(got_rows[b, :c], want.rows[b, :c], err_msg=f"query {b} rows")
+        np.testing.assert_array_equal(got_raw[b, :c], want.raw[b, :c], err_msg=f"query {b} raw")
+        np.testing.assert_array_equal(got_rep[b, :c], want.reported[b, :c], err_msg=f"query {b} reported")
+    return res
+
+
+def _store(rng, n, d, dup=True):
+    X = random_unit_vectors(rng, n, d)
+    if dup and n >= 4:
+        X[n // 2] = X[1]
+        X[n - 1] = X[1]
+    return X
+
+
+@pytest.mark.parametrize("d", [4, 8, 13, 64, 384, 768, 1024])
+@pytest.mark.parametrize("k", [1, 3, 10])
+def test_exact_matches_oracle(gpu, rng, d, k):
+    from paper_2506_21593_b200 import MODE_EXACT, FlatIndex
+
+    n = 3000
+    X = _store(rng, n, d)
+    Q = random_unit_vectors(rng, 33, d)
+    Q[0] = X[1]  # tie-heavy probe with self-snap
+    Q[1] = X[7]
+    idx = FlatIndex(dim=d)
+    idx.extend_arrays([f"e{i}" for i in range(n)], X)
+    _check(idx, X, Q, k, MODE_EXACT)
+
+
+@pytest.mark.parametrize("d", [64, 384, 768, 1024, 100])
+@pytest.mark.parametrize("k", [1, 5, 10])
+def test_tensor_path_matches_oracle(gpu, rng, d, k):
+    from paper_2506_21593_b200 import MODE_TENSOR, FlatIndex
+
+    n = 20000 + 77
+    X = _store(rng, n, d)
+    Q = random_unit_vectors(rng, 300, d)
+    Q[0] = X[1]
+    Q[5] = X[n - 3]
+    # planted near-duplicates
+    for i in range(10, 60):
+        v = X[(i * 131) % n] + 0.05 * random_unit_vectors(rng, 1, d)[0]
+        Q[i] = (v / np.linalg.norm(v.astype(np.float64))).astype(np.float32)
+    idx = FlatIndex(dim=d)
+    idx.extend_arrays([f"e{i}" for i in range(n)], X)
+    _check(idx, X, Q, k, MODE_TENSOR)
+    st = idx.stats()
+    assert st.path == MODE_TENSOR
+    assert st.fallback < Q.shape[0]
+
+
+def test_tensor_path_fallback_on_ties(gpu, rng):
+    """Massive exact ties (one-hot rows) defeat the certificate; the exact
+    rescan must still give the oracle's answer."""
+    from paper_2506_21593_b200 import MODE_TENSOR, FlatIndex
+
+    d, n = 64, 20000
+    X = np.zeros((n, d), dtype=np.float32)
+    X[np.arange(n), np.arange(n) % d] = 1.0
+    Q = random_unit_vectors(rng, 130, d)
+    Q[3] = X[5]
+    idx = FlatIndex(dim=d)
+    idx.extend_arrays([f"e{i}" for i in range(n)], X)
+    _check(idx, X, Q, 10, MODE_TENSOR)
+    assert idx.stats().fallback > 0
+
+
+def test_empty_and_small(gpu, rng):
+    from paper_2506_21593_b200 import MODE_AUTO, MODE_EXACT, FlatIndex
+
+    idx = FlatIndex(dim=8)
+    q = random_unit_vectors(rng, 1, 8)[0]
+    assert idx.search(q, 5) == []
+    assert idx.search_count == 1
+    idx.insert("a", np.eye(8, dtype=np.float32)[0])
+    idx.insert("b", np.eye(8, dtype=np.float32)[1])
+    hits = idx.search(np.eye(8, dtype=np.float32)[0], 10)
+    assert [(h.entry_id, h.score, h.rank) for h in hits] == [("a", 1.0, 1), ("b", 0.0, 2)]
+    with pytest.raises(ValueError):
+        idx.search(q, 0)
+
+
+def test_upsert_keeps_row(gpu, rng):
+    from paper_2506_21593_b200 import FlatIndex
+
+    idx = FlatIndex(dim=16)
+    vs = random_unit_vectors(rng, 3, 16)
+    idx.insert("x", vs[0], 1)
+    idx.insert("y", vs[1], 2)
+    idx.insert("x", vs[1], 3)  # now x and y hold the same vector; x keeps row 0
+    hits = idx.search(vs[1], 2)
+    assert [h.entry_id for h in hits] == ["x", "y"]
+    assert hits[0].score == 1.0
+    assert idx.payload("x") == 3 and len(idx) == 2
+
+
+def test_big_k(gpu, rng):
+    from paper_2506_21593_b200 import FlatIndex
+
+    X = _store(rng, 500, 32)
+    Q = random_unit_vectors(rng, 4, 32)
+    idx = FlatIndex(dim=32)
+    idx.extend_arrays([f"e{i}" for i in range(500)], X)
+    _check(idx, X, Q, 100, 0)
+    _check(idx, X, Q, 700, 0)  # k > n truncates
