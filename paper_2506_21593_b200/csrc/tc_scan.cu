@@ -24,17 +24,16 @@
 
 namespace pr {
 
-constexpr int TC_STAGES = 3;
+constexpr int TC_STAGES = 4;
 constexpr int TC_THREADS = 256;
 constexpr int TC_A_BYTES = TC_BLOCK_M * TC_BLOCK_K * 2;  // 16 KB
 constexpr int TC_B_BYTES = TC_BLOCK_N * TC_BLOCK_K * 2;  // 32 KB
-constexpr int TC_BUF = 16;                               // per-thread staging of new candidates
 constexpr int TC_EPI_THREADS = 128;
 constexpr int TC_TMEM_COLS = 512;
 
 constexpr size_t tc_smem_bytes() {
     return 1024 /*alignment slack*/ + (size_t)TC_STAGES * (TC_A_BYTES + TC_B_BYTES) +
-           (size_t)(TC_KP + TC_BUF) * TC_EPI_THREADS * 8 + 256 /*barriers*/;
+           (size_t)32 * TC_EPI_THREADS * 4 /*per-thread score spill for candidate chunks*/ + 256 /*barriers*/;
 }
 
 // ---------------------------------------------------------------------------
@@ -129,21 +128,24 @@ __device__ __forceinline__ float key_score(uint64_t key) {
 }
 __device__ __forceinline__ uint32_t key_row(uint64_t key) { return 0xFFFFFFFFu - (uint32_t)key; }
 
-// merge the per-thread staging buffer into the per-thread sorted list.
-// lists are [slot][thread] in smem (conflict-free when threads move together).
-__device__ __noinline__ float flush_candidates(uint64_t *list, uint64_t *buf, int nb, int t) {
-    for (int b = 0; b < nb; ++b) {
-        uint64_t key = buf[b * TC_EPI_THREADS + t];
-        if (key <= list[(TC_KP - 1) * TC_EPI_THREADS + t]) continue;
-        int pos = TC_KP - 1;
-        while (pos > 0 && key > list[(pos - 1) * TC_EPI_THREADS + t]) {
-            list[pos * TC_EPI_THREADS + t] = list[(pos - 1) * TC_EPI_THREADS + t];
-            --pos;
-        }
-        list[pos * TC_EPI_THREADS + t] = key;
+// Insert (s, r) into a register-resident list sorted by (score desc, row asc).
+// Caller guarantees s > ts[TC_KP-1].  Rows arrive in ascending order, so
+// strict '>' keeps an equal earlier score ahead (lexsort's secondary key).
+// Branch-free: every slot takes its upper neighbour, the new entry, or stays.
+__device__ __forceinline__ void topk_insert(float (&ts)[TC_KP], uint32_t (&tr)[TC_KP], float s, uint32_t r) {
+#pragma unroll
+    for (int i = TC_KP - 1; i > 0; --i) {
+        const bool up = s > ts[i - 1];
+        const bool here = s > ts[i];
+        const float ns = up ? ts[i - 1] : (here ? s : ts[i]);
+        const uint32_t nr = up ? tr[i - 1] : (here ? r : tr[i]);
+        ts[i] = ns;
+        tr[i] = nr;
     }
-    uint64_t last = list[(TC_KP - 1) * TC_EPI_THREADS + t];
-    return last ? key_score(last) : -INFINITY;
+    if (s > ts[0]) {
+        ts[0] = s;
+        tr[0] = r;
+    }
 }
 
 struct TcScanParams {
@@ -161,9 +163,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
     uint8_t *sA = smem;
     uint8_t *sB = sA + TC_STAGES * TC_A_BYTES;
-    uint64_t *list = reinterpret_cast<uint64_t *>(sB + TC_STAGES * TC_B_BYTES);  // [TC_KP][128]
-    uint64_t *buf = list + TC_KP * TC_EPI_THREADS;                                // [TC_BUF][128]
-    uint64_t *full = buf + TC_BUF * TC_EPI_THREADS;
+    float *spill = reinterpret_cast<float *>(sB + TC_STAGES * TC_B_BYTES);  // [32][128]
+    uint64_t *full = reinterpret_cast<uint64_t *>(spill + 32 * TC_EPI_THREADS);
     uint64_t *empty = full + TC_STAGES;
     uint64_t *tfull = empty + TC_STAGES;
     uint64_t *tempty = tfull + 2;
@@ -244,9 +245,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         // ---------------- epilogue: TMEM -> registers -> top-K' ----------------
         const int et = threadIdx.x - 128;  // 0..127 == TMEM lane == query within tile
         const int ew = warp - 4;
-        for (int s = 0; s < TC_KP; ++s) list[s * TC_EPI_THREADS + et] = 0;
-        float thr = -INFINITY;
-        int nb = 0;
+        float ts[TC_KP];
+        uint32_t tr[TC_KP];
+#pragma unroll
+        for (int i = 0; i < TC_KP; ++i) {
+            ts[i] = -INFINITY;
+            tr[i] = 0xFFFFFFFFu;
+        }
         for (int i = 0; i < nlocal; ++i) {
             const int acc = i & 1;
             const uint32_t aphase = (i >> 1) & 1;
@@ -261,26 +266,31 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 const int64_t rb = rbase + c * 32;
                 const int64_t rem_rows = p.n - rb;
                 const int lim = rem_rows < 32 ? (int)rem_rows : 32;
+                const float thr = ts[TC_KP - 1];
+                uint32_t mask = 0;
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const float s = __uint_as_float(v[j]);
-                    if (j < lim && s > thr) {
-                        buf[nb * TC_EPI_THREADS + et] = cand_key(s, (uint32_t)(rb + j));
-                        if (++nb == TC_BUF) {
-                            thr = flush_candidates(list, buf, nb, et);
-                            nb = 0;
-                        }
-                    }
+                for (int j = 0; j < 32; ++j) mask |= (__uint_as_float(v[j]) > thr ? 1u : 0u) << j;
+                if (lim < 32) mask &= (lim <= 0) ? 0u : (0xFFFFFFFFu >> (32 - lim));
+                if (mask) {
+                    // rare: spill this chunk to smem so candidates can be indexed dynamically
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) spill[j * TC_EPI_THREADS + et] = __uint_as_float(v[j]);
+                    do {
+                        const int j = __ffs(mask) - 1;
+                        mask &= mask - 1;
+                        const float s = spill[j * TC_EPI_THREADS + et];
+                        if (s > ts[TC_KP - 1]) topk_insert(ts, tr, s, (uint32_t)(rb + j));
+                    } while (mask);
                 }
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
         }
-        flush_candidates(list, buf, nb, et);
         const int64_t q = (int64_t)qtile * TC_BLOCK_M + et;
         uint64_t *out = p.cand + (q * p.nsplit + split) * TC_KP;
-        for (int s = 0; s < TC_KP; ++s) out[s] = list[s * TC_EPI_THREADS + et];
+#pragma unroll
+        for (int s = 0; s < TC_KP; ++s) out[s] = (tr[s] == 0xFFFFFFFFu) ? 0ull : cand_key(ts[s], tr[s]);
     }
 
     tc_fence_before();

@@ -13,7 +13,7 @@ struct alignas(64) TcStoreMap {
 };
 
 // Candidates kept per (query, row split) by the tcgen05 epilogue.
-constexpr int TC_KP = 32;
+constexpr int TC_KP = 16;
 constexpr int TC_BLOCK_M = 128;  // queries per CTA (TMEM lanes)
 constexpr int TC_BLOCK_N = 256;  // store rows per MMA tile (TMEM columns)
 constexpr int TC_BLOCK_K = 64;   // fp16 columns per stage = one 128B swizzle atom
