@@ -1,0 +1,448 @@
+#!/usr/bin/env python
+"""bench.py — PentaRAG L5 retrieval top-k over a 10M x 1024 chunk store on B200.
+
+Workload (BASELINE.json configs[3], the metric's "top-k search QPS at
+10M x 1024"): one step = one batch of 4096 queries (25% planted
+near-duplicates, 75% random unit vectors) searched for the exact top-5 over a
+10,000,000 x 1024 float32 unit-vector store — FlatIndex.search semantics
+(reference index.py:155-189), results bit-identical to the fp64 reference.
+With --gpus N the store is row-sharded over N ranks (contiguous blocks) and
+every step does ONE all-gather of the per-rank top-k lists + a device merge
+(strong scaling: the total store and batch are fixed).
+
+  value         queries/s, device-timed (CUDA events), inputs resident in HBM,
+                max over ranks; the 20 GB fp16 store per step is far larger
+                than the 126 MB L2, so no flush is needed between steps
+  e2e           the same through the public API with HOST buffers: pinned
+                query batch H2D + search + D2H of rows/scores, per step
+  roofline      the tcgen05 scan kernel, 2*n*d*B FLOP per launch / its CUDA-
+                event duration (recorded inside libpentarag on the launching
+                stream) vs the measured sustained bf16/fp16 peak
+  cpu_baseline  rank 0 at N=1: the numpy einsum+lexsort restatement of
+                FlatIndex.search (oracle/) timed on this host's cores over the
+                full store for a bounded query sample, also used as a parity
+                check of the GPU results at full size
+
+--impl reference times that CPU path alone (rank 0; other ranks exit).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "routed queries/s through cache+retrieval layers; top-k search QPS at 10M×1024"
+CHUNK = 1 << 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=10_000_000)
+    ap.add_argument("--dim", type=int, default=1024)
+    ap.add_argument("--batch", type=int, default=4096)
+    ap.add_argument("--k", type=int, default=5)
+    ap.add_argument("--cpu-queries", type=int, default=16)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-rows", type=int, default=1_000_000, help="reference arm: rows per timed sample")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return p, "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled DURING the timed region
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "200",
+                 "-i", str(self.dev)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = max(mx, float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# synthetic data (deterministic per global 1M-row chunk, identical for any N)
+def gen_chunk(c: int, rows: int, dim: int):
+    import torch
+
+    g = torch.Generator(device="cuda").manual_seed(7_000_003 + c)
+    x = torch.randn((rows, dim), generator=g, device="cuda", dtype=torch.float32)
+    x = x.double()
+    return (x / x.norm(dim=1, keepdim=True)).float()
+
+
+def build_shard(n_total: int, dim: int, lo: int, hi: int):
+    from paper_2506_21593_b200 import FlatIndex
+
+    idx = FlatIndex(dim=dim, capacity=hi - lo)
+    c0, c1 = lo // CHUNK, (hi - 1) // CHUNK
+    for c in range(c0, c1 + 1):
+        rows = min(CHUNK, n_total - c * CHUNK)
+        x = gen_chunk(c, rows, dim)
+        a, b = max(lo, c * CHUNK) - c * CHUNK, min(hi, c * CHUNK + rows) - c * CHUNK
+        part = x[a:b].contiguous()
+        idx.extend_arrays([str(c * CHUNK + a + i) for i in range(b - a)], part, validate=False)
+        del x, part
+    return idx
+
+
+def make_queries(n_total: int, dim: int, batch: int):
+    import torch
+
+    g = torch.Generator(device="cuda").manual_seed(11)
+    q = torch.randn((batch, dim), generator=g, device="cuda", dtype=torch.float64)
+    q = q / q.norm(dim=1, keepdim=True)
+    nplant = batch // 4
+    base = gen_chunk(0, min(CHUNK, n_total), dim).double()
+    pick = torch.randint(0, base.shape[0], (nplant,), generator=g, device="cuda")
+    noise = torch.randn((nplant, dim), generator=g, device="cuda", dtype=torch.float64)
+    noise = noise / noise.norm(dim=1, keepdim=True)
+    p = base[pick] + 0.3 * noise
+    q[:nplant] = p / p.norm(dim=1, keepdim=True)
+    return q.float().contiguous()
+
+
+# ---------------------------------------------------------------------------
+# CPU path: numpy einsum + lexsort (oracle/flat_index.py restates index.py:173-176)
+def cpu_search_chunks(chunk_iter, Q32: np.ndarray, k: int, threads: int):
+    """Returns (rows, raw, seconds_timed).  Timed = the per-chunk einsum of every
+    sample query (threads over queries) + the final lexsort; the fp32->fp64
+    upcast is the reference's stored copy (index.py:145) and is not timed."""
+    from oracle import flat_index as F
+
+    P = Q32.shape[0]
+    q64 = Q32.astype(np.float64)
+    parts: list[list[np.ndarray]] = [[] for _ in range(P)]
+    timed = 0.0
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        for X32 in chunk_iter:
+            X64 = X32.astype(np.float64)
+            t0 = time.perf_counter()
+            res = list(ex.map(lambda i: np.einsum("ij,j->i", X64, q64[i]), range(P)))
+            timed += time.perf_counter() - t0
+            for i in range(P):
+                parts[i].append(res[i])
+            del X64
+        t0 = time.perf_counter()
+        scores = [np.concatenate(p) for p in parts]
+        orders = list(ex.map(lambda s: F.topk_from_scores(s, k), scores))
+        timed += time.perf_counter() - t0
+    rows = np.stack([o.astype(np.int64) for o in orders])
+    raw = np.stack([scores[i][orders[i]] for i in range(P)])
+    return rows, raw, timed
+
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ---------------------------------------------------------------------------
+def run_reference(a):
+    """--impl reference: the CPU FlatIndex.search restatement on host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = host_threads()
+    P = max(1, min(a.cpu_queries, threads))
+    rows_s = min(a.ref_rows, a.n)
+    rng = np.random.default_rng([7, 0])
+    X = rng.standard_normal((rows_s, a.dim), dtype=np.float32)
+    X /= np.linalg.norm(X.astype(np.float64), axis=1, keepdims=True).astype(np.float32)
+    X64 = X.astype(np.float64)  # the reference keeps this copy (index.py:145)
+    qrng = np.random.default_rng(11)
+    times = []
+    from oracle import flat_index as F
+
+    with ThreadPoolExecutor(max_workers=P) as ex:
+        for step in range(a.warmup + a.steps):
+            Q = qrng.standard_normal((P, a.dim))
+            Q /= np.linalg.norm(Q, axis=1, keepdims=True)
+            q64 = Q.astype(np.float32).astype(np.float64)
+            t0 = time.perf_counter()
+            list(ex.map(lambda i: F.topk_from_scores(np.einsum("ij,j->i", X64, q64[i]), a.k), range(P)))
+            dt = time.perf_counter() - t0
+            if step >= a.warmup:
+                times.append(dt)
+    scale = a.n / rows_s
+    per_step = statistics.mean(times) * scale  # seconds for P queries over the full store
+    value = P / per_step
+    sample = (f"{P} queries per step over a {rows_s}-row x {a.dim} slice, scaled x{scale:g} to the "
+              f"{a.n}-row store (cost is linear in rows); numpy einsum+lexsort restatement of "
+              f"FlatIndex.search, {P} threads")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": a.gpus,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"L5 retrieval top-k={a.k} over {a.n} x {a.dim} chunk store, batch {a.batch}",
+                   "n_rows": a.n, "dim": a.dim, "batch": a.batch, "k": a.k},
+        "cpu_baseline": {"value": value, "unit": "queries/s", "cores": P, "kind": "port", "sample": sample,
+                         "host_threads": threads, "cpu": cpu_model(), "numpy": np.__version__},
+        "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+        return
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2506_21593_b200 import _lib
+    from paper_2506_21593_b200.sharded import ShardedFlatIndex, shard_range
+
+    L = _lib.load()
+    lo, hi = shard_range(a.n, rank, world)
+    t_build = time.time()
+    idx = build_shard(a.n, a.dim, lo, hi)
+    q = make_queries(a.n, a.dim, a.batch)
+    sh = ShardedFlatIndex(idx, lo)
+    torch.cuda.synchronize()
+    build_s = time.time() - t_build
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    # ---- warm-up
+    for _ in range(a.warmup):
+        res = sh.search_batch(q, a.k)
+    torch.cuda.synchronize()
+    barrier()
+
+    # ---- device-timed region (inputs resident in HBM)
+    idx.set_timing(True)
+    idx.scan_time()  # reset
+    launches0 = L.pr_launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        ev0.record()
+        for _ in range(a.steps):
+            res = sh.search_batch(q, a.k)
+        ev1.record()
+        torch.cuda.synchronize()
+        barrier()
+    launches = L.pr_launch_count() - launches0
+    ms_total = max_over_ranks(ev0.elapsed_time(ev1))
+    scan_ms, scan_n = idx.scan_time()
+    idx.set_timing(False)
+    st = idx.stats()
+    ms_step = ms_total / a.steps
+    value = a.batch * a.steps / (ms_total / 1e3)
+    gpu_launches = int(sum_over_ranks(float(launches)))
+
+    # ---- e2e through the public API with host buffers
+    q_host = q.cpu().pin_memory()
+    out_rows = torch.empty((a.batch, a.k), dtype=torch.int64).pin_memory()
+    out_scores = torch.empty((a.batch, a.k), dtype=torch.float64).pin_memory()
+    out_count = torch.empty((a.batch,), dtype=torch.int32).pin_memory()
+
+    def e2e_step():
+        qd = q_host.to("cuda", non_blocking=True)
+        r = sh.search_batch(qd, a.k)
+        out_rows.copy_(r.rows, non_blocking=True)
+        out_scores.copy_(r.scores, non_blocking=True)
+        out_count.copy_(r.count, non_blocking=True)
+
+    for _ in range(min(2, a.warmup)):
+        e2e_step()
+    torch.cuda.synchronize()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(a.steps):
+        e2e_step()
+    e1.record()
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1))
+    e2e_value = a.batch * a.steps / (e2e_ms / 1e3)
+    h2d = world * a.batch * a.dim * 4
+    d2h = world * a.batch * (a.k * 16 + 4)
+
+    # ---- roofline of the tcgen05 scan (per launch, this rank's shard)
+    pk, pk_kind = peaks()
+    n_local = hi - lo
+    flop = 2.0 * n_local * a.dim * a.batch
+    kern_ms = scan_ms / max(1, scan_n)
+    achieved = flop / (kern_ms / 1e3) / 1e12
+    peak = float(pk.get("bf16_tflops_sustained", pk.get("bf16_tflops")))
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "tc_scan_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            tj = json.load(fh)
+        if tj.get("n_rows") == n_local and tj.get("dim") == a.dim and tj.get("batch") == a.batch:
+            traffic = tj.get("dram_bytes_per_launch")
+    roof = {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
+            "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": "tc_scan_kernel",
+            "kernel_ms": round(kern_ms, 4), "kernel_share_of_step": round(kern_ms / ms_step, 4),
+            "peak_kind": f"{pk_kind} bf16_tflops_sustained (kernel timed inside back-to-back steps)",
+            "flop_per_launch": flop}
+
+    # ---- CPU baseline + full-size parity (rank 0, N=1 only)
+    cpu = None
+    parity = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        threads = host_threads()
+        P = max(1, min(a.cpu_queries, threads))
+        sel = np.unique(np.concatenate([np.arange(P // 2), a.batch - 1 - np.arange(P - P // 2)]))
+        Qs = q[torch.from_numpy(sel).cuda()].cpu().numpy()
+
+        def chunks():
+            for r0 in range(0, n_local, CHUNK):
+                m = min(CHUNK, n_local - r0)
+                yield idx.read_rows(r0, m).cpu().numpy()
+
+        rows_cpu, raw_cpu, secs = cpu_search_chunks(chunks(), Qs, a.k, P)
+        got_rows = res.rows[torch.from_numpy(sel).cuda()].cpu().numpy()
+        got_raw = res.raw[torch.from_numpy(sel).cuda()].cpu().numpy()
+        mism = int((got_rows != rows_cpu).any(axis=1).sum())
+        score_bits = int((got_raw != raw_cpu).any(axis=1).sum())
+        parity = {"queries_checked": int(len(sel)), "row_mismatches": mism, "raw_score_mismatches": score_bits,
+                  "oracle": "numpy einsum+lexsort over the full store (oracle/flat_index.py)"}
+        cpu_value = len(sel) / secs
+        cpu = {"value": cpu_value, "unit": "queries/s", "cores": P, "kind": "port",
+               "sample": f"{len(sel)} of the batch's queries (half planted, half random) over the full "
+                         f"{n_local} x {a.dim} store: numpy einsum per 1M-row chunk + lexsort over all "
+                         f"scores (FlatIndex.search restatement), {P} threads; fp64 upcast not timed",
+               "seconds": secs, "host_threads": threads, "cpu": cpu_model(), "numpy": np.__version__}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": "queries/s", "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "fp16",
+            "dtype_detail": "fp16 tcgen05 scan with fp32 TMEM accumulation; candidates rescored in fp64 "
+                            "numpy-einsum order (results bit-identical to the fp64 reference)",
+            "data": "synthetic",
+            "config": {"workload": f"L5 retrieval top-k={a.k} over {a.n} x {a.dim} chunk store, batch {a.batch} "
+                                   f"(BASELINE configs[3]); rows sharded over {world} GPU(s), all-gather merge",
+                       "n_rows": a.n, "dim": a.dim, "batch": a.batch, "k": a.k,
+                       "queries": "25% planted near-duplicates, 75% random unit vectors",
+                       "l2": "inputs larger than L2 (fp16 store 2 B x rows x dim per step vs 126 MB L2); no flush",
+                       "parallelism": f"rowshard{world}"},
+            "e2e": {"value": round(e2e_value, 1), "unit": "queries/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h,
+                    "path": "ShardedFlatIndex.search_batch from pinned host queries, results copied to host"},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "parity": parity,
+            "gpu_launches": gpu_launches,
+            "clocks": clk.summary(),
+            "search_stats": {"fallback_queries_last_step": int(st.fallback),
+                             "rescored_candidates_last_step": int(st.candidates)},
+            "build_seconds": round(build_s, 1),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -104,6 +104,14 @@ int pr_index_append_from(pr_index *h, const pr_index *src, const int64_t *d_src_
 int pr_index_search(pr_index *h, const float *d_q, int64_t nq, int k, uint32_t mode, int64_t *d_rows,
                     double *d_raw, double *d_reported, int32_t *d_count, void *stream);
 int pr_index_last_stats(pr_index *h, pr_search_stats *out);
+/* Record CUDA events around the dominant scan kernel of every search (the
+ * tcgen05 scan, or the exact scan on the exact path); pr_index_scan_time
+ * synchronises, returns the summed kernel time and the number of timed
+ * launches since the previous call, and resets. */
+int pr_index_set_timing(pr_index *h, int enable);
+int pr_index_scan_time(pr_index *h, double *total_ms, int64_t *launches);
+/* number of kernels this library has launched in this process */
+long long pr_launch_count(void);
 
 /* Merge per-shard top-k lists into the global top-k (the NCCL all-gather
  * merge of a row-sharded store).  d_rows/d_raw are [nshard, nq, k] with

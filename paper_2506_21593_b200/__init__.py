@@ -22,7 +22,13 @@ from .errors import (
     InvalidVector,
     NativeLibraryMissing,
 )
+from .caches import CacheEntry, FixedKVCache, SemanticCache, writeback
+from .errors import MalformedJsonl
+from .generation import StubBackend, StubKnowledgeTable, generate_with_context, memory_recall
 from .index import MODE_AUTO, MODE_EXACT, MODE_TENSOR, BatchResult, FlatIndex, SearchHit
+from .knowledge import AdaptiveKnowledgeMemory, MainKnowledgeBase, ingest_corpus
+from .router import CascadeRouter, LayerProbe, RouterConfig, RouteTraceEvent, TraceLog, export_triples
+from .sharded import ShardedFlatIndex, shard_range
 from .records import CASCADE_ORDER, AnswerRecord, LayerTag, Passage, Query, TrainingTriple, validate_query
 from .vectors import DIMENSION, HASH_SEED, EmbeddingVector, HashEmbedder, cosine, tokenize
 

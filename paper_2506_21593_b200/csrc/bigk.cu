@@ -88,14 +88,17 @@ int big_k_search(const float *x32, int64_t n, int dp8, int d, const float *q, in
     for (int64_t q0 = 0; q0 < nq; q0 += chunk) {
         const int64_t nqc = std::min(chunk, nq - q0);
         int g = (int)std::min<int64_t>(ceil_div<int64_t>(nqc * dp8, 256), 4096);
+        ::pr::count_launch();
         bigk_pad_kernel<<<g, 256, 0, st>>>(q + q0 * d, nqc, d, dp8, qp);
         g = (int)std::min<int64_t>(ceil_div<int64_t>(nqc * n, 256), (int64_t)sm_count() * 32);
+        ::pr::count_launch();
         bigk_scores_kernel<<<g, 256, 0, st>>>(x32, n, dp8, d, qp, nqc, k_in, v_in, offs);
         PR_LAUNCH_CHECK();
         size_t tb = temp_bytes;
         PR_CUDA(cub::DeviceSegmentedSort::StableSortPairsDescending(temp, tb, k_in, k_out, v_in, v_out, nqc * n,
                                                                      (int)nqc, offs, offs + 1, st));
         g = (int)std::min<int64_t>(nqc, (int64_t)sm_count() * 8);
+        ::pr::count_launch();
         bigk_finalize_kernel<<<g, 128, 0, st>>>(k_out, v_out, n, nqc, q0, k, x32, dp8, d, qp, rows, raw, rep, count);
         PR_LAUNCH_CHECK();
     }

@@ -46,6 +46,10 @@ __host__ __device__ constexpr T round_up(T a, T b) {
 
 int sm_count();
 
+// every kernel launch of the library goes through PR_KERNEL so the host can
+// report how many of OUR kernels ran in a timed region (bench gpu_launches)
+void count_launch();
+
 // bump allocator over the scratch block
 struct Carve {
     char *base;

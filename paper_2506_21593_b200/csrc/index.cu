@@ -12,7 +12,10 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstring>
+#include <atomic>
 #include <mutex>
+#include <utility>
+#include <vector>
 
 #include "common.cuh"
 #include "select.cuh"
@@ -30,6 +33,9 @@ void set_error(const char *fmt, ...) {
     va_end(ap);
 }
 const char *last_error() { return g_err; }
+
+static std::atomic<long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 int sm_count() {
     static int cached = -1;
@@ -456,6 +462,9 @@ struct pr_index {
     size_t scratch_bytes = 0;
     int32_t *d_counters = nullptr;  // [4]: fallback count, candidate count, ...
     cudaStream_t last_stream = nullptr;
+    // optional per-launch timing of the dominant scan kernel (bench roofline)
+    bool timing = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pending, ev_free;
 };
 
 namespace pr {
@@ -468,6 +477,23 @@ static int ensure_scratch(pr_index *h, size_t bytes, cudaStream_t st) {
     size_t b = std::max(bytes, (size_t)(1 << 20));
     PR_CUDA(cudaMallocAsync(&h->scratch, b, st));
     h->scratch_bytes = b;
+    return PR_OK;
+}
+
+static int timing_pair(pr_index *h, cudaEvent_t *a, cudaEvent_t *b) {
+    *a = *b = nullptr;
+    if (!h->timing) return PR_OK;
+    std::pair<cudaEvent_t, cudaEvent_t> p;
+    if (!h->ev_free.empty()) {
+        p = h->ev_free.back();
+        h->ev_free.pop_back();
+    } else {
+        PR_CUDA(cudaEventCreate(&p.first));
+        PR_CUDA(cudaEventCreate(&p.second));
+    }
+    h->ev_pending.push_back(p);
+    *a = p.first;
+    *b = p.second;
     return PR_OK;
 }
 
@@ -524,6 +550,7 @@ static int launch_scan_t(const ScanArgs &a, int grid, cudaStream_t st) {
         PR_CUDA(cudaFuncSetAttribute(exact_scan_kernel<QT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         attr_set = true;
     }
+    ::pr::count_launch();
     exact_scan_kernel<QT><<<grid, SCAN_THREADS, smem, st>>>(a);
     PR_LAUNCH_CHECK();
     return PR_OK;
@@ -553,7 +580,8 @@ static void choose_splits(int64_t n, int qtiles_hint, int *nsplit, int64_t *rows
 // Exact path over a (possibly device-sized) selection of queries.  Results
 // are scattered to the output positions qsel[i] (or i).
 int exact_search(pr_index *h, const float *Qp, const int32_t *qsel, const int32_t *nsel_dev, int nsel_max, int k,
-                 int64_t *rows, double *raw, double *rep, int32_t *count, Carve &cv, cudaStream_t st) {
+                 int64_t *rows, double *raw, double *rep, int32_t *count, Carve &cv, cudaStream_t st,
+                 bool time_it) {
     const int K = k;
     int QT = pick_qt(nsel_max, h->dp8, K);
     int nsplit;
@@ -566,11 +594,19 @@ int exact_search(pr_index *h, const float *Qp, const int32_t *qsel, const int32_
     int64_t work = (int64_t)ceil_div(nsel_max, QT) * nsplit;
     int grid = (int)std::min<int64_t>(work, (int64_t)sm_count() * 2);
     if (grid < 1) grid = 1;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (time_it) {
+        int trc = timing_pair(h, &e0, &e1);
+        if (trc) return trc;
+    }
+    if (e0) PR_CUDA(cudaEventRecord(e0, st));
     int rc = launch_scan(QT, a, grid, st);
     if (rc) return rc;
+    if (e1) PR_CUDA(cudaEventRecord(e1, st));
     MergeArgs m{ps, prr, nsplit, K, k, std::min<int64_t>(k, h->count), qsel, nsel_dev, nsel_max,
                 h->x32, h->dp8, h->dim, Qp, rows, raw, rep, count};
     int mgrid = std::max(1, std::min(nsel_max, sm_count() * 8));
+    ::pr::count_launch();
     merge_topk_kernel<<<mgrid, 128, 0, st>>>(m);
     PR_LAUNCH_CHECK();
     h->stats.nsplit = nsplit;
@@ -613,6 +649,7 @@ int pr_check_unit(const float *d_vecs, int64_t n, int dim, double tol, uint8_t *
     if (n < 0 || dim < 1) PR_FAIL(PR_ERR_BAD_ARG, "pr_check_unit: bad shape");
     if (n == 0) return PR_OK;
     int64_t threads = n * 32;
+    ::pr::count_launch();
     check_unit_kernel<<<(unsigned)ceil_div<int64_t>(threads, 256), 256, 0, as_stream(stream)>>>(d_vecs, n, dim, tol, d_bad);
     PR_LAUNCH_CHECK();
     return PR_OK;
@@ -643,6 +680,8 @@ int pr_index_destroy(pr_index *h) {
     if (h->x16) cudaFree(h->x16);
     if (h->scratch) cudaFree(h->scratch);
     if (h->d_counters) cudaFree(h->d_counters);
+    for (auto &p : h->ev_pending) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
+    for (auto &p : h->ev_free) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
     delete h;
     return PR_OK;
 }
@@ -661,6 +700,7 @@ int pr_index_append(pr_index *h, const float *d_vecs, int64_t n, void *stream) {
     cudaStream_t st = as_stream(stream);
     int rc = reserve(h, h->count + n, st);
     if (rc) return rc;
+    ::pr::count_launch();
     write_rows_kernel<<<grid_for(n * h->dp64), 256, 0, st>>>(d_vecs, n, h->dim, nullptr, h->count, h->x32, h->dp8,
                                                               h->x16, h->dp64);
     PR_LAUNCH_CHECK();
@@ -671,6 +711,7 @@ int pr_index_append(pr_index *h, const float *d_vecs, int64_t n, void *stream) {
 int pr_index_update_rows(pr_index *h, const int64_t *d_rows, const float *d_vecs, int64_t n, void *stream) {
     if (!h || n < 0) PR_FAIL(PR_ERR_BAD_ARG, "bad update");
     if (n == 0) return PR_OK;
+    ::pr::count_launch();
     write_rows_kernel<<<grid_for(n * h->dp64), 256, 0, as_stream(stream)>>>(d_vecs, n, h->dim, d_rows, 0, h->x32,
                                                                              h->dp8, h->x16, h->dp64);
     PR_LAUNCH_CHECK();
@@ -692,6 +733,7 @@ int pr_index_truncate(pr_index *h, int64_t n) {
 int pr_index_read_rows(const pr_index *h, int64_t row0, int64_t n, float *d_out, void *stream) {
     if (!h || row0 < 0 || n < 0 || row0 + n > h->count) PR_FAIL(PR_ERR_BAD_ARG, "read_rows out of range");
     if (n == 0) return PR_OK;
+    ::pr::count_launch();
     read_rows_kernel<<<grid_for(n * h->dim), 256, 0, as_stream(stream)>>>(h->x32, h->dp8, h->dim, row0, n, d_out);
     PR_LAUNCH_CHECK();
     return PR_OK;
@@ -703,6 +745,7 @@ int pr_index_append_from(pr_index *h, const pr_index *src, const int64_t *d_src_
     cudaStream_t st = as_stream(stream);
     int rc = reserve(h, h->count + n, st);
     if (rc) return rc;
+    ::pr::count_launch();
     gather_rows_kernel<<<grid_for(n * h->dp64), 256, 0, st>>>(src->x32, src->x16, d_src_rows, n, h->dp8, h->dp64,
                                                                h->count, h->x32, h->x16);
     PR_LAUNCH_CHECK();
@@ -723,6 +766,7 @@ int pr_index_search(pr_index *h, const float *d_q, int64_t nq, int k, uint32_t m
     if (nq == 0) return PR_OK;
     if (h->count == 0 || k > KMAX_EXACT) {
         if (h->count == 0) {
+            ::pr::count_launch();
             empty_result_kernel<<<(unsigned)ceil_div<int64_t>(nq * k, 256), 256, 0, st>>>(nq, k, d_rows, d_raw,
                                                                                          d_reported, d_count);
             PR_LAUNCH_CHECK();
@@ -741,12 +785,13 @@ int pr_index_search(pr_index *h, const float *d_q, int64_t nq, int k, uint32_t m
     if (rc) return rc;
     Carve cv{reinterpret_cast<char *>(h->scratch)};
     float *Qp = cv.take<float>((size_t)nq * h->dp8);
+    ::pr::count_launch();
     pad_queries_kernel<<<grid_for(nq * h->dp8), 256, 0, st>>>(d_q, nq, h->dim, h->dp8, Qp);
     PR_LAUNCH_CHECK();
 
     if (!use_tc) {
         h->stats.path = PR_SEARCH_EXACT;
-        return exact_search(h, Qp, nullptr, nullptr, (int)nq, k, d_rows, d_raw, d_reported, d_count, cv, st);
+        return exact_search(h, Qp, nullptr, nullptr, (int)nq, k, d_rows, d_raw, d_reported, d_count, cv, st, true);
     }
     h->stats.path = PR_SEARCH_TENSOR;
     if (!h->tmap_ok) {
@@ -771,12 +816,40 @@ int pr_index_search(pr_index *h, const float *d_q, int64_t nq, int k, uint32_t m
     ts.rep = d_reported;
     ts.count = d_count;
     ts.counters = h->d_counters;
+    rc = timing_pair(h, &ts.ev_begin, &ts.ev_end);
+    if (rc) return rc;
     rc = pr::tc_search(ts, cv, st, &h->stats);
     if (rc) return rc;
     // certificate failures -> exact rescan of just those queries (device-sized list)
     return exact_search(h, Qp, ts.fallback_list, h->d_counters, (int)nq, k, d_rows, d_raw, d_reported, d_count, cv,
-                        st);
+                        st, false);
 }
+
+int pr_index_set_timing(pr_index *h, int enable) {
+    if (!h) PR_FAIL(PR_ERR_BAD_ARG, "null handle");
+    h->timing = enable != 0;
+    return PR_OK;
+}
+
+int pr_index_scan_time(pr_index *h, double *total_ms, int64_t *launches) {
+    if (!h) PR_FAIL(PR_ERR_BAD_ARG, "null handle");
+    double tot = 0.0;
+    int64_t n = 0;
+    for (auto &p : h->ev_pending) {
+        PR_CUDA(cudaEventSynchronize(p.second));
+        float ms = 0.f;
+        PR_CUDA(cudaEventElapsedTime(&ms, p.first, p.second));
+        tot += ms;
+        ++n;
+        h->ev_free.push_back(p);
+    }
+    h->ev_pending.clear();
+    if (total_ms) *total_ms = tot;
+    if (launches) *launches = n;
+    return PR_OK;
+}
+
+long long pr_launch_count(void) { return g_launches.load(); }
 
 int pr_index_last_stats(pr_index *h, pr_search_stats *out) {
     if (!h || !out) PR_FAIL(PR_ERR_BAD_ARG, "null");
@@ -798,6 +871,7 @@ int pr_index_snap_flags(const pr_index *h, const float *d_q, int64_t nq, int k, 
     if (!h || nq < 0 || k < 1) PR_FAIL(PR_ERR_BAD_ARG, "bad snap_flags");
     if (nq == 0) return PR_OK;
     int64_t threads = nq * k * 32;
+    ::pr::count_launch();
     snap_flags_kernel<<<(unsigned)ceil_div<int64_t>(threads, 256), 256, 0, as_stream(stream)>>>(
         h->x32, h->dp8, h->dim, d_q, nq, k, d_rows, d_raw, d_count, row_offset, d_snap);
     PR_LAUNCH_CHECK();
@@ -809,6 +883,7 @@ int pr_merge_shards(const int64_t *d_rows, const double *d_raw, const uint8_t *d
                     int32_t *d_out_count, void *stream) {
     if (nshard < 1 || nshard > 64 || nq < 0 || k < 1) PR_FAIL(PR_ERR_BAD_ARG, "bad merge_shards");
     if (nq == 0) return PR_OK;
+    ::pr::count_launch();
     merge_shards_kernel<<<(unsigned)ceil_div<int64_t>(nq, 128), 128, 0, as_stream(stream)>>>(
         d_rows, d_raw, d_snap, d_count, nshard, nq, k, d_out_rows, d_out_raw, d_out_reported, d_out_count);
     PR_LAUNCH_CHECK();

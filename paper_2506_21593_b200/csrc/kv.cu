@@ -265,6 +265,7 @@ static int grow(pr_kv *h, int64_t need_keys, cudaStream_t st) {
     if (rc) return rc;
     PR_CUDA(cudaMemsetAsync(h->d_count, 0, 2 * sizeof(unsigned long long), st));
     int g = (int)std::min<int64_t>(ceil_div<int64_t>(on, 256), (int64_t)sm_count() * 16);
+    ::pr::count_launch();
     kv_reinsert_kernel<<<g, 256, 0, st>>>(os, ov, on, h->slots, h->vals, h->nslots, h->d_count);
     PR_LAUNCH_CHECK();
     PR_CUDA(cudaStreamSynchronize(st));
@@ -290,6 +291,7 @@ int pr_fingerprint(const uint8_t *d_bytes, const int64_t *d_off, int64_t n, uint
     if (n < 0) PR_FAIL(PR_ERR_BAD_ARG, "n < 0");
     if (n == 0) return PR_OK;
     int g = (int)std::min<int64_t>(ceil_div<int64_t>(n, 256), (int64_t)sm_count() * 16);
+    ::pr::count_launch();
     fingerprint_kernel<<<g, 256, 0, as_stream(stream)>>>(d_bytes, d_off, n, d_fp);
     PR_LAUNCH_CHECK();
     return PR_OK;
@@ -328,6 +330,7 @@ int pr_kv_put(pr_kv *h, const uint64_t *d_fp, const int64_t *d_vals, int64_t n, 
         int rc = grow(h, h->upper + n, st);
         if (rc) return rc;
     }
+    ::pr::count_launch();
     kv_probe_kernel<1><<<probe_grid(n), 256, 0, st>>>(h->slots, h->vals, h->nslots, h->d_count, d_fp, nullptr, nullptr,
                                                       n, d_vals, nullptr, nullptr);
     PR_LAUNCH_CHECK();
@@ -338,6 +341,7 @@ int pr_kv_put(pr_kv *h, const uint64_t *d_fp, const int64_t *d_vals, int64_t n, 
 int pr_kv_get(pr_kv *h, const uint64_t *d_fp, int64_t n, int64_t *d_vals, uint8_t *d_hit, void *stream) {
     if (!h || n < 0) PR_FAIL(PR_ERR_BAD_ARG, "bad kv_get");
     if (n == 0) return PR_OK;
+    ::pr::count_launch();
     kv_probe_kernel<0><<<probe_grid(n), 256, 0, as_stream(stream)>>>(h->slots, h->vals, h->nslots, h->d_count, d_fp,
                                                                      nullptr, nullptr, n, nullptr, d_vals, d_hit);
     PR_LAUNCH_CHECK();
@@ -348,6 +352,7 @@ int pr_kv_get_text(pr_kv *h, const uint8_t *d_bytes, const int64_t *d_off, int64
                    void *stream) {
     if (!h || n < 0) PR_FAIL(PR_ERR_BAD_ARG, "bad kv_get_text");
     if (n == 0) return PR_OK;
+    ::pr::count_launch();
     kv_probe_kernel<0><<<probe_grid(n), 256, 0, as_stream(stream)>>>(h->slots, h->vals, h->nslots, h->d_count, nullptr,
                                                                      d_bytes, d_off, n, nullptr, d_vals, d_hit);
     PR_LAUNCH_CHECK();
@@ -357,6 +362,7 @@ int pr_kv_get_text(pr_kv *h, const uint8_t *d_bytes, const int64_t *d_off, int64
 int pr_kv_erase(pr_kv *h, const uint64_t *d_fp, int64_t n, void *stream) {
     if (!h || n < 0) PR_FAIL(PR_ERR_BAD_ARG, "bad kv_erase");
     if (n == 0) return PR_OK;
+    ::pr::count_launch();
     kv_probe_kernel<2><<<probe_grid(n), 256, 0, as_stream(stream)>>>(h->slots, h->vals, h->nslots, h->d_count, d_fp,
                                                                      nullptr, nullptr, n, nullptr, nullptr, nullptr);
     PR_LAUNCH_CHECK();
@@ -389,6 +395,7 @@ int64_t pr_kv_export(pr_kv *h, uint64_t *d_fp, int64_t *d_vals, int64_t max, voi
     PR_CUDA(cudaMallocAsync(&cur, sizeof(unsigned long long), st));
     PR_CUDA(cudaMemsetAsync(cur, 0, sizeof(unsigned long long), st));
     int g = (int)std::min<int64_t>(ceil_div<int64_t>(h->nslots, 256), (int64_t)sm_count() * 16);
+    ::pr::count_launch();
     kv_export_kernel<<<g, 256, 0, st>>>(h->slots, h->vals, h->nslots, d_fp, d_vals, max, cur);
     PR_LAUNCH_CHECK();
     unsigned long long c = 0;

@@ -575,6 +575,7 @@ int tc_search(TcSearch &s, Carve &cv, cudaStream_t st, pr_search_stats *stats) {
     {
         int64_t total = nq_pad * s.dp64;
         int grid = (int)std::min<int64_t>(ceil_div<int64_t>(total, 256), (int64_t)sm_count() * 16);
+        ::pr::count_launch();
         queries_to_f16_kernel<<<grid, 256, 0, st>>>(s.qp, s.nq, s.dp8, s.d, nq_pad, s.dp64, q16);
         PR_LAUNCH_CHECK();
     }
@@ -589,13 +590,17 @@ int tc_search(TcSearch &s, Carve &cv, cudaStream_t st, pr_search_stats *stats) {
     }
     TcScanParams p{s.n, s.dp64 / TC_BLOCK_K, nsplit, tps, (int)ntiles, cand};
     dim3 grid((unsigned)qtiles, (unsigned)nsplit);
+    ::pr::count_launch();
+    if (s.ev_begin) PR_CUDA(cudaEventRecord(s.ev_begin, st));
     tc_scan_kernel<<<grid, TC_THREADS, tc_smem_bytes(), st>>>(qmap.map, s.store_map->map, p);
     PR_LAUNCH_CHECK();
+    if (s.ev_end) PR_CUDA(cudaEventRecord(s.ev_end, st));
 
     PR_CUDA(cudaMemsetAsync(s.counters, 0, 4 * sizeof(int32_t), st));
     RescoreArgs ra{cand, nsplit, s.nq, s.k, std::min<int64_t>(s.k, s.n), tc_error_bound(s.d, s.dp64), s.x32,
                    s.dp8, s.d, s.qp, s.rows, s.raw, s.rep, s.count, s.counters, s.fallback_list};
     int rgrid = (int)std::min<int64_t>(s.nq, (int64_t)sm_count() * 16);
+    ::pr::count_launch();
     tc_rescore_kernel<<<rgrid, RS_THREADS, 0, st>>>(ra);
     PR_LAUNCH_CHECK();
     stats->nsplit = nsplit;

@@ -35,6 +35,7 @@ struct TcSearch {
     int32_t *count;
     int32_t *counters;      // [0] fallback count, [1] rescored candidates
     int32_t *fallback_list; // out: query ids failing the certificate
+    cudaEvent_t ev_begin = nullptr, ev_end = nullptr;  // optional scan-kernel timing
 };
 
 bool tc_eligible(int d, int64_t n, int k);

@@ -69,3 +69,11 @@ class DeviceUnavailable(DeviceError):
 
 class NativeLibraryMissing(DeviceUnavailable):
     code = "native_library_missing"
+
+
+class MalformedJsonl(CascadeError):
+    code = "malformed_jsonl"
+
+    def __init__(self, message: str, line_number: int | None = None):
+        super().__init__(message)
+        self.line_number = line_number

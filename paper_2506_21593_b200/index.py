@@ -279,6 +279,16 @@ class FlatIndex:
                 _lib.check(rc, "pr_index_search")
         return out
 
+    def set_timing(self, enable: bool = True) -> None:
+        """Record CUDA events around the dominant scan kernel of every search."""
+        _lib.check(self._L.pr_index_set_timing(self._h, 1 if enable else 0), "set_timing")
+
+    def scan_time(self) -> tuple[float, int]:
+        """(summed kernel ms, launches) since the last call; synchronises."""
+        ms, n = ctypes.c_double(), ctypes.c_int64()
+        _lib.check(self._L.pr_index_scan_time(self._h, ctypes.byref(ms), ctypes.byref(n)), "scan_time")
+        return ms.value, n.value
+
     def stats(self) -> _lib.SearchStats:
         st = _lib.SearchStats()
         _lib.check(self._L.pr_index_last_stats(self._h, ctypes.byref(st)), "last_stats")

