@@ -49,7 +49,7 @@ CHUNK = 1 << 20
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--n", type=int, default=10_000_000)
@@ -74,14 +74,15 @@ def peaks():
 # ---------------------------------------------------------------------------
 # clocks sampled DURING the timed region
 class ClockSampler:
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, device_index: int):
         self.dev = device_index
         self.proc = None
-        self.lines: list[str] = []
+        self.lines: list[tuple[float, str]] = []
+        self.window = (0.0, float("inf"))
 
     def __enter__(self):
         try:
@@ -96,7 +97,10 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
+
+    def mark(self, t0: float, t1: float):
+        self.window = (t0, t1)
 
     def __exit__(self, *a):
         if self.proc:
@@ -109,7 +113,10 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lo, hi = self.window
+        for ts, ln in self.lines:
+            if not (lo - 0.25 <= ts <= hi + 0.25):  # arrival time of the sample line
+                continue
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 9:
                 continue
@@ -319,13 +326,16 @@ def main():
     launches0 = L.pr_launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
+        time.sleep(1.0)  # let nvidia-smi start sampling before the timed region
         barrier()
         torch.cuda.synchronize()
+        w0 = time.time()
         ev0.record()
         for _ in range(a.steps):
             res = sh.search_batch(q, a.k)
         ev1.record()
         torch.cuda.synchronize()
+        clk.mark(w0, time.time())
         barrier()
     launches = L.pr_launch_count() - launches0
     ms_total = max_over_ranks(ev0.elapsed_time(ev1))

@@ -51,7 +51,7 @@ def encode_texts(texts: Sequence[str]):
     off = np.zeros(len(bs) + 1, dtype=np.int64)
     if bs:
         np.cumsum([len(b) for b in bs], out=off[1:])
-    data = np.frombuffer(b"".join(bs) or b"\0", dtype=np.uint8)
+    data = np.frombuffer(b"".join(bs) or b"\0", dtype=np.uint8).copy()
     return data, off
 
 

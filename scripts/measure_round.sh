@@ -1,0 +1,21 @@
+#!/usr/bin/env bash
+# One GPU measurement pass (run under gpurun): bench line, reference arm, ncu
+# launch list of the bench command, one ncu --set full capture of the top
+# kernel.  Everything lands in gpurun_out/; the summaries worth keeping are
+# copied into profiles/ afterwards.
+set -u
+R=${1:-r01}
+mkdir -p gpurun_out
+timeout 900 python bench.py > gpurun_out/bench_${R}.json 2> gpurun_out/bench_${R}.err
+tail -c 3000 gpurun_out/bench_${R}.json
+timeout 600 python bench.py --impl reference > gpurun_out/bench_ref_${R}.json 2> gpurun_out/bench_ref_${R}.err
+tail -c 1500 gpurun_out/bench_ref_${R}.json
+# per-launch device times (cold-cache, serialised: compare shares, not absolutes)
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file gpurun_out/launches_${R}.csv python bench.py --steps 3 --warmup 1 --no-cpu-baseline \
+    > gpurun_out/launches_${R}.log 2>&1
+# full capture of one tcgen05 scan launch at the bench configuration
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:tc_scan_kernel -s 1 -c 1 \
+    -o gpurun_out/tc_scan_${R} python bench.py --steps 2 --warmup 1 --no-cpu-baseline \
+    > gpurun_out/ncu_full_${R}.log 2>&1
+tail -3 gpurun_out/ncu_full_${R}.log
