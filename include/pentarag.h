@@ -103,6 +103,12 @@ int pr_index_append_from(pr_index *h, const pr_index *src, const int64_t *d_src_
  * k must be >= 1 (PR_ERR_BAD_ARG otherwise). An empty index gives count 0. */
 int pr_index_search(pr_index *h, const float *d_q, int64_t nq, int k, uint32_t mode, int64_t *d_rows,
                     double *d_raw, double *d_reported, int32_t *d_count, void *stream);
+/* As pr_index_search, with a per-query visibility limit: query q only sees
+ * rows [0, d_row_limit[q]) (NULL = all rows).  This is the store "as of"
+ * an earlier point of a sequential stream: the batched cascade uses it so
+ * query j sees exactly the rows written back by queries i < j. */
+int pr_index_search_ex(pr_index *h, const float *d_q, int64_t nq, int k, uint32_t mode, const int64_t *d_row_limit,
+                       int64_t *d_rows, double *d_raw, double *d_reported, int32_t *d_count, void *stream);
 int pr_index_last_stats(pr_index *h, pr_search_stats *out);
 /* Record CUDA events around the dominant scan kernel of every search (the
  * tcgen05 scan, or the exact scan on the exact path); pr_index_scan_time

@@ -25,11 +25,12 @@ __global__ void bigk_pad_kernel(const float *__restrict__ q, int64_t nq, int d, 
 
 __global__ void bigk_scores_kernel(const float *__restrict__ x32, int64_t n, int dp8, int d, const float *__restrict__ qp,
                                    int64_t nqc, double *__restrict__ keys, int64_t *__restrict__ vals,
-                                   int64_t *__restrict__ offs) {
+                                   int64_t *__restrict__ offs, const int64_t *__restrict__ lim) {
     int64_t total = nqc * n;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
         int64_t qi = t / n, r = t - qi * n;
-        keys[t] = einsum_dot_f32(x32 + r * dp8, qp + qi * dp8, d);
+        // rows past the query's limit sort last and are never taken
+        keys[t] = (lim && r >= lim[qi]) ? -INFINITY : einsum_dot_f32(x32 + r * dp8, qp + qi * dp8, d);
         vals[t] = r;
         if (r == 0) offs[qi] = t;
         if (t == total - 1) offs[nqc] = total;
@@ -39,10 +40,11 @@ __global__ void bigk_scores_kernel(const float *__restrict__ x32, int64_t n, int
 __global__ void bigk_finalize_kernel(const double *__restrict__ keys, const int64_t *__restrict__ vals, int64_t n,
                                      int64_t nqc, int64_t q0, int k, const float *__restrict__ x32, int dp8, int d,
                                      const float *__restrict__ qp, int64_t *rows, double *raw, double *rep,
-                                     int32_t *count) {
-    const int64_t take = (int64_t)k < n ? (int64_t)k : n;
+                                     int32_t *count, const int64_t *__restrict__ lim) {
+    const int64_t take_all = (int64_t)k < n ? (int64_t)k : n;
     for (int64_t qi = blockIdx.x; qi < nqc; qi += gridDim.x) {
         const int64_t q = q0 + qi;
+        const int64_t take = lim ? min(take_all, max((int64_t)0, lim[qi])) : take_all;
         for (int64_t j = 0; j < k; ++j) {
             const int64_t o = q * k + j;
             if (j >= take) {
@@ -67,8 +69,8 @@ __global__ void bigk_finalize_kernel(const double *__restrict__ keys, const int6
     }
 }
 
-int big_k_search(const float *x32, int64_t n, int dp8, int d, const float *q, int64_t nq, int k, int64_t *rows,
-                 double *raw, double *rep, int32_t *count, cudaStream_t st) {
+int big_k_search(const float *x32, int64_t n, int dp8, int d, const float *q, int64_t nq, int k,
+                 const int64_t *row_limit, int64_t *rows, double *raw, double *rep, int32_t *count, cudaStream_t st) {
     const size_t budget = (size_t)256 << 20;
     int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(nq, (int64_t)(budget / ((size_t)n * 32 + 1))));
     float *qp = nullptr;
@@ -92,14 +94,16 @@ int big_k_search(const float *x32, int64_t n, int dp8, int d, const float *q, in
         bigk_pad_kernel<<<g, 256, 0, st>>>(q + q0 * d, nqc, d, dp8, qp);
         g = (int)std::min<int64_t>(ceil_div<int64_t>(nqc * n, 256), (int64_t)sm_count() * 32);
         ::pr::count_launch();
-        bigk_scores_kernel<<<g, 256, 0, st>>>(x32, n, dp8, d, qp, nqc, k_in, v_in, offs);
+        const int64_t *lim = row_limit ? row_limit + q0 : nullptr;
+        bigk_scores_kernel<<<g, 256, 0, st>>>(x32, n, dp8, d, qp, nqc, k_in, v_in, offs, lim);
         PR_LAUNCH_CHECK();
         size_t tb = temp_bytes;
         PR_CUDA(cub::DeviceSegmentedSort::StableSortPairsDescending(temp, tb, k_in, k_out, v_in, v_out, nqc * n,
                                                                      (int)nqc, offs, offs + 1, st));
         g = (int)std::min<int64_t>(nqc, (int64_t)sm_count() * 8);
         ::pr::count_launch();
-        bigk_finalize_kernel<<<g, 128, 0, st>>>(k_out, v_out, n, nqc, q0, k, x32, dp8, d, qp, rows, raw, rep, count);
+        bigk_finalize_kernel<<<g, 128, 0, st>>>(k_out, v_out, n, nqc, q0, k, x32, dp8, d, qp, rows, raw, rep, count,
+                                                lim);
         PR_LAUNCH_CHECK();
     }
     cudaFreeAsync(qp, st);

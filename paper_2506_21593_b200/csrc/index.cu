@@ -155,6 +155,7 @@ struct ScanArgs {
     double *part_s;
     int64_t *part_r;
     int32_t *part_c;
+    const int64_t *row_limit;  // per original query: rows >= limit are invisible (nullable)
 };
 
 constexpr int SCAN_THREADS = 256;
@@ -174,13 +175,31 @@ __global__ void __launch_bounds__(SCAN_THREADS) exact_scan_kernel(ScanArgs p) {
     const int qtiles = (nsel + QT - 1) / QT;
     const int64_t work = (int64_t)qtiles * p.nsplit;
     const int d = p.d, K = p.K;
+    __shared__ int64_t qlim[QT];
+    __shared__ int64_t tile_lim;
 
     for (int64_t w = blockIdx.x; w < work; w += gridDim.x) {
         const int qt = (int)(w / p.nsplit);
         const int split = (int)(w - (int64_t)qt * p.nsplit);
         const int64_t row_begin = (int64_t)split * p.rows_per_split;
-        const int64_t row_end = min(p.n, row_begin + p.rows_per_split);
         __syncthreads();
+        if (tid == 0) {
+            int64_t mx = 0;
+            for (int qi = 0; qi < QT; ++qi) {
+                const int sel = qt * QT + qi;
+                int64_t lim = 0;
+                if (sel < nsel) {
+                    const int qidx = p.qsel ? p.qsel[sel] : sel;
+                    lim = p.row_limit ? min(p.n, p.row_limit[qidx]) : p.n;
+                }
+                qlim[qi] = lim;
+                mx = max(mx, lim);
+            }
+            tile_lim = mx;
+        }
+        __syncthreads();
+        // rows no query of this tile can see are not scanned at all
+        const int64_t row_end = min(tile_lim, row_begin + p.rows_per_split);
         for (int i = tid; i < QT * qs_stride; i += SCAN_THREADS) {
             int qi = i / qs_stride, j = i - qi * qs_stride;
             int sel = qt * QT + qi;
@@ -243,7 +262,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) exact_scan_kernel(ScanArgs p) {
                 for (int c = 0; c < SCAN_THREADS / 32; ++c) {
                     const int64_t rr = r0 + c * 32 + lane;
                     const double s = sc[qi * SCAN_THREADS + c * 32 + lane];
-                    const bool valid = rr < row_end;
+                    const bool valid = rr < row_end && rr < qlim[qi];
                     double thr = (cnt == K) ? ls[K - 1] : -INFINITY;
                     unsigned m = __ballot_sync(0xffffffffu, valid && (cnt < K || s > thr));
                     while (m) {
@@ -320,6 +339,7 @@ struct MergeArgs {
     double *out_raw;
     double *out_rep;
     int32_t *out_count;
+    const int64_t *row_limit;  // nullable, per original query
 };
 
 __global__ void __launch_bounds__(128) merge_topk_kernel(MergeArgs a) {
@@ -332,12 +352,13 @@ __global__ void __launch_bounds__(128) merge_topk_kernel(MergeArgs a) {
         const double *ps = a.part_s + (int64_t)sel * M;
         const int64_t *pr_ = a.part_r + (int64_t)sel * M;
         const float *q = a.Q + (int64_t)qidx * a.xstride;
+        const int64_t take = a.row_limit ? min(a.take, max((int64_t)0, a.row_limit[qidx])) : a.take;
         double last_s = INFINITY;
         int64_t last_r = -1;
         for (int j = 0; j < a.k; ++j) {
             double bs = -INFINITY;
             int64_t br = -1;
-            if (j < a.take) {
+            if (j < take) {
                 for (int e = threadIdx.x; e < M; e += blockDim.x) {
                     int64_t r = pr_[e];
                     if (r < 0) continue;
@@ -366,7 +387,7 @@ __global__ void __launch_bounds__(128) merge_topk_kernel(MergeArgs a) {
             last_s = bs;
             last_r = br;
         }
-        if (threadIdx.x == 0) a.out_count[qidx] = (int32_t)a.take;
+        if (threadIdx.x == 0) a.out_count[qidx] = (int32_t)take;
     }
 }
 
@@ -547,7 +568,7 @@ static int launch_scan_t(const ScanArgs &a, int grid, cudaStream_t st) {
     size_t smem = scan_smem_bytes(QT, a.xstride, a.K);
     static bool attr_set = false;
     if (!attr_set) {
-        PR_CUDA(cudaFuncSetAttribute(exact_scan_kernel<QT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        PR_CUDA(cudaFuncSetAttribute(exact_scan_kernel<QT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 208 * 1024));
         attr_set = true;
     }
     ::pr::count_launch();
@@ -581,7 +602,7 @@ static void choose_splits(int64_t n, int qtiles_hint, int *nsplit, int64_t *rows
 // are scattered to the output positions qsel[i] (or i).
 int exact_search(pr_index *h, const float *Qp, const int32_t *qsel, const int32_t *nsel_dev, int nsel_max, int k,
                  int64_t *rows, double *raw, double *rep, int32_t *count, Carve &cv, cudaStream_t st,
-                 bool time_it) {
+                 bool time_it, const int64_t *row_limit) {
     const int K = k;
     int QT = pick_qt(nsel_max, h->dp8, K);
     int nsplit;
@@ -590,7 +611,8 @@ int exact_search(pr_index *h, const float *Qp, const int32_t *qsel, const int32_
     double *ps = cv.take<double>((size_t)nsel_max * nsplit * K);
     int64_t *prr = cv.take<int64_t>((size_t)nsel_max * nsplit * K);
     int32_t *pc = cv.take<int32_t>((size_t)nsel_max * nsplit);
-    ScanArgs a{h->x32, h->count, h->dp8, h->dim, Qp, qsel, nsel_dev, nsel_max, nsplit, rps, K, ps, prr, pc};
+    ScanArgs a{h->x32, h->count, h->dp8, h->dim, Qp, qsel, nsel_dev, nsel_max, nsplit, rps, K, ps, prr, pc,
+               row_limit};
     int64_t work = (int64_t)ceil_div(nsel_max, QT) * nsplit;
     int grid = (int)std::min<int64_t>(work, (int64_t)sm_count() * 2);
     if (grid < 1) grid = 1;
@@ -604,7 +626,7 @@ int exact_search(pr_index *h, const float *Qp, const int32_t *qsel, const int32_
     if (rc) return rc;
     if (e1) PR_CUDA(cudaEventRecord(e1, st));
     MergeArgs m{ps, prr, nsplit, K, k, std::min<int64_t>(k, h->count), qsel, nsel_dev, nsel_max,
-                h->x32, h->dp8, h->dim, Qp, rows, raw, rep, count};
+                h->x32, h->dp8, h->dim, Qp, rows, raw, rep, count, row_limit};
     int mgrid = std::max(1, std::min(nsel_max, sm_count() * 8));
     ::pr::count_launch();
     merge_topk_kernel<<<mgrid, 128, 0, st>>>(m);
@@ -755,6 +777,11 @@ int pr_index_append_from(pr_index *h, const pr_index *src, const int64_t *d_src_
 
 int pr_index_search(pr_index *h, const float *d_q, int64_t nq, int k, uint32_t mode, int64_t *d_rows, double *d_raw,
                     double *d_reported, int32_t *d_count, void *stream) {
+    return pr_index_search_ex(h, d_q, nq, k, mode, nullptr, d_rows, d_raw, d_reported, d_count, stream);
+}
+
+int pr_index_search_ex(pr_index *h, const float *d_q, int64_t nq, int k, uint32_t mode, const int64_t *d_row_limit,
+                       int64_t *d_rows, double *d_raw, double *d_reported, int32_t *d_count, void *stream) {
     if (!h) PR_FAIL(PR_ERR_BAD_ARG, "null handle");
     if (k < 1) PR_FAIL(PR_ERR_BAD_ARG, "k must be >= 1");  // index.py:161-162
     if (nq < 0 || nq > INT32_MAX / 2) PR_FAIL(PR_ERR_BAD_ARG, "bad query count");
@@ -773,7 +800,9 @@ int pr_index_search(pr_index *h, const float *d_q, int64_t nq, int k, uint32_t m
             return PR_OK;
         }
     }
-    if (k > KMAX_EXACT) return pr::big_k_search(h->x32, h->count, h->dp8, h->dim, d_q, nq, k, d_rows, d_raw, d_reported, d_count, st);
+    if (k > KMAX_EXACT)
+        return pr::big_k_search(h->x32, h->count, h->dp8, h->dim, d_q, nq, k, d_row_limit, d_rows, d_raw, d_reported,
+                                d_count, st);
 
     const bool tensor_ok = pr::tc_eligible(h->dim, h->count, k);
     bool use_tc = (mode == PR_SEARCH_TENSOR) || (mode == PR_SEARCH_AUTO && tensor_ok && pr::tc_worthwhile(h->count, nq));
@@ -791,7 +820,8 @@ int pr_index_search(pr_index *h, const float *d_q, int64_t nq, int k, uint32_t m
 
     if (!use_tc) {
         h->stats.path = PR_SEARCH_EXACT;
-        return exact_search(h, Qp, nullptr, nullptr, (int)nq, k, d_rows, d_raw, d_reported, d_count, cv, st, true);
+        return exact_search(h, Qp, nullptr, nullptr, (int)nq, k, d_rows, d_raw, d_reported, d_count, cv, st, true,
+                            d_row_limit);
     }
     h->stats.path = PR_SEARCH_TENSOR;
     if (!h->tmap_ok) {
@@ -816,13 +846,14 @@ int pr_index_search(pr_index *h, const float *d_q, int64_t nq, int k, uint32_t m
     ts.rep = d_reported;
     ts.count = d_count;
     ts.counters = h->d_counters;
+    ts.row_limit = d_row_limit;
     rc = timing_pair(h, &ts.ev_begin, &ts.ev_end);
     if (rc) return rc;
     rc = pr::tc_search(ts, cv, st, &h->stats);
     if (rc) return rc;
     // certificate failures -> exact rescan of just those queries (device-sized list)
     return exact_search(h, Qp, ts.fallback_list, h->d_counters, (int)nq, k, d_rows, d_raw, d_reported, d_count, cv,
-                        st, false);
+                        st, false, d_row_limit);
 }
 
 int pr_index_set_timing(pr_index *h, int enable) {

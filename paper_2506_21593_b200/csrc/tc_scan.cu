@@ -155,6 +155,8 @@ struct TcScanParams {
     int tiles_per_split;  // 256-row tiles per split
     int ntiles;
     uint64_t *cand;       // [nq_pad, nsplit, TC_KP] keys
+    const int64_t *row_limit;  // nullable
+    int64_t nq;
 };
 
 __global__ void __launch_bounds__(TC_THREADS, 1)
@@ -245,6 +247,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         // ---------------- epilogue: TMEM -> registers -> top-K' ----------------
         const int et = threadIdx.x - 128;  // 0..127 == TMEM lane == query within tile
         const int ew = warp - 4;
+        const int64_t my_q = (int64_t)qtile * TC_BLOCK_M + et;
+        const int64_t my_lim = (p.row_limit && my_q < p.nq) ? min(p.n, p.row_limit[my_q]) : p.n;
         float ts[TC_KP];
         uint32_t tr[TC_KP];
 #pragma unroll
@@ -264,7 +268,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 TMEM_LD32(tmem + ((uint32_t)(ew * 32) << 16) + acc * TC_BLOCK_N + c * 32, v);
                 tmem_wait_ld();
                 const int64_t rb = rbase + c * 32;
-                const int64_t rem_rows = p.n - rb;
+                const int64_t rem_rows = my_lim - rb;
                 const int lim = rem_rows < 32 ? (int)rem_rows : 32;
                 const float thr = ts[TC_KP - 1];
                 uint32_t mask = 0;
@@ -334,6 +338,7 @@ struct RescoreArgs {
     int32_t *count;
     int32_t *counters;
     int32_t *fallback;
+    const int64_t *row_limit;
 };
 
 __global__ void __launch_bounds__(RS_THREADS) tc_rescore_kernel(RescoreArgs a) {
@@ -346,6 +351,7 @@ __global__ void __launch_bounds__(RS_THREADS) tc_rescore_kernel(RescoreArgs a) {
     const int M = a.nsplit * TC_KP;
     for (int64_t q = blockIdx.x; q < a.nq; q += gridDim.x) {
         const uint64_t *cq = a.cand + q * (int64_t)M;
+        const int64_t take = a.row_limit ? min(a.take, max((int64_t)0, a.row_limit[q])) : a.take;
         // F: the largest approximate score a non-candidate can have
         double F = -INFINITY;
         for (int sp = threadIdx.x; sp < a.nsplit; sp += RS_THREADS) {
@@ -363,7 +369,7 @@ __global__ void __launch_bounds__(RS_THREADS) tc_rescore_kernel(RescoreArgs a) {
         }
         // a_k: take-th best approximate candidate (keys are unique)
         uint64_t last_key = ~0ull;
-        for (int64_t j = 0; j < a.take; ++j) {
+        for (int64_t j = 0; j < take; ++j) {
             uint64_t best = 0;
             for (int e = threadIdx.x; e < M; e += RS_THREADS) {
                 uint64_t key = cq[e];
@@ -415,7 +421,7 @@ __global__ void __launch_bounds__(RS_THREADS) tc_rescore_kernel(RescoreArgs a) {
         double last_s = INFINITY;
         int64_t last_r = -1;
         bool ok = true;
-        for (int64_t j = 0; j < a.take; ++j) {
+        for (int64_t j = 0; j < take; ++j) {
             double bs = -INFINITY;
             int64_t br = -1;
             for (int e = threadIdx.x; e < nr; e += RS_THREADS) {
@@ -444,7 +450,7 @@ __global__ void __launch_bounds__(RS_THREADS) tc_rescore_kernel(RescoreArgs a) {
         last_r = -1;
         for (int64_t j = 0; j < a.k; ++j) {
             const int64_t o = q * a.k + j;
-            if (j >= a.take) {
+            if (j >= take) {
                 if (threadIdx.x == 0) {
                     a.rows[o] = -1;
                     if (a.raw) a.raw[o] = 0.0;
@@ -471,7 +477,7 @@ __global__ void __launch_bounds__(RS_THREADS) tc_rescore_kernel(RescoreArgs a) {
             last_s = bs;
             last_r = br;
         }
-        if (threadIdx.x == 0) a.count[q] = (int32_t)a.take;
+        if (threadIdx.x == 0) a.count[q] = (int32_t)take;
         __syncthreads();
     }
 }
@@ -588,7 +594,7 @@ int tc_search(TcSearch &s, Carve &cv, cudaStream_t st, pr_search_stats *stats) {
         PR_CUDA(cudaFuncSetAttribute(tc_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc_smem_bytes()));
         attr = true;
     }
-    TcScanParams p{s.n, s.dp64 / TC_BLOCK_K, nsplit, tps, (int)ntiles, cand};
+    TcScanParams p{s.n, s.dp64 / TC_BLOCK_K, nsplit, tps, (int)ntiles, cand, s.row_limit, s.nq};
     dim3 grid((unsigned)qtiles, (unsigned)nsplit);
     ::pr::count_launch();
     if (s.ev_begin) PR_CUDA(cudaEventRecord(s.ev_begin, st));
@@ -598,7 +604,7 @@ int tc_search(TcSearch &s, Carve &cv, cudaStream_t st, pr_search_stats *stats) {
 
     PR_CUDA(cudaMemsetAsync(s.counters, 0, 4 * sizeof(int32_t), st));
     RescoreArgs ra{cand, nsplit, s.nq, s.k, std::min<int64_t>(s.k, s.n), tc_error_bound(s.d, s.dp64), s.x32,
-                   s.dp8, s.d, s.qp, s.rows, s.raw, s.rep, s.count, s.counters, s.fallback_list};
+                   s.dp8, s.d, s.qp, s.rows, s.raw, s.rep, s.count, s.counters, s.fallback_list, s.row_limit};
     int rgrid = (int)std::min<int64_t>(s.nq, (int64_t)sm_count() * 16);
     ::pr::count_launch();
     tc_rescore_kernel<<<rgrid, RS_THREADS, 0, st>>>(ra);

@@ -36,6 +36,7 @@ struct TcSearch {
     int32_t *counters;      // [0] fallback count, [1] rescored candidates
     int32_t *fallback_list; // out: query ids failing the certificate
     cudaEvent_t ev_begin = nullptr, ev_end = nullptr;  // optional scan-kernel timing
+    const int64_t *row_limit = nullptr;                  // per query: rows >= limit invisible
 };
 
 bool tc_eligible(int d, int64_t n, int k);
@@ -46,7 +47,7 @@ int tc_search(TcSearch &s, Carve &cv, cudaStream_t st, pr_search_stats *stats);
 // fp16 rounding + tensor-core accumulation error bound for unit vectors of dim d
 double tc_error_bound(int d, int dp64);
 
-int big_k_search(const float *x32, int64_t n, int dp8, int d, const float *q, int64_t nq, int k, int64_t *rows,
-                 double *raw, double *rep, int32_t *count, cudaStream_t st);
+int big_k_search(const float *x32, int64_t n, int dp8, int d, const float *q, int64_t nq, int k,
+                 const int64_t *row_limit, int64_t *rows, double *raw, double *rep, int32_t *count, cudaStream_t st);
 
 }  // namespace pr

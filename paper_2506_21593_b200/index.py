@@ -248,10 +248,12 @@ class FlatIndex:
 
     # -- search ----------------------------------------------------------------
     def search_batch(self, queries, k: int, *, mode: int = MODE_AUTO, validate: bool = True,
-                     out: BatchResult | None = None) -> BatchResult:
+                     out: BatchResult | None = None, row_limit=None, count: bool = True) -> BatchResult:
         """Batched FlatIndex.search.  ``queries``: [B, dim] float32 (torch
         tensor on any device, or numpy).  Returns device tensors; counts
-        ``search_count`` once per query like B sequential calls."""
+        ``search_count`` once per query like B sequential calls (unless
+        ``count=False``).  ``row_limit`` (int64 [B]) restricts query b to rows
+        [0, row_limit[b]) — the store as it was earlier in a sequential stream."""
         if k < 1:
             raise ValueError("k must be >= 1")
         torch = _torch()
@@ -269,11 +271,17 @@ class FlatIndex:
                 raw=torch.empty((B, k), dtype=torch.float64, device="cuda"),
                 count=torch.empty((B,), dtype=torch.int32, device="cuda"),
             )
+        lim = None
+        if row_limit is not None:
+            lim = torch.as_tensor(row_limit, dtype=torch.int64).to("cuda").contiguous()
+            if lim.shape != (B,):
+                raise ValueError("row_limit must have one entry per query")
         with self._lock:
-            self.search_count += B
+            if count:
+                self.search_count += B
             if B:
-                rc = self._L.pr_index_search(
-                    self._h, _lib.ptr(q), B, k, mode, _lib.ptr(out.rows), _lib.ptr(out.raw),
+                rc = self._L.pr_index_search_ex(
+                    self._h, _lib.ptr(q), B, k, mode, _lib.ptr(lim), _lib.ptr(out.rows), _lib.ptr(out.raw),
                     _lib.ptr(out.scores), _lib.ptr(out.count), _lib.stream_ptr(),
                 )
                 _lib.check(rc, "pr_index_search")

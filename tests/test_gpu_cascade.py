@@ -1,0 +1,140 @@
+"""route_batch == [route(q) for q in queries], against the reference's recorded runs.
+
+Sequential equivalence is checked three ways: the reference's router trace
+(tests/golden/router_trace.json, incl. an AKM hit that forces a batch split),
+the reference's two-session simulation logs (tests/golden/simulation.json),
+and random replays routed both ways on twin GPU routers under permuted /
+disabled layers and a non-empty recall table.
+"""
+from __future__ import annotations
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _golden(name):
+    with open(os.path.join(HERE, "golden", name)) as fh:
+        return json.load(fh)
+
+
+def _router(corpus, **kw):
+    from paper_2506_21593_b200 import CascadeRouter, HashEmbedder, StubBackend, ingest_corpus
+
+    emb = HashEmbedder()
+    kb = ingest_corpus((json.dumps(c) for c in corpus), emb)
+    backend = kw.pop("backend", None) or StubBackend()
+    return CascadeRouter(embedder=emb, backend=backend, knowledge_base=kb, **kw)
+
+
+def _sig(ans, ev):
+    return ([[p.layer.wire_name, p.outcome] for p in ev.layers_probed], ev.serving_layer.wire_name, ans.text,
+            list(ans.supporting_passage_ids), [pid for pid, _ in ev.supporting_passages])
+
+
+@pytest.mark.parametrize("batch", [1000, 64, 7])
+def test_route_batch_matches_reference_trace(gpu, batch):
+    from paper_2506_21593_b200 import validate_query
+
+    gold = _golden("router_trace.json")
+    router = _router(gold["corpus"])
+    qs = [validate_query(q["text"], "s1", query_id=f"q{i}", issued_at_ns=i) for i, q in enumerate(gold["queries"])]
+    got = []
+    for i in range(0, len(qs), batch):
+        got.extend(router.route_batch(qs[i:i + batch]))
+    assert len(got) == len(qs)
+    for i, ((ans, ev), q) in enumerate(zip(got, gold["queries"])):
+        assert [[p.layer.wire_name, p.outcome] for p in ev.layers_probed] == q["probes"], i
+        assert ev.serving_layer.wire_name == q["serving"], i
+        assert ans.text == q["answer"], i
+        assert list(ans.supporting_passage_ids) == q["passages"], i
+    st, g = router.stats(), gold["stats"]
+    assert st["layer_counts"] == g["layer_counts"]
+    assert st["fixed_kv"] == g["fixed_kv"]
+    assert st["semantic_cache"] == g["semantic_cache"]
+    assert st["adaptive_memory"] == g["adaptive_memory"]
+    assert st["knowledge_base_searches"] == g["knowledge_base_searches"]
+    assert router.semantic_cache.index.search_count == g["sc_searches"]
+    assert router.adaptive_memory.index.search_count == g["akm_searches"]
+    assert router.adaptive_memory.inserted_total == g["akm_inserted_total"]
+    assert router.backend.context_calls == g["context_calls"]
+    assert router.backend.recall_calls == g["recall_calls"]
+
+
+def test_route_batch_matches_reference_simulation(gpu):
+    from paper_2506_21593_b200 import validate_query
+
+    gold = _golden("simulation.json")
+    router = _router(gold["corpus"])
+    for lines in gold["sessions"]:
+        recs = [json.loads(ln) for ln in lines]
+        router.reset_session()
+        qs = [validate_query(r["query_text"], r["session_id"], query_id=r["query_id"], issued_at_ns=r["timestamp_ns"])
+              for r in recs]
+        got = router.route_batch(qs)
+        for i, ((ans, ev), r) in enumerate(zip(got, recs)):
+            assert [[p.layer.wire_name, p.outcome] for p in ev.layers_probed] == \
+                [[p["layer"], p["outcome"]] for p in r["layers_probed"]], i
+            assert ev.serving_layer.wire_name == r["serving_layer"], i
+            assert ans.text == r["answer_text"], i
+            assert [pid for pid, _ in ev.supporting_passages] == [p["id"] for p in r["supporting_passages"]], i
+
+
+@pytest.mark.parametrize("variant", ["default", "permuted", "disabled", "recall"])
+def test_route_batch_equals_sequential_random(gpu, variant):
+    from paper_2506_21593_b200 import LayerTag, RouterConfig, StubBackend, StubKnowledgeTable, validate_query
+
+    gold = _golden("simulation.json")
+    corpus, questions = gold["corpus"][:150], gold["questions"]
+    kw = {}
+    if variant == "permuted":
+        kw["config"] = RouterConfig(layer_order=(LayerTag.SEMANTIC_CACHE, LayerTag.ADAPTIVE_MEMORY,
+                                                 LayerTag.FIXED_KV, LayerTag.MEMORY_RECALL, LayerTag.NAIVE_RAG))
+    elif variant == "disabled":
+        kw["config"] = RouterConfig(disabled_layers=frozenset({LayerTag.FIXED_KV, LayerTag.MEMORY_RECALL}))
+    rng = np.random.default_rng(5)
+    texts = []
+    for i in range(300):
+        if texts and rng.random() < 0.5:
+            t = texts[int(rng.integers(len(texts)))]
+            if rng.random() < 0.5:
+                t = t.rstrip("?") if t.endswith("?") else t + "?"
+        else:
+            t = questions[int(rng.integers(len(questions)))]
+        texts.append(t)
+    # passages that equal later queries make AKM hits (and batch splits) likely
+    texts[150:150] = [corpus[3]["text"], corpus[7]["text"]]
+
+    def mk():
+        extra = dict(kw)
+        if variant == "recall":
+            tab = StubKnowledgeTable()
+            for t in texts[::9]:
+                tab.add(t, "recalled " + t[:10], 0.9)
+            extra["backend"] = StubBackend(tab)
+        return _router(corpus, **extra)
+
+    seq, bat = mk(), mk()
+    qs = [validate_query(t, "s", query_id=f"q{i}", issued_at_ns=i) for i, t in enumerate(texts)]
+    want = [_sig(*seq.route(q)) for q in qs]
+    got = []
+    for i in range(0, len(qs), 97):
+        got.extend(_sig(*r) for r in bat.route_batch(qs[i:i + 97]))
+    assert got == want
+    assert seq.stats() == bat.stats()
+    assert seq.backend.context_calls == bat.backend.context_calls
+    assert seq.backend.recall_calls == bat.backend.recall_calls
+    assert seq.adaptive_memory.ids() == bat.adaptive_memory.ids()
+    assert seq.adaptive_memory.index.entry_ids() == bat.adaptive_memory.index.entry_ids()
+    assert seq.adaptive_memory.pending_count() == bat.adaptive_memory.pending_count()
+    assert seq.semantic_cache.index.entry_ids() == bat.semantic_cache.index.entry_ids()
+    assert seq.semantic_cache.index.search_count == bat.semantic_cache.index.search_count
+    assert seq.adaptive_memory.index.search_count == bat.adaptive_memory.index.search_count
+    assert seq.knowledge_base.index.search_count == bat.knowledge_base.index.search_count
+    assert [e["query_text"] for e in seq.kv_cache.export_entries()] == \
+        [e["query_text"] for e in bat.kv_cache.export_entries()]
