@@ -59,6 +59,11 @@ def parse():
     ap.add_argument("--cpu-queries", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-rows", type=int, default=1_000_000, help="reference arm: rows per timed sample")
+    ap.add_argument("--configs", default="c2,c3,c5",
+                    help="secondary BASELINE configs measured after the headline (rank 0, N=1): c2,c3,c5 or ''")
+    ap.add_argument("--kv-keys", type=int, default=100_000_000)
+    ap.add_argument("--c5-queries", type=int, default=20_000, help="queries per C5 session")
+    ap.add_argument("--c5-sessions", type=int, default=2)
     return ap.parse_args()
 
 
@@ -423,6 +428,27 @@ def main():
                          f"scores (FlatIndex.search restatement), {P} threads; fp64 upcast not timed",
                "seconds": secs, "host_threads": threads, "cpu": cpu_model(), "numpy": np.__version__}
 
+    configs = {}
+    if rank == 0 and world == 1 and a.configs:
+        import traceback
+
+        from benchlib import configs as C
+
+        wanted = [c.strip() for c in a.configs.split(",") if c.strip()]
+        for name in wanted:
+            try:
+                if name == "c2":
+                    configs["c2_semantic_cache"] = C.c2_semantic(peak)
+                elif name == "c3":
+                    configs["c3_fixed_kv"] = C.c3_kv(float(pk.get("hbm_gbs", 6538.6)), n_keys=a.kv_keys)
+                elif name == "c5":
+                    configs["c5_routed"] = C.c5_routed(idx, a.n, n_sessions=a.c5_sessions,
+                                                       queries_per_session=a.c5_queries)
+            except Exception as exc:  # noqa: BLE001 - recorded, the headline stands
+                configs[name] = {"error": f"{type(exc).__name__}: {exc}",
+                                 "trace": traceback.format_exc()[-1500:]}
+            torch.cuda.empty_cache()
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": "queries/s", "n_gpus": world,
@@ -448,6 +474,7 @@ def main():
             "search_stats": {"fallback_queries_last_step": int(st.fallback),
                              "rescored_candidates_last_step": int(st.candidates)},
             "build_seconds": round(build_s, 1),
+            "configs": configs,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -1,0 +1,291 @@
+"""Secondary BASELINE.json configurations measured inside bench.py (rank 0, N=1).
+
+C2  semantic-cache top-1 + threshold 0.85 over 1M x 768, batch 4096
+C3  fixed-KV exact lookup, 100M keys, batch 65536 (fused fingerprint + probe)
+C5  routed replay through all five layers over the 10M x 1024 store (LLM stubbed):
+    nine-session-style warm-up sessions routed with route_batch
+
+Each returns a dict that bench.py nests under "configs"; every number is
+device-timed with CUDA events and comes with its own parity check.
+"""
+from __future__ import annotations
+
+import time
+
+import numpy as np
+
+
+def _events():
+    import torch
+
+    return torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+
+def _unit_rows(n, d, seed, device="cuda"):
+    import torch
+
+    g = torch.Generator(device=device).manual_seed(seed)
+    x = torch.randn((n, d), generator=g, device=device, dtype=torch.float64)
+    return (x / x.norm(dim=1, keepdim=True)).float()
+
+
+# ---------------------------------------------------------------- C2
+def c2_semantic(peak_tflops: float, n=1_000_000, d=768, batch=4096, steps=20, threshold=0.85, parity_q=8):
+    import torch
+
+    from oracle import flat_index as F
+    from paper_2506_21593_b200 import FlatIndex, HashEmbedder, SemanticCache
+
+    sc = SemanticCache(HashEmbedder(dim=d), threshold=threshold, dim=d)
+    X = _unit_rows(n, d, 21)
+    sc.index.extend_arrays([f"t{i}" for i in range(n)], X, validate=False)
+    g = torch.Generator(device="cuda").manual_seed(22)
+    B2 = batch // 2
+    # half: perturbed copies of stored rows with cosine ~ U(0.80, 0.99); half: fresh random
+    rows = torch.randint(0, n, (B2,), generator=g, device="cuda")
+    base = X[rows].double()
+    noise = torch.randn((B2, d), generator=g, device="cuda", dtype=torch.float64)
+    noise = noise - (noise * base).sum(1, keepdim=True) * base
+    noise = noise / noise.norm(dim=1, keepdim=True)
+    cos = 0.80 + 0.19 * torch.rand((B2, 1), generator=g, device="cuda", dtype=torch.float64)
+    near = cos * base + (1 - cos ** 2).sqrt() * noise
+    Q = torch.cat([near, _unit_rows(batch - B2, d, 23).double()])
+    Q = (Q / Q.norm(dim=1, keepdim=True)).float().contiguous()
+    for _ in range(3):
+        sc.lookup_batch(Q, account=False)
+    sc.index.set_timing(True)
+    sc.index.scan_time()
+    torch.cuda.synchronize()
+    e0, e1 = _events()
+    e0.record()
+    for _ in range(steps):
+        hit, row, score = sc.lookup_batch(Q, account=False)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    kms, kn = sc.index.scan_time()
+    sc.index.set_timing(False)
+    kern = kms / max(1, kn)
+    flop = 2.0 * n * d * batch
+    # parity: exact top-1 + threshold decision vs the oracle on sampled queries
+    sel = np.r_[0:parity_q // 2, batch - parity_q // 2:batch]
+    want = F.c_search(X.cpu().numpy(), Q[torch.from_numpy(sel).cuda()].cpu().numpy(), 1)
+    got_hit = hit.cpu().numpy()[sel]
+    got_row = row.cpu().numpy()[sel]
+    want_hit = (want.count > 0) & (want.reported[:, 0] >= threshold)
+    mism = int(((got_hit != want_hit) | (got_row != want.rows[:, 0])).sum())
+    return {
+        "workload": f"semantic-cache top-1 + threshold {threshold} over {n} x {d}, batch {batch} (configs[1])",
+        "value": batch / (ms / 1e3), "unit": "lookups/s", "ms_per_batch": ms,
+        "hit_fraction": float(hit.float().mean().item()),
+        "roofline": {"bound": "tensor", "achieved": flop / (kern / 1e3) / 1e12, "peak": peak_tflops,
+                     "unit": "TFLOP/s", "frac": flop / (kern / 1e3) / 1e12 / peak_tflops, "kernel_ms": kern},
+        "parity": {"queries_checked": int(sel.size), "mismatches": mism},
+    }
+
+
+# ---------------------------------------------------------------- C3
+def _key_arena(ids: np.ndarray):
+    """'query-%09d' (or wider) keys as a UTF-8 arena + offsets, built with numpy."""
+    digits = np.maximum(9, np.floor(np.log10(np.maximum(ids, 1))).astype(np.int64) + 1)
+    lens = 6 + digits
+    off = np.zeros(ids.size + 1, dtype=np.int64)
+    np.cumsum(lens, out=off[1:])
+    buf = np.empty(int(off[-1]), dtype=np.uint8)
+    prefix = np.frombuffer(b"query-", dtype=np.uint8)
+    for L in np.unique(lens):
+        m = lens == L
+        sub = ids[m]
+        nd = int(L) - 6
+        block = np.empty((sub.size, int(L)), dtype=np.uint8)
+        block[:, :6] = prefix
+        v = sub.copy()
+        for c in range(nd - 1, -1, -1):
+            block[:, 6 + c] = 48 + (v % 10)
+            v //= 10
+        starts = off[:-1][m]
+        idx = (starts[:, None] + np.arange(int(L))[None, :]).ravel()
+        buf[idx] = block.ravel()
+    return buf, off
+
+
+def c3_kv(hbm_gbs: float, n_keys=100_000_000, batch=65536, n_batches=32, steps=5, chunk=8_000_000):
+    import torch
+
+    from paper_2506_21593_b200 import _lib
+
+    L = _lib.load()
+    import ctypes
+
+    h = ctypes.c_void_p()
+    _lib.check(L.pr_kv_create(n_keys, ctypes.byref(h)))
+    s = _lib.stream_ptr()
+    t0 = time.time()
+    for c0 in range(0, n_keys, chunk):
+        ids = np.arange(c0, min(n_keys, c0 + chunk), dtype=np.int64)
+        buf, off = _key_arena(ids)
+        d_buf, d_off = torch.from_numpy(buf).cuda(), torch.from_numpy(off).cuda()
+        fp = torch.empty((ids.size, 2), dtype=torch.int64, device="cuda")
+        _lib.check(L.pr_fingerprint(_lib.ptr(d_buf), _lib.ptr(d_off), ids.size, _lib.ptr(fp), s))
+        vals = torch.from_numpy(ids).cuda()
+        _lib.check(L.pr_kv_put(h, _lib.ptr(fp), _lib.ptr(vals), ids.size, s))
+    torch.cuda.synchronize()
+    build_s = time.time() - t0
+    size = L.pr_kv_size(h)
+    rng = np.random.default_rng(3)
+    batches = []
+    for _ in range(n_batches):
+        present = rng.integers(0, n_keys, batch // 2)
+        absent = rng.integers(n_keys, 2 * n_keys, batch - batch // 2)
+        ids = np.concatenate([present, absent])
+        rng.shuffle(ids)
+        buf, off = _key_arena(ids)
+        batches.append((torch.from_numpy(buf).cuda(), torch.from_numpy(off).cuda(), torch.from_numpy(ids).cuda()))
+    out = torch.empty(batch, dtype=torch.int64, device="cuda")
+    hit = torch.empty(batch, dtype=torch.uint8, device="cuda")
+    for b in batches[:3]:
+        L.pr_kv_get_text(h, _lib.ptr(b[0]), _lib.ptr(b[1]), batch, _lib.ptr(out), _lib.ptr(hit), s)
+    torch.cuda.synchronize()
+    e0, e1 = _events()
+    e0.record()
+    for _ in range(steps):
+        for b in batches:
+            L.pr_kv_get_text(h, _lib.ptr(b[0]), _lib.ptr(b[1]), batch, _lib.ptr(out), _lib.ptr(hit), s)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    lookups = steps * n_batches * batch
+    # parity: every lookup of every batch against the construction (value = key id, absent -> -1)
+    bad = 0
+    for b in batches:
+        L.pr_kv_get_text(h, _lib.ptr(b[0]), _lib.ptr(b[1]), batch, _lib.ptr(out), _lib.ptr(hit), s)
+        want = torch.where(b[2] < n_keys, b[2], torch.full_like(b[2], -1))
+        bad += int(((out != want) | (hit.bool() != (b[2] < n_keys))).sum().item())
+    L.pr_kv_destroy(h)
+    per_s = lookups / (ms / 1e3)
+    gbs = per_s * 56 / 1e9
+    return {
+        "workload": f"fixed-KV exact lookup, {n_keys} keys, batch {batch}, 50% present (configs[2], 1 GPU)",
+        "value": per_s, "unit": "lookups/s", "us_per_batch": ms * 1e3 / (steps * n_batches),
+        "keys_live": int(size), "build_seconds": build_s,
+        "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm_gbs, "unit": "GB/s", "frac": gbs / hbm_gbs,
+                     "bytes_per_lookup": 56,
+                     "note": "16-B fingerprint + one 32-B table sector + 8-B value per lookup; one launch per "
+                             "65536-key batch, so launch latency is part of the time"},
+        "parity": {"lookups_checked": n_batches * batch, "mismatches": bad},
+    }
+
+
+# ---------------------------------------------------------------- C5
+class _RowVector:
+    """Passage.embedding of a dense distractor row, read from the device store on demand."""
+
+    def __init__(self, store, row):
+        self._store, self._row = store, row
+
+    @property
+    def values(self):
+        return self._store.read_rows(self._row, 1).cpu().numpy()[0]
+
+
+class _KBPayloads:
+    """Payload list of the 10M-row bench KB: real Passages for the QA contexts,
+    distractor Passages (own id, own stored vector) materialised on access."""
+
+    def __init__(self, store, real):
+        self._store, self._real, self._n = store, real, len(store._ids)
+
+    def __len__(self):
+        return self._n
+
+    def __getitem__(self, i):
+        from paper_2506_21593_b200 import Passage
+
+        if i < len(self._real):
+            return self._real[i]
+        return Passage(id=self._store.id_at(i), text=f"Distractor passage {i}. Unrelated archival material.",
+                       source="distractor", embedding=_RowVector(self._store, i), answer=None)
+
+
+def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_session=20_000, batch=4096,
+              seed=0, parity_queries=300, profile=False):
+    """Routed replay over the bench's 10M x 1024 store turned into a knowledge base:
+    rows [0, n_qa) hold HashEmbedder(context) of the QA pool, the rest stay dense
+    distractors."""
+    import torch
+
+    from benchlib.workloads import LatencyDraws, corpus_of, qa_rows, session_stream
+    from paper_2506_21593_b200 import (CascadeRouter, HashEmbedder, MainKnowledgeBase, Passage, StubBackend,
+                                       validate_query)
+    from paper_2506_21593_b200.vectors import EmbeddingVector
+
+    emb = HashEmbedder()
+    t0 = time.time()
+    rows = qa_rows(n_qa, seed=42)
+    corpus = corpus_of(rows)
+    ctx = emb.embed_matrix([c["text"] for c in corpus])
+    store._update_rows(np.arange(n_qa, dtype=np.int64), ctx)
+    real = [Passage(id=store.id_at(i), text=c["text"], source=c["source"],
+                    embedding=EmbeddingVector(values=ctx[i]), answer=c["answer"]) for i, c in enumerate(corpus)]
+    store._payloads = _KBPayloads(store, real)
+    kb = MainKnowledgeBase.from_index(store)
+    questions = [r["question"] for r in rows]
+    streams = [session_stream(questions, queries_per_session, seed, s) for s in range(n_sessions)]
+    vecs = [torch.from_numpy(emb.embed_matrix([t for t, _ in st])).cuda() for _, st in streams]
+    prep_s = time.time() - t0
+
+    def make_router():
+        r = CascadeRouter(embedder=emb, backend=StubBackend(), knowledge_base=kb)
+        r.latency_model = LatencyDraws(0.25)
+        return r
+
+    router = make_router()
+    router.profile_batches = profile
+    layer_counts = {}
+    e0, e1 = _events()
+    torch.cuda.synchronize()
+    total = 0
+    seq_total = 0
+    e0.record()
+    for s, ((sid, st), V) in enumerate(zip(streams, vecs)):
+        router.reset_session()
+        router.latency_model.reseed([seed, s, 1])
+        qs = [validate_query(t, sid, query_id=f"{sid}-q{i:05d}", issued_at_ns=0) for i, (t, _) in enumerate(st)]
+        for i in range(0, len(qs), batch):
+            res = router.route_batch(qs[i:i + batch], vectors=V[i:i + batch])
+            total += len(res)
+            seq_total += router.last_batch_stats["sequential"]
+            for a, _ in res:
+                layer_counts[a.layer.wire_name] = layer_counts.get(a.layer.wire_name, 0) + 1
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    # parity: the first parity_queries of session 0 routed one by one on a twin router
+    twin = make_router()
+    sid, st = streams[0]
+    twin.reset_session()
+    twin.latency_model.reseed([seed, 0, 1])
+    ref = make_router()
+    ref.reset_session()
+    ref.latency_model.reseed([seed, 0, 1])
+    qs = [validate_query(t, sid, query_id=f"{sid}-q{i:05d}", issued_at_ns=0) for i, (t, _) in enumerate(st)]
+    qs = qs[:parity_queries]
+    got = ref.route_batch(qs, vectors=vecs[0][:parity_queries])
+    mism = 0
+    for q, (a, ev) in zip(qs, got):
+        b, ev2 = twin.route(q)
+        if (a.text, a.layer, a.supporting_passage_ids, [p.outcome for p in ev.layers_probed]) != \
+                (b.text, b.layer, b.supporting_passage_ids, [p.outcome for p in ev2.layers_probed]):
+            mism += 1
+    return {
+        "workload": f"five-layer routed replay (L1/L2/L3/L4/L5, LLM stubbed) over a {n_store} x 1024 KB "
+                    f"({n_qa} HashEmbedder contexts + dense distractors), {n_sessions} warm-up sessions x "
+                    f"{queries_per_session} queries, batch {batch} (configs[4] shape, 1 GPU)",
+        "value": total / (ms / 1e3), "unit": "routed queries/s", "ms_total": ms,
+        "layer_counts": layer_counts, "queries_routed_sequentially": seq_total,
+        "stage_seconds": getattr(router, "batch_profile", None),
+        "query_vectors": "HashEmbedder on the host before the timed region",
+        "prep_seconds": prep_s,
+        "parity": {"queries_checked": len(qs), "mismatches": mism,
+                   "oracle": "twin router, sequential route() per query (reference semantics)"},
+    }

@@ -56,6 +56,7 @@ typedef struct pr_search_stats {
     int64_t candidates;     /* rows rescored in fp64 after the tensor scan      */
     int32_t nsplit;         /* row splits used by the scan grid                 */
     int32_t path;           /* PR_SEARCH_EXACT or PR_SEARCH_TENSOR              */
+    int64_t collected;      /* failed the certificate -> tcgen05 collect pass   */
 } pr_search_stats;
 
 /* ---- library ------------------------------------------------------------ */

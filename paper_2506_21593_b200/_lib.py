@@ -45,6 +45,7 @@ class SearchStats(ctypes.Structure):
         ("candidates", c_i64),
         ("nsplit", ctypes.c_int32),
         ("path", ctypes.c_int32),
+        ("collected", c_i64),
     ]
 
 

@@ -44,11 +44,14 @@ from . import generation
 from .caches import CacheEntry, FixedKVCache, SemanticCache, encode_texts
 from .index import MODE_AUTO, FlatIndex
 from .knowledge import AdaptiveKnowledgeMemory
-from .records import LayerTag
+from .records import AnswerRecord, LayerTag
 from .router import LayerProbe, RouteTraceEvent
 
 L1, L2, L3, L4, L5 = (LayerTag.FIXED_KV, LayerTag.SEMANTIC_CACHE, LayerTag.MEMORY_RECALL,
                       LayerTag.ADAPTIVE_MEMORY, LayerTag.NAIVE_RAG)
+# immutable probe records shared by every routed query (only the serving
+# layer's probe carries a latency and is built per query)
+_PROBE = {(L, o): LayerProbe(L, o) for L in LayerTag for o in ("hit", "miss", "rejected")}
 
 
 def batchable(router) -> bool:
@@ -121,6 +124,7 @@ def _route_prefix(router, qs, vectors, mode):
     kv, sc, akm, kb = router.kv_cache, router.semantic_cache, router.adaptive_memory, router.knowledge_base
     backend = router.backend
     t_start = time.perf_counter_ns()
+    prof = _Prof(getattr(router, "profile_batches", False))
     akm.settle()  # the first route() of the run would settle the pre-batch queue (router.py:284-285)
 
     B = len(qs)
@@ -128,6 +132,7 @@ def _route_prefix(router, qs, vectors, mode):
     Vd = _embed(router, texts, vectors)
     ar = np.arange(B)
 
+    prof.mark("settle+embed")
     # ---- L1: pre-batch probe + causal first-occurrence dedupe
     first_of: dict[str, int] = {}
     first = np.fromiter((first_of.setdefault(t, j) for j, t in enumerate(texts)), dtype=np.int64, count=B)
@@ -139,6 +144,7 @@ def _route_prefix(router, qs, vectors, mode):
         kv_val = vals.cpu().numpy()
         l1 = hit.cpu().numpy().astype(bool) | (first < ar)
 
+    prof.mark("l1")
     # ---- L2: append the rows write-back will create, then one row-limited top-1 search
     sc_index = sc.index
     n_pre_sc = len(sc_index)
@@ -151,9 +157,11 @@ def _route_prefix(router, qs, vectors, mode):
     sc_row = np.full(B, -1, dtype=np.int64)
     if L2 in pos and B:
         r = sc_index.search_batch(Vd, 1, mode=mode, validate=False, row_limit=sc_limit, count=False)
+        prof.note("sc", sc_index)
         sc_row = r.rows[:, 0].cpu().numpy()
         l2 = (r.count.cpu().numpy() > 0) & (r.scores[:, 0].cpu().numpy() >= sc.threshold)
 
+    prof.mark("l2")
     # ---- L4/L5 speculation for every query that can reach them
     vec_pos = min(pos.get(L4, 99), pos.get(L5, 99))
     blocked = np.zeros(B, dtype=bool)
@@ -170,11 +178,13 @@ def _route_prefix(router, qs, vectors, mode):
     if spec.size:
         Vs = Vd[torch.from_numpy(spec).cuda()]
         r = kb.index.search_batch(Vs, cfg.akm_seed_k, mode=mode, validate=False, count=False)
+        prof.note("kb", kb.index)
         kb_rows, kb_cnt = r.rows.cpu().numpy(), r.count.cpu().numpy()
         if L4 in pos:
             thr = akm.threshold
             if len(akm.index):
                 ra = akm.index.search_batch(Vs, 1, mode=mode, validate=False, count=False)
+                prof.note("akm", akm.index)
                 l4_unsure[spec] |= (ra.count.cpu().numpy() > 0) & (ra.scores[:, 0].cpu().numpy() >= thr)
             # superset of in-batch seeds: every seed of every earlier speculative query
             seed_rows = np.concatenate([kb_rows[s, : kb_cnt[s]] for s in range(spec.size)]) \
@@ -185,8 +195,10 @@ def _route_prefix(router, qs, vectors, mode):
                 scratch.append_rows_from(kb.index, seed_rows, [str(i) for i in range(seed_rows.size)],
                                          [None] * seed_rows.size)
                 rs = scratch.search_batch(Vs, 1, mode=mode, validate=False, row_limit=seeds_before, count=False)
+                prof.note("seeds", scratch)
                 l4_unsure[spec] |= (rs.count.cpu().numpy() > 0) & (rs.scores[:, 0].cpu().numpy() >= thr)
 
+    prof.mark("l4+l5")
     # ---- decision pass (query order), stopping before an uncertain L4 probe
     p = B
     serving, probes_all = [], []
@@ -208,7 +220,7 @@ def _route_prefix(router, qs, vectors, mode):
                 ok = rec is not None
                 if ok:
                     recalled[j] = rec
-                probes.append(LayerProbe(L, "hit" if ok else "rejected"))
+                probes.append(_PROBE[L, "hit" if ok else "rejected"])
                 if ok:
                     hit_layer = L
                     break
@@ -217,13 +229,14 @@ def _route_prefix(router, qs, vectors, mode):
                 ok = False
             else:
                 ok = True
-            probes.append(LayerProbe(L, "hit" if ok else "miss"))
+            probes.append(_PROBE[L, "hit" if ok else "miss"])
             if ok:
                 hit_layer = L
                 break
         serving.append(hit_layer)
         probes_all.append(probes)
 
+    prof.mark("decide")
     # ---- materialise answers, write back, account (exactly as p sequential routes)
     wall = (time.perf_counter_ns() - t_start) / 1e9
     synthetic = router.latency_model is not None
@@ -238,35 +251,37 @@ def _route_prefix(router, qs, vectors, mode):
             cnt[pr.layer][0] += 1
             cnt[pr.layer][1] += pr.outcome == "hit"
         seeds = ()
-        if L is L1:
-            a = latest.get(q.text) or kv.entry_at(int(kv_val[j])).answer
-            ans = a.served_as(L1, 0.0)
-        elif L is L2:
-            t = sc_index.id_at(int(sc_row[j]))
-            a = latest.get(t) or sc_index.payload_at(int(sc_row[j])).answer
-            ans = a.served_as(L2, 0.0)
+        lat = router.latency_model.sample(L) if synthetic else wall / max(1, p)
+        if L is L1 or L is L2:
+            if L is L1:
+                a = latest.get(q.text) or kv.entry_at(int(kv_val[j])).answer
+            else:
+                t = sc_index.id_at(int(sc_row[j]))
+                a = latest.get(t) or sc_index.payload_at(int(sc_row[j])).answer
+            # served_as(L, 0.0) then answer_with_latency (model.py:177-192): a
+            # cache-served copy of a validated record, passages dropped
+            ans = AnswerRecord._trusted(a.text, L, a.confidence, (), lat)
         elif L is L3:
-            ans = recalled[j]
+            a = recalled[j]
+            ans = AnswerRecord._trusted(a.text, L, a.confidence, (), lat)
         else:
             s = slot[j]
             rows = kb_rows[s, : kb_cnt[s]]
             seeds = [kb.index.payload_at(int(r)) for r in rows]
-            ans = generation.generate_with_context(backend, q, seeds[: cfg.retrieval_k], L5)
+            a = generation.generate_with_context(backend, q, seeds[: cfg.retrieval_k], L5)
+            ans = AnswerRecord._trusted(a.text, L5, a.confidence, a.supporting_passage_ids, lat)
             if j < p - 1:
                 seed_rows_settled.extend(int(r) for r in rows)
             else:
                 last_seeds = seeds
         if synthetic:
-            lat = router.latency_model.sample(L)
             probes[-1] = LayerProbe(probes[-1].layer, probes[-1].outcome, lat)
-        else:
-            lat = wall / max(1, p)
-        ans = generation.answer_with_latency(ans, lat)
         latest[q.text] = ans
         answers.append(ans)
         events.append(RouteTraceEvent(q.id, q.session_id, q.text, tuple(probes), L, lat, q.issued_at, ans.text,
                                       router._passage_pairs(ans, seeds)))
 
+    prof.mark("materialise")
     # write-back (router.py:333-337): KV in order (last write wins), SC rows/payloads
     kv.put_many(texts[:p], answers)
     n_new_kept = int(np.searchsorted(new_js, p, side="left"))
@@ -298,4 +313,41 @@ def _route_prefix(router, qs, vectors, mode):
     akm.index.search_count += cnt[L4][0]
     kb.index.search_count += cnt[L5][0]
     router.trace.extend(events)
+    prof.mark("writeback")
+    if prof.enabled:
+        hist = getattr(router, "batch_profile", None)
+        if hist is None:
+            hist = router.batch_profile = {}
+        for k, v in prof.times.items():
+            hist[k] = hist.get(k, 0.0) + v
     return p, list(zip(answers, events))
+
+
+class _Prof:
+    """Optional stage timer (synchronises the device at each mark)."""
+
+    def __init__(self, enabled: bool):
+        self.enabled = enabled
+        self.times: dict[str, float] = {}
+        self._t = time.perf_counter()
+
+    def note(self, name: str, index) -> None:
+        if not self.enabled:
+            return
+        st = index.stats()
+        self.mark(name)
+        self.times[f"{name}.rows"] = self.times.get(f"{name}.rows", 0) + len(index)
+        self.times[f"{name}.queries"] = self.times.get(f"{name}.queries", 0) + st.queries
+        self.times[f"{name}.fallback"] = self.times.get(f"{name}.fallback", 0) + st.fallback
+        self.times[f"{name}.collected"] = self.times.get(f"{name}.collected", 0) + st.collected
+        self.times[f"{name}.tensor_path"] = self.times.get(f"{name}.tensor_path", 0) + (st.path == 2)
+
+    def mark(self, name: str) -> None:
+        if not self.enabled:
+            return
+        import torch
+
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        self.times[name] = self.times.get(name, 0.0) + (t - self._t)
+        self._t = t

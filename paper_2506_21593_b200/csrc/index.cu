@@ -890,6 +890,7 @@ int pr_index_last_stats(pr_index *h, pr_search_stats *out) {
         PR_CUDA(cudaStreamSynchronize(h->last_stream));
         h->stats.fallback = c[0];
         h->stats.candidates = c[1];
+        h->stats.collected = c[2];
         h->stats.tensor_queries = h->stats.queries;
     }
     *out = h->stats;

@@ -157,10 +157,21 @@ struct TcScanParams {
     uint64_t *cand;       // [nq_pad, nsplit, TC_KP] keys
     const int64_t *row_limit;  // nullable
     int64_t nq;
+    // COLLECT mode (second pass for certificate failures): the query rows of the
+    // tile are the compacted list qmap[0..*nlist); every row with approx >= thr[slot]
+    // is appended to cbuf[slot][*] (ccount[slot] counts, capped at cap)
+    const int32_t *qmap;
+    const int32_t *nlist;
+    const float *thr;
+    int32_t *ccount;
+    int32_t *cbuf;
+    int cap;
 };
 
+template <bool COLLECT>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_scan_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tx, TcScanParams p) {
+    if (COLLECT && blockIdx.x * TC_BLOCK_M >= *p.nlist) return;  // uniform early exit: tile past the list
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
     uint8_t *sA = smem;
@@ -247,8 +258,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         // ---------------- epilogue: TMEM -> registers -> top-K' ----------------
         const int et = threadIdx.x - 128;  // 0..127 == TMEM lane == query within tile
         const int ew = warp - 4;
-        const int64_t my_q = (int64_t)qtile * TC_BLOCK_M + et;
-        const int64_t my_lim = (p.row_limit && my_q < p.nq) ? min(p.n, p.row_limit[my_q]) : p.n;
+        const int64_t my_slot = (int64_t)qtile * TC_BLOCK_M + et;
+        int64_t my_q = my_slot;
+        float cthr = INFINITY;
+        if (COLLECT) {
+            my_q = (my_slot < *p.nlist) ? p.qmap[my_slot] : -1;
+            if (my_q >= 0) cthr = p.thr[my_slot];
+        }
+        int64_t my_lim = (p.row_limit && my_q >= 0 && my_q < p.nq) ? min(p.n, p.row_limit[my_q]) : p.n;
+        if (my_q < 0) my_lim = 0;
         float ts[TC_KP];
         uint32_t tr[TC_KP];
 #pragma unroll
@@ -272,9 +290,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 const int lim = rem_rows < 32 ? (int)rem_rows : 32;
                 const float thr = ts[TC_KP - 1];
                 uint32_t mask = 0;
+                if (COLLECT) {
 #pragma unroll
-                for (int j = 0; j < 32; ++j) mask |= (__uint_as_float(v[j]) > thr ? 1u : 0u) << j;
+                    for (int j = 0; j < 32; ++j) mask |= (__uint_as_float(v[j]) >= cthr ? 1u : 0u) << j;
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) mask |= (__uint_as_float(v[j]) > thr ? 1u : 0u) << j;
+                }
                 if (lim < 32) mask &= (lim <= 0) ? 0u : (0xFFFFFFFFu >> (32 - lim));
+                if (COLLECT && mask) {
+                    const int cnt = __popc(mask);
+                    const int base = atomicAdd(&p.ccount[my_slot], cnt);
+                    int o = base;
+                    while (mask && o < p.cap) {
+                        const int j = __ffs(mask) - 1;
+                        mask &= mask - 1;
+                        p.cbuf[my_slot * (int64_t)p.cap + o] = (int32_t)(rb + j);
+                        ++o;
+                    }
+                    mask = 0;
+                }
                 if (mask) {
                     // rare: spill this chunk to smem so candidates can be indexed dynamically
 #pragma unroll
@@ -291,10 +326,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
         }
-        const int64_t q = (int64_t)qtile * TC_BLOCK_M + et;
-        uint64_t *out = p.cand + (q * p.nsplit + split) * TC_KP;
+        if (!COLLECT) {
+            uint64_t *out = p.cand + (my_slot * p.nsplit + split) * TC_KP;
 #pragma unroll
-        for (int s = 0; s < TC_KP; ++s) out[s] = (tr[s] == 0xFFFFFFFFu) ? 0ull : cand_key(ts[s], tr[s]);
+            for (int s = 0; s < TC_KP; ++s) out[s] = (tr[s] == 0xFFFFFFFFu) ? 0ull : cand_key(ts[s], tr[s]);
+        }
     }
 
     tc_fence_before();
@@ -339,7 +375,25 @@ struct RescoreArgs {
     int32_t *counters;
     int32_t *fallback;
     const int64_t *row_limit;
+    int32_t *clist;  // certificate failures -> collect pass: query ids (counters[2] counts)
+    float *cthr;     // ... and their collect thresholds (rounded down to fp32)
 };
+
+// hand a query whose certificate failed to the collect pass (or, without
+// one, straight to the exact rescan)
+__device__ __forceinline__ void defer_query(const RescoreArgs &a, int64_t q, double thr) {
+    if (threadIdx.x == 0) {
+        if (a.clist) {
+            const int slot = atomicAdd(&a.counters[2], 1);
+            a.clist[slot] = (int32_t)q;
+            a.cthr[slot] = __double2float_rd(thr);
+        } else {
+            const int slot = atomicAdd(&a.counters[0], 1);
+            a.fallback[slot] = (int32_t)q;
+        }
+    }
+    __syncthreads();
+}
 
 __global__ void __launch_bounds__(RS_THREADS) tc_rescore_kernel(RescoreArgs a) {
     __shared__ int64_t r_row[RS_MAX];
@@ -405,11 +459,8 @@ __global__ void __launch_bounds__(RS_THREADS) tc_rescore_kernel(RescoreArgs a) {
         __syncthreads();
         const int nr = r_n;
         if (nr > RS_MAX) {
-            if (threadIdx.x == 0) {
-                int slot = atomicAdd(&a.counters[0], 1);
-                a.fallback[slot] = (int32_t)q;
-            }
-            __syncthreads();
+            // every true top-k row has approx >= a_k - 2E
+            defer_query(a, q, cut);
             continue;
         }
         const float *qv = a.qp + q * (int64_t)a.dp8;
@@ -437,13 +488,14 @@ __global__ void __launch_bounds__(RS_THREADS) tc_rescore_kernel(RescoreArgs a) {
         }
         // every non-candidate scores <= F + E exactly; candidates outside R
         // score < a_k - E <= e_k
-        if (ok && !(last_s > F + a.err)) ok = false;
         if (!ok) {
-            if (threadIdx.x == 0) {
-                int slot = atomicAdd(&a.counters[0], 1);
-                a.fallback[slot] = (int32_t)q;
-            }
-            __syncthreads();
+            defer_query(a, q, cut);
+            continue;
+        }
+        if (!(last_s > F + a.err)) {
+            // exact ties (or near-ties) at the boundary: e_k(R) <= true e_k, so every
+            // true top-k row, incl. lower-row ties, has approx >= e_k(R) - E
+            defer_query(a, q, last_s - a.err);
             continue;
         }
         last_s = INFINITY;
@@ -467,6 +519,105 @@ __global__ void __launch_bounds__(RS_THREADS) tc_rescore_kernel(RescoreArgs a) {
                 if (after && (br < 0 || ranks_before(s, r, bs, br))) { bs = s; br = r; }
             }
             block_best(bs, br, red_s, red_r);
+            double rep;
+            finalize_hit(a.x32, a.dp8, a.d, qv, br, bs, &rep);
+            if (threadIdx.x == 0) {
+                a.rows[o] = br;
+                if (a.raw) a.raw[o] = bs;
+                if (a.rep) a.rep[o] = rep;
+            }
+            last_s = bs;
+            last_r = br;
+        }
+        if (threadIdx.x == 0) a.count[q] = (int32_t)take;
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// collect pass (certificate failures): exact rescoring of every collected row
+constexpr int CL_THREADS = 256;
+constexpr int CL_CAP = 8192;  // collected rows per query kept; more -> exact rescan
+
+__global__ void gather_q16_kernel(const __half *__restrict__ q16, int dp64, const int32_t *__restrict__ list,
+                                  const int32_t *__restrict__ nlist, __half *__restrict__ out) {
+    const int n = *nlist;
+    const int64_t total = (int64_t)n * dp64;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t / dp64;
+        out[t] = q16[(int64_t)list[i] * dp64 + (t - i * dp64)];
+    }
+}
+
+struct CollectArgs {
+    const int32_t *clist;
+    const int32_t *nlist;
+    const int32_t *ccount;
+    const int32_t *cbuf;
+    int cap;
+    int k;
+    int64_t take;
+    const int64_t *row_limit;
+    const float *x32;
+    int dp8, d;
+    const float *qp;
+    int64_t *rows;
+    double *raw, *rep;
+    int32_t *count;
+    int32_t *counters;
+    int32_t *fallback;
+};
+
+__global__ void __launch_bounds__(CL_THREADS) tc_collect_rescore_kernel(CollectArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double *ex = reinterpret_cast<double *>(smem);                // [cap]
+    int32_t *rw = reinterpret_cast<int32_t *>(ex + a.cap);        // [cap]
+    __shared__ double red_s[CL_THREADS / 32];
+    __shared__ int64_t red_r[CL_THREADS / 32];
+    const int n = *a.nlist;
+    for (int slot = blockIdx.x; slot < n; slot += gridDim.x) {
+        const int64_t q = a.clist[slot];
+        const int cnt = a.ccount[slot];
+        if (cnt > a.cap) {  // too many rows above the threshold: exact fp64 rescan
+            if (threadIdx.x == 0) {
+                const int f = atomicAdd(&a.counters[0], 1);
+                a.fallback[f] = (int32_t)q;
+            }
+            continue;
+        }
+        const int64_t take = a.row_limit ? min(a.take, max((int64_t)0, a.row_limit[q])) : a.take;
+        const float *qv = a.qp + q * (int64_t)a.dp8;
+        const int32_t *src = a.cbuf + (int64_t)slot * a.cap;
+        for (int e = threadIdx.x; e < cnt; e += CL_THREADS) {
+            const int32_t r = src[e];
+            rw[e] = r;
+            ex[e] = einsum_dot_f32(a.x32 + (int64_t)r * a.dp8, qv, a.d);
+        }
+        if (threadIdx.x == 0) atomicAdd(&a.counters[1], cnt);
+        __syncthreads();
+        double last_s = INFINITY;
+        int64_t last_r = -1;
+        for (int64_t j = 0; j < a.k; ++j) {
+            const int64_t o = q * a.k + j;
+            double bs = -INFINITY;
+            int64_t br = -1;
+            if (j < take) {
+                for (int e = threadIdx.x; e < cnt; e += CL_THREADS) {
+                    const double s = ex[e];
+                    const int64_t r = rw[e];
+                    const bool after = (last_r < 0) || ranks_before(last_s, last_r, s, r);
+                    if (after && (br < 0 || ranks_before(s, r, bs, br))) { bs = s; br = r; }
+                }
+            }
+            block_best(bs, br, red_s, red_r);
+            if (br < 0) {
+                if (threadIdx.x == 0) {
+                    a.rows[o] = -1;
+                    if (a.raw) a.raw[o] = 0.0;
+                    if (a.rep) a.rep[o] = 0.0;
+                }
+                continue;
+            }
             double rep;
             finalize_hit(a.x32, a.dp8, a.d, qv, br, bs, &rep);
             if (threadIdx.x == 0) {
@@ -537,7 +688,8 @@ size_t tc_scratch_bytes(int64_t nq, int dp64, int64_t n, int k) {
     int64_t nq_pad = round_up<int64_t>(nq, TC_BLOCK_M);
     int64_t ntiles = ceil_div<int64_t>(n, TC_BLOCK_N);
     int64_t maxsplit = std::min<int64_t>(ntiles, 4 * 148);
-    return (size_t)nq_pad * dp64 * 2 + (size_t)nq_pad * maxsplit * TC_KP * 8 + (size_t)nq * 4 + 4096;
+    return (size_t)nq_pad * dp64 * 2 * 2 + (size_t)nq_pad * maxsplit * TC_KP * 8 + (size_t)nq * (4 * 4 + 4 * CL_CAP) +
+           16384;
 }
 
 int tc_make_store_map(TcStoreMap *m, const __half *x16, int64_t rows, int dp64) {
@@ -591,23 +743,63 @@ int tc_search(TcSearch &s, Carve &cv, cudaStream_t st, pr_search_stats *stats) {
 
     static bool attr = false;
     if (!attr) {
-        PR_CUDA(cudaFuncSetAttribute(tc_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc_smem_bytes()));
+        PR_CUDA(cudaFuncSetAttribute(tc_scan_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)tc_smem_bytes()));
+        PR_CUDA(cudaFuncSetAttribute(tc_scan_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)tc_smem_bytes()));
+        PR_CUDA(cudaFuncSetAttribute(tc_collect_rescore_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     CL_CAP * 12 + 1024));
         attr = true;
     }
-    TcScanParams p{s.n, s.dp64 / TC_BLOCK_K, nsplit, tps, (int)ntiles, cand, s.row_limit, s.nq};
+    TcScanParams p{s.n, s.dp64 / TC_BLOCK_K, nsplit, tps, (int)ntiles, cand, s.row_limit, s.nq,
+                   nullptr, nullptr, nullptr, nullptr, nullptr, 0};
     dim3 grid((unsigned)qtiles, (unsigned)nsplit);
     ::pr::count_launch();
     if (s.ev_begin) PR_CUDA(cudaEventRecord(s.ev_begin, st));
-    tc_scan_kernel<<<grid, TC_THREADS, tc_smem_bytes(), st>>>(qmap.map, s.store_map->map, p);
+    tc_scan_kernel<false><<<grid, TC_THREADS, tc_smem_bytes(), st>>>(qmap.map, s.store_map->map, p);
     PR_LAUNCH_CHECK();
     if (s.ev_end) PR_CUDA(cudaEventRecord(s.ev_end, st));
 
     PR_CUDA(cudaMemsetAsync(s.counters, 0, 4 * sizeof(int32_t), st));
+    int32_t *clist = cv.take<int32_t>((size_t)s.nq);
+    float *cthr = cv.take<float>((size_t)s.nq);
+    int32_t *ccount = cv.take<int32_t>((size_t)s.nq);
+    int32_t *cbuf = cv.take<int32_t>((size_t)s.nq * CL_CAP);
+    __half *q16c = cv.take<__half>((size_t)nq_pad * s.dp64);
     RescoreArgs ra{cand, nsplit, s.nq, s.k, std::min<int64_t>(s.k, s.n), tc_error_bound(s.d, s.dp64), s.x32,
-                   s.dp8, s.d, s.qp, s.rows, s.raw, s.rep, s.count, s.counters, s.fallback_list, s.row_limit};
+                   s.dp8, s.d, s.qp, s.rows, s.raw, s.rep, s.count, s.counters, s.fallback_list, s.row_limit,
+                   clist, cthr};
     int rgrid = (int)std::min<int64_t>(s.nq, (int64_t)sm_count() * 16);
     ::pr::count_launch();
     tc_rescore_kernel<<<rgrid, RS_THREADS, 0, st>>>(ra);
+    PR_LAUNCH_CHECK();
+
+    // collect pass for certificate failures (device-sized list; tiles past it exit at once)
+    PR_CUDA(cudaMemsetAsync(ccount, 0, (size_t)s.nq * sizeof(int32_t), st));
+    {
+        int g = (int)std::min<int64_t>(ceil_div<int64_t>(nq_pad * s.dp64, 256), (int64_t)sm_count() * 8);
+        ::pr::count_launch();
+        gather_q16_kernel<<<g, 256, 0, st>>>(q16, s.dp64, clist, s.counters + 2, q16c);
+        PR_LAUNCH_CHECK();
+    }
+    TcStoreMap cmap;
+    rc = make_map(&cmap.map, q16c, nq_pad, s.dp64, TC_BLOCK_M);
+    if (rc) return rc;
+    TcScanParams pc = p;
+    pc.qmap = clist;
+    pc.nlist = s.counters + 2;
+    pc.thr = cthr;
+    pc.ccount = ccount;
+    pc.cbuf = cbuf;
+    pc.cap = CL_CAP;
+    ::pr::count_launch();
+    tc_scan_kernel<true><<<grid, TC_THREADS, tc_smem_bytes(), st>>>(cmap.map, s.store_map->map, pc);
+    PR_LAUNCH_CHECK();
+    CollectArgs ca{clist, s.counters + 2, ccount, cbuf, CL_CAP, s.k, std::min<int64_t>(s.k, s.n), s.row_limit,
+                   s.x32, s.dp8, s.d, s.qp, s.rows, s.raw, s.rep, s.count, s.counters, s.fallback_list};
+    ::pr::count_launch();
+    tc_collect_rescore_kernel<<<(unsigned)std::min<int64_t>(s.nq, (int64_t)sm_count() * 4), CL_THREADS,
+                                CL_CAP * 12, st>>>(ca);
     PR_LAUNCH_CHECK();
     stats->nsplit = nsplit;
     return PR_OK;

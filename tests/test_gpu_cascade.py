@@ -138,3 +138,18 @@ def test_route_batch_equals_sequential_random(gpu, variant):
     assert seq.knowledge_base.index.search_count == bat.knowledge_base.index.search_count
     assert [e["query_text"] for e in seq.kv_cache.export_entries()] == \
         [e["query_text"] for e in bat.kv_cache.export_entries()]
+
+
+def test_batched_simulation_logs_byte_identical(gpu):
+    """f3: session logs materialised from batched routing are byte-identical to
+    the reference's run_simulation output (simulation.py:268-314)."""
+    from benchlib.workloads import simulate_batched
+
+    gold = _golden("simulation.json")
+    router = _router(gold["corpus"])
+    logs = simulate_batched(router, gold["questions"], n_sessions=gold["n_sessions"],
+                            n_queries=gold["queries_per_session"], seed=gold["seed"], batch=64)
+    for s, (got, want) in enumerate(zip(logs, gold["sessions"])):
+        for i, (a, b) in enumerate(zip(got, want)):
+            assert a == b, (s, i)
+        assert len(got) == len(want)

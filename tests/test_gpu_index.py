@@ -98,6 +98,25 @@ def test_tensor_path_fallback_on_ties(gpu, rng):
     idx = FlatIndex(dim=d)
     idx.extend_arrays([f"e{i}" for i in range(n)], X)
     _check(idx, X, Q, 10, MODE_TENSOR)
+    st = idx.stats()
+    assert st.collected > 0  # ties defeat the certificate -> tcgen05 collect pass
+
+
+def test_tensor_path_tie_tier_beyond_collect_cap(gpu, rng):
+    """A tie tier larger than the collect capacity (8192 rows) must end in the
+    exact fp64 rescan and still match the oracle (lowest rows win ties)."""
+    from paper_2506_21593_b200 import MODE_TENSOR, FlatIndex
+
+    d, n = 32, 30000
+    X = random_unit_vectors(rng, n, d)
+    X[5000:25000] = X[3]  # 20000 identical rows
+    Q = random_unit_vectors(rng, 40, d)
+    Q[0] = X[3]
+    Q[1] = (X[3] + 0.01 * Q[1]) / np.linalg.norm((X[3] + 0.01 * Q[1]).astype(np.float64))
+    Q = Q.astype(np.float32)
+    idx = FlatIndex(dim=d)
+    idx.extend_arrays([f"e{i}" for i in range(n)], X)
+    _check(idx, X, Q, 10, MODE_TENSOR)
     assert idx.stats().fallback > 0
 
 

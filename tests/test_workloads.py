@@ -1,0 +1,33 @@
+"""The workload generators reproduce the reference's recorded streams (CPU only)."""
+from __future__ import annotations
+
+import json
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _sim():
+    with open(os.path.join(HERE, "golden", "simulation.json")) as fh:
+        return json.load(fh)
+
+
+def test_qa_rows_match_reference_dataset():
+    from benchlib.workloads import corpus_of, qa_rows
+
+    g = _sim()
+    rows = qa_rows(g["dataset_n"], seed=42)
+    assert [r["question"] for r in rows] == g["questions"]
+    assert corpus_of(rows) == g["corpus"]
+
+
+def test_session_streams_match_reference_logs():
+    from benchlib.workloads import session_stream
+
+    g = _sim()
+    for s, lines in enumerate(g["sessions"]):
+        recs = [json.loads(ln) for ln in lines]
+        sid, stream = session_stream(g["questions"], g["queries_per_session"], g["seed"], s)
+        assert sid == recs[0]["session_id"]
+        assert [t for t, _ in stream] == [r["query_text"] for r in recs]
+        assert [o for _, o in stream] == [r["origin"] for r in recs]
