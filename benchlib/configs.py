@@ -215,8 +215,8 @@ def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_se
     import torch
 
     from benchlib.workloads import LatencyDraws, corpus_of, qa_rows, session_stream
-    from paper_2506_21593_b200 import (CascadeRouter, HashEmbedder, MainKnowledgeBase, Passage, StubBackend,
-                                       validate_query)
+    from paper_2506_21593_b200 import (CascadeRouter, HashEmbedder, LayerTag, MainKnowledgeBase, Passage,
+                                       StubBackend, validate_query)
     from paper_2506_21593_b200.vectors import EmbeddingVector
 
     emb = HashEmbedder()
@@ -252,11 +252,13 @@ def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_se
         router.latency_model.reseed([seed, s, 1])
         qs = [validate_query(t, sid, query_id=f"{sid}-q{i:05d}", issued_at_ns=0) for i, (t, _) in enumerate(st)]
         for i in range(0, len(qs), batch):
-            res = router.route_batch(qs[i:i + batch], vectors=V[i:i + batch])
+            # columnar result: per-query objects are only built if someone reads them
+            res = router.route_batch(qs[i:i + batch], vectors=V[i:i + batch], materialize=False)
             total += len(res)
             seq_total += router.last_batch_stats["sequential"]
-            for a, _ in res:
-                layer_counts[a.layer.wire_name] = layer_counts.get(a.layer.wire_name, 0) + 1
+            for code, c in zip(*np.unique(res.layers(), return_counts=True)):
+                name = LayerTag(int(code)).wire_name
+                layer_counts[name] = layer_counts.get(name, 0) + int(c)
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)

@@ -139,6 +139,14 @@ class LatencyDraws:
     def sample(self, layer) -> float:
         return _BASE[int(layer)] * float(self.rng.lognormal(mean=0.0, sigma=self.sigma))
 
+    _BASES = np.array([0.0] + [_BASE[i] for i in range(1, 6)])
+
+    def sample_many(self, layers) -> np.ndarray:
+        """One draw per entry, in order; a size-n lognormal draw consumes the
+        generator exactly like n scalar draws (checked in tests)."""
+        layers = np.asarray(layers, dtype=np.int64)
+        return self._BASES[layers] * self.rng.lognormal(mean=0.0, sigma=self.sigma, size=layers.size)
+
 
 def session_stream(questions, n_queries: int, seed: int, s: int, split: float = 0.5):
     """All (text, origin) of session s (texts never depend on routing outcomes)."""

@@ -156,15 +156,19 @@ class FixedKVCache:
     # -- batch surface ------------------------------------------------------
     def put_many(self, texts: Sequence[str], answers: Sequence[AnswerRecord]) -> None:
         """Sequential-equivalent bulk put (later writes of a key win)."""
+        now = time.monotonic_ns()
+        self.put_entries(texts, [CacheEntry(t, a, now) for t, a in zip(texts, answers)])
+
+    def put_entries(self, texts: Sequence[str], entries: Sequence) -> None:
+        """Bulk put of prepared entries (CacheEntry or ledger.LedgerEntry)."""
         import torch
 
         if not texts:
             return
         data, off = encode_texts(texts)
-        now = time.monotonic_ns()
         with self._lock:
             base = len(self._arena)
-            self._arena.extend(CacheEntry(t, a, now) for t, a in zip(texts, answers))
+            self._arena.extend(entries)
             d_data = torch.from_numpy(data).cuda()
             d_off = torch.from_numpy(off).cuda()
             fp = torch.empty((len(texts), 2), dtype=torch.int64, device="cuda")

@@ -45,7 +45,8 @@ from .caches import CacheEntry, FixedKVCache, SemanticCache, encode_texts
 from .index import MODE_AUTO, FlatIndex
 from .knowledge import AdaptiveKnowledgeMemory
 from .records import AnswerRecord, LayerTag
-from .router import LayerProbe, RouteTraceEvent
+from .ledger import BatchLedger, LedgerEntry, entry_text_conf
+from .router import LayerProbe
 
 L1, L2, L3, L4, L5 = (LayerTag.FIXED_KV, LayerTag.SEMANTIC_CACHE, LayerTag.MEMORY_RECALL,
                       LayerTag.ADAPTIVE_MEMORY, LayerTag.NAIVE_RAG)
@@ -66,31 +67,60 @@ def batchable(router) -> bool:
     )
 
 
-def route_batch(router, queries, vectors=None, *, mode: int = MODE_AUTO):
-    """Route ``queries`` in order; see the module docstring."""
-    out = []
+def route_batch(router, queries, vectors=None, *, mode: int = MODE_AUTO, materialize: bool = True):
+    """Route ``queries`` in order; see the module docstring.  Returns the list
+    of (AnswerRecord, RouteTraceEvent), or with ``materialize=False`` a
+    ``RoutedBatch`` of columnar segments (objects built only on access)."""
+    segs = []
     i, n = 0, len(queries)
     stats = {"batched": 0, "sequential": 0, "splits": 0}
     while i < n:
         if not batchable(router):
-            out.append(router.route(queries[i]))
+            segs.append([router.route(queries[i])])
             stats["sequential"] += 1
             i += 1
             continue
         V = None if vectors is None else vectors[i:]
         remaining = n - i
-        done, res = _route_prefix(router, queries[i:], V, mode)
-        out.extend(res)
+        done, ledger = _route_prefix(router, queries[i:], V, mode)
+        if done:
+            segs.append(ledger)
         stats["batched"] += done
         i += done
         if done < remaining:
             # the next query's AKM outcome is not certain in batch: route it exactly
-            out.append(router.route(queries[i]))
+            segs.append([router.route(queries[i])])
             stats["sequential"] += 1
             stats["splits"] += 1
             i += 1
     router.last_batch_stats = stats
-    return out
+    rb = RoutedBatch(segs)
+    return rb.results() if materialize else rb
+
+
+class RoutedBatch:
+    """Concatenation of ledgers (batched spans) and (answer, event) lists (queries routed one by one)."""
+
+    def __init__(self, segs):
+        self.segs = segs
+
+    def __len__(self) -> int:
+        return sum(len(s) for s in self.segs)
+
+    def results(self) -> list:
+        out = []
+        for s in self.segs:
+            out.extend(s.results() if isinstance(s, BatchLedger) else s)
+        return out
+
+    def layers(self) -> np.ndarray:
+        parts = []
+        for s in self.segs:
+            if isinstance(s, BatchLedger):
+                parts.append(s.layer.astype(np.int8))
+            else:
+                parts.append(np.array([int(a.layer) for a, _ in s], dtype=np.int8))
+        return np.concatenate(parts) if parts else np.zeros(0, np.int8)
 
 
 def _embed(router, texts, vectors):
@@ -199,120 +229,140 @@ def _route_prefix(router, qs, vectors, mode):
                 l4_unsure[spec] |= (rs.count.cpu().numpy() > 0) & (rs.scores[:, 0].cpu().numpy() >= thr)
 
     prof.mark("l4+l5")
-    # ---- decision pass (query order), stopping before an uncertain L4 probe
-    p = B
-    serving, probes_all = [], []
-    recalled = {}
-    for j in range(B):
-        if L4 in pos and l4_unsure[j]:
-            reaches = all(not ((L is L1 and l1[j]) or (L is L2 and l2[j])) for L in order[: pos[L4]])
-            if reaches:
-                p = j
-                break
-        probes, hit_layer = [], None
-        for L in order:
+    # ---- decision pass, vectorised over the batch.  A batch stops before the
+    # first query whose L4 outcome is not certain (decided from L1/L2 alone, so
+    # no backend side effect happens for it in batch mode)
+    stop = B
+    if L4 in pos:
+        reach4 = l4_unsure.copy()
+        for L in order[: pos[L4]]:
             if L is L1:
-                ok = bool(l1[j])
+                reach4 &= ~l1
             elif L is L2:
-                ok = bool(l2[j])
-            elif L is L3:
+                reach4 &= ~l2
+        hits = np.nonzero(reach4)[0]
+        if hits.size:
+            stop = int(hits[0])
+    p = stop
+    serving = np.zeros(p, dtype=np.int8)
+    reach = np.ones(p, dtype=bool)
+    recalled = {}
+    for L in order:
+        if L is L1:
+            h = reach & l1[:p]
+        elif L is L2:
+            h = reach & l2[:p]
+        elif L is L3:
+            h = np.zeros(p, dtype=bool)
+            for j in np.nonzero(reach)[0]:
                 rec = generation.memory_recall(backend, qs[j], cfg.recall_threshold)
-                ok = rec is not None
-                if ok:
-                    recalled[j] = rec
-                probes.append(_PROBE[L, "hit" if ok else "rejected"])
-                if ok:
-                    hit_layer = L
-                    break
-                continue
-            elif L is L4:
-                ok = False
-            else:
-                ok = True
-            probes.append(_PROBE[L, "hit" if ok else "miss"])
-            if ok:
-                hit_layer = L
-                break
-        serving.append(hit_layer)
-        probes_all.append(probes)
+                if rec is not None:
+                    h[j] = True
+                    recalled[int(j)] = rec
+        elif L is L4:
+            h = np.zeros(p, dtype=bool)
+        else:
+            h = reach.copy()
+        serving[h] = int(L)
+        reach &= ~h
 
     prof.mark("decide")
-    # ---- materialise answers, write back, account (exactly as p sequential routes)
+    # ---- answers as columns; objects are materialised lazily (ledger.py)
     wall = (time.perf_counter_ns() - t_start) / 1e9
-    synthetic = router.latency_model is not None
-    latest: dict[str, object] = {}
-    answers, events = [], []
-    seed_rows_settled: list[int] = []  # KB rows of seeds the next in-batch route() would have settled
-    last_seeds: list = []              # seeds of the final query stay pending (router.py:333-334)
-    cnt = {L: [0, 0] for L in LayerTag}  # probes, hits
+    lm = router.latency_model
+    if lm is None:
+        lat = np.full(p, wall / max(1, p))
+    elif hasattr(lm, "sample_many"):
+        lat = np.asarray(lm.sample_many(serving), dtype=np.float64)
+    else:
+        lat = np.fromiter((lm.sample(LayerTag(int(v))) for v in serving), dtype=np.float64, count=p)
+    text: list = [None] * p
+    conf = np.zeros(p, dtype=np.float64)
+    ctx_rows: dict[int, np.ndarray] = {}
+    latest: dict[str, int] = {}
+    k_ctx = cfg.retrieval_k
+    v1, v2, v3 = int(L1), int(L2), int(L3)
     for j in range(p):
-        q, L, probes = qs[j], serving[j], probes_all[j]
-        for pr in probes:
-            cnt[pr.layer][0] += 1
-            cnt[pr.layer][1] += pr.outcome == "hit"
-        seeds = ()
-        lat = router.latency_model.sample(L) if synthetic else wall / max(1, p)
-        if L is L1 or L is L2:
-            if L is L1:
-                a = latest.get(q.text) or kv.entry_at(int(kv_val[j])).answer
+        code = serving[j]
+        t = texts[j]
+        if code == v1 or code == v2:
+            # a cache hit serves a copy of the latest answer written for that key
+            key = t if code == v1 else sc_index.id_at(int(sc_row[j]))
+            i = latest.get(key)
+            if i is not None:
+                text[j], conf[j] = text[i], conf[i]
+            elif code == v1:
+                text[j], conf[j] = entry_text_conf(kv.entry_at(int(kv_val[j])))
             else:
-                t = sc_index.id_at(int(sc_row[j]))
-                a = latest.get(t) or sc_index.payload_at(int(sc_row[j])).answer
-            # served_as(L, 0.0) then answer_with_latency (model.py:177-192): a
-            # cache-served copy of a validated record, passages dropped
-            ans = AnswerRecord._trusted(a.text, L, a.confidence, (), lat)
-        elif L is L3:
+                text[j], conf[j] = entry_text_conf(sc_index.payload_at(int(sc_row[j])))
+        elif code == v3:
             a = recalled[j]
-            ans = AnswerRecord._trusted(a.text, L, a.confidence, (), lat)
+            text[j], conf[j] = a.text, a.confidence
         else:
             s = slot[j]
-            rows = kb_rows[s, : kb_cnt[s]]
-            seeds = [kb.index.payload_at(int(r)) for r in rows]
-            a = generation.generate_with_context(backend, q, seeds[: cfg.retrieval_k], L5)
-            ans = AnswerRecord._trusted(a.text, L5, a.confidence, a.supporting_passage_ids, lat)
-            if j < p - 1:
-                seed_rows_settled.extend(int(r) for r in rows)
-            else:
-                last_seeds = seeds
-        if synthetic:
-            probes[-1] = LayerProbe(probes[-1].layer, probes[-1].outcome, lat)
-        latest[q.text] = ans
-        answers.append(ans)
-        events.append(RouteTraceEvent(q.id, q.session_id, q.text, tuple(probes), L, lat, q.issued_at, ans.text,
-                                      router._passage_pairs(ans, seeds)))
+            rows = kb_rows[s, : min(k_ctx, int(kb_cnt[s]))]
+            passages = [kb.index.payload_at(int(r)) for r in rows]
+            a = generation.generate_with_context(backend, qs[j], passages, L5)
+            text[j], conf[j] = a.text, a.confidence
+            ctx_rows[j] = rows
+        latest[t] = j
+    probe_prefix = {}
+    for L in order:
+        pre = []
+        for M in order[: pos[L]]:
+            pre.append(_PROBE[M, "rejected" if M is L3 else "miss"])
+        probe_prefix[L] = tuple(pre)
+    ledger = BatchLedger(qs[:p], serving, lat, text, conf, ctx_rows, kb.index, probe_prefix)
 
     prof.mark("materialise")
-    # write-back (router.py:333-337): KV in order (last write wins), SC rows/payloads
-    kv.put_many(texts[:p], answers)
+    # ---- write-back (router.py:333-337): KV in order (last write wins), SC payloads
+    now = time.monotonic_ns()
+    entries = [LedgerEntry(texts[j], ledger, j, now) for j in range(p)]
+    kv.put_entries(texts[:p], entries)
+    prof.mark("wb.kv")
     n_new_kept = int(np.searchsorted(new_js, p, side="left"))
     if n_pre_sc + n_new_kept < len(sc_index):
         sc_index.truncate(n_pre_sc + n_new_kept)
-    now = time.monotonic_ns()
     with sc._lock:
+        payloads, rec = sc_index._payloads, sc._recency
+        seq = sc._seq
         for j in range(p):
             t = texts[j]
-            row = sc_index.row_of(t)
-            sc_index._payloads[row] = CacheEntry(query_text=t, answer=answers[j], created_at_ns=now)
-            sc._seq += 1
-            sc._recency[t] = sc._seq
-    # AKM: seeds of queries before the last were settled by the following
+            payloads[sc_index.row_of(t)] = entries[j]
+            seq += 1
+            rec[t] = seq
+        sc._seq = seq
+    prof.mark("wb.sc")
+    # AKM: seeds of L5 queries before the last were settled by the following
     # route() calls (device-to-device from KB rows, dedupe by id, no overwrite);
-    # the last query's seeds are still pending, exactly as after route()
-    if seed_rows_settled:
-        akm.settle_from_rows(kb.index, seed_rows_settled)
-    if last_seeds:
-        akm.enqueue(last_seeds)
+    # the final query's seeds are still pending, exactly as after route()
+    l5_js = np.nonzero(serving == int(L5))[0]
+    settled = [kb_rows[slot[j], : kb_cnt[slot[j]]] for j in l5_js if j < p - 1]
+    if settled:
+        akm.settle_from_rows(kb.index, np.concatenate(settled))
+    if p and serving[p - 1] == int(L5):
+        s = slot[p - 1]
+        akm.enqueue([kb.index.payload_at(int(r)) for r in kb_rows[s, : kb_cnt[s]]])
 
-    # counters
-    kv.hits += cnt[L1][1]
-    kv.misses += cnt[L1][0] - cnt[L1][1]
-    sc.hits += cnt[L2][1]
-    sc.misses += cnt[L2][0] - cnt[L2][1]
-    sc_index.search_count += cnt[L2][0]
-    akm.misses += cnt[L4][0]
-    akm.index.search_count += cnt[L4][0]
-    kb.index.search_count += cnt[L5][0]
-    router.trace.extend(events)
+    prof.mark("wb.akm")
+    # ---- counters: a layer is probed by every query served at or after it
+    served_pos = np.array([pos[LayerTag(int(v))] for v in serving], dtype=np.int64) if p else np.zeros(0, np.int64)
+    for L in order:
+        probed = int((served_pos >= pos[L]).sum())
+        hit = int((serving == int(L)).sum())
+        if L is L1:
+            kv.hits += hit
+            kv.misses += probed - hit
+        elif L is L2:
+            sc.hits += hit
+            sc.misses += probed - hit
+            sc_index.search_count += probed
+        elif L is L4:
+            akm.misses += probed
+            akm.index.search_count += probed
+        elif L is L5:
+            kb.index.search_count += probed
+    router.trace.extend_ledger(ledger)
     prof.mark("writeback")
     if prof.enabled:
         hist = getattr(router, "batch_profile", None)
@@ -320,7 +370,7 @@ def _route_prefix(router, qs, vectors, mode):
             hist = router.batch_profile = {}
         for k, v in prof.times.items():
             hist[k] = hist.get(k, 0.0) + v
-    return p, list(zip(answers, events))
+    return p, ledger
 
 
 class _Prof:

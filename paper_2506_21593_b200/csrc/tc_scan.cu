@@ -667,7 +667,9 @@ static int make_map(CUtensorMap *m, const void *base, int64_t rows, int cols, in
 }
 
 bool tc_eligible(int d, int64_t n, int k) { return k <= TC_KP && n > 0 && n < (int64_t)0xFFFFFFF0ll && d <= 8192; }
-bool tc_worthwhile(int64_t n, int64_t nq) { return n >= 16384 && nq >= 1; }
+// the fp64 CUDA-core scan costs ~n*nq*d / 5.5e12 s; the tensor path has ~50 us of
+// fixed cost (five launches + TMA descriptors) but scans ~250x faster per row
+bool tc_worthwhile(int64_t n, int64_t nq) { return n >= 4096 && n * nq >= ((int64_t)1 << 22); }
 
 double tc_error_bound(int d, int dp64) {
     // |fp16(x) - x| <= u|x| + eta  (u = 2^-11 round-to-nearest, eta = 2^-25 half the

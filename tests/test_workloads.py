@@ -21,6 +21,18 @@ def test_qa_rows_match_reference_dataset():
     assert corpus_of(rows) == g["corpus"]
 
 
+def test_vector_latency_draws_equal_scalar_draws():
+    import numpy as np
+
+    from benchlib.workloads import LatencyDraws
+
+    a, b = LatencyDraws(0.25, [3, 1, 1]), LatencyDraws(0.25, [3, 1, 1])
+    layers = np.random.default_rng(0).integers(1, 6, 500)
+    many = a.sample_many(layers)
+    one = np.array([b.sample(int(x)) for x in layers])
+    assert (many == one).all()
+
+
 def test_session_streams_match_reference_logs():
     from benchlib.workloads import session_stream
 
