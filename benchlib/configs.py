@@ -231,7 +231,6 @@ def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_se
     kb = MainKnowledgeBase.from_index(store)
     questions = [r["question"] for r in rows]
     streams = [session_stream(questions, queries_per_session, seed, s) for s in range(n_sessions)]
-    vecs = [torch.from_numpy(emb.embed_matrix([t for t, _ in st])).cuda() for _, st in streams]
     prep_s = time.time() - t0
 
     def make_router():
@@ -247,13 +246,14 @@ def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_se
     total = 0
     seq_total = 0
     e0.record()
-    for s, ((sid, st), V) in enumerate(zip(streams, vecs)):
+    for s, (sid, st) in enumerate(streams):
         router.reset_session()
         router.latency_model.reseed([seed, s, 1])
         qs = [validate_query(t, sid, query_id=f"{sid}-q{i:05d}", issued_at_ns=0) for i, (t, _) in enumerate(st)]
         for i in range(0, len(qs), batch):
             # columnar result: per-query objects are only built if someone reads them
-            res = router.route_batch(qs[i:i + batch], vectors=V[i:i + batch], materialize=False)
+            # query texts in, embedded on the device inside route_batch (pr_hash_embed)
+            res = router.route_batch(qs[i:i + batch], materialize=False)
             total += len(res)
             seq_total += router.last_batch_stats["sequential"]
             for code, c in zip(*np.unique(res.layers(), return_counts=True)):
@@ -272,7 +272,7 @@ def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_se
     ref.latency_model.reseed([seed, 0, 1])
     qs = [validate_query(t, sid, query_id=f"{sid}-q{i:05d}", issued_at_ns=0) for i, (t, _) in enumerate(st)]
     qs = qs[:parity_queries]
-    got = ref.route_batch(qs, vectors=vecs[0][:parity_queries])
+    got = ref.route_batch(qs)
     mism = 0
     for q, (a, ev) in zip(qs, got):
         b, ev2 = twin.route(q)
@@ -286,7 +286,7 @@ def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_se
         "value": total / (ms / 1e3), "unit": "routed queries/s", "ms_total": ms,
         "layer_counts": layer_counts, "queries_routed_sequentially": seq_total,
         "stage_seconds": getattr(router, "batch_profile", None),
-        "query_vectors": "HashEmbedder on the host before the timed region",
+        "query_vectors": "device HashEmbedder (pr_hash_embed) inside the timed region, from raw query texts",
         "prep_seconds": prep_s,
         "parity": {"queries_checked": len(qs), "mismatches": mism,
                    "oracle": "twin router, sequential route() per query (reference semantics)"},

@@ -158,6 +158,17 @@ int64_t pr_kv_capacity(pr_kv *h);  /* slots */
 /* dump live (fingerprint, value) pairs; returns count written (<= max) or <0 */
 int64_t pr_kv_export(pr_kv *h, uint64_t *d_fp, int64_t *d_vals, int64_t max, void *stream);
 
+/* ---- device HashEmbedder: embedding.py:117-160 ------------
+ * Texts are a UTF-8 arena + offsets as for pr_fingerprint; d_out is fp32
+ * [n, dim], bit-identical to HashEmbedder(seed).embed(text).values for every
+ * text the device handles.  d_host_flag[i] = 1 marks texts the device leaves
+ * to the host (non-ASCII bytes, empty text, > 256 tokens). */
+int pr_hash_embed(const uint8_t *d_bytes, const int64_t *d_off, int64_t n, int dim, uint64_t seed, float *d_out,
+                  uint8_t *d_host_flag, void *stream);
+/* keyed blake2b (digest 8 bytes, key = seed big-endian) of prefix4 + data, as a
+ * big-endian integer — the embedder's token hash, callable on the host */
+uint64_t pr_blake2b64_host(uint64_t key, const char *prefix4, const uint8_t *data, int64_t len);
+
 #ifdef __cplusplus
 }
 #endif

@@ -86,6 +86,8 @@ SIGNATURES = {
     "pr_kv_size": (c_i64, [c_vp]),
     "pr_kv_capacity": (c_i64, [c_vp]),
     "pr_kv_export": (c_i64, [c_vp, c_vp, c_vp, c_i64, c_vp]),
+    "pr_hash_embed": (c_int, [c_vp, c_vp, c_i64, c_int, ctypes.c_uint64, c_vp, c_vp, c_vp]),
+    "pr_blake2b64_host": (ctypes.c_uint64, [ctypes.c_uint64, ctypes.c_char_p, c_vp, c_i64]),
 }
 
 

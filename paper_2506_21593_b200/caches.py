@@ -44,15 +44,7 @@ class CacheEntry:
     created_at_ns: int
 
 
-def encode_texts(texts: Sequence[str]):
-    """UTF-8 arena + int64 offsets (n+1) as host numpy arrays.  surrogatepass keeps
-    the str -> bytes map injective for every Python str."""
-    bs = [t.encode("utf-8", "surrogatepass") for t in texts]
-    off = np.zeros(len(bs) + 1, dtype=np.int64)
-    if bs:
-        np.cumsum([len(b) for b in bs], out=off[1:])
-    data = np.frombuffer(b"".join(bs) or b"\0", dtype=np.uint8).copy()
-    return data, off
+from .textarena import encode_texts  # noqa: E402  (re-exported for callers)
 
 
 def fingerprint_host(text: str) -> tuple[int, int]:

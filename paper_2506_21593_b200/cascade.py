@@ -128,6 +128,8 @@ def _embed(router, texts, vectors):
 
     if vectors is None:
         emb = router.embedder
+        if hasattr(emb, "embed_device"):  # HashEmbedder: hash the batch on the GPU (bit-identical)
+            return emb.embed_device(texts)
         if hasattr(emb, "embed_matrix"):
             V = emb.embed_matrix(texts)
         else:

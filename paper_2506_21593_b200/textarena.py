@@ -1,0 +1,24 @@
+"""Texts -> one UTF-8 byte arena + int64 offsets (the device-side text format)."""
+from __future__ import annotations
+
+from typing import Sequence
+
+import numpy as np
+
+
+def encode_texts(texts: Sequence[str]):
+    """(bytes uint8 [total], offsets int64 [n+1]) as host numpy arrays.
+    ``surrogatepass`` keeps the str -> bytes map injective for every Python str."""
+    bs = [t.encode("utf-8", "surrogatepass") for t in texts]
+    off = np.zeros(len(bs) + 1, dtype=np.int64)
+    if bs:
+        np.cumsum([len(b) for b in bs], out=off[1:])
+    data = np.frombuffer(b"".join(bs) or b"\0", dtype=np.uint8).copy()
+    return data, off
+
+
+def to_device(texts: Sequence[str]):
+    import torch
+
+    data, off = encode_texts(texts)
+    return torch.from_numpy(data).cuda(non_blocking=True), torch.from_numpy(off).cuda(non_blocking=True)

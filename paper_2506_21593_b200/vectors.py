@@ -141,6 +141,33 @@ class HashEmbedder:
     def embed_matrix(self, texts: Iterable[str]) -> np.ndarray:
         return np.stack([self.embed_array(t) for t in texts]) if texts else np.zeros((0, self.dim), np.float32)
 
+    def embed_device(self, texts) -> "object":
+        """Embed a batch on the GPU (libpentarag pr_hash_embed: keyed BLAKE2b token
+        hashing, warp per text) into a float32 CUDA tensor [n, dim], bit-identical
+        to ``embed``.  Texts the device does not take (non-ASCII, empty, > 256
+        tokens) are embedded on the host and patched in; an empty text raises
+        EmptyInput exactly like ``embed``."""
+        import torch
+
+        from . import _lib
+        from .textarena import to_device
+
+        texts = list(texts)
+        n = len(texts)
+        out = torch.empty((n, self.dim), dtype=torch.float32, device="cuda")
+        if n == 0:
+            return out
+        d_data, d_off = to_device(texts)
+        flag = torch.empty(n, dtype=torch.uint8, device="cuda")
+        L = _lib.load()
+        _lib.check(L.pr_hash_embed(_lib.ptr(d_data), _lib.ptr(d_off), n, self.dim, int.from_bytes(self._key, "big"),
+                                   _lib.ptr(out), _lib.ptr(flag), _lib.stream_ptr()), "hash_embed")
+        host = torch.nonzero(flag).flatten().cpu().tolist()
+        if host:
+            rows = np.stack([self.embed_array(texts[i]) for i in host])
+            out[torch.tensor(host, device="cuda")] = torch.from_numpy(rows).cuda()
+        return out
+
 
 def mean_cosine(reference, others: Iterable) -> float:
     vals = [cosine(reference, o) for o in others]

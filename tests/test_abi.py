@@ -71,6 +71,20 @@ def test_fingerprint_regression_value(lib):
     assert hi != lo
 
 
+@pytest.mark.parametrize("token", ["a", "Who", "ledger0007", "_", "9", "x" * 124, "y" * 125, "z" * 300, ""])
+@pytest.mark.parametrize("prefix", [b"tok:", b"raw:"])
+def test_blake2b_twin_matches_hashlib(lib, token, prefix):
+    """The device embedder's keyed BLAKE2b (host twin) == hashlib (embedding.py:131)."""
+    import hashlib
+
+    seed = 0x5EED_1024_CA5C_ADE5
+    b = token.encode()
+    buf = ctypes.create_string_buffer(b, max(1, len(b)))
+    got = lib.pr_blake2b64_host(seed, prefix, ctypes.cast(buf, ctypes.c_void_p), len(b))
+    want = int.from_bytes(hashlib.blake2b(prefix + b, digest_size=8, key=seed.to_bytes(8, "big")).digest(), "big")
+    assert got == want
+
+
 def test_product_path_refuses_without_gpu():
     import torch
 
