@@ -16,6 +16,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 
 #include "common.cuh"
@@ -154,6 +155,7 @@ struct TcScanParams {
     int nsplit;
     int tiles_per_split;  // 256-row tiles per split
     int ntiles;
+    int qtiles;
     uint64_t *cand;       // [nq_pad, nsplit, TC_KP] keys
     const int64_t *row_limit;  // nullable
     int64_t nq;
@@ -171,7 +173,6 @@ struct TcScanParams {
 template <bool COLLECT>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_scan_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tx, TcScanParams p) {
-    if (COLLECT && blockIdx.x * TC_BLOCK_M >= *p.nlist) return;  // uniform early exit: tile past the list
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
     uint8_t *sA = smem;
@@ -184,10 +185,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int qtile = blockIdx.x, split = blockIdx.y;
-    const int t0 = split * p.tiles_per_split;
-    const int t1 = min(p.ntiles, t0 + p.tiles_per_split);
-    const int nlocal = max(0, t1 - t0);
+    // persistent static schedule: work item = (query tile, row split), query tile
+    // fastest so CTAs running together stream the same store tiles through L2
+    const int nitems = p.qtiles * p.nsplit;
+    const int ntile_q = COLLECT ? (int)ceil_div<int64_t>(*p.nlist, TC_BLOCK_M) : p.qtiles;
+    auto item_of = [&](int item, int &qtile, int &split, int &t0, int &nloc) {
+        qtile = item % p.qtiles;
+        split = item / p.qtiles;
+        t0 = split * p.tiles_per_split;
+        const int t1 = min(p.ntiles, t0 + p.tiles_per_split);
+        nloc = (qtile < ntile_q) ? max(0, t1 - t0) : 0;  // COLLECT: tiles past the list do nothing
+    };
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tq);
@@ -218,14 +226,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int i = 0; i < nlocal; ++i) {
-                const int t = t0 + i;
-                for (int kb = 0; kb < p.nkb; ++kb) {
-                    mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_expect_tx(&full[stage], TC_A_BYTES + TC_B_BYTES);
-                    tma_load_2d(sA + stage * TC_A_BYTES, &tq, &full[stage], kb * TC_BLOCK_K, qtile * TC_BLOCK_M);
-                    tma_load_2d(sB + stage * TC_B_BYTES, &tx, &full[stage], kb * TC_BLOCK_K, t * TC_BLOCK_N);
-                    if (++stage == TC_STAGES) { stage = 0; phase ^= 1; }
+            for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+                int qtile, split, t0, nloc;
+                item_of(item, qtile, split, t0, nloc);
+                for (int i = 0; i < nloc; ++i) {
+                    const int t = t0 + i;
+                    for (int kb = 0; kb < p.nkb; ++kb) {
+                        mbar_wait(&empty[stage], phase ^ 1);
+                        mbar_expect_tx(&full[stage], TC_A_BYTES + TC_B_BYTES);
+                        tma_load_2d(sA + stage * TC_A_BYTES, &tq, &full[stage], kb * TC_BLOCK_K, qtile * TC_BLOCK_M);
+                        tma_load_2d(sB + stage * TC_B_BYTES, &tx, &full[stage], kb * TC_BLOCK_K, t * TC_BLOCK_N);
+                        if (++stage == TC_STAGES) { stage = 0; phase ^= 1; }
+                    }
                 }
             }
         }
@@ -234,102 +246,112 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int i = 0; i < nlocal; ++i) {
-                const int acc = i & 1;
-                const uint32_t aphase = (i >> 1) & 1;
-                mbar_wait(&tempty[acc], aphase ^ 1);
-                tc_fence_after();
-                const uint32_t d_tmem = tmem + acc * TC_BLOCK_N;
-                for (int kb = 0; kb < p.nkb; ++kb) {
-                    mbar_wait(&full[stage], phase);
+            int tix = 0;  // running accumulator-tile counter across items
+            for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+                int qtile, split, t0, nloc;
+                item_of(item, qtile, split, t0, nloc);
+                for (int i = 0; i < nloc; ++i, ++tix) {
+                    const int acc = tix & 1;
+                    const uint32_t aphase = (tix >> 1) & 1;
+                    mbar_wait(&tempty[acc], aphase ^ 1);
                     tc_fence_after();
-                    const uint64_t ad = sw128_desc(smem_u32(sA + stage * TC_A_BYTES));
-                    const uint64_t bd = sw128_desc(smem_u32(sB + stage * TC_B_BYTES));
+                    const uint32_t d_tmem = tmem + acc * TC_BLOCK_N;
+                    for (int kb = 0; kb < p.nkb; ++kb) {
+                        mbar_wait(&full[stage], phase);
+                        tc_fence_after();
+                        const uint64_t ad = sw128_desc(smem_u32(sA + stage * TC_A_BYTES));
+                        const uint64_t bd = sw128_desc(smem_u32(sB + stage * TC_B_BYTES));
 #pragma unroll
-                    for (int k = 0; k < TC_BLOCK_K / 16; ++k)  // +32 B per K=16 step inside the swizzle atom
-                        mma_f16(d_tmem, ad + 2 * k, bd + 2 * k, (kb | k) != 0);
-                    mma_commit(&empty[stage]);
-                    if (++stage == TC_STAGES) { stage = 0; phase ^= 1; }
+                        for (int k = 0; k < TC_BLOCK_K / 16; ++k)  // +32 B per K=16 step inside the swizzle atom
+                            mma_f16(d_tmem, ad + 2 * k, bd + 2 * k, (kb | k) != 0);
+                        mma_commit(&empty[stage]);
+                        if (++stage == TC_STAGES) { stage = 0; phase ^= 1; }
+                    }
+                    mma_commit(&tfull[acc]);
                 }
-                mma_commit(&tfull[acc]);
             }
         }
     } else if (warp >= 4) {
         // ---------------- epilogue: TMEM -> registers -> top-K' ----------------
         const int et = threadIdx.x - 128;  // 0..127 == TMEM lane == query within tile
         const int ew = warp - 4;
-        const int64_t my_slot = (int64_t)qtile * TC_BLOCK_M + et;
-        int64_t my_q = my_slot;
-        float cthr = INFINITY;
-        if (COLLECT) {
-            my_q = (my_slot < *p.nlist) ? p.qmap[my_slot] : -1;
-            if (my_q >= 0) cthr = p.thr[my_slot];
-        }
-        int64_t my_lim = (p.row_limit && my_q >= 0 && my_q < p.nq) ? min(p.n, p.row_limit[my_q]) : p.n;
-        if (my_q < 0) my_lim = 0;
-        float ts[TC_KP];
-        uint32_t tr[TC_KP];
-#pragma unroll
-        for (int i = 0; i < TC_KP; ++i) {
-            ts[i] = -INFINITY;
-            tr[i] = 0xFFFFFFFFu;
-        }
-        for (int i = 0; i < nlocal; ++i) {
-            const int acc = i & 1;
-            const uint32_t aphase = (i >> 1) & 1;
-            mbar_wait(&tfull[acc], aphase);
-            tc_fence_after();
-            const int64_t rbase = (int64_t)(t0 + i) * TC_BLOCK_N;
-#pragma unroll 1
-            for (int c = 0; c < TC_BLOCK_N / 32; ++c) {
-                uint32_t v[32];
-                TMEM_LD32(tmem + ((uint32_t)(ew * 32) << 16) + acc * TC_BLOCK_N + c * 32, v);
-                tmem_wait_ld();
-                const int64_t rb = rbase + c * 32;
-                const int64_t rem_rows = my_lim - rb;
-                const int lim = rem_rows < 32 ? (int)rem_rows : 32;
-                const float thr = ts[TC_KP - 1];
-                uint32_t mask = 0;
-                if (COLLECT) {
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) mask |= (__uint_as_float(v[j]) >= cthr ? 1u : 0u) << j;
-                } else {
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) mask |= (__uint_as_float(v[j]) > thr ? 1u : 0u) << j;
-                }
-                if (lim < 32) mask &= (lim <= 0) ? 0u : (0xFFFFFFFFu >> (32 - lim));
-                if (COLLECT && mask) {
-                    const int cnt = __popc(mask);
-                    const int base = atomicAdd(&p.ccount[my_slot], cnt);
-                    int o = base;
-                    while (mask && o < p.cap) {
-                        const int j = __ffs(mask) - 1;
-                        mask &= mask - 1;
-                        p.cbuf[my_slot * (int64_t)p.cap + o] = (int32_t)(rb + j);
-                        ++o;
-                    }
-                    mask = 0;
-                }
-                if (mask) {
-                    // rare: spill this chunk to smem so candidates can be indexed dynamically
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) spill[j * TC_EPI_THREADS + et] = __uint_as_float(v[j]);
-                    do {
-                        const int j = __ffs(mask) - 1;
-                        mask &= mask - 1;
-                        const float s = spill[j * TC_EPI_THREADS + et];
-                        if (s > ts[TC_KP - 1]) topk_insert(ts, tr, s, (uint32_t)(rb + j));
-                    } while (mask);
-                }
+        int tix = 0;
+        for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+            int qtile, split, t0, nloc;
+            item_of(item, qtile, split, t0, nloc);
+            const int64_t my_slot = (int64_t)qtile * TC_BLOCK_M + et;
+            int64_t my_q = my_slot;
+            float cthr = INFINITY;
+            if (COLLECT) {
+                my_q = (my_slot < *p.nlist) ? p.qmap[my_slot] : -1;
+                if (my_q >= 0) cthr = p.thr[my_slot];
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
-        }
-        if (!COLLECT) {
-            uint64_t *out = p.cand + (my_slot * p.nsplit + split) * TC_KP;
+            int64_t my_lim = (p.row_limit && my_q >= 0 && my_q < p.nq) ? min(p.n, p.row_limit[my_q]) : p.n;
+            if (my_q < 0) my_lim = 0;
+            float ts[TC_KP];
+            uint32_t tr[TC_KP];
 #pragma unroll
-            for (int s = 0; s < TC_KP; ++s) out[s] = (tr[s] == 0xFFFFFFFFu) ? 0ull : cand_key(ts[s], tr[s]);
+            for (int i = 0; i < TC_KP; ++i) {
+                ts[i] = -INFINITY;
+                tr[i] = 0xFFFFFFFFu;
+            }
+            for (int i = 0; i < nloc; ++i, ++tix) {
+                const int acc = tix & 1;
+                const uint32_t aphase = (tix >> 1) & 1;
+                mbar_wait(&tfull[acc], aphase);
+                tc_fence_after();
+                const int64_t rbase = (int64_t)(t0 + i) * TC_BLOCK_N;
+#pragma unroll 1
+                for (int c = 0; c < TC_BLOCK_N / 32; ++c) {
+                    uint32_t v[32];
+                    TMEM_LD32(tmem + ((uint32_t)(ew * 32) << 16) + acc * TC_BLOCK_N + c * 32, v);
+                    tmem_wait_ld();
+                    const int64_t rb = rbase + c * 32;
+                    const int64_t rem_rows = my_lim - rb;
+                    const int lim = rem_rows < 32 ? (int)rem_rows : 32;
+                    const float thr = ts[TC_KP - 1];
+                    uint32_t mask = 0;
+                    if (COLLECT) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) mask |= (__uint_as_float(v[j]) >= cthr ? 1u : 0u) << j;
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) mask |= (__uint_as_float(v[j]) > thr ? 1u : 0u) << j;
+                    }
+                    if (lim < 32) mask &= (lim <= 0) ? 0u : (0xFFFFFFFFu >> (32 - lim));
+                    if (COLLECT && mask) {
+                        const int cnt = __popc(mask);
+                        const int base = atomicAdd(&p.ccount[my_slot], cnt);
+                        int o = base;
+                        while (mask && o < p.cap) {
+                            const int j = __ffs(mask) - 1;
+                            mask &= mask - 1;
+                            p.cbuf[my_slot * (int64_t)p.cap + o] = (int32_t)(rb + j);
+                            ++o;
+                        }
+                        mask = 0;
+                    }
+                    if (mask) {
+                        // rare: spill this chunk to smem so candidates can be indexed dynamically
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) spill[j * TC_EPI_THREADS + et] = __uint_as_float(v[j]);
+                        do {
+                            const int j = __ffs(mask) - 1;
+                            mask &= mask - 1;
+                            const float s = spill[j * TC_EPI_THREADS + et];
+                            if (s > ts[TC_KP - 1]) topk_insert(ts, tr, s, (uint32_t)(rb + j));
+                        } while (mask);
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[acc]);
+            }
+            if (!COLLECT) {
+                uint64_t *out = p.cand + (my_slot * p.nsplit + split) * TC_KP;
+#pragma unroll
+                for (int s = 0; s < TC_KP; ++s) out[s] = (tr[s] == 0xFFFFFFFFu) ? 0ull : cand_key(ts[s], tr[s]);
+            }
         }
     }
 
@@ -698,19 +720,16 @@ int tc_make_store_map(TcStoreMap *m, const __half *x16, int64_t rows, int dp64) 
     return make_map(&m->map, x16, rows, dp64, TC_BLOCK_N);
 }
 
-static int choose_nsplit(int64_t qtiles, int64_t ntiles) {
+static int choose_nsplit_waves(int64_t qtiles, int64_t ntiles) {
     const int sms = sm_count();
     int best = 1;
     double best_eff = -1;
     int64_t lo = std::max<int64_t>(1, ceil_div<int64_t>(sms, qtiles));
     int64_t hi = std::min<int64_t>(ntiles, std::max<int64_t>(lo, 8 * sms / std::max<int64_t>(1, qtiles)));
-    hi = std::min<int64_t>(hi, 4 * 148);
     for (int64_t ns = lo; ns <= std::max(lo, hi); ++ns) {
         int64_t tps = ceil_div<int64_t>(ntiles, ns);
         int64_t real_ns = ceil_div<int64_t>(ntiles, tps);
-        int64_t ctas = qtiles * real_ns;
-        int64_t waves = ceil_div<int64_t>(ctas, sms);
-        // time ~ waves * tps ; useful work ~ qtiles * ntiles
+        int64_t waves = ceil_div<int64_t>(qtiles * real_ns, sms);
         double eff = (double)(qtiles * ntiles) / (double)(waves * sms * tps);
         if (eff > best_eff + 1e-3) {
             best_eff = eff;
@@ -718,15 +737,40 @@ static int choose_nsplit(int64_t qtiles, int64_t ntiles) {
         }
         if (ns > lo && eff > 0.97) break;
     }
+    return ntiles < 1 ? 1 : std::max(1, best);
+}
+
+static int choose_nsplit(int64_t qtiles, int64_t ntiles) {
+    // persistent CTAs take items (qtile, split) round-robin: the busiest CTA owns
+    // ceil(items / sms) items of tps tiles; pick the split count that minimises it
+    // (ties -> fewer splits = fewer candidates to rescore)
+    const int sms = sm_count();
     if (ntiles < 1) return 1;
-    return std::max(1, best);
+    int64_t best_ns = 1;
+    double best_cost = 1e300;
+    const int64_t hi = std::min<int64_t>(ntiles, std::max<int64_t>(1, (int64_t)16 * sms / std::max<int64_t>(1, qtiles)));
+    for (int64_t ns = 1; ns <= hi; ++ns) {
+        const int64_t tps = ceil_div<int64_t>(ntiles, ns);
+        const int64_t real_ns = ceil_div<int64_t>(ntiles, tps);
+        const int64_t items = qtiles * real_ns;
+        const double cost = (double)ceil_div<int64_t>(items, sms) * tps + 0.02 * real_ns;  // tiles on the busiest CTA
+        if (cost < best_cost - 1e-9) {
+            best_cost = cost;
+            best_ns = real_ns;
+        }
+    }
+    return (int)best_ns;
 }
 
 int tc_search(TcSearch &s, Carve &cv, cudaStream_t st, pr_search_stats *stats) {
     const int64_t nq_pad = round_up<int64_t>(s.nq, TC_BLOCK_M);
     const int64_t qtiles = nq_pad / TC_BLOCK_M;
     const int64_t ntiles = ceil_div<int64_t>(s.n, TC_BLOCK_N);
-    const int nsplit = choose_nsplit(qtiles, ntiles);
+    // default: one CTA per (query tile, split) item in whole waves; PR_TC_SCHEDULE=persistent
+    // runs one CTA per SM taking items round-robin (measured no faster: scripts/ab_sched.py)
+    const char *sched_env = getenv("PR_TC_SCHEDULE");
+    const bool waves = !(sched_env && sched_env[0] == 'p');
+    const int nsplit = waves ? choose_nsplit_waves(qtiles, ntiles) : choose_nsplit(qtiles, ntiles);
     const int tps = (int)ceil_div<int64_t>(ntiles, nsplit);
     __half *q16 = cv.take<__half>((size_t)nq_pad * s.dp64);
     uint64_t *cand = cv.take<uint64_t>((size_t)nq_pad * nsplit * TC_KP);
@@ -753,9 +797,10 @@ int tc_search(TcSearch &s, Carve &cv, cudaStream_t st, pr_search_stats *stats) {
                                      CL_CAP * 12 + 1024));
         attr = true;
     }
-    TcScanParams p{s.n, s.dp64 / TC_BLOCK_K, nsplit, tps, (int)ntiles, cand, s.row_limit, s.nq,
+    TcScanParams p{s.n, s.dp64 / TC_BLOCK_K, nsplit, tps, (int)ntiles, (int)qtiles, cand, s.row_limit, s.nq,
                    nullptr, nullptr, nullptr, nullptr, nullptr, 0};
-    dim3 grid((unsigned)qtiles, (unsigned)nsplit);
+    // persistent: one CTA per SM (1 CTA/SM by smem + TMEM), items assigned round-robin
+    dim3 grid((unsigned)(waves ? qtiles * nsplit : std::min<int64_t>(qtiles * nsplit, sm_count())));
     ::pr::count_launch();
     if (s.ev_begin) PR_CUDA(cudaEventRecord(s.ev_begin, st));
     tc_scan_kernel<false><<<grid, TC_THREADS, tc_smem_bytes(), st>>>(qmap.map, s.store_map->map, p);
