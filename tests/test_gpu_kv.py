@@ -94,3 +94,16 @@ def test_put_get_last_write_wins_and_erase(gpu):
     for i, t in enumerate(oracle):
         assert hit[i] == (0 if t in gs else 1)
     L.pr_kv_destroy(h)
+
+
+def test_sharded_kv_single_rank_device_path(gpu):
+    from paper_2506_21593_b200.sharded_kv import ShardedKV
+
+    kv = ShardedKV(capacity=10000)
+    keys = [f"query-{i:09d}" for i in range(5000)]
+    kv.put(keys + keys[:7], list(range(5000)) + [9000 + i for i in range(7)])
+    vals, hit = kv.get(keys + ["absent", "query-00000000"])
+    vals = vals.cpu().numpy()
+    assert list(vals[:7]) == [9000 + i for i in range(7)]
+    assert list(vals[7:5000]) == list(range(7, 5000))
+    assert vals[5000] == -1 and vals[5001] == -1 and not bool(hit[5000])
