@@ -187,11 +187,15 @@ def _route_prefix(router, qs, vectors, mode):
     sc_limit = n_pre_sc + np.searchsorted(new_js, ar, side="left")  # rows written by queries i < j
     l2 = np.zeros(B, dtype=bool)
     sc_row = np.full(B, -1, dtype=np.int64)
-    if L2 in pos and B:
-        r = sc_index.search_batch(Vd, 1, mode=mode, validate=False, row_limit=sc_limit, count=False)
+    # only queries that actually probe L2 are searched (an L1 hit in front of it ends the cascade)
+    need2 = ~l1 if (L1 in pos and L2 in pos and pos[L1] < pos[L2]) else np.ones(B, dtype=bool)
+    js2 = np.nonzero(need2)[0]
+    if L2 in pos and js2.size:
+        sel = torch.from_numpy(js2).cuda()
+        r = sc_index.search_batch(Vd[sel], 1, mode=mode, validate=False, row_limit=sc_limit[js2], count=False)
         prof.note("sc", sc_index)
-        sc_row = r.rows[:, 0].cpu().numpy()
-        l2 = (r.count.cpu().numpy() > 0) & (r.scores[:, 0].cpu().numpy() >= sc.threshold)
+        sc_row[js2] = r.rows[:, 0].cpu().numpy()
+        l2[js2] = (r.count.cpu().numpy() > 0) & (r.scores[:, 0].cpu().numpy() >= sc.threshold)
 
     prof.mark("l2")
     # ---- L4/L5 speculation for every query that can reach them

@@ -257,6 +257,8 @@ class FlatIndex:
         if k < 1:
             raise ValueError("k must be >= 1")
         torch = _torch()
+        if isinstance(queries, np.ndarray) and not queries.flags.writeable:
+            queries = np.array(queries)  # torch refuses read-only numpy memory (EmbeddingVector values)
         q = torch.as_tensor(queries, dtype=torch.float32)
         if q.dim() != 2 or q.shape[1] != self._dim:
             raise InvalidVector(f"expected [B, {self._dim}] queries, got {tuple(q.shape)}")
