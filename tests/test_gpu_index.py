@@ -149,6 +149,78 @@ def test_upsert_keeps_row(gpu, rng):
     assert idx.payload("x") == 3 and len(idx) == 2
 
 
+@pytest.mark.parametrize("mode,k", [(1, 5), (2, 5), (2, 1), (0, 80)])
+def test_row_limits_match_prefix_oracle(gpu, rng, mode, k):
+    """pr_index_search_ex: query q must see exactly rows [0, limit[q])."""
+    import torch
+
+    from oracle import flat_index as F
+    from paper_2506_21593_b200 import FlatIndex
+
+    n, d = 9000, 64
+    X = _store(rng, n, d)
+    X[4000:4100] = X[50]  # ties straddling some limits
+    Q = random_unit_vectors(rng, 130, d)
+    Q[:10] = X[50]
+    lim = rng.integers(0, n + 500, Q.shape[0])
+    lim[0], lim[1], lim[2] = 0, 51, 4050
+    idx = FlatIndex(dim=d)
+    idx.extend_arrays([f"e{i}" for i in range(n)], X)
+    res = idx.search_batch(torch.from_numpy(Q), k, mode=mode, row_limit=torch.from_numpy(lim))
+    rows, raw, cnt = res.rows.cpu().numpy(), res.raw.cpu().numpy(), res.count.cpu().numpy()
+    for b in range(Q.shape[0]):
+        m = int(min(lim[b], n))
+        want = F.search(X[:m], Q[b:b + 1], k)
+        assert cnt[b] == want.count[0], b
+        c = int(want.count[0])
+        np.testing.assert_array_equal(rows[b, :c], want.rows[0, :c], err_msg=f"q{b} lim {lim[b]}")
+        np.testing.assert_array_equal(raw[b, :c], want.raw[0, :c])
+
+
+def test_truncate_and_clear_hide_stale_rows(gpu, rng):
+    import torch
+
+    from oracle import flat_index as F
+    from paper_2506_21593_b200 import MODE_EXACT, MODE_TENSOR, FlatIndex
+
+    d = 128
+    X = random_unit_vectors(rng, 30000, d)
+    Q = random_unit_vectors(rng, 64, d)
+    Q[0] = X[25000]  # only present in the truncated tail
+    idx = FlatIndex(dim=d)
+    idx.extend_arrays([f"e{i}" for i in range(30000)], X)
+    idx.truncate(20000)
+    for mode in (MODE_EXACT, MODE_TENSOR):
+        res = idx.search_batch(torch.from_numpy(Q), 5, mode=mode)
+        want = F.search(X[:20000], Q, 5)
+        np.testing.assert_array_equal(res.rows.cpu().numpy(), want.rows)
+    idx.clear()
+    Y = random_unit_vectors(rng, 5000, d)
+    idx.extend_arrays([f"f{i}" for i in range(5000)], Y)
+    res = idx.search_batch(torch.from_numpy(Q), 5, mode=MODE_TENSOR)
+    np.testing.assert_array_equal(res.rows.cpu().numpy(), F.search(Y, Q, 5).rows)
+    # in-place update (upsert) is visible to both copies (fp32 exact + fp16 scan)
+    idx.insert("f7", Q[3])
+    Y[7] = Q[3]
+    res = idx.search_batch(torch.from_numpy(Q), 3, mode=MODE_TENSOR)
+    np.testing.assert_array_equal(res.rows.cpu().numpy(), F.search(Y, Q, 3).rows)
+    assert res.rows[3, 0].item() == 7 and res.scores[3, 0].item() == 1.0
+
+
+def test_tensor_request_with_large_k_and_empty_batch(gpu, rng):
+    import torch
+
+    from paper_2506_21593_b200 import MODE_TENSOR, FlatIndex
+
+    X = _store(rng, 20000, 64)
+    Q = random_unit_vectors(rng, 9, 64)
+    idx = FlatIndex(dim=64)
+    idx.extend_arrays([f"e{i}" for i in range(20000)], X)
+    _check(idx, X, Q, 40, MODE_TENSOR)  # k > 16 candidates/split: exact path serves it
+    res = idx.search_batch(torch.zeros((0, 64)), 5, mode=MODE_TENSOR)
+    assert res.rows.shape == (0, 5)
+
+
 def test_big_k(gpu, rng):
     from paper_2506_21593_b200 import FlatIndex
 
