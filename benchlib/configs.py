@@ -239,6 +239,12 @@ def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_se
         return r
 
     router = make_router()
+    # warm-up: one batch of an unrelated session (first-launch module loading, scratch allocation)
+    _, warm = session_stream(questions, batch, seed + 1000, 0)
+    router.route_batch([validate_query(t, "warmup", query_id=f"w{i}", issued_at_ns=0)
+                        for i, (t, _) in enumerate(warm)], materialize=False)
+    router.reset_session()
+    router.trace.clear()
     router.profile_batches = profile
     layer_counts = {}
     e0, e1 = _events()

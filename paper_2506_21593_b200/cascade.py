@@ -228,8 +228,7 @@ def _route_prefix(router, qs, vectors, mode):
             seeds_before = np.concatenate([[0], np.cumsum(kb_cnt)[:-1]]).astype(np.int64)
             if seed_rows.size:
                 scratch = _seed_scratch(router, kb.index.dim)
-                scratch.append_rows_from(kb.index, seed_rows, [str(i) for i in range(seed_rows.size)],
-                                         [None] * seed_rows.size)
+                scratch.append_anonymous_from(kb.index, seed_rows)
                 rs = scratch.search_batch(Vs, 1, mode=mode, validate=False, row_limit=seeds_before, count=False)
                 prof.note("seeds", scratch)
                 l4_unsure[spec] |= (rs.count.cpu().numpy() > 0) & (rs.scores[:, 0].cpu().numpy() >= thr)
@@ -288,6 +287,9 @@ def _route_prefix(router, qs, vectors, mode):
     latest: dict[str, int] = {}
     k_ctx = cfg.retrieval_k
     v1, v2, v3 = int(L1), int(L2), int(L3)
+    # the stub LLM answers with the top passage's annotation (generation.py:83-115):
+    # compute that directly instead of building a context answer object per query
+    stub = isinstance(backend, generation.StubBackend) and 0.0 <= backend.context_confidence <= 1.0
     for j in range(p):
         code = serving[j]
         t = texts[j]
@@ -307,9 +309,15 @@ def _route_prefix(router, qs, vectors, mode):
         else:
             s = slot[j]
             rows = kb_rows[s, : min(k_ctx, int(kb_cnt[s]))]
-            passages = [kb.index.payload_at(int(r)) for r in rows]
-            a = generation.generate_with_context(backend, qs[j], passages, L5)
-            text[j], conf[j] = a.text, a.confidence
+            if stub:
+                top = kb.index.payload_at(int(rows[0]))
+                backend.context_calls += 1
+                text[j] = top.answer if top.answer else generation.first_sentence(top.text)
+                conf[j] = backend.context_confidence
+            else:
+                passages = [kb.index.payload_at(int(r)) for r in rows]
+                a = generation.generate_with_context(backend, qs[j], passages, L5)
+                text[j], conf[j] = a.text, a.confidence
             ctx_rows[j] = rows
         latest[t] = j
     probe_prefix = {}

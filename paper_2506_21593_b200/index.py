@@ -44,6 +44,16 @@ class SearchHit:
     rank: int
 
 
+class RowRef:
+    """Deferred payload: "the payload of row ``row`` of ``index``" (resolved on first read)."""
+
+    __slots__ = ("index", "row")
+
+    def __init__(self, index, row: int):
+        self.index = index
+        self.row = row
+
+
 @dataclass
 class BatchResult:
     """Device tensors of one batched search."""
@@ -118,10 +128,14 @@ class FlatIndex:
 
     def payload(self, entry_id: str) -> Any:
         with self._lock:
-            return self._payloads[self._row_by_id[entry_id]]
+            return self.payload_at(self._row_by_id[entry_id])
 
     def payload_at(self, row: int) -> Any:
-        return self._payloads[row]
+        p = self._payloads[row]
+        if type(p) is RowRef:  # payload copied by reference from another index's row
+            p = p.index.payload_at(p.row)
+            self._payloads[row] = p
+        return p
 
     def vector(self, entry_id: str) -> np.ndarray:
         with self._lock:
@@ -202,6 +216,19 @@ class FlatIndex:
             self._ids.extend(ids)
             self._payloads.extend(payloads if payloads is not None else [None] * len(ids))
         return len(ids)
+
+    def append_anonymous_from(self, src: "FlatIndex", src_rows) -> None:
+        """Append rows copied from ``src`` without ids or payloads (scratch stores that
+        are only searched, never looked up by id)."""
+        torch = _torch()
+        r = torch.as_tensor(src_rows, dtype=torch.int64).to("cuda").contiguous()
+        with self._lock:
+            _lib.check(
+                self._L.pr_index_append_from(self._h, src.handle, _lib.ptr(r), r.numel(), _lib.stream_ptr()),
+                "append_from",
+            )
+            self._ids.extend([None] * r.numel())
+            self._payloads.extend([None] * r.numel())
 
     def append_rows_from(self, src: "FlatIndex", src_rows, ids: list[str], payloads: list[Any]) -> None:
         """Append rows copied device-to-device from another index (AKM settle
@@ -331,7 +358,7 @@ class FlatIndex:
         with self._lock:
             n = len(self._ids)
             vec_block = self.read_rows(0, n).cpu().numpy().tobytes() if n else b""
-            lines = [json.dumps({"id": self._ids[i], "payload": enc(self._payloads[i])}, ensure_ascii=False)
+            lines = [json.dumps({"id": self._ids[i], "payload": enc(self.payload_at(i))}, ensure_ascii=False)
                      for i in range(n)]
             meta = ("\n".join(lines) + ("\n" if lines else "")).encode("utf-8")
             body = vec_block + meta
