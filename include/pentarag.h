@@ -43,6 +43,8 @@ extern "C" {
 #define PR_SEARCH_AUTO 0   /* tensor-core scan when eligible, else exact  */
 #define PR_SEARCH_EXACT 1  /* fp64 einsum-order scan of every row          */
 #define PR_SEARCH_TENSOR 2 /* tcgen05 fp16 scan + certified fp64 rescoring */
+#define PR_SEARCH_TENSOR_I8 3 /* tcgen05 int8 scan with per-row error bounds + fp64 rescoring of the
+                                 complete candidate set (same results, ~1.6x the scan rate) */
 
 typedef struct pr_index pr_index;
 typedef struct pr_kv pr_kv;
@@ -55,8 +57,9 @@ typedef struct pr_search_stats {
     int64_t fallback;       /* failed the certificate -> exact fp64 rescan      */
     int64_t candidates;     /* rows rescored in fp64 after the tensor scan      */
     int32_t nsplit;         /* row splits used by the scan grid                 */
-    int32_t path;           /* PR_SEARCH_EXACT or PR_SEARCH_TENSOR              */
+    int32_t path;           /* PR_SEARCH_EXACT, PR_SEARCH_TENSOR or _TENSOR_I8  */
     int64_t collected;      /* failed the certificate -> tcgen05 collect pass   */
+    int64_t appended;       /* int8 path: rows appended by the scan (pre-filter) */
 } pr_search_stats;
 
 /* ---- library ------------------------------------------------------------ */
@@ -71,9 +74,10 @@ int pr_device_info(int *sm_count, int *cc_major, int *cc_minor);
 int pr_check_unit(const float *d_vecs, int64_t n, int dim, double tol, uint8_t *d_bad, void *stream);
 
 /* ---- flat index store: index.py:73-153 (FlatIndex storage, insert/extend) --
- * Rows are kept twice: fp32 (the exact copy every score is computed from, as
- * _vectors32/_vectors64 at index.py:82-83,144-145) and fp16 (the tensor-core
- * scan copy).  Row i is the i-th inserted entry id, so row order is the
+ * Rows are kept three times: fp32 (the exact copy every score is computed
+ * from, as _vectors32/_vectors64 at index.py:82-83,144-145), fp16 (the
+ * certified tensor-core scan copy) and int8 with a per-row scale and a
+ * rounded-up quantisation-error norm (the int8 tensor-core scan copy).  Row i is the i-th inserted entry id, so row order is the
  * reference's insertion (tie-break) order. */
 int pr_index_create(int dim, int64_t capacity, uint32_t flags, pr_index **out);
 int pr_index_destroy(pr_index *h);

@@ -25,7 +25,7 @@ from .errors import (
 from .caches import CacheEntry, FixedKVCache, SemanticCache, writeback
 from .errors import MalformedJsonl
 from .generation import StubBackend, StubKnowledgeTable, generate_with_context, memory_recall
-from .index import MODE_AUTO, MODE_EXACT, MODE_TENSOR, BatchResult, FlatIndex, SearchHit
+from .index import MODE_AUTO, MODE_EXACT, MODE_TENSOR, MODE_TENSOR_I8, BatchResult, FlatIndex, SearchHit
 from .knowledge import AdaptiveKnowledgeMemory, MainKnowledgeBase, ingest_corpus
 from .router import CascadeRouter, LayerProbe, RouterConfig, RouteTraceEvent, TraceLog, export_triples
 from .sharded import ShardedFlatIndex, shard_range

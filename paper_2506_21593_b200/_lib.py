@@ -27,6 +27,7 @@ c_vp = ctypes.c_void_p
 PR_SEARCH_AUTO = 0
 PR_SEARCH_EXACT = 1
 PR_SEARCH_TENSOR = 2
+PR_SEARCH_TENSOR_I8 = 3
 
 PR_OK = 0
 PR_ERR_BAD_ARG = -1
@@ -46,6 +47,7 @@ class SearchStats(ctypes.Structure):
         ("nsplit", ctypes.c_int32),
         ("path", ctypes.c_int32),
         ("collected", c_i64),
+        ("appended", c_i64),
     ]
 
 

@@ -471,12 +471,15 @@ __global__ void merge_shards_kernel(const int64_t *__restrict__ rows, const doub
 // ===========================================================================
 // handle
 struct pr_index {
-    int dim = 0, dp8 = 0, dp64 = 0;
+    int dim = 0, dp8 = 0, dp64 = 0, dp128 = 0;
     int64_t count = 0, cap = 0, cap256 = 0;
     float *x32 = nullptr;
     __half *x16 = nullptr;
+    pr::I8Rows r8;               // int8 scan copy [cap256, dp128] + per-row scale / error bound
     pr::TcStoreMap tmap;  // TMA descriptor of x16 (rebuilt on reallocation)
     bool tmap_ok = false;
+    pr::TcStoreMap tmap8;  // TMA descriptor of x8
+    bool tmap8_ok = false;
     pr_search_stats stats{};
     // device scratch (grown on demand, stream-ordered)
     void *scratch = nullptr;
@@ -525,25 +528,51 @@ static int reserve(pr_index *h, int64_t cap, cudaStream_t st) {
     int64_t c256 = round_up<int64_t>(c, 256);
     float *nx32 = nullptr;
     __half *nx16 = nullptr;
+    pr::I8Rows n8;
+    n8.maxnorm = h->r8.maxnorm;
+    const int64_t ntile = c256 / 256;
     PR_CUDA(cudaMalloc(&nx32, (size_t)c * h->dp8 * sizeof(float)));
     cudaError_t e = cudaMalloc(&nx16, (size_t)c256 * h->dp64 * sizeof(__half));
+    if (e == cudaSuccess) e = cudaMalloc(&n8.x8, (size_t)c256 * h->dp128);
+    if (e == cudaSuccess) e = cudaMalloc(&n8.xs, (size_t)c256 * sizeof(float));
+    if (e == cudaSuccess) e = cudaMalloc(&n8.xe, (size_t)c256 * sizeof(float));
+    if (e == cudaSuccess) e = cudaMalloc(&n8.xt, (size_t)ntile * sizeof(float4));
     if (e != cudaSuccess) {
         cudaFree(nx32);
+        cudaFree(nx16);
+        cudaFree(n8.x8);
+        cudaFree(n8.xs);
+        cudaFree(n8.xe);
         PR_FAIL(PR_ERR_NOMEM, "index reserve(%lld rows): %s", (long long)c, cudaGetErrorString(e));
     }
     PR_CUDA(cudaMemsetAsync(nx16, 0, (size_t)c256 * h->dp64 * sizeof(__half), st));
+    PR_CUDA(cudaMemsetAsync(n8.x8, 0, (size_t)c256 * h->dp128, st));
+    PR_CUDA(cudaMemsetAsync(n8.xs, 0, (size_t)c256 * sizeof(float), st));
+    PR_CUDA(cudaMemsetAsync(n8.xe, 0, (size_t)c256 * sizeof(float), st));
+    PR_CUDA(cudaMemsetAsync(n8.xt, 0, (size_t)ntile * sizeof(float4), st));
     if (h->count > 0) {
         PR_CUDA(cudaMemcpyAsync(nx32, h->x32, (size_t)h->count * h->dp8 * sizeof(float), cudaMemcpyDeviceToDevice, st));
         PR_CUDA(cudaMemcpyAsync(nx16, h->x16, (size_t)h->count * h->dp64 * sizeof(__half), cudaMemcpyDeviceToDevice, st));
+        PR_CUDA(cudaMemcpyAsync(n8.x8, h->r8.x8, (size_t)h->count * h->dp128, cudaMemcpyDeviceToDevice, st));
+        PR_CUDA(cudaMemcpyAsync(n8.xs, h->r8.xs, (size_t)h->count * sizeof(float), cudaMemcpyDeviceToDevice, st));
+        PR_CUDA(cudaMemcpyAsync(n8.xe, h->r8.xe, (size_t)h->count * sizeof(float), cudaMemcpyDeviceToDevice, st));
+        PR_CUDA(cudaMemcpyAsync(n8.xt, h->r8.xt, (size_t)(h->cap256 / 256) * sizeof(float4), cudaMemcpyDeviceToDevice,
+                                st));
     }
     PR_CUDA(cudaStreamSynchronize(st));
     if (h->x32) cudaFree(h->x32);
     if (h->x16) cudaFree(h->x16);
+    cudaFree(h->r8.x8);
+    cudaFree(h->r8.xs);
+    cudaFree(h->r8.xe);
+    cudaFree(h->r8.xt);
     h->x32 = nx32;
     h->x16 = nx16;
+    h->r8 = n8;
     h->cap = c;
     h->cap256 = c256;
     h->tmap_ok = false;
+    h->tmap8_ok = false;
     return PR_OK;
 }
 
@@ -607,7 +636,10 @@ int exact_search(pr_index *h, const float *Qp, const int32_t *qsel, const int32_
     int QT = pick_qt(nsel_max, h->dp8, K);
     int nsplit;
     int64_t rps;
-    choose_splits(h->count, ceil_div(nsel_max, QT), &nsplit, &rps);
+    // a device-sized selection (fallback list) is usually a handful of queries:
+    // split the rows finely enough to fill the GPU even then
+    const int tiles_hint = nsel_dev ? std::min(ceil_div(nsel_max, QT), 4) : ceil_div(nsel_max, QT);
+    choose_splits(h->count, tiles_hint, &nsplit, &rps);
     double *ps = cv.take<double>((size_t)nsel_max * nsplit * K);
     int64_t *prr = cv.take<int64_t>((size_t)nsel_max * nsplit * K);
     int32_t *pc = cv.take<int32_t>((size_t)nsel_max * nsplit);
@@ -685,12 +717,15 @@ int pr_index_create(int dim, int64_t capacity, uint32_t flags, pr_index **out) {
     h->dim = dim;
     h->dp8 = round_up(dim, 8);
     h->dp64 = round_up(dim, 64);
+    h->dp128 = round_up(dim, 128);
     int rc = reserve(h, std::max<int64_t>(capacity, 1024), nullptr);
     if (rc) {
         delete h;
         return rc;
     }
     PR_CUDA(cudaMalloc(&h->d_counters, 16 * sizeof(int32_t)));
+    PR_CUDA(cudaMalloc(&h->r8.maxnorm, sizeof(uint32_t)));
+    PR_CUDA(cudaMemset(h->r8.maxnorm, 0, sizeof(uint32_t)));
     *out = h;
     return PR_OK;
 }
@@ -700,6 +735,11 @@ int pr_index_destroy(pr_index *h) {
     cudaDeviceSynchronize();
     if (h->x32) cudaFree(h->x32);
     if (h->x16) cudaFree(h->x16);
+    cudaFree(h->r8.x8);
+    cudaFree(h->r8.xs);
+    cudaFree(h->r8.xe);
+    cudaFree(h->r8.xt);
+    cudaFree(h->r8.maxnorm);
     if (h->scratch) cudaFree(h->scratch);
     if (h->d_counters) cudaFree(h->d_counters);
     for (auto &p : h->ev_pending) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
@@ -726,6 +766,8 @@ int pr_index_append(pr_index *h, const float *d_vecs, int64_t n, void *stream) {
     write_rows_kernel<<<grid_for(n * h->dp64), 256, 0, st>>>(d_vecs, n, h->dim, nullptr, h->count, h->x32, h->dp8,
                                                               h->x16, h->dp64);
     PR_LAUNCH_CHECK();
+    rc = pr::i8_quantize_rows(d_vecs, n, h->dim, nullptr, h->count, h->dp128, h->r8, st);
+    if (rc) return rc;
     h->count += n;
     return PR_OK;
 }
@@ -737,7 +779,7 @@ int pr_index_update_rows(pr_index *h, const int64_t *d_rows, const float *d_vecs
     write_rows_kernel<<<grid_for(n * h->dp64), 256, 0, as_stream(stream)>>>(d_vecs, n, h->dim, d_rows, 0, h->x32,
                                                                              h->dp8, h->x16, h->dp64);
     PR_LAUNCH_CHECK();
-    return PR_OK;
+    return pr::i8_quantize_rows(d_vecs, n, h->dim, d_rows, 0, h->dp128, h->r8, as_stream(stream));
 }
 
 int pr_index_clear(pr_index *h) {
@@ -771,6 +813,8 @@ int pr_index_append_from(pr_index *h, const pr_index *src, const int64_t *d_src_
     gather_rows_kernel<<<grid_for(n * h->dp64), 256, 0, st>>>(src->x32, src->x16, d_src_rows, n, h->dp8, h->dp64,
                                                                h->count, h->x32, h->x16);
     PR_LAUNCH_CHECK();
+    rc = pr::i8_gather_rows(src->r8, d_src_rows, n, h->dp128, h->count, h->r8, st);
+    if (rc) return rc;
     h->count += n;
     return PR_OK;
 }
@@ -785,7 +829,7 @@ int pr_index_search_ex(pr_index *h, const float *d_q, int64_t nq, int k, uint32_
     if (!h) PR_FAIL(PR_ERR_BAD_ARG, "null handle");
     if (k < 1) PR_FAIL(PR_ERR_BAD_ARG, "k must be >= 1");  // index.py:161-162
     if (nq < 0 || nq > INT32_MAX / 2) PR_FAIL(PR_ERR_BAD_ARG, "bad query count");
-    if (mode > PR_SEARCH_TENSOR) PR_FAIL(PR_ERR_BAD_ARG, "bad mode");
+    if (mode > PR_SEARCH_TENSOR_I8) PR_FAIL(PR_ERR_BAD_ARG, "bad mode");
     cudaStream_t st = as_stream(stream);
     h->last_stream = st;
     h->stats = pr_search_stats{};
@@ -807,9 +851,12 @@ int pr_index_search_ex(pr_index *h, const float *d_q, int64_t nq, int k, uint32_
     const bool tensor_ok = pr::tc_eligible(h->dim, h->count, k);
     bool use_tc = (mode == PR_SEARCH_TENSOR) || (mode == PR_SEARCH_AUTO && tensor_ok && pr::tc_worthwhile(h->count, nq));
     if (use_tc && !tensor_ok) use_tc = false;
+    const bool use_i8 = mode == PR_SEARCH_TENSOR_I8 && tensor_ok && pr::tc8_eligible(h->dim);
+    if (mode == PR_SEARCH_TENSOR_I8 && !use_i8 && tensor_ok) use_tc = true;  // d > 2048: the fp16 scan
 
     size_t need = (size_t)nq * h->dp8 * sizeof(float) + exact_scratch_bytes((int)nq, k, h->count) + 65536;
     if (use_tc) need += pr::tc_scratch_bytes(nq, h->dp64, h->count, k);
+    if (use_i8) need += pr::tc8_scratch_bytes(nq, h->dp128, h->count);
     int rc = ensure_scratch(h, need, st);
     if (rc) return rc;
     Carve cv{reinterpret_cast<char *>(h->scratch)};
@@ -818,6 +865,38 @@ int pr_index_search_ex(pr_index *h, const float *d_q, int64_t nq, int k, uint32_
     pad_queries_kernel<<<grid_for(nq * h->dp8), 256, 0, st>>>(d_q, nq, h->dim, h->dp8, Qp);
     PR_LAUNCH_CHECK();
 
+    if (use_i8) {
+        h->stats.path = PR_SEARCH_TENSOR_I8;
+        if (!h->tmap8_ok) {
+            rc = pr::i8_make_store_map(&h->tmap8, h->r8.x8, h->cap256, h->dp128);
+            if (rc) return rc;
+            h->tmap8_ok = true;
+        }
+        pr::Tc8Search ts{};
+        ts.x32 = h->x32;
+        ts.store_map = &h->tmap8;
+        ts.rows8 = h->r8;
+        ts.n = h->count;
+        ts.d = h->dim;
+        ts.dp8 = h->dp8;
+        ts.dp128 = h->dp128;
+        ts.qp = Qp;
+        ts.nq = nq;
+        ts.k = k;
+        ts.rows = d_rows;
+        ts.raw = d_raw;
+        ts.rep = d_reported;
+        ts.count = d_count;
+        ts.counters = h->d_counters;
+        ts.row_limit = d_row_limit;
+        rc = timing_pair(h, &ts.ev_begin, &ts.ev_end);
+        if (rc) return rc;
+        rc = pr::tc8_search(ts, cv, st, &h->stats);
+        if (rc) return rc;
+        // candidate-buffer overflows -> exact rescan of just those queries
+        return exact_search(h, Qp, ts.fallback_list, h->d_counters, (int)nq, k, d_rows, d_raw, d_reported, d_count,
+                            cv, st, false, d_row_limit);
+    }
     if (!use_tc) {
         h->stats.path = PR_SEARCH_EXACT;
         return exact_search(h, Qp, nullptr, nullptr, (int)nq, k, d_rows, d_raw, d_reported, d_count, cv, st, true,
@@ -884,13 +963,16 @@ long long pr_launch_count(void) { return g_launches.load(); }
 
 int pr_index_last_stats(pr_index *h, pr_search_stats *out) {
     if (!h || !out) PR_FAIL(PR_ERR_BAD_ARG, "null");
-    if (h->stats.path == PR_SEARCH_TENSOR) {
+    if (h->stats.path == PR_SEARCH_TENSOR || h->stats.path == PR_SEARCH_TENSOR_I8) {
         int32_t c[4];
         PR_CUDA(cudaMemcpyAsync(c, h->d_counters, sizeof(c), cudaMemcpyDeviceToHost, h->last_stream));
         PR_CUDA(cudaStreamSynchronize(h->last_stream));
         h->stats.fallback = c[0];
         h->stats.candidates = c[1];
-        h->stats.collected = c[2];
+        if (h->stats.path == PR_SEARCH_TENSOR)
+            h->stats.collected = c[2];
+        else
+            h->stats.appended = c[3];
         h->stats.tensor_queries = h->stats.queries;
     }
     *out = h->stats;

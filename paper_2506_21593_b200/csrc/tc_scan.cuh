@@ -39,11 +39,47 @@ struct TcSearch {
     const int64_t *row_limit = nullptr;                  // per query: rows >= limit invisible
 };
 
+// int8 tcgen05 scan (tc_scan_i8.cu): per-row quantised store + complete candidate set
+struct I8Rows {
+    int8_t *x8 = nullptr;         // [cap256, dp128] quantised rows
+    float *xs = nullptr;          // [cap256] per-row scale s_r
+    float *xe = nullptr;          // [cap256] rounded-up ||x_r - s_r xq_r||_2
+    float4 *xt = nullptr;         // [cap256 / 256] {max xe over the 256-row tile, 0, 0, 0}
+    uint32_t *maxnorm = nullptr;  // device scalar: max ||x_r|| (fp32 bits, rounded up)
+};
+struct Tc8Search {
+    const float *x32;
+    const TcStoreMap *store_map;  // TMA map of rows8.x8
+    I8Rows rows8;
+    int64_t n;
+    int d, dp8, dp128;
+    const float *qp;  // padded fp32 queries [nq, dp8]
+    int64_t nq;
+    int k;
+    int64_t *rows;
+    double *raw, *rep;
+    int32_t *count;
+    int32_t *counters;       // [0] fallback, [1] rescored rows, [3] appended rows
+    int32_t *fallback_list;  // out: queries whose candidate buffer overflowed
+    cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
+    const int64_t *row_limit = nullptr;
+};
+int i8_quantize_rows(const float *src, int64_t n, int d, const int64_t *rows, int64_t row0, int dp128, I8Rows &m,
+                     cudaStream_t st);
+int i8_gather_rows(const I8Rows &src, const int64_t *src_rows, int64_t n, int dp128, int64_t row0, I8Rows &m,
+                   cudaStream_t st);
+int i8_make_store_map(TcStoreMap *m, const int8_t *x8, int64_t rows, int dp128);
+bool tc8_eligible(int d);
+size_t tc8_scratch_bytes(int64_t nq, int dp128, int64_t n);
+int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats);
+
 bool tc_eligible(int d, int64_t n, int k);
 bool tc_worthwhile(int64_t n, int64_t nq);
 size_t tc_scratch_bytes(int64_t nq, int dp64, int64_t n, int k);
 int tc_make_store_map(TcStoreMap *m, const __half *x16, int64_t rows, int dp64);
 int tc_search(TcSearch &s, Carve &cv, cudaStream_t st, pr_search_stats *stats);
+int make_map_2d(CUtensorMap *m, const void *base, int64_t rows, int cols, int elem_bytes, int box_cols, int box_rows);
+int choose_nsplit_waves(int64_t qtiles, int64_t ntiles);
 // fp16 rounding + tensor-core accumulation error bound for unit vectors of dim d
 double tc_error_bound(int d, int dp64);
 

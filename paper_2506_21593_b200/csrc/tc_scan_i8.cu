@@ -1,0 +1,959 @@
+// Int8 tensor-core score + select for FlatIndex.search (index.py:155-189), sm_100a.
+//
+// The fp16 scan (tc_scan.cu) is tensor-bound at ~0.93 of the sustained fp16
+// peak; kind::i8 runs the same contraction at ~1.6x the rate under the 1 kW
+// power cap (cuBLAS at the scan's shape: 1802 vs 1136 TOP/s sustained,
+// scripts/probe_lowp_peaks.py).  Exactness comes from a rigorous PER-ROW
+// bound on the quantisation error and a complete candidate set:
+//
+//   row r:   x ~= s_r * xq_r      (xq int8, ||xq||_2 <= 2047)   dx_r >= ||x_r - s_r xq_r||_2
+//   query q: q ~= t_q * qq       (qq int8)  A_q >= ||t_q qq||_2,  B_q >= ||q - t_q qq||_2
+//   acc = qq . xq_r exactly (int32 TMEM accumulator, |acc| < 2^22), ap = t_q s_r acc
+//   |q.x_r - ap| <= A_q dx_r + B_q ||x_r|| <= A_q dx_r + C_q,   C_q = B_q max||x|| + rounding slack
+//   u_r = ap + A_q dx_r + C_q  >=  exact score of row r (numpy einsum, fp64)
+//
+//   l_r = ap - A_q dx_r - C_q  <=  exact score of row r
+//
+// L = the k-th largest l over all rows is a lower bound on the true k-th score
+// e_k (k rows score >= L), and so is the exact k-th score of any k distinct
+// rows.  Every row of the true top-k (ties included) has u >= exact >= e_k.
+// 1) A pilot scan over every 32nd 256-row tile keeps per-thread top-k lists of
+//    l; the seed kernel scores the best k of them exactly: seeds + a first
+//    bound per query.  2) The main scan APPENDS every row with u >= the current
+//    bound (the max of the seed bound, the thread's running k-th l, and the
+//    running values other CTAs scanning the same query publish in global
+//    memory).  3) The post kernel streams the appended rows with u >= the
+//    seeds' k-th exact score through an exact running top-k and ranks by
+//    (score desc, row asc): the reference's top-k, bit for bit, with no
+//    certificate that can fail (only a per-query buffer overflow sends a
+//    query to the exact fp64 scan).
+#include <cuda.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "ptx.cuh"
+#include "select.cuh"
+#include "tc_scan.cuh"
+
+namespace pr {
+
+constexpr int I8_BLOCK_K = 128;  // int8 columns per stage = one 128-B swizzle atom
+constexpr int I8_STAGES = 4;
+constexpr int I8_THREADS = 256;
+constexpr int I8_EPI = 128;
+constexpr int I8_A_BYTES = TC_BLOCK_M * I8_BLOCK_K;  // 16 KB
+constexpr int I8_B_BYTES = TC_BLOCK_N * I8_BLOCK_K;  // 32 KB
+constexpr int I8_META_BYTES = TC_BLOCK_N * 4 * 2 + 16;  // s_r[256], dx_r[256], tile {dxmax, -, -, -}
+constexpr int I8_TMEM_COLS = 512;
+constexpr int I8_CAP = 32768;              // appended candidates per query before the exact fallback
+constexpr size_t I8_BUF_BYTES = 3ull << 30;  // ... unless the batch's buffers would exceed this
+// ||qq||_2, ||xq||_2 <= I8_KMAX, so |acc| <= I8_KMAX^2 < 2^22 and the int32 -> fp32
+// conversion is exact with one integer add + one fp32 subtract (no XU-pipe I2F)
+constexpr double I8_KMAX = 2047.0;
+constexpr int32_t I8_MAGIC_I = 0x4B400000;  // bits of 1.5 * 2^23
+constexpr float I8_MAGIC_F = 12582912.0f;
+
+// kind::i8 instruction descriptor: D = S32, A,B = signed int8 K-major, N = 256, M = 128
+constexpr uint32_t I8_IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TC_BLOCK_N >> 3) << 17) |
+                              ((uint32_t)(TC_BLOCK_M >> 4) << 24);
+
+constexpr size_t i8_smem_bytes() {
+    return 1024 + (size_t)I8_STAGES * (I8_A_BYTES + I8_B_BYTES) + 2 * (size_t)I8_META_BYTES +
+           (size_t)32 * I8_EPI * 4 + 256;
+}
+
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(I8_IDESC), "r"(accum)
+        : "memory");
+}
+
+// exact for |v| < 2^22
+__device__ __forceinline__ float i2f_exact(uint32_t v) {
+    return __fsub_rn(__int_as_float((int32_t)v + I8_MAGIC_I), I8_MAGIC_F);
+}
+
+// order-preserving float <-> uint32 (0 = below every float = "no bound yet")
+__device__ __forceinline__ uint32_t f2ord(float f) {
+    const uint32_t u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float ord2f(uint32_t u) {
+    if (u == 0) return -INFINITY;
+    return __uint_as_float((u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u);
+}
+
+struct I8ScanParams {
+    int64_t n;
+    int nkb;  // K blocks (dp128 / 128)
+    int nsplit, tiles_per_split, ntiles, qtiles;
+    int k;
+    const float *xs;      // [rows] s_r
+    const float *xe;      // [rows] dx_r
+    const float4 *xt;     // [tiles] {max dx_r over the tile, ...}
+    const float4 *qmeta;  // [nq_pad] {t_q, A_q, C_q, -}
+    const int64_t *row_limit;
+    int64_t nq;
+    uint32_t *lg;     // [nq] published lower bounds on e_k (f2ord, rounded down)
+    int32_t *acount;  // [nq] appended rows
+    uint2 *abuf;      // [nq][cap] {row, u bits}
+    int cap;
+    float thr_floor;  // measurement only: a floor under every bound (-inf normally)
+    // pilot mode: scan store tiles idx * tile_stride only, keep the per-thread top-k of
+    // l (no appends) and write it to pcand[(q * nsplit + split) * TC_KP + i]
+    int tile_stride;
+    uint64_t *pcand;
+};
+
+// loose per-tile test in the scaled domain: a row can pass u = t s acc + A dx + C >= thr
+// only if s * acc >= (thr - C - A dxmax) / t.  1e-6 (score units) absorbs every fp32
+// rounding of either side.
+__device__ __forceinline__ float loose_threshold(float thr, float t, float A, float C, float dxmax) {
+    if (thr == -INFINITY || t <= 0.f) return -INFINITY;
+    const float lhs = __fsub_rn(__fsub_rn(thr, __fmaf_ru(A, dxmax, C)), 1e-6f);
+    return __fdiv_rd(lhs, t);
+}
+
+// pilot: l = ap - A dx - C > thr needs ap > thr + C
+__device__ __forceinline__ float loose_pilot(float thr, float t, float C) {
+    if (thr == -INFINITY || t <= 0.f) return -INFINITY;
+    return __fdiv_rd(__fsub_rn(__fadd_rn(thr, C), 1e-6f), t);
+}
+
+// index of the n-th (0-based) set bit of m
+__device__ __forceinline__ int nth_set_bit(uint32_t m, int n) {
+    for (int i = 0; i < n; ++i) m &= m - 1;
+    return __ffs(m) - 1;
+}
+
+template <bool PILOT>
+__global__ void __launch_bounds__(I8_THREADS, 1)
+    tc8_scan_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tx, I8ScanParams p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // 1024-B alignment for SWIZZLE_128B, as an offset from the __shared__ array so
+    // every derived pointer stays in the shared window (LDS/STS, not generic LD/ST)
+    uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint8_t *sA = smem;
+    uint8_t *sB = sA + I8_STAGES * I8_A_BYTES;
+    uint8_t *smeta = sB + I8_STAGES * I8_B_BYTES;  // [2][I8_META_BYTES]
+    int32_t *spill = reinterpret_cast<int32_t *>(smeta + 2 * I8_META_BYTES);  // [32][128]
+    uint64_t *full = reinterpret_cast<uint64_t *>(spill + 32 * I8_EPI);
+    uint64_t *empty = full + I8_STAGES;
+    uint64_t *tfull = empty + I8_STAGES;
+    uint64_t *tempty = tfull + 2;
+    uint64_t *mfull = tempty + 2;
+    uint64_t *mempty = mfull + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(mempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nitems = p.qtiles * p.nsplit;
+    auto item_of = [&](int item, int &qtile, int &split, int &t0, int &nloc) {
+        qtile = item % p.qtiles;
+        split = item / p.qtiles;
+        t0 = split * p.tiles_per_split;
+        nloc = max(0, min(p.ntiles, t0 + p.tiles_per_split) - t0);
+    };
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tq);
+        tma_prefetch_desc(&tx);
+        for (int s = 0; s < I8_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], I8_EPI / 32);
+            mbar_init(&mfull[a], 1);
+            mbar_init(&mempty[a], I8_EPI / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(I8_TMEM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------- TMA producer: row meta per tile + operand K-slices ----------------
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            int tix = 0;
+            for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+                int qtile, split, t0, nloc;
+                item_of(item, qtile, split, t0, nloc);
+                for (int i = 0; i < nloc; ++i, ++tix) {
+                    const int t = (t0 + i) * p.tile_stride;
+                    const int acc = tix & 1;
+                    const uint32_t aphase = (tix >> 1) & 1;
+                    uint8_t *m = smeta + acc * I8_META_BYTES;
+                    mbar_wait(&mempty[acc], aphase ^ 1);
+                    mbar_expect_tx(&mfull[acc], I8_META_BYTES);
+                    bulk_load_1d(m, p.xs + (int64_t)t * TC_BLOCK_N, TC_BLOCK_N * 4, &mfull[acc]);
+                    bulk_load_1d(m + TC_BLOCK_N * 4, p.xe + (int64_t)t * TC_BLOCK_N, TC_BLOCK_N * 4, &mfull[acc]);
+                    bulk_load_1d(m + TC_BLOCK_N * 8, p.xt + t, 16, &mfull[acc]);
+                    for (int kb = 0; kb < p.nkb; ++kb) {
+                        mbar_wait(&empty[stage], phase ^ 1);
+                        mbar_expect_tx(&full[stage], I8_A_BYTES + I8_B_BYTES);
+                        tma_load_2d(sA + stage * I8_A_BYTES, &tq, &full[stage], kb * I8_BLOCK_K, qtile * TC_BLOCK_M);
+                        tma_load_2d(sB + stage * I8_B_BYTES, &tx, &full[stage], kb * I8_BLOCK_K, t * TC_BLOCK_N);
+                        if (++stage == I8_STAGES) { stage = 0; phase ^= 1; }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer (single thread) ----------------
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            int tix = 0;
+            for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+                int qtile, split, t0, nloc;
+                item_of(item, qtile, split, t0, nloc);
+                for (int i = 0; i < nloc; ++i, ++tix) {
+                    const int acc = tix & 1;
+                    const uint32_t aphase = (tix >> 1) & 1;
+                    mbar_wait(&tempty[acc], aphase ^ 1);
+                    tc_fence_after();
+                    const uint32_t d_tmem = tmem + acc * TC_BLOCK_N;
+                    for (int kb = 0; kb < p.nkb; ++kb) {
+                        mbar_wait(&full[stage], phase);
+                        tc_fence_after();
+                        const uint64_t ad = sw128_desc(smem_u32(sA + stage * I8_A_BYTES));
+                        const uint64_t bd = sw128_desc(smem_u32(sB + stage * I8_B_BYTES));
+#pragma unroll
+                        for (int k = 0; k < I8_BLOCK_K / 32; ++k)  // K = 32 int8 = 32 B per MMA inside the atom
+                            mma_i8(d_tmem, ad + 2 * k, bd + 2 * k, (kb | k) != 0);
+                        mma_commit(&empty[stage]);
+                        if (++stage == I8_STAGES) { stage = 0; phase ^= 1; }
+                    }
+                    mma_commit(&tfull[acc]);
+                }
+            }
+        }
+    } else if (warp >= 4) {
+        // ---------------- epilogue: TMEM -> bounds -> append + running top-k of l ----------------
+        const int et = threadIdx.x - 128;  // TMEM lane == query within the tile
+        const int ew = warp - 4;
+        int32_t *wspill = spill + ew * 32;  // this warp's columns of the [32][128] spill
+        int tix = 0;
+        for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+            int qtile, split, t0, nloc;
+            item_of(item, qtile, split, t0, nloc);
+            const int64_t q = (int64_t)qtile * TC_BLOCK_M + et;
+            const bool valid = q < p.nq;
+            float tq_ = 0.f, A = 0.f, C = 0.f;
+            int64_t lim = 0;
+            if (valid) {
+                const float4 qm = p.qmeta[q];
+                tq_ = qm.x;
+                A = qm.y;
+                C = qm.z;
+                lim = p.row_limit ? min(p.n, p.row_limit[q]) : p.n;
+            }
+            volatile uint32_t *lgq = p.lg + (valid ? q : 0);
+            // running top-k of l: the first TC_KP - k slots hold +inf sentinels that no
+            // insert displaces, so ts[TC_KP - 1] is always the k-th largest l seen
+            float ts[TC_KP];
+            uint32_t tr[TC_KP];
+#pragma unroll
+            for (int i = 0; i < TC_KP; ++i) {
+                ts[i] = (i < TC_KP - p.k) ? INFINITY : -INFINITY;
+                tr[i] = 0xFFFFFFFFu;
+            }
+            float Lpub = -INFINITY;
+            for (int i = 0; i < nloc; ++i, ++tix) {
+                const int acc = tix & 1;
+                const uint32_t aphase = (tix >> 1) & 1;
+                mbar_wait(&mfull[acc], aphase);
+                mbar_wait(&tfull[acc], aphase);
+                tc_fence_after();
+                const float *ss = reinterpret_cast<const float *>(smeta + acc * I8_META_BYTES);
+                const float *se = ss + TC_BLOCK_N;
+                const float dxmax = se[TC_BLOCK_N];
+                // main: append rows with u >= thr; pilot: insert rows with l > thr
+                float thr = fmaxf(ts[TC_KP - 1], p.thr_floor);
+                if (valid) thr = fmaxf(thr, ord2f(*lgq));
+                float thr2 = PILOT ? loose_pilot(thr, tq_, C) : loose_threshold(thr, tq_, A, C, dxmax);
+                const int64_t rbase = (int64_t)(t0 + i) * p.tile_stride * TC_BLOCK_N;
+                const uint32_t taddr = tmem + ((uint32_t)(ew * 32) << 16) + acc * TC_BLOCK_N;
+                uint32_t va[32], vb[32];
+                TMEM_LD32(taddr, va);
+                tmem_wait_ld();
+#pragma unroll 1
+                for (int cp = 0; cp < TC_BLOCK_N / 64; ++cp) {
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int c = 2 * cp + h;
+                        uint32_t(&v)[32] = h ? vb : va;
+                        // the next chunk streams in while this one is scored
+                        if (h == 0) {
+                            TMEM_LD32(taddr + (c + 1) * 32, vb);
+                        } else if (cp + 1 < TC_BLOCK_N / 64) {
+                            TMEM_LD32(taddr + (c + 1) * 32, va);
+                        }
+                        const float4 *s4 = reinterpret_cast<const float4 *>(ss + c * 32);
+                        // fast path: per 8-row group, max of s_r * acc (exact int -> fp32)
+                        float gm[4];
+#pragma unroll
+                        for (int g = 0; g < 4; ++g) {
+                            const float4 sa = s4[2 * g], sb = s4[2 * g + 1];
+                            float m0 = fmaxf(__fmul_rn(i2f_exact(v[8 * g + 0]), sa.x),
+                                             __fmul_rn(i2f_exact(v[8 * g + 1]), sa.y));
+                            float m1 = fmaxf(__fmul_rn(i2f_exact(v[8 * g + 2]), sa.z),
+                                             __fmul_rn(i2f_exact(v[8 * g + 3]), sa.w));
+                            m0 = fmaxf(m0, __fmul_rn(i2f_exact(v[8 * g + 4]), sb.x));
+                            m1 = fmaxf(m1, __fmul_rn(i2f_exact(v[8 * g + 5]), sb.y));
+                            m0 = fmaxf(m0, __fmul_rn(i2f_exact(v[8 * g + 6]), sb.z));
+                            m1 = fmaxf(m1, __fmul_rn(i2f_exact(v[8 * g + 7]), sb.w));
+                            gm[g] = fmaxf(m0, m1);
+                        }
+                        const int64_t rb = rbase + c * 32;
+                        uint32_t gmask = 0;
+#pragma unroll
+                        for (int g = 0; g < 4; ++g) gmask |= (gm[g] >= thr2 ? 1u : 0u) << g;
+                        if (rb >= lim) gmask = 0;
+                        // rare: the warp evaluates every flagged (query, 8-row group) pair
+                        // cooperatively, 4 pairs (32 rows) per pass, one row per lane
+                        if (__any_sync(0xffffffffu, gmask != 0)) {
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) wspill[j * I8_EPI + lane] = (int32_t)v[j];
+                            const uint32_t b0 = __ballot_sync(0xffffffffu, gmask & 1u);
+                            const uint32_t b1 = __ballot_sync(0xffffffffu, gmask & 2u);
+                            const uint32_t b2 = __ballot_sync(0xffffffffu, gmask & 4u);
+                            const uint32_t b3 = __ballot_sync(0xffffffffu, gmask & 8u);
+                            const int p1 = __popc(b0), p2 = p1 + __popc(b1), p3 = p2 + __popc(b2);
+                            const int npairs = p3 + __popc(b3);
+                            __syncwarp();
+                            const float kth = ts[TC_KP - 1];
+#pragma unroll 1
+                            for (int base = 0; base < npairs; base += 4) {
+                                const int pi = base + (lane >> 3);
+                                bool act = pi < npairs;
+                                const int g = (pi >= p3) ? 3 : (pi >= p2) ? 2 : (pi >= p1) ? 1 : 0;
+                                const uint32_t bg = (g == 3) ? b3 : (g == 2) ? b2 : (g == 1) ? b1 : b0;
+                                const int pg = (g == 3) ? p3 : (g == 2) ? p2 : (g == 1) ? p1 : 0;
+                                const int owner = act ? nth_set_bit(bg, pi - pg) : 0;
+                                const float o_t = __shfl_sync(0xffffffffu, tq_, owner);
+                                const float o_A = __shfl_sync(0xffffffffu, A, owner);
+                                const float o_C = __shfl_sync(0xffffffffu, C, owner);
+                                const float o_thr = __shfl_sync(0xffffffffu, thr, owner);
+                                const float o_kth = __shfl_sync(0xffffffffu, kth, owner);
+                                const int64_t o_lim = __shfl_sync(0xffffffffu, lim, owner);
+                                const int j = 8 * g + (lane & 7);
+                                const uint32_t row = (uint32_t)(rb + j);
+                                act = act && (int64_t)row < o_lim;
+                                float l = -INFINITY;
+                                if (act) {
+                                    const float dx = se[c * 32 + j];
+                                    const float ap =
+                                        __fmul_rn(__fmul_rn(i2f_exact(wspill[j * I8_EPI + owner]), ss[c * 32 + j]), o_t);
+                                    l = __fsub_rn(ap, __fmaf_rn(o_A, dx, o_C));
+                                    if (!PILOT) {
+                                        const float u = __fadd_rn(__fmaf_rn(o_A, dx, ap), o_C);
+                                        if (u >= o_thr) {
+                                            const int64_t oq = (int64_t)qtile * TC_BLOCK_M + ew * 32 + owner;
+                                            const int o = atomicAdd(&p.acount[oq], 1);
+                                            if (o < p.cap) p.abuf[oq * (int64_t)p.cap + o] = make_uint2(row, __float_as_uint(u));
+                                        }
+                                    }
+                                }
+                                // list inserts happen in the owner lane (rare)
+                                uint32_t wb = __ballot_sync(0xffffffffu, act && l > o_kth);
+                                while (wb) {
+                                    const int src = __ffs(wb) - 1;
+                                    wb &= wb - 1;
+                                    const float lv = __shfl_sync(0xffffffffu, l, src);
+                                    const uint32_t rv = __shfl_sync(0xffffffffu, row, src);
+                                    const int ow = __shfl_sync(0xffffffffu, owner, src);
+                                    if (lane == ow && lv > ts[TC_KP - 1]) {
+                                        topk_insert(ts, tr, lv, rv);
+                                        if (ts[TC_KP - 1] > thr) {
+                                            thr = ts[TC_KP - 1];
+                                            thr2 = PILOT ? loose_pilot(thr, tq_, C) : loose_threshold(thr, tq_, A, C, dxmax);
+                                        }
+                                    }
+                                }
+                            }
+                            __syncwarp();
+                        }
+                        if (h == 0 || cp + 1 < TC_BLOCK_N / 64) tmem_wait_ld();
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(&tempty[acc]);
+                    mbar_arrive(&mempty[acc]);
+                }
+                if (valid && ts[TC_KP - 1] > Lpub) {
+                    Lpub = ts[TC_KP - 1];
+                    atomicMax(const_cast<uint32_t *>(lgq), f2ord(Lpub));
+                }
+            }
+            if (PILOT && valid) {
+                uint64_t *out = p.pcand + (q * p.nsplit + split) * TC_KP;
+#pragma unroll
+                for (int s = 0; s < TC_KP; ++s)
+                    out[s] = (tr[s] == 0xFFFFFFFFu) ? 0ull : cand_key(ts[s], tr[s]);
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(I8_TMEM_COLS) : "memory");
+    }
+}
+
+// ---------------------------------------------------------------------------
+// per-row / per-query quantisation, one warp per vector.
+//   out8[dp128] = rint(v / s) (zero padded), s = max(max|v| / 127, ||v|| / (KMAX - sqrt(d)/2))
+//   so |out8| <= 127 and ||out8||_2 <= ||v|| / s + sqrt(d)/2 <= KMAX.
+//   err = ||v - s*out8||_2, nrm = ||v||_2, rec = ||s*out8||_2 — fp64 sums of squares
+__device__ __forceinline__ void quantize_vec_warp(const float *__restrict__ v, int d, int dp128, int8_t *__restrict__ out8,
+                                                  float *s_out, double *err2, double *nrm2, double *rec2) {
+    const int lane = threadIdx.x & 31;
+    float mx = 0.f;
+    double n2 = 0.0;
+    for (int j = lane; j < d; j += 32) {
+        mx = fmaxf(mx, fabsf(v[j]));
+        n2 = fma((double)v[j], (double)v[j], n2);
+    }
+    for (int o = 16; o; o >>= 1) {
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+    }
+    float s = 0.f;
+    if (mx > 0.f) {
+        const double nrm = sqrt(n2) * (1.0 + 1e-12);
+        s = __double2float_ru(fmax((double)mx / 127.0, nrm / (I8_KMAX - 0.5 * sqrt((double)d))));
+    }
+    double e2 = 0.0, r2 = 0.0;
+    for (int j = lane; j < dp128; j += 32) {
+        int qv = 0;
+        if (j < d && s > 0.f) {
+            const float x = v[j];
+            qv = (int)rintf(x / s);
+            qv = max(-127, min(127, qv));
+            const double rec = (double)s * (double)qv;  // exact: 24-bit x 8-bit product
+            const double dx = (double)x - rec;          // exact in fp64 (significands of 24 and 32 bits)
+            e2 = fma(dx, dx, e2);
+            r2 = fma(rec, rec, r2);
+        }
+        out8[j] = (int8_t)qv;
+    }
+    for (int o = 16; o; o >>= 1) {
+        e2 += __shfl_xor_sync(0xffffffffu, e2, o);
+        r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+    }
+    *s_out = s;
+    *err2 = e2;
+    *nrm2 = n2;
+    *rec2 = r2;
+}
+
+// sqrt of an fp64 sum of d squares, bounded above
+__device__ __forceinline__ double norm_up(double sumsq) { return sqrt(sumsq) * (1.0 + 1e-12) + 1e-30; }
+
+__global__ void quantize_rows_kernel(const float *__restrict__ src, int64_t n, int d, const int64_t *__restrict__ rows,
+                                     int64_t row0, int dp128, int8_t *__restrict__ x8, float *__restrict__ xs,
+                                     float *__restrict__ xe, float4 *__restrict__ xt, uint32_t *__restrict__ maxnorm) {
+    const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32;
+    if (w >= n) return;
+    const int64_t r = rows ? rows[w] : row0 + w;
+    float s;
+    double e2, n2, r2;
+    quantize_vec_warp(src + w * (int64_t)d, d, dp128, x8 + r * (int64_t)dp128, &s, &e2, &n2, &r2);
+    if ((threadIdx.x & 31) == 0) {
+        const float dx = __double2float_ru(norm_up(e2));
+        xs[r] = s;
+        xe[r] = dx;
+        // positive floats order as uints; both maxima only grow (stay valid bounds)
+        atomicMax(reinterpret_cast<uint32_t *>(&xt[r / TC_BLOCK_N].x), __float_as_uint(dx));
+        atomicMax(maxnorm, __float_as_uint(__double2float_ru(norm_up(n2))));
+    }
+}
+
+__global__ void gather_i8_kernel(const int8_t *__restrict__ sx8, const float *__restrict__ sxs,
+                                 const float *__restrict__ sxe, const uint32_t *__restrict__ smaxnorm,
+                                 const int64_t *__restrict__ src_rows, int64_t n, int dp128, int64_t row0,
+                                 int8_t *__restrict__ x8, float *__restrict__ xs, float *__restrict__ xe,
+                                 float4 *__restrict__ xt, uint32_t *__restrict__ maxnorm) {
+    // the gathered rows' norms are bounded by the source's maximum
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicMax(maxnorm, *smaxnorm);
+    const int64_t total = n * (int64_t)(dp128 / 16);
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t / (dp128 / 16);
+        const int j = (int)(t - i * (dp128 / 16));
+        const int64_t s = src_rows[i];
+        reinterpret_cast<int4 *>(x8 + (row0 + i) * dp128)[j] = reinterpret_cast<const int4 *>(sx8 + s * dp128)[j];
+        if (j == 0) {
+            const int64_t r = row0 + i;
+            xs[r] = sxs[s];
+            xe[r] = sxe[s];
+            atomicMax(reinterpret_cast<uint32_t *>(&xt[r / TC_BLOCK_N].x), __float_as_uint(sxe[s]));
+        }
+    }
+}
+
+// queries: padded fp32 [nq, dp8] -> int8 [nq_pad, dp128] + {t, A, C}
+__global__ void quantize_queries_kernel(const float *__restrict__ qp, int64_t nq, int64_t nq_pad, int dp8, int d,
+                                        int dp128, const uint32_t *__restrict__ maxnorm, int8_t *__restrict__ q8,
+                                        float4 *__restrict__ qmeta) {
+    const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32;
+    const int lane = threadIdx.x & 31;
+    if (w >= nq_pad) return;
+    if (w >= nq) {
+        for (int j = lane; j < dp128; j += 32) q8[w * dp128 + j] = 0;
+        if (lane == 0) qmeta[w] = make_float4(0.f, 0.f, 0.f, 0.f);
+        return;
+    }
+    float t;
+    double e2, n2, r2;
+    quantize_vec_warp(qp + w * (int64_t)dp8, d, dp128, q8 + w * dp128, &t, &e2, &n2, &r2);
+    if (lane == 0) {
+        const double nmax = (double)__uint_as_float(*maxnorm);
+        const double A = norm_up(r2), B = norm_up(e2);
+        // rounding slack: |fl(ap) - t s acc| <= 2 * 2^-24 * A * (nmax + dxmax) and a few
+        // fp32 roundings in u / l; 1e-6 * (1 + 2 A nmax) dominates both for any d <= 8192
+        const double C = B * nmax + 1e-6 * (1.0 + 2.0 * A * nmax);
+        qmeta[w] = make_float4(t, __double2float_ru(A), __double2float_ru(C), 0.f);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// exact rescoring, one WARP per query: seeds = the exact top-k over the scan's
+// per-split lists (k distinct rows, so their k-th score L <= e_k); stream the
+// appended rows with u >= L (L rising as better rows are scored) through an
+// exact running top-k.  A row with u < L has exact <= u < L <= e_k.
+constexpr int W8_WARPS = 8;
+constexpr int W8_BATCH = 16;  // rows scored per warp batch (2 lanes per row)
+
+// exact einsum-order partial of lane chain `ch` (0: elements 6,4,2,0 of each
+// block of 8, 1: 7,5,3,1 — einsum_dot_f32's two fp64 lanes); q in smem
+__device__ __forceinline__ double einsum_chain(const float *__restrict__ x, const float *__restrict__ q, int d, int ch) {
+    double a = 0.0;
+    int j = 0;
+#pragma unroll 8
+    for (; j + 8 <= d; j += 8) {
+        const float4 xa = __ldg(reinterpret_cast<const float4 *>(x + j));
+        const float4 xb = __ldg(reinterpret_cast<const float4 *>(x + j + 4));
+        const float4 qa = *reinterpret_cast<const float4 *>(q + j);
+        const float4 qb = *reinterpret_cast<const float4 *>(q + j + 4);
+        a = fma((double)(ch ? xb.w : xb.z), (double)(ch ? qb.w : qb.z), a);
+        a = fma((double)(ch ? xb.y : xb.x), (double)(ch ? qb.y : qb.x), a);
+        a = fma((double)(ch ? xa.w : xa.z), (double)(ch ? qa.w : qa.z), a);
+        a = fma((double)(ch ? xa.y : xa.x), (double)(ch ? qa.y : qa.x), a);
+    }
+    for (; j < d; j += 2) a = fma((double)x[j + ch], (double)q[j + ch], a);
+    return a;
+}
+
+// exact scores of rows[0..nb) (nb <= 16) by one warp: lane pair (2i, 2i+1) scores row i
+__device__ __forceinline__ void warp_score(const float *__restrict__ x32, int dp8, int d, const int32_t *rows, int nb,
+                                           const float *qs, double *out) {
+    const int lane = threadIdx.x & 31, r = lane >> 1, ch = lane & 1;
+    double a = 0.0;
+    if (r < nb) a = einsum_chain(x32 + (int64_t)rows[r] * dp8, qs, d, ch);
+    const double other = __shfl_xor_sync(0xffffffffu, a, 1);
+    if (ch == 0 && r < nb) out[r] = 0.0 + (a + other);
+    __syncwarp();
+}
+
+// lane 0: insert (sc, r) into the top list sorted by (score desc, row asc)
+__device__ __forceinline__ void top_insert(double *ts, int32_t *tr, int &n, int take, double sc, int32_t r) {
+    if (n == take && !ranks_before(sc, r, ts[take - 1], tr[take - 1])) return;
+    int pos = (n < take) ? n++ : take - 1;
+    while (pos > 0 && ranks_before(sc, r, ts[pos - 1], tr[pos - 1])) {
+        ts[pos] = ts[pos - 1];
+        tr[pos] = tr[pos - 1];
+        --pos;
+    }
+    ts[pos] = sc;
+    tr[pos] = r;
+}
+
+struct I8SeedArgs {
+    const uint64_t *pcand;  // [nq][nsplit][TC_KP] pilot keys (l, row), 0 = empty
+    int nsplit;
+    int64_t nq;
+    int k;
+    const float *x32;
+    int dp8, d;
+    const float *qp;
+    int32_t *seed_rows;  // [nq][TC_KP]
+    double *seed_s;      // [nq][TC_KP]
+    int32_t *seed_n;     // [nq]
+    uint32_t *lg;        // [nq] <- max(lg, rounded-down exact k-th seed score)
+};
+
+// per query (one warp): the k pilot rows with the largest l, scored exactly
+__global__ void __launch_bounds__(W8_WARPS * 32) tc8_seed_kernel(I8SeedArgs a) {
+    extern __shared__ __align__(16) float qdyn[];  // [W8_WARPS][dp8 + 8]
+    __shared__ int32_t rows_sh[W8_WARPS][TC_KP];
+    __shared__ double ex_sh[W8_WARPS][TC_KP];
+    __shared__ double ts_sh[W8_WARPS][TC_KP];
+    __shared__ int32_t tr_sh[W8_WARPS][TC_KP];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t wid = (int64_t)blockIdx.x * W8_WARPS + w;
+    const int64_t nw = (int64_t)gridDim.x * W8_WARPS;
+    const int M = a.nsplit * TC_KP;
+    float *qs = qdyn + w * (a.dp8 + 8);
+    for (int64_t q = wid; q < a.nq; q += nw) {
+        const uint64_t *cq = a.pcand + q * (int64_t)M;
+        uint64_t last = ~0ull;
+        int n = 0;
+        for (int j = 0; j < a.k; ++j) {
+            uint64_t best = 0;
+            for (int e = lane; e < M; e += 32) {
+                const uint64_t key = cq[e];
+                if (key < last && key > best) best = key;
+            }
+            for (int o = 16; o; o >>= 1) {
+                const uint64_t ob = __shfl_xor_sync(0xffffffffu, best, o);
+                best = ob > best ? ob : best;
+            }
+            if (best == 0) break;
+            if (lane == 0) rows_sh[w][n] = (int32_t)key_row(best);
+            ++n;
+            last = best;
+        }
+        const float *qv = a.qp + q * (int64_t)a.dp8;
+        for (int j = lane; j < a.dp8; j += 32) qs[j] = qv[j];
+        __syncwarp();
+        warp_score(a.x32, a.dp8, a.d, rows_sh[w], n, qs, ex_sh[w]);
+        if (lane == 0) {
+            int m = 0;
+            for (int j = 0; j < n; ++j) top_insert(ts_sh[w], tr_sh[w], m, a.k, ex_sh[w][j], rows_sh[w][j]);
+            for (int j = 0; j < m; ++j) {
+                a.seed_rows[q * TC_KP + j] = tr_sh[w][j];
+                a.seed_s[q * TC_KP + j] = ts_sh[w][j];
+            }
+            a.seed_n[q] = m;
+            // k distinct rows score >= ts[k-1] exactly: a lower bound on the true k-th score
+            if (m == a.k) atomicMax(&a.lg[q], f2ord(__double2float_rd(ts_sh[w][a.k - 1])));
+        }
+        __syncwarp();
+    }
+}
+
+struct I8PostArgs {
+    const int32_t *acount;
+    const uint2 *abuf;
+    int cap;
+    int64_t nq;
+    int k;
+    int64_t take;
+    const int64_t *row_limit;
+    const float *x32;
+    int dp8, d;
+    const float *qp;
+    const int32_t *seed_rows;  // [nq][TC_KP] exact seeds from the pilot (nullable)
+    const double *seed_s;
+    const int32_t *seed_n;
+    int64_t *rows;
+    double *raw, *rep;
+    int32_t *count;
+    int32_t *counters;  // [0] fallback, [1] rescored rows, [3] appended rows
+    int32_t *fallback;
+};
+
+__global__ void __launch_bounds__(W8_WARPS * 32) tc8_post_kernel(I8PostArgs a) {
+    extern __shared__ __align__(16) float qdyn[];  // [W8_WARPS][dp8 + 8]
+    __shared__ double top_s[W8_WARPS][TC_KP];
+    __shared__ int32_t top_r[W8_WARPS][TC_KP];
+    __shared__ int32_t cand[W8_WARPS][64];
+    __shared__ double bex[W8_WARPS][W8_BATCH];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t wid = (int64_t)blockIdx.x * W8_WARPS + w;
+    const int64_t nw = (int64_t)gridDim.x * W8_WARPS;
+    double *ts = top_s[w];
+    int32_t *tr = top_r[w];
+    float *qs = qdyn + w * (a.dp8 + 8);
+    for (int64_t q = wid; q < a.nq; q += nw) {
+        const int take = (int)(a.row_limit ? min(a.take, max((int64_t)0, a.row_limit[q])) : a.take);
+        const int cnt = a.acount[q];
+        if (lane == 0) atomicAdd(&a.counters[3], cnt);
+        if (take > 0 && cnt > a.cap) {
+            if (lane == 0) a.fallback[atomicAdd(&a.counters[0], 1)] = (int32_t)q;
+            continue;
+        }
+        const float *qv = a.qp + q * (int64_t)a.dp8;
+        int n = 0;  // entries in the top list (lane-uniform)
+        int scored = 0;
+        if (take > 0) {
+            for (int j = lane; j < a.dp8; j += 32) qs[j] = qv[j];
+            // seeds: the pilot's exact top-k ...
+            if (a.seed_n) {
+                n = min(a.seed_n[q], take);
+                if (lane < n) {
+                    ts[lane] = a.seed_s[q * TC_KP + lane];
+                    tr[lane] = a.seed_rows[q * TC_KP + lane];
+                }
+            }
+            __syncwarp();
+            const uint2 *e = a.abuf + q * (int64_t)a.cap;
+            {
+                // ... and the take appended rows with the largest (u, row) keys, scored exactly
+                uint64_t lastk = ~0ull;
+                int nb = 0;
+                for (int j = 0; j < take; ++j) {
+                    uint64_t best = 0;
+                    for (int i = lane; i < cnt; i += 32) {
+                        const uint2 v = e[i];
+                        const uint64_t key = cand_key(__uint_as_float(v.y), v.x);
+                        if (key < lastk && key > best) best = key;
+                    }
+                    for (int o = 16; o; o >>= 1) {
+                        const uint64_t ob = __shfl_xor_sync(0xffffffffu, best, o);
+                        best = ob > best ? ob : best;
+                    }
+                    if (best == 0) break;
+                    lastk = best;
+                    const int32_t row = (int32_t)key_row(best);
+                    bool dup = false;
+                    for (int t = 0; t < n; ++t) dup |= (tr[t] == row);
+                    if (!dup) {
+                        if (lane == 0) cand[w][nb] = row;
+                        ++nb;
+                    }
+                }
+                __syncwarp();
+                if (nb > 0) {
+                    warp_score(a.x32, a.dp8, a.d, cand[w], nb, qs, bex[w]);
+                    if (lane == 0)
+                        for (int j = 0; j < nb; ++j) top_insert(ts, tr, n, take, bex[w][j], cand[w][j]);
+                    scored += nb;
+                    n = __shfl_sync(0xffffffffu, n, 0);
+                    __syncwarp();
+                }
+            }
+            float L = (n == take) ? __double2float_rd(ts[take - 1]) : -INFINITY;
+            int pend = 0;  // rows waiting in cand[w][0..pend)
+            for (int base = 0; base < cnt || pend > 0; base += 32) {
+                if (base < cnt) {
+                    const int i = base + lane;
+                    bool pass = false;
+                    int32_t row = -1;
+                    if (i < cnt) {
+                        const uint2 v = e[i];
+                        row = (int32_t)v.x;
+                        pass = __uint_as_float(v.y) >= L;
+                        for (int j = 0; j < n && pass; ++j) pass = (tr[j] != row);
+                    }
+                    const unsigned m = __ballot_sync(0xffffffffu, pass);
+                    if (pass) cand[w][pend + __popc(m & ((1u << lane) - 1))] = row;
+                    pend += __popc(m);
+                    __syncwarp();
+                }
+                const bool last = base + 32 >= cnt;
+                while (pend >= W8_BATCH || (last && pend > 0)) {
+                    const int nb = min(pend, W8_BATCH);
+                    warp_score(a.x32, a.dp8, a.d, cand[w], nb, qs, bex[w]);
+                    if (lane == 0) {
+                        for (int j = 0; j < nb; ++j) top_insert(ts, tr, n, take, bex[w][j], cand[w][j]);
+                    }
+                    scored += nb;
+                    n = __shfl_sync(0xffffffffu, n, 0);
+                    // shift the remaining pending rows down
+                    const int32_t mv = (lane + nb < pend) ? cand[w][lane + nb] : 0;
+                    const int32_t mv2 = (lane + 32 + nb < pend) ? cand[w][lane + 32 + nb] : 0;
+                    __syncwarp();
+                    if (lane + nb < pend) cand[w][lane] = mv;
+                    if (lane + 32 + nb < pend) cand[w][lane + 32] = mv2;
+                    pend -= nb;
+                    __syncwarp();
+                    if (n == take) L = __double2float_rd(ts[take - 1]);
+                }
+                if (base >= cnt) break;
+            }
+            if (lane == 0) atomicAdd(&a.counters[1], scored);
+        }
+        // outputs: self-snap (element-wise equal stored row, index.py:180-181) + clamp (:185)
+        for (int j = 0; j < a.k; ++j) {
+            const int64_t o = q * a.k + j;
+            if (j >= n) {
+                if (lane == 0) {
+                    a.rows[o] = -1;
+                    if (a.raw) a.raw[o] = 0.0;
+                    if (a.rep) a.rep[o] = 0.0;
+                }
+                continue;
+            }
+            const double bs = ts[j];
+            const int64_t br = tr[j];
+            double rep = bs;
+            if (bs > 1.0 - 1e-6) {
+                const float *x = a.x32 + br * (int64_t)a.dp8;
+                int bad = 0;
+                for (int t = lane; t < a.d; t += 32) bad |= !(x[t] == qv[t]);
+                if (!__any_sync(0xffffffffu, bad)) rep = 1.0;
+            }
+            if (lane == 0) {
+                a.rows[o] = br;
+                if (a.raw) a.raw[o] = bs;
+                if (a.rep) a.rep[o] = fmax(-1.0, fmin(1.0, rep));
+            }
+        }
+        if (lane == 0) a.count[q] = n;
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+int i8_quantize_rows(const float *src, int64_t n, int d, const int64_t *rows, int64_t row0, int dp128, I8Rows &m,
+                     cudaStream_t st) {
+    if (n == 0) return PR_OK;
+    const int64_t threads = n * 32;
+    ::pr::count_launch();
+    quantize_rows_kernel<<<(unsigned)ceil_div<int64_t>(threads, 256), 256, 0, st>>>(src, n, d, rows, row0, dp128, m.x8,
+                                                                                   m.xs, m.xe, m.xt, m.maxnorm);
+    PR_LAUNCH_CHECK();
+    return PR_OK;
+}
+
+int i8_gather_rows(const I8Rows &src, const int64_t *src_rows, int64_t n, int dp128, int64_t row0, I8Rows &m,
+                   cudaStream_t st) {
+    if (n == 0) return PR_OK;
+    const int64_t total = n * (dp128 / 16);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div<int64_t>(total, 256), (int64_t)sm_count() * 16));
+    ::pr::count_launch();
+    gather_i8_kernel<<<grid, 256, 0, st>>>(src.x8, src.xs, src.xe, src.maxnorm, src_rows, n, dp128, row0, m.x8, m.xs,
+                                           m.xe, m.xt, m.maxnorm);
+    PR_LAUNCH_CHECK();
+    return PR_OK;
+}
+
+int i8_make_store_map(TcStoreMap *m, const int8_t *x8, int64_t rows, int dp128) {
+    return make_map_2d(&m->map, x8, rows, dp128, 1, I8_BLOCK_K, TC_BLOCK_N);
+}
+
+static int i8_cap(int64_t n, int64_t nq) {
+    int64_t cap = std::min<int64_t>(I8_CAP, (int64_t)(I8_BUF_BYTES / 8 / (size_t)std::max<int64_t>(nq, 1)));
+    cap = std::max<int64_t>(cap, 2048);
+    return (int)std::min<int64_t>(cap, round_up<int64_t>(std::max<int64_t>(n, 1), 256));
+}
+
+// pilot: every I8_PILOT_STRIDE-th 256-row tile (~3% of the scan) when the store has
+// at least I8_PILOT_MIN_TILES tiles
+constexpr int I8_PILOT_STRIDE = 32;
+constexpr int64_t I8_PILOT_MIN_TILES = 8 * I8_PILOT_STRIDE;
+
+static int pilot_splits(int64_t qtiles, int64_t ntiles) {
+    if (ntiles < I8_PILOT_MIN_TILES) return 0;
+    return choose_nsplit_waves(qtiles, ceil_div<int64_t>(ntiles, I8_PILOT_STRIDE));
+}
+
+bool tc8_eligible(int d) { return d <= 2048; }
+
+size_t tc8_scratch_bytes(int64_t nq, int dp128, int64_t n) {
+    const int64_t nq_pad = round_up<int64_t>(nq, TC_BLOCK_M);
+    const int64_t qtiles = nq_pad / TC_BLOCK_M, ntiles = ceil_div<int64_t>(n, TC_BLOCK_N);
+    const int ps = pilot_splits(qtiles, ntiles);
+    return (size_t)nq_pad * dp128 + (size_t)nq_pad * 16 + (size_t)nq * (4 + 4 + 4 + 4) +
+           (size_t)nq * i8_cap(n, nq) * 8 + (size_t)nq * ps * TC_KP * 8 + (size_t)nq * TC_KP * 12 + 65536;
+}
+
+int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats) {
+    const int64_t nq_pad = round_up<int64_t>(s.nq, TC_BLOCK_M);
+    const int64_t qtiles = nq_pad / TC_BLOCK_M;
+    const int64_t ntiles = ceil_div<int64_t>(s.n, TC_BLOCK_N);
+    const int nsplit = choose_nsplit_waves(qtiles, ntiles);
+    const int tps = (int)ceil_div<int64_t>(ntiles, nsplit);
+    const int cap = i8_cap(s.n, s.nq);
+    int8_t *q8 = cv.take<int8_t>((size_t)nq_pad * s.dp128);
+    float4 *qmeta = cv.take<float4>((size_t)nq_pad);
+    uint32_t *lg = cv.take<uint32_t>((size_t)s.nq);
+    int32_t *acount = cv.take<int32_t>((size_t)s.nq);
+    uint2 *abuf = cv.take<uint2>((size_t)s.nq * cap);
+    s.fallback_list = cv.take<int32_t>((size_t)s.nq);
+    PR_CUDA(cudaMemsetAsync(lg, 0, (size_t)s.nq * 4, st));
+    PR_CUDA(cudaMemsetAsync(acount, 0, (size_t)s.nq * 4, st));
+    PR_CUDA(cudaMemsetAsync(s.counters, 0, 4 * sizeof(int32_t), st));
+    {
+        const int64_t threads = nq_pad * 32;
+        ::pr::count_launch();
+        quantize_queries_kernel<<<(unsigned)ceil_div<int64_t>(threads, 256), 256, 0, st>>>(
+            s.qp, s.nq, nq_pad, s.dp8, s.d, s.dp128, s.rows8.maxnorm, q8, qmeta);
+        PR_LAUNCH_CHECK();
+    }
+    TcStoreMap qmap;
+    int rc = make_map_2d(&qmap.map, q8, nq_pad, s.dp128, 1, I8_BLOCK_K, TC_BLOCK_M);
+    if (rc) return rc;
+    const size_t wsmem = (size_t)W8_WARPS * (s.dp8 + 8) * sizeof(float);
+    static bool attr = false;
+    if (!attr) {
+        PR_CUDA(cudaFuncSetAttribute(tc8_scan_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)i8_smem_bytes()));
+        PR_CUDA(cudaFuncSetAttribute(tc8_scan_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)i8_smem_bytes()));
+        PR_CUDA(cudaFuncSetAttribute(tc8_seed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024));
+        PR_CUDA(cudaFuncSetAttribute(tc8_post_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024));
+        attr = true;
+    }
+    const char *ceil_env = getenv("PR_I8_CEILING");  // 1: no row can pass (results invalid): fast-path timing
+    const float floor_thr = (ceil_env && ceil_env[0] == '1') ? INFINITY : -INFINITY;
+    const unsigned wgrid = (unsigned)std::max<int64_t>(
+        1, std::min<int64_t>(ceil_div<int64_t>(s.nq, W8_WARPS), (int64_t)sm_count() * 8));
+
+    // 1) pilot over a tile subsample -> exact seeds and a first bound per query
+    const int psplit = pilot_splits(qtiles, ntiles);
+    int32_t *seed_rows = nullptr, *seed_n = nullptr;
+    double *seed_s = nullptr;
+    if (psplit > 0) {
+        const int64_t ptiles = ceil_div<int64_t>(ntiles, I8_PILOT_STRIDE);
+        uint64_t *pcand = cv.take<uint64_t>((size_t)s.nq * psplit * TC_KP);
+        seed_rows = cv.take<int32_t>((size_t)s.nq * TC_KP);
+        seed_s = cv.take<double>((size_t)s.nq * TC_KP);
+        seed_n = cv.take<int32_t>((size_t)s.nq);
+        I8ScanParams pp{s.n, s.dp128 / I8_BLOCK_K, psplit, (int)ceil_div<int64_t>(ptiles, psplit), (int)ptiles,
+                        (int)qtiles, s.k, s.rows8.xs, s.rows8.xe, s.rows8.xt, qmeta, s.row_limit, s.nq, lg, acount,
+                        abuf, cap, floor_thr, I8_PILOT_STRIDE, pcand};
+        ::pr::count_launch();
+        tc8_scan_kernel<true><<<(unsigned)(qtiles * psplit), I8_THREADS, i8_smem_bytes(), st>>>(
+            qmap.map, s.store_map->map, pp);
+        PR_LAUNCH_CHECK();
+        I8SeedArgs sa{pcand, psplit, s.nq, s.k, s.x32, s.dp8, s.d, s.qp, seed_rows, seed_s, seed_n, lg};
+        ::pr::count_launch();
+        tc8_seed_kernel<<<wgrid, W8_WARPS * 32, wsmem, st>>>(sa);
+        PR_LAUNCH_CHECK();
+    }
+    // 2) main scan: append every row whose upper bound reaches the running bound
+    I8ScanParams p{s.n, s.dp128 / I8_BLOCK_K, nsplit, tps, (int)ntiles, (int)qtiles, s.k, s.rows8.xs, s.rows8.xe,
+                   s.rows8.xt, qmeta, s.row_limit, s.nq, lg, acount, abuf, cap, floor_thr, 1, nullptr};
+    ::pr::count_launch();
+    if (s.ev_begin) PR_CUDA(cudaEventRecord(s.ev_begin, st));
+    tc8_scan_kernel<false><<<(unsigned)(qtiles * nsplit), I8_THREADS, i8_smem_bytes(), st>>>(qmap.map,
+                                                                                           s.store_map->map, p);
+    PR_LAUNCH_CHECK();
+    if (s.ev_end) PR_CUDA(cudaEventRecord(s.ev_end, st));
+    // 3) exact rescoring of the complete candidate set
+    I8PostArgs pa{acount, abuf, cap, s.nq, s.k, std::min<int64_t>(s.k, s.n), s.row_limit, s.x32, s.dp8, s.d, s.qp,
+                  seed_rows, seed_s, seed_n, s.rows, s.raw, s.rep, s.count, s.counters, s.fallback_list};
+    ::pr::count_launch();
+    tc8_post_kernel<<<wgrid, W8_WARPS * 32, wsmem, st>>>(pa);
+    PR_LAUNCH_CHECK();
+    stats->nsplit = nsplit;
+    return PR_OK;
+}
+
+}  // namespace pr

@@ -35,6 +35,7 @@ _HEADER = struct.Struct("<8sIIQQI")  # magic, version, dim, count, payload_len, 
 MODE_AUTO = _lib.PR_SEARCH_AUTO
 MODE_EXACT = _lib.PR_SEARCH_EXACT
 MODE_TENSOR = _lib.PR_SEARCH_TENSOR
+MODE_TENSOR_I8 = _lib.PR_SEARCH_TENSOR_I8
 
 
 @dataclass(frozen=True)

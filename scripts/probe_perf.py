@@ -10,7 +10,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import torch  # noqa: E402
 
-from paper_2506_21593_b200 import MODE_EXACT, MODE_TENSOR, FlatIndex  # noqa: E402
+from paper_2506_21593_b200 import MODE_EXACT, MODE_TENSOR, MODE_TENSOR_I8, FlatIndex  # noqa: E402
 
 
 def make_store(n, d, seed=7, chunk=1 << 20):
@@ -63,11 +63,21 @@ def main():
         q = make_queries(idx, b, d)
         torch.cuda.synchronize()
         build_s = time.time() - t0
-        ms = timeit(lambda: idx.search_batch(q, k, mode=MODE_TENSOR, validate=False))
-        st = idx.stats()
         flop = 2.0 * n * d * b
-        print(f"TC  n={n} d={d} B={b} k={k}: {ms:.2f} ms  {b / ms * 1e3:.0f} q/s  {flop / ms / 1e9:.1f} TFLOP/s(e2e)"
-              f"  nsplit={st.nsplit} fallback={st.fallback} cand={st.candidates} build={build_s:.1f}s", flush=True)
+        ref = None
+        for name, mode in (("TC16", MODE_TENSOR), ("TC8", MODE_TENSOR_I8)):
+            idx.set_timing(True)
+            ms = timeit(lambda: idx.search_batch(q, k, mode=mode, validate=False))
+            kms, kn = idx.scan_time()
+            st = idx.stats()
+            res = idx.search_batch(q, k, mode=mode, validate=False)
+            rows = res.rows.cpu()
+            same = "" if ref is None else f" rows==TC16: {bool((rows == ref).all())}"
+            ref = rows if ref is None else ref
+            print(f"{name} n={n} d={d} B={b} k={k}: {ms:.2f} ms  {b / ms * 1e3:.0f} q/s  "
+                  f"{flop / ms / 1e9:.1f} TOP/s(e2e)  scan {kms / max(kn, 1):.2f} ms/launch "
+                  f"nsplit={st.nsplit} fallback={st.fallback} cand={st.candidates} appended={st.appended} "
+                  f"build={build_s:.1f}s{same}", flush=True)
         if a.exact:
             bq = min(b, 256)
             ms = timeit(lambda: idx.search_batch(q[:bq], k, mode=MODE_EXACT, validate=False), reps=1)
