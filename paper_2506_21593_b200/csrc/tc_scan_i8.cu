@@ -41,9 +41,14 @@
 namespace pr {
 
 constexpr int I8_BLOCK_K = 128;  // int8 columns per stage = one 128-B swizzle atom
-constexpr int I8_STAGES = 4;
-constexpr int I8_THREADS = 256;
-constexpr int I8_EPI = 128;
+// epilogue: I8_EPI_WARPS warps; with 8, two warps per SM sub-partition split each
+// tile's columns (latency hiding), which leaves room for 3 operand stages
+constexpr int I8_EPI_WARPS = 8;
+constexpr int I8_HALVES = I8_EPI_WARPS / 4;
+constexpr int I8_CPW = (TC_BLOCK_N / 32) / I8_HALVES;  // 32-column chunks per epilogue warp per tile
+constexpr int I8_STAGES = I8_EPI_WARPS == 8 ? 3 : 4;
+constexpr int I8_EPI = 32 * I8_EPI_WARPS;
+constexpr int I8_THREADS = 128 + I8_EPI;
 constexpr int I8_A_BYTES = TC_BLOCK_M * I8_BLOCK_K;  // 16 KB
 constexpr int I8_B_BYTES = TC_BLOCK_N * I8_BLOCK_K;  // 32 KB
 constexpr int I8_META_BYTES = TC_BLOCK_N * 4 * 2 + 16;  // s_r[256], dx_r[256], tile {dxmax, -, -, -}
@@ -106,7 +111,7 @@ struct I8ScanParams {
     int cap;
     float thr_floor;  // measurement only: a floor under every bound (-inf normally)
     // pilot mode: scan store tiles idx * tile_stride only, keep the per-thread top-k of
-    // l (no appends) and write it to pcand[(q * nsplit + split) * TC_KP + i]
+    // l (no appends) and write it to pcand[((q * nsplit + split) * I8_HALVES + half) * TC_KP + i]
     int tile_stride;
     uint64_t *pcand;
 };
@@ -124,6 +129,14 @@ __device__ __forceinline__ float loose_threshold(float thr, float t, float A, fl
 __device__ __forceinline__ float loose_pilot(float thr, float t, float C) {
     if (thr == -INFINITY || t <= 0.f) return -INFINITY;
     return __fdiv_rd(__fsub_rn(__fadd_rn(thr, C), 1e-6f), t);
+}
+
+// relaxed gpu-scope load: the value is only consumed a tile later, so its
+// latency overlaps a whole tile of epilogue work
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
 }
 
 // index of the n-th (0-based) set bit of m
@@ -247,9 +260,10 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
         }
     } else if (warp >= 4) {
         // ---------------- epilogue: TMEM -> bounds -> append + running top-k of l ----------------
-        const int et = threadIdx.x - 128;  // TMEM lane == query within the tile
-        const int ew = warp - 4;
-        int32_t *wspill = spill + ew * 32;  // this warp's columns of the [32][128] spill
+        const int ew = (warp - 4) & 3;                // TMEM lane group
+        const int half = (warp - 4) >> 2;             // column slice of the tile
+        const int et = ew * 32 + lane;                // TMEM lane == query within the tile
+        int32_t *wspill = spill + (warp - 4) * 32;  // this warp's columns of the [32][I8_EPI] spill
         int tix = 0;
         for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
             int qtile, split, t0, nloc;
@@ -265,7 +279,8 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
                 C = qm.z;
                 lim = p.row_limit ? min(p.n, p.row_limit[q]) : p.n;
             }
-            volatile uint32_t *lgq = p.lg + (valid ? q : 0);
+            uint32_t *lgq = p.lg + (valid ? q : 0);
+            uint32_t lg_next = valid ? ld_relaxed(lgq) : 0u;
             // running top-k of l: the first TC_KP - k slots hold +inf sentinels that no
             // insert displaces, so ts[TC_KP - 1] is always the k-th largest l seen
             float ts[TC_KP];
@@ -286,24 +301,24 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
                 const float *se = ss + TC_BLOCK_N;
                 const float dxmax = se[TC_BLOCK_N];
                 // main: append rows with u >= thr; pilot: insert rows with l > thr
-                float thr = fmaxf(ts[TC_KP - 1], p.thr_floor);
-                if (valid) thr = fmaxf(thr, ord2f(*lgq));
+                float thr = fmaxf(fmaxf(ts[TC_KP - 1], p.thr_floor), ord2f(lg_next));
+                if (valid) lg_next = ld_relaxed(lgq);  // for the next tile
                 float thr2 = PILOT ? loose_pilot(thr, tq_, C) : loose_threshold(thr, tq_, A, C, dxmax);
                 const int64_t rbase = (int64_t)(t0 + i) * p.tile_stride * TC_BLOCK_N;
                 const uint32_t taddr = tmem + ((uint32_t)(ew * 32) << 16) + acc * TC_BLOCK_N;
                 uint32_t va[32], vb[32];
-                TMEM_LD32(taddr, va);
+                TMEM_LD32(taddr + half * I8_CPW * 32, va);
                 tmem_wait_ld();
 #pragma unroll 1
-                for (int cp = 0; cp < TC_BLOCK_N / 64; ++cp) {
+                for (int cp = 0; cp < I8_CPW / 2; ++cp) {
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
-                        const int c = 2 * cp + h;
+                        const int c = half * I8_CPW + 2 * cp + h;
                         uint32_t(&v)[32] = h ? vb : va;
                         // the next chunk streams in while this one is scored
                         if (h == 0) {
                             TMEM_LD32(taddr + (c + 1) * 32, vb);
-                        } else if (cp + 1 < TC_BLOCK_N / 64) {
+                        } else if (cp + 1 < I8_CPW / 2) {
                             TMEM_LD32(taddr + (c + 1) * 32, va);
                         }
                         const float4 *s4 = reinterpret_cast<const float4 *>(ss + c * 32);
@@ -391,7 +406,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
                             }
                             __syncwarp();
                         }
-                        if (h == 0 || cp + 1 < TC_BLOCK_N / 64) tmem_wait_ld();
+                        if (h == 0 || cp + 1 < I8_CPW / 2) tmem_wait_ld();
                     }
                 }
                 tc_fence_before();
@@ -402,11 +417,11 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
                 }
                 if (valid && ts[TC_KP - 1] > Lpub) {
                     Lpub = ts[TC_KP - 1];
-                    atomicMax(const_cast<uint32_t *>(lgq), f2ord(Lpub));
+                    atomicMax(lgq, f2ord(Lpub));
                 }
             }
             if (PILOT && valid) {
-                uint64_t *out = p.pcand + (q * p.nsplit + split) * TC_KP;
+                uint64_t *out = p.pcand + ((q * p.nsplit + split) * I8_HALVES + half) * TC_KP;
 #pragma unroll
                 for (int s = 0; s < TC_KP; ++s)
                     out[s] = (tr[s] == 0xFFFFFFFFu) ? 0ull : cand_key(ts[s], tr[s]);
@@ -614,7 +629,7 @@ __global__ void __launch_bounds__(W8_WARPS * 32) tc8_seed_kernel(I8SeedArgs a) {
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t wid = (int64_t)blockIdx.x * W8_WARPS + w;
     const int64_t nw = (int64_t)gridDim.x * W8_WARPS;
-    const int M = a.nsplit * TC_KP;
+    const int M = a.nsplit * I8_HALVES * TC_KP;
     float *qs = qdyn + w * (a.dp8 + 8);
     for (int64_t q = wid; q < a.nq; q += nw) {
         const uint64_t *cq = a.pcand + q * (int64_t)M;
@@ -870,7 +885,8 @@ size_t tc8_scratch_bytes(int64_t nq, int dp128, int64_t n) {
     const int64_t qtiles = nq_pad / TC_BLOCK_M, ntiles = ceil_div<int64_t>(n, TC_BLOCK_N);
     const int ps = pilot_splits(qtiles, ntiles);
     return (size_t)nq_pad * dp128 + (size_t)nq_pad * 16 + (size_t)nq * (4 + 4 + 4 + 4) +
-           (size_t)nq * i8_cap(n, nq) * 8 + (size_t)nq * ps * TC_KP * 8 + (size_t)nq * TC_KP * 12 + 65536;
+           (size_t)nq * i8_cap(n, nq) * 8 + (size_t)nq * ps * I8_HALVES * TC_KP * 8 + (size_t)nq * TC_KP * 12 +
+           65536;
 }
 
 int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats) {
@@ -921,7 +937,7 @@ int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats)
     double *seed_s = nullptr;
     if (psplit > 0) {
         const int64_t ptiles = ceil_div<int64_t>(ntiles, I8_PILOT_STRIDE);
-        uint64_t *pcand = cv.take<uint64_t>((size_t)s.nq * psplit * TC_KP);
+        uint64_t *pcand = cv.take<uint64_t>((size_t)s.nq * psplit * I8_HALVES * TC_KP);
         seed_rows = cv.take<int32_t>((size_t)s.nq * TC_KP);
         seed_s = cv.take<double>((size_t)s.nq * TC_KP);
         seed_n = cv.take<int32_t>((size_t)s.nq);
