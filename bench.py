@@ -11,13 +11,15 @@ every step does ONE all-gather of the per-rank top-k lists + a device merge
 (strong scaling: the total store and batch are fixed).
 
   value         queries/s, device-timed (CUDA events), inputs resident in HBM,
-                max over ranks; the 20 GB fp16 store per step is far larger
+                max over ranks; the 10 GB int8 scan copy read per step is far larger
                 than the 126 MB L2, so no flush is needed between steps
   e2e           the same through the public API with HOST buffers: pinned
                 query batch H2D + search + D2H of rows/scores, per step
-  roofline      the tcgen05 scan kernel, 2*n*d*B FLOP per launch / its CUDA-
-                event duration (recorded inside libpentarag on the launching
-                stream) vs the measured sustained bf16/fp16 peak
+  roofline      the int8 tcgen05 scan kernel (tc8_scan_kernel), 2*n*d*B ops per
+                launch / its CUDA-event duration (recorded inside libpentarag on
+                the launching stream) vs the sustained cuBLAS int8 GEMM rate
+                measured in this run (benchlib/peaks.py: MEASURED_PEAKS.json
+                holds bf16 only)
   cpu_baseline  rank 0 at N=1: the numpy einsum+lexsort restatement of
                 FlatIndex.search (oracle/) timed on this host's cores over the
                 full store for a bounded query sample, also used as a parity
@@ -380,25 +382,30 @@ def main():
     h2d = world * a.batch * a.dim * 4
     d2h = world * a.batch * (a.k * 16 + 4)
 
-    # ---- roofline of the tcgen05 scan (per launch, this rank's shard)
+    # ---- roofline of the int8 tcgen05 scan (per launch, this rank's shard)
     pk, pk_kind = peaks()
+    from benchlib.peaks import int8_peak
+
+    p8 = int8_peak()
     n_local = hi - lo
-    flop = 2.0 * n_local * a.dim * a.batch
+    ops = 2.0 * n_local * a.dim * a.batch
     kern_ms = scan_ms / max(1, scan_n)
-    achieved = flop / (kern_ms / 1e3) / 1e12
-    peak = float(pk.get("bf16_tflops_sustained", pk.get("bf16_tflops")))
+    achieved = ops / (kern_ms / 1e3) / 1e12
+    peak = float(p8["int8_tops_sustained"])
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", "tc_scan_traffic.json")
+    tpath = os.path.join(ROOT, "profiles", "tc8_scan_traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as fh:
             tj = json.load(fh)
         if tj.get("n_rows") == n_local and tj.get("dim") == a.dim and tj.get("batch") == a.batch:
             traffic = tj.get("dram_bytes_per_launch")
-    roof = {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
-            "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": "tc_scan_kernel",
+    roof = {"bound": "tensor", "achieved": round(achieved, 1), "peak": round(peak, 1), "unit": "TOP/s",
+            "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": "tc8_scan_kernel",
             "kernel_ms": round(kern_ms, 4), "kernel_share_of_step": round(kern_ms / ms_step, 4),
-            "peak_kind": f"{pk_kind} bf16_tflops_sustained (kernel timed inside back-to-back steps)",
-            "flop_per_launch": flop}
+            "peak_kind": "measured int8 sustained: " + p8["how"] + " (kernel timed inside back-to-back steps)",
+            "peak_burst": round(p8["int8_tops"], 1),
+            "frac_of_nominal_int8": round(achieved / 4500.0, 4),
+            "ops_per_launch": ops}
 
     # ---- CPU baseline + full-size parity (rank 0, N=1 only)
     cpu = None
@@ -438,7 +445,7 @@ def main():
         for name in wanted:
             try:
                 if name == "c2":
-                    configs["c2_semantic_cache"] = C.c2_semantic(peak)
+                    configs["c2_semantic_cache"] = C.c2_semantic(peak, p8["how"])
                 elif name == "c3":
                     configs["c3_fixed_kv"] = C.c3_kv(float(pk.get("hbm_gbs", 6538.6)), n_keys=a.kv_keys)
                 elif name == "c5":
@@ -453,15 +460,17 @@ def main():
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": "queries/s", "n_gpus": world,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "fp16",
-            "dtype_detail": "fp16 tcgen05 scan with fp32 TMEM accumulation; candidates rescored in fp64 "
-                            "numpy-einsum order (results bit-identical to the fp64 reference)",
+            "scaling": "strong", "vs_baseline": None, "dtype": "int8",
+            "dtype_detail": "int8 tcgen05 scan (s32 TMEM accumulation) with rigorous per-row quantisation "
+                            "bounds; every row that can reach the top-k is rescored in fp64 numpy-einsum order "
+                            "(results bit-identical to the fp64 reference)",
             "data": "synthetic",
             "config": {"workload": f"L5 retrieval top-k={a.k} over {a.n} x {a.dim} chunk store, batch {a.batch} "
                                    f"(BASELINE configs[3]); rows sharded over {world} GPU(s), all-gather merge",
                        "n_rows": a.n, "dim": a.dim, "batch": a.batch, "k": a.k,
                        "queries": "25% planted near-duplicates, 75% random unit vectors",
-                       "l2": "inputs larger than L2 (fp16 store 2 B x rows x dim per step vs 126 MB L2); no flush",
+                       "l2": "inputs larger than L2 (int8 scan copy 1 B x rows x dim = 10 GB per step vs 126 MB "
+                             "L2); no flush",
                        "parallelism": f"rowshard{world}"},
             "e2e": {"value": round(e2e_value, 1), "unit": "queries/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,

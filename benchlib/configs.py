@@ -30,7 +30,8 @@ def _unit_rows(n, d, seed, device="cuda"):
 
 
 # ---------------------------------------------------------------- C2
-def c2_semantic(peak_tflops: float, n=1_000_000, d=768, batch=4096, steps=20, threshold=0.85, parity_q=8):
+def c2_semantic(peak_tops: float, peak_how: str = "", n=1_000_000, d=768, batch=4096, steps=20, threshold=0.85,
+                parity_q=8):
     import torch
 
     from oracle import flat_index as F
@@ -78,8 +79,9 @@ def c2_semantic(peak_tflops: float, n=1_000_000, d=768, batch=4096, steps=20, th
         "workload": f"semantic-cache top-1 + threshold {threshold} over {n} x {d}, batch {batch} (configs[1])",
         "value": batch / (ms / 1e3), "unit": "lookups/s", "ms_per_batch": ms,
         "hit_fraction": float(hit.float().mean().item()),
-        "roofline": {"bound": "tensor", "achieved": flop / (kern / 1e3) / 1e12, "peak": peak_tflops,
-                     "unit": "TFLOP/s", "frac": flop / (kern / 1e3) / 1e12 / peak_tflops, "kernel_ms": kern},
+        "roofline": {"bound": "tensor", "achieved": flop / (kern / 1e3) / 1e12, "peak": peak_tops,
+                     "unit": "TOP/s", "frac": flop / (kern / 1e3) / 1e12 / peak_tops, "kernel_ms": kern,
+                     "kernel": "tc8_scan_kernel", "peak_kind": "measured int8 sustained: " + peak_how},
         "parity": {"queries_checked": int(sel.size), "mismatches": mism},
     }
 

@@ -12,10 +12,11 @@ timeout 600 python bench.py --impl reference > gpurun_out/bench_ref_${R}.json 2>
 tail -c 1500 gpurun_out/bench_ref_${R}.json
 # per-launch device times (cold-cache, serialised: compare shares, not absolutes)
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-    --log-file gpurun_out/launches_${R}.csv python bench.py --steps 3 --warmup 1 --no-cpu-baseline \
+    --log-file gpurun_out/launches_${R}.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --configs "" \
     > gpurun_out/launches_${R}.log 2>&1
-# full capture of one tcgen05 scan launch at the bench configuration
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:tc_scan_kernel -s 1 -c 1 \
-    -o gpurun_out/tc_scan_${R} python bench.py --steps 2 --warmup 1 --no-cpu-baseline \
+# full capture of the int8 scan at the bench configuration: launches 0 and 1 are the
+# first search's pilot and main scan (tc8_scan_kernel<true>, <false>)
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:tc8_scan_kernel -s 0 -c 2 \
+    -o gpurun_out/tc8_scan_${R} python bench.py --steps 1 --warmup 3 --no-cpu-baseline --configs "" \
     > gpurun_out/ncu_full_${R}.log 2>&1
 tail -3 gpurun_out/ncu_full_${R}.log

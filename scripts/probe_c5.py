@@ -1,22 +1,41 @@
-"""Stage profile of the routed C5 replay (route_batch) over an n-row store."""
-import argparse
-import json
+"""C5 routed-replay probe: stage timings and KB search stats per batch, for a
+given search mode (PR_MODE env: auto|tensor|i8)."""
+from __future__ import annotations
+
 import os
 import sys
+import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import torch  # noqa: E402
 
-import bench  # noqa: E402
 from benchlib import configs as C  # noqa: E402
+from scripts.probe_perf import make_store  # noqa: E402
 
-ap = argparse.ArgumentParser()
-ap.add_argument("--n", type=int, default=10_000_000)
-ap.add_argument("--queries", type=int, default=8000)
-ap.add_argument("--sessions", type=int, default=1)
-a = ap.parse_args()
-torch.cuda.set_device(0)
-idx = bench.build_shard(a.n, 1024, 0, a.n)
-r = C.c5_routed(idx, a.n, n_sessions=a.sessions, queries_per_session=a.queries, profile=True, parity_queries=50)
-print(json.dumps(r, indent=1))
+
+def main():
+    mode = {"auto": 0, "tensor": 2, "i8": 3, "exact": 1}[os.environ.get("PR_MODE", "auto")]
+    if mode:
+        from paper_2506_21593_b200 import router as R
+
+        orig = R.CascadeRouter.route_batch
+
+        def rb(self, queries, vectors=None, **kw):
+            kw.setdefault("mode", mode)
+            return orig(self, queries, vectors=vectors, **kw)
+
+        R.CascadeRouter.route_batch = rb
+    n = int(os.environ.get("N", "10000000"))
+    store = make_store(n, 1024)
+    t0 = time.time()
+    r = C.c5_routed(store, n, n_sessions=int(os.environ.get("S", "1")), queries_per_session=int(os.environ.get("Q", "12288")),
+                    profile=True)
+    print({k: v for k, v in r.items() if k in ("value", "layer_counts", "stage_seconds", "parity")})
+    st = store.stats()
+    print("last KB search: path", st.path, "fallback", st.fallback, "cand", st.candidates, "appended", st.appended,
+          "queries", st.queries, "wall", round(time.time() - t0, 1))
+
+
+if __name__ == "__main__":
+    main()
