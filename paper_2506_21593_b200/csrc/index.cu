@@ -536,7 +536,7 @@ static int reserve(pr_index *h, int64_t cap, cudaStream_t st) {
     if (e == cudaSuccess) e = cudaMalloc(&n8.x8, (size_t)c256 * h->dp128);
     if (e == cudaSuccess) e = cudaMalloc(&n8.xs, (size_t)c256 * sizeof(float));
     if (e == cudaSuccess) e = cudaMalloc(&n8.xe, (size_t)c256 * sizeof(float));
-    if (e == cudaSuccess) e = cudaMalloc(&n8.xt, (size_t)ntile * sizeof(float4));
+    if (e == cudaSuccess) e = cudaMalloc(&n8.xt, (size_t)ntile * sizeof(pr::I8TileMeta));
     if (e != cudaSuccess) {
         cudaFree(nx32);
         cudaFree(nx16);
@@ -549,15 +549,15 @@ static int reserve(pr_index *h, int64_t cap, cudaStream_t st) {
     PR_CUDA(cudaMemsetAsync(n8.x8, 0, (size_t)c256 * h->dp128, st));
     PR_CUDA(cudaMemsetAsync(n8.xs, 0, (size_t)c256 * sizeof(float), st));
     PR_CUDA(cudaMemsetAsync(n8.xe, 0, (size_t)c256 * sizeof(float), st));
-    PR_CUDA(cudaMemsetAsync(n8.xt, 0, (size_t)ntile * sizeof(float4), st));
+    PR_CUDA(cudaMemsetAsync(n8.xt, 0, (size_t)ntile * sizeof(pr::I8TileMeta), st));
     if (h->count > 0) {
         PR_CUDA(cudaMemcpyAsync(nx32, h->x32, (size_t)h->count * h->dp8 * sizeof(float), cudaMemcpyDeviceToDevice, st));
         PR_CUDA(cudaMemcpyAsync(nx16, h->x16, (size_t)h->count * h->dp64 * sizeof(__half), cudaMemcpyDeviceToDevice, st));
         PR_CUDA(cudaMemcpyAsync(n8.x8, h->r8.x8, (size_t)h->count * h->dp128, cudaMemcpyDeviceToDevice, st));
         PR_CUDA(cudaMemcpyAsync(n8.xs, h->r8.xs, (size_t)h->count * sizeof(float), cudaMemcpyDeviceToDevice, st));
         PR_CUDA(cudaMemcpyAsync(n8.xe, h->r8.xe, (size_t)h->count * sizeof(float), cudaMemcpyDeviceToDevice, st));
-        PR_CUDA(cudaMemcpyAsync(n8.xt, h->r8.xt, (size_t)(h->cap256 / 256) * sizeof(float4), cudaMemcpyDeviceToDevice,
-                                st));
+        PR_CUDA(cudaMemcpyAsync(n8.xt, h->r8.xt, (size_t)(h->cap256 / 256) * sizeof(pr::I8TileMeta),
+                                cudaMemcpyDeviceToDevice, st));
     }
     PR_CUDA(cudaStreamSynchronize(st));
     if (h->x32) cudaFree(h->x32);

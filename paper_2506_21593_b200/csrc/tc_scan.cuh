@@ -40,11 +40,18 @@ struct TcSearch {
 };
 
 // int8 tcgen05 scan (tc_scan_i8.cu): per-row quantised store + complete candidate set
+// per 256-row tile: max quantisation error bound and per-8-row-group max scale
+// (loose tests of the scan's fast path); both only grow, so they stay bounds
+struct alignas(16) I8TileMeta {
+    float dxmax;
+    float pad[3];
+    float gmax[32];
+};
 struct I8Rows {
     int8_t *x8 = nullptr;         // [cap256, dp128] quantised rows
     float *xs = nullptr;          // [cap256] per-row scale s_r
     float *xe = nullptr;          // [cap256] rounded-up ||x_r - s_r xq_r||_2
-    float4 *xt = nullptr;         // [cap256 / 256] {max xe over the 256-row tile, 0, 0, 0}
+    I8TileMeta *xt = nullptr;     // [cap256 / 256] per-tile bounds
     uint32_t *maxnorm = nullptr;  // device scalar: max ||x_r|| (fp32 bits, rounded up)
 };
 struct Tc8Search {

@@ -51,7 +51,7 @@ constexpr int I8_EPI = 32 * I8_EPI_WARPS;
 constexpr int I8_THREADS = 128 + I8_EPI;
 constexpr int I8_A_BYTES = TC_BLOCK_M * I8_BLOCK_K;  // 16 KB
 constexpr int I8_B_BYTES = TC_BLOCK_N * I8_BLOCK_K;  // 32 KB
-constexpr int I8_META_BYTES = TC_BLOCK_N * 4 * 2 + 16;  // s_r[256], dx_r[256], tile {dxmax, -, -, -}
+constexpr int I8_META_BYTES = TC_BLOCK_N * 4 * 2 + (int)sizeof(I8TileMeta);  // s_r[256], dx_r[256], tile bounds
 constexpr int I8_TMEM_COLS = 512;
 constexpr int I8_CAP = 32768;              // appended candidates per query before the exact fallback
 constexpr size_t I8_BUF_BYTES = 3ull << 30;  // ... unless the batch's buffers would exceed this
@@ -101,7 +101,7 @@ struct I8ScanParams {
     int k;
     const float *xs;      // [rows] s_r
     const float *xe;      // [rows] dx_r
-    const float4 *xt;     // [tiles] {max dx_r over the tile, ...}
+    const I8TileMeta *xt; // [tiles] per-tile bounds
     const float4 *qmeta;  // [nq_pad] {t_q, A_q, C_q, -}
     const int64_t *row_limit;
     int64_t nq;
@@ -110,6 +110,7 @@ struct I8ScanParams {
     uint2 *abuf;      // [nq][cap] {row, u bits}
     int cap;
     float thr_floor;  // measurement only: a floor under every bound (-inf normally)
+    int noepi;        // measurement only: the epilogue releases each tile untouched
     // pilot mode: scan store tiles idx * tile_stride only, keep the per-thread top-k of
     // l (no appends) and write it to pcand[((q * nsplit + split) * I8_HALVES + half) * TC_KP + i]
     int tile_stride;
@@ -217,7 +218,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
                     mbar_expect_tx(&mfull[acc], I8_META_BYTES);
                     bulk_load_1d(m, p.xs + (int64_t)t * TC_BLOCK_N, TC_BLOCK_N * 4, &mfull[acc]);
                     bulk_load_1d(m + TC_BLOCK_N * 4, p.xe + (int64_t)t * TC_BLOCK_N, TC_BLOCK_N * 4, &mfull[acc]);
-                    bulk_load_1d(m + TC_BLOCK_N * 8, p.xt + t, 16, &mfull[acc]);
+                    bulk_load_1d(m + TC_BLOCK_N * 8, p.xt + t, sizeof(I8TileMeta), &mfull[acc]);
                     for (int kb = 0; kb < p.nkb; ++kb) {
                         mbar_wait(&empty[stage], phase ^ 1);
                         mbar_expect_tx(&full[stage], I8_A_BYTES + I8_B_BYTES);
@@ -297,9 +298,19 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
                 mbar_wait(&mfull[acc], aphase);
                 mbar_wait(&tfull[acc], aphase);
                 tc_fence_after();
+                if (p.noepi) {
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) {
+                        mbar_arrive(&tempty[acc]);
+                        mbar_arrive(&mempty[acc]);
+                    }
+                    continue;
+                }
                 const float *ss = reinterpret_cast<const float *>(smeta + acc * I8_META_BYTES);
                 const float *se = ss + TC_BLOCK_N;
-                const float dxmax = se[TC_BLOCK_N];
+                const I8TileMeta *tm = reinterpret_cast<const I8TileMeta *>(se + TC_BLOCK_N);
+                const float dxmax = tm->dxmax;
                 // main: append rows with u >= thr; pilot: insert rows with l > thr
                 float thr = fmaxf(fmaxf(ts[TC_KP - 1], p.thr_floor), ord2f(lg_next));
                 if (valid) lg_next = ld_relaxed(lgq);  // for the next tile
@@ -489,7 +500,7 @@ __device__ __forceinline__ double norm_up(double sumsq) { return sqrt(sumsq) * (
 
 __global__ void quantize_rows_kernel(const float *__restrict__ src, int64_t n, int d, const int64_t *__restrict__ rows,
                                      int64_t row0, int dp128, int8_t *__restrict__ x8, float *__restrict__ xs,
-                                     float *__restrict__ xe, float4 *__restrict__ xt, uint32_t *__restrict__ maxnorm) {
+                                     float *__restrict__ xe, I8TileMeta *__restrict__ xt, uint32_t *__restrict__ maxnorm) {
     const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32;
     if (w >= n) return;
     const int64_t r = rows ? rows[w] : row0 + w;
@@ -501,7 +512,8 @@ __global__ void quantize_rows_kernel(const float *__restrict__ src, int64_t n, i
         xs[r] = s;
         xe[r] = dx;
         // positive floats order as uints; both maxima only grow (stay valid bounds)
-        atomicMax(reinterpret_cast<uint32_t *>(&xt[r / TC_BLOCK_N].x), __float_as_uint(dx));
+        atomicMax(reinterpret_cast<uint32_t *>(&xt[r / TC_BLOCK_N].dxmax), __float_as_uint(dx));
+        atomicMax(reinterpret_cast<uint32_t *>(&xt[r / TC_BLOCK_N].gmax[(r % TC_BLOCK_N) / 8]), __float_as_uint(s));
         atomicMax(maxnorm, __float_as_uint(__double2float_ru(norm_up(n2))));
     }
 }
@@ -510,7 +522,7 @@ __global__ void gather_i8_kernel(const int8_t *__restrict__ sx8, const float *__
                                  const float *__restrict__ sxe, const uint32_t *__restrict__ smaxnorm,
                                  const int64_t *__restrict__ src_rows, int64_t n, int dp128, int64_t row0,
                                  int8_t *__restrict__ x8, float *__restrict__ xs, float *__restrict__ xe,
-                                 float4 *__restrict__ xt, uint32_t *__restrict__ maxnorm) {
+                                 I8TileMeta *__restrict__ xt, uint32_t *__restrict__ maxnorm) {
     // the gathered rows' norms are bounded by the source's maximum
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicMax(maxnorm, *smaxnorm);
     const int64_t total = n * (int64_t)(dp128 / 16);
@@ -523,7 +535,9 @@ __global__ void gather_i8_kernel(const int8_t *__restrict__ sx8, const float *__
             const int64_t r = row0 + i;
             xs[r] = sxs[s];
             xe[r] = sxe[s];
-            atomicMax(reinterpret_cast<uint32_t *>(&xt[r / TC_BLOCK_N].x), __float_as_uint(sxe[s]));
+            atomicMax(reinterpret_cast<uint32_t *>(&xt[r / TC_BLOCK_N].dxmax), __float_as_uint(sxe[s]));
+            atomicMax(reinterpret_cast<uint32_t *>(&xt[r / TC_BLOCK_N].gmax[(r % TC_BLOCK_N) / 8]),
+                      __float_as_uint(sxs[s]));
         }
     }
 }
@@ -943,7 +957,7 @@ int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats)
         seed_n = cv.take<int32_t>((size_t)s.nq);
         I8ScanParams pp{s.n, s.dp128 / I8_BLOCK_K, psplit, (int)ceil_div<int64_t>(ptiles, psplit), (int)ptiles,
                         (int)qtiles, s.k, s.rows8.xs, s.rows8.xe, s.rows8.xt, qmeta, s.row_limit, s.nq, lg, acount,
-                        abuf, cap, floor_thr, I8_PILOT_STRIDE, pcand};
+                        abuf, cap, floor_thr, 0, I8_PILOT_STRIDE, pcand};
         ::pr::count_launch();
         tc8_scan_kernel<true><<<(unsigned)(qtiles * psplit), I8_THREADS, i8_smem_bytes(), st>>>(
             qmap.map, s.store_map->map, pp);
@@ -955,7 +969,9 @@ int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats)
     }
     // 2) main scan: append every row whose upper bound reaches the running bound
     I8ScanParams p{s.n, s.dp128 / I8_BLOCK_K, nsplit, tps, (int)ntiles, (int)qtiles, s.k, s.rows8.xs, s.rows8.xe,
-                   s.rows8.xt, qmeta, s.row_limit, s.nq, lg, acount, abuf, cap, floor_thr, 1, nullptr};
+                   s.rows8.xt, qmeta, s.row_limit, s.nq, lg, acount, abuf, cap, floor_thr, 0, 1, nullptr};
+    const char *noepi_env = getenv("PR_I8_NOEPI");  // 1: epilogue does nothing (results invalid): MMA/TMA timing
+    if (noepi_env && noepi_env[0] == '1') p.noepi = 1;
     ::pr::count_launch();
     if (s.ev_begin) PR_CUDA(cudaEventRecord(s.ev_begin, st));
     tc8_scan_kernel<false><<<(unsigned)(qtiles * nsplit), I8_THREADS, i8_smem_bytes(), st>>>(qmap.map,
