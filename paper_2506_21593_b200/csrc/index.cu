@@ -478,7 +478,8 @@ struct pr_index {
     pr::I8Rows r8;               // int8 scan copy [cap256, dp128] + per-row scale / error bound
     pr::TcStoreMap tmap;  // TMA descriptor of x16 (rebuilt on reallocation)
     bool tmap_ok = false;
-    pr::TcStoreMap tmap8;  // TMA descriptor of x8
+    pr::TcStoreMap tmap8;   // TMA descriptor of x8, 256-row boxes
+    pr::TcStoreMap tmap8h;  // ... 128-row boxes (2-CTA scan)
     bool tmap8_ok = false;
     pr_search_stats stats{};
     // device scratch (grown on demand, stream-ordered)
@@ -869,13 +870,16 @@ int pr_index_search_ex(pr_index *h, const float *d_q, int64_t nq, int k, uint32_
     if (use_i8) {
         h->stats.path = PR_SEARCH_TENSOR_I8;
         if (!h->tmap8_ok) {
-            rc = pr::i8_make_store_map(&h->tmap8, h->r8.x8, h->cap256, h->dp128);
+            rc = pr::i8_make_store_map(&h->tmap8, h->r8.x8, h->cap256, h->dp128, 256);
+            if (rc) return rc;
+            rc = pr::i8_make_store_map(&h->tmap8h, h->r8.x8, h->cap256, h->dp128, 128);
             if (rc) return rc;
             h->tmap8_ok = true;
         }
         pr::Tc8Search ts{};
         ts.x32 = h->x32;
         ts.store_map = &h->tmap8;
+        ts.store_map_half = &h->tmap8h;
         ts.rows8 = h->r8;
         ts.n = h->count;
         ts.d = h->dim;

@@ -56,7 +56,8 @@ struct I8Rows {
 };
 struct Tc8Search {
     const float *x32;
-    const TcStoreMap *store_map;  // TMA map of rows8.x8
+    const TcStoreMap *store_map;       // TMA map of rows8.x8, 256-row boxes (cta_group::1)
+    const TcStoreMap *store_map_half;  // ... 128-row boxes (cta_group::2: each CTA loads half a tile)
     I8Rows rows8;
     int64_t n;
     int d, dp8, dp128;
@@ -75,7 +76,7 @@ int i8_quantize_rows(const float *src, int64_t n, int d, const int64_t *rows, in
                      cudaStream_t st);
 int i8_gather_rows(const I8Rows &src, const int64_t *src_rows, int64_t n, int dp128, int64_t row0, I8Rows &m,
                    cudaStream_t st);
-int i8_make_store_map(TcStoreMap *m, const int8_t *x8, int64_t rows, int dp128);
+int i8_make_store_map(TcStoreMap *m, const int8_t *x8, int64_t rows, int dp128, int box_rows);
 bool tc8_eligible(int d);
 size_t tc8_scratch_bytes(int64_t nq, int dp128, int64_t n);
 int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats);

@@ -46,7 +46,8 @@ constexpr int I8_BLOCK_K = 128;  // int8 columns per stage = one 128-B swizzle a
 constexpr int I8_EPI_WARPS = 8;
 constexpr int I8_HALVES = I8_EPI_WARPS / 4;
 constexpr int I8_CPW = (TC_BLOCK_N / 32) / I8_HALVES;  // 32-column chunks per epilogue warp per tile
-constexpr int I8_STAGES = I8_EPI_WARPS == 8 ? 3 : 4;
+constexpr int I8_STAGES = I8_EPI_WARPS == 8 ? 3 : 4;  // cta_group::1: 48 KB per stage
+constexpr int I8_STAGES2 = 5;                          // cta_group::2: 32 KB per stage and CTA
 constexpr int I8_EPI = 32 * I8_EPI_WARPS;
 constexpr int I8_THREADS = 128 + I8_EPI;
 constexpr int I8_A_BYTES = TC_BLOCK_M * I8_BLOCK_K;  // 16 KB
@@ -65,9 +66,21 @@ constexpr float I8_MAGIC_F = 12582912.0f;
 constexpr uint32_t I8_IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TC_BLOCK_N >> 3) << 17) |
                               ((uint32_t)(TC_BLOCK_M >> 4) << 24);
 
+// CG = CTAs per MMA (tcgen05 cta_group): with 2, an SM pair computes a 256-query x
+// 256-row tile; each CTA stages its own 128 queries and HALF of the 256 store rows
+template <int CG>
+struct I8Cfg {
+    static constexpr int STAGES = CG == 2 ? I8_STAGES2 : I8_STAGES;
+    static constexpr int B_ROWS = TC_BLOCK_N / CG;
+    static constexpr int B_BYTES = B_ROWS * I8_BLOCK_K;
+};
+// in-kernel exact refiner (warps 2-3): job table + per-query exact lists
+constexpr int I8_RQ = 256;
+constexpr size_t I8_REFINER_BYTES = (size_t)I8_RQ * 8 + (size_t)TC_BLOCK_M * TC_KP * 8 + (size_t)TC_BLOCK_M * 8 + 64;
+template <int CG>
 constexpr size_t i8_smem_bytes() {
-    return 1024 + (size_t)I8_STAGES * (I8_A_BYTES + I8_B_BYTES) + 2 * (size_t)I8_META_BYTES +
-           (size_t)32 * I8_EPI * 4 + 256;
+    return 1024 + (size_t)I8Cfg<CG>::STAGES * (I8_A_BYTES + I8Cfg<CG>::B_BYTES) + 2 * (size_t)I8_META_BYTES +
+           (size_t)32 * I8_EPI * 4 + 256 + I8_REFINER_BYTES;
 }
 
 __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accum) {
@@ -76,6 +89,52 @@ __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
         "l"(adesc), "l"(bdesc), "r"(I8_IDESC), "r"(accum)
+        : "memory");
+}
+
+// M = 256 (both CTAs of the pair), N = 256
+constexpr uint32_t I8_IDESC2 = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TC_BLOCK_N >> 3) << 17) |
+                               ((uint32_t)(256 >> 4) << 24);
+__device__ __forceinline__ void mma_i8_cg2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(I8_IDESC2), "r"(accum)
+        : "memory");
+}
+// arrive on the same barrier in both CTAs of the pair when the issued MMAs complete
+__device__ __forceinline__ void mma_commit_cg2(uint64_t *bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+// shared::cluster address of the same smem offset in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t saddr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// 2-CTA TMA tile load: data lands in this CTA's smem, bytes are counted on the
+// leader CTA's barrier (cluster address)
+__device__ __forceinline__ void tma_load_2d_cg2(void *dst, const CUtensorMap *map, uint32_t bar_cluster, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+        "[%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1)
         : "memory");
 }
 
@@ -115,6 +174,11 @@ struct I8ScanParams {
     // l (no appends) and write it to pcand[((q * nsplit + split) * I8_HALVES + half) * TC_KP + i]
     int tile_stride;
     uint64_t *pcand;
+    // exact rows / queries for the in-kernel refiner
+    const float *x32;
+    const float *qp;
+    int dp8, d;
+    int refine;  // hand rows at the bound to the exact refiner warps
 };
 
 // loose per-tile test in the scaled domain: a row can pass u = t s acc + A dx + C >= thr
@@ -146,30 +210,54 @@ __device__ __forceinline__ int nth_set_bit(uint32_t m, int n) {
     return __ffs(m) - 1;
 }
 
-template <bool PILOT>
+template <bool PILOT, int CG>
 __global__ void __launch_bounds__(I8_THREADS, 1)
     tc8_scan_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tx, I8ScanParams p) {
+    constexpr int STAGES = I8Cfg<CG>::STAGES;
+    constexpr int B_BYTES = I8Cfg<CG>::B_BYTES;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-B alignment for SWIZZLE_128B, as an offset from the __shared__ array so
     // every derived pointer stays in the shared window (LDS/STS, not generic LD/ST)
     uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t *sA = smem;
-    uint8_t *sB = sA + I8_STAGES * I8_A_BYTES;
-    uint8_t *smeta = sB + I8_STAGES * I8_B_BYTES;  // [2][I8_META_BYTES]
-    int32_t *spill = reinterpret_cast<int32_t *>(smeta + 2 * I8_META_BYTES);  // [32][128]
+    uint8_t *sB = sA + STAGES * I8_A_BYTES;
+    uint8_t *smeta = sB + STAGES * B_BYTES;  // [2][I8_META_BYTES]
+    int32_t *spill = reinterpret_cast<int32_t *>(smeta + 2 * I8_META_BYTES);  // [32][I8_EPI]
     uint64_t *full = reinterpret_cast<uint64_t *>(spill + 32 * I8_EPI);
-    uint64_t *empty = full + I8_STAGES;
-    uint64_t *tfull = empty + I8_STAGES;
+    uint64_t *empty = full + STAGES;
+    uint64_t *tfull = empty + STAGES;
     uint64_t *tempty = tfull + 2;
     uint64_t *mfull = tempty + 2;
     uint64_t *mempty = mfull + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(mempty + 2);
+    uint64_t *rq = reinterpret_cast<uint64_t *>(smem + (size_t)STAGES * (I8_A_BYTES + B_BYTES) + 2 * I8_META_BYTES +
+                                                32 * I8_EPI * 4 + 256);  // [I8_RQ] refiner jobs {q+1, row}
+    double *rel = reinterpret_cast<double *>(rq + I8_RQ);                // [128][TC_KP] exact lists
+    int32_t *rown = reinterpret_cast<int32_t *>(rel + TC_BLOCK_M * TC_KP);  // [128] list owner (global q)
+    int32_t *rcnt = rown + TC_BLOCK_M;                                    // [128] entries
+    uint32_t *rq_tail = reinterpret_cast<uint32_t *>(rcnt + TC_BLOCK_M);
+    uint32_t *epi_done = rq_tail + 1;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nitems = p.qtiles * p.nsplit;
+    if (!PILOT) {
+        for (int i = threadIdx.x; i < I8_RQ; i += blockDim.x) rq[i] = 0ull;
+        for (int i = threadIdx.x; i < TC_BLOCK_M; i += blockDim.x) {
+            rown[i] = -1;
+            rcnt[i] = 0;
+        }
+        if (threadIdx.x == 0) {
+            *rq_tail = 0;
+            *epi_done = 0;
+        }
+    }
+    // CG == 2: the CTA pair (one cluster) shares items; rank r scans query tile 2*qp + r
+    const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
+    const int qgroups = p.qtiles / CG;
+    const int nitems = qgroups * p.nsplit;
+    const int item0 = blockIdx.x / CG, istride = gridDim.x / CG;
     auto item_of = [&](int item, int &qtile, int &split, int &t0, int &nloc) {
-        qtile = item % p.qtiles;
-        split = item / p.qtiles;
+        qtile = (item % qgroups) * CG + (int)rank;
+        split = item / qgroups;
         t0 = split * p.tiles_per_split;
         nloc = max(0, min(p.ntiles, t0 + p.tiles_per_split) - t0);
     };
@@ -177,26 +265,34 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tq);
         tma_prefetch_desc(&tx);
-        for (int s = 0; s < I8_STAGES; ++s) {
+        for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], I8_EPI / 32);
+            mbar_init(&tempty[a], CG * I8_EPI / 32);  // every epilogue warp of the pair (leader's copy)
             mbar_init(&mfull[a], 1);
             mbar_init(&mempty[a], I8_EPI / 32);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 2) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(I8_TMEM_COLS)
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        if (CG == 2) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                         "r"(I8_TMEM_COLS)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                         "r"(I8_TMEM_COLS)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        }
     }
     tc_fence_before();
     __syncthreads();
+    if (CG == 2) cluster_sync();  // peer barriers initialised before any remote arrive / TMA
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
@@ -206,7 +302,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
             int stage = 0;
             uint32_t phase = 0;
             int tix = 0;
-            for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+            for (int item = item0; item < nitems; item += istride) {
                 int qtile, split, t0, nloc;
                 item_of(item, qtile, split, t0, nloc);
                 for (int i = 0; i < nloc; ++i, ++tix) {
@@ -221,21 +317,30 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
                     bulk_load_1d(m + TC_BLOCK_N * 8, p.xt + t, sizeof(I8TileMeta), &mfull[acc]);
                     for (int kb = 0; kb < p.nkb; ++kb) {
                         mbar_wait(&empty[stage], phase ^ 1);
-                        mbar_expect_tx(&full[stage], I8_A_BYTES + I8_B_BYTES);
-                        tma_load_2d(sA + stage * I8_A_BYTES, &tq, &full[stage], kb * I8_BLOCK_K, qtile * TC_BLOCK_M);
-                        tma_load_2d(sB + stage * I8_B_BYTES, &tx, &full[stage], kb * I8_BLOCK_K, t * TC_BLOCK_N);
-                        if (++stage == I8_STAGES) { stage = 0; phase ^= 1; }
+                        if (CG == 2) {
+                            // the leader's barrier counts both CTAs' bytes; its producer posts the total
+                            if (rank == 0) mbar_expect_tx(&full[stage], CG * (I8_A_BYTES + B_BYTES));
+                            const uint32_t fb = mapa_u32(smem_u32(&full[stage]), 0);
+                            tma_load_2d_cg2(sA + stage * I8_A_BYTES, &tq, fb, kb * I8_BLOCK_K, qtile * TC_BLOCK_M);
+                            tma_load_2d_cg2(sB + stage * B_BYTES, &tx, fb, kb * I8_BLOCK_K,
+                                            t * TC_BLOCK_N + (int)rank * I8Cfg<CG>::B_ROWS);
+                        } else {
+                            mbar_expect_tx(&full[stage], I8_A_BYTES + B_BYTES);
+                            tma_load_2d(sA + stage * I8_A_BYTES, &tq, &full[stage], kb * I8_BLOCK_K, qtile * TC_BLOCK_M);
+                            tma_load_2d(sB + stage * B_BYTES, &tx, &full[stage], kb * I8_BLOCK_K, t * TC_BLOCK_N);
+                        }
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
                 }
             }
         }
     } else if (warp == 1) {
-        // ---------------- MMA issuer (single thread) ----------------
-        if (lane == 0) {
+        // ---------------- MMA issuer (single thread; the pair's leader for CG == 2) ----------------
+        if (lane == 0 && rank == 0) {
             int stage = 0;
             uint32_t phase = 0;
             int tix = 0;
-            for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+            for (int item = item0; item < nitems; item += istride) {
                 int qtile, split, t0, nloc;
                 item_of(item, qtile, split, t0, nloc);
                 for (int i = 0; i < nloc; ++i, ++tix) {
@@ -248,14 +353,24 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
                         mbar_wait(&full[stage], phase);
                         tc_fence_after();
                         const uint64_t ad = sw128_desc(smem_u32(sA + stage * I8_A_BYTES));
-                        const uint64_t bd = sw128_desc(smem_u32(sB + stage * I8_B_BYTES));
+                        const uint64_t bd = sw128_desc(smem_u32(sB + stage * B_BYTES));
 #pragma unroll
-                        for (int k = 0; k < I8_BLOCK_K / 32; ++k)  // K = 32 int8 = 32 B per MMA inside the atom
-                            mma_i8(d_tmem, ad + 2 * k, bd + 2 * k, (kb | k) != 0);
-                        mma_commit(&empty[stage]);
-                        if (++stage == I8_STAGES) { stage = 0; phase ^= 1; }
+                        for (int k = 0; k < I8_BLOCK_K / 32; ++k) {  // K = 32 int8 = 32 B per MMA inside the atom
+                            if (CG == 2)
+                                mma_i8_cg2(d_tmem, ad + 2 * k, bd + 2 * k, (kb | k) != 0);
+                            else
+                                mma_i8(d_tmem, ad + 2 * k, bd + 2 * k, (kb | k) != 0);
+                        }
+                        if (CG == 2)
+                            mma_commit_cg2(&empty[stage]);
+                        else
+                            mma_commit(&empty[stage]);
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
-                    mma_commit(&tfull[acc]);
+                    if (CG == 2)
+                        mma_commit_cg2(&tfull[acc]);
+                    else
+                        mma_commit(&tfull[acc]);
                 }
             }
         }
@@ -266,7 +381,9 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
         const int et = ew * 32 + lane;                // TMEM lane == query within the tile
         int32_t *wspill = spill + (warp - 4) * 32;  // this warp's columns of the [32][I8_EPI] spill
         int tix = 0;
-        for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+        // the MMA issuer waits on the leader's tempty: every epilogue warp of the pair arrives there
+        const uint32_t tempty_leader0 = mapa_u32(smem_u32(&tempty[0]), 0);
+        for (int item = item0; item < nitems; item += istride) {
             int qtile, split, t0, nloc;
             item_of(item, qtile, split, t0, nloc);
             const int64_t q = (int64_t)qtile * TC_BLOCK_M + et;
@@ -302,7 +419,10 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) {
-                        mbar_arrive(&tempty[acc]);
+                        if (CG == 2)
+                            mbar_arrive_cluster(tempty_leader0 + acc * 8);
+                        else
+                            mbar_arrive(&tempty[acc]);
                         mbar_arrive(&mempty[acc]);
                     }
                     continue;
@@ -356,12 +476,19 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
                         // rare: the warp evaluates every flagged (query, 8-row group) pair
                         // cooperatively, 4 pairs (32 rows) per pass, one row per lane
                         if (__any_sync(0xffffffffu, gmask != 0)) {
-#pragma unroll
-                            for (int j = 0; j < 32; ++j) wspill[j * I8_EPI + lane] = (int32_t)v[j];
                             const uint32_t b0 = __ballot_sync(0xffffffffu, gmask & 1u);
                             const uint32_t b1 = __ballot_sync(0xffffffffu, gmask & 2u);
                             const uint32_t b2 = __ballot_sync(0xffffffffu, gmask & 4u);
                             const uint32_t b3 = __ballot_sync(0xffffffffu, gmask & 8u);
+                            // spill only the groups some lane flagged (warp-uniform branches)
+#pragma unroll
+                            for (int g = 0; g < 4; ++g) {
+                                const uint32_t bg = g == 0 ? b0 : g == 1 ? b1 : g == 2 ? b2 : b3;
+                                if (bg) {
+#pragma unroll
+                                    for (int j = 8 * g; j < 8 * g + 8; ++j) wspill[j * I8_EPI + lane] = (int32_t)v[j];
+                                }
+                            }
                             const int p1 = __popc(b0), p2 = p1 + __popc(b1), p3 = p2 + __popc(b2);
                             const int npairs = p3 + __popc(b3);
                             __syncwarp();
@@ -395,6 +522,13 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
                                             const int64_t oq = (int64_t)qtile * TC_BLOCK_M + ew * 32 + owner;
                                             const int o = atomicAdd(&p.acount[oq], 1);
                                             if (o < p.cap) p.abuf[oq * (int64_t)p.cap + o] = make_uint2(row, __float_as_uint(u));
+                                            // approximate score at the bound: hand the row to the refiner
+                                            // (a full table just drops the job: the bound is a heuristic)
+                                            if (p.refine && ap >= o_thr) {
+                                                const uint32_t slot = atomicAdd(rq_tail, 1u) & (I8_RQ - 1);
+                                                atomicCAS(reinterpret_cast<unsigned long long *>(&rq[slot]), 0ull,
+                                                          ((unsigned long long)(oq + 1) << 32) | row);
+                                            }
                                         }
                                     }
                                 }
@@ -423,7 +557,10 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) {
-                    mbar_arrive(&tempty[acc]);
+                    if (CG == 2)
+                        mbar_arrive_cluster(tempty_leader0 + acc * 8);
+                    else
+                        mbar_arrive(&tempty[acc]);
                     mbar_arrive(&mempty[acc]);
                 }
                 if (valid && ts[TC_KP - 1] > Lpub) {
@@ -438,13 +575,75 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
                     out[s] = (tr[s] == 0xFFFFFFFFu) ? 0ull : cand_key(ts[s], tr[s]);
             }
         }
+        if (!PILOT) {
+            __threadfence_block();
+            __syncwarp();
+            if (lane == 0) atomicAdd(epi_done, 1u);
+        }
+    } else if (!PILOT && (warp == 2 || warp == 3)) {
+        // ---------------- exact refiner: score handed-over rows in fp64 einsum order ----------------
+        // warp 2 owns even local queries, warp 3 odd ones (each list has a single writer)
+        const uint32_t par = (uint32_t)(warp - 2);
+        for (;;) {
+            uint64_t job = 0;
+            for (int i = lane; i < I8_RQ && !job; i += 32) {
+                const uint64_t v = *reinterpret_cast<volatile uint64_t *>(&rq[i]);
+                if (v && ((uint32_t)((v >> 32) - 1) & 1u) == par)
+                    job = atomicExch(reinterpret_cast<unsigned long long *>(&rq[i]), 0ull);
+            }
+            const uint32_t has = __ballot_sync(0xffffffffu, job != 0);
+            if (!has) {
+                if (*reinterpret_cast<volatile uint32_t *>(epi_done) == I8_EPI / 32) {
+                    // the epilogue finished (its pushes precede the count): drain once more, then stop
+                    bool any = false;
+                    for (int i = lane; i < I8_RQ; i += 32) any |= *reinterpret_cast<volatile uint64_t *>(&rq[i]) != 0;
+                    if (!__any_sync(0xffffffffu, any)) break;
+                }
+                __nanosleep(500);
+                continue;
+            }
+            const int64_t qg = job ? (int64_t)(job >> 32) - 1 : 0;
+            const uint32_t row = (uint32_t)job;
+            double ex = 0.0;
+            if (job) ex = einsum_dot_f32(p.x32 + (int64_t)row * p.dp8, p.qp + qg * p.dp8, p.d);
+            for (uint32_t m = has; m; m &= m - 1) {
+                const int src = __ffs(m) - 1;
+                if (lane == src) {
+                    const int ql = (int)(qg % TC_BLOCK_M);
+                    if (rown[ql] != (int32_t)qg) {  // a new item brought new queries
+                        rown[ql] = (int32_t)qg;
+                        rcnt[ql] = 0;
+                    }
+                    double *L = rel + ql * TC_KP;
+                    int n = rcnt[ql];
+                    if (n < p.k || ex > L[p.k - 1]) {
+                        int pos = n < p.k ? n++ : p.k - 1;
+                        while (pos > 0 && ex > L[pos - 1]) {
+                            L[pos] = L[pos - 1];
+                            --pos;
+                        }
+                        L[pos] = ex;
+                        rcnt[ql] = n;
+                        // k distinct rows score >= L[k-1] exactly: a valid lower bound on e_k
+                        if (n == p.k) atomicMax(p.lg + qg, f2ord(__double2float_rd(L[p.k - 1])));
+                    }
+                }
+                __syncwarp();
+            }
+        }
     }
 
     tc_fence_before();
     __syncthreads();
+    if (CG == 2) cluster_sync();  // no CTA leaves while its peer may still signal its barriers
     if (warp == 2) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(I8_TMEM_COLS) : "memory");
+        if (CG == 2)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(I8_TMEM_COLS)
+                         : "memory");
+        else
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(I8_TMEM_COLS)
+                         : "memory");
     }
 }
 
@@ -872,8 +1071,8 @@ int i8_gather_rows(const I8Rows &src, const int64_t *src_rows, int64_t n, int dp
     return PR_OK;
 }
 
-int i8_make_store_map(TcStoreMap *m, const int8_t *x8, int64_t rows, int dp128) {
-    return make_map_2d(&m->map, x8, rows, dp128, 1, I8_BLOCK_K, TC_BLOCK_N);
+int i8_make_store_map(TcStoreMap *m, const int8_t *x8, int64_t rows, int dp128, int box_rows) {
+    return make_map_2d(&m->map, x8, rows, dp128, 1, I8_BLOCK_K, box_rows);
 }
 
 static int i8_cap(int64_t n, int64_t nq) {
@@ -884,18 +1083,63 @@ static int i8_cap(int64_t n, int64_t nq) {
 
 // pilot: every I8_PILOT_STRIDE-th 256-row tile (~3% of the scan) when the store has
 // at least I8_PILOT_MIN_TILES tiles
-constexpr int I8_PILOT_STRIDE = 32;
-constexpr int64_t I8_PILOT_MIN_TILES = 8 * I8_PILOT_STRIDE;
+static int pilot_stride() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("PR_I8_PILOT_STRIDE");  // measurement knob
+        v = e ? std::max(2, atoi(e)) : 32;
+    }
+    return v;
+}
+#define I8_PILOT_STRIDE pilot_stride()
 
 static int pilot_splits(int64_t qtiles, int64_t ntiles) {
-    if (ntiles < I8_PILOT_MIN_TILES) return 0;
+    if (ntiles < 8 * (int64_t)I8_PILOT_STRIDE) return 0;
     return choose_nsplit_waves(qtiles, ceil_div<int64_t>(ntiles, I8_PILOT_STRIDE));
 }
 
 bool tc8_eligible(int d) { return d <= 2048; }
 
+// PR_I8_CG=1 selects the single-CTA MMA (default: 2-CTA pairs)
+static int i8_cg() {
+    const char *e = getenv("PR_I8_CG");
+    return (e && e[0] == '1') ? 1 : 2;
+}
+
+template <bool PILOT, int CG>
+static int launch_scan8(int64_t ctas, const CUtensorMap &tq, const CUtensorMap &tx, const I8ScanParams &p,
+                        cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        PR_CUDA(cudaFuncSetAttribute(tc8_scan_kernel<PILOT, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)i8_smem_bytes<CG>()));
+        attr = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)ctas);
+    cfg.blockDim = dim3(I8_THREADS);
+    cfg.dynamicSmemBytes = i8_smem_bytes<CG>();
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CG;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    ::pr::count_launch();
+    PR_CUDA(cudaLaunchKernelEx(&cfg, tc8_scan_kernel<PILOT, CG>, tq, tx, p));
+    return PR_OK;
+}
+
+template <bool PILOT>
+static int launch_scan8_cg(int cg, int64_t ctas, const CUtensorMap &tq, const CUtensorMap &tx, const I8ScanParams &p,
+                           cudaStream_t st) {
+    return cg == 2 ? launch_scan8<PILOT, 2>(ctas, tq, tx, p, st) : launch_scan8<PILOT, 1>(ctas, tq, tx, p, st);
+}
+
 size_t tc8_scratch_bytes(int64_t nq, int dp128, int64_t n) {
-    const int64_t nq_pad = round_up<int64_t>(nq, TC_BLOCK_M);
+    const int64_t nq_pad = round_up<int64_t>(nq, 2 * TC_BLOCK_M);
     const int64_t qtiles = nq_pad / TC_BLOCK_M, ntiles = ceil_div<int64_t>(n, TC_BLOCK_N);
     const int ps = pilot_splits(qtiles, ntiles);
     return (size_t)nq_pad * dp128 + (size_t)nq_pad * 16 + (size_t)nq * (4 + 4 + 4 + 4) +
@@ -904,7 +1148,8 @@ size_t tc8_scratch_bytes(int64_t nq, int dp128, int64_t n) {
 }
 
 int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats) {
-    const int64_t nq_pad = round_up<int64_t>(s.nq, TC_BLOCK_M);
+    const int cg = i8_cg();
+    const int64_t nq_pad = round_up<int64_t>(s.nq, cg * TC_BLOCK_M);
     const int64_t qtiles = nq_pad / TC_BLOCK_M;
     const int64_t ntiles = ceil_div<int64_t>(s.n, TC_BLOCK_N);
     const int nsplit = choose_nsplit_waves(qtiles, ntiles);
@@ -930,12 +1175,9 @@ int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats)
     int rc = make_map_2d(&qmap.map, q8, nq_pad, s.dp128, 1, I8_BLOCK_K, TC_BLOCK_M);
     if (rc) return rc;
     const size_t wsmem = (size_t)W8_WARPS * (s.dp8 + 8) * sizeof(float);
+    const CUtensorMap &xmap = (cg == 2 ? s.store_map_half : s.store_map)->map;
     static bool attr = false;
     if (!attr) {
-        PR_CUDA(cudaFuncSetAttribute(tc8_scan_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)i8_smem_bytes()));
-        PR_CUDA(cudaFuncSetAttribute(tc8_scan_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)i8_smem_bytes()));
         PR_CUDA(cudaFuncSetAttribute(tc8_seed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024));
         PR_CUDA(cudaFuncSetAttribute(tc8_post_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024));
         attr = true;
@@ -957,11 +1199,9 @@ int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats)
         seed_n = cv.take<int32_t>((size_t)s.nq);
         I8ScanParams pp{s.n, s.dp128 / I8_BLOCK_K, psplit, (int)ceil_div<int64_t>(ptiles, psplit), (int)ptiles,
                         (int)qtiles, s.k, s.rows8.xs, s.rows8.xe, s.rows8.xt, qmeta, s.row_limit, s.nq, lg, acount,
-                        abuf, cap, floor_thr, 0, I8_PILOT_STRIDE, pcand};
-        ::pr::count_launch();
-        tc8_scan_kernel<true><<<(unsigned)(qtiles * psplit), I8_THREADS, i8_smem_bytes(), st>>>(
-            qmap.map, s.store_map->map, pp);
-        PR_LAUNCH_CHECK();
+                        abuf, cap, floor_thr, 0, I8_PILOT_STRIDE, pcand, s.x32, s.qp, s.dp8, s.d, 0};
+        rc = launch_scan8_cg<true>(cg, qtiles * psplit, qmap.map, xmap, pp, st);
+        if (rc) return rc;
         I8SeedArgs sa{pcand, psplit, s.nq, s.k, s.x32, s.dp8, s.d, s.qp, seed_rows, seed_s, seed_n, lg};
         ::pr::count_launch();
         tc8_seed_kernel<<<wgrid, W8_WARPS * 32, wsmem, st>>>(sa);
@@ -969,14 +1209,15 @@ int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats)
     }
     // 2) main scan: append every row whose upper bound reaches the running bound
     I8ScanParams p{s.n, s.dp128 / I8_BLOCK_K, nsplit, tps, (int)ntiles, (int)qtiles, s.k, s.rows8.xs, s.rows8.xe,
-                   s.rows8.xt, qmeta, s.row_limit, s.nq, lg, acount, abuf, cap, floor_thr, 0, 1, nullptr};
+                   s.rows8.xt, qmeta, s.row_limit, s.nq, lg, acount, abuf, cap, floor_thr, 0, 1, nullptr, s.x32, s.qp,
+                   s.dp8, s.d, 1};
+    const char *ref_env = getenv("PR_I8_REFINE");  // 0: no in-kernel refinement (A/B knob)
+    p.refine = !(ref_env && ref_env[0] == '0');
     const char *noepi_env = getenv("PR_I8_NOEPI");  // 1: epilogue does nothing (results invalid): MMA/TMA timing
     if (noepi_env && noepi_env[0] == '1') p.noepi = 1;
-    ::pr::count_launch();
     if (s.ev_begin) PR_CUDA(cudaEventRecord(s.ev_begin, st));
-    tc8_scan_kernel<false><<<(unsigned)(qtiles * nsplit), I8_THREADS, i8_smem_bytes(), st>>>(qmap.map,
-                                                                                           s.store_map->map, p);
-    PR_LAUNCH_CHECK();
+    rc = launch_scan8_cg<false>(cg, qtiles * nsplit, qmap.map, xmap, p, st);
+    if (rc) return rc;
     if (s.ev_end) PR_CUDA(cudaEventRecord(s.ev_end, st));
     // 3) exact rescoring of the complete candidate set
     I8PostArgs pa{acount, abuf, cap, s.nq, s.k, std::min<int64_t>(s.k, s.n), s.row_limit, s.x32, s.dp8, s.d, s.qp,
