@@ -484,7 +484,7 @@ struct pr_index {
     pr_search_stats stats{};
     // device scratch (grown on demand, stream-ordered)
     void *scratch = nullptr;
-    size_t scratch_bytes = 0;
+    size_t scratch_bytes = 0, scratch_peak = 0;
     int32_t *d_counters = nullptr;  // [4]: fallback count, candidate count, ...
     cudaStream_t last_stream = nullptr;
     // optional per-launch timing of the dominant scan kernel (bench roofline)
@@ -496,12 +496,26 @@ namespace pr {
 
 static int ensure_scratch(pr_index *h, size_t bytes, cudaStream_t st) {
     if (h->scratch_bytes >= bytes) return PR_OK;
+    static bool pool_kept = false;
+    if (!pool_kept) {
+        // keep freed scratch in the stream-ordered pool: a growing store (semantic
+        // cache, AKM) would otherwise unmap and re-map it at every synchronisation
+        int dev = 0;
+        cudaMemPool_t pool;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        pool_kept = true;
+    }
     if (h->scratch) PR_CUDA(cudaFreeAsync(h->scratch, st));
     h->scratch = nullptr;
     h->scratch_bytes = 0;
-    size_t b = std::max(bytes, (size_t)(1 << 20));
+    // geometric growth: a store that grows every batch reallocates O(log n) times
+    size_t b = std::max({bytes, (size_t)(1 << 20), h->scratch_peak + h->scratch_peak / 2});
     PR_CUDA(cudaMallocAsync(&h->scratch, b, st));
     h->scratch_bytes = b;
+    h->scratch_peak = b;
     return PR_OK;
 }
 

@@ -55,7 +55,7 @@ constexpr int I8_B_BYTES = TC_BLOCK_N * I8_BLOCK_K;  // 32 KB
 constexpr int I8_META_BYTES = TC_BLOCK_N * 4 * 2 + (int)sizeof(I8TileMeta);  // s_r[256], dx_r[256], tile bounds
 constexpr int I8_TMEM_COLS = 512;
 constexpr int I8_CAP = 32768;              // appended candidates per query before the exact fallback
-constexpr size_t I8_BUF_BYTES = 3ull << 30;  // ... unless the batch's buffers would exceed this
+
 // ||qq||_2, ||xq||_2 <= I8_KMAX, so |acc| <= I8_KMAX^2 < 2^22 and the int32 -> fp32
 // conversion is exact with one integer add + one fp32 subtract (no XU-pipe I2F)
 constexpr double I8_KMAX = 2047.0;
@@ -1075,14 +1075,17 @@ int i8_make_store_map(TcStoreMap *m, const int8_t *x8, int64_t rows, int dp128, 
     return make_map_2d(&m->map, x8, rows, dp128, 1, I8_BLOCK_K, box_rows);
 }
 
+// appended rows kept per query (a query that overflows is rescanned exactly):
+// min(32768, n), shrunk only when the batch's buffer would pass 1 GB
 static int i8_cap(int64_t n, int64_t nq) {
-    int64_t cap = std::min<int64_t>(I8_CAP, (int64_t)(I8_BUF_BYTES / 8 / (size_t)std::max<int64_t>(nq, 1)));
-    cap = std::max<int64_t>(cap, 2048);
-    return (int)std::min<int64_t>(cap, round_up<int64_t>(std::max<int64_t>(n, 1), 256));
+    int64_t cap = std::min<int64_t>(I8_CAP, round_up<int64_t>(std::max<int64_t>(n, 1), 256));
+    const int64_t budget = (int64_t)1 << 30;
+    if (cap * 8 * std::max<int64_t>(nq, 1) > budget) cap = std::max<int64_t>(4096, budget / (8 * std::max<int64_t>(nq, 1)));
+    return (int)cap;
 }
 
 // pilot: every I8_PILOT_STRIDE-th 256-row tile (~3% of the scan) when the store has
-// at least I8_PILOT_MIN_TILES tiles
+// at least 8 * I8_PILOT_STRIDE tiles
 static int pilot_stride() {
     static int v = -1;
     if (v < 0) {

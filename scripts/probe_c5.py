@@ -37,5 +37,35 @@ def main():
           "queries", st.queries, "wall", round(time.time() - t0, 1))
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and not os.environ.get("KB_REPEAT"):
     main()
+
+
+def kb_repeat(reps=12):
+    """Repeated identical KB searches on C5-style (HashEmbedder) queries."""
+    import numpy as np
+
+    from benchlib import configs as C
+    from benchlib.workloads import qa_rows, session_stream
+    from paper_2506_21593_b200 import HashEmbedder
+
+    n = int(os.environ.get("N", "10000000"))
+    store = make_store(n, 1024)
+    C.c5_routed(store, n, n_sessions=1, queries_per_session=4096)  # turns the store into the C5 KB
+    emb = HashEmbedder()
+    rows = qa_rows(120_000, seed=42)
+    _, st = session_stream([r["question"] for r in rows], 4096, 5, 0)
+    V = torch.from_numpy(np.stack([emb.embed(t).values for t, _ in st[:2048]])).cuda()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for i in range(reps):
+        s.record()
+        store.search_batch(V, 10, validate=False, count=False)
+        e.record()
+        torch.cuda.synchronize()
+        stt = store.stats()
+        print(f"rep {i}: {s.elapsed_time(e):.2f} ms appended={stt.appended} rescored={stt.candidates} "
+              f"fallback={stt.fallback}", flush=True)
+
+
+if __name__ == "__main__" and os.environ.get("KB_REPEAT"):
+    kb_repeat()
