@@ -94,3 +94,26 @@ def test_product_path_refuses_without_gpu():
 
     with pytest.raises(DeviceUnavailable):
         FlatIndex(dim=8)
+
+
+def test_search_stats_layout_matches_header():
+    """ctypes SearchStats mirrors pr_search_stats field by field (names, order, widths)."""
+    from paper_2506_21593_b200 import _lib
+
+    with open(os.path.join(ROOT, "include", "pentarag.h")) as fh:
+        text = fh.read()
+    body = re.search(r"typedef struct pr_search_stats \{(.*?)\} pr_search_stats;", text, re.S).group(1)
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    fields = re.findall(r"(int64_t|int32_t)\s+(\w+);", body)
+    width = {"int64_t": ctypes.c_int64, "int32_t": ctypes.c_int32}
+    assert [(n, width[t]) for t, n in fields] == list(_lib.SearchStats._fields_)
+
+
+def test_search_modes_match_header():
+    from paper_2506_21593_b200 import _lib
+
+    with open(os.path.join(ROOT, "include", "pentarag.h")) as fh:
+        text = fh.read()
+    modes = dict((m, int(v)) for m, v in re.findall(r"#define (PR_SEARCH_\w+) (\d+)", text))
+    assert modes == {k: getattr(_lib, k) for k in modes}
+    assert set(modes) == {"PR_SEARCH_AUTO", "PR_SEARCH_EXACT", "PR_SEARCH_TENSOR", "PR_SEARCH_TENSOR_I8"}
