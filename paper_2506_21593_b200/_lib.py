@@ -13,7 +13,8 @@ import threading
 from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpentarag.so")
+# PR_LIB overrides the in-tree library (measurement builds only)
+LIB_PATH = os.environ.get("PR_LIB") or os.path.join(_HERE, "libpentarag.so")
 
 _lib = None
 _lock = threading.Lock()

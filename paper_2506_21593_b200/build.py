@@ -25,6 +25,7 @@ NVCC_FLAGS = [
     "--expt-relaxed-constexpr",
     "-Xcompiler", "-fPIC",
     "-Xptxas", "-v",
+    *([f"-DPR_MBAR_SUSPEND_NS={os.environ['PR_MBAR_SUSPEND_NS']}u"] if os.environ.get("PR_MBAR_SUSPEND_NS") else []),
 ]
 
 

@@ -22,6 +22,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+#ifndef PR_MBAR_SUSPEND_NS
+#define PR_MBAR_SUSPEND_NS 1000u  // 1 us: longer hints oversleep on missed wake-ups (10 ms cost ~1 s per C5 run)
+#endif
 // try_wait with a suspend-time hint: a waiting warp sleeps until the phase
 // completes (or the hint expires) instead of spinning on issue slots that the
 // epilogue warps of the same SM sub-partition need
@@ -33,7 +36,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
             "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
             "selp.u32 %0, 1, 0, p;\n\t}"
             : "=r"(done)
-            : "r"(smem_u32(bar)), "r"(parity), "r"(0x989680u)
+            : "r"(smem_u32(bar)), "r"(parity), "r"(PR_MBAR_SUSPEND_NS)
             : "memory");
     } while (!done);
 }

@@ -30,6 +30,7 @@ def main():
     store = make_store(n, 1024)
     t0 = time.time()
     r = C.c5_routed(store, n, n_sessions=int(os.environ.get("S", "1")), queries_per_session=int(os.environ.get("Q", "12288")),
+                    batch=int(os.environ.get("B", "4096")),
                     profile=True)
     print({k: v for k, v in r.items() if k in ("value", "layer_counts", "stage_seconds", "parity")})
     st = store.stats()
