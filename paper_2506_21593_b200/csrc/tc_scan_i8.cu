@@ -1155,8 +1155,11 @@ int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats)
     const int64_t nq_pad = round_up<int64_t>(s.nq, cg * TC_BLOCK_M);
     const int64_t qtiles = nq_pad / TC_BLOCK_M;
     const int64_t ntiles = ceil_div<int64_t>(s.n, TC_BLOCK_N);
-    const int nsplit = choose_nsplit_waves(qtiles, ntiles);
+    int nsplit = choose_nsplit_waves(qtiles, ntiles);
+    const char *ns_env = getenv("PR_I8_NSPLIT");  // measurement knob
+    if (ns_env && atoi(ns_env) > 0) nsplit = (int)std::min<int64_t>(ntiles, atoi(ns_env));
     const int tps = (int)ceil_div<int64_t>(ntiles, nsplit);
+    nsplit = (int)ceil_div<int64_t>(ntiles, tps);
     const int cap = i8_cap(s.n, s.nq);
     int8_t *q8 = cv.take<int8_t>((size_t)nq_pad * s.dp128);
     float4 *qmeta = cv.take<float4>((size_t)nq_pad);
