@@ -450,7 +450,8 @@ def main():
                     configs["c3_fixed_kv"] = C.c3_kv(float(pk.get("hbm_gbs", 6538.6)), n_keys=a.kv_keys)
                 elif name == "c5":
                     configs["c5_routed"] = C.c5_routed(idx, a.n, n_sessions=a.c5_sessions,
-                                                       queries_per_session=a.c5_queries)
+                                                       queries_per_session=a.c5_queries,
+                                                       profile=bool(os.environ.get("BENCH_C5_PROFILE")))
             except Exception as exc:  # noqa: BLE001 - recorded, the headline stands
                 configs[name] = {"error": f"{type(exc).__name__}: {exc}",
                                  "trace": traceback.format_exc()[-1500:]}

@@ -40,7 +40,8 @@ extern "C" {
 #define PR_ERR_UNSUPPORTED (-6)    /* not built for / not running on sm_100a */
 
 /* ---- search modes ------------------------------------------------------ */
-#define PR_SEARCH_AUTO 0   /* int8 tensor-core scan when it pays (fp16 for dim > 2048), else exact */
+#define PR_SEARCH_AUTO 0   /* int8 tensor-core scan for stores >= 512k rows (dim <= 2048), fp16 tensor-core
+                              scan for smaller stores that still pay for a scan, else exact */
 #define PR_SEARCH_EXACT 1  /* fp64 einsum-order scan of every row          */
 #define PR_SEARCH_TENSOR 2 /* tcgen05 fp16 scan + certified fp64 rescoring */
 #define PR_SEARCH_TENSOR_I8 3 /* tcgen05 int8 scan with per-row error bounds + fp64 rescoring of the

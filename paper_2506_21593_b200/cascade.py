@@ -405,6 +405,9 @@ class _Prof:
         self.times[f"{name}.fallback"] = self.times.get(f"{name}.fallback", 0) + st.fallback
         self.times[f"{name}.collected"] = self.times.get(f"{name}.collected", 0) + st.collected
         self.times[f"{name}.tensor_path"] = self.times.get(f"{name}.tensor_path", 0) + (st.path == 2)
+        self.times[f"{name}.i8_path"] = self.times.get(f"{name}.i8_path", 0) + (st.path == 3)
+        self.times[f"{name}.appended"] = self.times.get(f"{name}.appended", 0) + st.appended
+        self.times[f"{name}.rescored"] = self.times.get(f"{name}.rescored", 0) + st.candidates
 
     def mark(self, name: str) -> None:
         if not self.enabled:
