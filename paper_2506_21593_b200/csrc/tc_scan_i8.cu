@@ -125,8 +125,11 @@ __device__ __forceinline__ uint32_t mapa_u32(uint32_t saddr, uint32_t rank) {
 __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// arrive on a (possibly remote) barrier of the cluster; default .release.cta semantics as
+// CUTLASS's ClusterBarrier::arrive — the TMEM reads it orders are covered by
+// tcgen05.fence::before_thread_sync, so no cluster-scope fence (ERRBAR) is needed
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 // 2-CTA TMA tile load: data lands in this CTA's smem, bytes are counted on the
 // leader CTA's barrier (cluster address)
@@ -184,16 +187,24 @@ struct I8ScanParams {
 // loose per-tile test in the scaled domain: a row can pass u = t s acc + A dx + C >= thr
 // only if s * acc >= (thr - C - A dxmax) / t.  1e-6 (score units) absorbs every fp32
 // rounding of either side.
-__device__ __forceinline__ float loose_threshold(float thr, float t, float A, float C, float dxmax) {
-    if (thr == -INFINITY || t <= 0.f) return -INFINITY;
+// inv = {rd(1/t), ru(1/t)}: lhs / t is bounded below by rd(lhs * rd(1/t)) for lhs >= 0
+// and by rd(lhs * ru(1/t)) for lhs < 0 (t > 0) — one FMUL, no division subroutine
+__device__ __forceinline__ float2 inv_bounds(float t) {
+    return t > 0.f ? make_float2(__frcp_rd(t), __frcp_ru(t)) : make_float2(0.f, 0.f);
+}
+__device__ __forceinline__ float div_down(float lhs, float2 inv) {
+    return __fmul_rd(lhs, lhs >= 0.f ? inv.x : inv.y);
+}
+__device__ __forceinline__ float loose_threshold(float thr, float2 inv, float A, float C, float dxmax) {
+    if (thr == -INFINITY || inv.x <= 0.f) return -INFINITY;
     const float lhs = __fsub_rn(__fsub_rn(thr, __fmaf_ru(A, dxmax, C)), 1e-6f);
-    return __fdiv_rd(lhs, t);
+    return div_down(lhs, inv);
 }
 
 // pilot: l = ap - A dx - C > thr needs ap > thr + C
-__device__ __forceinline__ float loose_pilot(float thr, float t, float C) {
-    if (thr == -INFINITY || t <= 0.f) return -INFINITY;
-    return __fdiv_rd(__fsub_rn(__fadd_rn(thr, C), 1e-6f), t);
+__device__ __forceinline__ float loose_pilot(float thr, float2 inv, float C) {
+    if (thr == -INFINITY || inv.x <= 0.f) return -INFINITY;
+    return div_down(__fsub_rn(__fadd_rn(thr, C), 1e-6f), inv);
 }
 
 // relaxed gpu-scope load: the value is only consumed a tile later, so its
@@ -399,6 +410,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
             }
             uint32_t *lgq = p.lg + (valid ? q : 0);
             uint32_t lg_next = valid ? ld_relaxed(lgq) : 0u;
+            const float2 inv = inv_bounds(tq_);
             // running top-k of l: the first TC_KP - k slots hold +inf sentinels that no
             // insert displaces, so ts[TC_KP - 1] is always the k-th largest l seen
             float ts[TC_KP];
@@ -434,7 +446,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
                 // main: append rows with u >= thr; pilot: insert rows with l > thr
                 float thr = fmaxf(fmaxf(ts[TC_KP - 1], p.thr_floor), ord2f(lg_next));
                 if (valid) lg_next = ld_relaxed(lgq);  // for the next tile
-                float thr2 = PILOT ? loose_pilot(thr, tq_, C) : loose_threshold(thr, tq_, A, C, dxmax);
+                float thr2 = PILOT ? loose_pilot(thr, inv, C) : loose_threshold(thr, inv, A, C, dxmax);
                 const int64_t rbase = (int64_t)(t0 + i) * p.tile_stride * TC_BLOCK_N;
                 const uint32_t taddr = tmem + ((uint32_t)(ew * 32) << 16) + acc * TC_BLOCK_N;
                 uint32_t va[32], vb[32];
@@ -544,7 +556,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
                                         topk_insert(ts, tr, lv, rv);
                                         if (ts[TC_KP - 1] > thr) {
                                             thr = ts[TC_KP - 1];
-                                            thr2 = PILOT ? loose_pilot(thr, tq_, C) : loose_threshold(thr, tq_, A, C, dxmax);
+                                            thr2 = PILOT ? loose_pilot(thr, inv, C) : loose_threshold(thr, inv, A, C, dxmax);
                                         }
                                     }
                                 }
@@ -599,7 +611,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
                     for (int i = lane; i < I8_RQ; i += 32) any |= *reinterpret_cast<volatile uint64_t *>(&rq[i]) != 0;
                     if (!__any_sync(0xffffffffu, any)) break;
                 }
-                __nanosleep(500);
+                __nanosleep(2000);  // jobs are rare: do not spin on the epilogue warps' issue slots
                 continue;
             }
             const int64_t qg = job ? (int64_t)(job >> 32) - 1 : 0;
