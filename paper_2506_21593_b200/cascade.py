@@ -45,6 +45,7 @@ from .caches import CacheEntry, FixedKVCache, SemanticCache, encode_texts
 from .index import MODE_AUTO, FlatIndex
 from .knowledge import AdaptiveKnowledgeMemory
 from .records import AnswerRecord, LayerTag
+from .errors import CascadeError
 from .ledger import BatchLedger, LedgerEntry, entry_text_conf
 from .router import LayerProbe
 
@@ -67,16 +68,31 @@ def batchable(router) -> bool:
     )
 
 
-def route_batch(router, queries, vectors=None, *, mode: int = MODE_AUTO, materialize: bool = True):
+def route_batch(router, queries, vectors=None, *, mode: int = MODE_AUTO, materialize: bool = True,
+                capture_errors: bool = False):
     """Route ``queries`` in order; see the module docstring.  Returns the list
     of (AnswerRecord, RouteTraceEvent), or with ``materialize=False`` a
-    ``RoutedBatch`` of columnar segments (objects built only on access)."""
+    ``RoutedBatch`` of columnar segments (objects built only on access).
+
+    ``capture_errors``: a query whose ``route`` raises a CascadeError (e.g.
+    AllLayersMissed, router.py:309-323 — no write-back happens for it) gets the
+    exception object as its result and the batch continues, exactly like
+    independent ``route`` calls would (service micro-batching)."""
     segs = []
     i, n = 0, len(queries)
     stats = {"batched": 0, "sequential": 0, "splits": 0}
+
+    def one(q):
+        if not capture_errors:
+            return router.route(q)
+        try:
+            return router.route(q)
+        except CascadeError as exc:
+            return exc
+
     while i < n:
         if not batchable(router):
-            segs.append([router.route(queries[i])])
+            segs.append([one(queries[i])])
             stats["sequential"] += 1
             i += 1
             continue
@@ -89,7 +105,7 @@ def route_batch(router, queries, vectors=None, *, mode: int = MODE_AUTO, materia
         i += done
         if done < remaining:
             # the next query's AKM outcome is not certain in batch: route it exactly
-            segs.append([router.route(queries[i])])
+            segs.append([one(queries[i])])
             stats["sequential"] += 1
             stats["splits"] += 1
             i += 1

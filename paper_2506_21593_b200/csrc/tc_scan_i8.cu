@@ -1099,12 +1099,8 @@ static int i8_cap(int64_t n, int64_t nq) {
 // pilot: every I8_PILOT_STRIDE-th 256-row tile (~3% of the scan) when the store has
 // at least 8 * I8_PILOT_STRIDE tiles
 static int pilot_stride() {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("PR_I8_PILOT_STRIDE");  // measurement knob
-        v = e ? std::max(2, atoi(e)) : 32;
-    }
-    return v;
+    const char *e = getenv("PR_I8_PILOT_STRIDE");  // measurement knob (read per search)
+    return e ? std::max(2, atoi(e)) : 32;
 }
 #define I8_PILOT_STRIDE pilot_stride()
 

@@ -17,6 +17,11 @@ Fixtures:
                    probes, serving layer, answer text, supporting passages,
                    and the final store counters
   simulation.json  run_simulation(2 sessions x 150 queries) session logs
+  snapshot.json    FlatIndex.snapshot bytes (RCFLATIX, index.py:198-220) of an index
+                   with upserts + payloads, restore() results (index.py:222-261) for
+                   it and for crafted duplicate-id / invalid-vector / corrupt blobs
+
+    python tests/golden/make_golden.py snapshot   # regenerate snapshot.json only
 """
 from __future__ import annotations
 
@@ -176,6 +181,70 @@ def simulation_logs():
             "sessions": [list(log.to_jsonl_lines()) for log in logs]}
 
 
+def snapshot_cases():
+    import base64
+    import struct
+    import zlib
+
+    rng = np.random.default_rng(77)
+    d = 16
+    idx = rc.FlatIndex(dim=d)
+    X = unit(rng, 30, d)
+    for i in range(30):
+        idx.insert(f"doc-{i:03d}", X[i], {"n": i, "tag": "π" if i % 7 == 0 else "x"})
+    # upserts keep their row: new vector + payload for two existing ids
+    idx.insert("doc-004", X[20], {"n": 4, "tag": "upsert"})
+    idx.insert("doc-011", unit(rng, 1, d)[0], None)
+    Q = unit(rng, 4, d)
+    Q[1] = X[20]
+    snap = idx.snapshot()
+    restored = rc.FlatIndex.restore(snap)
+
+    def hits(ix):
+        return [[(h.entry_id, h.score, h.rank) for h in ix.search(q, 5)] for q in Q]
+
+    out = {"dim": d, "snapshot_b64": base64.b64encode(snap).decode(), "queries": Q.tolist(),
+           "hits": hits(idx), "restored_hits": hits(restored),
+           "restored_ids": list(restored.entry_ids()),
+           "restored_payloads": [restored.payload(e) for e in restored.entry_ids()]}
+    assert out["hits"] == out["restored_hits"]
+    assert restored.snapshot() == snap
+
+    header = struct.Struct("<8sIIQQI")
+
+    def blob(vecs, recs, magic=b"RCFLATIX", version=1, crc_fix=0):
+        meta = ("\n".join(json.dumps(r, ensure_ascii=False) for r in recs) + "\n").encode()
+        body = np.asarray(vecs, dtype=np.float32).tobytes() + meta
+        return header.pack(magic, version, d, len(recs), len(meta), zlib.crc32(body) ^ crc_fix) + body
+
+    # duplicate id inside a snapshot: restore() upserts (the row stays, the last write wins)
+    V = unit(rng, 6, d)
+    recs = [{"id": f"k{i}", "payload": i} for i in range(6)]
+    recs[4] = {"id": "k1", "payload": "second"}
+    dup = blob(V, recs)
+    rdup = rc.FlatIndex.restore(dup)
+    out["dup_b64"] = base64.b64encode(dup).decode()
+    out["dup_ids"] = list(rdup.entry_ids())
+    out["dup_payloads"] = [rdup.payload(e) for e in rdup.entry_ids()]
+    out["dup_hits"] = [[(h.entry_id, h.score, h.rank) for h in rdup.search(q, 6)] for q in V[:3]]
+    out["dup_snapshot_b64"] = base64.b64encode(rdup.snapshot()).decode()
+    # failures
+    bad = {"bad_magic": blob(V, recs, magic=b"RCFLATIY"), "bad_version": blob(V, recs, version=2),
+           "bad_crc": blob(V, recs, crc_fix=1), "short": dup[:20]}
+    Vb = V.copy()
+    Vb[2] *= 2.0
+    bad["not_unit"] = blob(Vb, [{"id": f"k{i}", "payload": i} for i in range(6)])
+    out["bad"] = {}
+    for name, b in bad.items():
+        try:
+            rc.FlatIndex.restore(b)
+            err = None
+        except Exception as exc:  # noqa: BLE001
+            err = type(exc).__name__
+        out["bad"][name] = {"b64": base64.b64encode(b).decode(), "error": err}
+    return out
+
+
 def main():
     meta = {"flat_index_cases": flat_index_cases(), "numpy": np.__version__}
     with open(os.path.join(HERE, "flat_index.json"), "w") as fh:
@@ -192,4 +261,8 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["snapshot"]:
+        with open(os.path.join(HERE, "snapshot.json"), "w") as fh:
+            json.dump(snapshot_cases(), fh, indent=1, ensure_ascii=False)
+    else:
+        main()
