@@ -31,6 +31,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <climits>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -182,6 +183,11 @@ struct I8ScanParams {
     const float *qp;
     int dp8, d;
     int refine;  // hand rows at the bound to the exact refiner warps
+    // L2 lockstep: the SM pairs scanning one split read the same store tiles; a pair
+    // more than `window` tiles ahead of the slowest started pair of its split waits,
+    // so each tile is still in L2 when the others read it (0 = off)
+    int32_t *prog;  // [nsplit][qgroups]: tiles loaded + 1 (0 = not started, INT_MAX = done)
+    int window;
 };
 
 // loose per-tile test in the scaled domain: a row can pass u = t s acc + A dx + C >= thr
@@ -316,7 +322,25 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
             for (int item = item0; item < nitems; item += istride) {
                 int qtile, split, t0, nloc;
                 item_of(item, qtile, split, t0, nloc);
+                int32_t *myprog = nullptr, *splitprog = nullptr;
+                if (!PILOT && p.window > 0 && rank == 0) {
+                    splitprog = p.prog + (int64_t)split * qgroups;
+                    myprog = splitprog + item % qgroups;
+                }
                 for (int i = 0; i < nloc; ++i, ++tix) {
+                    if (myprog && (i & 7) == 0) {
+                        asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(myprog), "r"(i + 1) : "memory");
+                        for (;;) {  // wait while more than `window` tiles ahead of the slowest started pair
+                            int lo = INT_MAX;
+                            for (int g = 0; g < qgroups; ++g) {
+                                int v;
+                                asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(splitprog + g) : "memory");
+                                if (v > 0) lo = min(lo, v);
+                            }
+                            if (lo == INT_MAX || i + 1 - lo <= p.window) break;
+                            __nanosleep(1000);
+                        }
+                    }
                     const int t = (t0 + i) * p.tile_stride;
                     const int acc = tix & 1;
                     const uint32_t aphase = (tix >> 1) & 1;
@@ -343,6 +367,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
                 }
+                if (myprog) asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(myprog), "r"(INT_MAX) : "memory");
             }
         }
     } else if (warp == 1) {
@@ -1155,7 +1180,7 @@ size_t tc8_scratch_bytes(int64_t nq, int dp128, int64_t n) {
     const int ps = pilot_splits(qtiles, ntiles);
     return (size_t)nq_pad * dp128 + (size_t)nq_pad * 16 + (size_t)nq * (4 + 4 + 4 + 4) +
            (size_t)nq * i8_cap(n, nq) * 8 + (size_t)nq * ps * I8_HALVES * TC_KP * 8 + (size_t)nq * TC_KP * 12 +
-           65536;
+           (size_t)qtiles * 4 * 1024 + 65536;
 }
 
 int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats) {
@@ -1213,7 +1238,7 @@ int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats)
         seed_n = cv.take<int32_t>((size_t)s.nq);
         I8ScanParams pp{s.n, s.dp128 / I8_BLOCK_K, psplit, (int)ceil_div<int64_t>(ptiles, psplit), (int)ptiles,
                         (int)qtiles, s.k, s.rows8.xs, s.rows8.xe, s.rows8.xt, qmeta, s.row_limit, s.nq, lg, acount,
-                        abuf, cap, floor_thr, 0, I8_PILOT_STRIDE, pcand, s.x32, s.qp, s.dp8, s.d, 0};
+                        abuf, cap, floor_thr, 0, I8_PILOT_STRIDE, pcand, s.x32, s.qp, s.dp8, s.d, 0, nullptr, 0};
         rc = launch_scan8_cg<true>(cg, qtiles * psplit, qmap.map, xmap, pp, st);
         if (rc) return rc;
         I8SeedArgs sa{pcand, psplit, s.nq, s.k, s.x32, s.dp8, s.d, s.qp, seed_rows, seed_s, seed_n, lg};
@@ -1224,7 +1249,17 @@ int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats)
     // 2) main scan: append every row whose upper bound reaches the running bound
     I8ScanParams p{s.n, s.dp128 / I8_BLOCK_K, nsplit, tps, (int)ntiles, (int)qtiles, s.k, s.rows8.xs, s.rows8.xe,
                    s.rows8.xt, qmeta, s.row_limit, s.nq, lg, acount, abuf, cap, floor_thr, 0, 1, nullptr, s.x32, s.qp,
-                   s.dp8, s.d, 1};
+                   s.dp8, s.d, 1, nullptr, 0};
+    {
+        const char *w_env = getenv("PR_I8_WINDOW");  // tiles a pair may run ahead of its split (0 = off)
+        p.window = w_env ? atoi(w_env) : 0;  // measured: 48 tiles halves DRAM reads but costs 50 % time
+        if (cg == 2 && p.window > 0) {
+            p.prog = cv.take<int32_t>((size_t)nsplit * (qtiles / 2));
+            PR_CUDA(cudaMemsetAsync(p.prog, 0, (size_t)nsplit * (qtiles / 2) * sizeof(int32_t), st));
+        } else {
+            p.window = 0;
+        }
+    }
     const char *ref_env = getenv("PR_I8_REFINE");  // 0: no in-kernel refinement (A/B knob)
     p.refine = !(ref_env && ref_env[0] == '0');
     const char *noepi_env = getenv("PR_I8_NOEPI");  // 1: epilogue does nothing (results invalid): MMA/TMA timing
