@@ -227,3 +227,33 @@ def test_i8_pilot_one_hot(gpu, rng):
     idx = FlatIndex(dim=d)
     idx.extend_arrays([f"e{i}" for i in range(n)], X)
     _check(idx, X, Q, 10, _mode())
+
+
+@pytest.mark.parametrize("d", [1536, 2048])
+def test_i8_wide_rows(gpu, rng, d):
+    from paper_2506_21593_b200 import FlatIndex
+
+    n = 9000
+    X = _store(rng, n, d)
+    Q = random_unit_vectors(rng, 70, d)
+    Q[0] = X[1]
+    idx = FlatIndex(dim=d)
+    idx.extend_arrays([f"e{i}" for i in range(n)], X)
+    _check(idx, X, Q, 7, _mode())
+    assert idx.stats().path == _mode()
+
+
+@pytest.mark.parametrize("n,nq", [(1, 1), (5, 3), (255, 1), (257, 129), (3000, 257)])
+def test_i8_tiny_stores_and_odd_batches(gpu, rng, n, nq):
+    """Stores smaller than one 256-row tile, one query, and query counts that are not
+    a multiple of the 256-query SM-pair tile."""
+    from paper_2506_21593_b200 import FlatIndex
+
+    d = 64
+    X = random_unit_vectors(rng, n, d)
+    Q = random_unit_vectors(rng, nq, d)
+    Q[0] = X[n // 2]
+    idx = FlatIndex(dim=d)
+    idx.extend_arrays([f"e{i}" for i in range(n)], X)
+    for k in (1, 5, 16):
+        _check(idx, X, Q, k, _mode())
