@@ -621,7 +621,14 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
         // ---------------- exact refiner: score handed-over rows in fp64 einsum order ----------------
         // warp 2 owns even local queries, warp 3 odd ones (each list has a single writer)
         const uint32_t par = (uint32_t)(warp - 2);
+        uint32_t seen = 0;  // pushes observed so far: an idle poll is one shared load
         for (;;) {
+            const uint32_t tail = *reinterpret_cast<volatile uint32_t *>(rq_tail);
+            const bool done = *reinterpret_cast<volatile uint32_t *>(epi_done) == I8_EPI / 32;
+            if (tail == seen && !done) {
+                __nanosleep(2000);
+                continue;
+            }
             uint64_t job = 0;
             for (int i = lane; i < I8_RQ && !job; i += 32) {
                 const uint64_t v = *reinterpret_cast<volatile uint64_t *>(&rq[i]);
@@ -630,13 +637,13 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
             }
             const uint32_t has = __ballot_sync(0xffffffffu, job != 0);
             if (!has) {
-                if (*reinterpret_cast<volatile uint32_t *>(epi_done) == I8_EPI / 32) {
+                seen = tail;  // every job pushed before `tail` was read has been taken (by either warp)
+                if (done) {
                     // the epilogue finished (its pushes precede the count): drain once more, then stop
                     bool any = false;
                     for (int i = lane; i < I8_RQ; i += 32) any |= *reinterpret_cast<volatile uint64_t *>(&rq[i]) != 0;
                     if (!__any_sync(0xffffffffu, any)) break;
                 }
-                __nanosleep(2000);  // jobs are rare: do not spin on the epilogue warps' issue slots
                 continue;
             }
             const int64_t qg = job ? (int64_t)(job >> 32) - 1 : 0;
