@@ -69,20 +69,29 @@ constexpr uint32_t I8_IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(T
 
 // CG = CTAs per MMA (tcgen05 cta_group): with 2, an SM pair computes a 256-query x
 // 256-row tile; each CTA stages its own 128 queries and HALF of the 256 store rows
-template <int CG>
+// ARES (CG == 2, dp128 <= 1024): each CTA's 128-query A tile stays resident in smem for
+// the whole item, so per store tile only its half of B streams in (32 instead of 64
+// B/clk of TMA ingress per SM at the int8 MMA rate)
+constexpr int I8_ARES_BYTES = TC_BLOCK_M * 1024;  // 128 queries x up to 1024 int8 columns
+template <int CG, bool ARES = false>
 struct I8Cfg {
-    static constexpr int STAGES = CG == 2 ? I8_STAGES2 : I8_STAGES;
+    static constexpr int STAGES = ARES ? 4 : (CG == 2 ? I8_STAGES2 : I8_STAGES);
     static constexpr int B_ROWS = TC_BLOCK_N / CG;
     static constexpr int B_BYTES = B_ROWS * I8_BLOCK_K;
+    static constexpr int A_STAGE_BYTES = ARES ? 0 : I8_A_BYTES;
+    static constexpr int A_RES_BYTES = ARES ? I8_ARES_BYTES : 0;
 };
 // in-kernel exact refiner (warps 2-3): job table + per-query exact lists
 constexpr int I8_RQ = 256;
-constexpr size_t I8_REFINER_BYTES = (size_t)I8_RQ * 8 + (size_t)TC_BLOCK_M * TC_KP * 8 + (size_t)TC_BLOCK_M * 8 + 64;
-template <int CG>
+constexpr size_t I8_REFINER_BYTES = (size_t)I8_RQ * 8 + (size_t)TC_BLOCK_M * TC_KP * 4 + (size_t)TC_BLOCK_M * 8 + 64;
+template <int CG, bool ARES = false>
 constexpr size_t i8_smem_bytes() {
-    return 1024 + (size_t)I8Cfg<CG>::STAGES * (I8_A_BYTES + I8Cfg<CG>::B_BYTES) + 2 * (size_t)I8_META_BYTES +
-           (size_t)32 * I8_EPI * 4 + 256 + I8_REFINER_BYTES;
+    using Cf = I8Cfg<CG, ARES>;
+    return 1024 + (size_t)Cf::A_RES_BYTES + (size_t)Cf::STAGES * (Cf::A_STAGE_BYTES + Cf::B_BYTES) +
+           2 * (size_t)I8_META_BYTES + (size_t)16 * I8_EPI * 4 + 256 + I8_REFINER_BYTES;
 }
+static_assert(i8_smem_bytes<2, true>() <= 232448, "A-resident 2-CTA scan exceeds the 227 KB smem limit");
+static_assert(i8_smem_bytes<2, false>() <= 232448, "2-CTA scan exceeds the 227 KB smem limit");
 
 __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accum) {
     asm volatile(
@@ -227,29 +236,35 @@ __device__ __forceinline__ int nth_set_bit(uint32_t m, int n) {
     return __ffs(m) - 1;
 }
 
-template <bool PILOT, int CG>
+template <bool PILOT, int CG, bool ARES>
 __global__ void __launch_bounds__(I8_THREADS, 1)
     tc8_scan_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tx, I8ScanParams p) {
-    constexpr int STAGES = I8Cfg<CG>::STAGES;
-    constexpr int B_BYTES = I8Cfg<CG>::B_BYTES;
+    static_assert(!ARES || CG == 2, "A-resident operands are a 2-CTA variant");
+    constexpr int STAGES = I8Cfg<CG, ARES>::STAGES;
+    constexpr int B_BYTES = I8Cfg<CG, ARES>::B_BYTES;
+    constexpr int A_STAGE = I8Cfg<CG, ARES>::A_STAGE_BYTES;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-B alignment for SWIZZLE_128B, as an offset from the __shared__ array so
     // every derived pointer stays in the shared window (LDS/STS, not generic LD/ST)
     uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    uint8_t *sA = smem;
-    uint8_t *sB = sA + STAGES * I8_A_BYTES;
+    uint8_t *sAres = smem;                                      // [nkb][16 KB] (ARES) resident A
+    uint8_t *sA = sAres + I8Cfg<CG, ARES>::A_RES_BYTES;         // [STAGES][16 KB] streamed A (!ARES)
+    uint8_t *sB = sA + STAGES * A_STAGE;
     uint8_t *smeta = sB + STAGES * B_BYTES;  // [2][I8_META_BYTES]
-    int32_t *spill = reinterpret_cast<int32_t *>(smeta + 2 * I8_META_BYTES);  // [32][I8_EPI]
-    uint64_t *full = reinterpret_cast<uint64_t *>(spill + 32 * I8_EPI);
+    int32_t *spill = reinterpret_cast<int32_t *>(smeta + 2 * I8_META_BYTES);  // [16][I8_EPI]
+    uint64_t *full = reinterpret_cast<uint64_t *>(spill + 16 * I8_EPI);
     uint64_t *empty = full + STAGES;
     uint64_t *tfull = empty + STAGES;
     uint64_t *tempty = tfull + 2;
     uint64_t *mfull = tempty + 2;
     uint64_t *mempty = mfull + 2;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(mempty + 2);
-    uint64_t *rq = reinterpret_cast<uint64_t *>(smem + (size_t)STAGES * (I8_A_BYTES + B_BYTES) + 2 * I8_META_BYTES +
-                                                32 * I8_EPI * 4 + 256);  // [I8_RQ] refiner jobs {q+1, row}
-    double *rel = reinterpret_cast<double *>(rq + I8_RQ);                // [128][TC_KP] exact lists
+    uint64_t *afull = mempty + 2;   // ARES: the item's A tile landed (leader's copy counts both CTAs)
+    uint64_t *aempty = afull + 1;   // ARES: the item's MMAs are done with A
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(aempty + 1);
+    uint64_t *rq = reinterpret_cast<uint64_t *>(smem + (size_t)I8Cfg<CG, ARES>::A_RES_BYTES +
+                                                (size_t)STAGES * (A_STAGE + B_BYTES) + 2 * I8_META_BYTES +
+                                                16 * I8_EPI * 4 + 256);  // [I8_RQ] refiner jobs {q+1, row}
+    float *rel = reinterpret_cast<float *>(rq + I8_RQ);  // [128][TC_KP] exact lists, rounded down
     int32_t *rown = reinterpret_cast<int32_t *>(rel + TC_BLOCK_M * TC_KP);  // [128] list owner (global q)
     int32_t *rcnt = rown + TC_BLOCK_M;                                    // [128] entries
     uint32_t *rq_tail = reinterpret_cast<uint32_t *>(rcnt + TC_BLOCK_M);
@@ -292,6 +307,8 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
             mbar_init(&mfull[a], 1);
             mbar_init(&mempty[a], I8_EPI / 32);
         }
+        mbar_init(afull, 1);
+        mbar_init(aempty, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 2) {
@@ -319,9 +336,19 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
             int stage = 0;
             uint32_t phase = 0;
             int tix = 0;
+            uint32_t apar = 0;
             for (int item = item0; item < nitems; item += istride) {
                 int qtile, split, t0, nloc;
                 item_of(item, qtile, split, t0, nloc);
+                if (ARES) {
+                    // the item's query tile, once: wait until the previous item's MMAs released it
+                    mbar_wait(aempty, apar ^ 1);
+                    if (rank == 0) mbar_expect_tx(afull, CG * p.nkb * I8_A_BYTES);
+                    const uint32_t fa = mapa_u32(smem_u32(afull), 0);
+                    for (int kb = 0; kb < p.nkb; ++kb)
+                        tma_load_2d_cg2(sAres + kb * I8_A_BYTES, &tq, fa, kb * I8_BLOCK_K, qtile * TC_BLOCK_M);
+                    apar ^= 1;
+                }
                 int32_t *myprog = nullptr, *splitprog = nullptr;
                 if (!PILOT && p.window > 0 && rank == 0) {
                     splitprog = p.prog + (int64_t)split * qgroups;
@@ -352,16 +379,22 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
                     bulk_load_1d(m + TC_BLOCK_N * 8, p.xt + t, sizeof(I8TileMeta), &mfull[acc]);
                     for (int kb = 0; kb < p.nkb; ++kb) {
                         mbar_wait(&empty[stage], phase ^ 1);
+                        if (p.noepi == 2) {  // measurement only: no operand traffic (MMAs read stale smem)
+                            if (rank == 0) mbar_arrive(&full[stage]);
+                            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                            continue;
+                        }
                         if (CG == 2) {
                             // the leader's barrier counts both CTAs' bytes; its producer posts the total
-                            if (rank == 0) mbar_expect_tx(&full[stage], CG * (I8_A_BYTES + B_BYTES));
+                            if (rank == 0) mbar_expect_tx(&full[stage], CG * (A_STAGE + B_BYTES));
                             const uint32_t fb = mapa_u32(smem_u32(&full[stage]), 0);
-                            tma_load_2d_cg2(sA + stage * I8_A_BYTES, &tq, fb, kb * I8_BLOCK_K, qtile * TC_BLOCK_M);
+                            if (!ARES)
+                                tma_load_2d_cg2(sA + stage * A_STAGE, &tq, fb, kb * I8_BLOCK_K, qtile * TC_BLOCK_M);
                             tma_load_2d_cg2(sB + stage * B_BYTES, &tx, fb, kb * I8_BLOCK_K,
-                                            t * TC_BLOCK_N + (int)rank * I8Cfg<CG>::B_ROWS);
+                                            t * TC_BLOCK_N + (int)rank * I8Cfg<CG, ARES>::B_ROWS);
                         } else {
                             mbar_expect_tx(&full[stage], I8_A_BYTES + B_BYTES);
-                            tma_load_2d(sA + stage * I8_A_BYTES, &tq, &full[stage], kb * I8_BLOCK_K, qtile * TC_BLOCK_M);
+                            tma_load_2d(sA + stage * A_STAGE, &tq, &full[stage], kb * I8_BLOCK_K, qtile * TC_BLOCK_M);
                             tma_load_2d(sB + stage * B_BYTES, &tx, &full[stage], kb * I8_BLOCK_K, t * TC_BLOCK_N);
                         }
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -376,9 +409,14 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
             int stage = 0;
             uint32_t phase = 0;
             int tix = 0;
+            uint32_t apar = 0;
             for (int item = item0; item < nitems; item += istride) {
                 int qtile, split, t0, nloc;
                 item_of(item, qtile, split, t0, nloc);
+                if (ARES) {
+                    mbar_wait(afull, apar);
+                    tc_fence_after();
+                }
                 for (int i = 0; i < nloc; ++i, ++tix) {
                     const int acc = tix & 1;
                     const uint32_t aphase = (tix >> 1) & 1;
@@ -388,7 +426,8 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
                     for (int kb = 0; kb < p.nkb; ++kb) {
                         mbar_wait(&full[stage], phase);
                         tc_fence_after();
-                        const uint64_t ad = sw128_desc(smem_u32(sA + stage * I8_A_BYTES));
+                        const uint64_t ad =
+                            sw128_desc(smem_u32(ARES ? sAres + kb * I8_A_BYTES : sA + stage * A_STAGE));
                         const uint64_t bd = sw128_desc(smem_u32(sB + stage * B_BYTES));
 #pragma unroll
                         for (int k = 0; k < I8_BLOCK_K / 32; ++k) {  // K = 32 int8 = 32 B per MMA inside the atom
@@ -407,6 +446,10 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
                         mma_commit_cg2(&tfull[acc]);
                     else
                         mma_commit(&tfull[acc]);
+                }
+                if (ARES) {  // both producers may overwrite A once these MMAs complete
+                    mma_commit_cg2(aempty);
+                    apar ^= 1;
                 }
             }
         }
@@ -513,80 +556,84 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
                         // rare: the warp evaluates every flagged (query, 8-row group) pair
                         // cooperatively, 4 pairs (32 rows) per pass, one row per lane
                         if (__any_sync(0xffffffffu, gmask != 0)) {
-                            const uint32_t b0 = __ballot_sync(0xffffffffu, gmask & 1u);
-                            const uint32_t b1 = __ballot_sync(0xffffffffu, gmask & 2u);
-                            const uint32_t b2 = __ballot_sync(0xffffffffu, gmask & 4u);
-                            const uint32_t b3 = __ballot_sync(0xffffffffu, gmask & 8u);
-                            // spill only the groups some lane flagged (warp-uniform branches)
-#pragma unroll
-                            for (int g = 0; g < 4; ++g) {
-                                const uint32_t bg = g == 0 ? b0 : g == 1 ? b1 : g == 2 ? b2 : b3;
-                                if (bg) {
-#pragma unroll
-                                    for (int j = 8 * g; j < 8 * g + 8; ++j) wspill[j * I8_EPI + lane] = (int32_t)v[j];
-                                }
-                            }
-                            const int p1 = __popc(b0), p2 = p1 + __popc(b1), p3 = p2 + __popc(b2);
-                            const int npairs = p3 + __popc(b3);
-                            __syncwarp();
                             const float kth = ts[TC_KP - 1];
+                            // two passes of 16 rows (groups {0,1}, then {2,3}) through a 16-row spill
+#pragma unroll
+                            for (int hh = 0; hh < 2; ++hh) {
+                                const uint32_t bA = __ballot_sync(0xffffffffu, (gmask >> (2 * hh)) & 1u);
+                                const uint32_t bB = __ballot_sync(0xffffffffu, (gmask >> (2 * hh + 1)) & 1u);
+                                if (!(bA | bB)) continue;
+                                // spill only the groups some lane flagged (warp-uniform branches)
+                                if (bA) {
+#pragma unroll
+                                    for (int j = 0; j < 8; ++j) wspill[j * I8_EPI + lane] = (int32_t)v[16 * hh + j];
+                                }
+                                if (bB) {
+#pragma unroll
+                                    for (int j = 8; j < 16; ++j) wspill[j * I8_EPI + lane] = (int32_t)v[16 * hh + j];
+                                }
+                                const int p1 = __popc(bA);
+                                const int npairs = p1 + __popc(bB);
+                                __syncwarp();
 #pragma unroll 1
-                            for (int base = 0; base < npairs; base += 4) {
-                                const int pi = base + (lane >> 3);
-                                bool act = pi < npairs;
-                                const int g = (pi >= p3) ? 3 : (pi >= p2) ? 2 : (pi >= p1) ? 1 : 0;
-                                const uint32_t bg = (g == 3) ? b3 : (g == 2) ? b2 : (g == 1) ? b1 : b0;
-                                const int pg = (g == 3) ? p3 : (g == 2) ? p2 : (g == 1) ? p1 : 0;
-                                const int owner = act ? nth_set_bit(bg, pi - pg) : 0;
-                                const float o_t = __shfl_sync(0xffffffffu, tq_, owner);
-                                const float o_A = __shfl_sync(0xffffffffu, A, owner);
-                                const float o_C = __shfl_sync(0xffffffffu, C, owner);
-                                const float o_thr = __shfl_sync(0xffffffffu, thr, owner);
-                                const float o_kth = __shfl_sync(0xffffffffu, kth, owner);
-                                const int64_t o_lim = __shfl_sync(0xffffffffu, lim, owner);
-                                const int j = 8 * g + (lane & 7);
-                                const uint32_t row = (uint32_t)(rb + j);
-                                act = act && (int64_t)row < o_lim;
-                                float l = -INFINITY;
-                                if (act) {
-                                    const float dx = se[c * 32 + j];
-                                    const float ap =
-                                        __fmul_rn(__fmul_rn(i2f_exact(wspill[j * I8_EPI + owner]), ss[c * 32 + j]), o_t);
-                                    l = __fsub_rn(ap, __fmaf_rn(o_A, dx, o_C));
-                                    if (!PILOT) {
-                                        const float u = __fadd_rn(__fmaf_rn(o_A, dx, ap), o_C);
-                                        if (u >= o_thr) {
-                                            const int64_t oq = (int64_t)qtile * TC_BLOCK_M + ew * 32 + owner;
-                                            const int o = atomicAdd(&p.acount[oq], 1);
-                                            if (o < p.cap) p.abuf[oq * (int64_t)p.cap + o] = make_uint2(row, __float_as_uint(u));
-                                            // approximate score at the bound: hand the row to the refiner
-                                            // (a full table just drops the job: the bound is a heuristic)
-                                            if (p.refine && ap >= o_thr) {
-                                                const uint32_t slot = atomicAdd(rq_tail, 1u) & (I8_RQ - 1);
-                                                atomicCAS(reinterpret_cast<unsigned long long *>(&rq[slot]), 0ull,
-                                                          ((unsigned long long)(oq + 1) << 32) | row);
+                                for (int base = 0; base < npairs; base += 4) {
+                                    const int pi = base + (lane >> 3);
+                                    bool act = pi < npairs;
+                                    const int gl = pi >= p1 ? 1 : 0;
+                                    const int owner = act ? nth_set_bit(gl ? bB : bA, pi - (gl ? p1 : 0)) : 0;
+                                    const float o_t = __shfl_sync(0xffffffffu, tq_, owner);
+                                    const float o_A = __shfl_sync(0xffffffffu, A, owner);
+                                    const float o_C = __shfl_sync(0xffffffffu, C, owner);
+                                    const float o_thr = __shfl_sync(0xffffffffu, thr, owner);
+                                    const float o_kth = __shfl_sync(0xffffffffu, kth, owner);
+                                    const int64_t o_lim = __shfl_sync(0xffffffffu, lim, owner);
+                                    const int jl = 8 * gl + (lane & 7);  // row within this 16-row pass
+                                    const int j = 16 * hh + jl;          // row within the chunk
+                                    const uint32_t row = (uint32_t)(rb + j);
+                                    act = act && (int64_t)row < o_lim;
+                                    float l = -INFINITY;
+                                    if (act) {
+                                        const float dx = se[c * 32 + j];
+                                        const float ap = __fmul_rn(
+                                            __fmul_rn(i2f_exact(wspill[jl * I8_EPI + owner]), ss[c * 32 + j]), o_t);
+                                        l = __fsub_rn(ap, __fmaf_rn(o_A, dx, o_C));
+                                        if (!PILOT) {
+                                            const float u = __fadd_rn(__fmaf_rn(o_A, dx, ap), o_C);
+                                            if (u >= o_thr) {
+                                                const int64_t oq = (int64_t)qtile * TC_BLOCK_M + ew * 32 + owner;
+                                                const int o = atomicAdd(&p.acount[oq], 1);
+                                                if (o < p.cap)
+                                                    p.abuf[oq * (int64_t)p.cap + o] = make_uint2(row, __float_as_uint(u));
+                                                // approximate score at the bound: hand the row to the refiner
+                                                // (a full table just drops the job: the bound is a heuristic)
+                                                if (p.refine && ap >= o_thr) {
+                                                    const uint32_t slot = atomicAdd(rq_tail, 1u) & (I8_RQ - 1);
+                                                    atomicCAS(reinterpret_cast<unsigned long long *>(&rq[slot]), 0ull,
+                                                              ((unsigned long long)(oq + 1) << 32) | row);
+                                                }
+                                            }
+                                        }
+                                    }
+                                    // list inserts happen in the owner lane (rare)
+                                    uint32_t wb = __ballot_sync(0xffffffffu, act && l > o_kth);
+                                    while (wb) {
+                                        const int src = __ffs(wb) - 1;
+                                        wb &= wb - 1;
+                                        const float lv = __shfl_sync(0xffffffffu, l, src);
+                                        const uint32_t rv = __shfl_sync(0xffffffffu, row, src);
+                                        const int ow = __shfl_sync(0xffffffffu, owner, src);
+                                        if (lane == ow && lv > ts[TC_KP - 1]) {
+                                            topk_insert(ts, tr, lv, rv);
+                                            if (ts[TC_KP - 1] > thr) {
+                                                thr = ts[TC_KP - 1];
+                                                thr2 = PILOT ? loose_pilot(thr, inv, C)
+                                                             : loose_threshold(thr, inv, A, C, dxmax);
                                             }
                                         }
                                     }
                                 }
-                                // list inserts happen in the owner lane (rare)
-                                uint32_t wb = __ballot_sync(0xffffffffu, act && l > o_kth);
-                                while (wb) {
-                                    const int src = __ffs(wb) - 1;
-                                    wb &= wb - 1;
-                                    const float lv = __shfl_sync(0xffffffffu, l, src);
-                                    const uint32_t rv = __shfl_sync(0xffffffffu, row, src);
-                                    const int ow = __shfl_sync(0xffffffffu, owner, src);
-                                    if (lane == ow && lv > ts[TC_KP - 1]) {
-                                        topk_insert(ts, tr, lv, rv);
-                                        if (ts[TC_KP - 1] > thr) {
-                                            thr = ts[TC_KP - 1];
-                                            thr2 = PILOT ? loose_pilot(thr, inv, C) : loose_threshold(thr, inv, A, C, dxmax);
-                                        }
-                                    }
-                                }
+                                __syncwarp();
                             }
-                            __syncwarp();
                         }
                         if (h == 0 || cp + 1 < I8_CPW / 2) tmem_wait_ld();
                     }
@@ -658,18 +705,20 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
                         rown[ql] = (int32_t)qg;
                         rcnt[ql] = 0;
                     }
-                    double *L = rel + ql * TC_KP;
+                    // rounded-down exact scores: the k-th entry is still a lower bound on e_k
+                    float *L = rel + ql * TC_KP;
+                    const float exf = __double2float_rd(ex);
                     int n = rcnt[ql];
-                    if (n < p.k || ex > L[p.k - 1]) {
+                    if (n < p.k || exf > L[p.k - 1]) {
                         int pos = n < p.k ? n++ : p.k - 1;
-                        while (pos > 0 && ex > L[pos - 1]) {
+                        while (pos > 0 && exf > L[pos - 1]) {
                             L[pos] = L[pos - 1];
                             --pos;
                         }
-                        L[pos] = ex;
+                        L[pos] = exf;
                         rcnt[ql] = n;
-                        // k distinct rows score >= L[k-1] exactly: a valid lower bound on e_k
-                        if (n == p.k) atomicMax(p.lg + qg, f2ord(__double2float_rd(L[p.k - 1])));
+                        // k distinct rows score >= L[k-1]: a valid lower bound on e_k
+                        if (n == p.k) atomicMax(p.lg + qg, f2ord(L[p.k - 1]));
                     }
                 }
                 __syncwarp();
@@ -1149,19 +1198,19 @@ static int i8_cg() {
     return (e && e[0] == '1') ? 1 : 2;
 }
 
-template <bool PILOT, int CG>
+template <bool PILOT, int CG, bool ARES = false>
 static int launch_scan8(int64_t ctas, const CUtensorMap &tq, const CUtensorMap &tx, const I8ScanParams &p,
                         cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        PR_CUDA(cudaFuncSetAttribute(tc8_scan_kernel<PILOT, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)i8_smem_bytes<CG>()));
+        PR_CUDA(cudaFuncSetAttribute(tc8_scan_kernel<PILOT, CG, ARES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)i8_smem_bytes<CG, ARES>()));
         attr = true;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)ctas);
     cfg.blockDim = dim3(I8_THREADS);
-    cfg.dynamicSmemBytes = i8_smem_bytes<CG>();
+    cfg.dynamicSmemBytes = i8_smem_bytes<CG, ARES>();
     cfg.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -1171,14 +1220,22 @@ static int launch_scan8(int64_t ctas, const CUtensorMap &tq, const CUtensorMap &
     cfg.attrs = at;
     cfg.numAttrs = 1;
     ::pr::count_launch();
-    PR_CUDA(cudaLaunchKernelEx(&cfg, tc8_scan_kernel<PILOT, CG>, tq, tx, p));
+    PR_CUDA(cudaLaunchKernelEx(&cfg, tc8_scan_kernel<PILOT, CG, ARES>, tq, tx, p));
     return PR_OK;
 }
 
 template <bool PILOT>
-static int launch_scan8_cg(int cg, int64_t ctas, const CUtensorMap &tq, const CUtensorMap &tx, const I8ScanParams &p,
-                           cudaStream_t st) {
-    return cg == 2 ? launch_scan8<PILOT, 2>(ctas, tq, tx, p, st) : launch_scan8<PILOT, 1>(ctas, tq, tx, p, st);
+static int launch_scan8_cg(int cg, bool ares, int64_t ctas, const CUtensorMap &tq, const CUtensorMap &tx,
+                           const I8ScanParams &p, cudaStream_t st) {
+    if (cg == 2)
+        return ares ? launch_scan8<PILOT, 2, true>(ctas, tq, tx, p, st) : launch_scan8<PILOT, 2, false>(ctas, tq, tx, p, st);
+    return launch_scan8<PILOT, 1>(ctas, tq, tx, p, st);
+}
+
+// PR_I8_ARES=1 keeps the query tile resident (measured: no faster than streaming it, so off)
+static bool i8_ares(int cg, int dp128) {
+    const char *e = getenv("PR_I8_ARES");
+    return cg == 2 && dp128 <= 1024 && e && e[0] == '1';  // measured: not faster (default off)
 }
 
 size_t tc8_scratch_bytes(int64_t nq, int dp128, int64_t n) {
@@ -1246,7 +1303,7 @@ int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats)
         I8ScanParams pp{s.n, s.dp128 / I8_BLOCK_K, psplit, (int)ceil_div<int64_t>(ptiles, psplit), (int)ptiles,
                         (int)qtiles, s.k, s.rows8.xs, s.rows8.xe, s.rows8.xt, qmeta, s.row_limit, s.nq, lg, acount,
                         abuf, cap, floor_thr, 0, I8_PILOT_STRIDE, pcand, s.x32, s.qp, s.dp8, s.d, 0, nullptr, 0};
-        rc = launch_scan8_cg<true>(cg, qtiles * psplit, qmap.map, xmap, pp, st);
+        rc = launch_scan8_cg<true>(cg, i8_ares(cg, s.dp128), qtiles * psplit, qmap.map, xmap, pp, st);
         if (rc) return rc;
         I8SeedArgs sa{pcand, psplit, s.nq, s.k, s.x32, s.dp8, s.d, s.qp, seed_rows, seed_s, seed_n, lg};
         ::pr::count_launch();
@@ -1270,9 +1327,9 @@ int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats)
     const char *ref_env = getenv("PR_I8_REFINE");  // 0: no in-kernel refinement (A/B knob)
     p.refine = !(ref_env && ref_env[0] == '0');
     const char *noepi_env = getenv("PR_I8_NOEPI");  // 1: epilogue does nothing (results invalid): MMA/TMA timing
-    if (noepi_env && noepi_env[0] == '1') p.noepi = 1;
+    if (noepi_env && noepi_env[0] >= '1') p.noepi = noepi_env[0] - '0';  // 2: also skip operand loads
     if (s.ev_begin) PR_CUDA(cudaEventRecord(s.ev_begin, st));
-    rc = launch_scan8_cg<false>(cg, qtiles * nsplit, qmap.map, xmap, p, st);
+    rc = launch_scan8_cg<false>(cg, i8_ares(cg, s.dp128), qtiles * nsplit, qmap.map, xmap, p, st);
     if (rc) return rc;
     if (s.ev_end) PR_CUDA(cudaEventRecord(s.ev_end, st));
     // 3) exact rescoring of the complete candidate set
