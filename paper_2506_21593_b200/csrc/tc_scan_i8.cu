@@ -1232,10 +1232,13 @@ static int launch_scan8_cg(int cg, bool ares, int64_t ctas, const CUtensorMap &t
     return launch_scan8<PILOT, 1>(ctas, tq, tx, p, st);
 }
 
-// PR_I8_ARES=1 keeps the query tile resident (measured: no faster than streaming it, so off)
+// Query tile resident in smem (PR_I8_ARES=0 streams it with every store tile instead).  Measured in
+// continuous runs (scripts/clock_probe.sh): 35.1 vs 38.4 ms at 10M x 1024 — half the L2->SM bytes,
+// so the power-capped clock rises 1510 -> 1640 MHz.  (Interleaved in-process A/B cannot see this:
+// alternating calls share one power-averaging window.)
 static bool i8_ares(int cg, int dp128) {
     const char *e = getenv("PR_I8_ARES");
-    return cg == 2 && dp128 <= 1024 && e && e[0] == '1';  // measured: not faster (default off)
+    return cg == 2 && dp128 <= 1024 && !(e && e[0] == '0');
 }
 
 size_t tc8_scratch_bytes(int64_t nq, int dp128, int64_t n) {
