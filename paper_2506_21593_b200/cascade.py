@@ -391,7 +391,8 @@ def _route_prefix(router, qs, vectors, mode):
             akm.misses += probed
             akm.index.search_count += probed
         elif L is L5:
-            kb.index.search_count += probed
+            with kb.index._lock:  # the knowledge base may be shared by concurrently replayed sessions
+                kb.index.search_count += probed
     router.trace.extend_ledger(ledger)
     prof.mark("writeback")
     if prof.enabled:

@@ -487,6 +487,10 @@ struct pr_index {
     size_t scratch_bytes = 0, scratch_peak = 0;
     int32_t *d_counters = nullptr;  // [4]: fallback count, candidate count, ...
     cudaStream_t last_stream = nullptr;
+    // the scratch block and device counters are per handle: a search on another stream
+    // first waits for the previous search (handles may be shared by concurrent routers)
+    cudaEvent_t scratch_ev = nullptr;
+    bool scratch_ev_used = false;
     // optional per-launch timing of the dominant scan kernel (bench roofline)
     bool timing = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pending, ev_free;
@@ -757,6 +761,7 @@ int pr_index_destroy(pr_index *h) {
     cudaFree(h->r8.maxnorm);
     if (h->scratch) cudaFree(h->scratch);
     if (h->d_counters) cudaFree(h->d_counters);
+    if (h->scratch_ev) cudaEventDestroy(h->scratch_ev);
     for (auto &p : h->ev_pending) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
     for (auto &p : h->ev_free) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
     delete h;
@@ -839,7 +844,24 @@ int pr_index_search(pr_index *h, const float *d_q, int64_t nq, int k, uint32_t m
     return pr_index_search_ex(h, d_q, nq, k, mode, nullptr, d_rows, d_raw, d_reported, d_count, stream);
 }
 
+static int search_impl(pr_index *h, const float *d_q, int64_t nq, int k, uint32_t mode, const int64_t *d_row_limit,
+                       int64_t *d_rows, double *d_raw, double *d_reported, int32_t *d_count, void *stream);
+
 int pr_index_search_ex(pr_index *h, const float *d_q, int64_t nq, int k, uint32_t mode, const int64_t *d_row_limit,
+                       int64_t *d_rows, double *d_raw, double *d_reported, int32_t *d_count, void *stream) {
+    if (!h) PR_FAIL(PR_ERR_BAD_ARG, "null handle");
+    cudaStream_t st = as_stream(stream);
+    if (!h->scratch_ev) PR_CUDA(cudaEventCreateWithFlags(&h->scratch_ev, cudaEventDisableTiming));
+    if (h->scratch_ev_used && h->last_stream != st) PR_CUDA(cudaStreamWaitEvent(st, h->scratch_ev, 0));
+    const int rc = search_impl(h, d_q, nq, k, mode, d_row_limit, d_rows, d_raw, d_reported, d_count, stream);
+    if (rc == PR_OK) {
+        PR_CUDA(cudaEventRecord(h->scratch_ev, st));
+        h->scratch_ev_used = true;
+    }
+    return rc;
+}
+
+static int search_impl(pr_index *h, const float *d_q, int64_t nq, int k, uint32_t mode, const int64_t *d_row_limit,
                        int64_t *d_rows, double *d_raw, double *d_reported, int32_t *d_count, void *stream) {
     if (!h) PR_FAIL(PR_ERR_BAD_ARG, "null handle");
     if (k < 1) PR_FAIL(PR_ERR_BAD_ARG, "k must be >= 1");  // index.py:161-162
