@@ -230,3 +230,41 @@ def test_big_k(gpu, rng):
     idx.extend_arrays([f"e{i}" for i in range(500)], X)
     _check(idx, X, Q, 100, 0)
     _check(idx, X, Q, 700, 0)  # k > n truncates
+
+
+def test_shared_index_across_streams(gpu, rng):
+    """One index searched concurrently from two threads on two CUDA streams (e.g.
+    routers sharing a knowledge base): each search waits for the previous one's
+    scratch, so every answer equals the single-stream answer."""
+    import threading
+
+    import torch
+
+    from paper_2506_21593_b200 import MODE_TENSOR, MODE_TENSOR_I8, FlatIndex
+
+    d, n = 128, 40000
+    X = _store(rng, n, d)
+    Qa = torch.from_numpy(random_unit_vectors(rng, 300, d)).cuda()
+    Qb = torch.from_numpy(random_unit_vectors(rng, 200, d)).cuda()
+    idx = FlatIndex(dim=d)
+    idx.extend_arrays([f"e{i}" for i in range(n)], X)
+    for mode in (MODE_TENSOR_I8, MODE_TENSOR):
+        want_a = idx.search_batch(Qa, 5, mode=mode).rows.cpu()
+        want_b = idx.search_batch(Qb, 7, mode=mode).rows.cpu()
+        errors = []
+
+        def worker(Q, k, want):
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for _ in range(15):
+                    got = idx.search_batch(Q, k, mode=mode).rows
+                    s.synchronize()
+                    if not bool((got.cpu() == want).all()):
+                        errors.append(k)
+
+        ts = [threading.Thread(target=worker, args=(Qa, 5, want_a)), threading.Thread(target=worker, args=(Qb, 7, want_b))]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        assert not errors, f"mode {mode}: {len(errors)} wrong answers under concurrent streams"
