@@ -257,3 +257,26 @@ def test_i8_tiny_stores_and_odd_batches(gpu, rng, n, nq):
     idx.extend_arrays([f"e{i}" for i in range(n)], X)
     for k in (1, 5, 16):
         _check(idx, X, Q, k, _mode())
+
+
+@pytest.mark.parametrize("env", [{}, {"PR_I8_ARES": "0"}, {"PR_I8_CG": "1"}, {"PR_I8_REFINE": "0"},
+                                 {"PR_I8_PILOT_STRIDE": "4"}])
+def test_i8_kernel_variants(gpu, rng, env, monkeypatch):
+    """The scan variants behind the per-call knobs (streamed vs resident query tile,
+    single-CTA vs 2-CTA MMA, refiner off, a denser pilot) all give the oracle's answer."""
+    from paper_2506_21593_b200 import FlatIndex
+
+    for key, val in env.items():
+        monkeypatch.setenv(key, val)
+    d, n = 256, 70001
+    X = _store(rng, n, d)
+    X[40000:40050] = X[3]
+    Q = random_unit_vectors(rng, 300, d)
+    Q[0] = X[3]
+    for i in range(10, 40):
+        v = X[(i * 7919) % n] + 0.05 * random_unit_vectors(rng, 1, d)[0]
+        Q[i] = (v / np.linalg.norm(v.astype(np.float64))).astype(np.float32)
+    idx = FlatIndex(dim=d)
+    idx.extend_arrays([f"e{i}" for i in range(n)], X)
+    for k in (1, 10):
+        _check(idx, X, Q, k, _mode())
