@@ -154,10 +154,12 @@ def _embed(router, texts, vectors):
     return torch.as_tensor(vectors, dtype=torch.float32).cuda().contiguous()
 
 
-def _seed_scratch(router, dim) -> FlatIndex:
+def _seed_scratch(router, dim, rows_bound: int) -> FlatIndex:
+    """The router's reusable seed store, reserved for the batch's worst case up
+    front (growing it mid-run would reallocate between two dependent searches)."""
     s = getattr(router, "_seed_scratch", None)
     if s is None or s.dim != dim:
-        s = FlatIndex(dim=dim)
+        s = FlatIndex(dim=dim, capacity=rows_bound)
         router._seed_scratch = s
     s.clear()
     return s
@@ -250,7 +252,7 @@ def _route_prefix(router, qs, vectors, mode):
                 first_pos.sort()
                 seeds_before = np.searchsorted(first_pos, seeds_before, side="left").astype(np.int64)
                 seed_rows = seed_rows[first_pos]
-                scratch = _seed_scratch(router, kb.index.dim)
+                scratch = _seed_scratch(router, kb.index.dim, B * cfg.akm_seed_k)
                 scratch.append_anonymous_from(kb.index, seed_rows)
                 rs = scratch.search_batch(Vs, 1, mode=mode, validate=False, row_limit=seeds_before, count=False)
                 prof.note("seeds", scratch)

@@ -482,6 +482,7 @@ struct pr_index {
     pr::TcStoreMap tmap8;   // TMA descriptor of x8, 256-row boxes
     pr::TcStoreMap tmap8h;  // ... 128-row boxes (2-CTA scan)
     bool tmap8_ok = false;
+    bool pooled = false;  // store buffers come from the stream-ordered pool (small stores)
     pr_search_stats stats{};
     // device scratch (grown on demand, stream-ordered)
     void *scratch = nullptr;
@@ -499,20 +500,24 @@ struct pr_index {
 
 namespace pr {
 
+// keep freed blocks mapped in the device's stream-ordered pool: a growing store
+// (semantic cache, AKM, seed scratch) would otherwise unmap and re-map memory at every
+// growth step, and cudaFree of touched memory was measured to stall for 100+ ms at times
+static void keep_pool() {
+    static bool kept = false;
+    if (kept) return;
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    kept = true;
+}
+
 static int ensure_scratch(pr_index *h, size_t bytes, cudaStream_t st) {
     if (h->scratch_bytes >= bytes) return PR_OK;
-    static bool pool_kept = false;
-    if (!pool_kept) {
-        // keep freed scratch in the stream-ordered pool: a growing store (semantic
-        // cache, AKM) would otherwise unmap and re-map it at every synchronisation
-        int dev = 0;
-        cudaMemPool_t pool;
-        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t keep = UINT64_MAX;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-        }
-        pool_kept = true;
-    }
+    keep_pool();
     if (h->scratch) PR_CUDA(cudaFreeAsync(h->scratch, st));
     h->scratch = nullptr;
     h->scratch_bytes = 0;
@@ -557,18 +562,29 @@ static int reserve(pr_index *h, int64_t cap, cudaStream_t st) {
     pr::I8Rows n8;
     n8.maxnorm = h->r8.maxnorm;
     const int64_t ntile = c256 / 256;
-    PR_CUDA(cudaMalloc(&nx32, (size_t)c * h->dp8 * sizeof(float)));
-    cudaError_t e = cudaMalloc(&nx16, (size_t)c256 * h->dp64 * sizeof(__half));
-    if (e == cudaSuccess) e = cudaMalloc(&n8.x8, (size_t)c256 * h->dp128);
-    if (e == cudaSuccess) e = cudaMalloc(&n8.xs, (size_t)c256 * sizeof(float));
-    if (e == cudaSuccess) e = cudaMalloc(&n8.xe, (size_t)c256 * sizeof(float));
-    if (e == cudaSuccess) e = cudaMalloc(&n8.xt, (size_t)ntile * sizeof(pr::I8TileMeta));
+    const size_t b32 = (size_t)c * h->dp8 * sizeof(float), b16 = (size_t)c256 * h->dp64 * sizeof(__half),
+                 b8 = (size_t)c256 * h->dp128, bt = (size_t)ntile * sizeof(pr::I8TileMeta);
+    // stores up to 1 GiB live in the stream-ordered pool (growth reuses mapped memory);
+    // bigger ones (the knowledge base) use plain allocations the pool cannot hoard
+    const bool pooled = b32 + b16 + b8 + 2 * c256 * sizeof(float) + bt <= ((size_t)1 << 30);
+    if (pooled) keep_pool();
+    auto alloc = [&](void **p, size_t b) { return pooled ? cudaMallocAsync(p, b, st) : cudaMalloc(p, b); };
+    auto release = [&](void *p, bool was_pooled) {
+        if (p) was_pooled ? cudaFreeAsync(p, st) : cudaFree(p);
+    };
+    cudaError_t e = alloc((void **)&nx32, b32);
+    if (e == cudaSuccess) e = alloc((void **)&nx16, b16);
+    if (e == cudaSuccess) e = alloc((void **)&n8.x8, b8);
+    if (e == cudaSuccess) e = alloc((void **)&n8.xs, (size_t)c256 * sizeof(float));
+    if (e == cudaSuccess) e = alloc((void **)&n8.xe, (size_t)c256 * sizeof(float));
+    if (e == cudaSuccess) e = alloc((void **)&n8.xt, bt);
     if (e != cudaSuccess) {
-        cudaFree(nx32);
-        cudaFree(nx16);
-        cudaFree(n8.x8);
-        cudaFree(n8.xs);
-        cudaFree(n8.xe);
+        release(nx32, pooled);
+        release(nx16, pooled);
+        release(n8.x8, pooled);
+        release(n8.xs, pooled);
+        release(n8.xe, pooled);
+        cudaStreamSynchronize(st);
         PR_FAIL(PR_ERR_NOMEM, "index reserve(%lld rows): %s", (long long)c, cudaGetErrorString(e));
     }
     PR_CUDA(cudaMemsetAsync(nx16, 0, (size_t)c256 * h->dp64 * sizeof(__half), st));
@@ -586,14 +602,17 @@ static int reserve(pr_index *h, int64_t cap, cudaStream_t st) {
                                 cudaMemcpyDeviceToDevice, st));
     }
     const auto t1 = now();
-    PR_CUDA(cudaStreamSynchronize(st));
+    // the old buffers may still be read by a search queued on another stream
+    PR_CUDA(cudaDeviceSynchronize());
     const auto t2 = now();
-    if (h->x32) cudaFree(h->x32);
-    if (h->x16) cudaFree(h->x16);
-    cudaFree(h->r8.x8);
-    cudaFree(h->r8.xs);
-    cudaFree(h->r8.xe);
-    cudaFree(h->r8.xt);
+    release(h->x32, h->pooled);
+    release(h->x16, h->pooled);
+    release(h->r8.x8, h->pooled);
+    release(h->r8.xs, h->pooled);
+    release(h->r8.xe, h->pooled);
+    release(h->r8.xt, h->pooled);
+    PR_CUDA(cudaStreamSynchronize(st));  // pooled frees are stream-ordered
+    h->pooled = pooled;
     if (dbg)
         fprintf(stderr, "reserve %lld -> %lld rows: malloc+enqueue %.2f ms, sync %.2f ms, free %.2f ms\n",
                 (long long)h->cap, (long long)c, ms(t0, t1), ms(t1, t2), ms(t2, now()));
@@ -764,12 +783,11 @@ int pr_index_create(int dim, int64_t capacity, uint32_t flags, pr_index **out) {
 int pr_index_destroy(pr_index *h) {
     if (!h) return PR_OK;
     cudaDeviceSynchronize();
-    if (h->x32) cudaFree(h->x32);
-    if (h->x16) cudaFree(h->x16);
-    cudaFree(h->r8.x8);
-    cudaFree(h->r8.xs);
-    cudaFree(h->r8.xe);
-    cudaFree(h->r8.xt);
+    for (void *p : {(void *)h->x32, (void *)h->x16, (void *)h->r8.x8, (void *)h->r8.xs, (void *)h->r8.xe,
+                    (void *)h->r8.xt}) {
+        if (p) h->pooled ? cudaFreeAsync(p, 0) : cudaFree(p);
+    }
+    cudaDeviceSynchronize();
     cudaFree(h->r8.maxnorm);
     if (h->scratch) cudaFree(h->scratch);
     if (h->d_counters) cudaFree(h->d_counters);

@@ -14,6 +14,7 @@ host) and returns device tensors; it is what the cascade and the benches use.
 """
 from __future__ import annotations
 
+import bisect
 import ctypes
 import json
 import struct
@@ -45,14 +46,9 @@ class SearchHit:
     rank: int
 
 
-class RowRef:
-    """Deferred payload: "the payload of row ``row`` of ``index``" (resolved on first read)."""
-
-    __slots__ = ("index", "row")
-
-    def __init__(self, index, row: int):
-        self.index = index
-        self.row = row
+# payload slot of a row whose payload is "the payload of row r of another index",
+# resolved on first read (AKM rows settled device-to-device from knowledge-base rows)
+_DEFERRED = object()
 
 
 @dataclass
@@ -87,6 +83,8 @@ class FlatIndex:
         self._ids: list[str] = []
         self._row_by_id: dict[str, int] = {}
         self._payloads: list[Any] = []
+        # deferred payload segments: (first row, source index, source rows), ascending
+        self._deferred: list[tuple[int, "FlatIndex", np.ndarray]] = []
         self.search_count = 0
         self.last_stats: _lib.SearchStats | None = None
 
@@ -133,8 +131,9 @@ class FlatIndex:
 
     def payload_at(self, row: int) -> Any:
         p = self._payloads[row]
-        if type(p) is RowRef:  # payload copied by reference from another index's row
-            p = p.index.payload_at(p.row)
+        if p is _DEFERRED:  # payload copied by reference from another index's row
+            seg = self._deferred[bisect.bisect_right(self._deferred, row, key=lambda t: t[0]) - 1]
+            p = seg[1].payload_at(int(seg[2][row - seg[0]]))
             self._payloads[row] = p
         return p
 
@@ -230,11 +229,13 @@ class FlatIndex:
             self._ids.extend([None] * r.numel())
             self._payloads.extend([None] * r.numel())
 
-    def append_rows_from(self, src: "FlatIndex", src_rows, ids: list[str], payloads: list[Any]) -> None:
+    def append_rows_from(self, src: "FlatIndex", src_rows, ids: list[str], payloads: list[Any] | None = None) -> None:
         """Append rows copied device-to-device from another index (AKM settle
-        from knowledge-base rows)."""
+        from knowledge-base rows).  ``payloads=None``: each new row's payload is
+        the source row's, read from ``src`` on first access."""
         torch = _torch()
-        r = torch.as_tensor(src_rows, dtype=torch.int64).to("cuda").contiguous()
+        rows = np.asarray(src_rows, dtype=np.int64)
+        r = torch.from_numpy(rows).to("cuda")
         with self._lock:
             base = len(self._ids)
             _lib.check(
@@ -243,7 +244,11 @@ class FlatIndex:
             )
             self._row_by_id.update(zip(ids, range(base, base + len(ids))))
             self._ids.extend(ids)
-            self._payloads.extend(payloads)
+            if payloads is None:
+                self._deferred.append((base, src, rows))
+                self._payloads.extend([_DEFERRED] * len(ids))
+            else:
+                self._payloads.extend(payloads)
 
     def _append_rows(self, arr: np.ndarray) -> None:
         torch = _torch()
@@ -262,6 +267,7 @@ class FlatIndex:
             self._ids.clear()
             self._row_by_id.clear()
             self._payloads.clear()
+            self._deferred.clear()
             _lib.check(self._L.pr_index_clear(self._h), "clear")
 
     def truncate(self, n: int) -> None:
@@ -270,6 +276,8 @@ class FlatIndex:
                 del self._row_by_id[eid]
             del self._ids[n:]
             del self._payloads[n:]
+            while self._deferred and self._deferred[-1][0] >= n:
+                self._deferred.pop()
             _lib.check(self._L.pr_index_truncate(self._h, n), "truncate")
 
     # -- search ----------------------------------------------------------------

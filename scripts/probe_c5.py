@@ -28,6 +28,18 @@ def main():
         R.CascadeRouter.route_batch = rb
     n = int(os.environ.get("N", "10000000"))
     store = make_store(n, 1024)
+    if os.environ.get("MARK_BATCHES"):
+        from paper_2506_21593_b200 import router as R
+
+        orig_rb = R.CascadeRouter.route_batch
+        cnt = [0]
+
+        def rb_marked(self, queries, vectors=None, **kw):
+            print(f"--- batch {cnt[0]}", file=sys.stderr, flush=True)
+            cnt[0] += 1
+            return orig_rb(self, queries, vectors=vectors, **kw)
+
+        R.CascadeRouter.route_batch = rb_marked
     t0 = time.time()
     r = C.c5_routed(store, n, n_sessions=int(os.environ.get("S", "1")), queries_per_session=int(os.environ.get("Q", "12288")),
                     batch=int(os.environ.get("B", "4096")),
@@ -35,7 +47,7 @@ def main():
     print({k: v for k, v in r.items() if k in ("value", "layer_counts", "stage_seconds", "parity")})
     log = C._LAST_PROFILE_LOG
     for i, t in enumerate(log):
-        print(i, {k: round(v * 1e3, 1) for k, v in t.items() if "." not in k or k == "kb.appended"})
+        print(i, {k: round(v * 1e3, 1) for k, v in t.items() if "." not in k or k.startswith("wb.")})
     st = store.stats()
     print("last KB search: path", st.path, "fallback", st.fallback, "cand", st.candidates, "appended", st.appended,
           "queries", st.queries, "wall", round(time.time() - t0, 1))
