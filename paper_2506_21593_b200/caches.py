@@ -151,18 +151,24 @@ class FixedKVCache:
         now = time.monotonic_ns()
         self.put_entries(texts, [CacheEntry(t, a, now) for t, a in zip(texts, answers)])
 
-    def put_entries(self, texts: Sequence[str], entries: Sequence) -> None:
-        """Bulk put of prepared entries (CacheEntry or ledger.LedgerEntry)."""
+    def put_entries(self, texts: Sequence[str], entries: Sequence, *, arena=None) -> None:
+        """Bulk put of prepared entries (CacheEntry or ledger.LedgerEntry).
+        ``arena``: the device UTF-8 arena (data, offsets) of a batch whose first
+        ``len(texts)`` texts these are (skips re-encoding)."""
         import torch
 
         if not texts:
             return
-        data, off = encode_texts(texts)
+        if arena is None:
+            data, off = encode_texts(texts)
         with self._lock:
             base = len(self._arena)
             self._arena.extend(entries)
-            d_data = torch.from_numpy(data).cuda()
-            d_off = torch.from_numpy(off).cuda()
+            if arena is None:
+                d_data = torch.from_numpy(data).cuda()
+                d_off = torch.from_numpy(off).cuda()
+            else:
+                d_data, d_off = arena
             fp = torch.empty((len(texts), 2), dtype=torch.int64, device="cuda")
             seq = torch.arange(base, base + len(texts), dtype=torch.int64, device="cuda")
             s = _lib.stream_ptr()

@@ -41,13 +41,14 @@ import time
 import numpy as np
 
 from . import generation
-from .caches import CacheEntry, FixedKVCache, SemanticCache, encode_texts
+from .caches import CacheEntry, FixedKVCache, SemanticCache
 from .index import MODE_AUTO, FlatIndex
 from .knowledge import AdaptiveKnowledgeMemory
 from .records import AnswerRecord, LayerTag
 from .errors import CascadeError
-from .ledger import BatchLedger, LedgerEntry, entry_text_conf
+from .ledger import BatchLedger, CtxRows, LedgerEntry, entry_text_conf
 from .router import LayerProbe
+from .textarena import to_device
 
 L1, L2, L3, L4, L5 = (LayerTag.FIXED_KV, LayerTag.SEMANTIC_CACHE, LayerTag.MEMORY_RECALL,
                       LayerTag.ADAPTIVE_MEMORY, LayerTag.NAIVE_RAG)
@@ -139,19 +140,24 @@ class RoutedBatch:
         return np.concatenate(parts) if parts else np.zeros(0, np.int8)
 
 
-def _embed(router, texts, vectors):
+def _embed(router, texts, vectors, arena):
     import torch
 
     if vectors is None:
         emb = router.embedder
         if hasattr(emb, "embed_device"):  # HashEmbedder: hash the batch on the GPU (bit-identical)
-            return emb.embed_device(texts)
+            return emb.embed_device(texts, arena=arena)
         if hasattr(emb, "embed_matrix"):
             V = emb.embed_matrix(texts)
         else:
             V = np.stack([np.asarray(emb.embed(t).values, dtype=np.float32) for t in texts])
         return torch.from_numpy(np.ascontiguousarray(V, dtype=np.float32)).cuda()
     return torch.as_tensor(vectors, dtype=torch.float32).cuda().contiguous()
+
+
+def _recall_always_rejects(backend, threshold) -> bool:
+    return (type(backend) is generation.StubBackend and len(backend.knowledge) == 0
+            and 0.0 <= threshold <= 1.0)
 
 
 def _seed_scratch(router, dim, rows_bound: int) -> FlatIndex:
@@ -179,7 +185,8 @@ def _route_prefix(router, qs, vectors, mode):
 
     B = len(qs)
     texts = [q.text for q in qs]
-    Vd = _embed(router, texts, vectors)
+    arena = to_device(texts)  # one device UTF-8 arena: embedding, L1 probe, KV write-back
+    Vd = _embed(router, texts, vectors, arena)
     ar = np.arange(B)
 
     prof.mark("settle+embed")
@@ -189,8 +196,7 @@ def _route_prefix(router, qs, vectors, mode):
     l1 = np.zeros(B, dtype=bool)
     kv_val = np.full(B, -1, dtype=np.int64)
     if L1 in pos:
-        data, off = encode_texts(texts)
-        vals, hit = kv.probe_device(torch.from_numpy(data).cuda(), torch.from_numpy(off).cuda(), B)
+        vals, hit = kv.probe_device(arena[0], arena[1], B)
         kv_val = vals.cpu().numpy()
         l1 = hit.cpu().numpy().astype(bool) | (first < ar)
 
@@ -198,7 +204,10 @@ def _route_prefix(router, qs, vectors, mode):
     # ---- L2: append the rows write-back will create, then one row-limited top-1 search
     sc_index = sc.index
     n_pre_sc = len(sc_index)
-    new_js = np.array([j for j in range(B) if first[j] == j and texts[j] not in sc_index], dtype=np.int64)
+    with sc_index._lock:
+        sc_rows = sc_index._row_by_id
+        new_js = np.array([j for j in np.flatnonzero(first == ar).tolist() if texts[j] not in sc_rows],
+                          dtype=np.int64)
     if new_js.size:
         sc_index.extend_arrays([texts[j] for j in new_js], Vd[torch.from_numpy(new_js).cuda()],
                                payloads=[None] * int(new_js.size), validate=False)
@@ -282,6 +291,11 @@ def _route_prefix(router, qs, vectors, mode):
             h = reach & l1[:p]
         elif L is L2:
             h = reach & l2[:p]
+        elif L is L3 and _recall_always_rejects(backend, cfg.recall_threshold):
+            # the stub LLM with an empty recall table rejects every query (generation.py);
+            # only its call counter moves
+            h = np.zeros(p, dtype=bool)
+            backend.recall_calls += int(reach.sum())
         elif L is L3:
             h = np.zeros(p, dtype=bool)
             for j in np.nonzero(reach)[0]:
@@ -307,44 +321,51 @@ def _route_prefix(router, qs, vectors, mode):
     else:
         lat = np.fromiter((lm.sample(LayerTag(int(v))) for v in serving), dtype=np.float64, count=p)
     text: list = [None] * p
-    conf = np.zeros(p, dtype=np.float64)
-    ctx_rows: dict[int, np.ndarray] = {}
-    latest: dict[str, int] = {}
+    conf_l = [0.0] * p
     k_ctx = cfg.retrieval_k
-    v1, v2, v3 = int(L1), int(L2), int(L3)
-    # the stub LLM answers with the top passage's annotation (generation.py:83-115):
-    # compute that directly instead of building a context answer object per query
+    v1, v2, v5 = int(L1), int(L2), int(L5)
+    sv = serving[:p]
+    # L5 answers first: they depend on no other query of the batch.  The stub LLM
+    # answers with the top passage's annotation (generation.py:83-115): compute that
+    # directly instead of building a context answer object per query
     stub = isinstance(backend, generation.StubBackend) and 0.0 <= backend.context_confidence <= 1.0
-    for j in range(p):
-        code = serving[j]
-        t = texts[j]
-        if code == v1 or code == v2:
-            # a cache hit serves a copy of the latest answer written for that key
-            key = t if code == v1 else sc_index.id_at(int(sc_row[j]))
-            i = latest.get(key)
-            if i is not None:
-                text[j], conf[j] = text[i], conf[i]
-            elif code == v1:
-                text[j], conf[j] = entry_text_conf(kv.entry_at(int(kv_val[j])))
-            else:
-                text[j], conf[j] = entry_text_conf(sc_index.payload_at(int(sc_row[j])))
-        elif code == v3:
-            a = recalled[j]
-            text[j], conf[j] = a.text, a.confidence
+    l5_js = np.flatnonzero(sv == v5).tolist()
+    if l5_js:
+        l5_slots = slot[l5_js]
+        if stub:
+            payload_at, first_sentence = kb.index.payload_at, generation.first_sentence
+            cc = backend.context_confidence
+            for j, r in zip(l5_js, kb_rows[l5_slots, 0].tolist()):
+                top = payload_at(r)
+                text[j] = top.answer if top.answer else first_sentence(top.text)
+                conf_l[j] = cc
+            backend.context_calls += len(l5_js)
         else:
-            s = slot[j]
-            rows = kb_rows[s, : min(k_ctx, int(kb_cnt[s]))]
-            if stub:
-                top = kb.index.payload_at(int(rows[0]))
-                backend.context_calls += 1
-                text[j] = top.answer if top.answer else generation.first_sentence(top.text)
-                conf[j] = backend.context_confidence
-            else:
-                passages = [kb.index.payload_at(int(r)) for r in rows]
+            for j, s5 in zip(l5_js, l5_slots.tolist()):
+                passages = [kb.index.payload_at(int(r)) for r in kb_rows[s5, : min(k_ctx, int(kb_cnt[s5]))]]
                 a = generation.generate_with_context(backend, qs[j], passages, L5)
-                text[j], conf[j] = a.text, a.confidence
-            ctx_rows[j] = rows
-        latest[t] = j
+                text[j], conf_l[j] = a.text, a.confidence
+    for j, a in recalled.items():
+        text[j], conf_l[j] = a.text, a.confidence
+    # cache hits, in order: a hit serves a copy of the latest answer written for its key
+    hit = ((sv == v1) | (sv == v2)).tolist()
+    if any(hit):
+        codes, scr, kvv = sv.tolist(), sc_row[:p].tolist(), kv_val[:p].tolist()
+        sc_ids, kv_entry, sc_payload = sc_index._ids, kv.entry_at, sc_index.payload_at
+        latest: dict[str, int] = {}
+        for j, t in enumerate(texts[:p]):
+            if hit[j]:
+                code = codes[j]
+                i = latest.get(t if code == v1 else sc_ids[scr[j]])
+                if i is not None:
+                    text[j], conf_l[j] = text[i], conf_l[i]
+                elif code == v1:
+                    text[j], conf_l[j] = entry_text_conf(kv_entry(kvv[j]))
+                else:
+                    text[j], conf_l[j] = entry_text_conf(sc_payload(scr[j]))
+            latest[t] = j
+    conf = np.asarray(conf_l, dtype=np.float64)
+    ctx_rows = CtxRows(kb_rows, slot[:p], kb_cnt, k_ctx, sv == v5)
     probe_prefix = {}
     for L in order:
         pre = []
@@ -357,20 +378,18 @@ def _route_prefix(router, qs, vectors, mode):
     # ---- write-back (router.py:333-337): KV in order (last write wins), SC payloads
     now = time.monotonic_ns()
     entries = [LedgerEntry(texts[j], ledger, j, now) for j in range(p)]
-    kv.put_entries(texts[:p], entries)
+    kv.put_entries(texts[:p], entries, arena=arena)
     prof.mark("wb.kv")
     n_new_kept = int(np.searchsorted(new_js, p, side="left"))
     if n_pre_sc + n_new_kept < len(sc_index):
         sc_index.truncate(n_pre_sc + n_new_kept)
-    with sc._lock:
-        payloads, rec = sc_index._payloads, sc._recency
+    with sc._lock, sc_index._lock:
+        payloads, rowmap = sc_index._payloads, sc_index._row_by_id
+        for t, e in zip(texts[:p], entries):
+            payloads[rowmap[t]] = e  # in order: the last write of a text wins
         seq = sc._seq
-        for j in range(p):
-            t = texts[j]
-            payloads[sc_index.row_of(t)] = entries[j]
-            seq += 1
-            rec[t] = seq
-        sc._seq = seq
+        sc._recency.update(zip(texts[:p], range(seq + 1, seq + p + 1)))
+        sc._seq = seq + p
     prof.mark("wb.sc")
     # AKM: seeds of L5 queries before the last were settled by the following
     # route() calls (device-to-device from KB rows, dedupe by id, no overwrite);
@@ -385,7 +404,10 @@ def _route_prefix(router, qs, vectors, mode):
 
     prof.mark("wb.akm")
     # ---- counters: a layer is probed by every query served at or after it
-    served_pos = np.array([pos[LayerTag(int(v))] for v in serving], dtype=np.int64) if p else np.zeros(0, np.int64)
+    pos_of_code = np.full(max(int(L) for L in LayerTag) + 1, -1, dtype=np.int64)
+    for L in order:
+        pos_of_code[int(L)] = pos[L]
+    served_pos = pos_of_code[serving.astype(np.int64)]
     for L in order:
         probed = int((served_pos >= pos[L]).sum())
         hit = int((serving == int(L)).sum())

@@ -19,12 +19,28 @@ import numpy as np
 from .records import AnswerRecord, LayerTag, Query
 
 
+class CtxRows:
+    """j -> KB rows of query j's context passages (the first ``k`` of its retrieval
+    top-k) for queries answered from retrieval, else None; sliced on access."""
+
+    __slots__ = ("rows", "slot", "count", "k", "served")
+
+    def __init__(self, rows: np.ndarray, slot: np.ndarray, count: np.ndarray, k: int, served: np.ndarray):
+        self.rows, self.slot, self.count, self.k, self.served = rows, slot, count, k, served
+
+    def get(self, j: int):
+        if not self.served[j]:
+            return None
+        s = int(self.slot[j])
+        return self.rows[s, : min(self.k, int(self.count[s]))]
+
+
 class BatchLedger:
     __slots__ = ("queries", "layer", "latency", "text", "conf", "ctx_rows", "kb_index", "probe_prefix",
                  "_answers", "_events")
 
     def __init__(self, queries: Sequence[Query], layer: np.ndarray, latency: np.ndarray, text: list,
-                 conf: np.ndarray, ctx_rows: dict, kb_index, probe_prefix: dict):
+                 conf: np.ndarray, ctx_rows, kb_index, probe_prefix: dict):
         self.queries = queries          # the routed Query objects, in order
         self.layer = layer              # int8 [n] serving LayerTag value
         self.latency = latency          # float64 [n]

@@ -141,7 +141,7 @@ class HashEmbedder:
     def embed_matrix(self, texts: Iterable[str]) -> np.ndarray:
         return np.stack([self.embed_array(t) for t in texts]) if texts else np.zeros((0, self.dim), np.float32)
 
-    def embed_device(self, texts) -> "object":
+    def embed_device(self, texts, *, arena=None) -> "object":
         """Embed a batch on the GPU (libpentarag pr_hash_embed: keyed BLAKE2b token
         hashing, warp per text) into a float32 CUDA tensor [n, dim], bit-identical
         to ``embed``.  Texts the device does not take (non-ASCII, empty, > 256
@@ -157,7 +157,7 @@ class HashEmbedder:
         out = torch.empty((n, self.dim), dtype=torch.float32, device="cuda")
         if n == 0:
             return out
-        d_data, d_off = to_device(texts)
+        d_data, d_off = arena if arena is not None else to_device(texts)  # arena: the texts' device UTF-8 arena
         flag = torch.empty(n, dtype=torch.uint8, device="cuda")
         L = _lib.load()
         _lib.check(L.pr_hash_embed(_lib.ptr(d_data), _lib.ptr(d_off), n, self.dim, int.from_bytes(self._key, "big"),
