@@ -394,10 +394,11 @@ def _route_prefix(router, qs, vectors, mode):
     # AKM: seeds of L5 queries before the last were settled by the following
     # route() calls (device-to-device from KB rows, dedupe by id, no overwrite);
     # the final query's seeds are still pending, exactly as after route()
-    l5_js = np.nonzero(serving == int(L5))[0]
-    settled = [kb_rows[slot[j], : kb_cnt[slot[j]]] for j in l5_js if j < p - 1]
-    if settled:
-        akm.settle_from_rows(kb.index, np.concatenate(settled))
+    l5_slots = slot[np.flatnonzero(serving[: max(p - 1, 0)] == int(L5))]
+    if l5_slots.size:
+        # row-major boolean selection = the per-query seed lists concatenated in order
+        valid = np.arange(kb_rows.shape[1])[None, :] < kb_cnt[l5_slots][:, None]
+        akm.settle_from_rows(kb.index, kb_rows[l5_slots][valid])
     if p and serving[p - 1] == int(L5):
         s = slot[p - 1]
         akm.enqueue([kb.index.payload_at(int(r)) for r in kb_rows[s, : kb_cnt[s]]])

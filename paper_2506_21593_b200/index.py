@@ -85,6 +85,7 @@ class FlatIndex:
         self._payloads: list[Any] = []
         # deferred payload segments: (first row, source index, source rows), ascending
         self._deferred: list[tuple[int, "FlatIndex", np.ndarray]] = []
+        self.epoch = 0  # bumped whenever rows are removed (clear / truncate)
         self.search_count = 0
         self.last_stats: _lib.SearchStats | None = None
 
@@ -268,6 +269,7 @@ class FlatIndex:
             self._row_by_id.clear()
             self._payloads.clear()
             self._deferred.clear()
+            self.epoch += 1
             _lib.check(self._L.pr_index_clear(self._h), "clear")
 
     def truncate(self, n: int) -> None:
@@ -278,6 +280,7 @@ class FlatIndex:
             del self._payloads[n:]
             while self._deferred and self._deferred[-1][0] >= n:
                 self._deferred.pop()
+            self.epoch += 1
             _lib.check(self._L.pr_index_truncate(self._h, n), "truncate")
 
     # -- search ----------------------------------------------------------------
