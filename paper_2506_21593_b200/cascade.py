@@ -250,8 +250,8 @@ def _route_prefix(router, qs, vectors, mode):
                 prof.note("akm", akm.index)
                 l4_unsure[spec] |= (ra.count.cpu().numpy() > 0) & (ra.scores[:, 0].cpu().numpy() >= thr)
             # superset of in-batch seeds: every seed of every earlier speculative query
-            seed_rows = np.concatenate([kb_rows[s, : kb_cnt[s]] for s in range(spec.size)]) \
-                if spec.size else np.zeros(0, np.int64)
+            # row-major boolean selection = the per-query seed lists concatenated in order
+            seed_rows = kb_rows[np.arange(kb_rows.shape[1])[None, :] < kb_cnt[:, None]]
             seeds_before = np.concatenate([[0], np.cumsum(kb_cnt)[:-1]]).astype(np.int64)
             if seed_rows.size:
                 # keep the first occurrence of each KB row: query j sees the same SET of

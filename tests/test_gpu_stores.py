@@ -255,3 +255,48 @@ def test_router_semantics(gpu):
         empty.route(validate_query("anything at all", "s1"))
     assert err.value.trace_event.serving_layer is None
     assert len(empty.kv_cache) == 0 and len(empty.semantic_cache) == 0
+
+
+def test_akm_settle_from_rows_mixed_paths(gpu):
+    """settle_from_rows (device path, KB-row bitmap) interleaved with the host settle
+    path, direct index inserts, clear and a knowledge-base that grows: the AKM holds
+    exactly the ids the reference's settle would (first occurrence, no overwrite,
+    knowledge.py:217-228), rows in insertion order, payloads = the KB passages."""
+    from paper_2506_21593_b200 import AdaptiveKnowledgeMemory, HashEmbedder, Passage, ingest_corpus
+
+    emb = HashEmbedder()
+    lines = [json.dumps({"id": f"p{i}", "text": f"passage number {i} about subject {i % 7}", "source": "t"})
+             for i in range(60)]
+    kb = ingest_corpus(lines, emb)
+    akm = AdaptiveKnowledgeMemory()
+    want: list[str] = []
+
+    def model_settle(ids):
+        for pid in ids:
+            if pid not in want:
+                want.append(pid)
+
+    rng = np.random.default_rng(5)
+    for step in range(12):
+        rows = rng.integers(0, len(kb), 25)
+        if step == 3:  # host path: queued passages, some of them KB passages
+            ps = [kb.get(f"p{r}") for r in rows[:6]]
+            akm.enqueue(ps)
+            akm.settle()
+            model_settle([p.id for p in ps])
+        if step == 5:  # an id inserted straight into the index
+            p = kb.get("p59")
+            akm.index.insert(p.id, p.embedding, p)
+            model_settle([p.id])
+        if step == 7:
+            akm.clear()
+            want.clear()
+        if step == 9:  # the knowledge base grows: row marks are rebuilt
+            for i in range(5):
+                t = f"late passage {i}"
+                kb.add(Passage(id=f"q{i}", text=t, source="t", embedding=emb.embed(t)))
+        akm.settle_from_rows(kb.index, rows)
+        model_settle([kb.index.id_at(int(r)) for r in rows])
+        assert list(akm.index.entry_ids()) == want, step
+        for pid in want[:5]:
+            assert akm.index.payload(pid).id == pid
