@@ -65,7 +65,9 @@ def parse():
                     help="secondary BASELINE configs measured after the headline (rank 0, N=1): c2,c3,c5 or ''")
     ap.add_argument("--kv-keys", type=int, default=100_000_000)
     ap.add_argument("--c5-queries", type=int, default=20_000, help="queries per C5 session")
-    ap.add_argument("--c5-sessions", type=int, default=2)
+    ap.add_argument("--c5-sessions", type=int, default=4)
+    ap.add_argument("--c5-workers", type=int, default=2,
+                    help="C5 sessions replayed concurrently (one router per worker, shared knowledge base)")
     return ap.parse_args()
 
 
@@ -450,7 +452,7 @@ def main():
                     configs["c3_fixed_kv"] = C.c3_kv(float(pk.get("hbm_gbs", 6538.6)), n_keys=a.kv_keys)
                 elif name == "c5":
                     configs["c5_routed"] = C.c5_routed(idx, a.n, n_sessions=a.c5_sessions,
-                                                       queries_per_session=a.c5_queries,
+                                                       queries_per_session=a.c5_queries, workers=a.c5_workers,
                                                        profile=bool(os.environ.get("BENCH_C5_PROFILE")))
             except Exception as exc:  # noqa: BLE001 - recorded, the headline stands
                 configs[name] = {"error": f"{type(exc).__name__}: {exc}",

@@ -239,17 +239,18 @@ class _KBPayloads:
     distractor Passages (own id, own stored vector) materialised on access."""
 
     def __init__(self, store, real):
+        from paper_2506_21593_b200 import Passage
+
         self._store, self._real, self._n = store, real, len(store._ids)
+        self._n_real, self._passage = len(real), Passage
 
     def __len__(self):
         return self._n
 
     def __getitem__(self, i):
-        from paper_2506_21593_b200 import Passage
-
-        if i < len(self._real):
+        if i < self._n_real:
             return self._real[i]
-        return Passage(id=self._store.id_at(i), text=f"Distractor passage {i}. Unrelated archival material.",
+        return self._passage(id=self._store.id_at(i), text=f"Distractor passage {i}. Unrelated archival material.",
                        source="distractor", embedding=_RowVector(self._store, i), answer=None)
 
 
@@ -257,10 +258,17 @@ _LAST_PROFILE_LOG: list = []  # per-batch stage times of the last profiled c5_ro
 
 
 def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_session=20_000, batch=4096,
-              seed=0, parity_queries=300, profile=False):
+              seed=0, parity_queries=300, profile=False, workers=1):
     """Routed replay over the bench's 10M x 1024 store turned into a knowledge base:
     rows [0, n_qa) hold HashEmbedder(context) of the QA pool, the rest stay dense
-    distractors."""
+    distractors.
+
+    ``workers`` > 1: that many routers (each its own KV / semantic cache / AKM, one
+    shared knowledge base) replay the sessions concurrently from as many threads —
+    sessions are independent, and one worker's host-side Python then
+    overlaps another's device scans on the shared GPU."""
+    import threading
+
     import torch
 
     from benchlib.workloads import LatencyDraws, corpus_of, qa_rows, session_stream
@@ -287,44 +295,70 @@ def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_se
         r.latency_model = LatencyDraws(0.25)
         return r
 
-    router = make_router()
-    # warm-up: one whole session of an unrelated seed, untimed (first-launch module
-    # loading; the stores and search scratch grow to their per-session size, and
+    workers = max(1, min(int(workers), n_sessions))
+    routers = [make_router() for _ in range(workers)]
+    # warm-up: one whole session of an unrelated seed per router, untimed (first-launch
+    # module loading; the stores and search scratch grow to their per-session size, and
     # reset_session keeps that capacity, as in a serving process past its first session)
     _, warm = session_stream(questions, queries_per_session, seed + 1000, 0)
     wq = [validate_query(t, "warmup", query_id=f"w{i}", issued_at_ns=0) for i, (t, _) in enumerate(warm)]
-    for i in range(0, len(wq), batch):
-        router.route_batch(wq[i:i + batch], materialize=False)
-    router.reset_session()
-    router.trace.clear()
-    router.profile_batches = profile
+    for router in routers:
+        for i in range(0, len(wq), batch):
+            router.route_batch(wq[i:i + batch], materialize=False)
+        router.reset_session()
+        router.trace.clear()
+        router.profile_batches = profile
+    router = routers[0]
     # the loaded KB (10M ids, 120k passages) is permanent: keep it out of the cyclic
     # collector's full passes, which otherwise stall a batch for ~150 ms each
     # (measured, scripts/probe_growth.py) — standard practice for a loaded server
     gc.collect()
     gc.freeze()
-    layer_counts = {}
+    tallies = [{"total": 0, "sequential": 0, "layers": {}} for _ in range(workers)]
+    errors: list = []
+
+    def replay(w):
+        router, tally = routers[w], tallies[w]
+        try:
+            for s in range(w, n_sessions, workers):
+                sid, st = streams[s]
+                router.reset_session()
+                router.latency_model.reseed([seed, s, 1])
+                qs = [validate_query(t, sid, query_id=f"{sid}-q{i:05d}", issued_at_ns=0) for i, (t, _) in enumerate(st)]
+                for i in range(0, len(qs), batch):
+                    # columnar result: per-query objects are only built if someone reads them
+                    # query texts in, embedded on the device inside route_batch (pr_hash_embed)
+                    res = router.route_batch(qs[i:i + batch], materialize=False)
+                    tally["total"] += len(res)
+                    tally["sequential"] += router.last_batch_stats["sequential"]
+                    for code, c in zip(*np.unique(res.layers(), return_counts=True)):
+                        name = LayerTag(int(code)).wire_name
+                        tally["layers"][name] = tally["layers"].get(name, 0) + int(c)
+        except BaseException as exc:  # noqa: BLE001 - re-raised on the main thread
+            errors.append(exc)
+
     e0, e1 = _events()
     torch.cuda.synchronize()
-    total = 0
-    seq_total = 0
     e0.record()
-    for s, (sid, st) in enumerate(streams):
-        router.reset_session()
-        router.latency_model.reseed([seed, s, 1])
-        qs = [validate_query(t, sid, query_id=f"{sid}-q{i:05d}", issued_at_ns=0) for i, (t, _) in enumerate(st)]
-        for i in range(0, len(qs), batch):
-            # columnar result: per-query objects are only built if someone reads them
-            # query texts in, embedded on the device inside route_batch (pr_hash_embed)
-            res = router.route_batch(qs[i:i + batch], materialize=False)
-            total += len(res)
-            seq_total += router.last_batch_stats["sequential"]
-            for code, c in zip(*np.unique(res.layers(), return_counts=True)):
-                name = LayerTag(int(code)).wire_name
-                layer_counts[name] = layer_counts.get(name, 0) + int(c)
+    if workers == 1:
+        replay(0)
+    else:
+        pool = [threading.Thread(target=replay, args=(w,)) for w in range(workers)]
+        for t in pool:
+            t.start()
+        for t in pool:
+            t.join()
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
+    if errors:
+        raise errors[0]
+    total = sum(t["total"] for t in tallies)
+    seq_total = sum(t["sequential"] for t in tallies)
+    layer_counts: dict = {}
+    for t in tallies:
+        for name, c in t["layers"].items():
+            layer_counts[name] = layer_counts.get(name, 0) + c
     gc.unfreeze()
     # parity: the first parity_queries of session 0 routed one by one on a twin router
     twin = make_router()
@@ -348,8 +382,9 @@ def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_se
     return {
         "workload": f"five-layer routed replay (L1/L2/L3/L4/L5, LLM stubbed) over a {n_store} x 1024 KB "
                     f"({n_qa} HashEmbedder contexts + dense distractors), {n_sessions} warm-up sessions x "
-                    f"{queries_per_session} queries, batch {batch} (configs[4] shape, 1 GPU)",
-        "value": total / (ms / 1e3), "unit": "routed queries/s", "ms_total": ms,
+                    f"{queries_per_session} queries, batch {batch} (configs[4] shape, 1 GPU), "
+                    f"{workers} concurrent session worker(s)",
+        "value": total / (ms / 1e3), "unit": "routed queries/s", "ms_total": ms, "workers": workers,
         "layer_counts": layer_counts, "queries_routed_sequentially": seq_total,
         "stage_seconds": getattr(router, "batch_profile", None),
         "query_vectors": "device HashEmbedder (pr_hash_embed) inside the timed region, from raw query texts",

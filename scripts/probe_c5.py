@@ -43,7 +43,7 @@ def main():
     t0 = time.time()
     r = C.c5_routed(store, n, n_sessions=int(os.environ.get("S", "1")), queries_per_session=int(os.environ.get("Q", "12288")),
                     batch=int(os.environ.get("B", "4096")),
-                    profile=True)
+                    profile=not os.environ.get("C5_WORKERS"), workers=int(os.environ.get("C5_WORKERS", "1")))
     print({k: v for k, v in r.items() if k in ("value", "layer_counts", "stage_seconds", "parity")})
     log = C._LAST_PROFILE_LOG
     for i, t in enumerate(log):

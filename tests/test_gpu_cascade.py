@@ -153,3 +153,50 @@ def test_batched_simulation_logs_byte_identical(gpu):
         for i, (a, b) in enumerate(zip(got, want)):
             assert a == b, (s, i)
         assert len(got) == len(want)
+
+
+def test_concurrent_sessions_share_knowledge_base(gpu):
+    """Two routers (own caches / AKM) over ONE knowledge base, routing their sessions
+    from two threads at once (the C5 bench's session workers): each gets exactly what
+    it gets routing alone, and the shared KB's search counter sums both."""
+    import threading
+
+    from paper_2506_21593_b200 import CascadeRouter, HashEmbedder, StubBackend, ingest_corpus, validate_query
+
+    gold = _golden("simulation.json")
+    emb = HashEmbedder()
+    kb = ingest_corpus((json.dumps(c) for c in gold["corpus"]), emb)
+    rng = np.random.default_rng(9)
+    sessions = []
+    for s in range(2):
+        texts = []
+        for i in range(400):
+            if texts and rng.random() < 0.5:
+                texts.append(texts[int(rng.integers(len(texts)))])
+            else:
+                texts.append(gold["questions"][int(rng.integers(len(gold["questions"])))])
+        sessions.append([validate_query(t, f"s{s}", query_id=f"s{s}q{i}", issued_at_ns=i)
+                         for i, t in enumerate(texts)])
+
+    def mk():
+        return CascadeRouter(embedder=emb, backend=StubBackend(), knowledge_base=kb)
+
+    def run(router, qs, out):
+        for i in range(0, len(qs), 64):
+            out.extend(_sig(*r) for r in router.route_batch(qs[i:i + 64]))
+
+    c0 = kb.index.search_count
+    alone = []
+    for qs in sessions:
+        out: list = []
+        run(mk(), qs, out)
+        alone.append(out)
+    c1 = kb.index.search_count
+    routers, outs = [mk(), mk()], [[], []]
+    threads = [threading.Thread(target=run, args=(routers[s], sessions[s], outs[s])) for s in range(2)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert outs == alone
+    assert kb.index.search_count - c1 == c1 - c0  # the shared counter saw every probe of both
