@@ -42,7 +42,7 @@ import numpy as np
 
 from . import generation
 from .caches import CacheEntry, FixedKVCache, SemanticCache
-from .index import MODE_AUTO, FlatIndex
+from .index import MODE_AUTO, FlatIndex, first_occurrences
 from .knowledge import AdaptiveKnowledgeMemory
 from .records import AnswerRecord, LayerTag
 from .errors import CascadeError
@@ -160,6 +160,13 @@ def _recall_always_rejects(backend, threshold) -> bool:
             and 0.0 <= threshold <= 1.0)
 
 
+def _row_scratch(router, n: int) -> np.ndarray:
+    buf = getattr(router, "_row_pos", None)
+    if buf is None or buf.size < n:
+        buf = router._row_pos = np.empty(max(n, 1), dtype=np.int32)
+    return buf
+
+
 def _seed_scratch(router, dim, rows_bound: int) -> FlatIndex:
     """The router's reusable seed store, reserved for the batch's worst case up
     front (growing it mid-run would reallocate between two dependent searches)."""
@@ -191,8 +198,8 @@ def _route_prefix(router, qs, vectors, mode):
 
     prof.mark("settle+embed")
     # ---- L1: pre-batch probe + causal first-occurrence dedupe
-    first_of: dict[str, int] = {}
-    first = np.fromiter((first_of.setdefault(t, j) for j, t in enumerate(texts)), dtype=np.int64, count=B)
+    first_of = {t: j for j, t in zip(range(B - 1, -1, -1), reversed(texts))}  # earliest index wins
+    first = np.fromiter(map(first_of.__getitem__, texts), dtype=np.int64, count=B)
     l1 = np.zeros(B, dtype=bool)
     kv_val = np.full(B, -1, dtype=np.int64)
     if L1 in pos:
@@ -257,8 +264,7 @@ def _route_prefix(router, qs, vectors, mode):
                 # keep the first occurrence of each KB row: query j sees the same SET of
                 # vectors (a repeat only becomes visible after its first copy), and the
                 # scratch loses its bit-identical duplicates, which tie at every score
-                _, first_pos = np.unique(seed_rows, return_index=True)
-                first_pos.sort()
+                first_pos = first_occurrences(seed_rows, _row_scratch(router, len(kb.index)))
                 seeds_before = np.searchsorted(first_pos, seeds_before, side="left").astype(np.int64)
                 seed_rows = seed_rows[first_pos]
                 scratch = _seed_scratch(router, kb.index.dim, B * cfg.akm_seed_k)

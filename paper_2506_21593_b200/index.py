@@ -46,6 +46,18 @@ class SearchHit:
     rank: int
 
 
+def first_occurrences(rows: np.ndarray, pos: np.ndarray) -> np.ndarray:
+    """Ascending positions of the first occurrence of each value in ``rows`` (values
+    in [0, pos.size)); ``pos`` is caller-owned int32 scratch, no clearing needed:
+    O(len(rows)) instead of a sort."""
+    n = rows.size
+    if n == 0:
+        return np.zeros(0, dtype=np.int64)
+    ar = np.arange(n, dtype=np.int32)
+    pos[rows[::-1]] = ar[::-1]  # repeated indices: the last assignment (= earliest position) wins
+    return np.flatnonzero(pos[rows] == ar)
+
+
 # payload slot of a row whose payload is "the payload of row r of another index",
 # resolved on first read (AKM rows settled device-to-device from knowledge-base rows)
 _DEFERRED = object()

@@ -9,6 +9,12 @@ import numpy as np
 def encode_texts(texts: Sequence[str]):
     """(bytes uint8 [total], offsets int64 [n+1]) as host numpy arrays.
     ``surrogatepass`` keeps the str -> bytes map injective for every Python str."""
+    joined = "".join(texts)
+    if joined.isascii():  # one byte per character: no per-text encode
+        off = np.zeros(len(texts) + 1, dtype=np.int64)
+        if texts:
+            np.cumsum(np.fromiter(map(len, texts), dtype=np.int64, count=len(texts)), out=off[1:])
+        return np.frombuffer(joined.encode("ascii") or b"\0", dtype=np.uint8).copy(), off
     bs = [t.encode("utf-8", "surrogatepass") for t in texts]
     off = np.zeros(len(bs) + 1, dtype=np.int64)
     if bs:
