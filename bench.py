@@ -66,7 +66,7 @@ def parse():
     ap.add_argument("--kv-keys", type=int, default=100_000_000)
     ap.add_argument("--c5-queries", type=int, default=20_000, help="queries per C5 session")
     ap.add_argument("--c5-sessions", type=int, default=4)
-    ap.add_argument("--c5-workers", type=int, default=2,
+    ap.add_argument("--c5-workers", type=int, default=1,
                     help="C5 sessions replayed concurrently (one router per worker, shared knowledge base)")
     return ap.parse_args()
 

@@ -255,6 +255,7 @@ class _KBPayloads:
 
 
 _LAST_PROFILE_LOG: list = []  # per-batch stage times of the last profiled c5_routed run
+_LAST_BATCH_WALL: list = []  # (worker, session, batch, host wall ms) of every c5_routed batch
 
 
 def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_session=20_000, batch=4096,
@@ -317,26 +318,41 @@ def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_se
     tallies = [{"total": 0, "sequential": 0, "layers": {}} for _ in range(workers)]
     errors: list = []
 
+    # one CUDA stream per worker: a worker's small kernels (embedding, probes, write-back)
+    # need not queue behind another worker's knowledge-base scan (the shared KB handle
+    # orders its own searches across streams)
+    streams_w = [torch.cuda.current_stream()] if workers == 1 else [torch.cuda.Stream() for _ in range(workers)]
+    for st_w in streams_w:
+        st_w.wait_stream(torch.cuda.current_stream())
+
     def replay(w):
-        router, tally = routers[w], tallies[w]
         try:
-            for s in range(w, n_sessions, workers):
-                sid, st = streams[s]
-                router.reset_session()
-                router.latency_model.reseed([seed, s, 1])
-                qs = [validate_query(t, sid, query_id=f"{sid}-q{i:05d}", issued_at_ns=0) for i, (t, _) in enumerate(st)]
-                for i in range(0, len(qs), batch):
-                    # columnar result: per-query objects are only built if someone reads them
-                    # query texts in, embedded on the device inside route_batch (pr_hash_embed)
-                    res = router.route_batch(qs[i:i + batch], materialize=False)
-                    tally["total"] += len(res)
-                    tally["sequential"] += router.last_batch_stats["sequential"]
-                    for code, c in zip(*np.unique(res.layers(), return_counts=True)):
-                        name = LayerTag(int(code)).wire_name
-                        tally["layers"][name] = tally["layers"].get(name, 0) + int(c)
+            with torch.cuda.stream(streams_w[w]):
+                _replay_sessions(w, routers[w], tallies[w])
+            streams_w[w].synchronize()
         except BaseException as exc:  # noqa: BLE001 - re-raised on the main thread
             errors.append(exc)
 
+    def _replay_sessions(w, router, tally):
+        for s in range(w, n_sessions, workers):
+            sid, st = streams[s]
+            router.reset_session()
+            router.latency_model.reseed([seed, s, 1])
+            qs = [validate_query(t, sid, query_id=f"{sid}-q{i:05d}", issued_at_ns=0) for i, (t, _) in enumerate(st)]
+            for i in range(0, len(qs), batch):
+                # columnar result: per-query objects are only built if someone reads them
+                # query texts in, embedded on the device inside route_batch (pr_hash_embed)
+                t_b = time.perf_counter()
+                res = router.route_batch(qs[i:i + batch], materialize=False)
+                _LAST_BATCH_WALL.append((w, s, i // batch, (time.perf_counter() - t_b) * 1e3,
+                                         router.last_batch_stats["splits"]))
+                tally["total"] += len(res)
+                tally["sequential"] += router.last_batch_stats["sequential"]
+                for code, c in zip(*np.unique(res.layers(), return_counts=True)):
+                    name = LayerTag(int(code)).wire_name
+                    tally["layers"][name] = tally["layers"].get(name, 0) + int(c)
+
+    _LAST_BATCH_WALL.clear()
     e0, e1 = _events()
     torch.cuda.synchronize()
     e0.record()
@@ -348,6 +364,8 @@ def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_se
             t.start()
         for t in pool:
             t.join()
+    for st_w in streams_w:
+        torch.cuda.current_stream().wait_stream(st_w)
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)

@@ -521,8 +521,10 @@ static int ensure_scratch(pr_index *h, size_t bytes, cudaStream_t st) {
     if (h->scratch) PR_CUDA(cudaFreeAsync(h->scratch, st));
     h->scratch = nullptr;
     h->scratch_bytes = 0;
-    // geometric growth: a store that grows every batch reallocates O(log n) times
-    size_t b = std::max({bytes, (size_t)(1 << 20), h->scratch_peak + h->scratch_peak / 2});
+    // geometric growth (a store that grows every batch reallocates O(log n) times), and
+    // 25 % headroom from the first allocation: growing the pool by a GB was measured to
+    // stall 100-650 ms, so a batch a few queries larger than the last must not trigger it
+    size_t b = std::max({bytes + bytes / 4, (size_t)(1 << 20), h->scratch_peak + h->scratch_peak / 2});
     PR_CUDA(cudaMallocAsync(&h->scratch, b, st));
     if (getenv("PR_DEBUG_RESERVE")) fprintf(stderr, "scratch -> %.1f MB\n", b / 1048576.0);
     h->scratch_bytes = b;

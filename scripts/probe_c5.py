@@ -40,11 +40,46 @@ def main():
             return orig_rb(self, queries, vectors=vectors, **kw)
 
         R.CascadeRouter.route_batch = rb_marked
+    import gc
+
+    gc_log = []
+
+    def _gc_cb(phase, info, _t=[0.0]):
+        if phase == "start":
+            _t[0] = time.perf_counter()
+        elif (time.perf_counter() - _t[0]) > 0.005:
+            gc_log.append((info["generation"], round((time.perf_counter() - _t[0]) * 1e3, 1)))
+
+    gc.callbacks.append(_gc_cb)
+    if os.environ.get("KB_STATS"):
+        from paper_2506_21593_b200 import index as I
+
+        orig_sb = I.FlatIndex.search_batch
+        kb_log = []
+
+        def sb(self, queries, k, **kw):
+            if len(self) < 1_000_000:
+                return orig_sb(self, queries, k, **kw)
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            r = orig_sb(self, queries, k, **kw)
+            torch.cuda.synchronize()
+            st = self.stats()
+            kb_log.append((queries.shape[0], round((time.perf_counter() - t) * 1e3, 1), st.fallback, st.appended,
+                           st.candidates))
+            return r
+
+        I.FlatIndex.search_batch = sb
     t0 = time.time()
     r = C.c5_routed(store, n, n_sessions=int(os.environ.get("S", "1")), queries_per_session=int(os.environ.get("Q", "12288")),
                     batch=int(os.environ.get("B", "4096")),
                     profile=not os.environ.get("C5_WORKERS"), workers=int(os.environ.get("C5_WORKERS", "1")))
-    print({k: v for k, v in r.items() if k in ("value", "layer_counts", "stage_seconds", "parity")})
+    print({k: v for k, v in r.items() if k in ("value", "layer_counts", "stage_seconds", "parity", "queries_routed_sequentially")})
+    print("gc pauses > 5 ms (generation, ms):", gc_log)
+    if os.environ.get("KB_STATS"):
+        print("kb searches (nq, ms, fallback, appended, rescored):", kb_log[:26])
+    print("batch wall ms (worker, session, batch, ms, splits):",
+          [(w, s, b, round(ms, 1), sp) for w, s, b, ms, sp in C._LAST_BATCH_WALL])
     log = C._LAST_PROFILE_LOG
     for i, t in enumerate(log):
         print(i, {k: round(v * 1e3, 1) for k, v in t.items() if "." not in k or k.startswith("wb.")})
