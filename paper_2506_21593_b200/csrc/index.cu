@@ -295,6 +295,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) exact_scan_kernel(ScanArgs p) {
                         cnt = min(cnt + 1, K);
                     }
                 }
+                __syncwarp();  // every lane's last read of the list precedes lane 0's count write
                 if (lane == 0) tkc[qi] = cnt;
                 __syncwarp();
             }
