@@ -54,7 +54,8 @@ def first_occurrences(rows: np.ndarray, pos: np.ndarray) -> np.ndarray:
     if n == 0:
         return np.zeros(0, dtype=np.int64)
     ar = np.arange(n, dtype=np.int32)
-    pos[rows[::-1]] = ar[::-1]  # repeated indices: the last assignment (= earliest position) wins
+    pos[rows] = n
+    np.minimum.at(pos, rows, ar)  # unbuffered: every repeat is applied (plain fancy assignment has no order guarantee)
     return np.flatnonzero(pos[rows] == ar)
 
 
