@@ -61,8 +61,8 @@ def parse():
     ap.add_argument("--cpu-queries", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-rows", type=int, default=1_000_000, help="reference arm: rows per timed sample")
-    ap.add_argument("--configs", default="c2,c3,c5",
-                    help="secondary BASELINE configs measured after the headline (rank 0, N=1): c2,c3,c5 or ''")
+    ap.add_argument("--configs", default="c2,c3,c4sweep,c5",
+                    help="secondary BASELINE configs measured after the headline (rank 0, N=1): c2,c3,c4sweep,c5 or ''")
     ap.add_argument("--kv-keys", type=int, default=100_000_000)
     ap.add_argument("--c5-queries", type=int, default=20_000, help="queries per C5 session")
     ap.add_argument("--c5-sessions", type=int, default=4)
@@ -450,6 +450,8 @@ def main():
                     configs["c2_semantic_cache"] = C.c2_semantic(peak, p8["how"])
                 elif name == "c3":
                     configs["c3_fixed_kv"] = C.c3_kv(float(pk.get("hbm_gbs", 6538.6)), n_keys=a.kv_keys)
+                elif name == "c4sweep":
+                    configs["c4_batch_sweep"] = C.c4_batch_sweep(idx, make_queries, a.n, a.dim)
                 elif name == "c5":
                     configs["c5_routed"] = C.c5_routed(idx, a.n, n_sessions=a.c5_sessions,
                                                        queries_per_session=a.c5_queries, workers=a.c5_workers,

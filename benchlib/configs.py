@@ -87,6 +87,34 @@ def c2_semantic(peak_tops: float, peak_how: str = "", n=1_000_000, d=768, batch=
     }
 
 
+# ---------------------------------------------------------------- C4 batch sweep
+def c4_batch_sweep(idx, make_queries, n: int, d: int, batches=(256, 1024, 8192), k=5, warmup=3, steps=5):
+    """The headline search (top-5 over the n x d store) at other batch sizes (SURVEY §8d
+    C4: sweep 256..16384); each step is one search_batch over queries already in HBM,
+    the store (10 GB of int8) is far larger than L2."""
+    import torch
+
+    out = {"workload": f"top-{k} over the {n} x {d} bench store, batch sweep (configs[3] shape, 1 GPU)",
+           "unit": "queries/s", "points": []}
+    for B in batches:
+        q = make_queries(n, d, B)
+        for _ in range(warmup):
+            idx.search_batch(q, k, validate=False, count=False)
+        torch.cuda.synchronize()
+        e0, e1 = _events()
+        e0.record()
+        for _ in range(steps):
+            idx.search_batch(q, k, validate=False, count=False)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        st = idx.stats()
+        out["points"].append({"batch": B, "value": B / (ms / 1e3), "ms_per_step": ms, "path": int(st.path),
+                              "fallback_queries": int(st.fallback)})
+        del q
+    return out
+
+
 # ---------------------------------------------------------------- C3
 def _key_arena(ids: np.ndarray):
     """'query-%09d' (or wider) keys as a UTF-8 arena + offsets, built with numpy."""
