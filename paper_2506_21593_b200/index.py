@@ -266,13 +266,13 @@ class FlatIndex:
 
     def _append_rows(self, arr: np.ndarray) -> None:
         torch = _torch()
-        t = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float32)).to("cuda", non_blocking=False)
+        t = torch.from_numpy(np.require(arr, np.float32, ["C", "W"])).to("cuda", non_blocking=False)
         _lib.check(self._L.pr_index_append(self._h, _lib.ptr(t), t.shape[0], _lib.stream_ptr()), "append")
 
     def _update_rows(self, rows: np.ndarray, arr: np.ndarray) -> None:
         torch = _torch()
         r = torch.from_numpy(rows).to("cuda")
-        t = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float32)).to("cuda")
+        t = torch.from_numpy(np.require(arr, np.float32, ["C", "W"])).to("cuda")
         _lib.check(self._L.pr_index_update_rows(self._h, _lib.ptr(r), _lib.ptr(t), t.shape[0], _lib.stream_ptr()),
                    "update")
 

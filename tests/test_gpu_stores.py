@@ -300,3 +300,42 @@ def test_akm_settle_from_rows_mixed_paths(gpu):
         assert list(akm.index.entry_ids()) == want, step
         for pid in want[:5]:
             assert akm.index.payload(pid).id == pid
+
+
+def test_deferred_payload_segments(gpu, rng):
+    """append_rows_from without payloads defers each row's payload to the source row;
+    truncate / clear / explicit appends / upserts interleave with it correctly."""
+    from paper_2506_21593_b200 import FlatIndex
+
+    d = 32
+    X = random_unit_vectors(rng, 50, d)
+    src = FlatIndex(dim=d)
+    src.extend_arrays([f"s{i}" for i in range(50)], X, payloads=[("src", i) for i in range(50)])
+    dst = FlatIndex(dim=d)
+    want: list = []
+
+    def check():
+        assert len(dst) == len(want)
+        for r, (eid, p) in enumerate(want):
+            assert dst.id_at(r) == eid and dst.payload_at(r) == p, r
+            assert dst.payload(eid) == p
+
+    dst.append_rows_from(src, [3, 7, 9, 11], ["a3", "a7", "a9", "a11"])
+    want += [("a3", ("src", 3)), ("a7", ("src", 7)), ("a9", ("src", 9)), ("a11", ("src", 11))]
+    check()
+    dst.truncate(2)  # cuts into the segment
+    del want[2:]
+    dst.extend_arrays(["e0"], X[:1], payloads=["explicit"])
+    want.append(("e0", "explicit"))
+    dst.append_rows_from(src, [20, 21], ["a20", "a21"])
+    want += [("a20", ("src", 20)), ("a21", ("src", 21))]
+    check()
+    dst.insert("a20", X[5], "upserted")  # overwrite a deferred row in place
+    want[want.index(("a20", ("src", 20)))] = ("a20", "upserted")
+    check()
+    dst.clear()
+    want.clear()
+    dst.append_rows_from(src, [1], ["b1"])
+    want.append(("b1", ("src", 1)))
+    check()
+    assert dst.epoch == 2  # one truncate + one clear
