@@ -249,12 +249,15 @@ def _route_prefix(router, qs, vectors, mode):
         Vs = Vd[torch.from_numpy(spec).cuda()]
         r = kb.index.search_batch(Vs, cfg.akm_seed_k, mode=mode, validate=False, count=False)
         prof.note("kb", kb.index)
+        # the pre-batch AKM probe does not depend on the KB results: queue it behind the scan
+        ra = None
+        if L4 in pos and len(akm.index):
+            ra = akm.index.search_batch(Vs, 1, mode=mode, validate=False, count=False)
+            prof.note("akm", akm.index)
         kb_rows, kb_cnt = r.rows.cpu().numpy(), r.count.cpu().numpy()
         if L4 in pos:
             thr = akm.threshold
-            if len(akm.index):
-                ra = akm.index.search_batch(Vs, 1, mode=mode, validate=False, count=False)
-                prof.note("akm", akm.index)
+            if ra is not None:
                 l4_unsure[spec] |= (ra.count.cpu().numpy() > 0) & (ra.scores[:, 0].cpu().numpy() >= thr)
             # superset of in-batch seeds: every seed of every earlier speculative query
             # row-major boolean selection = the per-query seed lists concatenated in order
