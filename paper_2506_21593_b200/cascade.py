@@ -232,6 +232,27 @@ def _route_prefix(router, qs, vectors, mode):
         l2[js2] = (r.count.cpu().numpy() > 0) & (r.scores[:, 0].cpu().numpy() >= sc.threshold)
 
     prof.mark("l2")
+
+    def host_prep():
+        """Host work that needs no knowledge-base result (runs while the KB scan is in
+        flight): the batch's ledger shell, its cache entries, and for every L1/L2 hit
+        candidate the latest earlier query of the batch that wrote the same key."""
+        ledger = BatchLedger.__new__(BatchLedger)
+        now = time.monotonic_ns()
+        entries = [LedgerEntry(t, ledger, j, now) for j, t in enumerate(texts)]
+        l1l, l2l, scr = l1.tolist(), l2.tolist(), sc_row.tolist()
+        l1_first = L1 in pos and (L2 not in pos or pos[L1] < pos[L2])
+        sc_ids = sc_index._ids
+        src = [-1] * B
+        latest: dict[str, int] = {}
+        for j, t in enumerate(texts):
+            a, b = l1l[j], l2l[j]
+            if a or b:  # the serving one of L1 / L2 is the earlier of the two in probe order
+                src[j] = latest.get(t if (a and (l1_first or not b)) else sc_ids[scr[j]], -1)
+            latest[t] = j
+        return ledger, entries, src
+
+    prep = None
     # ---- L4/L5 speculation for every query that can reach them
     vec_pos = min(pos.get(L4, 99), pos.get(L5, 99))
     blocked = np.zeros(B, dtype=bool)
@@ -254,6 +275,7 @@ def _route_prefix(router, qs, vectors, mode):
         if L4 in pos and len(akm.index):
             ra = akm.index.search_batch(Vs, 1, mode=mode, validate=False, count=False)
             prof.note("akm", akm.index)
+        prep = host_prep()
         kb_rows, kb_cnt = r.rows.cpu().numpy(), r.count.cpu().numpy()
         if L4 in pos:
             thr = akm.threshold
@@ -357,22 +379,21 @@ def _route_prefix(router, qs, vectors, mode):
     for j, a in recalled.items():
         text[j], conf_l[j] = a.text, a.confidence
     # cache hits, in order: a hit serves a copy of the latest answer written for its key
-    hit = ((sv == v1) | (sv == v2)).tolist()
-    if any(hit):
+    if prep is None:
+        prep = host_prep()
+    ledger, entries, src = prep
+    hit_js = np.flatnonzero((sv == v1) | (sv == v2)).tolist()
+    if hit_js:
         codes, scr, kvv = sv.tolist(), sc_row[:p].tolist(), kv_val[:p].tolist()
-        sc_ids, kv_entry, sc_payload = sc_index._ids, kv.entry_at, sc_index.payload_at
-        latest: dict[str, int] = {}
-        for j, t in enumerate(texts[:p]):
-            if hit[j]:
-                code = codes[j]
-                i = latest.get(t if code == v1 else sc_ids[scr[j]])
-                if i is not None:
-                    text[j], conf_l[j] = text[i], conf_l[i]
-                elif code == v1:
-                    text[j], conf_l[j] = entry_text_conf(kv_entry(kvv[j]))
-                else:
-                    text[j], conf_l[j] = entry_text_conf(sc_payload(scr[j]))
-            latest[t] = j
+        kv_entry, sc_payload = kv.entry_at, sc_index.payload_at
+        for j in hit_js:  # ascending: an earlier writer's answer is already filled
+            i = src[j]
+            if i >= 0:
+                text[j], conf_l[j] = text[i], conf_l[i]
+            elif codes[j] == v1:
+                text[j], conf_l[j] = entry_text_conf(kv_entry(kvv[j]))
+            else:
+                text[j], conf_l[j] = entry_text_conf(sc_payload(scr[j]))
     conf = np.asarray(conf_l, dtype=np.float64)
     ctx_rows = CtxRows(kb_rows, slot[:p], kb_cnt, k_ctx, sv == v5)
     probe_prefix = {}
@@ -381,12 +402,11 @@ def _route_prefix(router, qs, vectors, mode):
         for M in order[: pos[L]]:
             pre.append(_PROBE[M, "rejected" if M is L3 else "miss"])
         probe_prefix[L] = tuple(pre)
-    ledger = BatchLedger(qs[:p], serving, lat, text, conf, ctx_rows, kb.index, probe_prefix)
+    ledger.__init__(qs[:p], serving, lat, text, conf, ctx_rows, kb.index, probe_prefix)
 
     prof.mark("materialise")
     # ---- write-back (router.py:333-337): KV in order (last write wins), SC payloads
-    now = time.monotonic_ns()
-    entries = [LedgerEntry(texts[j], ledger, j, now) for j in range(p)]
+    del entries[p:]
     kv.put_entries(texts[:p], entries, arena=arena)
     prof.mark("wb.kv")
     n_new_kept = int(np.searchsorted(new_js, p, side="left"))
