@@ -1,0 +1,54 @@
+"""The drop-in, end to end: the REAL reference router (``ragcascade.CascadeRouter``,
+installed offline into baseline/_ref — git-ignored, it travels to the GPU box with the
+tree) driving this package's GPU stores through the injection surface
+(src/router.py:195-223), replaying the reference's recorded 201-query trace.  Skipped
+when the reference install is absent; nothing reads /root/reference at run time."""
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+REF = os.path.join(os.path.dirname(HERE), "baseline", "_ref")
+
+
+@pytest.fixture(scope="module")
+def rc():
+    if not os.path.isdir(os.path.join(REF, "ragcascade")):
+        pytest.skip("reference not installed in baseline/_ref")
+    sys.path.insert(0, REF)
+    try:
+        import ragcascade
+    finally:
+        sys.path.remove(REF)
+    return ragcascade
+
+
+def test_reference_router_over_gpu_stores_replays_trace(gpu, rc):
+    import paper_2506_21593_b200 as g
+
+    with open(os.path.join(HERE, "golden", "router_trace.json")) as fh:
+        gold = json.load(fh)
+    emb = rc.HashEmbedder()
+    kb = g.ingest_corpus((json.dumps(c) for c in gold["corpus"]), emb)  # GPU store, reference vectors
+    router = rc.CascadeRouter(
+        embedder=emb, backend=rc.StubBackend(), knowledge_base=kb,
+        kv_cache=g.FixedKVCache(), semantic_cache=g.SemanticCache(emb), adaptive_memory=g.AdaptiveKnowledgeMemory(),
+    )
+    for i, q in enumerate(gold["queries"]):
+        if q["origin"] == "akm_probe":
+            router.adaptive_memory.settle()
+        answer, ev = router.route(rc.validate_query(q["text"], "s1"))
+        assert [[p.layer.wire_name, p.outcome] for p in ev.layers_probed] == q["probes"], i
+        assert ev.serving_layer.wire_name == q["serving"], i
+        assert answer.text == q["answer"], i
+        assert list(answer.supporting_passage_ids) == q["passages"], i
+    st, want = router.stats(), gold["stats"]
+    assert st["layer_counts"] == want["layer_counts"]
+    assert router.semantic_cache.index.search_count == want["sc_searches"]
+    assert router.adaptive_memory.index.search_count == want["akm_searches"]
+    assert router.adaptive_memory.inserted_total == want["akm_inserted_total"]
