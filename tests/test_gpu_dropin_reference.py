@@ -105,3 +105,108 @@ def test_reference_stores_on_gpu_flatindex_logs_identical(gpu, rc, monkeypatch):
                               seed=gold["seed"])
     logs = rc.run_simulation(cfg, router, rows)
     assert [list(log.to_jsonl_lines()) for log in logs] == gold["sessions"]
+
+
+def _sim_logs(rc, router, rows, n_sessions=2, per_session=150, seed=23):
+    cfg = rc.SimulationConfig(n_sessions=n_sessions, queries_per_session=per_session, seed=seed)
+    return [list(log.to_jsonl_lines()) for log in rc.run_simulation(cfg, router, rows)]
+
+
+@pytest.mark.parametrize("variant", ["lru_caches", "permuted", "disabled", "recall_table", "thresholds"])
+def test_live_ab_against_reference_stores(gpu, rc, variant):
+    """Live A/B on the GPU box: the reference simulation through the reference router, once
+    with the reference's own stores and once with the GPU drop-ins (same config, same seed),
+    under capped caches (LRU / recency eviction), permuted and disabled layers, a recall
+    table, and non-default thresholds.  Session logs must be byte-identical."""
+    import paper_2506_21593_b200 as g
+    from ragcascade.datagen import synthetic_qa_dataset
+    from ragcascade.simulation import dataset_to_corpus
+
+    L = rc.LayerTag
+    rows = synthetic_qa_dataset(300, seed=42)
+    corpus = [json.dumps(r) for r in dataset_to_corpus(rows)]
+    emb = rc.HashEmbedder()
+    cfg_kw, kv_kw, sc_kw = {}, {}, {}
+    if variant == "lru_caches":
+        kv_kw, sc_kw = {"max_entries": 40}, {"max_entries": 30}
+    elif variant == "permuted":
+        cfg_kw["layer_order"] = (L.SEMANTIC_CACHE, L.ADAPTIVE_MEMORY, L.FIXED_KV, L.MEMORY_RECALL, L.NAIVE_RAG)
+    elif variant == "disabled":
+        cfg_kw["disabled_layers"] = frozenset({L.FIXED_KV, L.ADAPTIVE_MEMORY})
+    elif variant == "thresholds":
+        cfg_kw.update(semantic_threshold=0.6, akm_threshold=0.5, retrieval_k=2, akm_seed_k=5)
+
+    def backend():
+        tab = rc.StubKnowledgeTable()
+        if variant == "recall_table":
+            for r in rows[::5]:
+                tab.add(r["question"], "recalled: " + r["answer"], 0.8)
+        return rc.StubBackend(tab)
+
+    def build(stores):
+        cfg = rc.RouterConfig(**cfg_kw)
+        if stores == "ref":
+            kb = rc.MainKnowledgeBase()
+            rc.ingest_corpus(iter(corpus), emb, kb=kb)
+            kw = dict(kv_cache=rc.FixedKVCache(**kv_kw),
+                      semantic_cache=rc.SemanticCache(emb, threshold=cfg.semantic_threshold, **sc_kw),
+                      adaptive_memory=rc.AdaptiveKnowledgeMemory(threshold=cfg.akm_threshold))
+        else:
+            kb = g.ingest_corpus(iter(corpus), emb)
+            kw = dict(kv_cache=g.FixedKVCache(**kv_kw),
+                      semantic_cache=g.SemanticCache(emb, threshold=cfg.semantic_threshold, **sc_kw),
+                      adaptive_memory=g.AdaptiveKnowledgeMemory(threshold=cfg.akm_threshold))
+        return rc.CascadeRouter(embedder=emb, backend=backend(), knowledge_base=kb, config=cfg, **kw)
+
+    want = _sim_logs(rc, build("ref"), rows)
+    got = _sim_logs(rc, build("gpu"), rows)
+    assert got == want
+
+
+@pytest.mark.parametrize("variant", ["default", "permuted", "disabled", "recall_table", "thresholds"])
+def test_live_ab_route_batch_against_reference(gpu, rc, variant):
+    """This package's CascadeRouter.route_batch (batches of 64, GPU stores) against the
+    reference's run_simulation with the reference router and stores, live on the box:
+    session logs byte-identical under each router configuration."""
+    import paper_2506_21593_b200 as g
+    from benchlib.workloads import simulate_batched
+    from ragcascade.datagen import synthetic_qa_dataset
+    from ragcascade.simulation import dataset_to_corpus
+
+    rows = synthetic_qa_dataset(300, seed=42)
+    corpus = [json.dumps(r) for r in dataset_to_corpus(rows)]
+
+    def cfg_kw(L):
+        if variant == "permuted":
+            return {"layer_order": (L.SEMANTIC_CACHE, L.ADAPTIVE_MEMORY, L.FIXED_KV, L.MEMORY_RECALL, L.NAIVE_RAG)}
+        if variant == "disabled":
+            return {"disabled_layers": frozenset({L.FIXED_KV, L.MEMORY_RECALL})}
+        if variant == "thresholds":
+            return {"semantic_threshold": 0.6, "akm_threshold": 0.5, "retrieval_k": 2, "akm_seed_k": 5}
+        return {}
+
+    def table(mod):
+        tab = mod.StubKnowledgeTable()
+        if variant == "recall_table":
+            for r in rows[::5]:
+                tab.add(r["question"], "recalled: " + r["answer"], 0.8)
+        return tab
+
+    # reference: its own router, stores and simulation driver
+    emb_r = rc.HashEmbedder()
+    kb_r = rc.MainKnowledgeBase()
+    rc.ingest_corpus(iter(corpus), emb_r, kb=kb_r)
+    cfg_r = rc.RouterConfig(**cfg_kw(rc.LayerTag))
+    ref = rc.CascadeRouter(embedder=emb_r, backend=rc.StubBackend(table(rc)), knowledge_base=kb_r, config=cfg_r,
+                           semantic_cache=rc.SemanticCache(emb_r, threshold=cfg_r.semantic_threshold),
+                           adaptive_memory=rc.AdaptiveKnowledgeMemory(threshold=cfg_r.akm_threshold))
+    sim = rc.SimulationConfig(n_sessions=2, queries_per_session=150, seed=29)
+    want = [list(log.to_jsonl_lines()) for log in rc.run_simulation(sim, ref, rows)]
+    # this package: route_batch over the GPU stores
+    emb = g.HashEmbedder()
+    cfg = g.RouterConfig(**cfg_kw(g.LayerTag))
+    mine = g.CascadeRouter(embedder=emb, backend=g.StubBackend(table(g)), knowledge_base=g.ingest_corpus(iter(corpus), emb),
+                           config=cfg, semantic_cache=g.SemanticCache(emb, threshold=cfg.semantic_threshold),
+                           adaptive_memory=g.AdaptiveKnowledgeMemory(threshold=cfg.akm_threshold))
+    got = simulate_batched(mine, [r["question"] for r in rows], n_sessions=2, n_queries=150, seed=29, batch=64)
+    assert got == want
