@@ -210,3 +210,72 @@ def test_live_ab_route_batch_against_reference(gpu, rc, variant):
                            adaptive_memory=g.AdaptiveKnowledgeMemory(threshold=cfg.akm_threshold))
     got = simulate_batched(mine, [r["question"] for r in rows], n_sessions=2, n_queries=150, seed=29, batch=64)
     assert got == want
+
+
+@pytest.mark.parametrize("mode_name", ["MODE_EXACT", "MODE_TENSOR", "MODE_TENSOR_I8", "MODE_AUTO"])
+def test_live_flatindex_search_against_reference(gpu, rc, rng, mode_name):
+    """GPU FlatIndex.search against the reference's own FlatIndex.search, live: ids, ranks
+    and score bits, on a store with exact duplicates (tie tiers), self-hits and near-hits."""
+    import numpy as np
+
+    import paper_2506_21593_b200 as g
+    from conftest import random_unit_vectors
+
+    mode = getattr(g, mode_name)
+    n, d = 6000, 256
+    X = random_unit_vectors(rng, n, d)
+    X[100:140] = X[7]  # a tier of 41 bit-identical rows
+    ref, mine = rc.FlatIndex(dim=d), g.FlatIndex(dim=d)
+    ids = [f"e{i}" for i in range(n)]
+    for i in range(n):
+        ref.insert(ids[i], X[i])
+    mine.extend_arrays(ids, X)
+    Q = random_unit_vectors(rng, 40, d)
+    Q[0], Q[1] = X[7], X[2500]  # self-hits (snap) incl. the tied tier
+    for i in range(2, 12):
+        v = X[int(rng.integers(n))] + 0.02 * random_unit_vectors(rng, 1, d)[0]
+        Q[i] = (v / np.linalg.norm(v.astype(np.float64))).astype(np.float32)
+    for k in (1, 5, 10):
+        for q in Q:
+            want = ref.search(q, k)
+            got = mine.search(q, k, mode=mode)
+            assert [(h.entry_id, h.score, h.rank) for h in got] == [(h.entry_id, h.score, h.rank) for h in want]
+
+
+def test_live_snapshot_interop_with_reference(gpu, rc, rng):
+    """RCFLATIX both ways, live: the reference restores the GPU index's snapshot and the GPU
+    index restores the reference's, each searching to the same hits."""
+    import paper_2506_21593_b200 as g
+    from conftest import random_unit_vectors
+
+    d = 64
+    X = random_unit_vectors(rng, 500, d)
+    ref = rc.FlatIndex(dim=d)
+    for i in range(500):
+        ref.insert(f"r{i}", X[i], {"i": i})
+    ref.insert("r3", X[9], {"i": "upserted"})
+    mine = g.FlatIndex.restore(ref.snapshot())
+    back = rc.FlatIndex.restore(mine.snapshot())
+    assert mine.snapshot() == ref.snapshot() == back.snapshot()
+    for q in random_unit_vectors(rng, 10, d):
+        want = [(h.entry_id, h.score) for h in ref.search(q, 7)]
+        assert [(h.entry_id, h.score) for h in mine.search(q, 7)] == want
+        assert [(h.entry_id, h.score) for h in back.search(q, 7)] == want
+
+
+def test_live_hash_embedder_against_reference(gpu, rc):
+    """Device HashEmbedder against the reference's HashEmbedder on mixed texts (ASCII, unicode
+    word characters, punctuation-only, long), bit for bit."""
+    import numpy as np
+
+    import paper_2506_21593_b200 as g
+
+    texts = ["What is the capital of France?", "naïve café über straße", "日本語のテキスト", "!!! ??? ...",
+             "x", "a_b c-d e.f", " ".join(f"tok{i}" for i in range(300)), "Mixed 123 numbers 4.5e6",
+             "tab\tseparated\nlines", "emoji 🙂 inside"]
+    texts += [f"question {i} about topic {i % 13} and item {i * 7}" for i in range(500)]
+    ref, mine = rc.HashEmbedder(), g.HashEmbedder()
+    V = mine.embed_device(texts).cpu().numpy()
+    for t, v in zip(texts, V):
+        w = np.asarray(ref.embed(t).values, dtype=np.float32)
+        assert np.array_equal(v, w), t
