@@ -279,3 +279,31 @@ def test_live_hash_embedder_against_reference(gpu, rc):
     for t, v in zip(texts, V):
         w = np.asarray(ref.embed(t).values, dtype=np.float32)
         assert np.array_equal(v, w), t
+
+
+@pytest.mark.parametrize("max_entries", [None, 25])
+def test_live_kv_cache_random_ops_against_reference(gpu, rc, rng, max_entries):
+    """Random put / get / clear sequences on the reference FixedKVCache and the GPU table
+    (unbounded and LRU-capped): every get, hit/miss counter and size agrees."""
+    import paper_2506_21593_b200 as g
+
+    ref, mine = rc.FixedKVCache(max_entries=max_entries), g.FixedKVCache(max_entries=max_entries)
+    keys = [f"key {i}" for i in range(60)] + ["", "é", "key 1 ", "KEY 1"]
+    for step in range(1500):
+        op = rng.random()
+        t = keys[int(rng.integers(len(keys)))]
+        if op < 0.45:
+            a = rc.AnswerRecord(text=f"answer {step}", layer=rc.LayerTag.NAIVE_RAG, confidence=0.5,
+                                supporting_passage_ids=("p",))
+            ref.put(t, a)
+            mine.put(t, a)
+        elif op < 0.995:
+            x, y = ref.get(t), mine.get(t)
+            assert (x is None) == (y is None), step
+            if x is not None:
+                assert (x.text, x.layer.wire_name) == (y.text, y.layer.wire_name), step
+        else:
+            ref.clear()
+            mine.clear()
+        assert len(ref) == len(mine), step
+    assert (ref.hits, ref.misses) == (mine.hits, mine.misses)
