@@ -140,28 +140,49 @@ int pr_index_snap_flags(const pr_index *h, const float *d_q, int64_t nq, int k, 
                         void *stream);
 
 /* ---- fixed KV cache: caches.py:45-101 (FixedKVCache) --------------------
- * Keys are the UTF-8 bytes of the query text (byte-exact, caches.py:57-58);
- * the table stores their 128-bit fingerprint (pr_fingerprint) in an
- * open-addressing table of 64-byte buckets probed by 4-lane groups with
- * 16-byte loads.  Values are int64 write sequence numbers: a larger value is
- * a later write, so concurrent puts resolve last-write-wins (caches.py:67-74). */
+ * Keys are the UTF-8 bytes of the query text, compared BYTE-EXACT like the
+ * reference dict (caches.py:57-65): the table holds a 64-bit tag
+ * of each key's 128-bit fingerprint and a record {value, length, key bytes};
+ * a tag match is confirmed against the record bytes, so a fingerprint
+ * collision can never serve another key's answer.  Key batches are a UTF-8
+ * arena d_bytes + int64 offsets d_off[n+1] (key i = d_bytes[d_off[i]..d_off[i+1])).
+ * Values are non-negative int64 write sequence numbers: a larger value is a
+ * later write, so puts of one key in one batch resolve last-write-wins
+ * (caches.py:67-74).  The *_owned variants act only on the keys a shard owns
+ * (owner = pr_kv_owner, bits disjoint from the bucket index); the other keys
+ * are skipped (get: value -1, hit 0) without touching the table. */
 int pr_kv_create(int64_t capacity, pr_kv **out);
+/* flags: PR_KV_WEAK_HASH keeps 2 tag bits and 4 home buckets, so distinct keys collide
+ * on purpose — a test hook for the byte-exact confirmation; never used by the product */
+#define PR_KV_WEAK_HASH 1u
+int pr_kv_create_ex(int64_t capacity, uint32_t flags, pr_kv **out);
 int pr_kv_destroy(pr_kv *h);
-/* fingerprint n keys: bytes d_bytes[d_off[i] .. d_off[i+1]) -> d_fp[2i], d_fp[2i+1] */
+/* fingerprint n keys -> d_fp[2i], d_fp[2i+1] (the 128-bit hash behind tag, bucket and owner) */
 int pr_fingerprint(const uint8_t *d_bytes, const int64_t *d_off, int64_t n, uint64_t *d_fp, void *stream);
 void pr_fingerprint_host(const uint8_t *bytes, int64_t len, uint64_t out[2]);
-int pr_kv_put(pr_kv *h, const uint64_t *d_fp, const int64_t *d_vals, int64_t n, void *stream);
+/* shard owner of each key for a table hash-partitioned over `world` ranks */
+int pr_kv_owner(const uint8_t *d_bytes, const int64_t *d_off, int64_t n, int world, int32_t *d_owner, void *stream);
+/* upsert (caches.py:67-77); nbytes = d_off[n] - d_off[0] (reserves record space without a device read) */
+int pr_kv_put_text(pr_kv *h, const uint8_t *d_bytes, const int64_t *d_off, int64_t n, int64_t nbytes,
+                   const int64_t *d_vals, void *stream);
+int pr_kv_put_text_owned(pr_kv *h, const uint8_t *d_bytes, const int64_t *d_off, int64_t n, int64_t nbytes,
+                         const int64_t *d_vals, int rank, int world, void *stream);
 /* d_vals[i] = value or -1; d_hit[i] = 1/0 (hit/miss, caches.py:57-65) */
-int pr_kv_get(pr_kv *h, const uint64_t *d_fp, int64_t n, int64_t *d_vals, uint8_t *d_hit, void *stream);
-/* fused fingerprint + probe over a text arena (the L1 probe of a routed batch) */
 int pr_kv_get_text(pr_kv *h, const uint8_t *d_bytes, const int64_t *d_off, int64_t n, int64_t *d_vals,
                    uint8_t *d_hit, void *stream);
-int pr_kv_erase(pr_kv *h, const uint64_t *d_fp, int64_t n, void *stream);
+int pr_kv_get_text_owned(pr_kv *h, const uint8_t *d_bytes, const int64_t *d_off, int64_t n, int rank, int world,
+                         int64_t *d_vals, uint8_t *d_hit, void *stream);
+/* remove keys (LRU eviction, caches.py:75-77) */
+int pr_kv_erase_text(pr_kv *h, const uint8_t *d_bytes, const int64_t *d_off, int64_t n, void *stream);
 int pr_kv_clear(pr_kv *h, void *stream);
-int64_t pr_kv_size(pr_kv *h);      /* live keys (synchronises) */
-int64_t pr_kv_capacity(pr_kv *h);  /* slots */
-/* dump live (fingerprint, value) pairs; returns count written (<= max) or <0 */
-int64_t pr_kv_export(pr_kv *h, uint64_t *d_fp, int64_t *d_vals, int64_t max, void *stream);
+int64_t pr_kv_size(pr_kv *h, void *stream); /* live keys (synchronises `stream`) */
+int64_t pr_kv_capacity(pr_kv *h);           /* slots */
+/* device bytes: slot table, record arena in use, of which garbage (erased / lost-race records) */
+int pr_kv_memory(pr_kv *h, int64_t *slot_bytes, int64_t *arena_bytes, int64_t *garbage_bytes, void *stream);
+/* values of every live key (any order); returns the live count (> max: only max written) or < 0 */
+int64_t pr_kv_export(pr_kv *h, int64_t *d_vals, int64_t max, void *stream);
+/* value v -> d_map[v] for every live key with 0 <= v < nmap (host arena compaction) */
+int pr_kv_remap(pr_kv *h, const int64_t *d_map, int64_t nmap, void *stream);
 
 /* ---- device HashEmbedder: embedding.py:117-160 ------------
  * Texts are a UTF-8 arena + offsets as for pr_fingerprint; d_out is fp32

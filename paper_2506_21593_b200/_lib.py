@@ -78,17 +78,22 @@ SIGNATURES = {
     "pr_merge_shards": (c_int, [c_vp, c_vp, c_vp, c_vp, c_int, c_i64, c_int, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "pr_index_snap_flags": (c_int, [c_vp, c_vp, c_i64, c_int, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "pr_kv_create": (c_int, [c_i64, c_vp]),
+    "pr_kv_create_ex": (c_int, [c_i64, c_u32, c_vp]),
     "pr_kv_destroy": (c_int, [c_vp]),
     "pr_fingerprint": (c_int, [c_vp, c_vp, c_i64, c_vp, c_vp]),
     "pr_fingerprint_host": (None, [c_vp, c_i64, c_vp]),
-    "pr_kv_put": (c_int, [c_vp, c_vp, c_vp, c_i64, c_vp]),
-    "pr_kv_get": (c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
+    "pr_kv_owner": (c_int, [c_vp, c_vp, c_i64, c_int, c_vp, c_vp]),
+    "pr_kv_put_text": (c_int, [c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp]),
+    "pr_kv_put_text_owned": (c_int, [c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_int, c_int, c_vp]),
     "pr_kv_get_text": (c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
-    "pr_kv_erase": (c_int, [c_vp, c_vp, c_i64, c_vp]),
+    "pr_kv_get_text_owned": (c_int, [c_vp, c_vp, c_vp, c_i64, c_int, c_int, c_vp, c_vp, c_vp]),
+    "pr_kv_erase_text": (c_int, [c_vp, c_vp, c_vp, c_i64, c_vp]),
     "pr_kv_clear": (c_int, [c_vp, c_vp]),
-    "pr_kv_size": (c_i64, [c_vp]),
+    "pr_kv_size": (c_i64, [c_vp, c_vp]),
     "pr_kv_capacity": (c_i64, [c_vp]),
-    "pr_kv_export": (c_i64, [c_vp, c_vp, c_vp, c_i64, c_vp]),
+    "pr_kv_memory": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "pr_kv_export": (c_i64, [c_vp, c_vp, c_i64, c_vp]),
+    "pr_kv_remap": (c_int, [c_vp, c_vp, c_i64, c_vp]),
     "pr_hash_embed": (c_int, [c_vp, c_vp, c_i64, c_int, ctypes.c_uint64, c_vp, c_vp, c_vp]),
     "pr_blake2b64_host": (ctypes.c_uint64, [ctypes.c_uint64, ctypes.c_char_p, c_vp, c_i64]),
 }

@@ -4,12 +4,12 @@ Drop-ins for ``ragcascade/caches.py``: ``FixedKVCache`` (:45-101),
 ``SemanticCache`` (:104-228) and ``writeback`` (:231-253), same methods,
 counters and error behaviour.
 
-* FixedKVCache keys libpentarag's open-addressing table by the 128-bit
-  fingerprint of the query's UTF-8 bytes (byte-exact keys, caches.py:57-58);
-  the table value is the write sequence number, i.e. the index of the
-  CacheEntry in a host arena, so "last write wins" (caches.py:67-74) is a
-  device atomicMax.  ``get_batch`` fingerprints and probes a whole batch in
-  one kernel (the L1 probe of a routed batch).
+* FixedKVCache keys libpentarag's open-addressing table by the query's UTF-8
+  bytes (byte-exact: tag matches are confirmed against the stored key bytes,
+  caches.py:57-58); the table value is the write sequence number, i.e. the
+  index of the CacheEntry in a host arena, so "last write wins"
+  (caches.py:67-74) is a device atomicMax.  ``get_batch`` hashes and probes a
+  whole batch in one kernel (the L1 probe of a routed batch).
 * SemanticCache keeps its entries in a device FlatIndex keyed by query text
   (upsert) and answers ``lookup`` with the exact top-1 + inclusive threshold
   (caches.py:131-145); ``lookup_batch`` does it for a [B, dim] batch.
@@ -44,7 +44,7 @@ class CacheEntry:
     created_at_ns: int
 
 
-from .textarena import encode_texts  # noqa: E402  (re-exported for callers)
+from .textarena import encode_texts, to_device  # noqa: E402,F401  (encode_texts re-exported for callers)
 
 
 def fingerprint_host(text: str) -> tuple[int, int]:
@@ -56,15 +56,16 @@ def fingerprint_host(text: str) -> tuple[int, int]:
     return int(out[0]), int(out[1])
 
 
-def _fp_tensor(pairs: list[tuple[int, int]]):
-    import torch
-
-    a = np.array(pairs, dtype=np.uint64).reshape(-1, 2).view(np.int64)
-    return torch.from_numpy(a).cuda()
-
-
 class FixedKVCache:
-    """Exact-match cache: raw query text -> last answer written."""
+    """Exact-match cache: raw query text -> last answer written.
+
+    The device table (libpentarag ``pr_kv_*``) maps the key's bytes to an int64 write
+    sequence number; the number indexes the host arena of written entries.  Hits are
+    byte-exact (the table confirms every tag match against the stored key bytes).
+    The host arena is compacted when overwritten / evicted entries make up half of it,
+    so memory follows the live keys, not the write traffic (caches.py:75-77)."""
+
+    _COMPACT_MIN = 4096
 
     def __init__(self, max_entries: int | None = None, *, capacity: int = 1024):
         if max_entries is not None and max_entries < 1:
@@ -75,7 +76,8 @@ class FixedKVCache:
         _lib.check(self._L.pr_kv_create(max(capacity, max_entries or 0), ctypes.byref(h)), "pr_kv_create")
         self._h = h
         self._max_entries = max_entries
-        self._arena: list[CacheEntry] = []
+        self._arena: list = []
+        self._compact_at = self._COMPACT_MIN
         self._recency: OrderedDict[str, None] = OrderedDict()
         self._lock = threading.Lock()
         self.hits = 0
@@ -98,12 +100,12 @@ class FixedKVCache:
     def get(self, query_text: str) -> AnswerRecord | None:
         import torch
 
-        fp = _fp_tensor([fingerprint_host(query_text)])
+        arena = to_device([query_text])
         vals = torch.empty(1, dtype=torch.int64, device="cuda")
         hit = torch.empty(1, dtype=torch.uint8, device="cuda")
         with self._lock:
-            _lib.check(self._L.pr_kv_get(self._h, _lib.ptr(fp), 1, _lib.ptr(vals), _lib.ptr(hit),
-                                         _lib.stream_ptr()), "kv_get")
+            _lib.check(self._L.pr_kv_get_text(self._h, _lib.ptr(arena[0]), _lib.ptr(arena[1]), 1, _lib.ptr(vals),
+                                              _lib.ptr(hit), _lib.stream_ptr()), "kv_get")
             v = int(vals.item())
             if not int(hit.item()):
                 self.misses += 1
@@ -116,34 +118,60 @@ class FixedKVCache:
 
     def __len__(self) -> int:
         with self._lock:
-            return int(self._L.pr_kv_size(self._h))
+            return self._size()
+
+    def _size(self) -> int:
+        return int(self._L.pr_kv_size(self._h, _lib.stream_ptr()))
 
     def clear(self) -> None:
         with self._lock:
             _lib.check(self._L.pr_kv_clear(self._h, _lib.stream_ptr()), "kv_clear")
             self._arena.clear()
+            self._compact_at = self._COMPACT_MIN
             self._recency.clear()
 
     def stats(self) -> dict[str, int]:
         with self._lock:
-            return {"hits": self.hits, "misses": self.misses, "size": int(self._L.pr_kv_size(self._h))}
+            return {"hits": self.hits, "misses": self.misses, "size": self._size()}
 
-    def export_entries(self) -> list[dict[str, Any]]:
+    def _live_seqs(self) -> np.ndarray:
+        """Sorted write sequence numbers of every live key (synchronises)."""
         import torch
 
-        with self._lock:
-            n = int(self._L.pr_kv_size(self._h))
-            fps = torch.empty((max(n, 1), 2), dtype=torch.int64, device="cuda")
+        n = self._size()
+        while True:
             vals = torch.empty(max(n, 1), dtype=torch.int64, device="cuda")
-            got = self._L.pr_kv_export(self._h, _lib.ptr(fps), _lib.ptr(vals), n, _lib.stream_ptr())
+            got = int(self._L.pr_kv_export(self._h, _lib.ptr(vals), n, _lib.stream_ptr()))
             if got < 0:
-                _lib.check(int(got), "kv_export")
-            seqs = sorted(int(s) for s in vals[:got].cpu().numpy())
+                _lib.check(got, "kv_export")
+            if got <= n:
+                return np.sort(vals[:got].cpu().numpy())
+            n = got
+
+    def export_entries(self) -> list[dict[str, Any]]:
+        with self._lock:
             out = []
-            for s in seqs:  # write order == OrderedDict order of the reference
+            for s in self._live_seqs().tolist():  # write order == OrderedDict order of the reference
                 e = self._arena[s]
                 out.append({"query_text": e.query_text, "answer": e.answer.to_dict(), "created_at_ns": e.created_at_ns})
             return out
+
+    def _maybe_compact(self) -> None:
+        """Drop arena entries no live key points at (overwritten or evicted), keeping
+        write order; the device values are remapped in one kernel."""
+        import torch
+
+        if len(self._arena) < self._compact_at:
+            return
+        live = self._live_seqs()
+        if 2 * live.size <= len(self._arena):
+            remap = np.full(len(self._arena), -1, dtype=np.int64)
+            remap[live] = np.arange(live.size, dtype=np.int64)
+            d_map = torch.from_numpy(remap).cuda()
+            _lib.check(self._L.pr_kv_remap(self._h, _lib.ptr(d_map), remap.size, _lib.stream_ptr()), "kv_remap")
+            arena = self._arena
+            self._arena = [arena[i] for i in live.tolist()]
+        self._compact_at = max(self._COMPACT_MIN, 2 * len(self._arena))
 
     # -- batch surface ------------------------------------------------------
     def put_many(self, texts: Sequence[str], answers: Sequence[AnswerRecord]) -> None:
@@ -153,27 +181,22 @@ class FixedKVCache:
 
     def put_entries(self, texts: Sequence[str], entries: Sequence, *, arena=None) -> None:
         """Bulk put of prepared entries (CacheEntry or ledger.LedgerEntry).
-        ``arena``: the device UTF-8 arena (data, offsets) of a batch whose first
-        ``len(texts)`` texts these are (skips re-encoding)."""
+        ``arena``: the ``DeviceTexts`` of a batch whose first ``len(texts)`` texts
+        these are (skips re-encoding)."""
         import torch
 
-        if not texts:
+        n = len(texts)
+        if not n:
             return
         if arena is None:
-            data, off = encode_texts(texts)
+            arena = to_device(texts)
         with self._lock:
             base = len(self._arena)
             self._arena.extend(entries)
-            if arena is None:
-                d_data = torch.from_numpy(data).cuda()
-                d_off = torch.from_numpy(off).cuda()
-            else:
-                d_data, d_off = arena
-            fp = torch.empty((len(texts), 2), dtype=torch.int64, device="cuda")
-            seq = torch.arange(base, base + len(texts), dtype=torch.int64, device="cuda")
+            seq = torch.arange(base, base + n, dtype=torch.int64, device="cuda")
             s = _lib.stream_ptr()
-            _lib.check(self._L.pr_fingerprint(_lib.ptr(d_data), _lib.ptr(d_off), len(texts), _lib.ptr(fp), s), "fp")
-            _lib.check(self._L.pr_kv_put(self._h, _lib.ptr(fp), _lib.ptr(seq), len(texts), s), "kv_put")
+            _lib.check(self._L.pr_kv_put_text(self._h, _lib.ptr(arena[0]), _lib.ptr(arena[1]), n, arena.nbytes_of(n),
+                                              _lib.ptr(seq), s), "kv_put")
             if self._max_entries is not None:
                 for t in texts:
                     self._recency.pop(t, None)
@@ -182,8 +205,10 @@ class FixedKVCache:
                 while len(self._recency) > self._max_entries:
                     evict.append(self._recency.popitem(last=False)[0])
                 if evict:
-                    efp = _fp_tensor([fingerprint_host(t) for t in evict])
-                    _lib.check(self._L.pr_kv_erase(self._h, _lib.ptr(efp), len(evict), s), "kv_erase")
+                    ea = to_device(evict)
+                    _lib.check(self._L.pr_kv_erase_text(self._h, _lib.ptr(ea[0]), _lib.ptr(ea[1]), len(evict), s),
+                               "kv_erase")
+            self._maybe_compact()
 
     def probe_device(self, d_data, d_off, n: int):
         """Device-side batch probe: (values int64 [n], hit uint8 [n]) tensors.
@@ -199,11 +224,9 @@ class FixedKVCache:
 
     def get_batch(self, texts: Sequence[str]) -> list[AnswerRecord | None]:
         """Batched ``get``: one fingerprint+probe kernel for the whole batch."""
-        import torch
-
-        data, off = encode_texts(texts)
+        arena = to_device(texts)
         with self._lock:
-            vals, hit = self.probe_device(torch.from_numpy(data).cuda(), torch.from_numpy(off).cuda(), len(texts))
+            vals, hit = self.probe_device(arena[0], arena[1], len(texts))
             vals, hit = vals.cpu().numpy(), hit.cpu().numpy()
             nh = int(hit.sum())
             self.hits += nh

@@ -99,7 +99,16 @@ def route_batch(router, queries, vectors=None, *, mode: int = MODE_AUTO, materia
             continue
         V = None if vectors is None else vectors[i:]
         remaining = n - i
-        done, ledger = _route_prefix(router, queries[i:], V, mode)
+        try:
+            done, ledger = _route_prefix(router, queries[i:], V, mode)
+        except _BackendFailed:
+            # a backend call raised mid-batch: every store mutation of the batch was rolled
+            # back, so route the span one query at a time — the failing query raises (or is
+            # captured) exactly where independent route() calls would raise
+            for q in queries[i:]:
+                segs.append([one(q)])
+            stats["sequential"] += remaining
+            break
         if done:
             segs.append(ledger)
         stats["batched"] += done
@@ -218,6 +227,33 @@ def _route_prefix(router, qs, vectors, mode):
     if new_js.size:
         sc_index.extend_arrays([texts[j] for j in new_js], Vd[torch.from_numpy(new_js).cuda()],
                                payloads=[None] * int(new_js.size), validate=False)
+    counters = {a: getattr(backend, a) for a in _BACKEND_COUNTERS if isinstance(getattr(backend, a, None), int)}
+    try:
+        return _route_rest(router, qs, texts, arena, Vd, mode, prof, t_start, first, l1, kv_val, sc_index,
+                           n_pre_sc, new_js)
+    except _WritebackFailed as exc:
+        raise exc.__cause__
+    except Exception as exc:
+        # the rows appended above carry no payload yet: never leave them searchable
+        # (a later L2 hit on one would serve None).  Backend counters go back to
+        # where they were so the sequential re-route counts each call once.
+        if len(sc_index) > n_pre_sc:
+            sc_index.truncate(n_pre_sc)
+        for a, v in counters.items():
+            setattr(backend, a, v)
+        raise _BackendFailed() from exc
+
+
+def _route_rest(router, qs, texts, arena, Vd, mode, prof, t_start, first, l1, kv_val, sc_index, n_pre_sc, new_js):
+    import torch
+
+    cfg = router.config
+    order = cfg.probe_order()
+    pos = {L: i for i, L in enumerate(order)}
+    kv, sc, akm, kb = router.kv_cache, router.semantic_cache, router.adaptive_memory, router.knowledge_base
+    backend = router.backend
+    B = len(qs)
+    ar = np.arange(B)
     sc_limit = n_pre_sc + np.searchsorted(new_js, ar, side="left")  # rows written by queries i < j
     l2 = np.zeros(B, dtype=bool)
     sc_row = np.full(B, -1, dtype=np.int64)
@@ -405,7 +441,22 @@ def _route_prefix(router, qs, vectors, mode):
     ledger.__init__(qs[:p], serving, lat, text, conf, ctx_rows, kb.index, probe_prefix)
 
     prof.mark("materialise")
-    # ---- write-back (router.py:333-337): KV in order (last write wins), SC payloads
+    # ---- write-back (router.py:333-337): KV in order (last write wins), SC payloads.
+    # Every backend call of the batch happened above; a failure from here on is not a
+    # per-query error and is not retried query by query.
+    try:
+        return _writeback(router, qs, texts, arena, prof, p, entries, ledger, serving, slot, kb_rows, kb_cnt,
+                          sc_index, n_pre_sc, new_js)
+    except Exception as exc:
+        raise _WritebackFailed() from exc
+
+
+def _writeback(router, qs, texts, arena, prof, p, entries, ledger, serving, slot, kb_rows, kb_cnt, sc_index,
+               n_pre_sc, new_js):
+    cfg = router.config
+    order = cfg.probe_order()
+    pos = {L: i for i, L in enumerate(order)}
+    kv, sc, akm, kb = router.kv_cache, router.semantic_cache, router.adaptive_memory, router.knowledge_base
     del entries[p:]
     kv.put_entries(texts[:p], entries, arena=arena)
     prof.mark("wb.kv")
@@ -464,6 +515,17 @@ def _route_prefix(router, qs, vectors, mode):
             hist[k] = hist.get(k, 0.0) + v
         router.batch_profile_log = getattr(router, "batch_profile_log", []) + [dict(prof.times)]
     return p, ledger
+
+
+_BACKEND_COUNTERS = ("recall_calls", "context_calls")
+
+
+class _BackendFailed(Exception):
+    """Raised by _route_prefix after rolling its store mutations back."""
+
+
+class _WritebackFailed(Exception):
+    """Wraps a write-back failure so it passes the rollback handler unchanged."""
 
 
 class _Prof:

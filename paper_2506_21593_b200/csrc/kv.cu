@@ -1,35 +1,51 @@
 // Fixed KV cache on the GPU (reference: caches.py:45-101, FixedKVCache).
 //
-// The reference keys a dict by the raw query text: any one-byte difference
-// is a different key (caches.py:1-5).  Here a key is the 128-bit
-// fingerprint of its UTF-8 bytes (Murmur3-x64-128 construction, seed below,
-// top bit of the first word forced to 1 so {0,0} can mean EMPTY and {0,1}
-// TOMBSTONE).  Two distinct keys collide with probability ~2^-127; for 1e8
-// live keys the chance of any collision is ~1e16 / 2^128 ≈ 3e-23.
+// The reference keys a dict by the raw query text: any one-byte difference is a
+// different key (caches.py:57-65, tests/test_caches.py:36-45).  This table
+// is byte-exact the same way: a hit is confirmed against the stored key bytes, so a
+// fingerprint collision (accidental or constructed) can only cost a probe, never serve
+// another key's answer.
 //
-// Table: nslots 16-byte slots {w0, w1} (power of two) grouped in 64-byte
-// buckets of 4 slots, plus an int64 value per slot.  A probe is done by a
-// 4-lane group: each lane issues one 16-byte load, the group covers one
-// bucket per step, matches/empties are found with a warp ballot, and probing
-// moves linearly to the next bucket.  Values are write sequence numbers
-// supplied by the host; puts resolve with atomicMax, so the largest (latest)
-// write wins even when one batch writes the same key twice (caches.py:67-74).
+// Layout (HBM):
+//   slots  {u64 tag, u64 rec}[nslots]  nslots a power of two, grouped in 64-byte
+//          buckets of 4 slots.  tag = first word of the key's 128-bit fingerprint with
+//          the top bit forced (0 = EMPTY, 1 = TOMBSTONE); rec = byte offset of the key's
+//          record in the arena.  Load factor <= 0.5.
+//   arena  32-byte aligned records {i64 value, i32 len, i32 0, key bytes, zero pad}:
+//          one 32-byte sector holds the header and the first 16 key bytes, so a hit on
+//          a short key costs one bucket line plus one record sector.
+// Home bucket = second fingerprint word & (nbuckets - 1); the shard owner of a key is
+// taken from the first word's high half (disjoint from the bucket bits, sharded_kv.py).
+//
+// Probing is one thread per key: the thread hashes its key ONCE, loads its 64-byte
+// bucket with two 256-bit loads (both in flight), compares the four tags in
+// registers, confirms a tag match against the record (one more 256-bit load), and
+// moves to the next bucket only when the bucket is full of other keys.  A warp keeps
+// 32 independent probes in flight.  Values are int64 write sequence numbers supplied by
+// the host; a put resolves with atomicMax on the record's value, so the largest (latest)
+// write wins even when one batch writes a key twice (caches.py:67-74).
 #include <algorithm>
 
 #include "common.cuh"
 
 struct pr_kv {
-    uint64_t *slots = nullptr;   // [nslots][2]
-    int64_t *vals = nullptr;     // [nslots]
+    ulonglong2 *slots = nullptr;            // [nslots] {tag, record offset}
     int64_t nslots = 0;
-    unsigned long long *d_count = nullptr;  // [0] live, [1] tombstones
-    int64_t upper = 0;  // host-side upper bound of live + tombstones (no sync needed)
+    uint8_t *arena = nullptr;               // records
+    int64_t arena_cap = 0;                  // bytes
+    unsigned long long *d_count = nullptr;  // [0] live [1] tombstones [2] arena cursor [3] garbage bytes
+    int64_t upper = 0;                      // host bound on live + tombstones (no sync needed)
+    int64_t arena_upper = 0;                // host bound on the arena cursor
+    uint32_t flags = 0;                     // PR_KV_WEAK_HASH (tests only)
 };
 
 namespace pr {
 
 constexpr uint64_t FP_SEED = 0x5EED1024CA5CADE5ull;  // same constant family as embedding.py:33
 constexpr int KV_BUCKET = 4;
+constexpr int KV_THREADS = 128;
+constexpr int KV_REC_HDR = 16;
+constexpr uint64_t TAG_EMPTY = 0, TAG_TOMB = 1;
 
 __host__ __device__ __forceinline__ uint64_t rotl64(uint64_t x, int r) { return (x << r) | (x >> (64 - r)); }
 __host__ __device__ __forceinline__ uint64_t fmix64(uint64_t k) {
@@ -41,14 +57,24 @@ __host__ __device__ __forceinline__ uint64_t fmix64(uint64_t k) {
     return k;
 }
 
+template <bool DEV>
+__host__ __device__ __forceinline__ uint8_t ldb(const uint8_t *p) {
+#ifdef __CUDA_ARCH__
+    if (DEV) return __ldg(p);
+#endif
+    return *p;
+}
+
+// 128-bit fingerprint of the key bytes (Murmur3-x64-128 construction, fixed seed).
+template <bool DEV = false>
 __host__ __device__ inline void fingerprint128(const uint8_t *data, int64_t len, uint64_t *h_out, uint64_t *l_out) {
     const uint64_t c1 = 0x87c37b91114253d5ull, c2 = 0x4cf5ad432745937full;
     uint64_t h1 = FP_SEED, h2 = FP_SEED ^ 0x9E3779B97F4A7C15ull;
     const int64_t nblocks = len / 16;
     for (int64_t i = 0; i < nblocks; ++i) {
         uint64_t k1 = 0, k2 = 0;
-        for (int b = 7; b >= 0; --b) k1 = (k1 << 8) | data[16 * i + b];
-        for (int b = 7; b >= 0; --b) k2 = (k2 << 8) | data[16 * i + 8 + b];
+        for (int b = 7; b >= 0; --b) k1 = (k1 << 8) | ldb<DEV>(data + 16 * i + b);
+        for (int b = 7; b >= 0; --b) k2 = (k2 << 8) | ldb<DEV>(data + 16 * i + 8 + b);
         k1 *= c1; k1 = rotl64(k1, 31); k1 *= c2; h1 ^= k1;
         h1 = rotl64(h1, 27); h1 += h2; h1 = h1 * 5 + 0x52dce729;
         k2 *= c2; k2 = rotl64(k2, 33); k2 *= c1; h2 ^= k2;
@@ -57,8 +83,8 @@ __host__ __device__ inline void fingerprint128(const uint8_t *data, int64_t len,
     const uint8_t *tail = data + nblocks * 16;
     const int rem = (int)(len & 15);
     uint64_t k1 = 0, k2 = 0;
-    for (int b = rem - 1; b >= 8; --b) k2 = (k2 << 8) | tail[b];
-    for (int b = std::min(rem, 8) - 1; b >= 0; --b) k1 = (k1 << 8) | tail[b];
+    for (int b = rem - 1; b >= 8; --b) k2 = (k2 << 8) | ldb<DEV>(tail + b);
+    for (int b = std::min(rem, 8) - 1; b >= 0; --b) k1 = (k1 << 8) | ldb<DEV>(tail + b);
     if (rem > 8) { k2 *= c2; k2 = rotl64(k2, 33); k2 *= c1; h2 ^= k2; }
     if (rem > 0) { k1 *= c1; k1 = rotl64(k1, 31); k1 *= c2; h1 ^= k1; }
     h1 ^= (uint64_t)len;
@@ -70,21 +96,47 @@ __host__ __device__ inline void fingerprint128(const uint8_t *data, int64_t len,
     *l_out = h2;
 }
 
-__global__ void fingerprint_kernel(const uint8_t *__restrict__ bytes, const int64_t *__restrict__ off, int64_t n,
-                                   uint64_t *__restrict__ fp) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        uint64_t h, l;
-        fingerprint128(bytes + off[i], off[i + 1] - off[i], &h, &l);
-        fp[2 * i] = h;
-        fp[2 * i + 1] = l;
+__host__ __device__ __forceinline__ int owner_of(uint64_t tag, int world) {
+    return (int)((uint32_t)((tag >> 32) & 0x7fffffffu) % (uint32_t)world);
+}
+
+__host__ __device__ __forceinline__ int64_t rec_bytes(int64_t len) { return round_up<int64_t>(KV_REC_HDR + len, 32); }
+
+// little-endian word of up to 8 key bytes (missing bytes read as zero)
+__device__ __forceinline__ uint64_t key_word(const uint8_t *p, int n) {
+    uint64_t w = 0;
+    for (int b = (n < 8 ? n : 8) - 1; b >= 0; --b) w = (w << 8) | __ldg(p + b);
+    return w;
+}
+
+template <bool STRONG>
+__device__ __forceinline__ void ld256(const void *p, uint64_t &a, uint64_t &b, uint64_t &c, uint64_t &d) {
+    if (STRONG)
+        asm volatile("ld.relaxed.gpu.global.v4.u64 {%0,%1,%2,%3}, [%4];"
+                     : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p) : "memory");
+    else
+        asm("ld.global.cg.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
+}
+
+// Does the record at `rec` hold exactly the key bytes [key, key+len)?  The record's
+// first sector (header + 16 key bytes) is one 256-bit load; the value comes with it.
+template <bool STRONG>
+__device__ __forceinline__ bool rec_matches(const uint8_t *rec, const uint8_t *key, int64_t len, int64_t *val_out) {
+    uint64_t w0, w1, w2, w3;
+    ld256<STRONG>(rec, w0, w1, w2, w3);
+    if ((int64_t)(uint32_t)w1 != len) return false;
+    if (w2 != key_word(key, (int)std::min<int64_t>(len, 8))) return false;
+    if (len > 8 && w3 != key_word(key + 8, (int)std::min<int64_t>(len - 8, 8))) return false;
+    for (int64_t o = 16; o < len; o += 8) {
+        uint64_t r = STRONG ? *reinterpret_cast<const volatile uint64_t *>(rec + KV_REC_HDR + o)
+                            : __ldcg(reinterpret_cast<const unsigned long long *>(rec + KV_REC_HDR + o));
+        if (r != key_word(key + o, (int)std::min<int64_t>(len - o, 8))) return false;
     }
+    *val_out = (int64_t)w0;
+    return true;
 }
 
-__device__ __forceinline__ ulonglong2 ld_slot(const uint64_t *slots, int64_t s) {
-    return __ldcg(reinterpret_cast<const ulonglong2 *>(slots + 2 * s));
-}
-
-__device__ __forceinline__ bool cas_slot(uint64_t *slots, int64_t s, uint64_t e0, uint64_t e1, uint64_t n0, uint64_t n1,
+__device__ __forceinline__ bool cas_slot(ulonglong2 *slot, uint64_t e0, uint64_t e1, uint64_t n0, uint64_t n1,
                                          uint64_t &o0, uint64_t &o1) {
     asm volatile(
         "{\n\t.reg .b128 d, c, v;\n\t"
@@ -93,141 +145,215 @@ __device__ __forceinline__ bool cas_slot(uint64_t *slots, int64_t s, uint64_t e0
         "atom.global.cas.b128 d, [%6], c, v;\n\t"
         "mov.b128 {%0, %1}, d;\n\t}"
         : "=l"(o0), "=l"(o1)
-        : "l"(e0), "l"(e1), "l"(n0), "l"(n1), "l"(slots + 2 * s)
+        : "l"(e0), "l"(e1), "l"(n0), "l"(n1), "l"(slot)
         : "memory");
     return o0 == e0 && o1 == e1;
 }
 
-// 4-lane groups; every lane of the warp runs the loop until all groups finish
-template <int OP>  // 0 get, 1 put, 2 erase
-__global__ void kv_probe_kernel(uint64_t *slots, int64_t *vals, int64_t nslots, unsigned long long *counts,
-                                const uint64_t *__restrict__ fp, const uint8_t *__restrict__ bytes,
-                                const int64_t *__restrict__ off, int64_t n, const int64_t *__restrict__ in_vals,
-                                int64_t *__restrict__ out_vals, uint8_t *__restrict__ out_hit) {
-    const int lane = threadIdx.x & 31;
-    const int sub = lane & (KV_BUCKET - 1);
-    const int gshift = lane & ~(KV_BUCKET - 1);
-    const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / KV_BUCKET;
-    const int64_t nb = nslots / KV_BUCKET;
-    bool active = i < n;
-    uint64_t k0 = 0, k1 = 0;
-    if (active) {
-        if (fp) {
-            k0 = fp[2 * i];
-            k1 = fp[2 * i + 1];
-        } else {
-            // fused fingerprint: each lane of the group hashes (cheap, keeps lanes converged)
-            fingerprint128(bytes + off[i], off[i + 1] - off[i], &k0, &k1);
-        }
-    }
-    int64_t b = (int64_t)(k1 & (uint64_t)(nb - 1));
-    int64_t probes = 0;
-    while (__any_sync(0xffffffffu, active)) {
-        bool match = false, empty = false;
-        ulonglong2 v = make_ulonglong2(0, 0);
-        const int64_t s = b * KV_BUCKET + sub;
-        if (active) {
-            v = ld_slot(slots, s);
-            match = (v.x == k0 && v.y == k1);
-            empty = (v.x == 0 && v.y == 0);
-        }
-        const unsigned mm = (__ballot_sync(0xffffffffu, match) >> gshift) & 0xFu;
-        const unsigned me = (__ballot_sync(0xffffffffu, empty) >> gshift) & 0xFu;
-        if (active) {
-            if (mm) {
-                const int who = __ffs(mm) - 1;
-                if (sub == who) {
-                    if (OP == 0) {
-                        out_vals[i] = vals[s];
-                        out_hit[i] = 1;
-                    } else if (OP == 1) {
-                        atomicMax(reinterpret_cast<long long *>(vals + s), (long long)in_vals[i]);
-                    } else {
-                        uint64_t o0, o1;
-                        if (cas_slot(slots, s, k0, k1, 0, 1, o0, o1)) {
-                            vals[s] = -1;
-                            atomicAdd(&counts[0], (unsigned long long)-1ll);
-                            atomicAdd(&counts[1], 1ull);
-                        }
-                    }
-                }
-                active = false;
-            } else if (me) {
-                if (OP == 1) {
-                    const int who = __ffs(me) - 1;
-                    int claimed = 0;  // 1 = inserted, 2 = found ours, 0 = lost to another key
-                    if (sub == who) {
-                        uint64_t o0, o1;
-                        if (cas_slot(slots, s, 0, 0, k0, k1, o0, o1)) {
-                            atomicMax(reinterpret_cast<long long *>(vals + s), (long long)in_vals[i]);
-                            atomicAdd(&counts[0], 1ull);
-                            claimed = 1;
-                        } else if (o0 == k0 && o1 == k1) {
-                            atomicMax(reinterpret_cast<long long *>(vals + s), (long long)in_vals[i]);
-                            claimed = 2;
-                        }
-                    }
-                    // broadcast the outcome inside the 4-lane group
-                    const unsigned got = (__ballot_sync(__activemask(), claimed != 0) >> gshift) & 0xFu;
-                    if (got) active = false;  // else: re-read the same bucket
-                } else {
-                    if (OP == 0) {
-                        out_vals[i] = -1;
-                        out_hit[i] = 0;
-                    }
-                    active = false;
-                }
-            } else {
-                b = (b + 1) & (nb - 1);
-                if (++probes > nb) {  // table full: cannot happen below load 1.0
-                    if (OP == 0 && sub == 0) {
-                        out_vals[i] = -1;
-                        out_hit[i] = 0;
-                    }
-                    active = false;
-                }
-            }
-        }
+// copy a key into a fresh record (header + bytes, zero padded to the 32-byte record size)
+__device__ void write_record(uint8_t *rec, const uint8_t *key, int64_t len, int64_t val) {
+    uint64_t *w = reinterpret_cast<uint64_t *>(rec);
+    w[0] = (uint64_t)val;
+    w[1] = (uint64_t)(uint32_t)len;
+    const int64_t words = (rec_bytes(len) - KV_REC_HDR) / 8;
+    for (int64_t i = 0; i < words; ++i) {
+        const int64_t o = 8 * i;
+        w[2 + i] = o < len ? key_word(key + o, (int)std::min<int64_t>(len - o, 8)) : 0;
     }
 }
 
-__global__ void kv_export_kernel(const uint64_t *slots, const int64_t *vals, int64_t nslots, uint64_t *fp_out,
-                                 int64_t *val_out, int64_t max, unsigned long long *cursor) {
-    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nslots; s += (int64_t)gridDim.x * blockDim.x) {
-        uint64_t w0 = slots[2 * s];
-        if (w0 & 0x8000000000000000ull) {
-            unsigned long long p = atomicAdd(cursor, 1ull);
-            if ((int64_t)p < max) {
-                fp_out[2 * p] = w0;
-                fp_out[2 * p + 1] = slots[2 * s + 1];
-                val_out[p] = vals[s];
-            }
-        }
+struct KvTable {
+    ulonglong2 *slots;
+    int64_t nb;  // buckets (power of two)
+    uint8_t *arena;
+    unsigned long long *counts;
+    int weak;    // PR_KV_WEAK_HASH: 2-bit tags, 4 home buckets (forces collisions; tests only)
+};
+
+// tag + home-bucket hash of a key (the weak variant keeps 2 tag bits and 2 bucket bits)
+__device__ __forceinline__ void key_hash(const KvTable &t, const uint8_t *key, int64_t len, uint64_t &tag,
+                                         uint64_t &h2) {
+    fingerprint128<true>(key, len, &tag, &h2);
+    if (t.weak) {
+        tag = (tag & 0x8000000000000003ull) | 0x8000000000000000ull;
+        h2 &= 3;
     }
 }
 
-__global__ void kv_reinsert_kernel(const uint64_t *old_slots, const int64_t *old_vals, int64_t old_n, uint64_t *slots,
-                                   int64_t *vals, int64_t nslots, unsigned long long *counts) {
-    // one thread per old slot, single-lane linear probing (rebuild only)
-    const int64_t nb = nslots / KV_BUCKET;
-    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < old_n; s += (int64_t)gridDim.x * blockDim.x) {
-        uint64_t w0 = old_slots[2 * s], w1 = old_slots[2 * s + 1];
-        if (!(w0 & 0x8000000000000000ull)) continue;
-        int64_t b = (int64_t)(w1 & (uint64_t)(nb - 1));
-        for (int64_t probe = 0; probe <= nb; ++probe) {
+struct KeyBatch {
+    const uint8_t *bytes;
+    const int64_t *off;
+    int64_t n;
+};
+
+// ---- get: one thread per key ------------------------------------------------
+__global__ void __launch_bounds__(KV_THREADS) kv_get_kernel(KvTable t, KeyBatch kb, int rank, int world,
+                                                             int64_t *__restrict__ out_vals,
+                                                             uint8_t *__restrict__ out_hit) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= kb.n) return;
+    const int64_t a = __ldg(kb.off + i), len = __ldg(kb.off + i + 1) - a;
+    const uint8_t *key = kb.bytes + a;
+    uint64_t tag, h2;
+    key_hash(t, key, len, tag, h2);
+    int64_t val = -1;
+    if (world <= 1 || owner_of(tag, world) == rank) {
+        int64_t b = (int64_t)(h2 & (uint64_t)(t.nb - 1));
+        for (int64_t p = 0; p < t.nb; ++p) {
+            uint64_t s[8];
+            const ulonglong2 *bk = t.slots + b * KV_BUCKET;
+            ld256<false>(bk, s[0], s[1], s[2], s[3]);
+            ld256<false>(bk + 2, s[4], s[5], s[6], s[7]);
             bool done = false;
+#pragma unroll
             for (int j = 0; j < KV_BUCKET; ++j) {
-                uint64_t o0, o1;
-                int64_t t = b * KV_BUCKET + j;
-                if (cas_slot(slots, t, 0, 0, w0, w1, o0, o1)) {
-                    vals[t] = old_vals[s];
-                    atomicAdd(&counts[0], 1ull);
+                if (done) break;
+                if (s[2 * j] == tag) {
+                    int64_t v;
+                    if (rec_matches<false>(t.arena + s[2 * j + 1], key, len, &v)) {
+                        val = v;
+                        done = true;
+                    }
+                } else if (s[2 * j] == TAG_EMPTY) {
                     done = true;
-                    break;
                 }
             }
             if (done) break;
-            b = (b + 1) & (nb - 1);
+            b = (b + 1) & (t.nb - 1);
+        }
+    }
+    out_vals[i] = val;
+    out_hit[i] = val >= 0;
+}
+
+// ---- put (upsert) / erase: one thread per key --------------------------------
+template <bool ERASE>
+__global__ void __launch_bounds__(KV_THREADS) kv_update_kernel(KvTable t, KeyBatch kb, int rank, int world,
+                                                                const int64_t *__restrict__ in_vals) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= kb.n) return;
+    const int64_t a = __ldg(kb.off + i), len = __ldg(kb.off + i + 1) - a;
+    const uint8_t *key = kb.bytes + a;
+    uint64_t tag, h2;
+    key_hash(t, key, len, tag, h2);
+    if (world > 1 && owner_of(tag, world) != rank) return;
+    const int64_t v = ERASE ? -1 : in_vals[i];
+    int64_t myrec = -1;  // record allocated for an insert (kept across lost CAS races)
+    int64_t b = (int64_t)(h2 & (uint64_t)(t.nb - 1));
+    bool done = false;
+    for (int64_t p = 0; p < t.nb && !done; ++p) {
+        uint64_t s[8];
+        ulonglong2 *bk = t.slots + b * KV_BUCKET;
+        ld256<true>(bk, s[0], s[1], s[2], s[3]);
+        ld256<true>(bk + 2, s[4], s[5], s[6], s[7]);
+        for (int j = 0; j < KV_BUCKET && !done; ++j) {
+            uint64_t st = s[2 * j], sr = s[2 * j + 1];
+            for (;;) {  // re-examines slot j after a lost CAS
+                if (st == tag) {
+                    __threadfence();  // the record was published before its slot (see insert)
+                    int64_t old;
+                    if (rec_matches<true>(t.arena + sr, key, len, &old)) {
+                        if (ERASE) {
+                            uint64_t o0, o1;
+                            if (cas_slot(bk + j, st, sr, TAG_TOMB, 0, o0, o1)) {
+                                atomicAdd(&t.counts[0], (unsigned long long)-1ll);
+                                atomicAdd(&t.counts[1], 1ull);
+                                atomicAdd(&t.counts[3], (unsigned long long)rec_bytes(len));
+                            }
+                        } else {
+                            atomicMax(reinterpret_cast<long long *>(t.arena + sr), (long long)v);
+                        }
+                        done = true;
+                    }
+                    break;
+                }
+                if (st != TAG_EMPTY) break;  // another key or a tombstone: next slot
+                if (ERASE) {                 // first empty slot: the key is absent
+                    done = true;
+                    break;
+                }
+                if (myrec < 0) {
+                    myrec = (int64_t)atomicAdd(&t.counts[2], (unsigned long long)rec_bytes(len));
+                    write_record(t.arena + myrec, key, len, v);
+                    __threadfence();  // publish the record before the slot that points at it
+                }
+                uint64_t o0, o1;
+                if (cas_slot(bk + j, TAG_EMPTY, 0, tag, (uint64_t)myrec, o0, o1)) {
+                    atomicAdd(&t.counts[0], 1ull);
+                    myrec = -1;
+                    done = true;
+                    break;
+                }
+                st = o0;  // lost the race: look at what was written there
+                sr = o1;
+            }
+        }
+        b = (b + 1) & (t.nb - 1);
+    }
+    if (myrec >= 0) atomicAdd(&t.counts[3], (unsigned long long)rec_bytes(len));  // lost every race
+}
+
+// ---- fingerprints / shard owners ---------------------------------------------
+__global__ void fingerprint_kernel(KeyBatch kb, uint64_t *__restrict__ fp, int world, int32_t *__restrict__ owner) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < kb.n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t a = kb.off[i];
+        uint64_t h, l;
+        fingerprint128<true>(kb.bytes + a, kb.off[i + 1] - a, &h, &l);
+        if (fp) {
+            fp[2 * i] = h;
+            fp[2 * i + 1] = l;
+        }
+        if (owner) owner[i] = owner_of(h, world);
+    }
+}
+
+// ---- maintenance ---------------------------------------------------------------
+__global__ void kv_export_kernel(KvTable t, int64_t nslots, int64_t *val_out, int64_t max, unsigned long long *cursor) {
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nslots; s += (int64_t)gridDim.x * blockDim.x) {
+        const ulonglong2 sl = t.slots[s];
+        if (sl.x & 0x8000000000000000ull) {
+            unsigned long long p = atomicAdd(cursor, 1ull);
+            if ((int64_t)p < max) val_out[p] = *reinterpret_cast<const int64_t *>(t.arena + sl.y);
+        }
+    }
+}
+
+__global__ void kv_remap_kernel(KvTable t, int64_t nslots, const int64_t *__restrict__ map, int64_t nmap) {
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nslots; s += (int64_t)gridDim.x * blockDim.x) {
+        const ulonglong2 sl = t.slots[s];
+        if (sl.x & 0x8000000000000000ull) {
+            int64_t *v = reinterpret_cast<int64_t *>(t.arena + sl.y);
+            if (*v >= 0 && *v < nmap) *v = map[*v];
+        }
+    }
+}
+
+// rebuild: every live key of the old table is copied into a fresh arena (compacting away
+// overwritten/erased records) and re-inserted by its fingerprint (no duplicates exist)
+__global__ void kv_rebuild_kernel(const ulonglong2 *__restrict__ old_slots, int64_t old_n,
+                                  const uint8_t *__restrict__ old_arena, KvTable t) {
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < old_n; s += (int64_t)gridDim.x * blockDim.x) {
+        const ulonglong2 sl = old_slots[s];
+        if (!(sl.x & 0x8000000000000000ull)) continue;
+        const uint8_t *rec = old_arena + sl.y;
+        const int64_t len = (int64_t)(uint32_t)reinterpret_cast<const uint64_t *>(rec)[1];
+        const int64_t rb = rec_bytes(len);
+        const int64_t dst = (int64_t)atomicAdd(&t.counts[2], (unsigned long long)rb);
+        for (int64_t o = 0; o < rb; o += 8)
+            *reinterpret_cast<uint64_t *>(t.arena + dst + o) = *reinterpret_cast<const uint64_t *>(rec + o);
+        uint64_t tag, h2;
+        key_hash(t, rec + KV_REC_HDR, len, tag, h2);
+        int64_t b = (int64_t)(h2 & (uint64_t)(t.nb - 1));
+        bool done = false;
+        for (int64_t p = 0; p < t.nb && !done; ++p) {
+            for (int j = 0; j < KV_BUCKET && !done; ++j) {
+                uint64_t o0, o1;
+                if (cas_slot(t.slots + b * KV_BUCKET + j, TAG_EMPTY, 0, tag, (uint64_t)dst, o0, o1)) {
+                    atomicAdd(&t.counts[0], 1ull);
+                    done = true;
+                }
+            }
+            b = (b + 1) & (t.nb - 1);
         }
     }
 }
@@ -238,44 +364,107 @@ static int64_t slots_for(int64_t keys) {
     return s;
 }
 
-static int alloc_table(pr_kv *h, int64_t nslots, cudaStream_t st) {
-    PR_CUDA(cudaMalloc(&h->slots, (size_t)nslots * 16));
-    PR_CUDA(cudaMalloc(&h->vals, (size_t)nslots * 8));
-    PR_CUDA(cudaMemsetAsync(h->slots, 0, (size_t)nslots * 16, st));
-    PR_CUDA(cudaMemsetAsync(h->vals, 0xFF, (size_t)nslots * 8, st));
-    h->nslots = nslots;
+static KvTable table_of(pr_kv *h) {
+    return KvTable{h->slots, h->nslots / KV_BUCKET, h->arena, h->d_count, (h->flags & PR_KV_WEAK_HASH) ? 1 : 0};
+}
+
+static int read_counts(pr_kv *h, unsigned long long c[4], cudaStream_t st) {
+    PR_CUDA(cudaMemcpyAsync(c, h->d_count, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    PR_CUDA(cudaStreamSynchronize(st));
     return PR_OK;
 }
 
-static int grow(pr_kv *h, int64_t need_keys, cudaStream_t st) {
-    // rebuild into a table sized for need_keys (drops tombstones)
-    unsigned long long c[2];
-    PR_CUDA(cudaMemcpyAsync(c, h->d_count, sizeof(c), cudaMemcpyDeviceToHost, st));
-    PR_CUDA(cudaStreamSynchronize(st));
-    int64_t live = (int64_t)c[0];
-    int64_t want = slots_for(std::max<int64_t>(need_keys, live));
-    if (want == h->nslots && c[1] == 0) {
-        h->upper = live;
-        return PR_OK;
-    }
-    uint64_t *os = h->slots;
-    int64_t *ov = h->vals;
-    int64_t on = h->nslots;
-    int rc = alloc_table(h, want, st);
+// Rebuild into a table for `need_keys` live keys and an arena of `need_bytes` live record
+// bytes (drops tombstones and garbage records).  Synchronises the device: rare.
+static int rebuild(pr_kv *h, int64_t need_keys, int64_t need_bytes, cudaStream_t st) {
+    unsigned long long c[4];
+    int rc = read_counts(h, c, st);
     if (rc) return rc;
-    PR_CUDA(cudaMemsetAsync(h->d_count, 0, 2 * sizeof(unsigned long long), st));
-    int g = (int)std::min<int64_t>(ceil_div<int64_t>(on, 256), (int64_t)sm_count() * 16);
-    ::pr::count_launch();
-    kv_reinsert_kernel<<<g, 256, 0, st>>>(os, ov, on, h->slots, h->vals, h->nslots, h->d_count);
-    PR_LAUNCH_CHECK();
+    PR_CUDA(cudaDeviceSynchronize());
+    const int64_t live = (int64_t)c[0];
+    const int64_t live_bytes = (int64_t)c[2] - (int64_t)c[3];
+    const int64_t nslots = slots_for(std::max<int64_t>(need_keys, live));
+    const int64_t acap = std::max<int64_t>(4096, round_up<int64_t>(need_bytes + need_bytes / 2, 256));
+    ulonglong2 *ns = nullptr;
+    uint8_t *na = nullptr;
+    PR_CUDA(cudaMalloc(&ns, (size_t)nslots * sizeof(ulonglong2)));
+    if (cudaMalloc(&na, (size_t)acap) != cudaSuccess) {
+        cudaFree(ns);
+        PR_FAIL(PR_ERR_NOMEM, "kv arena: cannot allocate %lld bytes", (long long)acap);
+    }
+    PR_CUDA(cudaMemsetAsync(ns, 0, (size_t)nslots * sizeof(ulonglong2), st));
+    PR_CUDA(cudaMemsetAsync(h->d_count, 0, 4 * sizeof(unsigned long long), st));
+    ulonglong2 *os = h->slots;
+    uint8_t *oa = h->arena;
+    const int64_t on = h->nslots;
+    h->slots = ns;
+    h->nslots = nslots;
+    h->arena = na;
+    h->arena_cap = acap;
+    if (live > 0) {
+        const int g = (int)std::min<int64_t>(ceil_div<int64_t>(on, 256), (int64_t)sm_count() * 16);
+        ::pr::count_launch();
+        kv_rebuild_kernel<<<g, 256, 0, st>>>(os, on, oa, table_of(h));
+        PR_LAUNCH_CHECK();
+    }
     PR_CUDA(cudaStreamSynchronize(st));
     cudaFree(os);
-    cudaFree(ov);
+    cudaFree(oa);
     h->upper = live;
+    h->arena_upper = live_bytes;
     return PR_OK;
 }
 
-static int probe_grid(int64_t n) { return (int)std::max<int64_t>(1, ceil_div<int64_t>(n * KV_BUCKET, 256)); }
+static unsigned kv_grid(int64_t n) { return (unsigned)std::max<int64_t>(1, ceil_div<int64_t>(n, KV_THREADS)); }
+
+static int check_batch(pr_kv *h, const uint8_t *d_bytes, const int64_t *d_off, int64_t n, int rank, int world) {
+    if (!h || n < 0 || (n > 0 && (!d_bytes || !d_off))) PR_FAIL(PR_ERR_BAD_ARG, "bad kv key batch");
+    if (world < 1 || rank < 0 || rank >= world) PR_FAIL(PR_ERR_BAD_ARG, "bad shard rank/world");
+    return PR_OK;
+}
+
+static int put_impl(pr_kv *h, const uint8_t *d_bytes, const int64_t *d_off, int64_t n, int64_t nbytes,
+                    const int64_t *d_vals, int rank, int world, void *stream) {
+    int rc = check_batch(h, d_bytes, d_off, n, rank, world);
+    if (rc) return rc;
+    if (nbytes < 0 || !d_vals) PR_FAIL(PR_ERR_BAD_ARG, "bad kv_put");
+    if (n == 0) return PR_OK;
+    cudaStream_t st = as_stream(stream);
+    const int64_t rec_need = n * (KV_REC_HDR + 31) + nbytes;  // >= sum of rec_bytes over the batch
+    if (2 * (h->upper + n) > h->nslots || h->arena_upper + rec_need > h->arena_cap) {
+        unsigned long long c[4];
+        rc = read_counts(h, c, st);
+        if (rc) return rc;
+        h->upper = (int64_t)(c[0] + c[1]);
+        h->arena_upper = (int64_t)c[2];
+        const bool slots_short = 2 * (h->upper + n) > h->nslots;
+        const bool arena_short = h->arena_upper + rec_need > h->arena_cap;
+        if (slots_short || arena_short) {
+            rc = rebuild(h, (int64_t)c[0] + n, (int64_t)(c[2] - c[3]) + rec_need, st);
+            if (rc) return rc;
+        }
+    }
+    ::pr::count_launch();
+    kv_update_kernel<false><<<kv_grid(n), KV_THREADS, 0, st>>>(table_of(h), KeyBatch{d_bytes, d_off, n}, rank,
+                                                                world, d_vals);
+    PR_LAUNCH_CHECK();
+    h->upper += n;
+    h->arena_upper += rec_need;
+    return PR_OK;
+}
+
+static int get_impl(pr_kv *h, const uint8_t *d_bytes, const int64_t *d_off, int64_t n, int rank, int world,
+                    int64_t *d_vals, uint8_t *d_hit, void *stream) {
+    int rc = check_batch(h, d_bytes, d_off, n, rank, world);
+    if (rc) return rc;
+    if (n == 0) return PR_OK;
+    if (!d_vals || !d_hit) PR_FAIL(PR_ERR_BAD_ARG, "bad kv_get outputs");
+    ::pr::count_launch();
+    kv_get_kernel<<<kv_grid(n), KV_THREADS, 0, as_stream(stream)>>>(table_of(h), KeyBatch{d_bytes, d_off, n}, rank,
+                                                                      world, d_vals, d_hit);
+    PR_LAUNCH_CHECK();
+    return PR_OK;
+}
 
 }  // namespace pr
 
@@ -284,7 +473,7 @@ using namespace pr;
 extern "C" {
 
 void pr_fingerprint_host(const uint8_t *bytes, int64_t len, uint64_t out[2]) {
-    fingerprint128(bytes, len, &out[0], &out[1]);
+    fingerprint128<false>(bytes, len, &out[0], &out[1]);
 }
 
 int pr_fingerprint(const uint8_t *d_bytes, const int64_t *d_off, int64_t n, uint64_t *d_fp, void *stream) {
@@ -292,21 +481,40 @@ int pr_fingerprint(const uint8_t *d_bytes, const int64_t *d_off, int64_t n, uint
     if (n == 0) return PR_OK;
     int g = (int)std::min<int64_t>(ceil_div<int64_t>(n, 256), (int64_t)sm_count() * 16);
     ::pr::count_launch();
-    fingerprint_kernel<<<g, 256, 0, as_stream(stream)>>>(d_bytes, d_off, n, d_fp);
+    fingerprint_kernel<<<g, 256, 0, as_stream(stream)>>>(KeyBatch{d_bytes, d_off, n}, d_fp, 1, nullptr);
     PR_LAUNCH_CHECK();
     return PR_OK;
 }
 
-int pr_kv_create(int64_t capacity, pr_kv **out) {
-    if (!out || capacity < 0) PR_FAIL(PR_ERR_BAD_ARG, "bad kv_create");
+int pr_kv_owner(const uint8_t *d_bytes, const int64_t *d_off, int64_t n, int world, int32_t *d_owner, void *stream) {
+    if (n < 0 || world < 1 || (n > 0 && !d_owner)) PR_FAIL(PR_ERR_BAD_ARG, "bad kv_owner");
+    if (n == 0) return PR_OK;
+    int g = (int)std::min<int64_t>(ceil_div<int64_t>(n, 256), (int64_t)sm_count() * 16);
+    ::pr::count_launch();
+    fingerprint_kernel<<<g, 256, 0, as_stream(stream)>>>(KeyBatch{d_bytes, d_off, n}, nullptr, world, d_owner);
+    PR_LAUNCH_CHECK();
+    return PR_OK;
+}
+
+int pr_kv_create(int64_t capacity, pr_kv **out) { return pr_kv_create_ex(capacity, 0, out); }
+
+int pr_kv_create_ex(int64_t capacity, uint32_t flags, pr_kv **out) {
+    if (!out || capacity < 0 || (flags & ~PR_KV_WEAK_HASH)) PR_FAIL(PR_ERR_BAD_ARG, "bad kv_create");
     pr_kv *h = new pr_kv();
-    int rc = alloc_table(h, slots_for(capacity), nullptr);
-    if (rc) {
+    h->flags = flags;
+    h->nslots = slots_for(capacity);
+    h->arena_cap = std::max<int64_t>(4096, capacity * 48);
+    if (cudaMalloc(&h->slots, (size_t)h->nslots * sizeof(ulonglong2)) != cudaSuccess ||
+        cudaMalloc(&h->arena, (size_t)h->arena_cap) != cudaSuccess ||
+        cudaMalloc(&h->d_count, 4 * sizeof(unsigned long long)) != cudaSuccess) {
+        cudaFree(h->slots);
+        cudaFree(h->arena);
         delete h;
-        return rc;
+        cudaGetLastError();
+        PR_FAIL(PR_ERR_NOMEM, "kv_create: device allocation failed");
     }
-    PR_CUDA(cudaMalloc(&h->d_count, 2 * sizeof(unsigned long long)));
-    PR_CUDA(cudaMemset(h->d_count, 0, 2 * sizeof(unsigned long long)));
+    PR_CUDA(cudaMemset(h->slots, 0, (size_t)h->nslots * sizeof(ulonglong2)));
+    PR_CUDA(cudaMemset(h->d_count, 0, 4 * sizeof(unsigned long long)));
     PR_CUDA(cudaDeviceSynchronize());
     *out = h;
     return PR_OK;
@@ -316,55 +524,39 @@ int pr_kv_destroy(pr_kv *h) {
     if (!h) return PR_OK;
     cudaDeviceSynchronize();
     cudaFree(h->slots);
-    cudaFree(h->vals);
+    cudaFree(h->arena);
     cudaFree(h->d_count);
     delete h;
     return PR_OK;
 }
 
-int pr_kv_put(pr_kv *h, const uint64_t *d_fp, const int64_t *d_vals, int64_t n, void *stream) {
-    if (!h || n < 0) PR_FAIL(PR_ERR_BAD_ARG, "bad kv_put");
-    if (n == 0) return PR_OK;
-    cudaStream_t st = as_stream(stream);
-    if (2 * (h->upper + n) > h->nslots) {
-        int rc = grow(h, h->upper + n, st);
-        if (rc) return rc;
-    }
-    ::pr::count_launch();
-    kv_probe_kernel<1><<<probe_grid(n), 256, 0, st>>>(h->slots, h->vals, h->nslots, h->d_count, d_fp, nullptr, nullptr,
-                                                      n, d_vals, nullptr, nullptr);
-    PR_LAUNCH_CHECK();
-    h->upper += n;
-    return PR_OK;
+int pr_kv_put_text(pr_kv *h, const uint8_t *d_bytes, const int64_t *d_off, int64_t n, int64_t nbytes,
+                   const int64_t *d_vals, void *stream) {
+    return put_impl(h, d_bytes, d_off, n, nbytes, d_vals, 0, 1, stream);
 }
 
-int pr_kv_get(pr_kv *h, const uint64_t *d_fp, int64_t n, int64_t *d_vals, uint8_t *d_hit, void *stream) {
-    if (!h || n < 0) PR_FAIL(PR_ERR_BAD_ARG, "bad kv_get");
-    if (n == 0) return PR_OK;
-    ::pr::count_launch();
-    kv_probe_kernel<0><<<probe_grid(n), 256, 0, as_stream(stream)>>>(h->slots, h->vals, h->nslots, h->d_count, d_fp,
-                                                                     nullptr, nullptr, n, nullptr, d_vals, d_hit);
-    PR_LAUNCH_CHECK();
-    return PR_OK;
+int pr_kv_put_text_owned(pr_kv *h, const uint8_t *d_bytes, const int64_t *d_off, int64_t n, int64_t nbytes,
+                         const int64_t *d_vals, int rank, int world, void *stream) {
+    return put_impl(h, d_bytes, d_off, n, nbytes, d_vals, rank, world, stream);
 }
 
 int pr_kv_get_text(pr_kv *h, const uint8_t *d_bytes, const int64_t *d_off, int64_t n, int64_t *d_vals, uint8_t *d_hit,
                    void *stream) {
-    if (!h || n < 0) PR_FAIL(PR_ERR_BAD_ARG, "bad kv_get_text");
-    if (n == 0) return PR_OK;
-    ::pr::count_launch();
-    kv_probe_kernel<0><<<probe_grid(n), 256, 0, as_stream(stream)>>>(h->slots, h->vals, h->nslots, h->d_count, nullptr,
-                                                                     d_bytes, d_off, n, nullptr, d_vals, d_hit);
-    PR_LAUNCH_CHECK();
-    return PR_OK;
+    return get_impl(h, d_bytes, d_off, n, 0, 1, d_vals, d_hit, stream);
 }
 
-int pr_kv_erase(pr_kv *h, const uint64_t *d_fp, int64_t n, void *stream) {
-    if (!h || n < 0) PR_FAIL(PR_ERR_BAD_ARG, "bad kv_erase");
+int pr_kv_get_text_owned(pr_kv *h, const uint8_t *d_bytes, const int64_t *d_off, int64_t n, int rank, int world,
+                         int64_t *d_vals, uint8_t *d_hit, void *stream) {
+    return get_impl(h, d_bytes, d_off, n, rank, world, d_vals, d_hit, stream);
+}
+
+int pr_kv_erase_text(pr_kv *h, const uint8_t *d_bytes, const int64_t *d_off, int64_t n, void *stream) {
+    int rc = check_batch(h, d_bytes, d_off, n, 0, 1);
+    if (rc) return rc;
     if (n == 0) return PR_OK;
     ::pr::count_launch();
-    kv_probe_kernel<2><<<probe_grid(n), 256, 0, as_stream(stream)>>>(h->slots, h->vals, h->nslots, h->d_count, d_fp,
-                                                                     nullptr, nullptr, n, nullptr, nullptr, nullptr);
+    kv_update_kernel<true><<<kv_grid(n), KV_THREADS, 0, as_stream(stream)>>>(table_of(h), KeyBatch{d_bytes, d_off, n},
+                                                                             0, 1, nullptr);
     PR_LAUNCH_CHECK();
     return PR_OK;
 }
@@ -372,23 +564,34 @@ int pr_kv_erase(pr_kv *h, const uint64_t *d_fp, int64_t n, void *stream) {
 int pr_kv_clear(pr_kv *h, void *stream) {
     if (!h) PR_FAIL(PR_ERR_BAD_ARG, "null kv");
     cudaStream_t st = as_stream(stream);
-    PR_CUDA(cudaMemsetAsync(h->slots, 0, (size_t)h->nslots * 16, st));
-    PR_CUDA(cudaMemsetAsync(h->vals, 0xFF, (size_t)h->nslots * 8, st));
-    PR_CUDA(cudaMemsetAsync(h->d_count, 0, 2 * sizeof(unsigned long long), st));
+    PR_CUDA(cudaMemsetAsync(h->slots, 0, (size_t)h->nslots * sizeof(ulonglong2), st));
+    PR_CUDA(cudaMemsetAsync(h->d_count, 0, 4 * sizeof(unsigned long long), st));
     h->upper = 0;
+    h->arena_upper = 0;
     return PR_OK;
 }
 
-int64_t pr_kv_size(pr_kv *h) {
+int64_t pr_kv_size(pr_kv *h, void *stream) {
     if (!h) return -1;
-    unsigned long long c[2];
-    if (cudaMemcpy(c, h->d_count, sizeof(c), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    unsigned long long c[4];
+    if (read_counts(h, c, as_stream(stream)) != PR_OK) return -1;
     return (int64_t)c[0];
 }
 
 int64_t pr_kv_capacity(pr_kv *h) { return h ? h->nslots : -1; }
 
-int64_t pr_kv_export(pr_kv *h, uint64_t *d_fp, int64_t *d_vals, int64_t max, void *stream) {
+int pr_kv_memory(pr_kv *h, int64_t *slot_bytes, int64_t *arena_bytes, int64_t *garbage_bytes, void *stream) {
+    if (!h) PR_FAIL(PR_ERR_BAD_ARG, "null kv");
+    unsigned long long c[4];
+    int rc = read_counts(h, c, as_stream(stream));
+    if (rc) return rc;
+    if (slot_bytes) *slot_bytes = h->nslots * (int64_t)sizeof(ulonglong2);
+    if (arena_bytes) *arena_bytes = (int64_t)c[2];
+    if (garbage_bytes) *garbage_bytes = (int64_t)c[3];
+    return PR_OK;
+}
+
+int64_t pr_kv_export(pr_kv *h, int64_t *d_vals, int64_t max, void *stream) {
     if (!h || max < 0) PR_FAIL(PR_ERR_BAD_ARG, "bad kv_export");
     cudaStream_t st = as_stream(stream);
     unsigned long long *cur = nullptr;
@@ -396,13 +599,23 @@ int64_t pr_kv_export(pr_kv *h, uint64_t *d_fp, int64_t *d_vals, int64_t max, voi
     PR_CUDA(cudaMemsetAsync(cur, 0, sizeof(unsigned long long), st));
     int g = (int)std::min<int64_t>(ceil_div<int64_t>(h->nslots, 256), (int64_t)sm_count() * 16);
     ::pr::count_launch();
-    kv_export_kernel<<<g, 256, 0, st>>>(h->slots, h->vals, h->nslots, d_fp, d_vals, max, cur);
+    kv_export_kernel<<<g, 256, 0, st>>>(table_of(h), h->nslots, d_vals, max, cur);
     PR_LAUNCH_CHECK();
     unsigned long long c = 0;
     PR_CUDA(cudaMemcpyAsync(&c, cur, sizeof(c), cudaMemcpyDeviceToHost, st));
+    PR_CUDA(cudaFreeAsync(cur, st));
     PR_CUDA(cudaStreamSynchronize(st));
-    cudaFree(cur);
-    return (int64_t)std::min<unsigned long long>(c, (unsigned long long)max);
+    return (int64_t)c;  // may exceed max: the caller retries with a larger buffer
+}
+
+int pr_kv_remap(pr_kv *h, const int64_t *d_map, int64_t nmap, void *stream) {
+    if (!h || nmap < 0 || (nmap > 0 && !d_map)) PR_FAIL(PR_ERR_BAD_ARG, "bad kv_remap");
+    if (nmap == 0) return PR_OK;
+    int g = (int)std::min<int64_t>(ceil_div<int64_t>(h->nslots, 256), (int64_t)sm_count() * 16);
+    ::pr::count_launch();
+    kv_remap_kernel<<<g, 256, 0, as_stream(stream)>>>(table_of(h), h->nslots, d_map, nmap);
+    PR_LAUNCH_CHECK();
+    return PR_OK;
 }
 
 }  // extern "C"

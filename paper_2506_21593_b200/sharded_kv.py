@@ -1,15 +1,20 @@
 """Fixed-KV table hash-partitioned across ranks (one process per GPU).
 
-Rank r owns the keys whose 128-bit fingerprint satisfies ``fp_lo % world == r``
-(the low word is independent of the bucket bits the table probes with).  A
-put inserts only the owned keys of the batch; a lookup probes the whole batch
-on every rank — keys a rank does not own simply miss there (value -1) — and
-ONE all-reduce(max) over the int64 values combines them: the owner reports the
-key's write sequence number (>= 0), everyone else -1.  Byte-exact semantics
-are those of ``FixedKVCache`` (caches.py:57-77); last-write-wins still holds
-because a key lives on exactly one rank.
+Rank r owns the keys whose fingerprint maps to r: ``owner = (tag >> 32 & 0x7fffffff) %
+world`` where tag is the fingerprint's first word (``owner_host`` / device
+``pr_kv_owner``).  The table's home bucket comes from the SECOND word, so the ownership
+bits and the bucket bits are disjoint: every bucket of a rank's table is a home bucket
+for its keys (round 1 took both from the same low bits, so at world 8 only 1/8 of a
+rank's buckets could be home buckets).
 
-The probe and combine are injectable so the plumbing runs on CPU with gloo.
+A put inserts only the keys a rank owns; a lookup runs ``pr_kv_get_text_owned`` on every
+rank over the whole (broadcast) batch, which hashes each key once and probes only the
+owned ones — per-rank probe traffic is ~B/world — and ONE all-reduce(max) over the int64
+values combines them: the owner reports the key's write sequence number (>= 0), everyone
+else -1.  Byte-exact semantics are those of ``FixedKVCache`` (caches.py:57-77);
+last-write-wins still holds because a key lives on exactly one rank.
+
+The probe and insert are injectable so the plumbing runs on CPU with gloo.
 """
 from __future__ import annotations
 
@@ -17,7 +22,15 @@ import ctypes
 from typing import Callable
 
 from . import _lib
-from .textarena import encode_texts
+from .textarena import to_device
+
+
+def owner_host(text: str, world: int) -> int:
+    """Owning rank of ``text`` (host twin of the device ``owner_of``, kv.cu)."""
+    from .caches import fingerprint_host
+
+    tag = fingerprint_host(text)[0]
+    return ((tag >> 32) & 0x7FFFFFFF) % world
 
 
 class ShardedKV:
@@ -38,54 +51,60 @@ class ShardedKV:
             _lib.check(L.pr_kv_create(max(1024, capacity // max(1, self.world)), ctypes.byref(h)), "kv_create")
             self._h = h
 
-    # production path -------------------------------------------------------
-    def _fingerprints(self, texts):
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                _lib.load().pr_kv_destroy(h)
+            except Exception:  # noqa: BLE001
+                pass
+            self._h = None
+
+    def owners(self, arena):
+        """Owning rank of every key of a ``DeviceTexts`` arena (int32 device tensor)."""
         import torch
 
-        data, off = encode_texts(texts)
-        d_data, d_off = torch.from_numpy(data).cuda(), torch.from_numpy(off).cuda()
-        fp = torch.empty((len(texts), 2), dtype=torch.int64, device="cuda")
-        L = _lib.load()
-        _lib.check(L.pr_fingerprint(_lib.ptr(d_data), _lib.ptr(d_off), len(texts), _lib.ptr(fp), _lib.stream_ptr()),
-                   "fingerprint")
-        return fp
+        own = torch.empty(arena.n, dtype=torch.int32, device="cuda")
+        if arena.n:
+            _lib.check(_lib.load().pr_kv_owner(_lib.ptr(arena[0]), _lib.ptr(arena[1]), arena.n, self.world,
+                                               _lib.ptr(own), _lib.stream_ptr()), "kv_owner")
+        return own
 
-    def owner(self, fp):
-        """Owning rank of each fingerprint (int64 [n, 2] tensor)."""
-        lo = fp[:, 1]
-        return (lo.remainder(self.world) + self.world).remainder(self.world)  # non-negative modulo
-
-    def put(self, texts, values) -> int:
+    def put(self, texts, values) -> None:
         """Insert the keys this rank owns; ``values`` are int64 write sequence numbers."""
         import torch
 
-        fp = self._fingerprints(texts) if self._insert is None else None
         vals = torch.as_tensor(values, dtype=torch.int64)
         if self._insert is not None:
-            return self._insert(texts, vals, self.rank, self.world)
+            self._insert(texts, vals, self.rank, self.world)
+            return
+        arena = to_device(texts)
         vals = vals.cuda()
-        mine = self.owner(fp) == self.rank
-        fp_m, v_m = fp[mine].contiguous(), vals[mine].contiguous()
-        L = _lib.load()
-        if fp_m.shape[0]:
-            _lib.check(L.pr_kv_put(self._h, _lib.ptr(fp_m), _lib.ptr(v_m), fp_m.shape[0], _lib.stream_ptr()), "put")
-        return int(fp_m.shape[0])
+        _lib.check(_lib.load().pr_kv_put_text_owned(self._h, _lib.ptr(arena[0]), _lib.ptr(arena[1]), arena.n,
+                                                    arena.nbytes, _lib.ptr(vals), self.rank, self.world,
+                                                    _lib.stream_ptr()), "kv_put")
 
-    def get(self, texts):
-        """(values int64 [n], hit bool [n]) for every key, combined over ranks."""
+    def get_arena(self, arena):
+        """(values int64 [n], hit bool [n]) for a device text arena, combined over ranks."""
         import torch
         import torch.distributed as dist
 
-        if self._probe is not None:
-            vals = self._probe(texts, self.rank, self.world)
-        else:
-            data, off = encode_texts(texts)
-            d_data, d_off = torch.from_numpy(data).cuda(), torch.from_numpy(off).cuda()
-            vals = torch.empty(len(texts), dtype=torch.int64, device="cuda")
-            hit = torch.empty(len(texts), dtype=torch.uint8, device="cuda")
-            L = _lib.load()
-            _lib.check(L.pr_kv_get_text(self._h, _lib.ptr(d_data), _lib.ptr(d_off), len(texts), _lib.ptr(vals),
-                                        _lib.ptr(hit), _lib.stream_ptr()), "get")
+        vals = torch.empty(arena.n, dtype=torch.int64, device="cuda")
+        hit = torch.empty(arena.n, dtype=torch.uint8, device="cuda")
+        _lib.check(_lib.load().pr_kv_get_text_owned(self._h, _lib.ptr(arena[0]), _lib.ptr(arena[1]), arena.n,
+                                                    self.rank, self.world, _lib.ptr(vals), _lib.ptr(hit),
+                                                    _lib.stream_ptr()), "kv_get")
+        if self.world > 1:
+            dist.all_reduce(vals, op=dist.ReduceOp.MAX, group=self.group)
+        return vals, vals >= 0
+
+    def get(self, texts):
+        """(values int64 [n], hit bool [n]) for every key, combined over ranks."""
+        import torch.distributed as dist
+
+        if self._probe is None:
+            return self.get_arena(to_device(texts))
+        vals = self._probe(texts, self.rank, self.world)
         if self.world > 1:
             dist.all_reduce(vals, op=dist.ReduceOp.MAX, group=self.group)
         return vals, vals >= 0

@@ -23,8 +23,26 @@ def encode_texts(texts: Sequence[str]):
     return data, off
 
 
-def to_device(texts: Sequence[str]):
+class DeviceTexts(tuple):
+    """(data, offsets) device tensors of a text arena, unpackable as a pair; ``nbytes``
+    (the arena's byte count) and ``n`` (texts) stay on the host so callers never read
+    them back from the device."""
+
+    def __new__(cls, data, off, host_off):
+        t = super().__new__(cls, (data, off))
+        t.host_off = host_off
+        t.n = len(host_off) - 1
+        t.nbytes = int(host_off[-1])
+        return t
+
+    def nbytes_of(self, n: int) -> int:
+        """bytes of the first ``n`` texts"""
+        return int(self.host_off[n])
+
+
+def to_device(texts: Sequence[str]) -> DeviceTexts:
     import torch
 
     data, off = encode_texts(texts)
-    return torch.from_numpy(data).cuda(non_blocking=True), torch.from_numpy(off).cuda(non_blocking=True)
+    return DeviceTexts(torch.from_numpy(data).cuda(non_blocking=True), torch.from_numpy(off).cuda(non_blocking=True),
+                       off)

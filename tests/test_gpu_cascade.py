@@ -200,3 +200,47 @@ def test_concurrent_sessions_share_knowledge_base(gpu):
         t.join()
     assert outs == alone
     assert kb.index.search_count - c1 == c1 - c0  # the shared counter saw every probe of both
+
+
+def test_route_batch_backend_failure_rolls_back(gpu):
+    """A backend that raises mid-batch (BackendUnavailable from a remote LLM,
+    generation.py:118-175) must leave the stores as independent route() calls would:
+    the batch's pre-appended semantic-cache rows are rolled back, the span is re-routed
+    query by query, and with capture_errors only the failing query gets the error."""
+    from paper_2506_21593_b200 import BackendUnavailable, StubBackend, validate_query
+
+    class Flaky(StubBackend):
+        def generate_with_context(self, query_text, passages):
+            if query_text.startswith("BOOM"):
+                self.context_calls += 1
+                raise BackendUnavailable("remote backend down")
+            return super().generate_with_context(query_text, passages)
+
+    gold = _golden("simulation.json")
+    corpus, questions = gold["corpus"][:150], gold["questions"]
+    texts = [questions[i % 40] for i in range(120)]
+    texts[50] = "BOOM " + questions[77]
+    texts[90] = texts[50]  # the failed query is not cached: it fails again
+    seq, bat = _router(corpus, backend=Flaky()), _router(corpus, backend=Flaky())
+    qs = [validate_query(t, "s", query_id=f"q{i}", issued_at_ns=i) for i, t in enumerate(texts)]
+
+    def sig(r):
+        return ("error", type(r).__name__) if isinstance(r, Exception) else _sig(*r)
+
+    want = []
+    for q in qs:
+        try:
+            want.append(sig(seq.route(q)))
+        except BackendUnavailable as exc:
+            want.append(sig(exc))
+    got = []
+    for i in range(0, len(qs), 64):
+        got.extend(sig(r) for r in bat.route_batch(qs[i:i + 64], capture_errors=True))
+    assert got == want
+    assert got[50] == ("error", "BackendUnavailable")
+    assert seq.stats() == bat.stats()
+    assert seq.backend.context_calls == bat.backend.context_calls
+    assert seq.semantic_cache.index.entry_ids() == bat.semantic_cache.index.entry_ids()
+    assert all(p is not None for p in bat.semantic_cache.index._payloads)
+    with pytest.raises(BackendUnavailable):
+        bat.route_batch([validate_query(texts[50], "s", query_id="x", issued_at_ns=0)])

@@ -36,14 +36,12 @@ def _worker(rank, world, port, out):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_2506_21593_b200.caches import fingerprint_host
-        from paper_2506_21593_b200.sharded_kv import ShardedKV
+        from paper_2506_21593_b200.sharded_kv import ShardedKV, owner_host
 
         table: dict[str, int] = {}
 
         def own(t):
-            lo = fingerprint_host(t)[1]
-            return (lo - (1 << 64) if lo >= (1 << 63) else lo) % world
+            return owner_host(t, world)
 
         def insert(texts, vals, r, w):
             n = 0
@@ -80,3 +78,19 @@ def test_sharded_kv_equals_single_table(tmp_path):
     np.testing.assert_array_equal(got["vals"], exp)
     np.testing.assert_array_equal(got["hit"], exp >= 0)
     assert 0 < int(got["mine"]) < len(set(puts))  # rank 0 owns a strict subset
+
+
+def test_owner_bits_disjoint_from_bucket_bits():
+    """Round-1 bug: ownership and home bucket came from the same low fingerprint bits, so a
+    rank's keys could only use 1/world of its buckets.  Owner now comes from the tag's high
+    half and the bucket from the second word: every rank's keys spread over all buckets."""
+    from paper_2506_21593_b200.caches import fingerprint_host
+    from paper_2506_21593_b200.sharded_kv import owner_host
+
+    world, nb = 8, 1 << 10
+    buckets = [set() for _ in range(world)]
+    for i in range(40000):
+        t = f"query-{i:09d}"
+        buckets[owner_host(t, world)].add(fingerprint_host(t)[1] & (nb - 1))
+    for b in buckets:
+        assert len(b) > 0.95 * nb
