@@ -395,7 +395,8 @@ def _route_rest(router, qs, texts, arena, Vd, mode, prof, t_start, first, l1, kv
     # L5 answers first: they depend on no other query of the batch.  The stub LLM
     # answers with the top passage's annotation (generation.py:83-115): compute that
     # directly instead of building a context answer object per query
-    stub = isinstance(backend, generation.StubBackend) and 0.0 <= backend.context_confidence <= 1.0
+    # exact type: a subclass may override generate_with_context (and must be called)
+    stub = type(backend) is generation.StubBackend and 0.0 <= backend.context_confidence <= 1.0
     l5_js = np.flatnonzero(sv == v5).tolist()
     if l5_js:
         l5_slots = slot[l5_js]
