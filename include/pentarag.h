@@ -141,9 +141,9 @@ int pr_index_snap_flags(const pr_index *h, const float *d_q, int64_t nq, int k, 
 
 /* ---- fixed KV cache: caches.py:45-101 (FixedKVCache) --------------------
  * Keys are the UTF-8 bytes of the query text, compared BYTE-EXACT like the
- * reference dict (caches.py:57-65): the table holds a 64-bit tag
- * of each key's 128-bit fingerprint and a record {value, length, key bytes};
- * a tag match is confirmed against the record bytes, so a fingerprint
+ * reference dict (caches.py:57-65): 32-byte buckets of four
+ * {32-bit tag, record index} slots and 32-byte aligned records {value, length,
+ * key bytes}; a tag match is confirmed against the record bytes, so a hash
  * collision can never serve another key's answer.  Key batches are a UTF-8
  * arena d_bytes + int64 offsets d_off[n+1] (key i = d_bytes[d_off[i]..d_off[i+1])).
  * Values are non-negative int64 write sequence numbers: a larger value is a
@@ -157,7 +157,8 @@ int pr_kv_create(int64_t capacity, pr_kv **out);
 #define PR_KV_WEAK_HASH 1u
 int pr_kv_create_ex(int64_t capacity, uint32_t flags, pr_kv **out);
 int pr_kv_destroy(pr_kv *h);
-/* fingerprint n keys -> d_fp[2i], d_fp[2i+1] (the 128-bit hash behind tag, bucket and owner) */
+/* hash n keys -> d_fp[2i] = tag (32-bit, top bit set; also picks the shard owner),
+ * d_fp[2i+1] = bucket hash (32-bit, independent chain) */
 int pr_fingerprint(const uint8_t *d_bytes, const int64_t *d_off, int64_t n, uint64_t *d_fp, void *stream);
 void pr_fingerprint_host(const uint8_t *bytes, int64_t len, uint64_t out[2]);
 /* shard owner of each key for a table hash-partitioned over `world` ranks */
@@ -183,6 +184,9 @@ int pr_kv_memory(pr_kv *h, int64_t *slot_bytes, int64_t *arena_bytes, int64_t *g
 int64_t pr_kv_export(pr_kv *h, int64_t *d_vals, int64_t max, void *stream);
 /* value v -> d_map[v] for every live key with 0 <= v < nmap (host arena compaction) */
 int pr_kv_remap(pr_kv *h, const int64_t *d_map, int64_t nmap, void *stream);
+/* device L2 fetch granularity limit (cudaLimitMaxL2FetchGranularity, bytes; <= 0 only reads
+ * it): random 32-byte probes waste DRAM bandwidth when L2 fetches whole 128-byte lines */
+int pr_l2_fetch_granularity(int bytes, int *previous);
 
 /* ---- device HashEmbedder: embedding.py:117-160 ------------
  * Texts are a UTF-8 arena + offsets as for pr_fingerprint; d_out is fp32

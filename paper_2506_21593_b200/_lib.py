@@ -94,6 +94,7 @@ SIGNATURES = {
     "pr_kv_memory": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp]),
     "pr_kv_export": (c_i64, [c_vp, c_vp, c_i64, c_vp]),
     "pr_kv_remap": (c_int, [c_vp, c_vp, c_i64, c_vp]),
+    "pr_l2_fetch_granularity": (c_int, [c_int, c_vp]),
     "pr_hash_embed": (c_int, [c_vp, c_vp, c_i64, c_int, ctypes.c_uint64, c_vp, c_vp, c_vp]),
     "pr_blake2b64_host": (ctypes.c_uint64, [ctypes.c_uint64, ctypes.c_char_p, c_vp, c_i64]),
 }

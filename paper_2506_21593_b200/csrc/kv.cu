@@ -2,34 +2,37 @@
 //
 // The reference keys a dict by the raw query text: any one-byte difference is a
 // different key (caches.py:57-65, tests/test_caches.py:36-45).  This table
-// is byte-exact the same way: a hit is confirmed against the stored key bytes, so a
-// fingerprint collision (accidental or constructed) can only cost a probe, never serve
-// another key's answer.
+// is byte-exact the same way: a hit is confirmed against the stored key bytes, so a hash
+// collision (accidental or constructed) can only cost a probe, never serve another key's
+// answer.
 //
 // Layout (HBM):
-//   slots  {u64 tag, u64 rec}[nslots]  nslots a power of two, grouped in 64-byte
-//          buckets of 4 slots.  tag = first word of the key's 128-bit fingerprint with
-//          the top bit forced (0 = EMPTY, 1 = TOMBSTONE); rec = byte offset of the key's
-//          record in the arena.  Load factor <= 0.5.
-//   arena  32-byte aligned records {i64 value, i32 len, i32 0, key bytes, zero pad}:
-//          one 32-byte sector holds the header and the first 16 key bytes, so a hit on
-//          a short key costs one bucket line plus one record sector.
-// Home bucket = second fingerprint word & (nbuckets - 1); the shard owner of a key is
-// taken from the first word's high half (disjoint from the bucket bits, sharded_kv.py).
+//   slots  u64[nslots] = {u32 tag | u32 rec << 32}, nslots a power of two, grouped in
+//          32-byte buckets of 4 slots (ONE DRAM sector per bucket).  tag = 32-bit key hash
+//          with the top bit forced (0 = EMPTY, 1 = TOMBSTONE); rec = the key's record in
+//          32-byte units.  Load factor <= 0.5.
+//   arena  32-byte aligned records {i64 value, u32 len, u32 0, key bytes, zero pad}: one
+//          sector holds the header and the first 16 key bytes, so a hit on a short key
+//          costs one bucket sector plus one record sector.
+// Hash: two 32-bit multiply-rotate chains over the key's little-endian words (murmur3_32
+// round function, two seeds).  hA -> tag (and shard owner), hB -> home bucket: the
+// ownership bits and the bucket bits come from independent chains.  Only 32-bit integer
+// multiplies (no 64-bit emulation): the hash is a short dependency chain per key.
 //
-// Probing is one thread per key: the thread hashes its key ONCE, loads its 64-byte
-// bucket with two 256-bit loads (both in flight), compares the four tags in
-// registers, confirms a tag match against the record (one more 256-bit load), and
-// moves to the next bucket only when the bucket is full of other keys.  A warp keeps
-// 32 independent probes in flight.  Values are int64 write sequence numbers supplied by
-// the host; a put resolves with atomicMax on the record's value, so the largest (latest)
-// write wins even when one batch writes a key twice (caches.py:67-74).
+// Probing is one thread per key: it hashes its key ONCE (aligned 32-bit loads + funnel
+// shifts, not byte loads), reads its bucket with one 256-bit load, compares the four tags
+// in registers, confirms a tag match against the record (one more 256-bit load, which
+// also carries the value), and moves to the next bucket only when the bucket is full of
+// other keys.  A warp keeps 32 independent probes in flight.  Values are non-negative
+// int64 write sequence numbers supplied by the host; a put resolves with atomicMax on the
+// record's value, so the largest (latest) write wins even when one batch writes a key
+// twice (caches.py:67-74).
 #include <algorithm>
 
 #include "common.cuh"
 
 struct pr_kv {
-    ulonglong2 *slots = nullptr;            // [nslots] {tag, record offset}
+    unsigned long long *slots = nullptr;    // [nslots] {tag, record index}
     int64_t nslots = 0;
     uint8_t *arena = nullptr;               // records
     int64_t arena_cap = 0;                  // bytes
@@ -41,72 +44,104 @@ struct pr_kv {
 
 namespace pr {
 
-constexpr uint64_t FP_SEED = 0x5EED1024CA5CADE5ull;  // same constant family as embedding.py:33
-constexpr int KV_BUCKET = 4;
+constexpr int KV_BUCKET = 4;  // slots per 32-byte bucket
 constexpr int KV_THREADS = 128;
 constexpr int KV_REC_HDR = 16;
-constexpr uint64_t TAG_EMPTY = 0, TAG_TOMB = 1;
+constexpr uint32_t TAG_EMPTY = 0, TAG_TOMB = 1;
+constexpr uint32_t SEED_A = 0x5EED1024u, SEED_B = 0xCA5CADE5u;  // the HASH_SEED family (embedding.py:33)
+constexpr int64_t KV_MAX_ARENA = (int64_t)32 << 32;              // 32-bit record index x 32 bytes
 
-__host__ __device__ __forceinline__ uint64_t rotl64(uint64_t x, int r) { return (x << r) | (x >> (64 - r)); }
-__host__ __device__ __forceinline__ uint64_t fmix64(uint64_t k) {
-    k ^= k >> 33;
-    k *= 0xff51afd7ed558ccdull;
-    k ^= k >> 33;
-    k *= 0xc4ceb9fe1a85ec53ull;
-    k ^= k >> 33;
-    return k;
+__host__ __device__ __forceinline__ uint32_t rotl32(uint32_t x, int r) { return (x << r) | (x >> (32 - r)); }
+__host__ __device__ __forceinline__ uint32_t fmix32(uint32_t h) {
+    h ^= h >> 16;
+    h *= 0x85ebca6bu;
+    h ^= h >> 13;
+    h *= 0xc2b2ae35u;
+    h ^= h >> 16;
+    return h;
+}
+__host__ __device__ __forceinline__ uint32_t mix32(uint32_t h, uint32_t k) {
+    k *= 0xcc9e2d51u;
+    k = rotl32(k, 15);
+    k *= 0x1b873593u;
+    h ^= k;
+    h = rotl32(h, 13);
+    return h * 5u + 0xe6546b64u;
 }
 
-template <bool DEV>
-__host__ __device__ __forceinline__ uint8_t ldb(const uint8_t *p) {
-#ifdef __CUDA_ARCH__
-    if (DEV) return __ldg(p);
-#endif
-    return *p;
-}
-
-// 128-bit fingerprint of the key bytes (Murmur3-x64-128 construction, fixed seed).
-template <bool DEV = false>
-__host__ __device__ inline void fingerprint128(const uint8_t *data, int64_t len, uint64_t *h_out, uint64_t *l_out) {
-    const uint64_t c1 = 0x87c37b91114253d5ull, c2 = 0x4cf5ad432745937full;
-    uint64_t h1 = FP_SEED, h2 = FP_SEED ^ 0x9E3779B97F4A7C15ull;
-    const int64_t nblocks = len / 16;
-    for (int64_t i = 0; i < nblocks; ++i) {
-        uint64_t k1 = 0, k2 = 0;
-        for (int b = 7; b >= 0; --b) k1 = (k1 << 8) | ldb<DEV>(data + 16 * i + b);
-        for (int b = 7; b >= 0; --b) k2 = (k2 << 8) | ldb<DEV>(data + 16 * i + 8 + b);
-        k1 *= c1; k1 = rotl64(k1, 31); k1 *= c2; h1 ^= k1;
-        h1 = rotl64(h1, 27); h1 += h2; h1 = h1 * 5 + 0x52dce729;
-        k2 *= c2; k2 = rotl64(k2, 33); k2 *= c1; h2 ^= k2;
-        h2 = rotl64(h2, 31); h2 += h1; h2 = h2 * 5 + 0x38495ab5;
+// The two hash chains over little-endian 32-bit key words (the last one zero padded).
+struct KeyHash {
+    uint32_t a, b;
+    __host__ __device__ __forceinline__ void init(int64_t len) {
+        a = SEED_A ^ (uint32_t)len;
+        b = SEED_B ^ (uint32_t)(len * 0x9E3779B1u);
     }
-    const uint8_t *tail = data + nblocks * 16;
-    const int rem = (int)(len & 15);
-    uint64_t k1 = 0, k2 = 0;
-    for (int b = rem - 1; b >= 8; --b) k2 = (k2 << 8) | ldb<DEV>(tail + b);
-    for (int b = std::min(rem, 8) - 1; b >= 0; --b) k1 = (k1 << 8) | ldb<DEV>(tail + b);
-    if (rem > 8) { k2 *= c2; k2 = rotl64(k2, 33); k2 *= c1; h2 ^= k2; }
-    if (rem > 0) { k1 *= c1; k1 = rotl64(k1, 31); k1 *= c2; h1 ^= k1; }
-    h1 ^= (uint64_t)len;
-    h2 ^= (uint64_t)len;
-    h1 += h2; h2 += h1;
-    h1 = fmix64(h1); h2 = fmix64(h2);
-    h1 += h2; h2 += h1;
-    *h_out = h1 | 0x8000000000000000ull;  // never EMPTY/TOMBSTONE
-    *l_out = h2;
-}
+    __host__ __device__ __forceinline__ void word(uint32_t w) {
+        a = mix32(a, w);
+        b = mix32(b, w * 0x9E3779B1u + 0x7F4A7C15u);
+    }
+    __host__ __device__ __forceinline__ void fin(int64_t len, uint32_t &tag, uint32_t &hb) {
+        tag = fmix32(a ^ (uint32_t)len) | 0x80000000u;  // never EMPTY/TOMBSTONE
+        hb = fmix32(b ^ (uint32_t)(len >> 32) ^ 0x2545F491u);
+    }
+};
 
-__host__ __device__ __forceinline__ int owner_of(uint64_t tag, int world) {
-    return (int)((uint32_t)((tag >> 32) & 0x7fffffffu) % (uint32_t)world);
+__host__ __device__ __forceinline__ int owner_of(uint32_t tag, int world) {
+    return (int)((tag & 0x7fffffffu) % (uint32_t)world);
 }
 
 __host__ __device__ __forceinline__ int64_t rec_bytes(int64_t len) { return round_up<int64_t>(KV_REC_HDR + len, 32); }
 
-// little-endian word of up to 8 key bytes (missing bytes read as zero)
-__device__ __forceinline__ uint64_t key_word(const uint8_t *p, int n) {
-    uint64_t w = 0;
-    for (int b = (n < 8 ? n : 8) - 1; b >= 0; --b) w = (w << 8) | __ldg(p + b);
-    return w;
+// A key in device memory, read as aligned 32-bit words: word j = bytes [4j, 4j+4) of the
+// key (little-endian, zero beyond len).  Only words that hold key bytes are loaded.
+struct KeyRef {
+    const uint32_t *w;  // aligned base
+    int sh;             // misalignment in bits
+    int64_t len;
+    int64_t last;       // index (from w) of the aligned word holding the last key byte
+    __device__ __forceinline__ KeyRef(const uint8_t *p, int64_t n) {
+        const uintptr_t u = reinterpret_cast<uintptr_t>(p);
+        w = reinterpret_cast<const uint32_t *>(u & ~(uintptr_t)3);
+        sh = (int)(u & 3) * 8;
+        len = n;
+        last = n > 0 ? ((u & 3) + n - 1) >> 2 : -1;
+    }
+    __device__ __forceinline__ uint32_t ld(int64_t j) const { return j <= last ? __ldg(w + j) : 0u; }
+    // word j given the aligned words j and j+1 already loaded
+    __device__ __forceinline__ uint32_t join(uint32_t lo, uint32_t hi, int64_t j) const {
+        uint32_t v = sh ? __funnelshift_r(lo, hi, sh) : lo;
+        const int64_t rem = len - 4 * j;
+        return rem >= 4 ? v : (rem <= 0 ? 0u : v & ((1u << (8 * rem)) - 1u));
+    }
+    __device__ __forceinline__ uint32_t word(int64_t j) const { return join(ld(j), sh ? ld(j + 1) : 0u, j); }
+};
+
+__device__ __forceinline__ void hash_key(const KeyRef &k, int weak, uint32_t &tag, uint32_t &hb) {
+    KeyHash h;
+    h.init(k.len);
+    const int64_t nw = (k.len + 3) >> 2;
+    uint32_t lo = k.ld(0);
+    for (int64_t j = 0; j < nw; ++j) {
+        const uint32_t hi = k.sh ? k.ld(j + 1) : 0u;
+        h.word(k.join(lo, hi, j));
+        lo = k.sh ? hi : k.ld(j + 1);
+    }
+    h.fin(k.len, tag, hb);
+    if (weak) {  // PR_KV_WEAK_HASH: 2 tag bits, 4 home buckets
+        tag = (tag & 3u) | 0x80000000u;
+        hb &= 3u;
+    }
+}
+
+static inline void hash_host(const uint8_t *p, int64_t len, uint32_t &tag, uint32_t &hb) {
+    KeyHash h;
+    h.init(len);
+    for (int64_t o = 0; o < len; o += 4) {
+        uint32_t v = 0;
+        for (int b = (int)std::min<int64_t>(4, len - o) - 1; b >= 0; --b) v = (v << 8) | p[o + b];
+        h.word(v);
+    }
+    h.fin(len, tag, hb);
 }
 
 template <bool STRONG>
@@ -118,67 +153,53 @@ __device__ __forceinline__ void ld256(const void *p, uint64_t &a, uint64_t &b, u
         asm("ld.global.cg.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
 }
 
-// Does the record at `rec` hold exactly the key bytes [key, key+len)?  The record's
-// first sector (header + 16 key bytes) is one 256-bit load; the value comes with it.
 template <bool STRONG>
-__device__ __forceinline__ bool rec_matches(const uint8_t *rec, const uint8_t *key, int64_t len, int64_t *val_out) {
+__device__ __forceinline__ void ld128(const void *p, uint32_t &a, uint32_t &b, uint32_t &c, uint32_t &d) {
+    if (STRONG)
+        asm volatile("ld.relaxed.gpu.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "l"(p) : "memory");
+    else
+        asm("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "l"(p));
+}
+
+// Does the record at `rec` hold exactly the key's bytes?  The record's first sector
+// (header + key words 0..3) is one 256-bit load; the value comes with it.
+template <bool STRONG>
+__device__ __forceinline__ bool rec_matches(const uint8_t *rec, const KeyRef &k, int64_t *val_out) {
     uint64_t w0, w1, w2, w3;
     ld256<STRONG>(rec, w0, w1, w2, w3);
-    if ((int64_t)(uint32_t)w1 != len) return false;
-    if (w2 != key_word(key, (int)std::min<int64_t>(len, 8))) return false;
-    if (len > 8 && w3 != key_word(key + 8, (int)std::min<int64_t>(len - 8, 8))) return false;
-    for (int64_t o = 16; o < len; o += 8) {
-        uint64_t r = STRONG ? *reinterpret_cast<const volatile uint64_t *>(rec + KV_REC_HDR + o)
-                            : __ldcg(reinterpret_cast<const unsigned long long *>(rec + KV_REC_HDR + o));
-        if (r != key_word(key + o, (int)std::min<int64_t>(len - o, 8))) return false;
+    if ((int64_t)(uint32_t)w1 != k.len) return false;
+    if ((uint32_t)w2 != k.word(0) || (uint32_t)(w2 >> 32) != k.word(1) || (uint32_t)w3 != k.word(2) ||
+        (uint32_t)(w3 >> 32) != k.word(3))
+        return false;
+    for (int64_t g = 1; 16 * g < k.len; ++g) {
+        uint32_t r[4];
+        ld128<STRONG>(rec + KV_REC_HDR + 16 * g, r[0], r[1], r[2], r[3]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (r[q] != k.word(4 * g + q)) return false;
     }
     *val_out = (int64_t)w0;
     return true;
 }
 
-__device__ __forceinline__ bool cas_slot(ulonglong2 *slot, uint64_t e0, uint64_t e1, uint64_t n0, uint64_t n1,
-                                         uint64_t &o0, uint64_t &o1) {
-    asm volatile(
-        "{\n\t.reg .b128 d, c, v;\n\t"
-        "mov.b128 c, {%2, %3};\n\t"
-        "mov.b128 v, {%4, %5};\n\t"
-        "atom.global.cas.b128 d, [%6], c, v;\n\t"
-        "mov.b128 {%0, %1}, d;\n\t}"
-        : "=l"(o0), "=l"(o1)
-        : "l"(e0), "l"(e1), "l"(n0), "l"(n1), "l"(slot)
-        : "memory");
-    return o0 == e0 && o1 == e1;
-}
-
 // copy a key into a fresh record (header + bytes, zero padded to the 32-byte record size)
-__device__ void write_record(uint8_t *rec, const uint8_t *key, int64_t len, int64_t val) {
-    uint64_t *w = reinterpret_cast<uint64_t *>(rec);
-    w[0] = (uint64_t)val;
-    w[1] = (uint64_t)(uint32_t)len;
-    const int64_t words = (rec_bytes(len) - KV_REC_HDR) / 8;
-    for (int64_t i = 0; i < words; ++i) {
-        const int64_t o = 8 * i;
-        w[2 + i] = o < len ? key_word(key + o, (int)std::min<int64_t>(len - o, 8)) : 0;
-    }
+__device__ void write_record(uint8_t *rec, const KeyRef &k, int64_t val) {
+    uint64_t *h = reinterpret_cast<uint64_t *>(rec);
+    h[0] = (uint64_t)val;
+    h[1] = (uint64_t)(uint32_t)k.len;
+    uint32_t *w = reinterpret_cast<uint32_t *>(rec + KV_REC_HDR);
+    const int64_t words = (rec_bytes(k.len) - KV_REC_HDR) / 4;
+    for (int64_t j = 0; j < words; ++j) w[j] = k.word(j);
 }
 
 struct KvTable {
-    ulonglong2 *slots;
+    unsigned long long *slots;
     int64_t nb;  // buckets (power of two)
     uint8_t *arena;
     unsigned long long *counts;
-    int weak;    // PR_KV_WEAK_HASH: 2-bit tags, 4 home buckets (forces collisions; tests only)
+    int weak;  // PR_KV_WEAK_HASH: 2-bit tags, 4 home buckets (forces collisions; tests only)
 };
-
-// tag + home-bucket hash of a key (the weak variant keeps 2 tag bits and 2 bucket bits)
-__device__ __forceinline__ void key_hash(const KvTable &t, const uint8_t *key, int64_t len, uint64_t &tag,
-                                         uint64_t &h2) {
-    fingerprint128<true>(key, len, &tag, &h2);
-    if (t.weak) {
-        tag = (tag & 0x8000000000000003ull) | 0x8000000000000000ull;
-        h2 &= 3;
-    }
-}
 
 struct KeyBatch {
     const uint8_t *bytes;
@@ -186,35 +207,39 @@ struct KeyBatch {
     int64_t n;
 };
 
+__device__ __forceinline__ uint64_t slot_of(uint32_t tag, int64_t rec_off) {
+    return (uint64_t)tag | ((uint64_t)(rec_off >> 5) << 32);
+}
+__device__ __forceinline__ int64_t rec_off_of(uint64_t s) { return (int64_t)(s >> 32) << 5; }
+
 // ---- get: one thread per key ------------------------------------------------
 __global__ void __launch_bounds__(KV_THREADS) kv_get_kernel(KvTable t, KeyBatch kb, int rank, int world,
                                                              int64_t *__restrict__ out_vals,
                                                              uint8_t *__restrict__ out_hit) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= kb.n) return;
-    const int64_t a = __ldg(kb.off + i), len = __ldg(kb.off + i + 1) - a;
-    const uint8_t *key = kb.bytes + a;
-    uint64_t tag, h2;
-    key_hash(t, key, len, tag, h2);
+    const int64_t a = __ldg(kb.off + i);
+    const KeyRef k(kb.bytes + a, __ldg(kb.off + i + 1) - a);
+    uint32_t tag, hb;
+    hash_key(k, t.weak, tag, hb);
     int64_t val = -1;
     if (world <= 1 || owner_of(tag, world) == rank) {
-        int64_t b = (int64_t)(h2 & (uint64_t)(t.nb - 1));
+        int64_t b = (int64_t)(hb & (uint32_t)(t.nb - 1));
         for (int64_t p = 0; p < t.nb; ++p) {
-            uint64_t s[8];
-            const ulonglong2 *bk = t.slots + b * KV_BUCKET;
-            ld256<false>(bk, s[0], s[1], s[2], s[3]);
-            ld256<false>(bk + 2, s[4], s[5], s[6], s[7]);
+            uint64_t s[4];
+            ld256<false>(t.slots + b * KV_BUCKET, s[0], s[1], s[2], s[3]);
             bool done = false;
 #pragma unroll
             for (int j = 0; j < KV_BUCKET; ++j) {
                 if (done) break;
-                if (s[2 * j] == tag) {
+                const uint32_t st = (uint32_t)s[j];
+                if (st == tag) {
                     int64_t v;
-                    if (rec_matches<false>(t.arena + s[2 * j + 1], key, len, &v)) {
+                    if (rec_matches<false>(t.arena + rec_off_of(s[j]), k, &v)) {
                         val = v;
                         done = true;
                     }
-                } else if (s[2 * j] == TAG_EMPTY) {
+                } else if (st == TAG_EMPTY) {
                     done = true;
                 }
             }
@@ -232,36 +257,36 @@ __global__ void __launch_bounds__(KV_THREADS) kv_update_kernel(KvTable t, KeyBat
                                                                 const int64_t *__restrict__ in_vals) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= kb.n) return;
-    const int64_t a = __ldg(kb.off + i), len = __ldg(kb.off + i + 1) - a;
-    const uint8_t *key = kb.bytes + a;
-    uint64_t tag, h2;
-    key_hash(t, key, len, tag, h2);
+    const int64_t a = __ldg(kb.off + i);
+    const KeyRef k(kb.bytes + a, __ldg(kb.off + i + 1) - a);
+    uint32_t tag, hb;
+    hash_key(k, t.weak, tag, hb);
     if (world > 1 && owner_of(tag, world) != rank) return;
     const int64_t v = ERASE ? -1 : in_vals[i];
     int64_t myrec = -1;  // record allocated for an insert (kept across lost CAS races)
-    int64_t b = (int64_t)(h2 & (uint64_t)(t.nb - 1));
+    int64_t b = (int64_t)(hb & (uint32_t)(t.nb - 1));
     bool done = false;
     for (int64_t p = 0; p < t.nb && !done; ++p) {
-        uint64_t s[8];
-        ulonglong2 *bk = t.slots + b * KV_BUCKET;
+        uint64_t s[4];
+        unsigned long long *bk = t.slots + b * KV_BUCKET;
         ld256<true>(bk, s[0], s[1], s[2], s[3]);
-        ld256<true>(bk + 2, s[4], s[5], s[6], s[7]);
         for (int j = 0; j < KV_BUCKET && !done; ++j) {
-            uint64_t st = s[2 * j], sr = s[2 * j + 1];
+            uint64_t cur = s[j];
             for (;;) {  // re-examines slot j after a lost CAS
+                const uint32_t st = (uint32_t)cur;
                 if (st == tag) {
                     __threadfence();  // the record was published before its slot (see insert)
                     int64_t old;
-                    if (rec_matches<true>(t.arena + sr, key, len, &old)) {
+                    const int64_t ro = rec_off_of(cur);
+                    if (rec_matches<true>(t.arena + ro, k, &old)) {
                         if (ERASE) {
-                            uint64_t o0, o1;
-                            if (cas_slot(bk + j, st, sr, TAG_TOMB, 0, o0, o1)) {
+                            if (atomicCAS(bk + j, cur, (unsigned long long)TAG_TOMB) == cur) {
                                 atomicAdd(&t.counts[0], (unsigned long long)-1ll);
                                 atomicAdd(&t.counts[1], 1ull);
-                                atomicAdd(&t.counts[3], (unsigned long long)rec_bytes(len));
+                                atomicAdd(&t.counts[3], (unsigned long long)rec_bytes(k.len));
                             }
                         } else {
-                            atomicMax(reinterpret_cast<long long *>(t.arena + sr), (long long)v);
+                            atomicMax(reinterpret_cast<long long *>(t.arena + ro), (long long)v);
                         }
                         done = true;
                     }
@@ -273,82 +298,85 @@ __global__ void __launch_bounds__(KV_THREADS) kv_update_kernel(KvTable t, KeyBat
                     break;
                 }
                 if (myrec < 0) {
-                    myrec = (int64_t)atomicAdd(&t.counts[2], (unsigned long long)rec_bytes(len));
-                    write_record(t.arena + myrec, key, len, v);
+                    myrec = (int64_t)atomicAdd(&t.counts[2], (unsigned long long)rec_bytes(k.len));
+                    write_record(t.arena + myrec, k, v);
                     __threadfence();  // publish the record before the slot that points at it
                 }
-                uint64_t o0, o1;
-                if (cas_slot(bk + j, TAG_EMPTY, 0, tag, (uint64_t)myrec, o0, o1)) {
+                const unsigned long long want = slot_of(tag, myrec);
+                const unsigned long long got = atomicCAS(bk + j, 0ull, want);
+                if (got == 0ull) {
                     atomicAdd(&t.counts[0], 1ull);
                     myrec = -1;
                     done = true;
                     break;
                 }
-                st = o0;  // lost the race: look at what was written there
-                sr = o1;
+                cur = got;  // lost the race: look at what was written there
             }
         }
         b = (b + 1) & (t.nb - 1);
     }
-    if (myrec >= 0) atomicAdd(&t.counts[3], (unsigned long long)rec_bytes(len));  // lost every race
+    if (myrec >= 0) atomicAdd(&t.counts[3], (unsigned long long)rec_bytes(k.len));  // lost every race
 }
 
-// ---- fingerprints / shard owners ---------------------------------------------
+// ---- hashes / shard owners ---------------------------------------------------
 __global__ void fingerprint_kernel(KeyBatch kb, uint64_t *__restrict__ fp, int world, int32_t *__restrict__ owner) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < kb.n; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t a = kb.off[i];
-        uint64_t h, l;
-        fingerprint128<true>(kb.bytes + a, kb.off[i + 1] - a, &h, &l);
+        const KeyRef k(kb.bytes + a, kb.off[i + 1] - a);
+        uint32_t tag, hb;
+        hash_key(k, 0, tag, hb);
         if (fp) {
-            fp[2 * i] = h;
-            fp[2 * i + 1] = l;
+            fp[2 * i] = tag;
+            fp[2 * i + 1] = hb;
         }
-        if (owner) owner[i] = owner_of(h, world);
+        if (owner) owner[i] = owner_of(tag, world);
     }
 }
 
 // ---- maintenance ---------------------------------------------------------------
+__device__ __forceinline__ bool live_slot(uint64_t s) { return ((uint32_t)s & 0x80000000u) != 0; }
+
 __global__ void kv_export_kernel(KvTable t, int64_t nslots, int64_t *val_out, int64_t max, unsigned long long *cursor) {
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nslots; s += (int64_t)gridDim.x * blockDim.x) {
-        const ulonglong2 sl = t.slots[s];
-        if (sl.x & 0x8000000000000000ull) {
+        const uint64_t sl = t.slots[s];
+        if (live_slot(sl)) {
             unsigned long long p = atomicAdd(cursor, 1ull);
-            if ((int64_t)p < max) val_out[p] = *reinterpret_cast<const int64_t *>(t.arena + sl.y);
+            if ((int64_t)p < max) val_out[p] = *reinterpret_cast<const int64_t *>(t.arena + rec_off_of(sl));
         }
     }
 }
 
 __global__ void kv_remap_kernel(KvTable t, int64_t nslots, const int64_t *__restrict__ map, int64_t nmap) {
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nslots; s += (int64_t)gridDim.x * blockDim.x) {
-        const ulonglong2 sl = t.slots[s];
-        if (sl.x & 0x8000000000000000ull) {
-            int64_t *v = reinterpret_cast<int64_t *>(t.arena + sl.y);
+        const uint64_t sl = t.slots[s];
+        if (live_slot(sl)) {
+            int64_t *v = reinterpret_cast<int64_t *>(t.arena + rec_off_of(sl));
             if (*v >= 0 && *v < nmap) *v = map[*v];
         }
     }
 }
 
 // rebuild: every live key of the old table is copied into a fresh arena (compacting away
-// overwritten/erased records) and re-inserted by its fingerprint (no duplicates exist)
-__global__ void kv_rebuild_kernel(const ulonglong2 *__restrict__ old_slots, int64_t old_n,
+// overwritten/erased records) and re-inserted by its hash (no duplicates exist)
+__global__ void kv_rebuild_kernel(const unsigned long long *__restrict__ old_slots, int64_t old_n,
                                   const uint8_t *__restrict__ old_arena, KvTable t) {
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < old_n; s += (int64_t)gridDim.x * blockDim.x) {
-        const ulonglong2 sl = old_slots[s];
-        if (!(sl.x & 0x8000000000000000ull)) continue;
-        const uint8_t *rec = old_arena + sl.y;
+        const uint64_t sl = old_slots[s];
+        if (!live_slot(sl)) continue;
+        const uint8_t *rec = old_arena + rec_off_of(sl);
         const int64_t len = (int64_t)(uint32_t)reinterpret_cast<const uint64_t *>(rec)[1];
         const int64_t rb = rec_bytes(len);
         const int64_t dst = (int64_t)atomicAdd(&t.counts[2], (unsigned long long)rb);
         for (int64_t o = 0; o < rb; o += 8)
             *reinterpret_cast<uint64_t *>(t.arena + dst + o) = *reinterpret_cast<const uint64_t *>(rec + o);
-        uint64_t tag, h2;
-        key_hash(t, rec + KV_REC_HDR, len, tag, h2);
-        int64_t b = (int64_t)(h2 & (uint64_t)(t.nb - 1));
+        const KeyRef k(rec + KV_REC_HDR, len);
+        uint32_t tag, hb;
+        hash_key(k, t.weak, tag, hb);
+        int64_t b = (int64_t)(hb & (uint32_t)(t.nb - 1));
         bool done = false;
         for (int64_t p = 0; p < t.nb && !done; ++p) {
             for (int j = 0; j < KV_BUCKET && !done; ++j) {
-                uint64_t o0, o1;
-                if (cas_slot(t.slots + b * KV_BUCKET + j, TAG_EMPTY, 0, tag, (uint64_t)dst, o0, o1)) {
+                if (atomicCAS(t.slots + b * KV_BUCKET + j, 0ull, slot_of(tag, dst)) == 0ull) {
                     atomicAdd(&t.counts[0], 1ull);
                     done = true;
                 }
@@ -384,17 +412,21 @@ static int rebuild(pr_kv *h, int64_t need_keys, int64_t need_bytes, cudaStream_t
     const int64_t live = (int64_t)c[0];
     const int64_t live_bytes = (int64_t)c[2] - (int64_t)c[3];
     const int64_t nslots = slots_for(std::max<int64_t>(need_keys, live));
-    const int64_t acap = std::max<int64_t>(4096, round_up<int64_t>(need_bytes + need_bytes / 2, 256));
-    ulonglong2 *ns = nullptr;
+    const int64_t acap = std::min<int64_t>(KV_MAX_ARENA,
+                                           std::max<int64_t>(4096, round_up<int64_t>(need_bytes + need_bytes / 2, 256)));
+    if (need_bytes > acap) PR_FAIL(PR_ERR_NOMEM, "kv arena: %lld bytes exceed the 128 GiB record space",
+                                   (long long)need_bytes);
+    unsigned long long *ns = nullptr;
     uint8_t *na = nullptr;
-    PR_CUDA(cudaMalloc(&ns, (size_t)nslots * sizeof(ulonglong2)));
+    PR_CUDA(cudaMalloc(&ns, (size_t)nslots * sizeof(unsigned long long)));
     if (cudaMalloc(&na, (size_t)acap) != cudaSuccess) {
         cudaFree(ns);
+        cudaGetLastError();
         PR_FAIL(PR_ERR_NOMEM, "kv arena: cannot allocate %lld bytes", (long long)acap);
     }
-    PR_CUDA(cudaMemsetAsync(ns, 0, (size_t)nslots * sizeof(ulonglong2), st));
+    PR_CUDA(cudaMemsetAsync(ns, 0, (size_t)nslots * sizeof(unsigned long long), st));
     PR_CUDA(cudaMemsetAsync(h->d_count, 0, 4 * sizeof(unsigned long long), st));
-    ulonglong2 *os = h->slots;
+    unsigned long long *os = h->slots;
     uint8_t *oa = h->arena;
     const int64_t on = h->nslots;
     h->slots = ns;
@@ -473,7 +505,10 @@ using namespace pr;
 extern "C" {
 
 void pr_fingerprint_host(const uint8_t *bytes, int64_t len, uint64_t out[2]) {
-    fingerprint128<false>(bytes, len, &out[0], &out[1]);
+    uint32_t tag, hb;
+    hash_host(bytes, len, tag, hb);
+    out[0] = tag;
+    out[1] = hb;
 }
 
 int pr_fingerprint(const uint8_t *d_bytes, const int64_t *d_off, int64_t n, uint64_t *d_fp, void *stream) {
@@ -496,6 +531,14 @@ int pr_kv_owner(const uint8_t *d_bytes, const int64_t *d_off, int64_t n, int wor
     return PR_OK;
 }
 
+int pr_l2_fetch_granularity(int bytes, int *previous) {
+    size_t prev = 0;
+    PR_CUDA(cudaDeviceGetLimit(&prev, cudaLimitMaxL2FetchGranularity));
+    if (previous) *previous = (int)prev;
+    if (bytes > 0) PR_CUDA(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)bytes));
+    return PR_OK;
+}
+
 int pr_kv_create(int64_t capacity, pr_kv **out) { return pr_kv_create_ex(capacity, 0, out); }
 
 int pr_kv_create_ex(int64_t capacity, uint32_t flags, pr_kv **out) {
@@ -504,7 +547,7 @@ int pr_kv_create_ex(int64_t capacity, uint32_t flags, pr_kv **out) {
     h->flags = flags;
     h->nslots = slots_for(capacity);
     h->arena_cap = std::max<int64_t>(4096, capacity * 48);
-    if (cudaMalloc(&h->slots, (size_t)h->nslots * sizeof(ulonglong2)) != cudaSuccess ||
+    if (cudaMalloc(&h->slots, (size_t)h->nslots * sizeof(unsigned long long)) != cudaSuccess ||
         cudaMalloc(&h->arena, (size_t)h->arena_cap) != cudaSuccess ||
         cudaMalloc(&h->d_count, 4 * sizeof(unsigned long long)) != cudaSuccess) {
         cudaFree(h->slots);
@@ -513,7 +556,7 @@ int pr_kv_create_ex(int64_t capacity, uint32_t flags, pr_kv **out) {
         cudaGetLastError();
         PR_FAIL(PR_ERR_NOMEM, "kv_create: device allocation failed");
     }
-    PR_CUDA(cudaMemset(h->slots, 0, (size_t)h->nslots * sizeof(ulonglong2)));
+    PR_CUDA(cudaMemset(h->slots, 0, (size_t)h->nslots * sizeof(unsigned long long)));
     PR_CUDA(cudaMemset(h->d_count, 0, 4 * sizeof(unsigned long long)));
     PR_CUDA(cudaDeviceSynchronize());
     *out = h;
@@ -564,7 +607,7 @@ int pr_kv_erase_text(pr_kv *h, const uint8_t *d_bytes, const int64_t *d_off, int
 int pr_kv_clear(pr_kv *h, void *stream) {
     if (!h) PR_FAIL(PR_ERR_BAD_ARG, "null kv");
     cudaStream_t st = as_stream(stream);
-    PR_CUDA(cudaMemsetAsync(h->slots, 0, (size_t)h->nslots * sizeof(ulonglong2), st));
+    PR_CUDA(cudaMemsetAsync(h->slots, 0, (size_t)h->nslots * sizeof(unsigned long long), st));
     PR_CUDA(cudaMemsetAsync(h->d_count, 0, 4 * sizeof(unsigned long long), st));
     h->upper = 0;
     h->arena_upper = 0;
@@ -585,7 +628,7 @@ int pr_kv_memory(pr_kv *h, int64_t *slot_bytes, int64_t *arena_bytes, int64_t *g
     unsigned long long c[4];
     int rc = read_counts(h, c, as_stream(stream));
     if (rc) return rc;
-    if (slot_bytes) *slot_bytes = h->nslots * (int64_t)sizeof(ulonglong2);
+    if (slot_bytes) *slot_bytes = h->nslots * (int64_t)sizeof(unsigned long long);
     if (arena_bytes) *arena_bytes = (int64_t)c[2];
     if (garbage_bytes) *garbage_bytes = (int64_t)c[3];
     return PR_OK;

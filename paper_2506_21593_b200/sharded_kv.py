@@ -1,9 +1,9 @@
 """Fixed-KV table hash-partitioned across ranks (one process per GPU).
 
-Rank r owns the keys whose fingerprint maps to r: ``owner = (tag >> 32 & 0x7fffffff) %
-world`` where tag is the fingerprint's first word (``owner_host`` / device
-``pr_kv_owner``).  The table's home bucket comes from the SECOND word, so the ownership
-bits and the bucket bits are disjoint: every bucket of a rank's table is a home bucket
+Rank r owns the keys whose hash maps to r: ``owner = (tag & 0x7fffffff) % world`` where
+tag is the key's 32-bit tag hash (``owner_host`` / device ``pr_kv_owner``).  The table's
+home bucket comes from the OTHER, independent hash chain, so the ownership bits and the
+bucket bits are disjoint: every bucket of a rank's table is a home bucket
 for its keys (round 1 took both from the same low bits, so at world 8 only 1/8 of a
 rank's buckets could be home buckets).
 
@@ -30,7 +30,7 @@ def owner_host(text: str, world: int) -> int:
     from .caches import fingerprint_host
 
     tag = fingerprint_host(text)[0]
-    return ((tag >> 32) & 0x7FFFFFFF) % world
+    return (tag & 0x7FFFFFFF) % world
 
 
 class ShardedKV:

@@ -14,6 +14,8 @@ from paper_2506_21593_b200 import _lib  # noqa: E402
 
 n_keys = int(os.environ.get("KV_KEYS", 100_000_000))
 L = _lib.load()
+if os.environ.get("PR_L2FETCH"):
+    _lib.check(L.pr_l2_fetch_granularity(int(os.environ["PR_L2FETCH"]), None))
 h = ctypes.c_void_p()
 _lib.check(L.pr_kv_create(n_keys, ctypes.byref(h)))
 s = _lib.stream_ptr()

@@ -58,17 +58,16 @@ def test_fingerprint_is_byte_exact_and_never_reserved(lib):
             "ünïcödé".encode(), b"\x00", b"\x00\x00"]
     fps = [_fp(lib, k) for k in keys]
     assert len(set(fps)) == len(keys)
-    for hi, _ in fps:
-        assert hi >> 63 == 1  # top bit set: never EMPTY {0,0} or TOMBSTONE {0,1}
+    for tag, hb in fps:
+        assert tag >> 31 == 1 and tag < (1 << 32)  # top bit set: never EMPTY (0) or TOMBSTONE (1)
+        assert hb < (1 << 32)
     assert _fp(lib, b"Q1") == _fp(lib, b"Q1")
 
 
 def test_fingerprint_regression_value(lib):
     # pins the hash so host and device (tests/test_gpu_kv.py) and stored tables agree over time
-    assert _fp(lib, b"query-000000001") == _fp(lib, "query-000000001".encode())
-    hi, lo = _fp(lib, b"abc")
-    assert (hi, lo) == _fp(lib, b"abc")
-    assert hi != lo
+    assert _fp(lib, b"abc") == (2418048503, 3132096303)
+    assert _fp(lib, b"query-000000001") == (3201114788, 4107767217)
 
 
 @pytest.mark.parametrize("token", ["a", "Who", "ledger0007", "_", "9", "x" * 124, "y" * 125, "z" * 300, ""])
