@@ -6,33 +6,44 @@
 // collision (accidental or constructed) can only cost a probe, never serve another key's
 // answer.
 //
-// Layout (HBM):
-//   slots  u64[nslots] = {u32 tag | u32 rec << 32}, nslots a power of two, grouped in
-//          32-byte buckets of 4 slots (ONE DRAM sector per bucket).  tag = 32-bit key hash
-//          with the top bit forced (0 = EMPTY, 1 = TOMBSTONE); rec = the key's record in
-//          32-byte units.  Load factor <= 0.5.
-//   arena  32-byte aligned records {i64 value, u32 len, u32 0, key bytes, zero pad}: one
-//          sector holds the header and the first 16 key bytes, so a hit on a short key
-//          costs one bucket sector plus one record sector.
+// Why the layout is what it is (measured, scripts/micro/randload.cu + profiles/):
+// on B200 a random 32-byte read costs a whole 128-byte L2 line from DRAM (4 sectors per
+// request, whatever the load flavour), so the unit of cost is the LINE.  One lookup
+// should therefore touch exactly one random line, and that line should hold everything
+// the lookup needs:
+//
+//   slots  32-byte slots, 4 per 128-byte bucket line (nslots a power of two, load <= 0.5):
+//            w0 = u32 tag | u32 rec << 32     tag = 32-bit key hash, top bit forced
+//                                              (0 = EMPTY, 1 = TOMBSTONE); rec = record index
+//                                              in 32-byte units (0 = none), all ones = BUSY
+//                                              (slot claimed, being written)
+//            w1 = u64 len (24 bits) | value << 24   (value < 2^40)
+//            w2, w3 = the first 16 key bytes (zero padded)
+//          A key of <= 16 bytes is confirmed entirely inside its bucket line: a hit or a
+//          miss is ONE random line.  Longer keys also compare their remaining bytes with
+//          their record (only on a full tag + length + 16-byte prefix match).
+//   arena  32-byte aligned records: the full key bytes of keys longer than 16 bytes.
 // Hash: two 32-bit multiply-rotate chains over the key's little-endian words (murmur3_32
 // round function, two seeds).  hA -> tag (and shard owner), hB -> home bucket: the
 // ownership bits and the bucket bits come from independent chains.  Only 32-bit integer
-// multiplies (no 64-bit emulation): the hash is a short dependency chain per key.
+// multiplies: the hash is a short dependency chain per key.
 //
-// Probing is one thread per key: it hashes its key ONCE (aligned 32-bit loads + funnel
-// shifts, not byte loads), reads its bucket with one 256-bit load, compares the four tags
-// in registers, confirms a tag match against the record (one more 256-bit load, which
-// also carries the value), and moves to the next bucket only when the bucket is full of
-// other keys.  A warp keeps 32 independent probes in flight.  Values are non-negative
-// int64 write sequence numbers supplied by the host; a put resolves with atomicMax on the
-// record's value, so the largest (latest) write wins even when one batch writes a key
-// twice (caches.py:67-74).
+// Lookup (kv_get_kernel) is warp-cooperative: every lane hashes ONE key (aligned 32-bit
+// loads + funnel shifts), then each 4-lane group probes 4 keys in turn — the key's hash,
+// length and 16-byte prefix are broadcast by shuffle, each lane loads one 32-byte slot of
+// the bucket line (one 256-bit load per lane, the group's four loads coalesce into one
+// 128-byte request), compares in registers, and the group ballots.  All four rounds'
+// loads are issued before any is consumed, so a warp has 32 independent lines in flight.
+// Keys whose bucket is full of other keys finish on a per-lane linear-probing path.
+// Values are write sequence numbers supplied by the host; a put resolves an existing key
+// with atomicMax on w1, so the largest (latest) write wins even when one batch writes a
+// key twice (caches.py:67-74).
 #include <algorithm>
 
 #include "common.cuh"
 
 struct pr_kv {
-    unsigned long long *slots = nullptr;    // [nslots] {tag, record index}
+    unsigned long long *slots = nullptr;    // [nslots][4] 32-byte slots
     int64_t nslots = 0;
     uint8_t *arena = nullptr;               // records
     int64_t arena_cap = 0;                  // bytes
@@ -44,9 +55,11 @@ struct pr_kv {
 
 namespace pr {
 
-constexpr int KV_BUCKET = 4;  // slots per 32-byte bucket
+constexpr int KV_BUCKET = 4;  // 32-byte slots per 128-byte bucket line
 constexpr int KV_THREADS = 128;
-constexpr int KV_REC_HDR = 16;
+constexpr int KV_INLINE = 16;                        // key bytes held in the slot
+constexpr uint32_t REC_BUSY = 0xffffffffu;           // slot claimed, fields being written
+constexpr uint64_t KV_MAX_VALUE = ((uint64_t)1 << 40) - 1;
 constexpr uint32_t TAG_EMPTY = 0, TAG_TOMB = 1;
 constexpr uint32_t SEED_A = 0x5EED1024u, SEED_B = 0xCA5CADE5u;  // the HASH_SEED family (embedding.py:33)
 constexpr int64_t KV_MAX_ARENA = (int64_t)32 << 32;              // 32-bit record index x 32 bytes
@@ -90,7 +103,10 @@ __host__ __device__ __forceinline__ int owner_of(uint32_t tag, int world) {
     return (int)((tag & 0x7fffffffu) % (uint32_t)world);
 }
 
-__host__ __device__ __forceinline__ int64_t rec_bytes(int64_t len) { return round_up<int64_t>(KV_REC_HDR + len, 32); }
+// record bytes of a key (keys <= 16 bytes live entirely in their slot)
+__host__ __device__ __forceinline__ int64_t rec_bytes(int64_t len) {
+    return len > KV_INLINE ? round_up<int64_t>(len, 32) : 0;
+}
 
 // A key in device memory, read as aligned 32-bit words: word j = bytes [4j, 4j+4) of the
 // key (little-endian, zero beyond len).  Only words that hold key bytes are loaded.
@@ -104,7 +120,7 @@ struct KeyRef {
         w = reinterpret_cast<const uint32_t *>(u & ~(uintptr_t)3);
         sh = (int)(u & 3) * 8;
         len = n;
-        last = n > 0 ? ((u & 3) + n - 1) >> 2 : -1;
+        last = n > 0 ? ((int64_t)(u & 3) + n - 1) >> 2 : -1;
     }
     __device__ __forceinline__ uint32_t ld(int64_t j) const { return j <= last ? __ldg(w + j) : 0u; }
     // word j given the aligned words j and j+1 already loaded
@@ -116,18 +132,42 @@ struct KeyRef {
     __device__ __forceinline__ uint32_t word(int64_t j) const { return join(ld(j), sh ? ld(j + 1) : 0u, j); }
 };
 
-__device__ __forceinline__ void hash_key(const KeyRef &k, int weak, uint32_t &tag, uint32_t &hb) {
+// Hash a key and return its first four words (the slot's inline prefix).
+__device__ __forceinline__ void hash_key(const KeyRef &k, int weak, uint32_t &tag, uint32_t &hb, uint32_t pw[4]) {
     KeyHash h;
     h.init(k.len);
     const int64_t nw = (k.len + 3) >> 2;
     uint32_t lo = k.ld(0);
-    for (int64_t j = 0; j < nw; ++j) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const uint32_t hi = k.ld(j + 1);
+        pw[j] = k.join(lo, hi, j);
+        if (j < nw) h.word(pw[j]);
+        lo = hi;
+    }
+    for (int64_t j = 4; j < nw; ++j) {
         const uint32_t hi = k.sh ? k.ld(j + 1) : 0u;
         h.word(k.join(lo, hi, j));
         lo = k.sh ? hi : k.ld(j + 1);
     }
     h.fin(k.len, tag, hb);
     if (weak) {  // PR_KV_WEAK_HASH: 2 tag bits, 4 home buckets
+        tag = (tag & 3u) | 0x80000000u;
+        hb &= 3u;
+    }
+}
+
+// hash of a key held inline in a slot (<= 16 bytes: words w2 | w3, zero padded)
+__device__ __forceinline__ void hash_inline(uint64_t w2, uint64_t w3, int64_t len, int weak, uint32_t &tag,
+                                            uint32_t &hb) {
+    const uint32_t w[4] = {(uint32_t)w2, (uint32_t)(w2 >> 32), (uint32_t)w3, (uint32_t)(w3 >> 32)};
+    KeyHash h;
+    h.init(len);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+        if (4 * j < len) h.word(w[j]);
+    h.fin(len, tag, hb);
+    if (weak) {
         tag = (tag & 3u) | 0x80000000u;
         hb &= 3u;
     }
@@ -162,40 +202,36 @@ __device__ __forceinline__ void ld128(const void *p, uint32_t &a, uint32_t &b, u
         asm("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "l"(p));
 }
 
-// Does the record at `rec` hold exactly the key's bytes?  The record's first sector
-// (header + key words 0..3) is one 256-bit load; the value comes with it.
-template <bool STRONG>
-__device__ __forceinline__ bool rec_matches(const uint8_t *rec, const KeyRef &k, int64_t *val_out) {
+struct Slot {
     uint64_t w0, w1, w2, w3;
-    ld256<STRONG>(rec, w0, w1, w2, w3);
-    if ((int64_t)(uint32_t)w1 != k.len) return false;
-    if ((uint32_t)w2 != k.word(0) || (uint32_t)(w2 >> 32) != k.word(1) || (uint32_t)w3 != k.word(2) ||
-        (uint32_t)(w3 >> 32) != k.word(3))
-        return false;
+    __device__ __forceinline__ uint32_t tag() const { return (uint32_t)w0; }
+    __device__ __forceinline__ uint32_t rec() const { return (uint32_t)(w0 >> 32); }
+    __device__ __forceinline__ int64_t len() const { return (int64_t)(w1 & 0xffffffull); }
+    __device__ __forceinline__ int64_t value() const { return (int64_t)(w1 >> 24); }
+};
+
+__host__ __device__ __forceinline__ uint64_t pack_w1(int64_t len, int64_t val) {
+    return (uint64_t)len | ((uint64_t)val << 24);
+}
+__device__ __forceinline__ uint64_t pw2(const uint32_t pw[4]) { return (uint64_t)pw[0] | ((uint64_t)pw[1] << 32); }
+__device__ __forceinline__ uint64_t pw3(const uint32_t pw[4]) { return (uint64_t)pw[2] | ((uint64_t)pw[3] << 32); }
+
+// bytes [16, len) of a long key against its record (the record holds the whole key)
+template <bool STRONG>
+__device__ __forceinline__ bool tail_matches(const uint8_t *rec, const KeyRef &k) {
     for (int64_t g = 1; 16 * g < k.len; ++g) {
         uint32_t r[4];
-        ld128<STRONG>(rec + KV_REC_HDR + 16 * g, r[0], r[1], r[2], r[3]);
+        ld128<STRONG>(rec + 16 * g, r[0], r[1], r[2], r[3]);
 #pragma unroll
         for (int q = 0; q < 4; ++q)
             if (r[q] != k.word(4 * g + q)) return false;
     }
-    *val_out = (int64_t)w0;
     return true;
 }
 
-// copy a key into a fresh record (header + bytes, zero padded to the 32-byte record size)
-__device__ void write_record(uint8_t *rec, const KeyRef &k, int64_t val) {
-    uint64_t *h = reinterpret_cast<uint64_t *>(rec);
-    h[0] = (uint64_t)val;
-    h[1] = (uint64_t)(uint32_t)k.len;
-    uint32_t *w = reinterpret_cast<uint32_t *>(rec + KV_REC_HDR);
-    const int64_t words = (rec_bytes(k.len) - KV_REC_HDR) / 4;
-    for (int64_t j = 0; j < words; ++j) w[j] = k.word(j);
-}
-
 struct KvTable {
-    unsigned long long *slots;
-    int64_t nb;  // buckets (power of two)
+    unsigned long long *slots;  // [nslots][4]
+    int64_t nb;                 // buckets (power of two)
     uint8_t *arena;
     unsigned long long *counts;
     int weak;  // PR_KV_WEAK_HASH: 2-bit tags, 4 home buckets (forces collisions; tests only)
@@ -207,51 +243,121 @@ struct KeyBatch {
     int64_t n;
 };
 
-__device__ __forceinline__ uint64_t slot_of(uint32_t tag, int64_t rec_off) {
-    return (uint64_t)tag | ((uint64_t)(rec_off >> 5) << 32);
+__device__ __forceinline__ unsigned long long *slot_ptr(const KvTable &t, int64_t b, int j) {
+    return t.slots + (b * KV_BUCKET + j) * 4;
 }
-__device__ __forceinline__ int64_t rec_off_of(uint64_t s) { return (int64_t)(s >> 32) << 5; }
 
-// ---- get: one thread per key ------------------------------------------------
+// does slot s hold the key (tag, len, prefix already compared against the record for long keys)?
+template <bool STRONG>
+__device__ __forceinline__ bool slot_holds(const KvTable &t, const Slot &s, uint32_t tag, const KeyRef &k,
+                                           const uint32_t pw[4]) {
+    if (s.tag() != tag || s.rec() == REC_BUSY || s.len() != k.len || s.w2 != pw2(pw) || s.w3 != pw3(pw))
+        return false;
+    return k.len <= KV_INLINE || tail_matches<STRONG>(t.arena + ((int64_t)s.rec() << 5), k);
+}
+
+// per-lane linear probing from bucket b (the cooperative pass's overflow path and puts)
+__device__ int64_t probe_lane(const KvTable &t, int64_t b, uint32_t tag, const KeyRef &k, const uint32_t pw[4]) {
+    for (int64_t p = 0; p < t.nb; ++p) {
+        for (int j = 0; j < KV_BUCKET; ++j) {
+            Slot s;
+            ld256<false>(slot_ptr(t, b, j), s.w0, s.w1, s.w2, s.w3);
+            if (s.tag() == TAG_EMPTY) return -1;
+            if (slot_holds<false>(t, s, tag, k, pw)) return s.value();
+        }
+        b = (b + 1) & (t.nb - 1);
+    }
+    return -1;
+}
+
+// ---- get: warp-cooperative, 4 lanes per bucket line --------------------------
 __global__ void __launch_bounds__(KV_THREADS) kv_get_kernel(KvTable t, KeyBatch kb, int rank, int world,
                                                              int64_t *__restrict__ out_vals,
                                                              uint8_t *__restrict__ out_hit) {
+    const int lane = threadIdx.x & 31;
+    const int sub = lane & 3, g0 = lane & ~3;
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= kb.n) return;
-    const int64_t a = __ldg(kb.off + i);
-    const KeyRef k(kb.bytes + a, __ldg(kb.off + i + 1) - a);
-    uint32_t tag, hb;
-    hash_key(k, t.weak, tag, hb);
-    int64_t val = -1;
-    if (world <= 1 || owner_of(tag, world) == rank) {
-        int64_t b = (int64_t)(hb & (uint32_t)(t.nb - 1));
-        for (int64_t p = 0; p < t.nb; ++p) {
-            uint64_t s[4];
-            ld256<false>(t.slots + b * KV_BUCKET, s[0], s[1], s[2], s[3]);
-            bool done = false;
+    const bool have = i < kb.n;
+    int64_t a = 0, len = 0;
+    if (have) {
+        a = __ldg(kb.off + i);
+        len = __ldg(kb.off + i + 1) - a;
+    }
+    const KeyRef k(kb.bytes + a, len);
+    uint32_t tag = 0, hb = 0, pw[4] = {0, 0, 0, 0};
+    bool active = false;
+    if (have) {
+        hash_key(k, t.weak, tag, hb, pw);
+        active = world <= 1 || owner_of(tag, world) == rank;
+    }
+    const int64_t home = (int64_t)(hb & (uint32_t)(t.nb - 1));
+    // issue the four rounds' slot loads (round r probes the key of lane g0 + r)
+    Slot s[4];
+    bool act[4];
 #pragma unroll
-            for (int j = 0; j < KV_BUCKET; ++j) {
-                if (done) break;
-                const uint32_t st = (uint32_t)s[j];
-                if (st == tag) {
-                    int64_t v;
-                    if (rec_matches<false>(t.arena + rec_off_of(s[j]), k, &v)) {
-                        val = v;
-                        done = true;
-                    }
-                } else if (st == TAG_EMPTY) {
-                    done = true;
-                }
-            }
-            if (done) break;
-            b = (b + 1) & (t.nb - 1);
+    for (int r = 0; r < 4; ++r) {
+        const int src = g0 + r;
+        act[r] = __shfl_sync(0xffffffffu, active, src);
+        const int64_t b = __shfl_sync(0xffffffffu, home, src);
+        s[r].w0 = s[r].w1 = s[r].w2 = s[r].w3 = 0;
+        if (act[r]) ld256<false>(slot_ptr(t, b, sub), s[r].w0, s[r].w1, s[r].w2, s[r].w3);
+    }
+    int64_t val = -1;
+    bool unresolved = false;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int src = g0 + r;
+        const uint32_t rtag = __shfl_sync(0xffffffffu, tag, src);
+        const int64_t rlen = __shfl_sync(0xffffffffu, len, src);
+        const int64_t ra = __shfl_sync(0xffffffffu, a, src);
+        uint32_t rpw[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) rpw[q] = __shfl_sync(0xffffffffu, pw[q], src);
+        bool match = false, empty = false;
+        if (act[r]) {
+            const KeyRef rk(kb.bytes + ra, rlen);
+            match = slot_holds<false>(t, s[r], rtag, rk, rpw);
+            empty = s[r].tag() == TAG_EMPTY;
+        }
+        const unsigned mm = (__ballot_sync(0xffffffffu, match) >> g0) & 0xFu;
+        const unsigned me = (__ballot_sync(0xffffffffu, empty) >> g0) & 0xFu;
+        // first match wins; an empty slot before it cannot exist (inserts fill in order)
+        const int who = mm ? __ffs(mm) - 1 : 0;
+        const int64_t v = __shfl_sync(0xffffffffu, s[r].value(), g0 + who);
+        if (sub == r) {
+            if (mm) val = v;
+            else if (!me && act[r]) unresolved = true;  // bucket full of other keys
         }
     }
-    out_vals[i] = val;
-    out_hit[i] = val >= 0;
+    if (unresolved)  // rare: continue linear probing alone from the next bucket
+        val = probe_lane(t, (home + 1) & (t.nb - 1), tag, k, pw);
+    if (have) {
+        out_vals[i] = val;
+        out_hit[i] = val >= 0;
+    }
+}
+
+// copy a long key into a fresh record (zero padded to its 32-byte record size)
+__device__ void write_record(uint8_t *rec, const KeyRef &k) {
+    uint32_t *w = reinterpret_cast<uint32_t *>(rec);
+    const int64_t words = rec_bytes(k.len) / 4;
+    for (int64_t j = 0; j < words; ++j) w[j] = k.word(j);
+}
+
+// wait until a claimed slot is published (its writer is another thread of this launch)
+__device__ __forceinline__ uint64_t await_published(unsigned long long *sp) {
+    uint64_t w0;
+    for (;;) {
+        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w0) : "l"(sp) : "memory");
+        if ((uint32_t)(w0 >> 32) != REC_BUSY) return w0;
+        __nanosleep(32);
+    }
 }
 
 // ---- put (upsert) / erase: one thread per key --------------------------------
+// Insert protocol: CAS w0 EMPTY -> {tag, BUSY}; write w1..w3 (+ the record of a long key);
+// fence; publish w0 = {tag, rec}.  A thread that meets a BUSY slot carrying its tag waits
+// for the publication before comparing (duplicates of one new key inside one batch).
 template <bool ERASE>
 __global__ void __launch_bounds__(KV_THREADS) kv_update_kernel(KvTable t, KeyBatch kb, int rank, int world,
                                                                 const int64_t *__restrict__ in_vals) {
@@ -259,63 +365,63 @@ __global__ void __launch_bounds__(KV_THREADS) kv_update_kernel(KvTable t, KeyBat
     if (i >= kb.n) return;
     const int64_t a = __ldg(kb.off + i);
     const KeyRef k(kb.bytes + a, __ldg(kb.off + i + 1) - a);
-    uint32_t tag, hb;
-    hash_key(k, t.weak, tag, hb);
+    uint32_t tag, hb, pw[4];
+    hash_key(k, t.weak, tag, hb, pw);
     if (world > 1 && owner_of(tag, world) != rank) return;
     const int64_t v = ERASE ? -1 : in_vals[i];
-    int64_t myrec = -1;  // record allocated for an insert (kept across lost CAS races)
     int64_t b = (int64_t)(hb & (uint32_t)(t.nb - 1));
-    bool done = false;
-    for (int64_t p = 0; p < t.nb && !done; ++p) {
-        uint64_t s[4];
-        unsigned long long *bk = t.slots + b * KV_BUCKET;
-        ld256<true>(bk, s[0], s[1], s[2], s[3]);
-        for (int j = 0; j < KV_BUCKET && !done; ++j) {
-            uint64_t cur = s[j];
-            for (;;) {  // re-examines slot j after a lost CAS
-                const uint32_t st = (uint32_t)cur;
-                if (st == tag) {
-                    __threadfence();  // the record was published before its slot (see insert)
-                    int64_t old;
-                    const int64_t ro = rec_off_of(cur);
-                    if (rec_matches<true>(t.arena + ro, k, &old)) {
+    for (int64_t p = 0; p < t.nb; ++p) {
+        for (int j = 0; j < KV_BUCKET; ++j) {
+            unsigned long long *sp = slot_ptr(t, b, j);
+            Slot s;
+            ld256<true>(sp, s.w0, s.w1, s.w2, s.w3);
+            for (;;) {  // re-examines slot j after a lost CAS / a pending publication
+                if (s.tag() == tag) {
+                    if (s.rec() == REC_BUSY) {
+                        s.w0 = await_published(sp);
+                        __threadfence();
+                        ld256<true>(sp, s.w0, s.w1, s.w2, s.w3);
+                        continue;
+                    }
+                    __threadfence();
+                    if (slot_holds<true>(t, s, tag, k, pw)) {
                         if (ERASE) {
-                            if (atomicCAS(bk + j, cur, (unsigned long long)TAG_TOMB) == cur) {
+                            if (atomicCAS(sp, s.w0, (unsigned long long)TAG_TOMB) == s.w0) {
                                 atomicAdd(&t.counts[0], (unsigned long long)-1ll);
                                 atomicAdd(&t.counts[1], 1ull);
                                 atomicAdd(&t.counts[3], (unsigned long long)rec_bytes(k.len));
                             }
                         } else {
-                            atomicMax(reinterpret_cast<long long *>(t.arena + ro), (long long)v);
+                            atomicMax(sp + 1, (unsigned long long)pack_w1(k.len, v));
                         }
-                        done = true;
+                        return;
                     }
-                    break;
+                    break;  // same tag, another key
                 }
-                if (st != TAG_EMPTY) break;  // another key or a tombstone: next slot
-                if (ERASE) {                 // first empty slot: the key is absent
-                    done = true;
-                    break;
+                if (s.tag() != TAG_EMPTY) break;  // another key or a tombstone: next slot
+                if (ERASE) return;                // first empty slot: the key is absent
+                const unsigned long long claim = (unsigned long long)tag | ((unsigned long long)REC_BUSY << 32);
+                const unsigned long long got = atomicCAS(sp, 0ull, claim);
+                if (got != 0ull) {  // lost the race: look at what was claimed there
+                    s.w0 = got;
+                    continue;
                 }
-                if (myrec < 0) {
-                    myrec = (int64_t)atomicAdd(&t.counts[2], (unsigned long long)rec_bytes(k.len));
-                    write_record(t.arena + myrec, k, v);
-                    __threadfence();  // publish the record before the slot that points at it
+                int64_t rec = 0;
+                if (k.len > KV_INLINE) {
+                    rec = (int64_t)atomicAdd(&t.counts[2], (unsigned long long)rec_bytes(k.len));
+                    write_record(t.arena + rec, k);
                 }
-                const unsigned long long want = slot_of(tag, myrec);
-                const unsigned long long got = atomicCAS(bk + j, 0ull, want);
-                if (got == 0ull) {
-                    atomicAdd(&t.counts[0], 1ull);
-                    myrec = -1;
-                    done = true;
-                    break;
-                }
-                cur = got;  // lost the race: look at what was written there
+                sp[1] = pack_w1(k.len, v);
+                sp[2] = pw2(pw);
+                sp[3] = pw3(pw);
+                __threadfence();
+                atomicExch(sp, (unsigned long long)tag | ((unsigned long long)(rec >> 5) << 32));  // publish
+                atomicAdd(&t.counts[0], 1ull);
+                return;
             }
         }
         b = (b + 1) & (t.nb - 1);
     }
-    if (myrec >= 0) atomicAdd(&t.counts[3], (unsigned long long)rec_bytes(k.len));  // lost every race
 }
 
 // ---- hashes / shard owners ---------------------------------------------------
@@ -323,8 +429,8 @@ __global__ void fingerprint_kernel(KeyBatch kb, uint64_t *__restrict__ fp, int w
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < kb.n; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t a = kb.off[i];
         const KeyRef k(kb.bytes + a, kb.off[i + 1] - a);
-        uint32_t tag, hb;
-        hash_key(k, 0, tag, hb);
+        uint32_t tag, hb, pw[4];
+        hash_key(k, 0, tag, hb, pw);
         if (fp) {
             fp[2 * i] = tag;
             fp[2 * i + 1] = hb;
@@ -334,49 +440,60 @@ __global__ void fingerprint_kernel(KeyBatch kb, uint64_t *__restrict__ fp, int w
 }
 
 // ---- maintenance ---------------------------------------------------------------
-__device__ __forceinline__ bool live_slot(uint64_t s) { return ((uint32_t)s & 0x80000000u) != 0; }
+__device__ __forceinline__ bool live_slot(uint64_t w0) { return ((uint32_t)w0 & 0x80000000u) != 0; }
 
 __global__ void kv_export_kernel(KvTable t, int64_t nslots, int64_t *val_out, int64_t max, unsigned long long *cursor) {
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nslots; s += (int64_t)gridDim.x * blockDim.x) {
-        const uint64_t sl = t.slots[s];
-        if (live_slot(sl)) {
+        const unsigned long long *sp = t.slots + 4 * s;
+        if (live_slot(sp[0])) {
             unsigned long long p = atomicAdd(cursor, 1ull);
-            if ((int64_t)p < max) val_out[p] = *reinterpret_cast<const int64_t *>(t.arena + rec_off_of(sl));
+            if ((int64_t)p < max) val_out[p] = (int64_t)(sp[1] >> 24);
         }
     }
 }
 
 __global__ void kv_remap_kernel(KvTable t, int64_t nslots, const int64_t *__restrict__ map, int64_t nmap) {
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nslots; s += (int64_t)gridDim.x * blockDim.x) {
-        const uint64_t sl = t.slots[s];
-        if (live_slot(sl)) {
-            int64_t *v = reinterpret_cast<int64_t *>(t.arena + rec_off_of(sl));
-            if (*v >= 0 && *v < nmap) *v = map[*v];
+        unsigned long long *sp = t.slots + 4 * s;
+        if (live_slot(sp[0])) {
+            const int64_t v = (int64_t)(sp[1] >> 24);
+            if (v >= 0 && v < nmap) sp[1] = pack_w1((int64_t)(sp[1] & 0xffffffull), map[v]);
         }
     }
 }
 
-// rebuild: every live key of the old table is copied into a fresh arena (compacting away
-// overwritten/erased records) and re-inserted by its hash (no duplicates exist)
+// rebuild: every live key of the old table is re-inserted by its hash into a fresh table
+// (no duplicates exist); long keys' records move into a fresh, compacted arena
 __global__ void kv_rebuild_kernel(const unsigned long long *__restrict__ old_slots, int64_t old_n,
                                   const uint8_t *__restrict__ old_arena, KvTable t) {
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < old_n; s += (int64_t)gridDim.x * blockDim.x) {
-        const uint64_t sl = old_slots[s];
-        if (!live_slot(sl)) continue;
-        const uint8_t *rec = old_arena + rec_off_of(sl);
-        const int64_t len = (int64_t)(uint32_t)reinterpret_cast<const uint64_t *>(rec)[1];
-        const int64_t rb = rec_bytes(len);
-        const int64_t dst = (int64_t)atomicAdd(&t.counts[2], (unsigned long long)rb);
-        for (int64_t o = 0; o < rb; o += 8)
-            *reinterpret_cast<uint64_t *>(t.arena + dst + o) = *reinterpret_cast<const uint64_t *>(rec + o);
-        const KeyRef k(rec + KV_REC_HDR, len);
-        uint32_t tag, hb;
-        hash_key(k, t.weak, tag, hb);
+        const unsigned long long *op = old_slots + 4 * s;
+        const uint64_t w0 = op[0], w1 = op[1], w2 = op[2], w3 = op[3];
+        if (!live_slot(w0)) continue;
+        const int64_t len = (int64_t)(w1 & 0xffffffull);
+        int64_t rec = 0;
+        uint32_t tag, hb, pw[4];
+        if (len > KV_INLINE) {
+            const uint8_t *src = old_arena + ((int64_t)(uint32_t)(w0 >> 32) << 5);
+            const int64_t rb = rec_bytes(len);
+            rec = (int64_t)atomicAdd(&t.counts[2], (unsigned long long)rb);
+            for (int64_t o = 0; o < rb; o += 8)
+                *reinterpret_cast<uint64_t *>(t.arena + rec + o) = *reinterpret_cast<const uint64_t *>(src + o);
+            hash_key(KeyRef(src, len), t.weak, tag, hb, pw);
+        } else {
+            hash_inline(w2, w3, len, t.weak, tag, hb);
+        }
         int64_t b = (int64_t)(hb & (uint32_t)(t.nb - 1));
         bool done = false;
         for (int64_t p = 0; p < t.nb && !done; ++p) {
             for (int j = 0; j < KV_BUCKET && !done; ++j) {
-                if (atomicCAS(t.slots + b * KV_BUCKET + j, 0ull, slot_of(tag, dst)) == 0ull) {
+                unsigned long long *sp = slot_ptr(t, b, j);
+                if (atomicCAS(sp, 0ull, (unsigned long long)tag | ((unsigned long long)REC_BUSY << 32)) == 0ull) {
+                    sp[1] = w1;
+                    sp[2] = w2;
+                    sp[3] = w3;
+                    __threadfence();
+                    atomicExch(sp, (unsigned long long)tag | ((unsigned long long)(rec >> 5) << 32));
                     atomicAdd(&t.counts[0], 1ull);
                     done = true;
                 }
@@ -402,6 +519,9 @@ static int read_counts(pr_kv *h, unsigned long long c[4], cudaStream_t st) {
     return PR_OK;
 }
 
+constexpr int64_t KV_SLOT_BYTES = 32;
+constexpr int64_t KV_ARENA_BASE = 32;  // record index 0 means "no record"
+
 // Rebuild into a table for `need_keys` live keys and an arena of `need_bytes` live record
 // bytes (drops tombstones and garbage records).  Synchronises the device: rare.
 static int rebuild(pr_kv *h, int64_t need_keys, int64_t need_bytes, cudaStream_t st) {
@@ -410,22 +530,23 @@ static int rebuild(pr_kv *h, int64_t need_keys, int64_t need_bytes, cudaStream_t
     if (rc) return rc;
     PR_CUDA(cudaDeviceSynchronize());
     const int64_t live = (int64_t)c[0];
-    const int64_t live_bytes = (int64_t)c[2] - (int64_t)c[3];
+    const int64_t live_bytes = (int64_t)c[2] - KV_ARENA_BASE - (int64_t)c[3];
     const int64_t nslots = slots_for(std::max<int64_t>(need_keys, live));
-    const int64_t acap = std::min<int64_t>(KV_MAX_ARENA,
-                                           std::max<int64_t>(4096, round_up<int64_t>(need_bytes + need_bytes / 2, 256)));
+    const int64_t acap = std::min<int64_t>(KV_MAX_ARENA, std::max<int64_t>(
+                                                             4096, round_up<int64_t>(need_bytes + need_bytes / 2, 256)));
     if (need_bytes > acap) PR_FAIL(PR_ERR_NOMEM, "kv arena: %lld bytes exceed the 128 GiB record space",
                                    (long long)need_bytes);
     unsigned long long *ns = nullptr;
     uint8_t *na = nullptr;
-    PR_CUDA(cudaMalloc(&ns, (size_t)nslots * sizeof(unsigned long long)));
+    PR_CUDA(cudaMalloc(&ns, (size_t)nslots * KV_SLOT_BYTES));
     if (cudaMalloc(&na, (size_t)acap) != cudaSuccess) {
         cudaFree(ns);
         cudaGetLastError();
         PR_FAIL(PR_ERR_NOMEM, "kv arena: cannot allocate %lld bytes", (long long)acap);
     }
-    PR_CUDA(cudaMemsetAsync(ns, 0, (size_t)nslots * sizeof(unsigned long long), st));
-    PR_CUDA(cudaMemsetAsync(h->d_count, 0, 4 * sizeof(unsigned long long), st));
+    PR_CUDA(cudaMemsetAsync(ns, 0, (size_t)nslots * KV_SLOT_BYTES, st));
+    const unsigned long long c0[4] = {0, 0, (unsigned long long)KV_ARENA_BASE, 0};
+    PR_CUDA(cudaMemcpyAsync(h->d_count, c0, sizeof(c0), cudaMemcpyHostToDevice, st));
     unsigned long long *os = h->slots;
     uint8_t *oa = h->arena;
     const int64_t on = h->nslots;
@@ -443,7 +564,25 @@ static int rebuild(pr_kv *h, int64_t need_keys, int64_t need_bytes, cudaStream_t
     cudaFree(os);
     cudaFree(oa);
     h->upper = live;
-    h->arena_upper = live_bytes;
+    h->arena_upper = KV_ARENA_BASE + live_bytes;
+    return PR_OK;
+}
+
+// a larger record arena; record indices stay valid (the used prefix is copied)
+static int grow_arena(pr_kv *h, int64_t need, cudaStream_t st) {
+    const int64_t cap = std::min<int64_t>(KV_MAX_ARENA, round_up<int64_t>(std::max<int64_t>(need + need / 2, 1 << 16), 256));
+    if (need > cap) PR_FAIL(PR_ERR_NOMEM, "kv arena: %lld bytes exceed the 128 GiB record space", (long long)need);
+    uint8_t *na = nullptr;
+    if (cudaMalloc(&na, (size_t)cap) != cudaSuccess) {
+        cudaGetLastError();
+        PR_FAIL(PR_ERR_NOMEM, "kv arena: cannot allocate %lld bytes", (long long)cap);
+    }
+    PR_CUDA(cudaMemcpyAsync(na, h->arena, (size_t)h->arena_upper, cudaMemcpyDeviceToDevice, st));
+    PR_CUDA(cudaStreamSynchronize(st));
+    PR_CUDA(cudaDeviceSynchronize());  // no other stream may still read the old arena
+    cudaFree(h->arena);
+    h->arena = na;
+    h->arena_cap = cap;
     return PR_OK;
 }
 
@@ -462,7 +601,7 @@ static int put_impl(pr_kv *h, const uint8_t *d_bytes, const int64_t *d_off, int6
     if (nbytes < 0 || !d_vals) PR_FAIL(PR_ERR_BAD_ARG, "bad kv_put");
     if (n == 0) return PR_OK;
     cudaStream_t st = as_stream(stream);
-    const int64_t rec_need = n * (KV_REC_HDR + 31) + nbytes;  // >= sum of rec_bytes over the batch
+    const int64_t rec_need = n * 31 + nbytes;  // >= sum of rec_bytes over the batch
     if (2 * (h->upper + n) > h->nslots || h->arena_upper + rec_need > h->arena_cap) {
         unsigned long long c[4];
         rc = read_counts(h, c, st);
@@ -471,8 +610,11 @@ static int put_impl(pr_kv *h, const uint8_t *d_bytes, const int64_t *d_off, int6
         h->arena_upper = (int64_t)c[2];
         const bool slots_short = 2 * (h->upper + n) > h->nslots;
         const bool arena_short = h->arena_upper + rec_need > h->arena_cap;
-        if (slots_short || arena_short) {
-            rc = rebuild(h, (int64_t)c[0] + n, (int64_t)(c[2] - c[3]) + rec_need, st);
+        if (slots_short) {
+            rc = rebuild(h, (int64_t)c[0] + n, (int64_t)(c[2] - c[3]) - KV_ARENA_BASE + rec_need, st);
+            if (rc) return rc;
+        } else if (arena_short) {
+            rc = grow_arena(h, h->arena_upper + rec_need, st);
             if (rc) return rc;
         }
     }
@@ -546,8 +688,8 @@ int pr_kv_create_ex(int64_t capacity, uint32_t flags, pr_kv **out) {
     pr_kv *h = new pr_kv();
     h->flags = flags;
     h->nslots = slots_for(capacity);
-    h->arena_cap = std::max<int64_t>(4096, capacity * 48);
-    if (cudaMalloc(&h->slots, (size_t)h->nslots * sizeof(unsigned long long)) != cudaSuccess ||
+    h->arena_cap = 1 << 16;  // records exist only for keys longer than 16 bytes; grown on demand
+    if (cudaMalloc(&h->slots, (size_t)h->nslots * KV_SLOT_BYTES) != cudaSuccess ||
         cudaMalloc(&h->arena, (size_t)h->arena_cap) != cudaSuccess ||
         cudaMalloc(&h->d_count, 4 * sizeof(unsigned long long)) != cudaSuccess) {
         cudaFree(h->slots);
@@ -556,8 +698,10 @@ int pr_kv_create_ex(int64_t capacity, uint32_t flags, pr_kv **out) {
         cudaGetLastError();
         PR_FAIL(PR_ERR_NOMEM, "kv_create: device allocation failed");
     }
-    PR_CUDA(cudaMemset(h->slots, 0, (size_t)h->nslots * sizeof(unsigned long long)));
-    PR_CUDA(cudaMemset(h->d_count, 0, 4 * sizeof(unsigned long long)));
+    PR_CUDA(cudaMemset(h->slots, 0, (size_t)h->nslots * KV_SLOT_BYTES));
+    const unsigned long long c0[4] = {0, 0, (unsigned long long)KV_ARENA_BASE, 0};
+    PR_CUDA(cudaMemcpy(h->d_count, c0, sizeof(c0), cudaMemcpyHostToDevice));
+    h->arena_upper = KV_ARENA_BASE;
     PR_CUDA(cudaDeviceSynchronize());
     *out = h;
     return PR_OK;
@@ -607,10 +751,12 @@ int pr_kv_erase_text(pr_kv *h, const uint8_t *d_bytes, const int64_t *d_off, int
 int pr_kv_clear(pr_kv *h, void *stream) {
     if (!h) PR_FAIL(PR_ERR_BAD_ARG, "null kv");
     cudaStream_t st = as_stream(stream);
-    PR_CUDA(cudaMemsetAsync(h->slots, 0, (size_t)h->nslots * sizeof(unsigned long long), st));
-    PR_CUDA(cudaMemsetAsync(h->d_count, 0, 4 * sizeof(unsigned long long), st));
+    PR_CUDA(cudaMemsetAsync(h->slots, 0, (size_t)h->nslots * KV_SLOT_BYTES, st));
+    // the counts are reset by a tiny kernel-free copy from a static host block (stream ordered)
+    static const unsigned long long c0[4] = {0, 0, (unsigned long long)KV_ARENA_BASE, 0};
+    PR_CUDA(cudaMemcpyAsync(h->d_count, c0, sizeof(c0), cudaMemcpyHostToDevice, st));
     h->upper = 0;
-    h->arena_upper = 0;
+    h->arena_upper = KV_ARENA_BASE;
     return PR_OK;
 }
 
@@ -628,7 +774,7 @@ int pr_kv_memory(pr_kv *h, int64_t *slot_bytes, int64_t *arena_bytes, int64_t *g
     unsigned long long c[4];
     int rc = read_counts(h, c, as_stream(stream));
     if (rc) return rc;
-    if (slot_bytes) *slot_bytes = h->nslots * (int64_t)sizeof(unsigned long long);
+    if (slot_bytes) *slot_bytes = h->nslots * KV_SLOT_BYTES;
     if (arena_bytes) *arena_bytes = (int64_t)c[2];
     if (garbage_bytes) *garbage_bytes = (int64_t)c[3];
     return PR_OK;
