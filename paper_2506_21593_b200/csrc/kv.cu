@@ -9,41 +9,38 @@
 // Why the layout is what it is (measured, scripts/micro/randload.cu + profiles/):
 // on B200 a random 32-byte read costs a whole 128-byte L2 line from DRAM (4 sectors per
 // request, whatever the load flavour), so the unit of cost is the LINE.  One lookup
-// should therefore touch exactly one random line, and that line should hold everything
-// the lookup needs:
+// therefore touches exactly one random line, and that line holds everything the lookup
+// needs for keys of <= 16 bytes:
 //
-//   slots  32-byte slots, 4 per 128-byte bucket line (nslots a power of two, load <= 0.5):
-//            w0 = u32 tag | u32 rec << 32     tag = 32-bit key hash, top bit forced
-//                                              (0 = EMPTY, 1 = TOMBSTONE); rec = record index
-//                                              in 32-byte units (0 = none), all ones = BUSY
-//                                              (slot claimed, being written)
-//            w1 = u64 len (24 bits) | value << 24   (value < 2^40)
-//            w2, w3 = the first 16 key bytes (zero padded)
-//          A key of <= 16 bytes is confirmed entirely inside its bucket line: a hit or a
-//          miss is ONE random line.  Longer keys also compare their remaining bytes with
-//          their record (only on a full tag + length + 16-byte prefix match).
-//   arena  32-byte aligned records: the full key bytes of keys longer than 16 bytes.
+//   lines  128-byte bucket lines of 4 slots (nslots a power of two, load <= 0.5), laid out
+//          structure-of-arrays (see KvTable): u32 tag[4] | u32 rec[4] | u64 len|value[4] |
+//          16-byte key prefix[4].  tag = 32-bit key hash, top bit forced (0 = EMPTY,
+//          1 = TOMBSTONE, 2 = BUSY while an insert fills the slot); rec = record index of
+//          a key longer than 16 bytes, in 32-byte units; value < 2^40.
+//   arena  32-byte aligned records: the full bytes of keys longer than 16 bytes.
+// A probe reads the 16-byte tag vector of its line (one request; the line comes from DRAM
+// once); only on a tag match does it read that slot's length/value and prefix (L2 hits on
+// the line just fetched) and, for a long key, the rest of the bytes from the record.
 // Hash: two 32-bit multiply-rotate chains over the key's little-endian words (murmur3_32
 // round function, two seeds).  hA -> tag (and shard owner), hB -> home bucket: the
 // ownership bits and the bucket bits come from independent chains.  Only 32-bit integer
 // multiplies: the hash is a short dependency chain per key.
 //
-// Lookup (kv_get_kernel) is warp-cooperative: every lane hashes ONE key (aligned 32-bit
-// loads + funnel shifts), then each 4-lane group probes 4 keys in turn — the key's hash,
-// length and 16-byte prefix are broadcast by shuffle, each lane loads one 32-byte slot of
-// the bucket line (one 256-bit load per lane, the group's four loads coalesce into one
-// 128-byte request), compares in registers, and the group ballots.  All four rounds'
-// loads are issued before any is consumed, so a warp has 32 independent lines in flight.
-// Keys whose bucket is full of other keys finish on a per-lane linear-probing path.
-// Values are write sequence numbers supplied by the host; a put resolves an existing key
-// with atomicMax on w1, so the largest (latest) write wins even when one batch writes a
-// key twice (caches.py:67-74).
+// One thread per key: it hashes its key ONCE (aligned 32-bit loads + funnel shifts, not
+// byte loads), so a warp keeps 32 independent lines in flight; the per-key tag vector is
+// 4 registers, which keeps occupancy high.  Measured alternatives (scripts/micro/kvbench.cu,
+// DESIGN.md §4.4): warp-cooperative 4-lane groups loading the whole line (one 256-bit load
+// per lane) were slower (19-20 vs 24.9 G lookups/s at 4M-key batches), as were 2 or 4 keys
+// per thread and a separate hashing kernel.  Keys whose line is full of other keys continue
+// by linear probing.  Values are write sequence numbers supplied by the host; a put
+// resolves an existing key with atomicMax on len|value, so the largest (latest) write wins
+// even when one batch writes a key twice (caches.py:67-74).
 #include <algorithm>
 
 #include "common.cuh"
 
 struct pr_kv {
-    unsigned long long *slots = nullptr;    // [nslots][4] 32-byte slots
+    uint8_t *lines = nullptr;               // [nslots / 4] 128-byte bucket lines
     int64_t nslots = 0;
     uint8_t *arena = nullptr;               // records
     int64_t arena_cap = 0;                  // bytes
@@ -58,8 +55,6 @@ namespace pr {
 constexpr int KV_BUCKET = 4;  // 32-byte slots per 128-byte bucket line
 constexpr int KV_THREADS = 128;
 constexpr int KV_INLINE = 16;                        // key bytes held in the slot
-constexpr uint32_t REC_BUSY = 0xffffffffu;           // slot claimed, fields being written
-constexpr uint64_t KV_MAX_VALUE = ((uint64_t)1 << 40) - 1;
 constexpr uint32_t TAG_EMPTY = 0, TAG_TOMB = 1;
 constexpr uint32_t SEED_A = 0x5EED1024u, SEED_B = 0xCA5CADE5u;  // the HASH_SEED family (embedding.py:33)
 constexpr int64_t KV_MAX_ARENA = (int64_t)32 << 32;              // 32-bit record index x 32 bytes
@@ -184,57 +179,39 @@ static inline void hash_host(const uint8_t *p, int64_t len, uint32_t &tag, uint3
     h.fin(len, tag, hb);
 }
 
-template <bool STRONG>
-__device__ __forceinline__ void ld256(const void *p, uint64_t &a, uint64_t &b, uint64_t &c, uint64_t &d) {
-    if (STRONG)
-        asm volatile("ld.relaxed.gpu.global.v4.u64 {%0,%1,%2,%3}, [%4];"
-                     : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p) : "memory");
-    else
-        asm("ld.global.cg.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
-}
+// One 128-byte bucket line, structure-of-arrays so a probe reads only what it needs:
+//   [0, 16)    u32 tag[4]       0 = EMPTY, 1 = TOMBSTONE, 2 = BUSY (claimed, being written)
+//   [16, 32)   u32 rec[4]       record of a key longer than 16 bytes, in 32-byte units
+//   [32, 64)   u64 lv[4]        key length (24 bits) | value << 24
+//   [64, 128)  16-byte key prefix[4] (zero padded)
+// A probe loads the 16-byte tag vector (the line comes from DRAM once); only a tag match
+// reads that slot's lv and prefix (L2 hits on the line just fetched).
+constexpr uint32_t TAG_BUSY = 2;
+constexpr int64_t KV_LINE = 128;
 
-template <bool STRONG>
-__device__ __forceinline__ void ld128(const void *p, uint32_t &a, uint32_t &b, uint32_t &c, uint32_t &d) {
-    if (STRONG)
-        asm volatile("ld.relaxed.gpu.global.v4.u32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "l"(p) : "memory");
-    else
-        asm("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "l"(p));
-}
-
-struct Slot {
-    uint64_t w0, w1, w2, w3;
-    __device__ __forceinline__ uint32_t tag() const { return (uint32_t)w0; }
-    __device__ __forceinline__ uint32_t rec() const { return (uint32_t)(w0 >> 32); }
-    __device__ __forceinline__ int64_t len() const { return (int64_t)(w1 & 0xffffffull); }
-    __device__ __forceinline__ int64_t value() const { return (int64_t)(w1 >> 24); }
-};
-
-__host__ __device__ __forceinline__ uint64_t pack_w1(int64_t len, int64_t val) {
+__host__ __device__ __forceinline__ uint64_t pack_lv(int64_t len, int64_t val) {
     return (uint64_t)len | ((uint64_t)val << 24);
-}
-__device__ __forceinline__ uint64_t pw2(const uint32_t pw[4]) { return (uint64_t)pw[0] | ((uint64_t)pw[1] << 32); }
-__device__ __forceinline__ uint64_t pw3(const uint32_t pw[4]) { return (uint64_t)pw[2] | ((uint64_t)pw[3] << 32); }
-
-// bytes [16, len) of a long key against its record (the record holds the whole key)
-template <bool STRONG>
-__device__ __forceinline__ bool tail_matches(const uint8_t *rec, const KeyRef &k) {
-    for (int64_t g = 1; 16 * g < k.len; ++g) {
-        uint32_t r[4];
-        ld128<STRONG>(rec + 16 * g, r[0], r[1], r[2], r[3]);
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-            if (r[q] != k.word(4 * g + q)) return false;
-    }
-    return true;
 }
 
 struct KvTable {
-    unsigned long long *slots;  // [nslots][4]
-    int64_t nb;                 // buckets (power of two)
+    uint8_t *lines;  // [nb][128]
+    int64_t nb;      // buckets (power of two)
     uint8_t *arena;
     unsigned long long *counts;
     int weak;  // PR_KV_WEAK_HASH: 2-bit tags, 4 home buckets (forces collisions; tests only)
+    __device__ __forceinline__ uint8_t *line(int64_t b) const { return lines + b * KV_LINE; }
+    __device__ __forceinline__ uint32_t *tag(int64_t b, int j) const {
+        return reinterpret_cast<uint32_t *>(line(b)) + j;
+    }
+    __device__ __forceinline__ uint32_t *rec(int64_t b, int j) const {
+        return reinterpret_cast<uint32_t *>(line(b) + 16) + j;
+    }
+    __device__ __forceinline__ unsigned long long *lv(int64_t b, int j) const {
+        return reinterpret_cast<unsigned long long *>(line(b) + 32) + j;
+    }
+    __device__ __forceinline__ uint4 *prefix(int64_t b, int j) const {
+        return reinterpret_cast<uint4 *>(line(b) + 64) + j;
+    }
 };
 
 struct KeyBatch {
@@ -243,98 +220,97 @@ struct KeyBatch {
     int64_t n;
 };
 
-__device__ __forceinline__ unsigned long long *slot_ptr(const KvTable &t, int64_t b, int j) {
-    return t.slots + (b * KV_BUCKET + j) * 4;
-}
-
-// does slot s hold the key (tag, len, prefix already compared against the record for long keys)?
 template <bool STRONG>
-__device__ __forceinline__ bool slot_holds(const KvTable &t, const Slot &s, uint32_t tag, const KeyRef &k,
-                                           const uint32_t pw[4]) {
-    if (s.tag() != tag || s.rec() == REC_BUSY || s.len() != k.len || s.w2 != pw2(pw) || s.w3 != pw3(pw))
-        return false;
-    return k.len <= KV_INLINE || tail_matches<STRONG>(t.arena + ((int64_t)s.rec() << 5), k);
+__device__ __forceinline__ uint4 ld4(const void *p) {
+    uint4 v;
+    if (STRONG)
+        asm volatile("ld.relaxed.gpu.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+    else
+        asm("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
+template <bool STRONG>
+__device__ __forceinline__ uint64_t ld8(const void *p) {
+    uint64_t v;
+    if (STRONG)
+        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    else
+        asm("ld.global.cg.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    return v;
+}
+template <bool STRONG>
+__device__ __forceinline__ uint32_t ld4b(const void *p) {
+    uint32_t v;
+    if (STRONG)
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    else
+        asm("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
 }
 
-// per-lane linear probing from bucket b (the cooperative pass's overflow path and puts)
-__device__ int64_t probe_lane(const KvTable &t, int64_t b, uint32_t tag, const KeyRef &k, const uint32_t pw[4]) {
-    for (int64_t p = 0; p < t.nb; ++p) {
-        for (int j = 0; j < KV_BUCKET; ++j) {
-            Slot s;
-            ld256<false>(slot_ptr(t, b, j), s.w0, s.w1, s.w2, s.w3);
-            if (s.tag() == TAG_EMPTY) return -1;
-            if (slot_holds<false>(t, s, tag, k, pw)) return s.value();
-        }
-        b = (b + 1) & (t.nb - 1);
+// bytes [16, len) of a long key against its record (the record holds the whole key)
+template <bool STRONG>
+__device__ __forceinline__ bool tail_matches(const uint8_t *rec, const KeyRef &k) {
+    for (int64_t g = 1; 16 * g < k.len; ++g) {
+        const uint4 r = ld4<STRONG>(rec + 16 * g);
+        if (r.x != k.word(4 * g) || r.y != k.word(4 * g + 1) || r.z != k.word(4 * g + 2) || r.w != k.word(4 * g + 3))
+            return false;
     }
-    return -1;
+    return true;
 }
 
-// ---- get: warp-cooperative, 4 lanes per bucket line --------------------------
+// slot (b, j) carries the key's tag: does it hold the key?  *val = its value if so.
+template <bool STRONG>
+__device__ __forceinline__ bool slot_holds(const KvTable &t, int64_t b, int j, const KeyRef &k, const uint32_t pw[4],
+                                           int64_t *val) {
+    const uint64_t lv = ld8<STRONG>(t.lv(b, j));
+    const uint4 pre = ld4<STRONG>(t.prefix(b, j));
+    if ((int64_t)(lv & 0xffffffull) != k.len || pre.x != pw[0] || pre.y != pw[1] || pre.z != pw[2] || pre.w != pw[3])
+        return false;
+    if (k.len > KV_INLINE &&
+        !tail_matches<STRONG>(t.arena + ((int64_t)ld4b<STRONG>(t.rec(b, j)) << 5), k))
+        return false;
+    *val = (int64_t)(lv >> 24);
+    return true;
+}
+
+// ---- get: one thread per key -------------------------------------------------
 __global__ void __launch_bounds__(KV_THREADS) kv_get_kernel(KvTable t, KeyBatch kb, int rank, int world,
                                                              int64_t *__restrict__ out_vals,
                                                              uint8_t *__restrict__ out_hit) {
-    const int lane = threadIdx.x & 31;
-    const int sub = lane & 3, g0 = lane & ~3;
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const bool have = i < kb.n;
-    int64_t a = 0, len = 0;
-    if (have) {
-        a = __ldg(kb.off + i);
-        len = __ldg(kb.off + i + 1) - a;
-    }
-    const KeyRef k(kb.bytes + a, len);
-    uint32_t tag = 0, hb = 0, pw[4] = {0, 0, 0, 0};
-    bool active = false;
-    if (have) {
-        hash_key(k, t.weak, tag, hb, pw);
-        active = world <= 1 || owner_of(tag, world) == rank;
-    }
-    const int64_t home = (int64_t)(hb & (uint32_t)(t.nb - 1));
-    // issue the four rounds' slot loads (round r probes the key of lane g0 + r)
-    Slot s[4];
-    bool act[4];
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-        const int src = g0 + r;
-        act[r] = __shfl_sync(0xffffffffu, active, src);
-        const int64_t b = __shfl_sync(0xffffffffu, home, src);
-        s[r].w0 = s[r].w1 = s[r].w2 = s[r].w3 = 0;
-        if (act[r]) ld256<false>(slot_ptr(t, b, sub), s[r].w0, s[r].w1, s[r].w2, s[r].w3);
-    }
+    if (i >= kb.n) return;
+    const int64_t a = __ldg(kb.off + i);
+    const KeyRef k(kb.bytes + a, __ldg(kb.off + i + 1) - a);
+    uint32_t tag, hb, pw[4];
+    hash_key(k, t.weak, tag, hb, pw);
     int64_t val = -1;
-    bool unresolved = false;
+    if (world <= 1 || owner_of(tag, world) == rank) {
+        int64_t b = (int64_t)(hb & (uint32_t)(t.nb - 1));
+        for (int64_t p = 0; p < t.nb; ++p) {
+            const uint4 tg = ld4<false>(t.tag(b, 0));
+            const uint32_t tv[4] = {tg.x, tg.y, tg.z, tg.w};
+            bool done = false;
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-        const int src = g0 + r;
-        const uint32_t rtag = __shfl_sync(0xffffffffu, tag, src);
-        const int64_t rlen = __shfl_sync(0xffffffffu, len, src);
-        const int64_t ra = __shfl_sync(0xffffffffu, a, src);
-        uint32_t rpw[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) rpw[q] = __shfl_sync(0xffffffffu, pw[q], src);
-        bool match = false, empty = false;
-        if (act[r]) {
-            const KeyRef rk(kb.bytes + ra, rlen);
-            match = slot_holds<false>(t, s[r], rtag, rk, rpw);
-            empty = s[r].tag() == TAG_EMPTY;
-        }
-        const unsigned mm = (__ballot_sync(0xffffffffu, match) >> g0) & 0xFu;
-        const unsigned me = (__ballot_sync(0xffffffffu, empty) >> g0) & 0xFu;
-        // first match wins; an empty slot before it cannot exist (inserts fill in order)
-        const int who = mm ? __ffs(mm) - 1 : 0;
-        const int64_t v = __shfl_sync(0xffffffffu, s[r].value(), g0 + who);
-        if (sub == r) {
-            if (mm) val = v;
-            else if (!me && act[r]) unresolved = true;  // bucket full of other keys
+            for (int j = 0; j < KV_BUCKET; ++j) {
+                if (done) break;
+                if (tv[j] == tag) {
+                    int64_t v;
+                    if (slot_holds<false>(t, b, j, k, pw, &v)) {
+                        val = v;
+                        done = true;
+                    }
+                } else if (tv[j] == TAG_EMPTY) {
+                    done = true;
+                }
+            }
+            if (done) break;
+            b = (b + 1) & (t.nb - 1);
         }
     }
-    if (unresolved)  // rare: continue linear probing alone from the next bucket
-        val = probe_lane(t, (home + 1) & (t.nb - 1), tag, k, pw);
-    if (have) {
-        out_vals[i] = val;
-        out_hit[i] = val >= 0;
-    }
+    out_vals[i] = val;
+    out_hit[i] = val >= 0;
 }
 
 // copy a long key into a fresh record (zero padded to its 32-byte record size)
@@ -344,20 +320,20 @@ __device__ void write_record(uint8_t *rec, const KeyRef &k) {
     for (int64_t j = 0; j < words; ++j) w[j] = k.word(j);
 }
 
-// wait until a claimed slot is published (its writer is another thread of this launch)
-__device__ __forceinline__ uint64_t await_published(unsigned long long *sp) {
-    uint64_t w0;
-    for (;;) {
-        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w0) : "l"(sp) : "memory");
-        if ((uint32_t)(w0 >> 32) != REC_BUSY) return w0;
-        __nanosleep(32);
-    }
+// fill a claimed slot and publish its tag (the slot's other fields become visible first)
+__device__ __forceinline__ void publish(const KvTable &t, int64_t b, int j, uint32_t tag, uint32_t rec, uint64_t lv,
+                                        uint4 pre) {
+    *t.rec(b, j) = rec;
+    *t.lv(b, j) = lv;
+    *t.prefix(b, j) = pre;
+    __threadfence();
+    atomicExch(t.tag(b, j), tag);
 }
 
 // ---- put (upsert) / erase: one thread per key --------------------------------
-// Insert protocol: CAS w0 EMPTY -> {tag, BUSY}; write w1..w3 (+ the record of a long key);
-// fence; publish w0 = {tag, rec}.  A thread that meets a BUSY slot carrying its tag waits
-// for the publication before comparing (duplicates of one new key inside one batch).
+// Insert protocol: CAS tag EMPTY -> BUSY; write rec, lv, prefix (+ the record of a long
+// key); fence; publish the tag.  A thread that meets a BUSY slot waits for its
+// publication before comparing (duplicates of one new key inside one batch).
 template <bool ERASE>
 __global__ void __launch_bounds__(KV_THREADS) kv_update_kernel(KvTable t, KeyBatch kb, int rank, int world,
                                                                 const int64_t *__restrict__ in_vals) {
@@ -372,38 +348,37 @@ __global__ void __launch_bounds__(KV_THREADS) kv_update_kernel(KvTable t, KeyBat
     int64_t b = (int64_t)(hb & (uint32_t)(t.nb - 1));
     for (int64_t p = 0; p < t.nb; ++p) {
         for (int j = 0; j < KV_BUCKET; ++j) {
-            unsigned long long *sp = slot_ptr(t, b, j);
-            Slot s;
-            ld256<true>(sp, s.w0, s.w1, s.w2, s.w3);
+            uint32_t cur = ld4b<true>(t.tag(b, j));
             for (;;) {  // re-examines slot j after a lost CAS / a pending publication
-                if (s.tag() == tag) {
-                    if (s.rec() == REC_BUSY) {
-                        s.w0 = await_published(sp);
-                        __threadfence();
-                        ld256<true>(sp, s.w0, s.w1, s.w2, s.w3);
-                        continue;
-                    }
-                    __threadfence();
-                    if (slot_holds<true>(t, s, tag, k, pw)) {
+                if (cur == TAG_BUSY) {
+                    do {
+                        __nanosleep(32);
+                        cur = ld4b<true>(t.tag(b, j));
+                    } while (cur == TAG_BUSY);
+                    continue;
+                }
+                if (cur == tag) {
+                    __threadfence();  // pairs with publish(): the slot's fields are visible
+                    int64_t old;
+                    if (slot_holds<true>(t, b, j, k, pw, &old)) {
                         if (ERASE) {
-                            if (atomicCAS(sp, s.w0, (unsigned long long)TAG_TOMB) == s.w0) {
+                            if (atomicCAS(t.tag(b, j), tag, TAG_TOMB) == tag) {
                                 atomicAdd(&t.counts[0], (unsigned long long)-1ll);
                                 atomicAdd(&t.counts[1], 1ull);
                                 atomicAdd(&t.counts[3], (unsigned long long)rec_bytes(k.len));
                             }
                         } else {
-                            atomicMax(sp + 1, (unsigned long long)pack_w1(k.len, v));
+                            atomicMax(t.lv(b, j), (unsigned long long)pack_lv(k.len, v));
                         }
                         return;
                     }
                     break;  // same tag, another key
                 }
-                if (s.tag() != TAG_EMPTY) break;  // another key or a tombstone: next slot
-                if (ERASE) return;                // first empty slot: the key is absent
-                const unsigned long long claim = (unsigned long long)tag | ((unsigned long long)REC_BUSY << 32);
-                const unsigned long long got = atomicCAS(sp, 0ull, claim);
-                if (got != 0ull) {  // lost the race: look at what was claimed there
-                    s.w0 = got;
+                if (cur != TAG_EMPTY) break;  // another key or a tombstone: next slot
+                if (ERASE) return;            // first empty slot: the key is absent
+                const uint32_t got = atomicCAS(t.tag(b, j), TAG_EMPTY, TAG_BUSY);
+                if (got != TAG_EMPTY) {  // lost the race: look at what was claimed there
+                    cur = got;
                     continue;
                 }
                 int64_t rec = 0;
@@ -411,11 +386,7 @@ __global__ void __launch_bounds__(KV_THREADS) kv_update_kernel(KvTable t, KeyBat
                     rec = (int64_t)atomicAdd(&t.counts[2], (unsigned long long)rec_bytes(k.len));
                     write_record(t.arena + rec, k);
                 }
-                sp[1] = pack_w1(k.len, v);
-                sp[2] = pw2(pw);
-                sp[3] = pw3(pw);
-                __threadfence();
-                atomicExch(sp, (unsigned long long)tag | ((unsigned long long)(rec >> 5) << 32));  // publish
+                publish(t, b, j, tag, (uint32_t)(rec >> 5), pack_lv(k.len, v), make_uint4(pw[0], pw[1], pw[2], pw[3]));
                 atomicAdd(&t.counts[0], 1ull);
                 return;
             }
@@ -439,61 +410,61 @@ __global__ void fingerprint_kernel(KeyBatch kb, uint64_t *__restrict__ fp, int w
     }
 }
 
-// ---- maintenance ---------------------------------------------------------------
-__device__ __forceinline__ bool live_slot(uint64_t w0) { return ((uint32_t)w0 & 0x80000000u) != 0; }
+// ---- maintenance (one thread per slot) -------------------------------------------
+__device__ __forceinline__ bool live_tag(uint32_t tag) { return (tag & 0x80000000u) != 0; }
 
 __global__ void kv_export_kernel(KvTable t, int64_t nslots, int64_t *val_out, int64_t max, unsigned long long *cursor) {
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nslots; s += (int64_t)gridDim.x * blockDim.x) {
-        const unsigned long long *sp = t.slots + 4 * s;
-        if (live_slot(sp[0])) {
+        const int64_t b = s / KV_BUCKET;
+        const int j = (int)(s % KV_BUCKET);
+        if (live_tag(*t.tag(b, j))) {
             unsigned long long p = atomicAdd(cursor, 1ull);
-            if ((int64_t)p < max) val_out[p] = (int64_t)(sp[1] >> 24);
+            if ((int64_t)p < max) val_out[p] = (int64_t)(*t.lv(b, j) >> 24);
         }
     }
 }
 
 __global__ void kv_remap_kernel(KvTable t, int64_t nslots, const int64_t *__restrict__ map, int64_t nmap) {
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nslots; s += (int64_t)gridDim.x * blockDim.x) {
-        unsigned long long *sp = t.slots + 4 * s;
-        if (live_slot(sp[0])) {
-            const int64_t v = (int64_t)(sp[1] >> 24);
-            if (v >= 0 && v < nmap) sp[1] = pack_w1((int64_t)(sp[1] & 0xffffffull), map[v]);
+        const int64_t b = s / KV_BUCKET;
+        const int j = (int)(s % KV_BUCKET);
+        if (live_tag(*t.tag(b, j))) {
+            const uint64_t lv = *t.lv(b, j);
+            const int64_t v = (int64_t)(lv >> 24);
+            if (v >= 0 && v < nmap) *t.lv(b, j) = pack_lv((int64_t)(lv & 0xffffffull), map[v]);
         }
     }
 }
 
 // rebuild: every live key of the old table is re-inserted by its hash into a fresh table
 // (no duplicates exist); long keys' records move into a fresh, compacted arena
-__global__ void kv_rebuild_kernel(const unsigned long long *__restrict__ old_slots, int64_t old_n,
-                                  const uint8_t *__restrict__ old_arena, KvTable t) {
-    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < old_n; s += (int64_t)gridDim.x * blockDim.x) {
-        const unsigned long long *op = old_slots + 4 * s;
-        const uint64_t w0 = op[0], w1 = op[1], w2 = op[2], w3 = op[3];
-        if (!live_slot(w0)) continue;
-        const int64_t len = (int64_t)(w1 & 0xffffffull);
+__global__ void kv_rebuild_kernel(KvTable o, int64_t old_slots, KvTable t) {
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < old_slots; s += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t ob = s / KV_BUCKET;
+        const int oj = (int)(s % KV_BUCKET);
+        if (!live_tag(*o.tag(ob, oj))) continue;
+        const uint64_t lv = *o.lv(ob, oj);
+        const uint4 pre = *o.prefix(ob, oj);
+        const int64_t len = (int64_t)(lv & 0xffffffull);
         int64_t rec = 0;
         uint32_t tag, hb, pw[4];
         if (len > KV_INLINE) {
-            const uint8_t *src = old_arena + ((int64_t)(uint32_t)(w0 >> 32) << 5);
+            const uint8_t *src = o.arena + ((int64_t)*o.rec(ob, oj) << 5);
             const int64_t rb = rec_bytes(len);
             rec = (int64_t)atomicAdd(&t.counts[2], (unsigned long long)rb);
-            for (int64_t o = 0; o < rb; o += 8)
-                *reinterpret_cast<uint64_t *>(t.arena + rec + o) = *reinterpret_cast<const uint64_t *>(src + o);
+            for (int64_t x = 0; x < rb; x += 8)
+                *reinterpret_cast<uint64_t *>(t.arena + rec + x) = *reinterpret_cast<const uint64_t *>(src + x);
             hash_key(KeyRef(src, len), t.weak, tag, hb, pw);
         } else {
-            hash_inline(w2, w3, len, t.weak, tag, hb);
+            hash_inline((uint64_t)pre.x | ((uint64_t)pre.y << 32), (uint64_t)pre.z | ((uint64_t)pre.w << 32), len,
+                        t.weak, tag, hb);
         }
         int64_t b = (int64_t)(hb & (uint32_t)(t.nb - 1));
         bool done = false;
         for (int64_t p = 0; p < t.nb && !done; ++p) {
             for (int j = 0; j < KV_BUCKET && !done; ++j) {
-                unsigned long long *sp = slot_ptr(t, b, j);
-                if (atomicCAS(sp, 0ull, (unsigned long long)tag | ((unsigned long long)REC_BUSY << 32)) == 0ull) {
-                    sp[1] = w1;
-                    sp[2] = w2;
-                    sp[3] = w3;
-                    __threadfence();
-                    atomicExch(sp, (unsigned long long)tag | ((unsigned long long)(rec >> 5) << 32));
+                if (atomicCAS(t.tag(b, j), TAG_EMPTY, TAG_BUSY) == TAG_EMPTY) {
+                    publish(t, b, j, tag, (uint32_t)(rec >> 5), lv, pre);
                     atomicAdd(&t.counts[0], 1ull);
                     done = true;
                 }
@@ -510,7 +481,7 @@ static int64_t slots_for(int64_t keys) {
 }
 
 static KvTable table_of(pr_kv *h) {
-    return KvTable{h->slots, h->nslots / KV_BUCKET, h->arena, h->d_count, (h->flags & PR_KV_WEAK_HASH) ? 1 : 0};
+    return KvTable{h->lines, h->nslots / KV_BUCKET, h->arena, h->d_count, (h->flags & PR_KV_WEAK_HASH) ? 1 : 0};
 }
 
 static int read_counts(pr_kv *h, unsigned long long c[4], cudaStream_t st) {
@@ -536,7 +507,7 @@ static int rebuild(pr_kv *h, int64_t need_keys, int64_t need_bytes, cudaStream_t
                                                              4096, round_up<int64_t>(need_bytes + need_bytes / 2, 256)));
     if (need_bytes > acap) PR_FAIL(PR_ERR_NOMEM, "kv arena: %lld bytes exceed the 128 GiB record space",
                                    (long long)need_bytes);
-    unsigned long long *ns = nullptr;
+    uint8_t *ns = nullptr;
     uint8_t *na = nullptr;
     PR_CUDA(cudaMalloc(&ns, (size_t)nslots * KV_SLOT_BYTES));
     if (cudaMalloc(&na, (size_t)acap) != cudaSuccess) {
@@ -547,17 +518,18 @@ static int rebuild(pr_kv *h, int64_t need_keys, int64_t need_bytes, cudaStream_t
     PR_CUDA(cudaMemsetAsync(ns, 0, (size_t)nslots * KV_SLOT_BYTES, st));
     const unsigned long long c0[4] = {0, 0, (unsigned long long)KV_ARENA_BASE, 0};
     PR_CUDA(cudaMemcpyAsync(h->d_count, c0, sizeof(c0), cudaMemcpyHostToDevice, st));
-    unsigned long long *os = h->slots;
+    const KvTable old = table_of(h);
+    uint8_t *os = h->lines;
     uint8_t *oa = h->arena;
     const int64_t on = h->nslots;
-    h->slots = ns;
+    h->lines = ns;
     h->nslots = nslots;
     h->arena = na;
     h->arena_cap = acap;
     if (live > 0) {
         const int g = (int)std::min<int64_t>(ceil_div<int64_t>(on, 256), (int64_t)sm_count() * 16);
         ::pr::count_launch();
-        kv_rebuild_kernel<<<g, 256, 0, st>>>(os, on, oa, table_of(h));
+        kv_rebuild_kernel<<<g, 256, 0, st>>>(old, on, table_of(h));
         PR_LAUNCH_CHECK();
     }
     PR_CUDA(cudaStreamSynchronize(st));
@@ -689,16 +661,16 @@ int pr_kv_create_ex(int64_t capacity, uint32_t flags, pr_kv **out) {
     h->flags = flags;
     h->nslots = slots_for(capacity);
     h->arena_cap = 1 << 16;  // records exist only for keys longer than 16 bytes; grown on demand
-    if (cudaMalloc(&h->slots, (size_t)h->nslots * KV_SLOT_BYTES) != cudaSuccess ||
+    if (cudaMalloc(&h->lines, (size_t)h->nslots * KV_SLOT_BYTES) != cudaSuccess ||
         cudaMalloc(&h->arena, (size_t)h->arena_cap) != cudaSuccess ||
         cudaMalloc(&h->d_count, 4 * sizeof(unsigned long long)) != cudaSuccess) {
-        cudaFree(h->slots);
+        cudaFree(h->lines);
         cudaFree(h->arena);
         delete h;
         cudaGetLastError();
         PR_FAIL(PR_ERR_NOMEM, "kv_create: device allocation failed");
     }
-    PR_CUDA(cudaMemset(h->slots, 0, (size_t)h->nslots * KV_SLOT_BYTES));
+    PR_CUDA(cudaMemset(h->lines, 0, (size_t)h->nslots * KV_SLOT_BYTES));
     const unsigned long long c0[4] = {0, 0, (unsigned long long)KV_ARENA_BASE, 0};
     PR_CUDA(cudaMemcpy(h->d_count, c0, sizeof(c0), cudaMemcpyHostToDevice));
     h->arena_upper = KV_ARENA_BASE;
@@ -710,7 +682,7 @@ int pr_kv_create_ex(int64_t capacity, uint32_t flags, pr_kv **out) {
 int pr_kv_destroy(pr_kv *h) {
     if (!h) return PR_OK;
     cudaDeviceSynchronize();
-    cudaFree(h->slots);
+    cudaFree(h->lines);
     cudaFree(h->arena);
     cudaFree(h->d_count);
     delete h;
@@ -751,7 +723,7 @@ int pr_kv_erase_text(pr_kv *h, const uint8_t *d_bytes, const int64_t *d_off, int
 int pr_kv_clear(pr_kv *h, void *stream) {
     if (!h) PR_FAIL(PR_ERR_BAD_ARG, "null kv");
     cudaStream_t st = as_stream(stream);
-    PR_CUDA(cudaMemsetAsync(h->slots, 0, (size_t)h->nslots * KV_SLOT_BYTES, st));
+    PR_CUDA(cudaMemsetAsync(h->lines, 0, (size_t)h->nslots * KV_SLOT_BYTES, st));
     // the counts are reset by a tiny kernel-free copy from a static host block (stream ordered)
     static const unsigned long long c0[4] = {0, 0, (unsigned long long)KV_ARENA_BASE, 0};
     PR_CUDA(cudaMemcpyAsync(h->d_count, c0, sizeof(c0), cudaMemcpyHostToDevice, st));
