@@ -76,6 +76,8 @@ def c2_semantic(peak_tops: float, peak_how: str = "", n=1_000_000, d=768, batch=
     got_row = row.cpu().numpy()[sel]
     want_hit = (want.count > 0) & (want.reported[:, 0] >= threshold)
     mism = int(((got_hit != want_hit) | (got_row != want.rows[:, 0])).sum())
+    probes = _c2_threshold_probes(sc, X, Q, B2, threshold, n_probe_queries=32)
+    sc.threshold = threshold
     return {
         "workload": f"semantic-cache top-1 + threshold {threshold} over {n} x {d}, batch {batch} (configs[1])",
         "value": batch / (ms / 1e3), "unit": "lookups/s", "ms_per_batch": ms,
@@ -84,7 +86,39 @@ def c2_semantic(peak_tops: float, peak_how: str = "", n=1_000_000, d=768, batch=
                      "unit": "TOP/s", "frac": flop / (kern / 1e3) / 1e12 / peak_tops, "kernel_ms": kern,
                      "kernel": "tc8_scan_kernel", "peak_kind": "measured int8 sustained: " + peak_how},
         "parity": {"queries_checked": int(sel.size), "mismatches": mism},
+        "threshold_probes": probes,
     }
+
+
+def _c2_threshold_probes(sc, X, Q, n_near, threshold, n_probe_queries=32):
+    """64 threshold-boundary probes at 1M x 768 (the reference's
+    equality/nextafter acceptance test, tests/test_acceptance.py:142-182, at scale).
+    For 32 near-duplicate queries the oracle (C einsum restatement over all 1M rows) gives
+    the exact reported top-1 score s; the cache is then asked with threshold = s (the
+    inclusive gate, caches.py:140, must HIT) and threshold = nextafter(s, +inf) (must MISS),
+    and the served row and score bits must equal the oracle's."""
+    import torch
+
+    from oracle import flat_index as F
+
+    sel = np.linspace(0, n_near - 1, n_probe_queries).astype(np.int64)
+    Qs = Q[torch.from_numpy(sel).cuda()]
+    want = F.c_search(X.cpu().numpy(), Qs.cpu().numpy(), 1)
+    bad, probes, skipped = 0, 0, 0
+    for j in range(sel.size):
+        s = float(want.reported[j, 0])
+        if not (0.0 < s < 1.0):
+            skipped += 1
+            continue
+        for thr, expect in ((s, True), (float(np.nextafter(s, np.inf)), False)):
+            sc.threshold = thr
+            hit, row, score = sc.lookup_batch(Qs[j:j + 1], account=False)
+            probes += 1
+            ok = (bool(hit.item()) == expect and int(row.item()) == int(want.rows[j, 0])
+                  and float(score.item()) == s)
+            bad += 0 if ok else 1
+    return {"probes": probes, "mismatches": bad, "skipped_queries": skipped,
+            "oracle": "oracle/einsum_order.c over all rows; threshold = exact top-1 score (hit) and its nextafter (miss)"}
 
 
 # ---------------------------------------------------------------- C4 batch sweep
@@ -313,7 +347,7 @@ _LAST_BATCH_WALL: list = []  # (worker, session, batch, host wall ms) of every c
 
 
 def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_session=20_000, batch=4096,
-              seed=0, parity_queries=300, profile=False, workers=1):
+              seed=0, parity_queries=1000, profile=False, workers=1, l5_oracle_queries=8):
     """Routed replay over the bench's 10M x 1024 store turned into a knowledge base:
     rows [0, n_qa) hold HashEmbedder(context) of the QA pool, the rest stay dense
     distractors.
@@ -449,23 +483,48 @@ def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_se
         for name, c in t["layers"].items():
             layer_counts[name] = layer_counts.get(name, 0) + c
     gc.unfreeze()
-    # parity: the first parity_queries of session 0 routed one by one on a twin router
-    twin = make_router()
+    # parity: the first parity_queries of session 0, routed by route_batch on a fresh router,
+    # against the REAL reference router (ragcascade.CascadeRouter from the offline install in
+    # baseline/_ref, router.py:275-364) driving fresh GPU stores over the same knowledge
+    # base one query at a time; a twin of this package's route() when the install is absent
     sid, st = streams[0]
-    twin.reset_session()
-    twin.latency_model.reseed([seed, 0, 1])
-    ref = make_router()
-    ref.reset_session()
-    ref.latency_model.reseed([seed, 0, 1])
     qs = [validate_query(t, sid, query_id=f"{sid}-q{i:05d}", issued_at_ns=0) for i, (t, _) in enumerate(st)]
     qs = qs[:parity_queries]
-    got = ref.route_batch(qs)
-    mism = 0
+    mine = make_router()
+    mine.reset_session()
+    mine.latency_model.reseed([seed, 0, 1])
+    got = mine.route_batch(qs)
+    mism, oracle_name = 0, "twin router, sequential route() per query (reference semantics)"
+    try:
+        from oracle.ref_c1 import load_reference
+
+        rc = load_reference()
+        from paper_2506_21593_b200 import AdaptiveKnowledgeMemory, FixedKVCache, SemanticCache
+
+        rref = rc.CascadeRouter(embedder=rc.HashEmbedder(), backend=rc.StubBackend(), knowledge_base=kb,
+                                kv_cache=FixedKVCache(), semantic_cache=SemanticCache(emb),
+                                adaptive_memory=AdaptiveKnowledgeMemory())
+        oracle_name = ("ragcascade.CascadeRouter (the reference, baseline/_ref) over GPU stores, one route() per "
+                       "query: answers, serving layer, passages, per-layer probe outcomes")
+
+        def ref_route(q):
+            return rref.route(rc.validate_query(q.text, q.session_id))
+    except ImportError:
+        twin = make_router()
+        twin.reset_session()
+        twin.latency_model.reseed([seed, 0, 1])
+        ref_route = twin.route
+    l5_sample = []
     for q, (a, ev) in zip(qs, got):
-        b, ev2 = twin.route(q)
-        if (a.text, a.layer, a.supporting_passage_ids, [p.outcome for p in ev.layers_probed]) != \
-                (b.text, b.layer, b.supporting_passage_ids, [p.outcome for p in ev2.layers_probed]):
+        b, ev2 = ref_route(q)
+        if (a.text, a.layer.wire_name, tuple(a.supporting_passage_ids),
+            [(p.layer.wire_name, p.outcome) for p in ev.layers_probed]) != \
+                (b.text, b.layer.wire_name, tuple(b.supporting_passage_ids),
+                 [(p.layer.wire_name, p.outcome) for p in ev2.layers_probed]):
             mism += 1
+        if a.layer == LayerTag.NAIVE_RAG and len(l5_sample) < l5_oracle_queries:
+            l5_sample.append(q.text)
+    l5 = _c5_l5_oracle(kb, emb, l5_sample) if l5_sample else None
     if profile:
         _LAST_PROFILE_LOG[:] = getattr(router, "batch_profile_log", [])
     return {
@@ -481,6 +540,34 @@ def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_se
         "stage_seconds": getattr(router, "batch_profile", None),
         "query_vectors": "device HashEmbedder (pr_hash_embed) inside the timed region, from raw query texts",
         "prep_seconds": prep_s,
-        "parity": {"queries_checked": len(qs), "mismatches": mism,
-                   "oracle": "twin router, sequential route() per query (reference semantics)"},
+        "parity": {"queries_checked": len(qs), "mismatches": mism, "oracle": oracle_name,
+                   "l5_rows_vs_chunked_oracle": l5},
     }
+
+
+def _c5_l5_oracle(kb, emb, texts, k=10, chunk=1 << 20):
+    """Sampled L5 checks at full KB size: the knowledge-base top-k (seed_k) of each query
+    from the GPU index vs the C einsum restatement streamed over all rows in 1M-row chunks
+    (per-row scores are chunk-invariant), ranked by (score desc, row asc)."""
+    from oracle import flat_index as F
+
+    V = np.stack([emb.embed_array(t) for t in texts]).astype(np.float32)
+    res = kb.index.search_batch(V, k, validate=False, count=False)
+    rows, raw = res.rows.cpu().numpy(), res.raw.cpu().numpy()
+    n = len(kb.index)
+    cand_s, cand_r = [], []
+    for r0 in range(0, n, chunk):
+        m = min(chunk, n - r0)
+        Xc = kb.index.read_rows(r0, m).cpu().numpy()
+        o = F.c_search(Xc, V, k)
+        cand_s.append(o.raw)
+        cand_r.append(np.where(o.rows >= 0, o.rows + r0, -1))
+    S, R = np.concatenate(cand_s, axis=1), np.concatenate(cand_r, axis=1)
+    bad_rows = bad_scores = 0
+    for q in range(len(texts)):
+        ok = R[q] >= 0
+        order = np.lexsort((R[q][ok], -S[q][ok]))[:k]
+        wr, ws = R[q][ok][order], S[q][ok][order]
+        bad_rows += int(not np.array_equal(wr, rows[q, :wr.size]))
+        bad_scores += int(not np.array_equal(ws, raw[q, :ws.size]))
+    return {"queries": len(texts), "k": k, "row_mismatches": bad_rows, "raw_score_mismatches": bad_scores}
