@@ -115,6 +115,16 @@ int pr_index_search(pr_index *h, const float *d_q, int64_t nq, int k, uint32_t m
  * query j sees exactly the rows written back by queries i < j. */
 int pr_index_search_ex(pr_index *h, const float *d_q, int64_t nq, int k, uint32_t mode, const int64_t *d_row_limit,
                        int64_t *d_rows, double *d_raw, double *d_reported, int32_t *d_count, void *stream);
+/* The miss-list hand-off of the on-device cascade: search the queries a device-side
+ * compaction selected, without reading the list back.  Listed position i searches
+ * d_q[d_list[i]] (d_q is [*, dim] fp32) for i < *d_nlist (DEVICE int32); outputs are
+ * [nq_max, k] in list order, positions past the live count are left undefined.
+ * nq_hint (host) is the expected live count: the tensor-core grid is shaped for it (any
+ * count <= nq_max is correct).  d_row_limit, if given, is per listed position.  The int8
+ * and exact paths skip the dead positions; the fp16 path (small stores) scans nq_max. */
+int pr_index_search_list(pr_index *h, const float *d_q, const int32_t *d_list, const int32_t *d_nlist, int64_t nq_max,
+                         int64_t nq_hint, int k, uint32_t mode, const int64_t *d_row_limit, int64_t *d_rows,
+                         double *d_raw, double *d_reported, int32_t *d_count, void *stream);
 int pr_index_last_stats(pr_index *h, pr_search_stats *out);
 /* Record CUDA events around the dominant scan kernel of every search (the
  * tcgen05 scan, or the exact scan on the exact path); pr_index_scan_time
@@ -187,6 +197,28 @@ int pr_kv_remap(pr_kv *h, const int64_t *d_map, int64_t nmap, void *stream);
 /* device L2 fetch granularity limit (cudaLimitMaxL2FetchGranularity, bytes; <= 0 only reads
  * it): random 32-byte probes waste DRAM bandwidth when L2 fetches whole 128-byte lines */
 int pr_l2_fetch_granularity(int bytes, int *previous);
+
+/* ---- on-device cascade: router.py:227-273 (_probe), :275-364 (route) ----------
+ * The fast layers' outcome for a batch of B queries and the ONE compacted miss list the
+ * vector layers consume (pr_index_search_list), without a host round trip:
+ *   l1[j] = d_kv_hit[j] || d_rep[j]   (pre-batch KV probe, or an earlier in-window write)
+ *   l2[j] = d_sc_count[j] > 0 && d_sc_score[j] >= sc_threshold   (caches.py:140, inclusive)
+ * A query hit by a fast layer probed before the vector layers (l1_blocks / l2_blocks) is
+ * dropped; the rest, in query order, form d_list[0..*d_nlist) and d_slot[j] = position or -1.
+ * d_kv_hit NULL = L1 not probed; d_sc_count NULL = L2 not probed. */
+int pr_cascade_gate(int64_t B, const uint8_t *d_kv_hit, const uint8_t *d_rep, const int32_t *d_sc_count,
+                    const double *d_sc_score, double sc_threshold, int l1_blocks, int l2_blocks, uint8_t *d_l1,
+                    uint8_t *d_l2, int32_t *d_list, int32_t *d_nlist, int32_t *d_slot, void *stream);
+/* The adaptive-memory guard (knowledge.py:217-228: L5 seeds settle before the next query):
+ * the seeds (top seed_k knowledge-base rows) of the previous span's listed queries, then of
+ * this span's, deduplicated by KB row in first-occurrence order -> d_out_rows[0..*d_nout)
+ * (padded with row 0 up to out_max), and d_before[i] = deduplicated seeds visible to this
+ * span's listed query i.  d_mark is a KB-row-sized int32 scratch, initialised once with
+ * pr_cascade_mark_init and restored by every call.  Previous span arguments may be NULL. */
+int pr_cascade_mark_init(int32_t *d_mark, int64_t n, void *stream);
+int pr_cascade_seeds(const int64_t *d_prev_rows, const int32_t *d_prev_cnt, const int32_t *d_prev_n,
+                     const int64_t *d_rows, const int32_t *d_cnt, const int32_t *d_n, int seed_k, int32_t *d_mark,
+                     int64_t *d_out_rows, int64_t out_max, int32_t *d_nout, int64_t *d_before, void *stream);
 
 /* ---- device HashEmbedder: embedding.py:117-160 ------------
  * Texts are a UTF-8 arena + offsets as for pr_fingerprint; d_out is fp32

@@ -71,6 +71,12 @@ SIGNATURES = {
     "pr_index_append_from": (c_int, [c_vp, c_vp, c_vp, c_i64, c_vp]),
     "pr_index_search": (c_int, [c_vp, c_vp, c_i64, c_int, c_u32, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "pr_index_search_ex": (c_int, [c_vp, c_vp, c_i64, c_int, c_u32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "pr_index_search_list": (c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_int, c_u32, c_vp, c_vp, c_vp, c_vp,
+                                     c_vp, c_vp]),
+    "pr_cascade_gate": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_dbl, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                c_vp]),
+    "pr_cascade_mark_init": (c_int, [c_vp, c_i64, c_vp]),
+    "pr_cascade_seeds": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
     "pr_index_last_stats": (c_int, [c_vp, ctypes.POINTER(SearchStats)]),
     "pr_index_set_timing": (c_int, [c_vp, c_int]),
     "pr_index_scan_time": (c_int, [c_vp, ctypes.POINTER(c_dbl), ctypes.POINTER(c_i64)]),

@@ -1,0 +1,200 @@
+// On-device cascade of a routed batch (reference: router.py:227-273 _probe, :275-364 route).
+//
+// The router probes its layers in probe_order() and the first hit serves the query.  For a
+// batch, the vector layers (L4 adaptive memory, L5 retrieval) only need the queries that
+// neither fast layer answered, so the batch hands ONE compacted miss list from the fast
+// layers to the scans, on the device:
+//
+//   pr_cascade_gate    L1 (fixed-KV probe result, OR an earlier in-window write of the same
+//                      text) and L2 (semantic-cache top-1 >= threshold, caches.py:140) per
+//                      query; a query blocked by a fast layer probed before the vector
+//                      layers leaves the list; the survivors are compacted in query order
+//                      (block-wide prefix sum) into list / count / slot — no host round trip.
+//                      The knowledge-base scan then runs on the list (pr_index_search_list).
+//   pr_cascade_seeds   the AKM-hit guard: the superset of seeds (top seed_k KB rows) every
+//                      earlier listed query could settle into the AKM before a later query
+//                      probes it (knowledge.py:217-228), deduplicated by KB row in first-
+//                      occurrence order (a KB-sized mark array, atomicMin of positions), with
+//                      each listed query's visible prefix length (row limit of the guard scan).
+//
+// Both run as one CTA (1024 threads) over the batch: the batch is a few thousand queries
+// and tens of thousands of seed rows; the cost is a few microseconds, and one launch
+// avoids any grid-wide synchronisation.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace pr {
+
+constexpr int CG_THREADS = 1024;
+
+// exclusive block scan of one int per thread; returns the block total
+__device__ __forceinline__ int block_exclusive_scan(int v, int *warp_sums, int &total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sums[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        int w = lane < nwarp ? warp_sums[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        if (lane < nwarp) warp_sums[lane] = w;
+    }
+    __syncthreads();
+    const int base = warp > 0 ? warp_sums[warp - 1] : 0;
+    total = warp_sums[nwarp - 1];
+    __syncthreads();
+    return base + x - v;
+}
+
+struct GateArgs {
+    int64_t B;
+    const uint8_t *kv_hit;    // [B] pre-batch fixed-KV probe (nullable: L1 absent)
+    const uint8_t *rep;       // [B] text written earlier in the window (nullable)
+    const int32_t *sc_count;  // [B] semantic-cache top-1 count (nullable: L2 absent)
+    const double *sc_score;   // [B] reported top-1 score
+    double sc_threshold;
+    int l1_blocks, l2_blocks;  // the layer is probed before the vector layers
+    uint8_t *l1, *l2;          // [B] out
+    int32_t *list;             // [B] out: queries that reach the vector layers, in order
+    int32_t *nlist;            // [1] out
+    int32_t *slot;             // [B] out: position in list or -1
+};
+
+__global__ void __launch_bounds__(CG_THREADS) cascade_gate_kernel(GateArgs a) {
+    __shared__ int warp_sums[32];
+    int base = 0;
+    for (int64_t c0 = 0; c0 < a.B; c0 += blockDim.x) {
+        const int64_t j = c0 + threadIdx.x;
+        int keep = 0;
+        if (j < a.B) {
+            const bool h1 = a.kv_hit && (a.kv_hit[j] || (a.rep && a.rep[j]));
+            const bool h2 = a.sc_count && a.sc_count[j] > 0 && a.sc_score[j] >= a.sc_threshold;
+            a.l1[j] = h1;
+            a.l2[j] = h2;
+            keep = !((h1 && a.l1_blocks) || (h2 && a.l2_blocks));
+        }
+        int total;
+        const int pos = block_exclusive_scan(keep, warp_sums, total);
+        if (j < a.B) {
+            a.slot[j] = keep ? base + pos : -1;
+            if (keep) a.list[base + pos] = (int32_t)j;
+        }
+        base += total;
+    }
+    if (threadIdx.x == 0) *a.nlist = base;
+}
+
+struct SeedArgs {
+    // previous span (its listed queries' seeds were not settled when this span was launched)
+    const int64_t *prev_rows;  // [prev_max, sk] (nullable)
+    const int32_t *prev_cnt;   // [prev_max]
+    const int32_t *prev_n;     // [1] live listed queries
+    // this span
+    const int64_t *rows;  // [nq_max, sk]
+    const int32_t *cnt;   // [nq_max]
+    const int32_t *n;     // [1]
+    int sk;
+    int32_t *mark;       // [KB rows] INT_MAX between calls (restored on exit)
+    int64_t *out_rows;   // [(prev_max + nq_max) * sk] deduplicated seed rows, junk (row 0) past *nout
+    int64_t out_max;
+    int32_t *nout;       // [1]
+    int64_t *before;     // [nq_max] deduplicated seeds visible to listed query i
+};
+
+// sequence position p -> (row) over prev then cur, each listed query contributing cnt rows
+__device__ __forceinline__ int64_t seq_row(const SeedArgs &a, int np, int64_t p) {
+    const int64_t pp = (int64_t)np * a.sk;
+    if (p < pp) return a.prev_rows[p];
+    return a.rows[p - pp];
+}
+__device__ __forceinline__ bool seq_valid(const SeedArgs &a, int np, int64_t p) {
+    const int64_t pp = (int64_t)np * a.sk;
+    if (p < pp) return (p % a.sk) < a.prev_cnt[p / a.sk];
+    const int64_t q = p - pp;
+    return (q % a.sk) < a.cnt[q / a.sk];
+}
+
+__global__ void __launch_bounds__(CG_THREADS) cascade_seeds_kernel(SeedArgs a) {
+    __shared__ int warp_sums[32];
+    const int np = a.prev_rows ? max(0, *a.prev_n) : 0;
+    const int nc = max(0, *a.n);
+    const int64_t total = (int64_t)(np + nc) * a.sk;
+    // 1) first occurrence of every KB row in sequence order
+    for (int64_t p = threadIdx.x; p < total; p += blockDim.x)
+        if (seq_valid(a, np, p)) atomicMin(&a.mark[seq_row(a, np, p)], (int32_t)p);
+    __syncthreads();
+    // 2) compact first occurrences; before[i] = firsts strictly before listed query i's seeds
+    int base = 0;
+    const int64_t cur0 = (int64_t)np * a.sk;
+    for (int64_t c0 = 0; c0 < total; c0 += blockDim.x) {
+        const int64_t p = c0 + threadIdx.x;
+        int first = 0;
+        int64_t r = 0;
+        if (p < total && seq_valid(a, np, p)) {
+            r = seq_row(a, np, p);
+            first = a.mark[r] == (int32_t)p;
+        }
+        int tot;
+        const int pos = block_exclusive_scan(first, warp_sums, tot);
+        if (first) a.out_rows[base + pos] = r;
+        if (p < total && p >= cur0 && (p - cur0) % a.sk == 0) a.before[(p - cur0) / a.sk] = base + pos;
+        base += tot;
+    }
+    __syncthreads();
+    // 3) restore the marks; pad the row list with a valid junk row (never visible)
+    for (int64_t p = threadIdx.x; p < total; p += blockDim.x)
+        if (seq_valid(a, np, p)) a.mark[seq_row(a, np, p)] = INT32_MAX;
+    for (int64_t p = base + threadIdx.x; p < a.out_max; p += blockDim.x) a.out_rows[p] = 0;
+    if (threadIdx.x == 0) *a.nout = base;
+}
+
+}  // namespace pr
+
+using namespace pr;
+
+extern "C" {
+
+int pr_cascade_gate(int64_t B, const uint8_t *d_kv_hit, const uint8_t *d_rep, const int32_t *d_sc_count,
+                    const double *d_sc_score, double sc_threshold, int l1_blocks, int l2_blocks, uint8_t *d_l1,
+                    uint8_t *d_l2, int32_t *d_list, int32_t *d_nlist, int32_t *d_slot, void *stream) {
+    if (B < 0 || !d_l1 || !d_l2 || !d_list || !d_nlist || !d_slot || (d_sc_count && !d_sc_score))
+        PR_FAIL(PR_ERR_BAD_ARG, "bad cascade_gate");
+    GateArgs a{B, d_kv_hit, d_rep, d_sc_count, d_sc_score, sc_threshold, l1_blocks, l2_blocks, d_l1, d_l2,
+               d_list, d_nlist, d_slot};
+    ::pr::count_launch();
+    cascade_gate_kernel<<<1, CG_THREADS, 0, as_stream(stream)>>>(a);
+    PR_LAUNCH_CHECK();
+    return PR_OK;
+}
+
+int pr_cascade_mark_init(int32_t *d_mark, int64_t n, void *stream) {
+    if (n < 0 || (n > 0 && !d_mark)) PR_FAIL(PR_ERR_BAD_ARG, "bad mark_init");
+    if (n == 0) return PR_OK;
+    PR_CUDA(cudaMemsetAsync(d_mark, 0x7f, (size_t)n * sizeof(int32_t), as_stream(stream)));  // >= INT32_MAX - 0x808080
+    return PR_OK;
+}
+
+int pr_cascade_seeds(const int64_t *d_prev_rows, const int32_t *d_prev_cnt, const int32_t *d_prev_n,
+                     const int64_t *d_rows, const int32_t *d_cnt, const int32_t *d_n, int seed_k, int32_t *d_mark,
+                     int64_t *d_out_rows, int64_t out_max, int32_t *d_nout, int64_t *d_before, void *stream) {
+    if (seed_k < 1 || !d_rows || !d_cnt || !d_n || !d_mark || !d_out_rows || !d_nout || !d_before ||
+        (d_prev_rows && (!d_prev_cnt || !d_prev_n)))
+        PR_FAIL(PR_ERR_BAD_ARG, "bad cascade_seeds");
+    SeedArgs a{d_prev_rows, d_prev_cnt, d_prev_n, d_rows, d_cnt, d_n, seed_k, d_mark, d_out_rows, out_max, d_nout,
+               d_before};
+    ::pr::count_launch();
+    cascade_seeds_kernel<<<1, CG_THREADS, 0, as_stream(stream)>>>(a);
+    PR_LAUNCH_CHECK();
+    return PR_OK;
+}
+
+}  // extern "C"

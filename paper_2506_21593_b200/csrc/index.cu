@@ -125,6 +125,21 @@ __global__ void pad_queries_kernel(const float *__restrict__ q, int64_t nq, int 
     }
 }
 
+// listed queries: row i of the output = q[list[i]] for i < *nlist; rows past the live
+// count repeat the first listed query (valid input for every scan path; never reported)
+__global__ void gather_pad_queries_kernel(const float *__restrict__ q, const int32_t *__restrict__ list,
+                                          const int32_t *__restrict__ nlist, int64_t nq_max, int d, int dp8,
+                                          float *__restrict__ out) {
+    const int64_t total = nq_max * (int64_t)dp8;
+    const int32_t live = *nlist;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t / dp8;
+        const int c = (int)(t % dp8);
+        const int64_t src = live > 0 ? list[i < live ? i : 0] : -1;
+        out[t] = (src >= 0 && c < d) ? q[src * d + c] : 0.f;
+    }
+}
+
 static int grid_for(int64_t total, int block = 256) {
     int64_t g = (total + block - 1) / block;
     int64_t cap = (int64_t)sm_count() * 16;
@@ -877,16 +892,24 @@ int pr_index_search(pr_index *h, const float *d_q, int64_t nq, int k, uint32_t m
     return pr_index_search_ex(h, d_q, nq, k, mode, nullptr, d_rows, d_raw, d_reported, d_count, stream);
 }
 
-static int search_impl(pr_index *h, const float *d_q, int64_t nq, int k, uint32_t mode, const int64_t *d_row_limit,
-                       int64_t *d_rows, double *d_raw, double *d_reported, int32_t *d_count, void *stream);
+struct QueryList {
+    const int32_t *list = nullptr;   // device: query index per listed position
+    const int32_t *nlist = nullptr;  // device: live count
+    int64_t hint = 0;                // host estimate of the live count (grid shape)
+};
 
-int pr_index_search_ex(pr_index *h, const float *d_q, int64_t nq, int k, uint32_t mode, const int64_t *d_row_limit,
-                       int64_t *d_rows, double *d_raw, double *d_reported, int32_t *d_count, void *stream) {
+static int search_impl(pr_index *h, const float *d_q, int64_t nq, int k, uint32_t mode, const int64_t *d_row_limit,
+                       int64_t *d_rows, double *d_raw, double *d_reported, int32_t *d_count, void *stream,
+                       const QueryList &ql);
+
+static int search_entry(pr_index *h, const float *d_q, int64_t nq, int k, uint32_t mode, const int64_t *d_row_limit,
+                        int64_t *d_rows, double *d_raw, double *d_reported, int32_t *d_count, void *stream,
+                        const QueryList &ql) {
     if (!h) PR_FAIL(PR_ERR_BAD_ARG, "null handle");
     cudaStream_t st = as_stream(stream);
     if (!h->scratch_ev) PR_CUDA(cudaEventCreateWithFlags(&h->scratch_ev, cudaEventDisableTiming));
     if (h->scratch_ev_used && h->last_stream != st) PR_CUDA(cudaStreamWaitEvent(st, h->scratch_ev, 0));
-    const int rc = search_impl(h, d_q, nq, k, mode, d_row_limit, d_rows, d_raw, d_reported, d_count, stream);
+    const int rc = search_impl(h, d_q, nq, k, mode, d_row_limit, d_rows, d_raw, d_reported, d_count, stream, ql);
     if (rc == PR_OK) {
         PR_CUDA(cudaEventRecord(h->scratch_ev, st));
         h->scratch_ev_used = true;
@@ -894,8 +917,22 @@ int pr_index_search_ex(pr_index *h, const float *d_q, int64_t nq, int k, uint32_
     return rc;
 }
 
-static int search_impl(pr_index *h, const float *d_q, int64_t nq, int k, uint32_t mode, const int64_t *d_row_limit,
+int pr_index_search_list(pr_index *h, const float *d_q, const int32_t *d_list, const int32_t *d_nlist, int64_t nq_max,
+                         int64_t nq_hint, int k, uint32_t mode, const int64_t *d_row_limit, int64_t *d_rows,
+                         double *d_raw, double *d_reported, int32_t *d_count, void *stream) {
+    if (!d_list || !d_nlist) PR_FAIL(PR_ERR_BAD_ARG, "search_list needs a device list and count");
+    QueryList ql{d_list, d_nlist, nq_hint > 0 ? nq_hint : nq_max};
+    return search_entry(h, d_q, nq_max, k, mode, d_row_limit, d_rows, d_raw, d_reported, d_count, stream, ql);
+}
+
+int pr_index_search_ex(pr_index *h, const float *d_q, int64_t nq, int k, uint32_t mode, const int64_t *d_row_limit,
                        int64_t *d_rows, double *d_raw, double *d_reported, int32_t *d_count, void *stream) {
+    return search_entry(h, d_q, nq, k, mode, d_row_limit, d_rows, d_raw, d_reported, d_count, stream, QueryList{});
+}
+
+static int search_impl(pr_index *h, const float *d_q, int64_t nq, int k, uint32_t mode, const int64_t *d_row_limit,
+                       int64_t *d_rows, double *d_raw, double *d_reported, int32_t *d_count, void *stream,
+                       const QueryList &ql) {
     if (!h) PR_FAIL(PR_ERR_BAD_ARG, "null handle");
     if (k < 1) PR_FAIL(PR_ERR_BAD_ARG, "k must be >= 1");  // index.py:161-162
     if (nq < 0 || nq > INT32_MAX / 2) PR_FAIL(PR_ERR_BAD_ARG, "bad query count");
@@ -905,6 +942,7 @@ static int search_impl(pr_index *h, const float *d_q, int64_t nq, int k, uint32_
     h->stats = pr_search_stats{};
     h->stats.queries = nq;
     if (nq == 0) return PR_OK;
+    if (ql.list && k > KMAX_EXACT) PR_FAIL(PR_ERR_BAD_ARG, "listed search supports k <= %d", KMAX_EXACT);
     if (h->count == 0 || k > KMAX_EXACT) {
         if (h->count == 0) {
             ::pr::count_launch();
@@ -924,7 +962,7 @@ static int search_impl(pr_index *h, const float *d_q, int64_t nq, int k, uint32_
     // The int8 scan's per-(query, split) bounds start cold, so it needs long row splits to
     // amortise the start: below ~512k rows the fp16 scan is faster (40k x 1024, 2048
     // queries, k=10: 0.42 ms fp16 vs 3.5 ms int8; 10M rows: int8 1.6x faster).
-    const bool tc_pays = mode == PR_SEARCH_AUTO && tensor_ok && pr::tc_worthwhile(h->count, nq);
+    const bool tc_pays = mode == PR_SEARCH_AUTO && tensor_ok && pr::tc_worthwhile(h->count, ql.list ? ql.hint : nq);
     const bool i8_pays = tc_pays && h->count >= ((int64_t)1 << 19);
     const bool use_i8 = (mode == PR_SEARCH_TENSOR_I8 || i8_pays) && tensor_ok && pr::tc8_eligible(h->dim);
     bool use_tc = !use_i8 && tensor_ok && (mode == PR_SEARCH_TENSOR || mode == PR_SEARCH_TENSOR_I8 || tc_pays);
@@ -937,7 +975,11 @@ static int search_impl(pr_index *h, const float *d_q, int64_t nq, int k, uint32_
     Carve cv{reinterpret_cast<char *>(h->scratch)};
     float *Qp = cv.take<float>((size_t)nq * h->dp8);
     ::pr::count_launch();
-    pad_queries_kernel<<<grid_for(nq * h->dp8), 256, 0, st>>>(d_q, nq, h->dim, h->dp8, Qp);
+    if (ql.list)
+        gather_pad_queries_kernel<<<std::min(grid_for(nq * h->dp8), sm_count() * 16), 256, 0, st>>>(
+            d_q, ql.list, ql.nlist, nq, h->dim, h->dp8, Qp);
+    else
+        pad_queries_kernel<<<grid_for(nq * h->dp8), 256, 0, st>>>(d_q, nq, h->dim, h->dp8, Qp);
     PR_LAUNCH_CHECK();
 
     if (use_i8) {
@@ -967,6 +1009,8 @@ static int search_impl(pr_index *h, const float *d_q, int64_t nq, int k, uint32_
         ts.count = d_count;
         ts.counters = h->d_counters;
         ts.row_limit = d_row_limit;
+        ts.nq_dev = ql.nlist;
+        ts.nq_hint = ql.hint;
         rc = timing_pair(h, &ts.ev_begin, &ts.ev_end);
         if (rc) return rc;
         rc = pr::tc8_search(ts, cv, st, &h->stats);
@@ -977,7 +1021,7 @@ static int search_impl(pr_index *h, const float *d_q, int64_t nq, int k, uint32_
     }
     if (!use_tc) {
         h->stats.path = PR_SEARCH_EXACT;
-        return exact_search(h, Qp, nullptr, nullptr, (int)nq, k, d_rows, d_raw, d_reported, d_count, cv, st, true,
+        return exact_search(h, Qp, nullptr, ql.nlist, (int)nq, k, d_rows, d_raw, d_reported, d_count, cv, st, true,
                             d_row_limit);
     }
     h->stats.path = PR_SEARCH_TENSOR;

@@ -71,6 +71,10 @@ struct Tc8Search {
     int32_t *fallback_list;  // out: queries whose candidate buffer overflowed
     cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
     const int64_t *row_limit = nullptr;
+    // device-resident query count (a compacted miss list): queries [*nq_dev, nq) are
+    // skipped by every kernel; the grid is shaped for nq_hint queries (host estimate)
+    const int32_t *nq_dev = nullptr;
+    int64_t nq_hint = 0;
 };
 int i8_quantize_rows(const float *src, int64_t n, int d, const int64_t *rows, int64_t row0, int dp128, I8Rows &m,
                      cudaStream_t st);

@@ -197,7 +197,13 @@ struct I8ScanParams {
     // so each tile is still in L2 when the others read it (0 = off)
     int32_t *prog;  // [nsplit][qgroups]: tiles loaded + 1 (0 = not started, INT_MAX = done)
     int window;
+    const int32_t *nq_dev;  // device query count (nullable): queries >= *nq_dev are skipped
 };
+
+// the live query count of a search: the device count of a compacted list, else nq
+__device__ __forceinline__ int64_t live_nq(const int32_t *nq_dev, int64_t nq) {
+    return nq_dev ? min(nq, (int64_t)max(0, __ldg(nq_dev))) : nq;
+}
 
 // loose per-tile test in the scaled domain: a row can pass u = t s acc + A dx + C >= thr
 // only if s * acc >= (thr - C - A dxmax) / t.  1e-6 (score units) absorbs every fp32
@@ -284,7 +290,10 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
     }
     // CG == 2: the CTA pair (one cluster) shares items; rank r scans query tile 2*qp + r
     const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
-    const int qgroups = p.qtiles / CG;
+    // with a device query count only the query groups that hold live queries get items
+    // (the grid is shaped for the host's estimate; CTAs past the live items exit)
+    const int64_t nq_live = live_nq(p.nq_dev, p.nq);
+    const int qgroups = p.nq_dev ? (int)ceil_div<int64_t>(nq_live, (int64_t)CG * TC_BLOCK_M) : p.qtiles / CG;
     const int nitems = qgroups * p.nsplit;
     const int item0 = blockIdx.x / CG, istride = gridDim.x / CG;
     auto item_of = [&](int item, int &qtile, int &split, int &t0, int &nloc) {
@@ -466,7 +475,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
             int qtile, split, t0, nloc;
             item_of(item, qtile, split, t0, nloc);
             const int64_t q = (int64_t)qtile * TC_BLOCK_M + et;
-            const bool valid = q < p.nq;
+            const bool valid = q < nq_live;
             float tq_ = 0.f, A = 0.f, C = 0.f;
             int64_t lim = 0;
             if (valid) {
@@ -837,10 +846,11 @@ __global__ void gather_i8_kernel(const int8_t *__restrict__ sx8, const float *__
 // queries: padded fp32 [nq, dp8] -> int8 [nq_pad, dp128] + {t, A, C}
 __global__ void quantize_queries_kernel(const float *__restrict__ qp, int64_t nq, int64_t nq_pad, int dp8, int d,
                                         int dp128, const uint32_t *__restrict__ maxnorm, int8_t *__restrict__ q8,
-                                        float4 *__restrict__ qmeta) {
+                                        float4 *__restrict__ qmeta, const int32_t *__restrict__ nq_dev) {
     const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32;
     const int lane = threadIdx.x & 31;
     if (w >= nq_pad) return;
+    nq = live_nq(nq_dev, nq);
     if (w >= nq) {
         for (int j = lane; j < dp128; j += 32) q8[w * dp128 + j] = 0;
         if (lane == 0) qmeta[w] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -923,6 +933,7 @@ struct I8SeedArgs {
     double *seed_s;      // [nq][TC_KP]
     int32_t *seed_n;     // [nq]
     uint32_t *lg;        // [nq] <- max(lg, rounded-down exact k-th seed score)
+    const int32_t *nq_dev;
 };
 
 // per query (one warp): the k pilot rows with the largest l, scored exactly
@@ -937,7 +948,8 @@ __global__ void __launch_bounds__(W8_WARPS * 32) tc8_seed_kernel(I8SeedArgs a) {
     const int64_t nw = (int64_t)gridDim.x * W8_WARPS;
     const int M = a.nsplit * I8_HALVES * TC_KP;
     float *qs = qdyn + w * (a.dp8 + 8);
-    for (int64_t q = wid; q < a.nq; q += nw) {
+    const int64_t nq_live = live_nq(a.nq_dev, a.nq);
+    for (int64_t q = wid; q < nq_live; q += nw) {
         const uint64_t *cq = a.pcand + q * (int64_t)M;
         uint64_t last = ~0ull;
         int n = 0;
@@ -994,6 +1006,7 @@ struct I8PostArgs {
     int32_t *count;
     int32_t *counters;  // [0] fallback, [1] rescored rows, [3] appended rows
     int32_t *fallback;
+    const int32_t *nq_dev;
 };
 
 __global__ void __launch_bounds__(W8_WARPS * 32) tc8_post_kernel(I8PostArgs a) {
@@ -1008,7 +1021,8 @@ __global__ void __launch_bounds__(W8_WARPS * 32) tc8_post_kernel(I8PostArgs a) {
     double *ts = top_s[w];
     int32_t *tr = top_r[w];
     float *qs = qdyn + w * (a.dp8 + 8);
-    for (int64_t q = wid; q < a.nq; q += nw) {
+    const int64_t nq_live = live_nq(a.nq_dev, a.nq);
+    for (int64_t q = wid; q < nq_live; q += nw) {
         const int take = (int)(a.row_limit ? min(a.take, max((int64_t)0, a.row_limit[q])) : a.take);
         const int cnt = a.acount[q];
         if (lane == 0) atomicAdd(&a.counters[3], cnt);
@@ -1255,7 +1269,11 @@ int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats)
     const int64_t nq_pad = round_up<int64_t>(s.nq, cg * TC_BLOCK_M);
     const int64_t qtiles = nq_pad / TC_BLOCK_M;
     const int64_t ntiles = ceil_div<int64_t>(s.n, TC_BLOCK_N);
-    int nsplit = choose_nsplit_waves(qtiles, ntiles);
+    // a device-sized query list: shape the grid for the host's estimate of the live count
+    const int64_t qtiles_hint =
+        s.nq_dev ? round_up<int64_t>(ceil_div<int64_t>(std::max<int64_t>(1, std::min(s.nq_hint, s.nq)), TC_BLOCK_M), cg)
+                 : qtiles;
+    int nsplit = choose_nsplit_waves(qtiles_hint, ntiles);
     const char *ns_env = getenv("PR_I8_NSPLIT");  // measurement knob
     if (ns_env && atoi(ns_env) > 0) nsplit = (int)std::min<int64_t>(ntiles, atoi(ns_env));
     const int tps = (int)ceil_div<int64_t>(ntiles, nsplit);
@@ -1274,7 +1292,7 @@ int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats)
         const int64_t threads = nq_pad * 32;
         ::pr::count_launch();
         quantize_queries_kernel<<<(unsigned)ceil_div<int64_t>(threads, 256), 256, 0, st>>>(
-            s.qp, s.nq, nq_pad, s.dp8, s.d, s.dp128, s.rows8.maxnorm, q8, qmeta);
+            s.qp, s.nq, nq_pad, s.dp8, s.d, s.dp128, s.rows8.maxnorm, q8, qmeta, s.nq_dev);
         PR_LAUNCH_CHECK();
     }
     TcStoreMap qmap;
@@ -1294,7 +1312,7 @@ int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats)
         1, std::min<int64_t>(ceil_div<int64_t>(s.nq, W8_WARPS), (int64_t)sm_count() * 8));
 
     // 1) pilot over a tile subsample -> exact seeds and a first bound per query
-    const int psplit = pilot_splits(qtiles, ntiles);
+    const int psplit = pilot_splits(qtiles_hint, ntiles);
     int32_t *seed_rows = nullptr, *seed_n = nullptr;
     double *seed_s = nullptr;
     if (psplit > 0) {
@@ -1305,10 +1323,11 @@ int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats)
         seed_n = cv.take<int32_t>((size_t)s.nq);
         I8ScanParams pp{s.n, s.dp128 / I8_BLOCK_K, psplit, (int)ceil_div<int64_t>(ptiles, psplit), (int)ptiles,
                         (int)qtiles, s.k, s.rows8.xs, s.rows8.xe, s.rows8.xt, qmeta, s.row_limit, s.nq, lg, acount,
-                        abuf, cap, floor_thr, 0, I8_PILOT_STRIDE, pcand, s.x32, s.qp, s.dp8, s.d, 0, nullptr, 0};
-        rc = launch_scan8_cg<true>(cg, i8_ares(cg, s.dp128), qtiles * psplit, qmap.map, xmap, pp, st);
+                        abuf, cap, floor_thr, 0, I8_PILOT_STRIDE, pcand, s.x32, s.qp, s.dp8, s.d, 0, nullptr, 0, s.nq_dev};
+        rc = launch_scan8_cg<true>(cg, i8_ares(cg, s.dp128), (s.nq_dev ? qtiles_hint : qtiles) * psplit, qmap.map, xmap,
+                                   pp, st);
         if (rc) return rc;
-        I8SeedArgs sa{pcand, psplit, s.nq, s.k, s.x32, s.dp8, s.d, s.qp, seed_rows, seed_s, seed_n, lg};
+        I8SeedArgs sa{pcand, psplit, s.nq, s.k, s.x32, s.dp8, s.d, s.qp, seed_rows, seed_s, seed_n, lg, s.nq_dev};
         ::pr::count_launch();
         tc8_seed_kernel<<<wgrid, W8_WARPS * 32, wsmem, st>>>(sa);
         PR_LAUNCH_CHECK();
@@ -1316,11 +1335,11 @@ int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats)
     // 2) main scan: append every row whose upper bound reaches the running bound
     I8ScanParams p{s.n, s.dp128 / I8_BLOCK_K, nsplit, tps, (int)ntiles, (int)qtiles, s.k, s.rows8.xs, s.rows8.xe,
                    s.rows8.xt, qmeta, s.row_limit, s.nq, lg, acount, abuf, cap, floor_thr, 0, 1, nullptr, s.x32, s.qp,
-                   s.dp8, s.d, 1, nullptr, 0};
+                   s.dp8, s.d, 1, nullptr, 0, s.nq_dev};
     {
         const char *w_env = getenv("PR_I8_WINDOW");  // tiles a pair may run ahead of its split (0 = off)
         p.window = w_env ? atoi(w_env) : 0;  // measured: 48 tiles halves DRAM reads but costs 50 % time
-        if (cg == 2 && p.window > 0) {
+        if (cg == 2 && p.window > 0 && !s.nq_dev) {
             p.prog = cv.take<int32_t>((size_t)nsplit * (qtiles / 2));
             PR_CUDA(cudaMemsetAsync(p.prog, 0, (size_t)nsplit * (qtiles / 2) * sizeof(int32_t), st));
         } else {
@@ -1332,12 +1351,13 @@ int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats)
     const char *noepi_env = getenv("PR_I8_NOEPI");  // 1: epilogue does nothing (results invalid): MMA/TMA timing
     if (noepi_env && noepi_env[0] >= '1') p.noepi = noepi_env[0] - '0';  // 2: also skip operand loads
     if (s.ev_begin) PR_CUDA(cudaEventRecord(s.ev_begin, st));
-    rc = launch_scan8_cg<false>(cg, i8_ares(cg, s.dp128), qtiles * nsplit, qmap.map, xmap, p, st);
+    rc = launch_scan8_cg<false>(cg, i8_ares(cg, s.dp128), (s.nq_dev ? qtiles_hint : qtiles) * nsplit, qmap.map, xmap,
+                                p, st);
     if (rc) return rc;
     if (s.ev_end) PR_CUDA(cudaEventRecord(s.ev_end, st));
     // 3) exact rescoring of the complete candidate set
     I8PostArgs pa{acount, abuf, cap, s.nq, s.k, std::min<int64_t>(s.k, s.n), s.row_limit, s.x32, s.dp8, s.d, s.qp,
-                  seed_rows, seed_s, seed_n, s.rows, s.raw, s.rep, s.count, s.counters, s.fallback_list};
+                  seed_rows, seed_s, seed_n, s.rows, s.raw, s.rep, s.count, s.counters, s.fallback_list, s.nq_dev};
     ::pr::count_launch();
     tc8_post_kernel<<<wgrid, W8_WARPS * 32, wsmem, st>>>(pa);
     PR_LAUNCH_CHECK();
