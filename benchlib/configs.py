@@ -392,8 +392,7 @@ def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_se
     _, warm = session_stream(questions, queries_per_session, seed + 1000, 0)
     wq = [validate_query(t, "warmup", query_id=f"w{i}", issued_at_ns=0) for i, (t, _) in enumerate(warm)]
     for router in routers:
-        for i in range(0, len(wq), batch):
-            router.route_batch(wq[i:i + batch], materialize=False)
+        router.route_batch(wq, materialize=False, span=batch)
         router.reset_session()
         router.trace.clear()
         router.profile_batches = profile
@@ -431,18 +430,22 @@ def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_se
             router.reset_session()
             router.latency_model.reseed([seed, s, 1])
             qs = session_queries[s]
-            for i in range(0, len(qs), batch):
-                # columnar result: per-query objects are only built if someone reads them
-                # query texts in, embedded on the device inside route_batch (pr_hash_embed)
-                t_b = time.perf_counter()
-                res = router.route_batch(qs[i:i + batch], materialize=False)
-                _LAST_BATCH_WALL.append((w, s, i // batch, (time.perf_counter() - t_b) * 1e3,
-                                         router.last_batch_stats["splits"]))
-                tally["total"] += len(res)
-                tally["sequential"] += router.last_batch_stats["sequential"]
-                for code, c in zip(*np.unique(res.layers(), return_counts=True)):
-                    name = LayerTag(int(code)).wire_name
-                    tally["layers"][name] = tally["layers"].get(name, 0) + int(c)
+            # ONE route_batch call per session: spans of `batch` queries, span i+1's device
+            # stage queued before span i's host stage (cascade.py); columnar result (per-query
+            # objects are only built if someone reads them); query texts in, embedded on the
+            # device inside the call (pr_hash_embed)
+            t_b = time.perf_counter()
+            res = router.route_batch(qs, materialize=False, span=batch)
+            st = router.last_batch_stats
+            _LAST_BATCH_WALL.append((w, s, st["spans"], (time.perf_counter() - t_b) * 1e3 / max(1, st["spans"]),
+                                     st["splits"]))
+            tally["total"] += len(res)
+            tally["sequential"] += st["sequential"]
+            tally["spans"] = tally.get("spans", 0) + st["spans"]
+            tally["pipelined"] = tally.get("pipelined", 0) + st["pipelined"]
+            for code, c in zip(*np.unique(res.layers(), return_counts=True)):
+                name = LayerTag(int(code)).wire_name
+                tally["layers"][name] = tally["layers"].get(name, 0) + int(c)
 
     _LAST_BATCH_WALL.clear()
     gc_ms = [0.0, 0.0]  # total, longest collection inside the timed region
@@ -493,7 +496,7 @@ def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_se
     mine = make_router()
     mine.reset_session()
     mine.latency_model.reseed([seed, 0, 1])
-    got = mine.route_batch(qs)
+    got = mine.route_batch(qs, span=256)  # several pipelined spans over the full-size KB
     mism, oracle_name = 0, "twin router, sequential route() per query (reference semantics)"
     try:
         from oracle.ref_c1 import load_reference
@@ -534,7 +537,8 @@ def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_se
                     f"{workers} concurrent session worker(s)",
         "value": total / (ms / 1e3), "unit": "routed queries/s", "ms_total": ms, "workers": workers,
         "layer_counts": layer_counts, "queries_routed_sequentially": seq_total,
-        "batch_wall_ms": {"n": int(walls.size), "median": float(np.median(walls)), "p90": float(np.percentile(walls, 90)),
+        "spans": sum(t.get("spans", 0) for t in tallies), "spans_pipelined": sum(t.get("pipelined", 0) for t in tallies),
+        "span_wall_ms_mean_per_session": {"n": int(walls.size), "median": float(np.median(walls)), "p90": float(np.percentile(walls, 90)),
                           "max": float(walls.max()), "sum": float(walls.sum())},
         "gc_ms_in_timed_region": {"total": gc_ms[0], "longest": gc_ms[1]},
         "stage_seconds": getattr(router, "batch_profile", None),

@@ -169,10 +169,8 @@ def simulate_batched(router, questions, *, n_sessions: int, n_queries: int, seed
         router.latency_model.reseed([seed, s, 1])
         sid, stream = session_stream(questions, n_queries, seed, s)
         qs = [validate_query(t, sid, query_id=f"{sid}-q{i:05d}", issued_at_ns=0) for i, (t, _) in enumerate(stream)]
-        res = []
-        for i in range(0, len(qs), batch):
-            V = vectors_for(qs[i:i + batch]) if vectors_for else None
-            res.extend(router.route_batch(qs[i:i + batch], vectors=V))
+        V = vectors_for(qs) if vectors_for else None
+        res = router.route_batch(qs, vectors=V, span=batch)  # one call: spans pipelined (cascade.py)
         clock, lines = 0, []
         for (ans, ev), (_, origin) in zip(res, stream):
             ev = dataclasses.replace(ev, timestamp_ns=clock)

@@ -78,6 +78,7 @@ class FixedKVCache:
         self._max_entries = max_entries
         self._arena: list = []
         self._compact_at = self._COMPACT_MIN
+        self._compact_hold = 0  # > 0 while a routed batch holds probe results (arena indices)
         self._recency: OrderedDict[str, None] = OrderedDict()
         self._lock = threading.Lock()
         self.hits = 0
@@ -161,7 +162,7 @@ class FixedKVCache:
         write order; the device values are remapped in one kernel."""
         import torch
 
-        if len(self._arena) < self._compact_at:
+        if len(self._arena) < self._compact_at or self._compact_hold:
             return
         live = self._live_seqs()
         if 2 * live.size <= len(self._arena):

@@ -1,38 +1,47 @@
-"""Batched, sequential-equivalent routing.
+"""Batched, sequential-equivalent routing with the cascade on the device.
 
-``route_batch(router, queries)`` returns exactly what
-``[router.route(q) for q in queries]`` returns — answers, trace events,
-store contents and every counter — while doing the per-layer work as a few
-batched device calls:
+``route_batch(router, queries)`` returns exactly what ``[router.route(q) for q in queries]``
+returns — answers, trace events, store contents and every counter.  The queries are cut
+into spans (``span`` queries, 4096 by default) and every span runs in two stages:
 
-* L1 (fixed KV): one fused fingerprint+probe kernel over the batch's UTF-8
-  arena; a query also hits if an EARLIER query in the batch had the same text,
-  because every served answer is written back before the next query
-  (router.py:333-337) — a causal first-occurrence dedupe.
-* L2 (semantic cache): the first occurrence of every new text is appended to
-  the cache store up front (that is what write-back will do), and ONE
-  row-limited top-1 search (pr_index_search_ex) lets query j see exactly the
-  pre-batch rows plus the rows written by queries i < j.  Ties keep the
-  earlier row, as sequential upserts would.
-* L4 (adaptive memory) depends on which earlier queries were served by L5
-  (their seeds are settled before the next query, router.py:284-285), a
-  routing OUTCOME.  The batch proves L4 misses instead: top-1 over the
-  pre-batch AKM and over a superset of every seed any earlier query of the
-  batch could contribute (row-limited search over a scratch store gathered
-  device-to-device from knowledge-base rows).  If that bound reaches the AKM
-  threshold for some query, the batch stops before it and that query is
-  routed by ``router.route`` exactly; batching resumes after it.
-* L5: one top-seed_k search for every query that can reach it.
+DEVICE stage (``_launch``, enqueued on the router's CUDA stream, no host read-back):
 
-All scores are the exact fp64 reference scores (bit-identical), so every
-threshold decision is the reference's.  The decision pass over the batch is
-O(B) host work; latencies come from the router's synthetic latency model in
-query order (or the batch wall time split evenly when there is none).
+* L1 (fixed KV, router.py:232): one fused hash + probe kernel over the span's UTF-8 arena;
+  a query also hits if an EARLIER query of the span or of the previous span had the same
+  text (every served answer is written back before the next query, router.py:333-337) —
+  the window's first-occurrence map is host-side (texts only), uploaded as a mask.
+* L2 (semantic cache, caches.py:131-145): the first occurrence of every text new to the
+  cache is appended up front (that is what write-back will do), and ONE row-limited top-1
+  search lets query j see exactly the rows written by queries before it.
+* Gate (``pr_cascade_gate``): L1 / L2 outcomes in probe order, and the ONE compacted miss
+  list — the queries no fast layer answered — built on the device by a prefix sum.
+* L5 (knowledge base, knowledge.py:65-85): one top-seed_k scan of the listed queries only
+  (``pr_index_search_list``: the list and its count never leave the device).
+* L4 guard: L4 depends on which earlier queries were served by L5 (their seeds settle into
+  the AKM before the next query, router.py:284-285), a routing OUTCOME.  The span proves L4
+  misses instead: top-1 over the AKM and over a superset of every seed an earlier query
+  could contribute (``pr_cascade_seeds``: seeds of the previous span's and this span's
+  listed queries, deduplicated on the device; row-limited scan of a scratch store).
+* The outcomes are packed and copied to pinned host memory: the span's ONE read-back.
 
-Regimes that need per-query state changes inside the batch fall back to
-``route`` per query: no knowledge base / NAIVE_RAG disabled (queries may
-miss every layer and skip write-back), capped caches (LRU eviction), or a
-non-deterministic AKM settle thread.
+HOST stage (``_finish``): the decision pass over the span (vectorised), answers as
+columns (``ledger.BatchLedger``; objects are built lazily), write-back (KV put on the
+device, semantic-cache payloads, AKM settle device-to-device from KB rows) and counters.
+If the L4 guard cannot prove a miss for some query, the span stops before it, that query
+is routed by ``router.route`` exactly, and batching resumes after it.
+
+Pipelining: span i+1's device stage is enqueued BEFORE span i's host stage, so the host's
+bookkeeping of span i overlaps the GPU's scans of span i+1.  This is exact because span
+i+1's device stage depends on span i only through texts and vectors (L1 window mask, the
+semantic-cache rows appended up front) and through span i's seeds (included in the L4 guard
+superset), never through span i's answers.  If span i stops early, span i+1's speculative
+results are discarded (its cache rows are rolled back) and the pipeline restarts.
+
+All scores are the exact fp64 reference scores (bit-identical), so every threshold
+decision is the reference's.  Regimes that need per-query state changes inside a span
+fall back to ``route`` per query: no knowledge base / NAIVE_RAG disabled (queries may miss
+every layer and skip write-back), capped caches (LRU eviction), or a non-deterministic AKM
+settle thread.
 """
 from __future__ import annotations
 
@@ -40,13 +49,13 @@ import time
 
 import numpy as np
 
-from . import generation
-from .caches import CacheEntry, FixedKVCache, SemanticCache
-from .index import MODE_AUTO, FlatIndex, first_occurrences
-from .knowledge import AdaptiveKnowledgeMemory
-from .records import AnswerRecord, LayerTag
+from . import _lib, generation
+from .caches import FixedKVCache, SemanticCache
 from .errors import CascadeError
+from .index import MODE_AUTO, FlatIndex
+from .knowledge import AdaptiveKnowledgeMemory
 from .ledger import BatchLedger, CtxRows, LedgerEntry, entry_text_conf
+from .records import LayerTag
 from .router import LayerProbe
 from .textarena import to_device
 
@@ -55,6 +64,7 @@ L1, L2, L3, L4, L5 = (LayerTag.FIXED_KV, LayerTag.SEMANTIC_CACHE, LayerTag.MEMOR
 # immutable probe records shared by every routed query (only the serving
 # layer's probe carries a latency and is built per query)
 _PROBE = {(L, o): LayerProbe(L, o) for L in LayerTag for o in ("hit", "miss", "rejected")}
+DEFAULT_SPAN = 4096
 
 
 def batchable(router) -> bool:
@@ -70,7 +80,7 @@ def batchable(router) -> bool:
 
 
 def route_batch(router, queries, vectors=None, *, mode: int = MODE_AUTO, materialize: bool = True,
-                capture_errors: bool = False):
+                capture_errors: bool = False, span: int = DEFAULT_SPAN):
     """Route ``queries`` in order; see the module docstring.  Returns the list
     of (AnswerRecord, RouteTraceEvent), or with ``materialize=False`` a
     ``RoutedBatch`` of columnar segments (objects built only on access).
@@ -81,7 +91,9 @@ def route_batch(router, queries, vectors=None, *, mode: int = MODE_AUTO, materia
     independent ``route`` calls would (service micro-batching)."""
     segs = []
     i, n = 0, len(queries)
-    stats = {"batched": 0, "sequential": 0, "splits": 0}
+    stats = {"batched": 0, "sequential": 0, "splits": 0, "spans": 0, "pipelined": 0}
+    span = max(1, int(span))
+    kv = router.kv_cache
 
     def one(q):
         if not capture_errors:
@@ -91,34 +103,61 @@ def route_batch(router, queries, vectors=None, *, mode: int = MODE_AUTO, materia
         except CascadeError as exc:
             return exc
 
-    while i < n:
-        if not batchable(router):
-            segs.append([one(queries[i])])
-            stats["sequential"] += 1
-            i += 1
-            continue
-        V = None if vectors is None else vectors[i:]
-        remaining = n - i
-        try:
-            done, ledger = _route_prefix(router, queries[i:], V, mode)
-        except _BackendFailed:
-            # a backend call raised mid-batch: every store mutation of the batch was rolled
-            # back, so route the span one query at a time — the failing query raises (or is
-            # captured) exactly where independent route() calls would raise
-            for q in queries[i:]:
-                segs.append([one(q)])
-            stats["sequential"] += remaining
-            break
-        if done:
-            segs.append(ledger)
-        stats["batched"] += done
-        i += done
-        if done < remaining:
-            # the next query's AKM outcome is not certain in batch: route it exactly
-            segs.append([one(queries[i])])
-            stats["sequential"] += 1
-            stats["splits"] += 1
-            i += 1
+    pending = None
+    hold = isinstance(kv, FixedKVCache)
+    if hold:
+        kv._compact_hold += 1  # KV values read by a launched span stay valid until its host stage
+    try:
+        while i < n:
+            if not batchable(router):
+                pending = None
+                segs.append([one(queries[i])])
+                stats["sequential"] += 1
+                i += 1
+                continue
+            if pending is not None and pending.start == i:
+                cur, pending = pending, None
+                stats["pipelined"] += 1
+            else:
+                router.adaptive_memory.settle()  # the first route() would settle the queue (router.py:284-285)
+                cur = _launch(router, queries, vectors, i, min(n, i + span), mode, None)
+            if cur.end < n:
+                # span i+1's device work is queued before span i's host stage (module doc)
+                pending = _launch(router, queries, vectors, cur.end, min(n, cur.end + span), mode, cur)
+            stats["spans"] += 1
+            try:
+                done, ledger = _finish(router, cur, more_follow=cur.end < n)
+            except _BackendFailed:
+                # a backend call raised: every store mutation of the span (and of the
+                # speculative next span) was rolled back — route the rest one by one, so
+                # the failing query raises (or is captured) where independent route()
+                # calls would raise
+                pending = None
+                for q in queries[i:]:
+                    segs.append([one(q)])
+                stats["sequential"] += n - i
+                break
+            if done:
+                segs.append(ledger)
+            stats["batched"] += done
+            i += done
+            if done < cur.size:
+                # the next query's AKM outcome is not certain: route it exactly.  The
+                # speculative next span assumed this span was served in full: drop it
+                # (its cache rows went with the truncation in _writeback)
+                pending = None
+                segs.append([one(queries[i])])
+                stats["sequential"] += 1
+                stats["splits"] += 1
+                i += 1
+    finally:
+        if pending is not None:
+            _discard(router, pending)
+        if hold:
+            kv._compact_hold -= 1
+            if not kv._compact_hold:
+                with kv._lock:
+                    kv._maybe_compact()
     router.last_batch_stats = stats
     rb = RoutedBatch(segs)
     return rb.results() if materialize else rb
@@ -169,175 +208,273 @@ def _recall_always_rejects(backend, threshold) -> bool:
             and 0.0 <= threshold <= 1.0)
 
 
-def _row_scratch(router, n: int) -> np.ndarray:
-    buf = getattr(router, "_row_pos", None)
-    if buf is None or buf.size < n:
-        buf = router._row_pos = np.empty(max(n, 1), dtype=np.int32)
-    return buf
+class _Scratch:
+    """Per-router device buffers of the cascade: the seed-guard stores and the KB-row mark
+    array (one int32 per knowledge-base row, restored by every pr_cascade_seeds)."""
+
+    def __init__(self, dim: int):
+        self.dim = dim
+        self.stores: list[FlatIndex] = []
+        self.mark = None
+        self.turn = 0
+
+    def store(self, rows_bound: int) -> FlatIndex:
+        # two stores, alternating: a launched span's guard store must survive until its
+        # queued scan has run, while the next span fills the other one
+        if len(self.stores) < 2:
+            self.stores.append(FlatIndex(dim=self.dim, capacity=rows_bound))
+        s = self.stores[self.turn]
+        self.turn ^= 1
+        s.clear()
+        return s
+
+    def marks(self, n: int):
+        import torch
+
+        if self.mark is None or self.mark.numel() < n:
+            self.mark = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+            _lib.check(_lib.load().pr_cascade_mark_init(_lib.ptr(self.mark), self.mark.numel(), _lib.stream_ptr()),
+                       "mark_init")
+        return self.mark
 
 
-def _seed_scratch(router, dim, rows_bound: int) -> FlatIndex:
-    """The router's reusable seed store, reserved for the batch's worst case up
-    front (growing it mid-run would reallocate between two dependent searches)."""
-    s = getattr(router, "_seed_scratch", None)
+def _scratch(router, dim) -> _Scratch:
+    s = getattr(router, "_cascade_scratch", None)
     if s is None or s.dim != dim:
-        s = FlatIndex(dim=dim, capacity=rows_bound)
-        router._seed_scratch = s
-    s.clear()
+        s = router._cascade_scratch = _Scratch(dim)
     return s
 
 
-def _route_prefix(router, qs, vectors, mode):
+class _Span:
+    """A span whose device stage has been enqueued."""
+
+    __slots__ = ("start", "end", "size", "B", "qs", "texts", "arena", "n_pre_sc", "new_js", "prev_last",
+                 "prev", "host", "event", "kb_rows_d", "kb_cnt_d", "nlist_d", "t_start", "entries")
+
+
+def _launch(router, queries, vectors, start: int, end: int, mode: int, prev: "_Span | None") -> _Span:
+    """Enqueue a span's device stage (see the module doc); nothing is read back here."""
     import torch
 
+    L = _lib.load()
     cfg = router.config
     order = cfg.probe_order()
-    pos = {L: i for i, L in enumerate(order)}
+    pos = {Lr: i for i, Lr in enumerate(order)}
     kv, sc, akm, kb = router.kv_cache, router.semantic_cache, router.adaptive_memory, router.knowledge_base
-    backend = router.backend
-    t_start = time.perf_counter_ns()
-    prof = _Prof(getattr(router, "profile_batches", False))
-    akm.settle()  # the first route() of the run would settle the pre-batch queue (router.py:284-285)
+    sp = _Span()
+    sp.t_start = time.perf_counter_ns()
+    sp.start, sp.end = start, end
+    qs = queries[start:end]
+    B = sp.size = sp.B = len(qs)
+    sp.qs = qs
+    texts = sp.texts = [q.text for q in qs]
+    sp.entries = None
+    arena = sp.arena = to_device(texts)  # one device UTF-8 arena: embedding, L1 probe, KV write-back
+    Vd = _embed(router, texts, None if vectors is None else vectors[start:end], arena)
+    s = _lib.stream_ptr()
+    dev = "cuda"
 
-    B = len(qs)
-    texts = [q.text for q in qs]
-    arena = to_device(texts)  # one device UTF-8 arena: embedding, L1 probe, KV write-back
-    Vd = _embed(router, texts, vectors, arena)
-    ar = np.arange(B)
-
-    prof.mark("settle+embed")
-    # ---- L1: pre-batch probe + causal first-occurrence dedupe
+    # ---- window dedupe (host, texts only): an earlier write of the same text in this span
+    # or in the previous one (that span is written back before this span's queries route)
     first_of = {t: j for j, t in zip(range(B - 1, -1, -1), reversed(texts))}  # earliest index wins
     first = np.fromiter(map(first_of.__getitem__, texts), dtype=np.int64, count=B)
-    l1 = np.zeros(B, dtype=bool)
-    kv_val = np.full(B, -1, dtype=np.int64)
-    if L1 in pos:
-        vals, hit = kv.probe_device(arena[0], arena[1], B)
-        kv_val = vals.cpu().numpy()
-        l1 = hit.cpu().numpy().astype(bool) | (first < ar)
+    ar = np.arange(B)
+    rep = first < ar
+    sp.prev_last = None
+    sp.prev = prev
+    if prev is not None:
+        prev_last = {t: j for j, t in enumerate(prev.texts)}  # latest writer in the previous span
+        sp.prev_last = prev_last
+        rep |= np.fromiter(map(prev_last.__contains__, texts), dtype=bool, count=B)
 
-    prof.mark("l1")
-    # ---- L2: append the rows write-back will create, then one row-limited top-1 search
+    # ---- L2 rows write-back will create: first occurrences of texts new to the cache
     sc_index = sc.index
-    n_pre_sc = len(sc_index)
+    sp.n_pre_sc = n_pre_sc = len(sc_index)
     with sc_index._lock:
         sc_rows = sc_index._row_by_id
         new_js = np.array([j for j in np.flatnonzero(first == ar).tolist() if texts[j] not in sc_rows],
                           dtype=np.int64)
+    sp.new_js = new_js
     if new_js.size:
-        sc_index.extend_arrays([texts[j] for j in new_js], Vd[torch.from_numpy(new_js).cuda()],
+        sc_index.extend_arrays([texts[j] for j in new_js], Vd[torch.from_numpy(new_js).to(dev)],
                                payloads=[None] * int(new_js.size), validate=False)
-    counters = {a: getattr(backend, a) for a in _BACKEND_COUNTERS if isinstance(getattr(backend, a, None), int)}
-    try:
-        return _route_rest(router, qs, texts, arena, Vd, mode, prof, t_start, first, l1, kv_val, sc_index,
-                           n_pre_sc, new_js)
-    except _WritebackFailed as exc:
-        raise exc.__cause__
-    except Exception as exc:
-        # the rows appended above carry no payload yet: never leave them searchable
-        # (ADVICE r1: a later L2 hit on one would serve None).  Backend counters go back to
-        # where they were so the sequential re-route counts each call once.
-        if len(sc_index) > n_pre_sc:
-            sc_index.truncate(n_pre_sc)
-        for a, v in counters.items():
-            setattr(backend, a, v)
-        raise _BackendFailed() from exc
+    sc_limit = n_pre_sc + np.searchsorted(new_js, ar, side="left")  # rows written by queries i < j
+
+    # ---- L1 probe, L2 top-1, gate + miss-list compaction: all on the device
+    u8, i64 = torch.uint8, torch.int64
+    kv_hit = kv_val = None
+    if L1 in pos:
+        kv_val, kv_hit = kv.probe_device(arena[0], arena[1], B)
+    rep_d = torch.from_numpy(rep.astype(np.uint8)).to(dev, non_blocking=True)
+    r2 = None
+    if L2 in pos:
+        r2 = sc_index.search_batch(Vd, 1, mode=mode, validate=False, row_limit=sc_limit, count=False)
+    vec_pos = min(pos.get(L4, 99), pos.get(L5, 99))
+    l1_d = torch.empty(B, dtype=u8, device=dev)
+    l2_d = torch.empty(B, dtype=u8, device=dev)
+    lst = torch.empty(B, dtype=torch.int32, device=dev)
+    nlist = torch.empty(1, dtype=torch.int32, device=dev)
+    slot = torch.empty(B, dtype=torch.int32, device=dev)
+    sc_cnt = r2.count if r2 is not None else None
+    sc_score = r2.scores[:, 0].contiguous() if r2 is not None else None
+    _lib.check(L.pr_cascade_gate(B, _lib.ptr(kv_hit), _lib.ptr(rep_d), _lib.ptr(sc_cnt), _lib.ptr(sc_score),
+                                 float(sc.threshold), int(L1 in pos and pos[L1] < vec_pos),
+                                 int(L2 in pos and pos[L2] < vec_pos), _lib.ptr(l1_d), _lib.ptr(l2_d), _lib.ptr(lst),
+                                 _lib.ptr(nlist), _lib.ptr(slot), s), "cascade_gate")
+
+    # ---- L5: the knowledge-base scan of the listed queries only
+    sk = cfg.akm_seed_k
+    kbi = kb.index
+    kb_rows = torch.empty((B, sk), dtype=i64, device=dev)
+    kb_raw = torch.empty((B, sk), dtype=torch.float64, device=dev)
+    kb_rep = torch.empty((B, sk), dtype=torch.float64, device=dev)
+    kb_cnt = torch.empty(B, dtype=torch.int32, device=dev)
+    hint = int(min(B, max(1, getattr(router, "_cascade_nlist_hint", B // 2 + 1))))
+    with kbi._lock:
+        _lib.check(L.pr_index_search_list(kbi.handle, _lib.ptr(Vd), _lib.ptr(lst), _lib.ptr(nlist), B, hint, sk, mode,
+                                          None, _lib.ptr(kb_rows), _lib.ptr(kb_raw), _lib.ptr(kb_rep),
+                                          _lib.ptr(kb_cnt), s), "search_list")
+    sp.kb_rows_d, sp.kb_cnt_d, sp.nlist_d = kb_rows, kb_cnt, nlist
+
+    # ---- L4 guard: the AKM as it is now, and the superset of seeds settled before each query
+    l4 = torch.zeros(B, dtype=torch.bool, device=dev)
+    if L4 in pos:
+        thr = akm.threshold
+        if len(akm.index):
+            ra = akm.index.search_batch(Vd, 1, mode=mode, validate=False, count=False)
+            l4 |= (ra.count > 0) & (ra.scores[:, 0] >= thr)
+        scr = _scratch(router, kbi.dim)
+        prev_b = prev.B if prev is not None else 0
+        out_max = (prev_b + B) * sk
+        out_rows = torch.empty(out_max, dtype=i64, device=dev)
+        nout = torch.empty(1, dtype=torch.int32, device=dev)
+        before = torch.empty(B, dtype=i64, device=dev)
+        mark = scr.marks(len(kbi))
+        _lib.check(L.pr_cascade_seeds(
+            _lib.ptr(prev.kb_rows_d) if prev is not None else None,
+            _lib.ptr(prev.kb_cnt_d) if prev is not None else None,
+            _lib.ptr(prev.nlist_d) if prev is not None else None,
+            _lib.ptr(kb_rows), _lib.ptr(kb_cnt), _lib.ptr(nlist), sk, _lib.ptr(mark), _lib.ptr(out_rows), out_max,
+            _lib.ptr(nout), _lib.ptr(before), s), "cascade_seeds")
+        store = scr.store(out_max)
+        store.append_anonymous_from(kbi, out_rows)
+        lim = torch.where(slot >= 0, before[slot.clamp(min=0).long()], torch.zeros_like(before))
+        rs = store.search_batch(Vd, 1, mode=mode, validate=False, row_limit=lim, count=False)
+        l4 |= (rs.count > 0) & (rs.scores[:, 0] >= thr)
+        l4 &= slot >= 0
+
+    # ---- the span's one read-back: outcomes + the listed queries' KB rows
+    cols = [l1_d.to(i64), l2_d.to(i64), slot.to(i64), l4.to(i64),
+            (r2.rows[:, 0] if r2 is not None else torch.full((B,), -1, dtype=i64, device=dev)),
+            (kv_val if kv_val is not None else torch.full((B,), -1, dtype=i64, device=dev)),
+            kb_cnt.to(i64), nlist.to(i64)]
+    packed = torch.cat([c.reshape(-1) for c in cols] + [kb_rows.reshape(-1)])
+    host = torch.empty(packed.shape, dtype=i64, pin_memory=True)
+    host.copy_(packed, non_blocking=True)
+    ev = torch.cuda.Event()
+    ev.record()
+    sp.host, sp.event = host, ev
+    return sp
 
 
-def _route_rest(router, qs, texts, arena, Vd, mode, prof, t_start, first, l1, kv_val, sc_index, n_pre_sc, new_js):
-    import torch
+def _discard(router, sp: _Span) -> None:
+    """Drop a speculative span: its appended cache rows go (they are the newest rows)."""
+    sc_index = router.semantic_cache.index
+    if len(sc_index) > sp.n_pre_sc:
+        sc_index.truncate(sp.n_pre_sc)
 
+
+def _unpack(sp: _Span, sk: int):
+    sp.event.synchronize()
+    h = sp.host.numpy()
+    B = sp.B
+    l1, l2, slot, l4, sc_row, kv_val, kb_cnt = (h[i * B:(i + 1) * B] for i in range(7))
+    nl = int(h[7 * B])
+    kb_rows = h[7 * B + 1:].reshape(B, sk)
+    return l1.astype(bool), l2.astype(bool), slot, l4.astype(bool), sc_row, kv_val, kb_rows[:nl], kb_cnt[:nl], nl
+
+
+def _finish(router, sp: _Span, *, more_follow: bool):
+    """The span's host stage: decisions, answers, write-back, counters.  Returns
+    (queries routed, ledger); stops before a query whose L4 outcome is uncertain."""
     cfg = router.config
     order = cfg.probe_order()
     pos = {L: i for i, L in enumerate(order)}
-    kv, sc, akm, kb = router.kv_cache, router.semantic_cache, router.adaptive_memory, router.knowledge_base
     backend = router.backend
-    B = len(qs)
-    ar = np.arange(B)
-    sc_limit = n_pre_sc + np.searchsorted(new_js, ar, side="left")  # rows written by queries i < j
-    l2 = np.zeros(B, dtype=bool)
-    sc_row = np.full(B, -1, dtype=np.int64)
-    # only queries that actually probe L2 are searched (an L1 hit in front of it ends the cascade)
-    need2 = ~l1 if (L1 in pos and L2 in pos and pos[L1] < pos[L2]) else np.ones(B, dtype=bool)
-    js2 = np.nonzero(need2)[0]
-    if L2 in pos and js2.size:
-        sel = torch.from_numpy(js2).cuda()
-        r = sc_index.search_batch(Vd[sel], 1, mode=mode, validate=False, row_limit=sc_limit[js2], count=False)
-        prof.note("sc", sc_index)
-        sc_row[js2] = r.rows[:, 0].cpu().numpy()
-        l2[js2] = (r.count.cpu().numpy() > 0) & (r.scores[:, 0].cpu().numpy() >= sc.threshold)
-
-    prof.mark("l2")
-
-    def host_prep():
-        """Host work that needs no knowledge-base result (runs while the KB scan is in
-        flight): the batch's ledger shell, its cache entries, and for every L1/L2 hit
-        candidate the latest earlier query of the batch that wrote the same key."""
-        ledger = BatchLedger.__new__(BatchLedger)
-        now = time.monotonic_ns()
-        entries = [LedgerEntry(t, ledger, j, now) for j, t in enumerate(texts)]
-        l1l, l2l, scr = l1.tolist(), l2.tolist(), sc_row.tolist()
-        l1_first = L1 in pos and (L2 not in pos or pos[L1] < pos[L2])
+    qs, texts = sp.qs, sp.texts
+    sc_index = router.semantic_cache.index
+    kv = router.kv_cache
+    prof = _Prof(getattr(router, "profile_batches", False))
+    # host work that needs no device result: the ledger shell and the span's cache entries
+    ledger = BatchLedger.__new__(BatchLedger)
+    now = time.monotonic_ns()
+    entries = sp.entries = [LedgerEntry(t, ledger, j, now) for j, t in enumerate(texts)]
+    prof.mark("prep")
+    l1, l2, slot, l4_unsure, sc_row, kv_val, kb_rows, kb_cnt, nlist = _unpack(sp, cfg.akm_seed_k)
+    router._cascade_nlist_hint = max(1, nlist)
+    prof.mark("wait")
+    counters = {a: getattr(backend, a) for a in _BACKEND_COUNTERS if isinstance(getattr(backend, a, None), int)}
+    try:
+        p, serving, lat, text, conf_l, recalled = _decide(router, sp, l1, l2, slot, l4_unsure, kb_rows, kb_cnt,
+                                                           prof)
+    except Exception as exc:
+        # the rows appended up front carry no payload yet: never leave them searchable
+        # (ADVICE r1: a later L2 hit on one would serve None).  Backend counters go back to
+        # where they were so the sequential re-route counts each call once.
+        if len(sc_index) > sp.n_pre_sc:
+            sc_index.truncate(sp.n_pre_sc)
+        for a, v in counters.items():
+            setattr(backend, a, v)
+        raise _BackendFailed() from exc
+    # ---- cache hits, in order: a hit serves a copy of the latest answer written for its key
+    v1, v2, v5 = int(L1), int(L2), int(L5)
+    sv = serving
+    hit_js = np.flatnonzero((sv == v1) | (sv == v2))
+    if hit_js.size:
         sc_ids = sc_index._ids
-        src = [-1] * B
+        kv_entry, sc_payload = kv.entry_at, sc_index.payload_at
+        prev_last = sp.prev_last
+        prev_entries = sp.prev.entries if sp.prev is not None else None
         latest: dict[str, int] = {}
-        for j, t in enumerate(texts):
-            a, b = l1l[j], l2l[j]
-            if a or b:  # the serving one of L1 / L2 is the earlier of the two in probe order
-                src[j] = latest.get(t if (a and (l1_first or not b)) else sc_ids[scr[j]], -1)
-            latest[t] = j
-        return ledger, entries, src
+        nxt = 0
+        hl = hit_js.tolist()
+        for j in hl:
+            latest.update(zip(texts[nxt:j], range(nxt, j)))  # writers since the previous hit
+            nxt = j
+            key = texts[j] if sv[j] == v1 else sc_ids[int(sc_row[j])]  # the serving layer's key
+            i = latest.get(key, -1)
+            if i >= 0:  # an earlier query of this span wrote the key
+                text[j], conf_l[j] = text[i], conf_l[i]
+            elif prev_last is not None and key in prev_last:  # the previous span wrote it last
+                text[j], conf_l[j] = entry_text_conf(prev_entries[prev_last[key]])
+            elif sv[j] == v1:
+                text[j], conf_l[j] = entry_text_conf(kv_entry(int(kv_val[j])))
+            else:
+                text[j], conf_l[j] = entry_text_conf(sc_payload(int(sc_row[j])))
+    for j, a in recalled.items():
+        text[j], conf_l[j] = a.text, a.confidence
+    conf = np.asarray(conf_l, dtype=np.float64)
+    ctx_rows = CtxRows(kb_rows, slot[:p], kb_cnt, cfg.retrieval_k, sv == v5)
+    probe_prefix = {}
+    for L in order:
+        probe_prefix[L] = tuple(_PROBE[M, "rejected" if M is L3 else "miss"] for M in order[: pos[L]])
+    ledger.__init__(qs[:p], serving, lat, text, conf, ctx_rows, router.knowledge_base.index, probe_prefix)
+    prof.mark("materialise")
+    _writeback(router, sp, p, entries, ledger, serving, slot, kb_rows, kb_cnt, more_follow, prof)
+    sp.prev = sp.prev_last = None  # the previous span is no longer read: no chain of spans stays alive
+    return p, ledger
 
-    prep = None
-    # ---- L4/L5 speculation for every query that can reach them
-    vec_pos = min(pos.get(L4, 99), pos.get(L5, 99))
-    blocked = np.zeros(B, dtype=bool)
-    if L1 in pos and pos[L1] < vec_pos:
-        blocked |= l1
-    if L2 in pos and pos[L2] < vec_pos:
-        blocked |= l2
-    spec = np.nonzero(~blocked)[0]
-    slot = np.full(B, -1, dtype=np.int64)
-    slot[spec] = np.arange(spec.size)
-    kb_rows = np.zeros((0, cfg.akm_seed_k), dtype=np.int64)
-    kb_cnt = np.zeros(0, dtype=np.int32)
-    l4_unsure = np.zeros(B, dtype=bool)
-    if spec.size:
-        Vs = Vd[torch.from_numpy(spec).cuda()]
-        r = kb.index.search_batch(Vs, cfg.akm_seed_k, mode=mode, validate=False, count=False)
-        prof.note("kb", kb.index)
-        # the pre-batch AKM probe does not depend on the KB results: queue it behind the scan
-        ra = None
-        if L4 in pos and len(akm.index):
-            ra = akm.index.search_batch(Vs, 1, mode=mode, validate=False, count=False)
-            prof.note("akm", akm.index)
-        prep = host_prep()
-        kb_rows, kb_cnt = r.rows.cpu().numpy(), r.count.cpu().numpy()
-        if L4 in pos:
-            thr = akm.threshold
-            if ra is not None:
-                l4_unsure[spec] |= (ra.count.cpu().numpy() > 0) & (ra.scores[:, 0].cpu().numpy() >= thr)
-            # superset of in-batch seeds: every seed of every earlier speculative query
-            # row-major boolean selection = the per-query seed lists concatenated in order
-            seed_rows = kb_rows[np.arange(kb_rows.shape[1])[None, :] < kb_cnt[:, None]]
-            seeds_before = np.concatenate([[0], np.cumsum(kb_cnt)[:-1]]).astype(np.int64)
-            if seed_rows.size:
-                # keep the first occurrence of each KB row: query j sees the same SET of
-                # vectors (a repeat only becomes visible after its first copy), and the
-                # scratch loses its bit-identical duplicates, which tie at every score
-                first_pos = first_occurrences(seed_rows, _row_scratch(router, len(kb.index)))
-                seeds_before = np.searchsorted(first_pos, seeds_before, side="left").astype(np.int64)
-                seed_rows = seed_rows[first_pos]
-                scratch = _seed_scratch(router, kb.index.dim, B * cfg.akm_seed_k)
-                scratch.append_anonymous_from(kb.index, seed_rows)
-                rs = scratch.search_batch(Vs, 1, mode=mode, validate=False, row_limit=seeds_before, count=False)
-                prof.note("seeds", scratch)
-                l4_unsure[spec] |= (rs.count.cpu().numpy() > 0) & (rs.scores[:, 0].cpu().numpy() >= thr)
 
-    prof.mark("l4+l5")
-    # ---- decision pass, vectorised over the batch.  A batch stops before the
-    # first query whose L4 outcome is not certain (decided from L1/L2 alone, so
-    # no backend side effect happens for it in batch mode)
+def _decide(router, sp, l1, l2, slot, l4_unsure, kb_rows, kb_cnt, prof):
+    """Decision pass, vectorised over the span; answers of retrieval and recall."""
+    cfg = router.config
+    order = cfg.probe_order()
+    pos = {L: i for i, L in enumerate(order)}
+    backend = router.backend
+    kb = router.knowledge_base
+    qs, B = sp.qs, sp.B
+    # a span stops before the first query whose L4 outcome is not certain (decided from
+    # L1/L2 alone, so no backend side effect happens for it in batch mode)
     stop = B
     if L4 in pos:
         reach4 = l4_unsure.copy()
@@ -346,7 +483,7 @@ def _route_rest(router, qs, texts, arena, Vd, mode, prof, t_start, first, l1, kv
                 reach4 &= ~l1
             elif L is L2:
                 reach4 &= ~l2
-        hits = np.nonzero(reach4)[0]
+        hits = np.flatnonzero(reach4)
         if hits.size:
             stop = int(hits[0])
     p = stop
@@ -365,7 +502,7 @@ def _route_rest(router, qs, texts, arena, Vd, mode, prof, t_start, first, l1, kv
             backend.recall_calls += int(reach.sum())
         elif L is L3:
             h = np.zeros(p, dtype=bool)
-            for j in np.nonzero(reach)[0]:
+            for j in np.flatnonzero(reach):
                 rec = generation.memory_recall(backend, qs[j], cfg.recall_threshold)
                 if rec is not None:
                     h[j] = True
@@ -376,10 +513,8 @@ def _route_rest(router, qs, texts, arena, Vd, mode, prof, t_start, first, l1, kv
             h = reach.copy()
         serving[h] = int(L)
         reach &= ~h
-
     prof.mark("decide")
-    # ---- answers as columns; objects are materialised lazily (ledger.py)
-    wall = (time.perf_counter_ns() - t_start) / 1e9
+    wall = (time.perf_counter_ns() - sp.t_start) / 1e9
     lm = router.latency_model
     if lm is None:
         lat = np.full(p, wall / max(1, p))
@@ -390,14 +525,12 @@ def _route_rest(router, qs, texts, arena, Vd, mode, prof, t_start, first, l1, kv
     text: list = [None] * p
     conf_l = [0.0] * p
     k_ctx = cfg.retrieval_k
-    v1, v2, v5 = int(L1), int(L2), int(L5)
-    sv = serving[:p]
-    # L5 answers first: they depend on no other query of the batch.  The stub LLM
-    # answers with the top passage's annotation (generation.py:83-115): compute that
-    # directly instead of building a context answer object per query
-    # exact type: a subclass may override generate_with_context (and must be called)
+    v5 = int(L5)
+    # retrieval answers first: they depend on no other query of the span.  The stub LLM
+    # answers with the top passage's annotation (generation.py:83-115): computed directly
+    # (exact type: a subclass may override generate_with_context and must be called)
     stub = type(backend) is generation.StubBackend and 0.0 <= backend.context_confidence <= 1.0
-    l5_js = np.flatnonzero(sv == v5).tolist()
+    l5_js = np.flatnonzero(serving == v5).tolist()
     if l5_js:
         l5_slots = slot[l5_js]
         if stub:
@@ -413,57 +546,25 @@ def _route_rest(router, qs, texts, arena, Vd, mode, prof, t_start, first, l1, kv
                 passages = [kb.index.payload_at(int(r)) for r in kb_rows[s5, : min(k_ctx, int(kb_cnt[s5]))]]
                 a = generation.generate_with_context(backend, qs[j], passages, L5)
                 text[j], conf_l[j] = a.text, a.confidence
-    for j, a in recalled.items():
-        text[j], conf_l[j] = a.text, a.confidence
-    # cache hits, in order: a hit serves a copy of the latest answer written for its key
-    if prep is None:
-        prep = host_prep()
-    ledger, entries, src = prep
-    hit_js = np.flatnonzero((sv == v1) | (sv == v2)).tolist()
-    if hit_js:
-        codes, scr, kvv = sv.tolist(), sc_row[:p].tolist(), kv_val[:p].tolist()
-        kv_entry, sc_payload = kv.entry_at, sc_index.payload_at
-        for j in hit_js:  # ascending: an earlier writer's answer is already filled
-            i = src[j]
-            if i >= 0:
-                text[j], conf_l[j] = text[i], conf_l[i]
-            elif codes[j] == v1:
-                text[j], conf_l[j] = entry_text_conf(kv_entry(kvv[j]))
-            else:
-                text[j], conf_l[j] = entry_text_conf(sc_payload(scr[j]))
-    conf = np.asarray(conf_l, dtype=np.float64)
-    ctx_rows = CtxRows(kb_rows, slot[:p], kb_cnt, k_ctx, sv == v5)
-    probe_prefix = {}
-    for L in order:
-        pre = []
-        for M in order[: pos[L]]:
-            pre.append(_PROBE[M, "rejected" if M is L3 else "miss"])
-        probe_prefix[L] = tuple(pre)
-    ledger.__init__(qs[:p], serving, lat, text, conf, ctx_rows, kb.index, probe_prefix)
-
-    prof.mark("materialise")
-    # ---- write-back (router.py:333-337): KV in order (last write wins), SC payloads.
-    # Every backend call of the batch happened above; a failure from here on is not a
-    # per-query error and is not retried query by query.
-    try:
-        return _writeback(router, qs, texts, arena, prof, p, entries, ledger, serving, slot, kb_rows, kb_cnt,
-                          sc_index, n_pre_sc, new_js)
-    except Exception as exc:
-        raise _WritebackFailed() from exc
+    return p, serving, lat, text, conf_l, recalled
 
 
-def _writeback(router, qs, texts, arena, prof, p, entries, ledger, serving, slot, kb_rows, kb_cnt, sc_index,
-               n_pre_sc, new_js):
+def _writeback(router, sp, p, entries, ledger, serving, slot, kb_rows, kb_cnt, more_follow, prof):
+    """Write-back (router.py:333-337) and counters of the span's first p queries."""
     cfg = router.config
     order = cfg.probe_order()
     pos = {L: i for i, L in enumerate(order)}
     kv, sc, akm, kb = router.kv_cache, router.semantic_cache, router.adaptive_memory, router.knowledge_base
-    del entries[p:]
-    kv.put_entries(texts[:p], entries, arena=arena)
+    sc_index = sc.index
+    texts = sp.texts
+    kv.put_entries(texts[:p], entries[:p], arena=sp.arena)
     prof.mark("wb.kv")
-    n_new_kept = int(np.searchsorted(new_js, p, side="left"))
-    if n_pre_sc + n_new_kept < len(sc_index):
-        sc_index.truncate(n_pre_sc + n_new_kept)
+    if p < sp.B:
+        # a stopped span: the rows of its unrouted queries go, and with them every row a
+        # speculative next span appended after them (that span is discarded)
+        n_new_kept = int(np.searchsorted(sp.new_js, p, side="left"))
+        if sp.n_pre_sc + n_new_kept < len(sc_index):
+            sc_index.truncate(sp.n_pre_sc + n_new_kept)
     with sc._lock, sc_index._lock:
         payloads, rowmap = sc_index._payloads, sc_index._row_by_id
         for t, e in zip(texts[:p], entries):
@@ -472,18 +573,19 @@ def _writeback(router, qs, texts, arena, prof, p, entries, ledger, serving, slot
         sc._recency.update(zip(texts[:p], range(seq + 1, seq + p + 1)))
         sc._seq = seq + p
     prof.mark("wb.sc")
-    # AKM: seeds of L5 queries before the last were settled by the following
-    # route() calls (device-to-device from KB rows, dedupe by id, no overwrite);
-    # the final query's seeds are still pending, exactly as after route()
-    l5_slots = slot[np.flatnonzero(serving[: max(p - 1, 0)] == int(L5))]
+    # AKM: seeds of retrieval-served queries settle before the next query routes
+    # (device-to-device from KB rows, dedupe by id, no overwrite).  The last query's
+    # seeds stay pending, exactly as after route(), unless more queries of this call
+    # follow — the next one would settle them first anyway.
+    upto = p if (more_follow or p < sp.B) else max(p - 1, 0)
+    l5_slots = slot[np.flatnonzero(serving[:upto] == int(L5))]
     if l5_slots.size:
         # row-major boolean selection = the per-query seed lists concatenated in order
         valid = np.arange(kb_rows.shape[1])[None, :] < kb_cnt[l5_slots][:, None]
         akm.settle_from_rows(kb.index, kb_rows[l5_slots][valid])
-    if p and serving[p - 1] == int(L5):
+    if upto < p and serving[p - 1] == int(L5):
         s = slot[p - 1]
         akm.enqueue([kb.index.payload_at(int(r)) for r in kb_rows[s, : kb_cnt[s]]])
-
     prof.mark("wb.akm")
     # ---- counters: a layer is probed by every query served at or after it
     pos_of_code = np.full(max(int(L) for L in LayerTag) + 1, -1, dtype=np.int64)
@@ -515,48 +617,26 @@ def _writeback(router, qs, texts, arena, prof, p, entries, ledger, serving, slot
         for k, v in prof.times.items():
             hist[k] = hist.get(k, 0.0) + v
         router.batch_profile_log = getattr(router, "batch_profile_log", []) + [dict(prof.times)]
-    return p, ledger
 
 
 _BACKEND_COUNTERS = ("recall_calls", "context_calls")
 
 
 class _BackendFailed(Exception):
-    """Raised by _route_prefix after rolling its store mutations back."""
-
-
-class _WritebackFailed(Exception):
-    """Wraps a write-back failure so it passes the rollback handler unchanged."""
+    """Raised by _finish after rolling its store mutations back."""
 
 
 class _Prof:
-    """Optional stage timer (synchronises the device at each mark)."""
+    """Optional stage timer (wall time of the host stage's parts)."""
 
     def __init__(self, enabled: bool):
         self.enabled = enabled
         self.times: dict[str, float] = {}
         self._t = time.perf_counter()
 
-    def note(self, name: str, index) -> None:
-        if not self.enabled:
-            return
-        st = index.stats()
-        self.mark(name)
-        self.times[f"{name}.rows"] = self.times.get(f"{name}.rows", 0) + len(index)
-        self.times[f"{name}.queries"] = self.times.get(f"{name}.queries", 0) + st.queries
-        self.times[f"{name}.fallback"] = self.times.get(f"{name}.fallback", 0) + st.fallback
-        self.times[f"{name}.collected"] = self.times.get(f"{name}.collected", 0) + st.collected
-        self.times[f"{name}.tensor_path"] = self.times.get(f"{name}.tensor_path", 0) + (st.path == 2)
-        self.times[f"{name}.i8_path"] = self.times.get(f"{name}.i8_path", 0) + (st.path == 3)
-        self.times[f"{name}.appended"] = self.times.get(f"{name}.appended", 0) + st.appended
-        self.times[f"{name}.rescored"] = self.times.get(f"{name}.rescored", 0) + st.candidates
-
     def mark(self, name: str) -> None:
         if not self.enabled:
             return
-        import torch
-
-        torch.cuda.synchronize()
         t = time.perf_counter()
         self.times[name] = self.times.get(name, 0.0) + (t - self._t)
         self._t = t

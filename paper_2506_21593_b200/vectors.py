@@ -144,9 +144,11 @@ class HashEmbedder:
     def embed_device(self, texts, *, arena=None) -> "object":
         """Embed a batch on the GPU (libpentarag pr_hash_embed: keyed BLAKE2b token
         hashing, warp per text) into a float32 CUDA tensor [n, dim], bit-identical
-        to ``embed``.  Texts the device does not take (non-ASCII, empty, > 256
-        tokens) are embedded on the host and patched in; an empty text raises
-        EmptyInput exactly like ``embed``."""
+        to ``embed``.  The device takes every non-empty ASCII text of at most 512
+        characters (so at most 256 tokens); the others are picked out on the host
+        BEFORE the launch, embedded there and patched in — no device-to-host read, so
+        the call never waits for the GPU.  An empty text raises EmptyInput exactly
+        like ``embed``."""
         import torch
 
         from . import _lib
@@ -162,7 +164,7 @@ class HashEmbedder:
         L = _lib.load()
         _lib.check(L.pr_hash_embed(_lib.ptr(d_data), _lib.ptr(d_off), n, self.dim, int.from_bytes(self._key, "big"),
                                    _lib.ptr(out), _lib.ptr(flag), _lib.stream_ptr()), "hash_embed")
-        host = torch.nonzero(flag).flatten().cpu().tolist()
+        host = [i for i, t in enumerate(texts) if not (t and t.isascii() and len(t) <= 512)]
         if host:
             rows = np.stack([self.embed_array(texts[i]) for i in host])
             out[torch.tensor(host, device="cuda")] = torch.from_numpy(rows).cuda()

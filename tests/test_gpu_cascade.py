@@ -37,16 +37,23 @@ def _sig(ans, ev):
             list(ans.supporting_passage_ids), [pid for pid, _ in ev.supporting_passages])
 
 
-@pytest.mark.parametrize("batch", [1000, 64, 7])
-def test_route_batch_matches_reference_trace(gpu, batch):
+@pytest.mark.parametrize("batch,pipelined", [(1000, False), (64, False), (7, False), (64, True), (7, True)])
+def test_route_batch_matches_reference_trace(gpu, batch, pipelined):
+    """pipelined: ONE route_batch call over the whole trace cut into spans of `batch`, so
+    span i+1's device stage runs before span i's host stage (incl. an AKM hit that stops a
+    span and discards the speculative next one)."""
     from paper_2506_21593_b200 import validate_query
 
     gold = _golden("router_trace.json")
     router = _router(gold["corpus"])
     qs = [validate_query(q["text"], "s1", query_id=f"q{i}", issued_at_ns=i) for i, q in enumerate(gold["queries"])]
     got = []
-    for i in range(0, len(qs), batch):
-        got.extend(router.route_batch(qs[i:i + batch]))
+    if pipelined:
+        got = router.route_batch(qs, span=batch)
+        assert router.last_batch_stats["pipelined"] > 0
+    else:
+        for i in range(0, len(qs), batch):
+            got.extend(router.route_batch(qs[i:i + batch]))
     assert len(got) == len(qs)
     for i, ((ans, ev), q) in enumerate(zip(got, gold["queries"])):
         assert [[p.layer.wire_name, p.outcome] for p in ev.layers_probed] == q["probes"], i
@@ -85,8 +92,9 @@ def test_route_batch_matches_reference_simulation(gpu):
             assert [pid for pid, _ in ev.supporting_passages] == [p["id"] for p in r["supporting_passages"]], i
 
 
+@pytest.mark.parametrize("span", [4096, 29])
 @pytest.mark.parametrize("variant", ["default", "permuted", "disabled", "recall"])
-def test_route_batch_equals_sequential_random(gpu, variant):
+def test_route_batch_equals_sequential_random(gpu, variant, span):
     from paper_2506_21593_b200 import LayerTag, RouterConfig, StubBackend, StubKnowledgeTable, validate_query
 
     gold = _golden("simulation.json")
@@ -124,7 +132,7 @@ def test_route_batch_equals_sequential_random(gpu, variant):
     want = [_sig(*seq.route(q)) for q in qs]
     got = []
     for i in range(0, len(qs), 97):
-        got.extend(_sig(*r) for r in bat.route_batch(qs[i:i + 97]))
+        got.extend(_sig(*r) for r in bat.route_batch(qs[i:i + 97], span=span))
     assert got == want
     assert seq.stats() == bat.stats()
     assert seq.backend.context_calls == bat.backend.context_calls
@@ -235,7 +243,7 @@ def test_route_batch_backend_failure_rolls_back(gpu):
             want.append(sig(exc))
     got = []
     for i in range(0, len(qs), 64):
-        got.extend(sig(r) for r in bat.route_batch(qs[i:i + 64], capture_errors=True))
+        got.extend(sig(r) for r in bat.route_batch(qs[i:i + 64], capture_errors=True, span=16))
     assert got == want
     assert got[50] == ("error", "BackendUnavailable")
     assert seq.stats() == bat.stats()
