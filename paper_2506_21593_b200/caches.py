@@ -117,6 +117,12 @@ class FixedKVCache:
     def put(self, query_text: str, answer: AnswerRecord) -> None:
         self.put_many([query_text], [answer])
 
+    def __bool__(self) -> bool:
+        # an EMPTY store is still a store: the reference router injects stores with
+        # ``kv_cache or FixedKVCache()`` (router.py:213-220), which would silently replace
+        # an empty drop-in by a CPU store if emptiness made it falsy
+        return True
+
     def __len__(self) -> int:
         with self._lock:
             return self._size()
@@ -308,6 +314,12 @@ class SemanticCache:
         fresh.search_count = old.search_count
         self._index = fresh
         self._recency = {t: self._recency[t] for t in keep}
+
+    def __bool__(self) -> bool:
+        # an EMPTY store is still a store: the reference router injects stores with
+        # ``kv_cache or FixedKVCache()`` (router.py:213-220), which would silently replace
+        # an empty drop-in by a CPU store if emptiness made it falsy
+        return True
 
     def __len__(self) -> int:
         return len(self._index)

@@ -426,6 +426,8 @@ def _finish(router, sp: _Span, *, more_follow: bool):
         for a, v in counters.items():
             setattr(backend, a, v)
         raise _BackendFailed() from exc
+    for j, a in recalled.items():  # before the cache hits: a later hit may copy a recalled answer
+        text[j], conf_l[j] = a.text, a.confidence
     # ---- cache hits, in order: a hit serves a copy of the latest answer written for its key
     v1, v2, v5 = int(L1), int(L2), int(L5)
     sv = serving
@@ -451,8 +453,6 @@ def _finish(router, sp: _Span, *, more_follow: bool):
                 text[j], conf_l[j] = entry_text_conf(kv_entry(int(kv_val[j])))
             else:
                 text[j], conf_l[j] = entry_text_conf(sc_payload(int(sc_row[j])))
-    for j, a in recalled.items():
-        text[j], conf_l[j] = a.text, a.confidence
     conf = np.asarray(conf_l, dtype=np.float64)
     ctx_rows = CtxRows(kb_rows, slot[:p], kb_cnt, cfg.retrieval_k, sv == v5)
     probe_prefix = {}

@@ -35,10 +35,11 @@ def test_reference_router_over_gpu_stores_replays_trace(gpu, rc):
         gold = json.load(fh)
     emb = rc.HashEmbedder()
     kb = g.ingest_corpus((json.dumps(c) for c in gold["corpus"]), emb)  # GPU store, reference vectors
-    router = rc.CascadeRouter(
-        embedder=emb, backend=rc.StubBackend(), knowledge_base=kb,
-        kv_cache=g.FixedKVCache(), semantic_cache=g.SemanticCache(emb), adaptive_memory=g.AdaptiveKnowledgeMemory(),
-    )
+    stores = dict(kv_cache=g.FixedKVCache(), semantic_cache=g.SemanticCache(emb),
+                  adaptive_memory=g.AdaptiveKnowledgeMemory())
+    router = rc.CascadeRouter(embedder=emb, backend=rc.StubBackend(), knowledge_base=kb, **stores)
+    for name, store in stores.items():  # empty drop-ins are truthy: the router keeps them (router.py:213-220)
+        assert getattr(router, name) is store
     for i, q in enumerate(gold["queries"]):
         if q["origin"] == "akm_probe":
             router.adaptive_memory.settle()
@@ -67,10 +68,11 @@ def test_reference_simulation_over_gpu_stores_logs_identical(gpu, rc):
     emb = rc.HashEmbedder()
     rows = synthetic_qa_dataset(gold["dataset_n"], seed=42)
     kb = g.ingest_corpus((json.dumps(r) for r in dataset_to_corpus(rows)), emb)
-    router = rc.CascadeRouter(
-        embedder=emb, backend=rc.StubBackend(), knowledge_base=kb,
-        kv_cache=g.FixedKVCache(), semantic_cache=g.SemanticCache(emb), adaptive_memory=g.AdaptiveKnowledgeMemory(),
-    )
+    stores = dict(kv_cache=g.FixedKVCache(), semantic_cache=g.SemanticCache(emb),
+                  adaptive_memory=g.AdaptiveKnowledgeMemory())
+    router = rc.CascadeRouter(embedder=emb, backend=rc.StubBackend(), knowledge_base=kb, **stores)
+    for name, store in stores.items():  # empty drop-ins are truthy: the router keeps them (router.py:213-220)
+        assert getattr(router, name) is store
     cfg = rc.SimulationConfig(n_sessions=gold["n_sessions"], queries_per_session=gold["queries_per_session"],
                               seed=gold["seed"])
     logs = rc.run_simulation(cfg, router, rows)
@@ -156,7 +158,13 @@ def test_live_ab_against_reference_stores(gpu, rc, variant):
             kw = dict(kv_cache=g.FixedKVCache(**kv_kw),
                       semantic_cache=g.SemanticCache(emb, threshold=cfg.semantic_threshold, **sc_kw),
                       adaptive_memory=g.AdaptiveKnowledgeMemory(threshold=cfg.akm_threshold))
-        return rc.CascadeRouter(embedder=emb, backend=backend(), knowledge_base=kb, config=cfg, **kw)
+        r = rc.CascadeRouter(embedder=emb, backend=backend(), knowledge_base=kb, config=cfg, **kw)
+        # the reference injects with ``kv_cache or FixedKVCache()`` (router.py:213-220): its OWN
+        # empty stores are falsy and get replaced (dropping e.g. max_entries); pin the stores
+        # passed on both sides so the A/B compares exactly these stores
+        for name, store in kw.items():
+            setattr(r, name, store)
+        return r
 
     want = _sim_logs(rc, build("ref"), rows)
     got = _sim_logs(rc, build("gpu"), rows)
