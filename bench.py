@@ -275,6 +275,16 @@ def ref_search(X64: np.ndarray, q64: np.ndarray, k: int) -> np.ndarray:
     return F.topk_from_scores(np.concatenate(parts), k)
 
 
+def workload_config(a, world: int) -> dict:
+    """The workload both arms report (the driver compares the two lines' configs)."""
+    return {"workload": f"L5 retrieval top-k={a.k} over {a.n} x {a.dim} chunk store, batch {a.batch} "
+                        f"(BASELINE configs[3]); rows sharded over {world} GPU(s), all-gather merge",
+            "n_rows": a.n, "dim": a.dim, "batch": a.batch, "k": a.k,
+            "queries": "25% planted near-duplicates, 75% random unit vectors",
+            "l2": "inputs larger than L2 (int8 scan copy 1 B x rows x dim = 10 GB per step vs 126 MB L2); no flush",
+            "parallelism": f"rowshard{world}"}
+
+
 def run_reference(a):
     """--impl reference: the reference's CPU FlatIndex.search path (numpy einsum + lexsort,
     index.py:155-189, restated in oracle/flat_index.py) on this host's cores, on the SAME
@@ -330,8 +340,7 @@ def run_reference(a):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": a.gpus,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"L5 retrieval top-k={a.k} over {a.n} x {a.dim} chunk store, batch {a.batch}",
-                   "n_rows": a.n, "dim": a.dim, "batch": a.batch, "k": a.k},
+        "config": workload_config(a, a.gpus),
         "cpu_baseline": {"value": value, "unit": "queries/s", "cores": P, "kind": "port", "sample": sample,
                          "host_threads": threads, "cpu": cpu_model(), "numpy": np.__version__,
                          "rows_scanned": rows,
@@ -536,13 +545,7 @@ def main():
                             "bounds; every row that can reach the top-k is rescored in fp64 numpy-einsum order "
                             "(results bit-identical to the fp64 reference)",
             "data": "synthetic",
-            "config": {"workload": f"L5 retrieval top-k={a.k} over {a.n} x {a.dim} chunk store, batch {a.batch} "
-                                   f"(BASELINE configs[3]); rows sharded over {world} GPU(s), all-gather merge",
-                       "n_rows": a.n, "dim": a.dim, "batch": a.batch, "k": a.k,
-                       "queries": "25% planted near-duplicates, 75% random unit vectors",
-                       "l2": "inputs larger than L2 (int8 scan copy 1 B x rows x dim = 10 GB per step vs 126 MB "
-                             "L2); no flush",
-                       "parallelism": f"rowshard{world}"},
+            "config": workload_config(a, world),
             "e2e": {"value": round(e2e_value, 1), "unit": "queries/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
                     "path": "ShardedFlatIndex.search_batch from pinned host queries, results copied to host"},

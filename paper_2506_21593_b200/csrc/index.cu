@@ -995,6 +995,7 @@ static int search_impl(pr_index *h, const float *d_q, int64_t nq, int k, uint32_
         ts.x32 = h->x32;
         ts.store_map = &h->tmap8;
         ts.store_map_half = &h->tmap8h;
+        ts.x8_rows = h->cap256;
         ts.rows8 = h->r8;
         ts.n = h->count;
         ts.d = h->dim;

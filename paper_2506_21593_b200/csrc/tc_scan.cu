@@ -638,6 +638,27 @@ int choose_nsplit_waves(int64_t qtiles, int64_t ntiles) {
     return ntiles < 1 ? 1 : std::max(1, best);
 }
 
+// the same for work units of which `slots` run at once (clusters of several CTA pairs)
+int choose_nsplit_slots(int64_t units, int64_t ntiles, int slots) {
+    slots = std::max(1, slots);
+    int best = 1;
+    double best_eff = -1;
+    const int64_t lo = std::max<int64_t>(1, ceil_div<int64_t>(slots, units));
+    const int64_t hi = std::min<int64_t>(ntiles, std::max<int64_t>(lo, 8 * (int64_t)slots / std::max<int64_t>(1, units)));
+    for (int64_t ns = lo; ns <= std::max(lo, hi); ++ns) {
+        const int64_t tps = ceil_div<int64_t>(ntiles, ns);
+        const int64_t real_ns = ceil_div<int64_t>(ntiles, tps);
+        const int64_t waves = ceil_div<int64_t>(units * real_ns, slots);
+        const double eff = (double)(units * ntiles) / (double)(waves * slots * tps);
+        if (eff > best_eff + 1e-3) {
+            best_eff = eff;
+            best = (int)real_ns;
+        }
+        if (ns > lo && eff > 0.97) break;
+    }
+    return ntiles < 1 ? 1 : std::max(1, best);
+}
+
 static int choose_nsplit(int64_t qtiles, int64_t ntiles) {
     // persistent CTAs take items (qtile, split) round-robin: the busiest CTA owns
     // ceil(items / sms) items of tps tiles; pick the split count that minimises it

@@ -59,6 +59,7 @@ struct Tc8Search {
     const TcStoreMap *store_map;       // TMA map of rows8.x8, 256-row boxes (cta_group::1)
     const TcStoreMap *store_map_half;  // ... 128-row boxes (cta_group::2: each CTA loads half a tile)
     I8Rows rows8;
+    int64_t x8_rows = 0;  // rows of rows8.x8 (the TMA maps' extent)
     int64_t n;
     int d, dp8, dp128;
     const float *qp;  // padded fp32 queries [nq, dp8]
@@ -92,6 +93,7 @@ int tc_make_store_map(TcStoreMap *m, const __half *x16, int64_t rows, int dp64);
 int tc_search(TcSearch &s, Carve &cv, cudaStream_t st, pr_search_stats *stats);
 int make_map_2d(CUtensorMap *m, const void *base, int64_t rows, int cols, int elem_bytes, int box_cols, int box_rows);
 int choose_nsplit_waves(int64_t qtiles, int64_t ntiles);
+int choose_nsplit_slots(int64_t units, int64_t ntiles, int slots);
 // fp16 rounding + tensor-core accumulation error bound for unit vectors of dim d
 double tc_error_bound(int d, int dp64);
 

@@ -260,10 +260,12 @@ def test_i8_tiny_stores_and_odd_batches(gpu, rng, n, nq):
 
 
 @pytest.mark.parametrize("env", [{}, {"PR_I8_ARES": "0"}, {"PR_I8_CG": "1"}, {"PR_I8_REFINE": "0"},
-                                 {"PR_I8_PILOT_STRIDE": "4"}])
+                                 {"PR_I8_PILOT_STRIDE": "4"}, {"PR_I8_MC": "2"}, {"PR_I8_MC": "4"},
+                                 {"PR_I8_COARSE": "1"}])
 def test_i8_kernel_variants(gpu, rng, env, monkeypatch):
     """The scan variants behind the per-call knobs (streamed vs resident query tile,
-    single-CTA vs 2-CTA MMA, refiner off, a denser pilot) all give the oracle's answer."""
+    single-CTA vs 2-CTA MMA, refiner off, a denser pilot, 1 (default) / 2 / 4 CTA pairs per
+    multicast cluster, per-row instead of per-group fast-path bounds) all give the oracle's answer."""
     from paper_2506_21593_b200 import FlatIndex
 
     for key, val in env.items():
@@ -280,3 +282,20 @@ def test_i8_kernel_variants(gpu, rng, env, monkeypatch):
     idx.extend_arrays([f"e{i}" for i in range(n)], X)
     for k in (1, 10):
         _check(idx, X, Q, k, _mode())
+
+
+@pytest.mark.parametrize("mc", ["1", "2", "4"])
+@pytest.mark.parametrize("nq", [1, 255, 257, 700, 1500])
+def test_i8_multicast_cluster_padding(gpu, rng, mc, nq, monkeypatch):
+    """Query-group counts that do not fill the last multicast cluster: its spare pairs load
+    and multiply zero query tiles in lockstep and report nothing."""
+    from paper_2506_21593_b200 import FlatIndex
+
+    monkeypatch.setenv("PR_I8_MC", mc)
+    d, n = 384, 90001
+    X = _store(rng, n, d)
+    Q = random_unit_vectors(rng, nq, d)
+    Q[0] = X[77]
+    idx = FlatIndex(dim=d)
+    idx.extend_arrays([f"e{i}" for i in range(n)], X)
+    _check(idx, X, Q, 5, _mode())
