@@ -85,11 +85,16 @@ struct I8Cfg {
 // in-kernel exact refiner (warps 2-3): job table + per-query exact lists
 constexpr int I8_RQ = 256;
 constexpr size_t I8_REFINER_BYTES = (size_t)I8_RQ * 8 + (size_t)TC_BLOCK_M * TC_KP * 4 + (size_t)TC_BLOCK_M * 8 + 64;
+// per epilogue warp: queued (query, 8-row group) records awaiting evaluation (16 spill rows x
+// 32 ints = 64 records of 8 accumulators) and their {owner lane, chunk, group} tags
+constexpr int I8_QCAP = 64;
+constexpr size_t I8_QUEUE_BYTES = (size_t)I8_EPI_WARPS * I8_QCAP * 2;
 template <int CG, bool ARES = false>
 constexpr size_t i8_smem_bytes() {
     using Cf = I8Cfg<CG, ARES>;
     return 1024 + (size_t)Cf::A_RES_BYTES + (size_t)Cf::STAGES * (Cf::A_STAGE_BYTES + Cf::B_BYTES) +
-           2 * (size_t)I8_META_BYTES + (size_t)16 * I8_EPI * 4 + 256 + I8_REFINER_BYTES;
+           2 * (size_t)I8_META_BYTES + (size_t)16 * I8_EPI * 4 + 256 + I8_REFINER_BYTES +
+           I8_QUEUE_BYTES;
 }
 static_assert(i8_smem_bytes<2, true>() <= 232448, "A-resident 2-CTA scan exceeds the 227 KB smem limit");
 static_assert(i8_smem_bytes<2, false>() <= 232448, "2-CTA scan exceeds the 227 KB smem limit");
@@ -197,7 +202,6 @@ struct I8ScanParams {
     int cap;
     float thr_floor;  // measurement only: a floor under every bound (-inf normally)
     int noepi;        // measurement only: the epilogue releases each tile untouched
-    int coarse;       // fast path bounds 8-row groups by max(acc) * max(s_r) (PR_I8_COARSE=1; default per row)
     // pilot mode: scan store tiles idx * tile_stride only, keep the per-thread top-k of
     // l (no appends) and write it to pcand[((q * nsplit + split) * I8_HALVES + half) * TC_KP + i]
     int tile_stride;
@@ -213,6 +217,9 @@ struct I8ScanParams {
     int32_t *prog;  // [nsplit][qgroups]: tiles loaded + 1 (0 = not started, INT_MAX = done)
     int window;
     const int32_t *nq_dev;  // device query count (nullable): queries >= *nq_dev are skipped
+    // measurement only (PR_I8_VERBOSE): [0] warp-chunks that took the cooperative path,
+    // [1] warp-chunks, [2] flagged (query, 8-row group) pairs
+    uint32_t *dbg;
 };
 
 // the live query count of a search: the device count of a compacted list, else nq
@@ -296,6 +303,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
     int32_t *rcnt = rown + TC_BLOCK_M;                                    // [128] entries
     uint32_t *rq_tail = reinterpret_cast<uint32_t *>(rcnt + TC_BLOCK_M);
     uint32_t *epi_done = rq_tail + 1;
+    uint16_t *wqmeta = reinterpret_cast<uint16_t *>(reinterpret_cast<uint8_t *>(rq) + I8_REFINER_BYTES);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (!PILOT) {
@@ -500,7 +508,8 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
         const int ew = (warp - 4) & 3;                // TMEM lane group
         const int half = (warp - 4) >> 2;             // column slice of the tile
         const int et = ew * 32 + lane;                // TMEM lane == query within the tile
-        int32_t *wspill = spill + (warp - 4) * 32;  // this warp's columns of the [32][I8_EPI] spill
+        int32_t *wspill = spill + (warp - 4) * 32;  // this warp's columns of the [16][I8_EPI] spill: the queue
+        uint16_t *wq = wqmeta + (warp - 4) * I8_QCAP;  // queued records {owner lane, chunk, group}
         int tix = 0;
         // the MMA issuer waits on the leader's tempty: every epilogue warp of the pair arrives there
         const uint32_t tempty_leader0 = mapa_u32(smem_u32(&tempty[0]), leader);
@@ -531,6 +540,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
                 tr[i] = 0xFFFFFFFFu;
             }
             float Lpub = -INFINITY;
+            uint32_t n_coop = 0, n_chunks = 0, n_flag = 0;
             for (int i = 0; i < nloc; ++i, ++tix) {
                 const int acc = tix & 1;
                 const uint32_t aphase = (tix >> 1) & 1;
@@ -559,6 +569,74 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
                 float thr2 = PILOT ? loose_pilot(thr, inv, C) : loose_threshold(thr, inv, A, C, dxmax);
                 const int64_t rbase = (int64_t)(t0 + i) * p.tile_stride * TC_BLOCK_N;
                 const uint32_t taddr = tmem + ((uint32_t)(ew * 32) << 16) + acc * TC_BLOCK_N;
+                // Flagged (query, 8-row group) pairs are QUEUED (their 8 accumulators in this
+                // warp's spill rows, {owner lane, chunk, group} in wq) and evaluated after the
+                // accumulator is released, so the rare expensive groups do not hold TMEM while
+                // the next tile's MMAs wait for it.  The tile's row meta (ss, se) stays valid
+                // until mempty is released after the queue drains.
+                int qn = 0;
+                // evaluate the queue cooperatively: 4 records (32 rows) per pass, one row per lane,
+                // the owner lane's (query's) constants by shuffle
+                auto drain = [&]() {
+                    __syncwarp();
+#pragma unroll 1
+                    for (int base = 0; base < qn; base += 4) {
+                        const int r = base + (lane >> 3);
+                        bool act = r < qn;
+                        const int mt = act ? (int)wq[r] : 0;
+                        const int owner = mt & 31;
+                        const int j = ((mt >> 5) & 7) * 32 + ((mt >> 8) & 3) * 8 + (lane & 7);  // row in the tile
+                        const float o_t = __shfl_sync(0xffffffffu, tq_, owner);
+                        const float o_A = __shfl_sync(0xffffffffu, A, owner);
+                        const float o_C = __shfl_sync(0xffffffffu, C, owner);
+                        const float o_thr = __shfl_sync(0xffffffffu, thr, owner);
+                        const float o_kth = __shfl_sync(0xffffffffu, ts[TC_KP - 1], owner);
+                        const int64_t o_lim = __shfl_sync(0xffffffffu, lim, owner);
+                        const uint32_t row = (uint32_t)(rbase + j);
+                        act = act && (int64_t)row < o_lim;
+                        float l = -INFINITY;
+                        if (act) {
+                            const int e = r * 8 + (lane & 7);
+                            const float dx = se[j];
+                            const float ap =
+                                __fmul_rn(__fmul_rn(i2f_exact((uint32_t)wspill[(e >> 5) * I8_EPI + (e & 31)]), ss[j]), o_t);
+                            l = __fsub_rn(ap, __fmaf_rn(o_A, dx, o_C));
+                            if (!PILOT) {
+                                const float u = __fadd_rn(__fmaf_rn(o_A, dx, ap), o_C);
+                                if (u >= o_thr) {
+                                    const int64_t oq = (int64_t)qtile * TC_BLOCK_M + ew * 32 + owner;
+                                    const int o = atomicAdd(&p.acount[oq], 1);
+                                    if (o < p.cap) p.abuf[oq * (int64_t)p.cap + o] = make_uint2(row, __float_as_uint(u));
+                                    // approximate score at the bound: hand the row to the refiner
+                                    // (a full table just drops the job: the bound is a heuristic)
+                                    if (p.refine && ap >= o_thr) {
+                                        const uint32_t slot = atomicAdd(rq_tail, 1u) & (I8_RQ - 1);
+                                        atomicCAS(reinterpret_cast<unsigned long long *>(&rq[slot]), 0ull,
+                                                  ((unsigned long long)(oq + 1) << 32) | row);
+                                    }
+                                }
+                            }
+                        }
+                        // list inserts happen in the owner lane
+                        uint32_t wb = __ballot_sync(0xffffffffu, act && l > o_kth);
+                        while (wb) {
+                            const int src = __ffs(wb) - 1;
+                            wb &= wb - 1;
+                            const float lv = __shfl_sync(0xffffffffu, l, src);
+                            const uint32_t rv = __shfl_sync(0xffffffffu, row, src);
+                            const int ow = __shfl_sync(0xffffffffu, owner, src);
+                            if (lane == ow && lv > ts[TC_KP - 1]) {
+                                topk_insert(ts, tr, lv, rv);
+                                if (ts[TC_KP - 1] > thr) {
+                                    thr = ts[TC_KP - 1];
+                                    thr2 = PILOT ? loose_pilot(thr, inv, C) : loose_threshold(thr, inv, A, C, dxmax);
+                                }
+                            }
+                        }
+                    }
+                    qn = 0;
+                    __syncwarp();
+                };
                 uint32_t va[32], vb[32];
                 TMEM_LD32(taddr + half * I8_CPW * 32, va);
                 tmem_wait_ld();
@@ -574,26 +652,9 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
                         } else if (cp + 1 < I8_CPW / 2) {
                             TMEM_LD32(taddr + (c + 1) * 32, va);
                         }
-                        // fast path, per 8-row group: an upper bound on max_r s_r * acc_r.
-                        //   coarse: max(max_r acc_r, 0) * max_r s_r (the tile meta's
-                        //   per-group max scale) — one integer max per score; rounding is
-                        //   monotone, so it bounds every row's fl(s_r * acc_r) from above
-                        //   default: the per-row products (four ops per score; fewer groups flagged)
-                        float gm[4];
-                        if (p.coarse) {
-                            const float4 sg = *reinterpret_cast<const float4 *>(tm->gmax + c * 4);
-                            const float sgv[4] = {sg.x, sg.y, sg.z, sg.w};
-#pragma unroll
-                            for (int g = 0; g < 4; ++g) {
-                                int32_t m0 = max((int32_t)v[8 * g + 0], (int32_t)v[8 * g + 1]);
-                                int32_t m1 = max((int32_t)v[8 * g + 2], (int32_t)v[8 * g + 3]);
-                                int32_t m2 = max((int32_t)v[8 * g + 4], (int32_t)v[8 * g + 5]);
-                                int32_t m3 = max((int32_t)v[8 * g + 6], (int32_t)v[8 * g + 7]);
-                                const int32_t m = max(max(max(m0, m1), max(m2, m3)), 0);
-                                gm[g] = __fmul_rn(i2f_exact((uint32_t)m), sgv[g]);
-                            }
-                        } else {
+                        // fast path: per 8-row group, max of s_r * acc (exact int -> fp32)
                         const float4 *s4 = reinterpret_cast<const float4 *>(ss + c * 32);
+                        float gm[4];
 #pragma unroll
                         for (int g = 0; g < 4; ++g) {
                             const float4 sa = s4[2 * g], sb = s4[2 * g + 1];
@@ -607,97 +668,43 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
                             m1 = fmaxf(m1, __fmul_rn(i2f_exact(v[8 * g + 7]), sb.w));
                             gm[g] = fmaxf(m0, m1);
                         }
-                        }
                         const int64_t rb = rbase + c * 32;
                         uint32_t gmask = 0;
 #pragma unroll
                         for (int g = 0; g < 4; ++g) gmask |= (gm[g] >= thr2 ? 1u : 0u) << g;
                         if (rb >= lim) gmask = 0;
-                        // rare: the warp evaluates every flagged (query, 8-row group) pair
-                        // cooperatively, 4 pairs (32 rows) per pass, one row per lane
+                        if (p.dbg) {
+                            ++n_chunks;
+                            n_flag += __popc(gmask);
+                        }
                         if (__any_sync(0xffffffffu, gmask != 0)) {
-                            const float kth = ts[TC_KP - 1];
-                            // two passes of 16 rows (groups {0,1}, then {2,3}) through a 16-row spill
+                            if (p.dbg) ++n_coop;
+                            uint32_t bg[4];
 #pragma unroll
-                            for (int hh = 0; hh < 2; ++hh) {
-                                const uint32_t bA = __ballot_sync(0xffffffffu, (gmask >> (2 * hh)) & 1u);
-                                const uint32_t bB = __ballot_sync(0xffffffffu, (gmask >> (2 * hh + 1)) & 1u);
-                                if (!(bA | bB)) continue;
-                                // spill only the groups some lane flagged (warp-uniform branches)
-                                if (bA) {
+                            for (int g = 0; g < 4; ++g) bg[g] = __ballot_sync(0xffffffffu, (gmask >> g) & 1u);
+                            const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
-                                    for (int j = 0; j < 8; ++j) wspill[j * I8_EPI + lane] = (int32_t)v[16 * hh + j];
-                                }
-                                if (bB) {
+                            for (int g = 0; g < 4; ++g) {
+                                // groups {0,1} then {2,3}: at most 64 records each; a full queue is
+                                // evaluated first, while TMEM is still held (rare: cold bounds)
+                                if ((g & 1) == 0 && qn + __popc(bg[g]) + __popc(bg[g + 1]) > I8_QCAP) drain();
+                                if (!bg[g]) continue;
+                                if ((gmask >> g) & 1u) {
+                                    const int r = qn + __popc(bg[g] & lt);
 #pragma unroll
-                                    for (int j = 8; j < 16; ++j) wspill[j * I8_EPI + lane] = (int32_t)v[16 * hh + j];
-                                }
-                                const int p1 = __popc(bA);
-                                const int npairs = p1 + __popc(bB);
-                                __syncwarp();
-#pragma unroll 1
-                                for (int base = 0; base < npairs; base += 4) {
-                                    const int pi = base + (lane >> 3);
-                                    bool act = pi < npairs;
-                                    const int gl = pi >= p1 ? 1 : 0;
-                                    const int owner = act ? nth_set_bit(gl ? bB : bA, pi - (gl ? p1 : 0)) : 0;
-                                    const float o_t = __shfl_sync(0xffffffffu, tq_, owner);
-                                    const float o_A = __shfl_sync(0xffffffffu, A, owner);
-                                    const float o_C = __shfl_sync(0xffffffffu, C, owner);
-                                    const float o_thr = __shfl_sync(0xffffffffu, thr, owner);
-                                    const float o_kth = __shfl_sync(0xffffffffu, kth, owner);
-                                    const int64_t o_lim = __shfl_sync(0xffffffffu, lim, owner);
-                                    const int jl = 8 * gl + (lane & 7);  // row within this 16-row pass
-                                    const int j = 16 * hh + jl;          // row within the chunk
-                                    const uint32_t row = (uint32_t)(rb + j);
-                                    act = act && (int64_t)row < o_lim;
-                                    float l = -INFINITY;
-                                    if (act) {
-                                        const float dx = se[c * 32 + j];
-                                        const float ap = __fmul_rn(
-                                            __fmul_rn(i2f_exact(wspill[jl * I8_EPI + owner]), ss[c * 32 + j]), o_t);
-                                        l = __fsub_rn(ap, __fmaf_rn(o_A, dx, o_C));
-                                        if (!PILOT) {
-                                            const float u = __fadd_rn(__fmaf_rn(o_A, dx, ap), o_C);
-                                            if (u >= o_thr) {
-                                                const int64_t oq = (int64_t)qtile * TC_BLOCK_M + ew * 32 + owner;
-                                                const int o = atomicAdd(&p.acount[oq], 1);
-                                                if (o < p.cap)
-                                                    p.abuf[oq * (int64_t)p.cap + o] = make_uint2(row, __float_as_uint(u));
-                                                // approximate score at the bound: hand the row to the refiner
-                                                // (a full table just drops the job: the bound is a heuristic)
-                                                if (p.refine && ap >= o_thr) {
-                                                    const uint32_t slot = atomicAdd(rq_tail, 1u) & (I8_RQ - 1);
-                                                    atomicCAS(reinterpret_cast<unsigned long long *>(&rq[slot]), 0ull,
-                                                              ((unsigned long long)(oq + 1) << 32) | row);
-                                                }
-                                            }
-                                        }
+                                    for (int x = 0; x < 8; ++x) {
+                                        const int e = r * 8 + x;
+                                        wspill[(e >> 5) * I8_EPI + (e & 31)] = (int32_t)v[8 * g + x];
                                     }
-                                    // list inserts happen in the owner lane (rare)
-                                    uint32_t wb = __ballot_sync(0xffffffffu, act && l > o_kth);
-                                    while (wb) {
-                                        const int src = __ffs(wb) - 1;
-                                        wb &= wb - 1;
-                                        const float lv = __shfl_sync(0xffffffffu, l, src);
-                                        const uint32_t rv = __shfl_sync(0xffffffffu, row, src);
-                                        const int ow = __shfl_sync(0xffffffffu, owner, src);
-                                        if (lane == ow && lv > ts[TC_KP - 1]) {
-                                            topk_insert(ts, tr, lv, rv);
-                                            if (ts[TC_KP - 1] > thr) {
-                                                thr = ts[TC_KP - 1];
-                                                thr2 = PILOT ? loose_pilot(thr, inv, C)
-                                                             : loose_threshold(thr, inv, A, C, dxmax);
-                                            }
-                                        }
-                                    }
+                                    wq[r] = (uint16_t)(lane | (c << 5) | (g << 8));
                                 }
-                                __syncwarp();
+                                qn += __popc(bg[g]);
                             }
                         }
                         if (h == 0 || cp + 1 < I8_CPW / 2) tmem_wait_ld();
                     }
                 }
+                // release the accumulator, then evaluate the queued groups
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) {
@@ -705,11 +712,20 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
                         mbar_arrive_cluster(tempty_leader0 + acc * 8);
                     else
                         mbar_arrive(&tempty[acc]);
-                    mbar_arrive(&mempty[acc]);
                 }
+                if (qn) drain();
+                if (lane == 0) mbar_arrive(&mempty[acc]);
                 if (valid && ts[TC_KP - 1] > Lpub) {
                     Lpub = ts[TC_KP - 1];
                     atomicMax(lgq, f2ord(Lpub));
+                }
+            }
+            if (p.dbg) {
+                n_flag = __reduce_add_sync(0xffffffffu, n_flag);
+                if (lane == 0) {
+                    atomicAdd(&p.dbg[0], n_coop);
+                    atomicAdd(&p.dbg[1], n_chunks);
+                    atomicAdd(&p.dbg[2], n_flag);
                 }
             }
             if (PILOT && valid) {
@@ -1413,10 +1429,6 @@ int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats)
     const unsigned wgrid = (unsigned)std::max<int64_t>(
         1, std::min<int64_t>(ceil_div<int64_t>(s.nq, W8_WARPS), (int64_t)sm_count() * 8));
 
-    // 1: per-group fast-path bounds (measured slower: 34.5 vs 31.8 ms at C4 — the looser
-    // bound sends more 8-row groups to the cooperative evaluation)
-    const char *coarse_env = getenv("PR_I8_COARSE");
-    const int coarse = coarse_env && coarse_env[0] == '1';
     // 1) pilot over a tile subsample -> exact seeds and a first bound per query
     const int psplit = pilot_splits(qtiles_hint, ntiles);
     int32_t *seed_rows = nullptr, *seed_n = nullptr;
@@ -1429,7 +1441,7 @@ int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats)
         seed_n = cv.take<int32_t>((size_t)s.nq);
         I8ScanParams pp{s.n, s.dp128 / I8_BLOCK_K, psplit, (int)ceil_div<int64_t>(ptiles, psplit), (int)ptiles,
                         (int)qtiles, s.k, s.rows8.xs, s.rows8.xe, s.rows8.xt, qmeta, s.row_limit, s.nq, lg, acount,
-                        abuf, cap, floor_thr, 0, coarse, I8_PILOT_STRIDE, pcand, s.x32, s.qp, s.dp8, s.d, 0, nullptr, 0, s.nq_dev};
+                        abuf, cap, floor_thr, 0, I8_PILOT_STRIDE, pcand, s.x32, s.qp, s.dp8, s.d, 0, nullptr, 0, s.nq_dev};
         rc = launch_scan8_cg<true>(cg, ares, (s.nq_dev ? qtiles_hint : qtiles) * psplit, qmap.map, xmap,
                                    pp, st);
         if (rc) return rc;
@@ -1440,7 +1452,7 @@ int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats)
     }
     // 2) main scan: append every row whose upper bound reaches the running bound
     I8ScanParams p{s.n, s.dp128 / I8_BLOCK_K, nsplit, tps, (int)ntiles, (int)qtiles, s.k, s.rows8.xs, s.rows8.xe,
-                   s.rows8.xt, qmeta, s.row_limit, s.nq, lg, acount, abuf, cap, floor_thr, 0, coarse, 1, nullptr, s.x32, s.qp,
+                   s.rows8.xt, qmeta, s.row_limit, s.nq, lg, acount, abuf, cap, floor_thr, 0, 1, nullptr, s.x32, s.qp,
                    s.dp8, s.d, 1, nullptr, 0, s.nq_dev};
     {
         const char *w_env = getenv("PR_I8_WINDOW");  // tiles a pair may run ahead of its split (0 = off)
@@ -1456,6 +1468,11 @@ int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats)
     p.refine = !(ref_env && ref_env[0] == '0');
     const char *noepi_env = getenv("PR_I8_NOEPI");  // 1: epilogue does nothing (results invalid): MMA/TMA timing
     if (noepi_env && noepi_env[0] >= '1') p.noepi = noepi_env[0] - '0';  // 2: also skip operand loads
+    const bool verbose = getenv("PR_I8_VERBOSE") != nullptr;
+    if (verbose) {
+        p.dbg = cv.take<uint32_t>(4);
+        PR_CUDA(cudaMemsetAsync(p.dbg, 0, 16, st));
+    }
     if (s.ev_begin) PR_CUDA(cudaEventRecord(s.ev_begin, st));
     if (mc > 1) {
         const int64_t units = ceil_div<int64_t>(s.nq_dev ? qtiles_hint : qtiles, 2 * mc);
@@ -1466,6 +1483,13 @@ int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats)
     }
     if (rc) return rc;
     if (s.ev_end) PR_CUDA(cudaEventRecord(s.ev_end, st));
+    if (verbose) {  // measurement only: synchronises the stream
+        uint32_t h[4];
+        PR_CUDA(cudaMemcpyAsync(h, p.dbg, 16, cudaMemcpyDeviceToHost, st));
+        PR_CUDA(cudaStreamSynchronize(st));
+        fprintf(stderr, "tc8_search: cooperative warp-chunks %u of %u (%.4f), flagged groups %u (%.2f per query)\n", h[0],
+                h[1], h[1] ? (double)h[0] / h[1] : 0.0, h[2], (double)h[2] / std::max<int64_t>(1, s.nq));
+    }
     // 3) exact rescoring of the complete candidate set
     I8PostArgs pa{acount, abuf, cap, s.nq, s.k, std::min<int64_t>(s.k, s.n), s.row_limit, s.x32, s.dp8, s.d, s.qp,
                   seed_rows, seed_s, seed_n, s.rows, s.raw, s.rep, s.count, s.counters, s.fallback_list, s.nq_dev};

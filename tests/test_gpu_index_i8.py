@@ -260,12 +260,11 @@ def test_i8_tiny_stores_and_odd_batches(gpu, rng, n, nq):
 
 
 @pytest.mark.parametrize("env", [{}, {"PR_I8_ARES": "0"}, {"PR_I8_CG": "1"}, {"PR_I8_REFINE": "0"},
-                                 {"PR_I8_PILOT_STRIDE": "4"}, {"PR_I8_MC": "2"}, {"PR_I8_MC": "4"},
-                                 {"PR_I8_COARSE": "1"}])
+                                 {"PR_I8_PILOT_STRIDE": "4"}, {"PR_I8_MC": "2"}, {"PR_I8_MC": "4"}])
 def test_i8_kernel_variants(gpu, rng, env, monkeypatch):
     """The scan variants behind the per-call knobs (streamed vs resident query tile,
     single-CTA vs 2-CTA MMA, refiner off, a denser pilot, 1 (default) / 2 / 4 CTA pairs per
-    multicast cluster, per-row instead of per-group fast-path bounds) all give the oracle's answer."""
+    multicast cluster) all give the oracle's answer."""
     from paper_2506_21593_b200 import FlatIndex
 
     for key, val in env.items():
