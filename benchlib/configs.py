@@ -462,6 +462,7 @@ def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_se
     e0, e1 = _events()
     torch.cuda.synchronize()
     e0.record()
+    torch.cuda.nvtx.range_push("c5_timed")  # ncu --nvtx-include c5_timed/ (launch lists of the replay only)
     if workers == 1:
         replay(0)
     else:
@@ -473,6 +474,7 @@ def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_se
     for st_w in streams_w:
         torch.cuda.current_stream().wait_stream(st_w)
     e1.record()
+    torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     gc.callbacks.remove(_gc_timer)

@@ -181,3 +181,27 @@ def stream_ptr(stream=None) -> int:
 
 def ptr(t) -> int:
     return 0 if t is None else int(t.data_ptr())
+
+
+def h2d(x, dtype=None):
+    """Host array / CPU tensor -> device tensor WITHOUT blocking the host on queued device
+    work: staged through the process-wide pinned ring (pinned.py) and copied on the
+    current stream.  A pageable source makes the copy synchronous, which stalls a
+    pipelined route_batch behind the next span's knowledge-base scan; a fresh pinned
+    allocation per call costs milliseconds.  Device tensors pass through."""
+    import numpy as np
+    import torch
+
+    from . import pinned
+
+    if isinstance(x, torch.Tensor):
+        if x.is_cuda:
+            return x if dtype is None or x.dtype == dtype else x.to(dtype)
+        x = x.numpy()
+    a = np.asarray(x)
+    if dtype is not None:
+        a = a.astype(pinned._NUMPY_OF[dtype], copy=False)
+    r = pinned.ring()
+    if a.nbytes <= r.cap // 8:
+        return r.h2d(a)
+    return torch.from_numpy(np.ascontiguousarray(a)).pin_memory().to("cuda", non_blocking=True)

@@ -49,7 +49,7 @@ import time
 
 import numpy as np
 
-from . import _lib, generation
+from . import _lib, generation, pinned
 from .caches import FixedKVCache, SemanticCache
 from .errors import CascadeError
 from .index import MODE_AUTO, FlatIndex
@@ -263,6 +263,7 @@ def _launch(router, queries, vectors, start: int, end: int, mode: int, prev: "_S
     kv, sc, akm, kb = router.kv_cache, router.semantic_cache, router.adaptive_memory, router.knowledge_base
     sp = _Span()
     sp.t_start = time.perf_counter_ns()
+    prof = _Prof(getattr(router, "profile_batches", False))
     sp.start, sp.end = start, end
     qs = queries[start:end]
     B = sp.size = sp.B = len(qs)
@@ -272,6 +273,7 @@ def _launch(router, queries, vectors, start: int, end: int, mode: int, prev: "_S
     arena = sp.arena = to_device(texts)  # one device UTF-8 arena: embedding, L1 probe, KV write-back
     Vd = _embed(router, texts, None if vectors is None else vectors[start:end], arena)
     s = _lib.stream_ptr()
+    prof.mark("L.embed")
     dev = "cuda"
 
     # ---- window dedupe (host, texts only): an earlier write of the same text in this span
@@ -296,16 +298,17 @@ def _launch(router, queries, vectors, start: int, end: int, mode: int, prev: "_S
                           dtype=np.int64)
     sp.new_js = new_js
     if new_js.size:
-        sc_index.extend_arrays([texts[j] for j in new_js], Vd[torch.from_numpy(new_js).to(dev)],
+        sc_index.extend_arrays([texts[j] for j in new_js], Vd[_lib.h2d(new_js)],
                                payloads=[None] * int(new_js.size), validate=False)
     sc_limit = n_pre_sc + np.searchsorted(new_js, ar, side="left")  # rows written by queries i < j
+    prof.mark("L.dedupe+sc_extend")
 
     # ---- L1 probe, L2 top-1, gate + miss-list compaction: all on the device
     u8, i64 = torch.uint8, torch.int64
     kv_hit = kv_val = None
     if L1 in pos:
         kv_val, kv_hit = kv.probe_device(arena[0], arena[1], B)
-    rep_d = torch.from_numpy(rep.astype(np.uint8)).to(dev, non_blocking=True)
+    rep_d = _lib.h2d(rep.astype(np.uint8))
     r2 = None
     if L2 in pos:
         r2 = sc_index.search_batch(Vd, 1, mode=mode, validate=False, row_limit=sc_limit, count=False)
@@ -322,6 +325,7 @@ def _launch(router, queries, vectors, start: int, end: int, mode: int, prev: "_S
                                  int(L2 in pos and pos[L2] < vec_pos), _lib.ptr(l1_d), _lib.ptr(l2_d), _lib.ptr(lst),
                                  _lib.ptr(nlist), _lib.ptr(slot), s), "cascade_gate")
 
+    prof.mark("L.l1l2gate")
     # ---- L5: the knowledge-base scan of the listed queries only
     sk = cfg.akm_seed_k
     kbi = kb.index
@@ -335,6 +339,7 @@ def _launch(router, queries, vectors, start: int, end: int, mode: int, prev: "_S
                                           None, _lib.ptr(kb_rows), _lib.ptr(kb_raw), _lib.ptr(kb_rep),
                                           _lib.ptr(kb_cnt), s), "search_list")
     sp.kb_rows_d, sp.kb_cnt_d, sp.nlist_d = kb_rows, kb_cnt, nlist
+    prof.mark("L.kb")
 
     # ---- L4 guard: the AKM as it is now, and the superset of seeds settled before each query
     l4 = torch.zeros(B, dtype=torch.bool, device=dev)
@@ -363,17 +368,16 @@ def _launch(router, queries, vectors, start: int, end: int, mode: int, prev: "_S
         l4 |= (rs.count > 0) & (rs.scores[:, 0] >= thr)
         l4 &= slot >= 0
 
+    prof.mark("L.l4guard")
     # ---- the span's one read-back: outcomes + the listed queries' KB rows
     cols = [l1_d.to(i64), l2_d.to(i64), slot.to(i64), l4.to(i64),
             (r2.rows[:, 0] if r2 is not None else torch.full((B,), -1, dtype=i64, device=dev)),
             (kv_val if kv_val is not None else torch.full((B,), -1, dtype=i64, device=dev)),
             kb_cnt.to(i64), nlist.to(i64)]
     packed = torch.cat([c.reshape(-1) for c in cols] + [kb_rows.reshape(-1)])
-    host = torch.empty(packed.shape, dtype=i64, pin_memory=True)
-    host.copy_(packed, non_blocking=True)
-    ev = torch.cuda.Event()
-    ev.record()
-    sp.host, sp.event = host, ev
+    sp.host, sp.event = pinned.ring().d2h(packed)
+    prof.mark("L.pack")
+    prof.merge_into(router)
     return sp
 
 
@@ -386,7 +390,7 @@ def _discard(router, sp: _Span) -> None:
 
 def _unpack(sp: _Span, sk: int):
     sp.event.synchronize()
-    h = sp.host.numpy()
+    h = sp.host.copy()  # out of the pinned ring: the ledger keeps views of it
     B = sp.B
     l1, l2, slot, l4, sc_row, kv_val, kb_cnt = (h[i * B:(i + 1) * B] for i in range(7))
     nl = int(h[7 * B])
@@ -633,6 +637,15 @@ class _Prof:
         self.enabled = enabled
         self.times: dict[str, float] = {}
         self._t = time.perf_counter()
+
+    def merge_into(self, router) -> None:
+        if not self.enabled:
+            return
+        hist = getattr(router, "batch_profile", None)
+        if hist is None:
+            hist = router.batch_profile = {}
+        for k, v in self.times.items():
+            hist[k] = hist.get(k, 0.0) + v
 
     def mark(self, name: str) -> None:
         if not self.enabled:

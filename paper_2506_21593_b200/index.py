@@ -234,7 +234,7 @@ class FlatIndex:
         """Append rows copied from ``src`` without ids or payloads (scratch stores that
         are only searched, never looked up by id)."""
         torch = _torch()
-        r = torch.as_tensor(src_rows, dtype=torch.int64).to("cuda").contiguous()
+        r = _lib.h2d(src_rows, torch.int64)
         with self._lock:
             _lib.check(
                 self._L.pr_index_append_from(self._h, src.handle, _lib.ptr(r), r.numel(), _lib.stream_ptr()),
@@ -249,7 +249,7 @@ class FlatIndex:
         the source row's, read from ``src`` on first access."""
         torch = _torch()
         rows = np.asarray(src_rows, dtype=np.int64)
-        r = torch.from_numpy(rows).to("cuda")
+        r = _lib.h2d(rows)
         with self._lock:
             base = len(self._ids)
             _lib.check(
@@ -312,7 +312,7 @@ class FlatIndex:
         q = torch.as_tensor(queries, dtype=torch.float32)
         if q.dim() != 2 or q.shape[1] != self._dim:
             raise InvalidVector(f"expected [B, {self._dim}] queries, got {tuple(q.shape)}")
-        q = q.to("cuda", non_blocking=True).contiguous()
+        q = _lib.h2d(q).contiguous()
         B = q.shape[0]
         if validate and B:
             check_unit(q, INDEX_NORM_TOLERANCE)
@@ -325,7 +325,7 @@ class FlatIndex:
             )
         lim = None
         if row_limit is not None:
-            lim = torch.as_tensor(row_limit, dtype=torch.int64).to("cuda").contiguous()
+            lim = _lib.h2d(row_limit, torch.int64).contiguous()
             if lim.shape != (B,):
                 raise ValueError("row_limit must have one entry per query")
         with self._lock:

@@ -41,8 +41,7 @@ class DeviceTexts(tuple):
 
 
 def to_device(texts: Sequence[str]) -> DeviceTexts:
-    import torch
+    from ._lib import h2d
 
     data, off = encode_texts(texts)
-    return DeviceTexts(torch.from_numpy(data).cuda(non_blocking=True), torch.from_numpy(off).cuda(non_blocking=True),
-                       off)
+    return DeviceTexts(h2d(data), h2d(off), off)
