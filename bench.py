@@ -63,8 +63,9 @@ def parse():
     ap.add_argument("--configs", default="c2,c3,c4sweep,c5",
                     help="secondary BASELINE configs measured after the headline (rank 0, N=1): c2,c3,c4sweep,c5 or ''")
     ap.add_argument("--kv-keys", type=int, default=100_000_000)
-    ap.add_argument("--c5-queries", type=int, default=20_000, help="queries per C5 session")
-    ap.add_argument("--c5-sessions", type=int, default=4)
+    ap.add_argument("--c5-queries", type=int, default=111_112,
+                    help="queries per C5 session (configs[4]: nine sessions, 1M queries)")
+    ap.add_argument("--c5-sessions", type=int, default=9)
     ap.add_argument("--c5-workers", type=int, default=1,
                     help="C5 sessions replayed concurrently (one router per worker, shared knowledge base)")
     return ap.parse_args()

@@ -181,7 +181,7 @@ def _kv_get(L, h, b, out, hit, stream):
                      _lib.ptr(hit), stream)
 
 
-def c3_kv(hbm_gbs: float, n_keys=100_000_000, batch=65536, n_batches=32, steps=5, chunk=8_000_000, streams=4):
+def c3_kv(hbm_gbs: float, n_keys=100_000_000, batch=65536, n_batches=32, steps=5, chunk=8_000_000, streams=8):
     """C3: byte-exact fixed-KV lookups (pr_kv_get_text: hash + probe + record confirm) over a
     100M-key table, batches of 65536.  The batch stream is replayed as one CUDA graph whose
     batches run on ``streams`` concurrent branches (independent request batches in flight at
@@ -534,9 +534,9 @@ def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_se
         _LAST_PROFILE_LOG[:] = getattr(router, "batch_profile_log", [])
     return {
         "workload": f"five-layer routed replay (L1/L2/L3/L4/L5, LLM stubbed) over a {n_store} x 1024 KB "
-                    f"({n_qa} HashEmbedder contexts + dense distractors), {n_sessions} warm-up sessions x "
-                    f"{queries_per_session} queries, batch {batch} (configs[4] shape, 1 GPU), "
-                    f"{workers} concurrent session worker(s)",
+                    f"({n_qa} HashEmbedder contexts + dense distractors), {n_sessions} cache-warming sessions x "
+                    f"{queries_per_session} queries = {n_sessions * queries_per_session} routed queries, spans of "
+                    f"{batch} (configs[4], 1 GPU), {workers} concurrent session worker(s)",
         "value": total / (ms / 1e3), "unit": "routed queries/s", "ms_total": ms, "workers": workers,
         "layer_counts": layer_counts, "queries_routed_sequentially": seq_total,
         "spans": sum(t.get("spans", 0) for t in tallies), "spans_pipelined": sum(t.get("pipelined", 0) for t in tallies),

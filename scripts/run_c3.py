@@ -12,6 +12,6 @@ prev = ctypes.c_int()
 _lib.check(_lib.load().pr_l2_fetch_granularity(int(os.environ.get("PR_L2FETCH", "0")), ctypes.byref(prev)))
 now = ctypes.c_int()
 _lib.check(_lib.load().pr_l2_fetch_granularity(0, ctypes.byref(now)))
-r = C.c3_kv(6539.2, streams=int(os.environ.get("C3_STREAMS", "4")))
+r = C.c3_kv(6539.2, streams=int(os.environ.get("C3_STREAMS", "8")))
 r["l2_fetch_granularity"] = {"before": prev.value, "used": now.value}
 print(json.dumps(r))
