@@ -60,8 +60,9 @@ def parse():
     ap.add_argument("--k", type=int, default=5)
     ap.add_argument("--cpu-queries", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--configs", default="c2,c3,c4sweep,c5",
-                    help="secondary BASELINE configs measured after the headline (rank 0, N=1): c2,c3,c4sweep,c5 or ''")
+    ap.add_argument("--configs", default="c1,c2,c3,c4sweep,c5",
+                    help="secondary BASELINE configs measured after the headline (rank 0, N=1): "
+                         "c1,c2,c3,c4sweep,c5 or '' (c1 includes the reference router's CPU timing; c1gpu without)")
     ap.add_argument("--kv-keys", type=int, default=100_000_000)
     ap.add_argument("--c5-queries", type=int, default=111_112,
                     help="queries per C5 session (configs[4]: nine sessions, 1M queries)")
@@ -522,7 +523,9 @@ def main():
         wanted = [c.strip() for c in a.configs.split(",") if c.strip()]
         for name in wanted:
             try:
-                if name == "c2":
+                if name in ("c1", "c1gpu"):
+                    configs["c1_simulation"] = C.c1_routed(reference=name == "c1")
+                elif name == "c2":
                     configs["c2_semantic_cache"] = C.c2_semantic(peak, p8["how"])
                 elif name == "c3":
                     configs["c3_fixed_kv"] = C.c3_kv(float(pk.get("hbm_gbs", 6538.6)), n_keys=a.kv_keys)

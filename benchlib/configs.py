@@ -577,3 +577,85 @@ def _c5_l5_oracle(kb, emb, texts, k=10, chunk=1 << 20):
         bad_rows += int(not np.array_equal(wr, rows[q, :wr.size]))
         bad_scores += int(not np.array_equal(ws, raw[q, :ws.size]))
     return {"queries": len(texts), "k": k, "row_mismatches": bad_rows, "raw_score_mismatches": bad_scores}
+
+
+def c1_routed(reference: bool = True, procs: int = 9, batch: int = 4096, reps: int = 3):
+    """C1 (BASELINE configs[0]): the reference's nine-session cache-warming simulation —
+    KB = dataset_to_corpus(synthetic_qa_dataset(100_000, 42)) at dim 384, Q/A pool = its first
+    10k rows, SimulationConfig(9, 1000, seed=0) (simulation.py:268-314) — routed by
+    ``route_batch`` over GPU stores.  ``value`` = routed queries/s of the whole simulation
+    (``simulate_batched``: session logs materialised as JSONL, the reference's output),
+    median of ``reps`` runs; parity = every session's lines byte-identical to the real
+    reference's (fixture tests/golden/c1_sessions.json.gz, written by tests/golden/make_c1.py).
+
+    ``reference``: the REAL reference router (baseline/_ref) on this host's cores, one process
+    per session (sessions are independent; BASELINE.md §3 mode ii) — the C1
+    CPU baseline; each process also checks its session's lines against the fixture."""
+    import gzip
+    import hashlib
+    import json
+    import os
+
+    import torch
+
+    from benchlib.workloads import corpus_of, qa_rows, simulate_batched
+    from paper_2506_21593_b200 import CascadeRouter, HashEmbedder, StubBackend, ingest_corpus
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with gzip.open(os.path.join(root, "tests", "golden", "c1_sessions.json.gz"), "rt") as fh:
+        fx = json.load(fh)
+    cfg = fx["config"]
+    t0 = time.perf_counter()
+    rows = qa_rows(cfg["kb_rows"], seed=cfg["dataset_seed"])
+    emb = HashEmbedder(dim=cfg["dim"])
+    kb = ingest_corpus((json.dumps(c) for c in corpus_of(rows)), emb)
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    questions = [r["question"] for r in rows[:cfg["qa_rows"]]]
+    n_s, n_q = cfg["n_sessions"], cfg["queries_per_session"]
+    router = CascadeRouter(embedder=emb, backend=StubBackend(), knowledge_base=kb)
+    simulate_batched(router, questions, n_sessions=2, n_queries=n_q, seed=cfg["seed"] + 1000, batch=batch)  # warm-up
+    times, logs = [], None
+    for _ in range(reps):
+        router = CascadeRouter(embedder=emb, backend=StubBackend(), knowledge_base=kb)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        logs = simulate_batched(router, questions, n_sessions=n_s, n_queries=n_q, seed=cfg["seed"], batch=batch)
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+    digests = [hashlib.sha256("\n".join(s).encode()).hexdigest() for s in logs]
+    sec = float(np.median(times))
+    out = {
+        "workload": f"C1 (configs[0]): reference nine-session cache-warming simulation, {cfg['kb_rows']} chunks x "
+                    f"dim {cfg['dim']}, {n_s} sessions x {n_q} queries, route_batch spans of {batch} (1 GPU)",
+        "value": n_s * n_q / sec, "unit": "routed queries/s", "seconds": sec, "runs": times,
+        "timed": "simulate_batched: validate + route_batch + JSONL session logs, wall clock, after a warm-up",
+        "kb_build_seconds": build_s,
+        "layer_counts": {k: int(v) for k, v in router.stats()["layer_counts"].items() if v},
+        "parity": {"sessions": n_s, "sessions_identical": int(sum(d == w for d, w in zip(digests, fx["sha256"]))),
+                   "oracle": "real reference run_simulation session logs (sha256 per session, fixture)"},
+    }
+    if reference:
+        try:
+            from oracle import ref_c1 as R
+
+            R.load_reference()
+        except ImportError as exc:
+            out["cpu_baseline"] = {"unavailable": f"reference not importable: {exc}"}
+            return out
+        sess = list(range(n_s))
+        got, secs, wall = R.run_sessions_parallel(sess, n_q, procs=min(procs, n_s))
+        route_max = max(secs.values())
+        same = sum(hashlib.sha256("\n".join(got[s]).encode()).hexdigest() == fx["sha256"][s] for s in sess)
+        out["cpu_baseline"] = {
+            "value": n_s * n_q / route_max, "unit": "routed queries/s", "cores": min(procs, n_s), "kind": "reference",
+            "sample": f"the full C1 simulation: {n_s} sessions, one process per session running the unmodified "
+                      "reference router (baseline/_ref ragcascade, dim shim SURVEY §0.5); value = queries / the "
+                      "slowest session's routing time (KB ingest per process not counted)",
+            "route_seconds": {str(k): v for k, v in secs.items()}, "wall_seconds_incl_ingest": wall,
+            "single_process_estimate": {"value": n_s * n_q / sum(secs.values()), "unit": "routed queries/s",
+                                        "how": "queries / summed per-session routing time (mode i: one core)"},
+            "sessions_identical_to_fixture": int(same),
+        }
+        out["speedup_vs_cpu_baseline"] = out["value"] / out["cpu_baseline"]["value"]
+    return out
