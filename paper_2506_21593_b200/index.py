@@ -15,6 +15,7 @@ host) and returns device tensors; it is what the cascade and the benches use.
 from __future__ import annotations
 
 import bisect
+import weakref
 import ctypes
 import json
 import struct
@@ -98,6 +99,10 @@ class FlatIndex:
         self._payloads: list[Any] = []
         # deferred payload segments: (first row, source index, source rows), ascending
         self._deferred: list[tuple[int, "FlatIndex", np.ndarray]] = []
+        # indices holding deferred payloads that point at rows of THIS index: pinned to the
+        # current payload objects before any of this index's payloads change (upsert, clear,
+        # truncate), so they keep the payload they had when copied (AKM settle semantics)
+        self._dependents: "weakref.WeakSet[FlatIndex]" = weakref.WeakSet()
         self.epoch = 0  # bumped whenever rows are removed (clear / truncate)
         self.search_count = 0
         self.last_stats: _lib.SearchStats | None = None
@@ -143,6 +148,26 @@ class FlatIndex:
         with self._lock:
             return self.payload_at(self._row_by_id[entry_id])
 
+    def _pin_deferred_from(self, src: "FlatIndex") -> None:
+        """Resolve every deferred payload that points at ``src`` now (``src`` is about to
+        change its payloads)."""
+        with self._lock:
+            keep = []
+            for i, (base, s_idx, rows) in enumerate(self._deferred):
+                if s_idx is not src:
+                    keep.append((base, s_idx, rows))
+                    continue
+                for j, r in enumerate(rows.tolist()):
+                    if self._payloads[base + j] is _DEFERRED:
+                        self._payloads[base + j] = src.payload_at(r)
+            self._deferred = keep
+
+    def _release_dependents(self) -> None:
+        deps = list(self._dependents)
+        self._dependents = weakref.WeakSet()
+        for d in deps:
+            d._pin_deferred_from(self)
+
     def payload_at(self, row: int) -> Any:
         p = self._payloads[row]
         if p is _DEFERRED:  # payload copied by reference from another index's row
@@ -175,6 +200,7 @@ class FlatIndex:
                 self._ids.append(entry_id)
                 self._payloads.append(payload)
             else:
+                self._release_dependents()
                 self._payloads[row] = payload
                 self._update_rows(np.array([row], dtype=np.int64), arr[None, :])
 
@@ -196,6 +222,8 @@ class FlatIndex:
                     self._payloads.append(payload)
                     new_vecs.append(arr)
                 else:
+                    if row < base:
+                        self._release_dependents()
                     self._payloads[row] = payload
                     if row >= base:
                         new_vecs[row - base] = arr
@@ -260,6 +288,7 @@ class FlatIndex:
             self._ids.extend(ids)
             if payloads is None:
                 self._deferred.append((base, src, rows))
+                src._dependents.add(self)
                 self._payloads.extend([_DEFERRED] * len(ids))
             else:
                 self._payloads.extend(payloads)
@@ -278,6 +307,7 @@ class FlatIndex:
 
     def clear(self) -> None:
         with self._lock:
+            self._release_dependents()
             self._ids.clear()
             self._row_by_id.clear()
             self._payloads.clear()
@@ -287,6 +317,8 @@ class FlatIndex:
 
     def truncate(self, n: int) -> None:
         with self._lock:
+            if n < len(self._ids):
+                self._release_dependents()
             for eid in self._ids[n:]:
                 del self._row_by_id[eid]
             del self._ids[n:]

@@ -339,3 +339,31 @@ def test_deferred_payload_segments(gpu, rng):
     want.append(("b1", ("src", 1)))
     check()
     assert dst.epoch == 2  # one truncate + one clear
+
+
+def test_akm_payload_outlives_knowledge_base_changes(gpu):
+    """AKM rows settled device-to-device keep deferred payloads (references to
+    KB rows).  The reference AKM keeps the Passage object it settled (knowledge.py:217-228),
+    so a later upsert, truncation or clear of the KB must not change what the AKM returns."""
+    from paper_2506_21593_b200 import AdaptiveKnowledgeMemory, HashEmbedder, Passage, ingest_corpus
+
+    emb = HashEmbedder()
+    lines = [json.dumps({"id": f"p{i}", "text": f"passage number {i} about subject {i % 5}", "source": "t"})
+             for i in range(40)]
+    kb = ingest_corpus(lines, emb)
+    akm = AdaptiveKnowledgeMemory()
+    akm.settle_from_rows(kb.index, np.array([3, 7, 11, 30], dtype=np.int64))
+    before = {pid: akm.index.payload(pid) for pid in ("p3", "p7", "p11", "p30")}
+    # upsert p7 in the KB: same id, new passage
+    t = "a completely different passage"
+    kb.add(Passage(id="p7", text=t, source="t2", embedding=emb.embed(t)))
+    assert kb.get("p7").text == t
+    assert akm.index.payload("p7") is before["p7"] and akm.index.payload("p7").text != t
+    # settle more rows after the upsert: they reference the KB as it is now
+    akm.settle_from_rows(kb.index, np.array([7, 12], dtype=np.int64))
+    assert akm.index.payload("p12").id == "p12"
+    # truncate / clear the KB: settled payloads survive
+    kb.index.truncate(20)
+    assert akm.index.payload("p30") is before["p30"]
+    kb.index.clear()
+    assert akm.index.payload("p3") is before["p3"] and akm.index.payload("p12").id == "p12"
