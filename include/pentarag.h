@@ -135,6 +135,12 @@ int pr_index_scan_time(pr_index *h, double *total_ms, int64_t *launches);
 /* number of kernels this library has launched in this process */
 long long pr_launch_count(void);
 
+/* Row-sharded stores (sharded.py): d_out[i] = the stored fp32 row d_rows[i] - row_offset
+ * when this shard holds it (0 <= d_rows[i] - row_offset < count), else all zeros — a SUM
+ * all-reduce of the int32 bit patterns over the shards assembles the exact rows (the AKM
+ * settle and the cascade's seed guard copy knowledge-base rows, knowledge.py:217-228). */
+int pr_index_gather_rows(const pr_index *h, const int64_t *d_rows, int64_t n, int64_t row_offset, float *d_out,
+                         void *stream);
 /* Merge per-shard top-k lists into the global top-k (the NCCL all-gather
  * merge of a row-sharded store).  d_rows/d_raw are [nshard, nq, k] with
  * global row ids; d_count is [nshard, nq].  Output as pr_index_search, with

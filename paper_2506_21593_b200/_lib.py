@@ -81,6 +81,7 @@ SIGNATURES = {
     "pr_index_set_timing": (c_int, [c_vp, c_int]),
     "pr_index_scan_time": (c_int, [c_vp, ctypes.POINTER(c_dbl), ctypes.POINTER(c_i64)]),
     "pr_launch_count": (ctypes.c_longlong, []),
+    "pr_index_gather_rows": (c_int, [c_vp, c_vp, c_i64, c_i64, c_vp, c_vp]),
     "pr_merge_shards": (c_int, [c_vp, c_vp, c_vp, c_vp, c_int, c_i64, c_int, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "pr_index_snap_flags": (c_int, [c_vp, c_vp, c_i64, c_int, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "pr_kv_create": (c_int, [c_i64, c_vp]),

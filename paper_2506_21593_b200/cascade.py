@@ -335,9 +335,12 @@ def _launch(router, queries, vectors, start: int, end: int, mode: int, prev: "_S
     kb_cnt = torch.empty(B, dtype=torch.int32, device=dev)
     hint = int(min(B, max(1, getattr(router, "_cascade_nlist_hint", B // 2 + 1))))
     with kbi._lock:
-        _lib.check(L.pr_index_search_list(kbi.handle, _lib.ptr(Vd), _lib.ptr(lst), _lib.ptr(nlist), B, hint, sk, mode,
-                                          None, _lib.ptr(kb_rows), _lib.ptr(kb_raw), _lib.ptr(kb_rep),
-                                          _lib.ptr(kb_cnt), s), "search_list")
+        if getattr(kbi, "sharded", False):  # row-sharded KB: local scan + one all-gather merge (sharded.py)
+            kbi.search_list(Vd, lst, nlist, B, hint, sk, mode, kb_rows, kb_raw, kb_rep, kb_cnt)
+        else:
+            _lib.check(L.pr_index_search_list(kbi.handle, _lib.ptr(Vd), _lib.ptr(lst), _lib.ptr(nlist), B, hint, sk,
+                                              mode, None, _lib.ptr(kb_rows), _lib.ptr(kb_raw), _lib.ptr(kb_rep),
+                                              _lib.ptr(kb_cnt), s), "search_list")
     sp.kb_rows_d, sp.kb_cnt_d, sp.nlist_d = kb_rows, kb_cnt, nlist
     prof.mark("L.kb")
 

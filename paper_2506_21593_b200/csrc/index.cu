@@ -83,6 +83,22 @@ __global__ void gather_rows_kernel(const float *__restrict__ sx32, const __half 
     }
 }
 
+// rows of a row-sharded store: the rows this shard holds (global row - row_offset in
+// [0, count)) are copied, every other row is zero, so a SUM all-reduce over the shards'
+// int32 bit patterns assembles the exact fp32 rows
+__global__ void gather_owned_kernel(const float *__restrict__ x32, int dp8, int d, int64_t count,
+                                    const int64_t *__restrict__ rows, int64_t n, int64_t row_offset,
+                                    float *__restrict__ out) {
+    const int64_t total = n * (int64_t)d;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t / d;
+        const int j = (int)(t - i * d);
+        const int64_t r = rows[i] - row_offset;
+        out[t] = (r >= 0 && r < count) ? x32[r * dp8 + j] : 0.f;
+    }
+}
+
 __global__ void read_rows_kernel(const float *__restrict__ x32, int dp8, int d, int64_t row0, int64_t n,
                                  float *__restrict__ out) {
     int64_t total = n * (int64_t)d;
@@ -867,6 +883,17 @@ int pr_index_read_rows(const pr_index *h, int64_t row0, int64_t n, float *d_out,
     if (n == 0) return PR_OK;
     ::pr::count_launch();
     read_rows_kernel<<<grid_for(n * h->dim), 256, 0, as_stream(stream)>>>(h->x32, h->dp8, h->dim, row0, n, d_out);
+    PR_LAUNCH_CHECK();
+    return PR_OK;
+}
+
+int pr_index_gather_rows(const pr_index *h, const int64_t *d_rows, int64_t n, int64_t row_offset, float *d_out,
+                         void *stream) {
+    if (!h || n < 0) PR_FAIL(PR_ERR_BAD_ARG, "bad gather_rows");
+    if (n == 0) return PR_OK;
+    ::pr::count_launch();
+    gather_owned_kernel<<<std::min(grid_for(n * h->dim), pr::sm_count() * 16), 256, 0, as_stream(stream)>>>(
+        h->x32, h->dp8, h->dim, h->count, d_rows, n, row_offset, d_out);
     PR_LAUNCH_CHECK();
     return PR_OK;
 }

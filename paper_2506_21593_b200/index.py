@@ -264,10 +264,7 @@ class FlatIndex:
         torch = _torch()
         r = _lib.h2d(src_rows, torch.int64)
         with self._lock:
-            _lib.check(
-                self._L.pr_index_append_from(self._h, src.handle, _lib.ptr(r), r.numel(), _lib.stream_ptr()),
-                "append_from",
-            )
+            self._copy_rows_from(src, r)
             self._ids.extend([None] * r.numel())
             self._payloads.extend([None] * r.numel())
 
@@ -280,10 +277,7 @@ class FlatIndex:
         r = _lib.h2d(rows)
         with self._lock:
             base = len(self._ids)
-            _lib.check(
-                self._L.pr_index_append_from(self._h, src.handle, _lib.ptr(r), r.numel(), _lib.stream_ptr()),
-                "append_from",
-            )
+            self._copy_rows_from(src, r)
             self._row_by_id.update(zip(ids, range(base, base + len(ids))))
             self._ids.extend(ids)
             if payloads is None:
@@ -292,6 +286,17 @@ class FlatIndex:
                 self._payloads.extend([_DEFERRED] * len(ids))
             else:
                 self._payloads.extend(payloads)
+
+    def _copy_rows_from(self, src: "FlatIndex", r) -> None:
+        """Append the device rows ``r`` (int64 device tensor) of ``src``: device to device,
+        or for a row-sharded source (sharded.ShardedRowIndex) its exact fp32 rows gathered
+        from their owning ranks."""
+        if getattr(src, "sharded", False):
+            v = src.gather_vectors(r)
+            _lib.check(self._L.pr_index_append(self._h, _lib.ptr(v), v.shape[0], _lib.stream_ptr()), "append")
+            return
+        _lib.check(self._L.pr_index_append_from(self._h, src.handle, _lib.ptr(r), r.numel(), _lib.stream_ptr()),
+                   "append_from")
 
     def _append_rows(self, arr: np.ndarray) -> None:
         torch = _torch()

@@ -15,6 +15,7 @@ can be exercised on CPU with gloo; in production both are libpentarag calls.
 """
 from __future__ import annotations
 
+import weakref
 from dataclasses import dataclass
 from typing import Callable
 
@@ -126,3 +127,174 @@ def device_merge(parts: list[LocalHits], B: int, k: int) -> BatchResult:
                                  _lib.ptr(out.rows), _lib.ptr(out.raw), _lib.ptr(out.scores), _lib.ptr(out.count),
                                  _lib.stream_ptr()), "merge_shards")
     return out
+
+
+class _LocalView(FlatIndex):
+    """A FlatIndex sharing another index's device handle (never destroys it)."""
+
+    def __del__(self):
+        pass
+
+
+class ShardedRowIndex(FlatIndex):
+    """A ``FlatIndex`` drop-in whose device rows are row-sharded over the ranks of a process
+    group (the knowledge base of a multi-GPU cascade): rank r's device store
+    holds the contiguous global block ``shard_range(n, r, world)``, while the host side —
+    ids, payloads, counters — covers every row on every rank, so the router's host logic
+    (answers, AKM ids, write-back bookkeeping) runs unchanged and identically on all ranks.
+
+    * ``search_batch`` / ``search_list``: local exact top-k on the shard, per-rank self-snap
+      flags, ONE all-gather of B·(3k+1) int64, device merge (``pr_merge_shards``) — the
+      unsharded answer bit for bit (contiguous blocks keep global row order).
+    * ``gather_vectors``: exact fp32 rows of arbitrary global rows (owners copy, the rest
+      zero, one SUM all-reduce of the int32 bit patterns) — how the AKM settle and the
+      cascade's seed guard copy knowledge-base rows that live on other ranks.
+
+    Every rank must make the same calls in the same order (the cascade is deterministic and
+    replicated, so it does).  The store is loaded once (``load``); upserts / truncation are
+    not supported."""
+
+    sharded = True
+
+    def __init__(self, dim: int, *, group=None):
+        import torch.distributed as dist
+
+        super().__init__(dim=dim)
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.row_offset = 0
+        self.n_local = 0
+
+    @classmethod
+    def load(cls, ids: list[str], payloads: list, local_vectors, *, dim: int, group=None,
+             validate: bool = True) -> "ShardedRowIndex":
+        """``ids`` / ``payloads``: every global row (same on all ranks); ``local_vectors``:
+        this rank's block ``shard_range(len(ids), rank, world)`` as a [n_r, dim] array."""
+        self = cls(dim, group=group)
+        lo, hi = shard_range(len(ids), self.rank, self.world)
+        t = _lib.h2d(local_vectors).float().contiguous() if local_vectors is not None else None
+        if t is None or t.shape != (hi - lo, dim):
+            raise ValueError(f"rank {self.rank}: expected local rows [{lo}, {hi}) x {dim}")
+        self.local_store().extend_arrays([str(i) for i in range(lo, hi)], t, validate=validate)
+        self.row_offset, self.n_local = lo, hi - lo
+        self._ids = list(ids)
+        self._row_by_id = {e: i for i, e in enumerate(ids)}
+        self._payloads = list(payloads)
+        return self
+
+    def local_store(self) -> FlatIndex:
+        """This rank's device rows as a plain FlatIndex view (the handle is shared)."""
+        v = _LocalView.__new__(_LocalView)
+        v.__dict__.update({k: getattr(self, k) for k in ("_L", "_dim", "_h", "_lock")})
+        v._ids, v._row_by_id, v._payloads, v._deferred = [], {}, [], []
+        v._dependents = weakref.WeakSet()
+        v.epoch = v.search_count = 0
+        v.last_stats = None
+        v._view_of = self  # keeps the owner (and its handle) alive
+        return v
+
+    def __del__(self):
+        FlatIndex.__del__(self)
+
+    # -- collectives -----------------------------------------------------------
+    def _all_gather(self, buf):
+        import torch.distributed as dist
+
+        if self.world == 1:
+            return [buf]
+        bufs = [buf.new_empty(buf.shape) for _ in range(self.world)]
+        dist.all_gather(bufs, buf, group=self.group)
+        return bufs
+
+    def gather_vectors(self, rows):
+        """[m, dim] float32 device tensor of the global rows ``rows`` (device int64)."""
+        import torch
+        import torch.distributed as dist
+
+        rows = _lib.h2d(rows, torch.int64).contiguous()
+        out = torch.empty((rows.numel(), self._dim), dtype=torch.float32, device="cuda")
+        if rows.numel():
+            _lib.check(self._L.pr_index_gather_rows(self._h, _lib.ptr(rows), rows.numel(), self.row_offset,
+                                                    _lib.ptr(out), _lib.stream_ptr()), "gather_rows")
+        if self.world > 1:
+            iv = out.view(torch.int32)
+            dist.all_reduce(iv, op=dist.ReduceOp.SUM, group=self.group)
+        return out
+
+    def _merge_local(self, q, k, rows, raw, count) -> BatchResult:
+        import torch
+
+        B = q.shape[0]
+        snap = torch.empty((B, k), dtype=torch.uint8, device="cuda")
+        _lib.check(self._L.pr_index_snap_flags(self._h, _lib.ptr(q), B, k, _lib.ptr(rows), _lib.ptr(raw),
+                                               _lib.ptr(count), 0, _lib.ptr(snap), _lib.stream_ptr()), "snap_flags")
+        g = torch.where(rows >= 0, rows + self.row_offset, rows)
+        mine = LocalHits(g, raw, snap, count)
+        if self.world == 1:
+            parts = [mine]
+        else:
+            parts = [unpack(b, B, k) for b in self._all_gather(pack(mine))]
+        return device_merge(parts, B, k)
+
+    # -- search ----------------------------------------------------------------
+    def search_batch(self, queries, k: int, *, mode: int = MODE_AUTO, validate: bool = True,
+                     out: BatchResult | None = None, row_limit=None, count: bool = True) -> BatchResult:
+        import torch
+
+        q = _lib.h2d(torch.as_tensor(queries, dtype=torch.float32) if not isinstance(queries, torch.Tensor)
+                     else queries.float()).contiguous()
+        lim = None
+        if row_limit is not None:
+            lim = (_lib.h2d(row_limit, torch.int64) - self.row_offset).clamp(0, self.n_local).contiguous()
+        local = FlatIndex.search_batch(self.local_store(), q, k, mode=mode, validate=validate, row_limit=lim,
+                                       count=False)
+        res = self._merge_local(q, k, local.rows, local.raw, local.count)
+        if count:
+            with self._lock:
+                self.search_count += q.shape[0]
+        if out is not None:
+            for f in ("rows", "scores", "raw", "count"):
+                getattr(out, f).copy_(getattr(res, f))
+            return out
+        return res
+
+    def search_list(self, Vd, lst, nlist, B: int, hint: int, k: int, mode: int, rows, raw, rep, cnt) -> None:
+        """pr_index_search_list over the shard + all-gather merge; outputs per listed position
+        (positions >= *nlist report count 0), global rows."""
+        import torch
+
+        lrows = torch.empty((B, k), dtype=torch.int64, device="cuda")
+        lraw = torch.empty((B, k), dtype=torch.float64, device="cuda")
+        lrep = torch.empty((B, k), dtype=torch.float64, device="cuda")
+        lcnt = torch.empty(B, dtype=torch.int32, device="cuda")
+        with self._lock:
+            _lib.check(self._L.pr_index_search_list(self._h, _lib.ptr(Vd), _lib.ptr(lst), _lib.ptr(nlist), B, hint, k,
+                                                    mode, None, _lib.ptr(lrows), _lib.ptr(lraw), _lib.ptr(lrep),
+                                                    _lib.ptr(lcnt), _lib.stream_ptr()), "search_list")
+        live = torch.arange(B, device="cuda") < nlist.to(torch.int64)
+        lcnt = torch.where(live, lcnt, torch.zeros_like(lcnt))
+        lrows = torch.where(live[:, None], lrows, torch.full_like(lrows, -1))
+        lraw = torch.where(live[:, None], lraw, torch.zeros_like(lraw))
+        qc = Vd.index_select(0, lst.long().clamp(0, max(0, Vd.shape[0] - 1))).contiguous()
+        res = self._merge_local(qc, k, lrows, lraw, lcnt)
+        rows.copy_(res.rows)
+        raw.copy_(res.raw)
+        rep.copy_(res.scores)
+        cnt.copy_(res.count)
+
+    def read_rows(self, row0: int, n: int):
+        import torch
+
+        return self.gather_vectors(torch.arange(row0, row0 + n, dtype=torch.int64, device="cuda"))
+
+    # -- the store is loaded once ------------------------------------------------
+    def _unsupported(self, *a, **kw):
+        raise NotImplementedError("ShardedRowIndex is loaded once (ShardedRowIndex.load); no in-place edits")
+
+    insert = extend = extend_arrays = append_anonymous_from = append_rows_from = _unsupported
+    _append_rows = _update_rows = clear = truncate = _unsupported
+
+    @property
+    def handle(self):
+        raise AttributeError("a ShardedRowIndex has no single device handle: use search_list / gather_vectors")
