@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--n", type=int, default=10_000_000)
+    ap.add_argument("--rows", "--n", dest="n", type=int, default=10_000_000)
     ap.add_argument("--dim", type=int, default=1024)
     ap.add_argument("--batch", type=int, default=4096)
     ap.add_argument("--k", type=int, default=5)
@@ -366,9 +366,16 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # BENCH_SAME_GPU=1 (plumbing checks only, never a bench number): every rank on cuda:0, gloo
+    same_gpu = os.environ.get("BENCH_SAME_GPU") == "1"
+    if same_gpu:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if same_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     from paper_2506_21593_b200 import _lib
     from paper_2506_21593_b200.sharded import ShardedFlatIndex, shard_range
@@ -515,6 +522,22 @@ def main():
                "seconds": secs, "host_threads": threads, "cpu": cpu_model(), "numpy": np.__version__}
 
     configs = {}
+    if world > 1 and "c5" in [c.strip() for c in a.configs.split(",")]:
+        # C5 at N GPUs: every rank routes the same sessions over a knowledge base row-sharded
+        # across the ranks (sharded.ShardedRowIndex: the L5 scan of each span is split N ways,
+        # one all-gather merge); throughput = routed queries / the slowest rank's time
+        from benchlib import configs as C
+
+        try:
+            r5 = C.c5_routed(idx, a.n, n_sessions=a.c5_sessions, queries_per_session=a.c5_queries, shard=lo)
+            ms_max = max_over_ranks(r5["ms_total"])
+            r5.update(value=r5["value"] * r5["ms_total"] / ms_max, ms_total=ms_max, timing="max over ranks")
+            configs["c5_routed_sharded"] = r5
+        except Exception as exc:  # noqa: BLE001 - recorded, the headline stands
+            import traceback
+
+            configs["c5_routed_sharded"] = {"error": f"{type(exc).__name__}: {exc}",
+                                            "trace": traceback.format_exc()[-1500:]}
     if rank == 0 and world == 1 and a.configs:
         import traceback
 

@@ -347,7 +347,7 @@ _LAST_BATCH_WALL: list = []  # (worker, session, batch, host wall ms) of every c
 
 
 def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_session=20_000, batch=4096,
-              seed=0, parity_queries=1000, profile=False, workers=1, l5_oracle_queries=8):
+              seed=0, parity_queries=1000, profile=False, workers=1, l5_oracle_queries=8, shard=None):
     """Routed replay over the bench's 10M x 1024 store turned into a knowledge base:
     rows [0, n_qa) hold HashEmbedder(context) of the QA pool, the rest stay dense
     distractors.
@@ -370,7 +370,22 @@ def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_se
     rows = qa_rows(n_qa, seed=42)
     corpus = corpus_of(rows)
     ctx = emb.embed_matrix([c["text"] for c in corpus])
-    store._update_rows(np.arange(n_qa, dtype=np.int64), ctx)
+    if shard is None:
+        store._update_rows(np.arange(n_qa, dtype=np.int64), ctx)
+    else:
+        # row-sharded knowledge base (multi-GPU): ``store`` is this rank's block of global rows
+        # [row0, row0 + len(store)); the contexts' rows are updated where they live, and the
+        # KB the routers see is the sharded view (sharded.ShardedRowIndex)
+        from paper_2506_21593_b200.sharded import ShardedRowIndex
+
+        row0 = int(shard)
+        a, b = row0, min(row0 + len(store), n_qa)
+        if a < b:
+            store._update_rows(np.arange(a, b, dtype=np.int64) - row0, ctx[a:b])
+        store = ShardedRowIndex.wrap(store, [str(i) for i in range(n_store)], None, row0)
+        parity_queries = min(parity_queries, 200)
+        l5_oracle_queries = 0
+        workers = 1
     real = [Passage(id=store.id_at(i), text=c["text"], source=c["source"],
                     embedding=EmbeddingVector(values=ctx[i]), answer=c["answer"]) for i, c in enumerate(corpus)]
     store._payloads = _KBPayloads(store, real)
@@ -536,8 +551,12 @@ def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_se
         "workload": f"five-layer routed replay (L1/L2/L3/L4/L5, LLM stubbed) over a {n_store} x 1024 KB "
                     f"({n_qa} HashEmbedder contexts + dense distractors), {n_sessions} cache-warming sessions x "
                     f"{queries_per_session} queries = {n_sessions * queries_per_session} routed queries, spans of "
-                    f"{batch} (configs[4], 1 GPU), {workers} concurrent session worker(s)",
+                    f"{batch} (configs[4], {'1 GPU' if shard is None else 'KB row-sharded over all ranks'}), "
+                    f"{workers} concurrent session worker(s)",
         "value": total / (ms / 1e3), "unit": "routed queries/s", "ms_total": ms, "workers": workers,
+        "knowledge_base": ("one GPU" if shard is None else
+                           f"row-sharded: this rank holds rows [{int(shard)}, {int(shard) + store.n_local}); local "
+                           "list scan + one all-gather merge per span, seed/AKM rows gathered from their owners"),
         "layer_counts": layer_counts, "queries_routed_sequentially": seq_total,
         "spans": sum(t.get("spans", 0) for t in tallies), "spans_pipelined": sum(t.get("pipelined", 0) for t in tallies),
         "span_wall_ms_mean_per_session": {"n": int(walls.size), "median": float(np.median(walls)), "p90": float(np.percentile(walls, 90)),

@@ -15,9 +15,12 @@ can be exercised on CPU with gloo; in production both are libpentarag calls.
 """
 from __future__ import annotations
 
+import threading
 import weakref
 from dataclasses import dataclass
 from typing import Callable
+
+import numpy as np
 
 from . import _lib
 from .index import MODE_AUTO, BatchResult, FlatIndex
@@ -183,6 +186,28 @@ class ShardedRowIndex(FlatIndex):
         self._payloads = list(payloads)
         return self
 
+    @classmethod
+    def wrap(cls, local: FlatIndex, ids: list[str], payloads, row_offset: int, *, group=None) -> "ShardedRowIndex":
+        """A sharded view over an already loaded local block (``local`` holds global rows
+        [row_offset, row_offset + len(local))); ``ids`` / ``payloads`` cover every row."""
+        import torch.distributed as dist
+
+        self = cls.__new__(cls)
+        self._L, self._dim, self._h = local._L, local._dim, local._h
+        self._lock = threading.RLock()
+        self._owner, self._owns_handle = local, False
+        self._ids = list(ids)
+        self._row_by_id = {e: i for i, e in enumerate(self._ids)}
+        self._payloads = payloads
+        self._deferred, self._dependents = [], weakref.WeakSet()
+        self.epoch = self.search_count = 0
+        self.last_stats = None
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.row_offset, self.n_local = int(row_offset), len(local)
+        return self
+
     def local_store(self) -> FlatIndex:
         """This rank's device rows as a plain FlatIndex view (the handle is shared)."""
         v = _LocalView.__new__(_LocalView)
@@ -195,7 +220,8 @@ class ShardedRowIndex(FlatIndex):
         return v
 
     def __del__(self):
-        FlatIndex.__del__(self)
+        if getattr(self, "_owns_handle", True):
+            FlatIndex.__del__(self)
 
     # -- collectives -----------------------------------------------------------
     def _all_gather(self, buf):
@@ -242,8 +268,8 @@ class ShardedRowIndex(FlatIndex):
                      out: BatchResult | None = None, row_limit=None, count: bool = True) -> BatchResult:
         import torch
 
-        q = _lib.h2d(torch.as_tensor(queries, dtype=torch.float32) if not isinstance(queries, torch.Tensor)
-                     else queries.float()).contiguous()
+        q = _lib.h2d(queries.float() if isinstance(queries, torch.Tensor)
+                     else np.asarray(queries, dtype=np.float32)).contiguous()
         lim = None
         if row_limit is not None:
             lim = (_lib.h2d(row_limit, torch.int64) - self.row_offset).clamp(0, self.n_local).contiguous()
