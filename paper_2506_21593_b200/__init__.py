@@ -29,7 +29,7 @@ from .index import MODE_AUTO, MODE_EXACT, MODE_TENSOR, MODE_TENSOR_I8, BatchResu
 from .knowledge import AdaptiveKnowledgeMemory, MainKnowledgeBase, ingest_corpus
 from .router import CascadeRouter, LayerProbe, RouterConfig, RouteTraceEvent, TraceLog, export_triples
 from .service import MicroBatcher
-from .sharded import ShardedFlatIndex, shard_range
+from .sharded import ShardedFlatIndex, ShardedRowIndex, shard_range
 from .records import CASCADE_ORDER, AnswerRecord, LayerTag, Passage, Query, TrainingTriple, validate_query
 from .vectors import DIMENSION, HASH_SEED, EmbeddingVector, HashEmbedder, cosine, tokenize
 
