@@ -31,7 +31,7 @@ def _unit_rows(n, d, seed, device="cuda"):
 
 
 # ---------------------------------------------------------------- C2
-def c2_semantic(peak_tops: float, peak_how: str = "", n=1_000_000, d=768, batch=4096, steps=20, threshold=0.85,
+def c2_semantic(peak_tops: float, peak_how: str = "", p8=None, n=1_000_000, d=768, batch=4096, steps=20, threshold=0.85,
                 parity_q=8):
     import torch
 
@@ -84,7 +84,9 @@ def c2_semantic(peak_tops: float, peak_how: str = "", n=1_000_000, d=768, batch=
         "hit_fraction": float(hit.float().mean().item()),
         "roofline": {"bound": "tensor", "achieved": flop / (kern / 1e3) / 1e12, "peak": peak_tops,
                      "unit": "TOP/s", "frac": flop / (kern / 1e3) / 1e12 / peak_tops, "kernel_ms": kern,
-                     "kernel": "tc8_scan_kernel", "peak_kind": "measured int8 sustained: " + peak_how},
+                     "kernel": "tc8_scan_kernel", "peak_kind": peak_how,
+                     "frac_of_inrun_cublas_int8": (flop / (kern / 1e3) / 1e12 / p8["int8_tops_sustained"]
+                                                   if p8 else None)},
         "parity": {"queries_checked": int(sel.size), "mismatches": mism},
         "threshold_probes": probes,
     }

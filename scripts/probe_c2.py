@@ -8,6 +8,6 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 from benchlib import configs as C  # noqa: E402
 
-r = C.c2_semantic(2400.0, "probe", steps=int(os.environ.get("STEPS", "20")))
+r = C.c2_semantic(2760.0, "probe", None, steps=int(os.environ.get("STEPS", "20")))
 print("c2", round(r["value"] / 1e6, 3), "M/s", round(r["ms_per_batch"], 3), "ms/batch kernel", round(r["roofline"]["kernel_ms"], 3),
       "ms parity", r["parity"])
