@@ -209,12 +209,21 @@ int pr_l2_fetch_granularity(int bytes, int *previous);
  * vector layers consume (pr_index_search_list), without a host round trip:
  *   l1[j] = d_kv_hit[j] || d_rep[j]   (pre-batch KV probe, or an earlier in-window write)
  *   l2[j] = d_sc_count[j] > 0 && d_sc_score[j] >= sc_threshold   (caches.py:140, inclusive)
- * A query hit by a fast layer probed before the vector layers (l1_blocks / l2_blocks) is
+ *   l3[j] = d_l3_hit[j]               (accepted recall, pr_recall_gate)
+ * A query hit by a fast layer probed before the vector layers (l1/l2/l3_blocks) is
  * dropped; the rest, in query order, form d_list[0..*d_nlist) and d_slot[j] = position or -1.
- * d_kv_hit NULL = L1 not probed; d_sc_count NULL = L2 not probed. */
+ * d_kv_hit NULL = L1 not probed; d_sc_count NULL = L2 not probed; d_l3_hit NULL = no recall
+ * outcome on the device. */
 int pr_cascade_gate(int64_t B, const uint8_t *d_kv_hit, const uint8_t *d_rep, const int32_t *d_sc_count,
-                    const double *d_sc_score, double sc_threshold, int l1_blocks, int l2_blocks, uint8_t *d_l1,
-                    uint8_t *d_l2, int32_t *d_list, int32_t *d_nlist, int32_t *d_slot, void *stream);
+                    const double *d_sc_score, double sc_threshold, const uint8_t *d_l3_hit, int l1_blocks,
+                    int l2_blocks, int l3_blocks, uint8_t *d_l1, uint8_t *d_l2, int32_t *d_list, int32_t *d_nlist,
+                    int32_t *d_slot, void *stream);
+/* The L3 recall gate (generation.py:203-224 memory_recall over StubBackend.recall :110-115)
+ * for a recall table kept in a pr_kv table (value = index into d_conf): d_out[j] = d_hit[j] &&
+ * 0 <= d_vals[j] < nconf && d_conf[d_vals[j]] >= threshold.  d_conf holds -1 for an entry
+ * whose answer is empty (never accepted).  threshold outside [0, 1] -> PR_ERR_BAD_ARG. */
+int pr_recall_gate(int64_t n, const int64_t *d_vals, const uint8_t *d_hit, const double *d_conf, int64_t nconf,
+                   double threshold, uint8_t *d_out, void *stream);
 /* The adaptive-memory guard (knowledge.py:217-228: L5 seeds settle before the next query):
  * the seeds (top seed_k knowledge-base rows) of the previous span's listed queries, then of
  * this span's, deduplicated by KB row in first-occurrence order -> d_out_rows[0..*d_nout)

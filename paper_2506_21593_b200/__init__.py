@@ -24,7 +24,8 @@ from .errors import (
 )
 from .caches import CacheEntry, FixedKVCache, SemanticCache, writeback
 from .errors import MalformedJsonl
-from .generation import StubBackend, StubKnowledgeTable, generate_with_context, memory_recall
+from .generation import (DeviceKnowledgeTable, StubBackend, StubKnowledgeTable, generate_with_context,
+                         memory_recall)
 from .index import MODE_AUTO, MODE_EXACT, MODE_TENSOR, MODE_TENSOR_I8, BatchResult, FlatIndex, SearchHit
 from .knowledge import AdaptiveKnowledgeMemory, MainKnowledgeBase, ingest_corpus
 from .router import CascadeRouter, LayerProbe, RouterConfig, RouteTraceEvent, TraceLog, export_triples

@@ -52,6 +52,7 @@ class SearchStats(ctypes.Structure):
     ]
 
 
+ABI_VERSION = 2  # pr_abi_version() of the library these signatures describe
 # name -> (restype, argtypes); the exported surface of include/pentarag.h
 SIGNATURES = {
     "pr_last_error": (ctypes.c_char_p, []),
@@ -73,8 +74,9 @@ SIGNATURES = {
     "pr_index_search_ex": (c_int, [c_vp, c_vp, c_i64, c_int, c_u32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "pr_index_search_list": (c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_int, c_u32, c_vp, c_vp, c_vp, c_vp,
                                      c_vp, c_vp]),
-    "pr_cascade_gate": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_dbl, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp,
-                                c_vp]),
+    "pr_cascade_gate": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_dbl, c_vp, c_int, c_int, c_int, c_vp, c_vp, c_vp,
+                                c_vp, c_vp, c_vp]),
+    "pr_recall_gate": (c_int, [c_i64, c_vp, c_vp, c_vp, c_i64, c_dbl, c_vp, c_vp]),
     "pr_cascade_mark_init": (c_int, [c_vp, c_i64, c_vp]),
     "pr_cascade_seeds": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
     "pr_index_last_stats": (c_int, [c_vp, ctypes.POINTER(SearchStats)]),
@@ -124,6 +126,10 @@ def load(path: str = LIB_PATH):
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args
+        if L.pr_abi_version() != ABI_VERSION:
+            raise errors.NativeLibraryMissing(
+                f"{path} has ABI {L.pr_abi_version()}, this package binds ABI {ABI_VERSION}: rebuild it "
+                "(`python -m paper_2506_21593_b200.build`)")
         _lib = L
     return _lib
 

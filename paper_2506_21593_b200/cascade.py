@@ -13,8 +13,11 @@ DEVICE stage (``_launch``, enqueued on the router's CUDA stream, no host read-ba
 * L2 (semantic cache, caches.py:131-145): the first occurrence of every text new to the
   cache is appended up front (that is what write-back will do), and ONE row-limited top-1
   search lets query j see exactly the rows written by queries before it.
-* Gate (``pr_cascade_gate``): L1 / L2 outcomes in probe order, and the ONE compacted miss
-  list — the queries no fast layer answered — built on the device by a prefix sum.
+* L3 (memory recall, generation.py:203-224), when the backend is the stub LLM over a
+  ``DeviceKnowledgeTable``: one probe of the recall hash table + the confidence gate
+  (``pr_recall_gate``).  The table never changes while routing, so no window is needed.
+* Gate (``pr_cascade_gate``): L1 / L2 / L3 outcomes in probe order, and the ONE compacted
+  miss list — the queries no fast layer answered — built on the device by a prefix sum.
 * L5 (knowledge base, knowledge.py:65-85): one top-seed_k scan of the listed queries only
   (``pr_index_search_list``: the list and its count never leave the device).
 * L4 guard: L4 depends on which earlier queries were served by L5 (their seeds settle into
@@ -203,9 +206,26 @@ def _embed(router, texts, vectors, arena):
     return torch.as_tensor(vectors, dtype=torch.float32).cuda().contiguous()
 
 
+def _is_stub(backend) -> bool:
+    """The stub LLM, this package's or the reference's (same recall semantics,
+    generation.py:83-115); a subclass may override recall and must be called."""
+    t = type(backend)
+    return t is generation.StubBackend or (t.__name__ == "StubBackend" and t.__module__ == "ragcascade.generation")
+
+
 def _recall_always_rejects(backend, threshold) -> bool:
-    return (type(backend) is generation.StubBackend and len(backend.knowledge) == 0
-            and 0.0 <= threshold <= 1.0)
+    return (_is_stub(backend) and not isinstance(backend.knowledge, generation.DeviceKnowledgeTable)
+            and len(backend.knowledge) == 0 and 0.0 <= threshold <= 1.0)
+
+
+def _device_recall(router):
+    """The recall table whose L3 outcome is decided on the device, or None."""
+    backend = router.backend
+    tab = getattr(backend, "knowledge", None)
+    if (_is_stub(backend) and isinstance(tab, generation.DeviceKnowledgeTable)
+            and 0.0 <= router.config.recall_threshold <= 1.0):
+        return tab
+    return None
 
 
 class _Scratch:
@@ -249,7 +269,8 @@ class _Span:
     """A span whose device stage has been enqueued."""
 
     __slots__ = ("start", "end", "size", "B", "qs", "texts", "arena", "n_pre_sc", "new_js", "prev_last",
-                 "prev", "host", "event", "kb_rows_d", "kb_cnt_d", "nlist_d", "t_start", "entries")
+                 "prev", "host", "event", "kb_rows_d", "kb_cnt_d", "nlist_d", "t_start", "entries", "recall",
+                 "l3", "l3_val")
 
 
 def _launch(router, queries, vectors, start: int, end: int, mode: int, prev: "_Span | None") -> _Span:
@@ -309,6 +330,10 @@ def _launch(router, queries, vectors, start: int, end: int, mode: int, prev: "_S
     if L1 in pos:
         kv_val, kv_hit = kv.probe_device(arena[0], arena[1], B)
     rep_d = _lib.h2d(rep.astype(np.uint8))
+    l3_val = l3_d = None
+    sp.recall = _device_recall(router) if L3 in pos else None
+    if sp.recall is not None:
+        l3_val, l3_d = sp.recall.gate_device(arena[0], arena[1], B, cfg.recall_threshold)
     r2 = None
     if L2 in pos:
         r2 = sc_index.search_batch(Vd, 1, mode=mode, validate=False, row_limit=sc_limit, count=False)
@@ -321,11 +346,12 @@ def _launch(router, queries, vectors, start: int, end: int, mode: int, prev: "_S
     sc_cnt = r2.count if r2 is not None else None
     sc_score = r2.scores[:, 0].contiguous() if r2 is not None else None
     _lib.check(L.pr_cascade_gate(B, _lib.ptr(kv_hit), _lib.ptr(rep_d), _lib.ptr(sc_cnt), _lib.ptr(sc_score),
-                                 float(sc.threshold), int(L1 in pos and pos[L1] < vec_pos),
-                                 int(L2 in pos and pos[L2] < vec_pos), _lib.ptr(l1_d), _lib.ptr(l2_d), _lib.ptr(lst),
-                                 _lib.ptr(nlist), _lib.ptr(slot), s), "cascade_gate")
+                                 float(sc.threshold), _lib.ptr(l3_d), int(L1 in pos and pos[L1] < vec_pos),
+                                 int(L2 in pos and pos[L2] < vec_pos), int(L3 in pos and pos[L3] < vec_pos),
+                                 _lib.ptr(l1_d), _lib.ptr(l2_d), _lib.ptr(lst), _lib.ptr(nlist), _lib.ptr(slot), s),
+               "cascade_gate")
 
-    prof.mark("L.l1l2gate")
+    prof.mark("L.l1l2l3gate")
     # ---- L5: the knowledge-base scan of the listed queries only
     sk = cfg.akm_seed_k
     kbi = kb.index
@@ -373,10 +399,14 @@ def _launch(router, queries, vectors, start: int, end: int, mode: int, prev: "_S
 
     prof.mark("L.l4guard")
     # ---- the span's one read-back: outcomes + the listed queries' KB rows
+    none = torch.full((B,), -1, dtype=i64, device=dev)
     cols = [l1_d.to(i64), l2_d.to(i64), slot.to(i64), l4.to(i64),
-            (r2.rows[:, 0] if r2 is not None else torch.full((B,), -1, dtype=i64, device=dev)),
-            (kv_val if kv_val is not None else torch.full((B,), -1, dtype=i64, device=dev)),
-            kb_cnt.to(i64), nlist.to(i64)]
+            (r2.rows[:, 0] if r2 is not None else none),
+            (kv_val if kv_val is not None else none),
+            kb_cnt.to(i64),
+            (l3_d.to(i64) if l3_d is not None else none),
+            (l3_val if l3_val is not None else none),
+            nlist.to(i64)]
     packed = torch.cat([c.reshape(-1) for c in cols] + [kb_rows.reshape(-1)])
     sp.host, sp.event = pinned.ring().d2h(packed)
     prof.mark("L.pack")
@@ -395,9 +425,10 @@ def _unpack(sp: _Span, sk: int):
     sp.event.synchronize()
     h = sp.host.copy()  # out of the pinned ring: the ledger keeps views of it
     B = sp.B
-    l1, l2, slot, l4, sc_row, kv_val, kb_cnt = (h[i * B:(i + 1) * B] for i in range(7))
-    nl = int(h[7 * B])
-    kb_rows = h[7 * B + 1:].reshape(B, sk)
+    l1, l2, slot, l4, sc_row, kv_val, kb_cnt, l3, l3_val = (h[i * B:(i + 1) * B] for i in range(9))
+    nl = int(h[9 * B])
+    kb_rows = h[9 * B + 1:].reshape(B, sk)
+    sp.l3, sp.l3_val = l3 > 0, l3_val
     return l1.astype(bool), l2.astype(bool), slot, l4.astype(bool), sc_row, kv_val, kb_rows[:nl], kb_cnt[:nl], nl
 
 
@@ -434,7 +465,7 @@ def _finish(router, sp: _Span, *, more_follow: bool):
             setattr(backend, a, v)
         raise _BackendFailed() from exc
     for j, a in recalled.items():  # before the cache hits: a later hit may copy a recalled answer
-        text[j], conf_l[j] = a.text, a.confidence
+        text[j], conf_l[j] = a
     # ---- cache hits, in order: a hit serves a copy of the latest answer written for its key
     v1, v2, v5 = int(L1), int(L2), int(L5)
     sv = serving
@@ -502,6 +533,14 @@ def _decide(router, sp, l1, l2, slot, l4_unsure, kb_rows, kb_cnt, prof):
             h = reach & l1[:p]
         elif L is L2:
             h = reach & l2[:p]
+        elif L is L3 and sp.recall is not None:
+            # decided on the device (pr_recall_gate); every query reaching L3 is one recall call
+            h = reach & sp.l3[:p]
+            backend.recall_calls += int(reach.sum())
+            entry_at = sp.recall.entry_at
+            for j, v in zip(np.flatnonzero(h).tolist(), sp.l3_val[:p][h].tolist()):
+                e = entry_at(v)
+                recalled[j] = (e.answer, e.confidence)
         elif L is L3 and _recall_always_rejects(backend, cfg.recall_threshold):
             # the stub LLM with an empty recall table rejects every query (generation.py);
             # only its call counter moves
@@ -513,7 +552,7 @@ def _decide(router, sp, l1, l2, slot, l4_unsure, kb_rows, kb_cnt, prof):
                 rec = generation.memory_recall(backend, qs[j], cfg.recall_threshold)
                 if rec is not None:
                     h[j] = True
-                    recalled[int(j)] = rec
+                    recalled[int(j)] = (rec.text, rec.confidence)
         elif L is L4:
             h = np.zeros(p, dtype=bool)
         else:

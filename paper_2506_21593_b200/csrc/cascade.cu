@@ -11,6 +11,11 @@
 //                      layers leaves the list; the survivors are compacted in query order
 //                      (block-wide prefix sum) into list / count / slot — no host round trip.
 //                      The knowledge-base scan then runs on the list (pr_index_search_list).
+//   pr_recall_gate     L3 (memory recall, generation.py:203-224) when the backend's recall
+//                      table is a device hash table: accept iff the question is in the table,
+//                      its confidence >= the recall threshold and its answer is non-empty
+//                      (the confidence array holds -1 for an empty answer).  Its output
+//                      feeds pr_cascade_gate like the L1/L2 outcomes.
 //   pr_cascade_seeds   the AKM-hit guard: the superset of seeds (top seed_k KB rows) every
 //                      earlier listed query could settle into the AKM before a later query
 //                      probes it (knowledge.py:217-228), deduplicated by KB row in first-
@@ -62,7 +67,8 @@ struct GateArgs {
     const int32_t *sc_count;  // [B] semantic-cache top-1 count (nullable: L2 absent)
     const double *sc_score;   // [B] reported top-1 score
     double sc_threshold;
-    int l1_blocks, l2_blocks;  // the layer is probed before the vector layers
+    const uint8_t *l3_hit;     // [B] accepted recall (nullable: L3 absent or not on the device)
+    int l1_blocks, l2_blocks, l3_blocks;  // the layer is probed before the vector layers
     uint8_t *l1, *l2;          // [B] out
     int32_t *list;             // [B] out: queries that reach the vector layers, in order
     int32_t *nlist;            // [1] out
@@ -80,7 +86,8 @@ __global__ void __launch_bounds__(CG_THREADS) cascade_gate_kernel(GateArgs a) {
             const bool h2 = a.sc_count && a.sc_count[j] > 0 && a.sc_score[j] >= a.sc_threshold;
             a.l1[j] = h1;
             a.l2[j] = h2;
-            keep = !((h1 && a.l1_blocks) || (h2 && a.l2_blocks));
+            const bool h3 = a.l3_hit && a.l3_hit[j];
+            keep = !((h1 && a.l1_blocks) || (h2 && a.l2_blocks) || (h3 && a.l3_blocks));
         }
         int total;
         const int pos = block_exclusive_scan(keep, warp_sums, total);
@@ -91,6 +98,15 @@ __global__ void __launch_bounds__(CG_THREADS) cascade_gate_kernel(GateArgs a) {
         base += total;
     }
     if (threadIdx.x == 0) *a.nlist = base;
+}
+
+__global__ void recall_gate_kernel(int64_t n, const int64_t *__restrict__ vals, const uint8_t *__restrict__ hit,
+                                   const double *__restrict__ conf, int64_t nconf, double threshold,
+                                   uint8_t *__restrict__ out) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = vals[j];
+        out[j] = hit[j] && v >= 0 && v < nconf && conf[v] >= threshold;
+    }
 }
 
 struct SeedArgs {
@@ -164,14 +180,29 @@ using namespace pr;
 extern "C" {
 
 int pr_cascade_gate(int64_t B, const uint8_t *d_kv_hit, const uint8_t *d_rep, const int32_t *d_sc_count,
-                    const double *d_sc_score, double sc_threshold, int l1_blocks, int l2_blocks, uint8_t *d_l1,
-                    uint8_t *d_l2, int32_t *d_list, int32_t *d_nlist, int32_t *d_slot, void *stream) {
+                    const double *d_sc_score, double sc_threshold, const uint8_t *d_l3_hit, int l1_blocks,
+                    int l2_blocks, int l3_blocks, uint8_t *d_l1, uint8_t *d_l2, int32_t *d_list, int32_t *d_nlist,
+                    int32_t *d_slot, void *stream) {
     if (B < 0 || !d_l1 || !d_l2 || !d_list || !d_nlist || !d_slot || (d_sc_count && !d_sc_score))
         PR_FAIL(PR_ERR_BAD_ARG, "bad cascade_gate");
-    GateArgs a{B, d_kv_hit, d_rep, d_sc_count, d_sc_score, sc_threshold, l1_blocks, l2_blocks, d_l1, d_l2,
-               d_list, d_nlist, d_slot};
+    GateArgs a{B, d_kv_hit, d_rep, d_sc_count, d_sc_score, sc_threshold, d_l3_hit, l1_blocks, l2_blocks, l3_blocks,
+               d_l1, d_l2, d_list, d_nlist, d_slot};
     ::pr::count_launch();
     cascade_gate_kernel<<<1, CG_THREADS, 0, as_stream(stream)>>>(a);
+    PR_LAUNCH_CHECK();
+    return PR_OK;
+}
+
+int pr_recall_gate(int64_t n, const int64_t *d_vals, const uint8_t *d_hit, const double *d_conf, int64_t nconf,
+                   double threshold, uint8_t *d_out, void *stream) {
+    if (n < 0 || nconf < 0 || (n > 0 && (!d_vals || !d_hit || !d_out)) || (nconf > 0 && !d_conf))
+        PR_FAIL(PR_ERR_BAD_ARG, "bad recall_gate");
+    if (!(threshold >= 0.0 && threshold <= 1.0)) PR_FAIL(PR_ERR_BAD_ARG, "recall threshold outside [0, 1]");
+    if (n == 0) return PR_OK;
+    ::pr::count_launch();
+    const int threads = 256;
+    const int blocks = (int)std::min<int64_t>((n + threads - 1) / threads, 148 * 8);
+    recall_gate_kernel<<<blocks, threads, 0, as_stream(stream)>>>(n, d_vals, d_hit, d_conf, nconf, threshold, d_out);
     PR_LAUNCH_CHECK();
     return PR_OK;
 }

@@ -768,7 +768,7 @@ using namespace pr;
 extern "C" {
 
 const char *pr_last_error(void) { return pr::last_error(); }
-int pr_abi_version(void) { return 1; }
+int pr_abi_version(void) { return 2; }  // 2: pr_cascade_gate takes the L3 outcome
 
 int pr_device_info(int *sms, int *major, int *minor) {
     int dev = 0;

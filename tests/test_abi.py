@@ -42,7 +42,7 @@ def test_python_binding_covers_header():
 
 
 def test_abi_version(lib):
-    assert lib.pr_abi_version() == 1
+    assert lib.pr_abi_version() == 2
 
 
 def _fp(lib, b: bytes):

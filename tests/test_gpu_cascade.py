@@ -93,9 +93,15 @@ def test_route_batch_matches_reference_simulation(gpu):
 
 
 @pytest.mark.parametrize("span", [4096, 29])
-@pytest.mark.parametrize("variant", ["default", "permuted", "disabled", "recall"])
+@pytest.mark.parametrize("variant", ["default", "permuted", "disabled", "recall", "device_recall",
+                                     "device_recall_first"])
 def test_route_batch_equals_sequential_random(gpu, variant, span):
-    from paper_2506_21593_b200 import LayerTag, RouterConfig, StubBackend, StubKnowledgeTable, validate_query
+    """device_recall*: the batched router's recall table is a DeviceKnowledgeTable (L3
+    decided on the device, pr_recall_gate), the sequential twin's the host
+    StubKnowledgeTable with the same adds — low confidences, empty answers, overwrites,
+    an inclusive threshold boundary, and L3 probed first."""
+    from paper_2506_21593_b200 import (DeviceKnowledgeTable, LayerTag, RouterConfig, StubBackend, StubKnowledgeTable,
+                                       validate_query)
 
     gold = _golden("simulation.json")
     corpus, questions = gold["corpus"][:150], gold["questions"]
@@ -105,6 +111,9 @@ def test_route_batch_equals_sequential_random(gpu, variant, span):
                                                  LayerTag.FIXED_KV, LayerTag.MEMORY_RECALL, LayerTag.NAIVE_RAG))
     elif variant == "disabled":
         kw["config"] = RouterConfig(disabled_layers=frozenset({LayerTag.FIXED_KV, LayerTag.MEMORY_RECALL}))
+    elif variant == "device_recall_first":
+        kw["config"] = RouterConfig(layer_order=(LayerTag.MEMORY_RECALL, LayerTag.FIXED_KV, LayerTag.SEMANTIC_CACHE,
+                                                 LayerTag.ADAPTIVE_MEMORY, LayerTag.NAIVE_RAG), recall_threshold=0.3)
     rng = np.random.default_rng(5)
     texts = []
     for i in range(300):
@@ -118,16 +127,27 @@ def test_route_batch_equals_sequential_random(gpu, variant, span):
     # passages that equal later queries make AKM hits (and batch splits) likely
     texts[150:150] = [corpus[3]["text"], corpus[7]["text"]]
 
-    def mk():
+    def mk(device=False):
         extra = dict(kw)
         if variant == "recall":
             tab = StubKnowledgeTable()
             for t in texts[::9]:
                 tab.add(t, "recalled " + t[:10], 0.9)
             extra["backend"] = StubBackend(tab)
+        elif variant.startswith("device_recall"):
+            tab = DeviceKnowledgeTable() if device else StubKnowledgeTable()
+            for t in texts[::9]:
+                tab.add(t, "recalled " + t[:10], 0.9)
+            for t in texts[2::11]:
+                tab.add(t, "shaky " + t[:8], 0.3)  # rejected at 0.5, accepted at 0.3 (inclusive)
+            for t in texts[4::13]:
+                tab.add(t, "", 0.95)  # an empty answer is never accepted
+            for t in texts[::27]:
+                tab.add(t, "rewritten " + t[:6], 0.6)  # overwrite: the latest add wins
+            extra["backend"] = StubBackend(tab)
         return _router(corpus, **extra)
 
-    seq, bat = mk(), mk()
+    seq, bat = mk(), mk(device=True)
     qs = [validate_query(t, "s", query_id=f"q{i}", issued_at_ns=i) for i, t in enumerate(texts)]
     want = [_sig(*seq.route(q)) for q in qs]
     got = []

@@ -114,7 +114,8 @@ def _sim_logs(rc, router, rows, n_sessions=2, per_session=150, seed=23):
     return [list(log.to_jsonl_lines()) for log in rc.run_simulation(cfg, router, rows)]
 
 
-@pytest.mark.parametrize("variant", ["lru_caches", "permuted", "disabled", "recall_table", "thresholds"])
+@pytest.mark.parametrize("variant", ["lru_caches", "permuted", "disabled", "recall_table", "thresholds",
+                                     "device_recall_table"])
 def test_live_ab_against_reference_stores(gpu, rc, variant):
     """Live A/B on the GPU box: the reference simulation through the reference router, once
     with the reference's own stores and once with the GPU drop-ins (same config, same seed),
@@ -138,11 +139,13 @@ def test_live_ab_against_reference_stores(gpu, rc, variant):
     elif variant == "thresholds":
         cfg_kw.update(semantic_threshold=0.6, akm_threshold=0.5, retrieval_k=2, akm_seed_k=5)
 
-    def backend():
-        tab = rc.StubKnowledgeTable()
-        if variant == "recall_table":
-            for r in rows[::5]:
-                tab.add(r["question"], "recalled: " + r["answer"], 0.8)
+    def backend(stores):
+        # device_recall_table: the reference's StubBackend over the GPU recall table
+        tab = g.DeviceKnowledgeTable() if variant == "device_recall_table" and stores == "gpu" else \
+            rc.StubKnowledgeTable()
+        if variant in ("recall_table", "device_recall_table"):
+            for i, r in enumerate(rows[::5]):
+                tab.add(r["question"], "recalled: " + r["answer"], 0.8 if i % 4 else 0.4)
         return rc.StubBackend(tab)
 
     def build(stores):
@@ -158,7 +161,7 @@ def test_live_ab_against_reference_stores(gpu, rc, variant):
             kw = dict(kv_cache=g.FixedKVCache(**kv_kw),
                       semantic_cache=g.SemanticCache(emb, threshold=cfg.semantic_threshold, **sc_kw),
                       adaptive_memory=g.AdaptiveKnowledgeMemory(threshold=cfg.akm_threshold))
-        r = rc.CascadeRouter(embedder=emb, backend=backend(), knowledge_base=kb, config=cfg, **kw)
+        r = rc.CascadeRouter(embedder=emb, backend=backend(stores), knowledge_base=kb, config=cfg, **kw)
         # the reference injects with ``kv_cache or FixedKVCache()`` (router.py:213-220): its OWN
         # empty stores are falsy and get replaced (dropping e.g. max_entries); pin the stores
         # passed on both sides so the A/B compares exactly these stores
@@ -171,7 +174,8 @@ def test_live_ab_against_reference_stores(gpu, rc, variant):
     assert got == want
 
 
-@pytest.mark.parametrize("variant", ["default", "permuted", "disabled", "recall_table", "thresholds"])
+@pytest.mark.parametrize("variant", ["default", "permuted", "disabled", "recall_table", "thresholds",
+                                     "device_recall_table", "device_recall_first"])
 def test_live_ab_route_batch_against_reference(gpu, rc, variant):
     """This package's CascadeRouter.route_batch (batches of 64, GPU stores) against the
     reference's run_simulation with the reference router and stores, live on the box:
@@ -191,13 +195,22 @@ def test_live_ab_route_batch_against_reference(gpu, rc, variant):
             return {"disabled_layers": frozenset({L.FIXED_KV, L.MEMORY_RECALL})}
         if variant == "thresholds":
             return {"semantic_threshold": 0.6, "akm_threshold": 0.5, "retrieval_k": 2, "akm_seed_k": 5}
+        if variant == "device_recall_first":
+            return {"layer_order": (L.MEMORY_RECALL, L.FIXED_KV, L.SEMANTIC_CACHE, L.ADAPTIVE_MEMORY, L.NAIVE_RAG),
+                    "recall_threshold": 0.4}
         return {}
 
     def table(mod):
-        tab = mod.StubKnowledgeTable()
-        if variant == "recall_table":
-            for r in rows[::5]:
-                tab.add(r["question"], "recalled: " + r["answer"], 0.8)
+        # device_recall_*: this package's side keeps the table on the GPU (L3 decided by
+        # pr_recall_gate inside route_batch); the reference keeps its dict
+        dev = variant.startswith("device_recall") and mod is g
+        tab = g.DeviceKnowledgeTable() if dev else mod.StubKnowledgeTable()
+        if variant == "recall_table" or variant.startswith("device_recall"):
+            for i, r in enumerate(rows[::5]):
+                tab.add(r["question"], "recalled: " + r["answer"], 0.8 if i % 4 else 0.4)
+            if variant.startswith("device_recall"):
+                for r in rows[1::17]:
+                    tab.add(r["question"], "", 0.9)  # empty answers are rejected
         return tab
 
     # reference: its own router, stores and simulation driver

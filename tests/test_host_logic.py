@@ -90,3 +90,20 @@ def test_vector_contract():
         coerce_index_vector(bad, 8)
     with pytest.raises(DimensionMismatch):
         EmbeddingVector.wrap(v)  # default dim 1024
+
+
+def test_triples_reader_strict(tmp_path):
+    """generation._read_triples follows ragcascade/jsonl.py:12-49: blank lines skipped,
+    malformed JSON or a non-object raises MalformedJsonl with the 1-based line number."""
+    from paper_2506_21593_b200 import MalformedJsonl
+    from paper_2506_21593_b200.generation import _read_triples
+
+    p = tmp_path / "ok.jsonl"
+    p.write_text('{"question": "a", "answer": "b"}\n\n  \n{"question": "c", "answer": "d"}\n', encoding="utf-8")
+    assert [o["question"] for o in _read_triples(p)] == ["a", "c"]
+    for body, line in (('{"q": 1}\n{oops\n', 2), ('"str"\n', 1)):
+        bad = tmp_path / "bad.jsonl"
+        bad.write_text(body, encoding="utf-8")
+        with pytest.raises(MalformedJsonl) as ei:
+            _read_triples(bad)
+        assert ei.value.line_number == line
