@@ -157,24 +157,25 @@ int pr_index_snap_flags(const pr_index *h, const float *d_q, int64_t nq, int k, 
 
 /* ---- fixed KV cache: caches.py:45-101 (FixedKVCache) --------------------
  * Keys are the UTF-8 bytes of the query text, compared BYTE-EXACT like the
- * reference dict (caches.py:57-65): 32-byte buckets of four
- * {32-bit tag, record index} slots and 32-byte aligned records {value, length,
- * key bytes}; a tag match is confirmed against the record bytes, so a hash
- * collision can never serve another key's answer.  Key batches are a UTF-8
+ * reference dict (caches.py:57-65): a linear-probing array of
+ * 32-byte slots {16-byte key prefix, length|value, 32-bit tag, record index},
+ * one 256-bit load per probe step, keys longer than 16 bytes completed by a
+ * 32-byte aligned record; a hit is confirmed against the stored key bytes, so a
+ * hash collision can never serve another key's answer.  Key batches are a UTF-8
  * arena d_bytes + int64 offsets d_off[n+1] (key i = d_bytes[d_off[i]..d_off[i+1])).
  * Values are non-negative int64 write sequence numbers: a larger value is a
  * later write, so puts of one key in one batch resolve last-write-wins
  * (caches.py:67-74).  The *_owned variants act only on the keys a shard owns
- * (owner = pr_kv_owner, bits disjoint from the bucket index); the other keys
+ * (owner = pr_kv_owner, bits disjoint from the slot index); the other keys
  * are skipped (get: value -1, hit 0) without touching the table. */
 int pr_kv_create(int64_t capacity, pr_kv **out);
-/* flags: PR_KV_WEAK_HASH keeps 2 tag bits and 4 home buckets, so distinct keys collide
+/* flags: PR_KV_WEAK_HASH keeps 2 tag bits and 4 home slots, so distinct keys collide
  * on purpose — a test hook for the byte-exact confirmation; never used by the product */
 #define PR_KV_WEAK_HASH 1u
 int pr_kv_create_ex(int64_t capacity, uint32_t flags, pr_kv **out);
 int pr_kv_destroy(pr_kv *h);
 /* hash n keys -> d_fp[2i] = tag (32-bit, top bit set; also picks the shard owner),
- * d_fp[2i+1] = bucket hash (32-bit, independent chain) */
+ * d_fp[2i+1] = home-slot hash (32-bit, independent chain) */
 int pr_fingerprint(const uint8_t *d_bytes, const int64_t *d_off, int64_t n, uint64_t *d_fp, void *stream);
 void pr_fingerprint_host(const uint8_t *bytes, int64_t len, uint64_t out[2]);
 /* shard owner of each key for a table hash-partitioned over `world` ranks */

@@ -6,41 +6,44 @@
 // collision (accidental or constructed) can only cost a probe, never serve another key's
 // answer.
 //
-// Why the layout is what it is (measured, scripts/micro/randload.cu + profiles/):
-// on B200 a random 32-byte read costs a whole 128-byte L2 line from DRAM (4 sectors per
-// request, whatever the load flavour), so the unit of cost is the LINE.  One lookup
-// therefore touches exactly one random line, and that line holds everything the lookup
-// needs for keys of <= 16 bytes:
+// Why the layout is what it is (measured on B200, scripts/micro/{randline,kvbench,kvslot}.cu):
+// * a random read costs one 128-byte line of DRAM whatever its width, and HBM3e serves
+//   ~45 G random lines/s (5.8 TB/s) — random lines are NOT the problem;
+// * two or more loads in flight to the same missing line are far slower than one (three
+//   16-byte loads of one line: 12 G lookups/s vs 24), and a dependent second access to a
+//   line just fetched (an L2 hit) still costs a full L2 round trip per lookup;
+// so a lookup should be ONE load of ONE sector.  The table is an array of 32-byte SLOTS
+// (one sector each, nslots a power of two, load <= 3/8), probed with one 256-bit load:
 //
-//   lines  128-byte bucket lines of 4 slots (nslots a power of two, load <= 0.5), laid out
-//          structure-of-arrays (see KvTable): u32 tag[4] | u32 rec[4] | u64 len|value[4] |
-//          16-byte key prefix[4].  tag = 32-bit key hash, top bit forced (0 = EMPTY,
-//          1 = TOMBSTONE, 2 = BUSY while an insert fills the slot); rec = record index of
-//          a key longer than 16 bytes, in 32-byte units; value < 2^40.
+//   slot   [0,16) key prefix (zero padded; keys <= 16 bytes live here whole)
+//          [16,24) u64 len (24 bits) | value << 24
+//          [24,28) u32 tag: 0 = EMPTY, 1 = TOMBSTONE, 2 = BUSY (claimed, being written),
+//                  else the 32-bit key hash with its top bit set
+//          [28,32) u32 record index of a key longer than 16 bytes, in 32-byte units
 //   arena  32-byte aligned records: the full bytes of keys longer than 16 bytes.
-// A probe reads the 16-byte tag vector of its line (one request; the line comes from DRAM
-// once); only on a tag match does it read that slot's length/value and prefix (L2 hits on
-// the line just fetched) and, for a long key, the rest of the bytes from the record.
+//
+// A key of <= 16 bytes is confirmed byte for byte from the slot it loaded (tag, length and
+// the 16 bytes); a longer key also compares its tail against its record.  Linear probing by
+// slot: at load <= 3/8 most keys are found (or proven absent by an EMPTY slot) in the home
+// slot, and the next slot is the adjacent sector of the same line.  Round 2's 128-byte
+// bucket lines (tag vector first, slot body on a match) ran 24 G lookups/s at 4M-key
+// batches; one 32-byte slot per load runs ~32 G at this load (kvslot.cu).
 // Hash: two 32-bit multiply-rotate chains over the key's little-endian words (murmur3_32
-// round function, two seeds).  hA -> tag (and shard owner), hB -> home bucket: the
-// ownership bits and the bucket bits come from independent chains.  Only 32-bit integer
+// round function, two seeds).  hA -> tag (and shard owner), hB -> home slot: the
+// ownership bits and the slot bits come from independent chains.  Only 32-bit integer
 // multiplies: the hash is a short dependency chain per key.
 //
 // One thread per key: it hashes its key ONCE (aligned 32-bit loads + funnel shifts, not
-// byte loads), so a warp keeps 32 independent lines in flight; the per-key tag vector is
-// 4 registers, which keeps occupancy high.  Measured alternatives (scripts/micro/kvbench.cu,
-// DESIGN.md §4.4): warp-cooperative 4-lane groups loading the whole line (one 256-bit load
-// per lane) were slower (19-20 vs 24.9 G lookups/s at 4M-key batches), as were 2 or 4 keys
-// per thread and a separate hashing kernel.  Keys whose line is full of other keys continue
-// by linear probing.  Values are write sequence numbers supplied by the host; a put
-// resolves an existing key with atomicMax on len|value, so the largest (latest) write wins
-// even when one batch writes a key twice (caches.py:67-74).
+// byte loads), so a warp keeps 32 independent slots in flight.  Values are write sequence
+// numbers supplied by the host; a put resolves an existing key with atomicMax on len|value,
+// so the largest (latest) write wins even when one batch writes a key twice
+// (caches.py:67-74).
 #include <algorithm>
 
 #include "common.cuh"
 
 struct pr_kv {
-    uint8_t *lines = nullptr;               // [nslots / 4] 128-byte bucket lines
+    uint8_t *lines = nullptr;               // [nslots] 32-byte slots
     int64_t nslots = 0;
     uint8_t *arena = nullptr;               // records
     int64_t arena_cap = 0;                  // bytes
@@ -52,7 +55,6 @@ struct pr_kv {
 
 namespace pr {
 
-constexpr int KV_BUCKET = 4;  // 32-byte slots per 128-byte bucket line
 constexpr int KV_THREADS = 128;
 constexpr int KV_INLINE = 16;                        // key bytes held in the slot
 constexpr uint32_t TAG_EMPTY = 0, TAG_TOMB = 1;
@@ -179,39 +181,27 @@ static inline void hash_host(const uint8_t *p, int64_t len, uint32_t &tag, uint3
     h.fin(len, tag, hb);
 }
 
-// One 128-byte bucket line, structure-of-arrays so a probe reads only what it needs:
-//   [0, 16)    u32 tag[4]       0 = EMPTY, 1 = TOMBSTONE, 2 = BUSY (claimed, being written)
-//   [16, 32)   u32 rec[4]       record of a key longer than 16 bytes, in 32-byte units
-//   [32, 64)   u64 lv[4]        key length (24 bits) | value << 24
-//   [64, 128)  16-byte key prefix[4] (zero padded)
-// A probe loads the 16-byte tag vector (the line comes from DRAM once); only a tag match
-// reads that slot's lv and prefix (L2 hits on the line just fetched).
+// One 32-byte slot (see the file comment): prefix | len|value | tag | record index.
 constexpr uint32_t TAG_BUSY = 2;
-constexpr int64_t KV_LINE = 128;
+constexpr int64_t KV_SLOT = 32;
 
 __host__ __device__ __forceinline__ uint64_t pack_lv(int64_t len, int64_t val) {
     return (uint64_t)len | ((uint64_t)val << 24);
 }
 
 struct KvTable {
-    uint8_t *lines;  // [nb][128]
-    int64_t nb;      // buckets (power of two)
+    uint8_t *slots;  // [ns][32]
+    int64_t ns;      // slots (power of two)
     uint8_t *arena;
     unsigned long long *counts;
-    int weak;  // PR_KV_WEAK_HASH: 2-bit tags, 4 home buckets (forces collisions; tests only)
-    __device__ __forceinline__ uint8_t *line(int64_t b) const { return lines + b * KV_LINE; }
-    __device__ __forceinline__ uint32_t *tag(int64_t b, int j) const {
-        return reinterpret_cast<uint32_t *>(line(b)) + j;
+    int weak;  // PR_KV_WEAK_HASH: 2-bit tags, 4 home slots (forces collisions; tests only)
+    __device__ __forceinline__ uint8_t *slot(int64_t s) const { return slots + s * KV_SLOT; }
+    __device__ __forceinline__ uint4 *prefix(int64_t s) const { return reinterpret_cast<uint4 *>(slot(s)); }
+    __device__ __forceinline__ unsigned long long *lv(int64_t s) const {
+        return reinterpret_cast<unsigned long long *>(slot(s) + 16);
     }
-    __device__ __forceinline__ uint32_t *rec(int64_t b, int j) const {
-        return reinterpret_cast<uint32_t *>(line(b) + 16) + j;
-    }
-    __device__ __forceinline__ unsigned long long *lv(int64_t b, int j) const {
-        return reinterpret_cast<unsigned long long *>(line(b) + 32) + j;
-    }
-    __device__ __forceinline__ uint4 *prefix(int64_t b, int j) const {
-        return reinterpret_cast<uint4 *>(line(b) + 64) + j;
-    }
+    __device__ __forceinline__ uint32_t *tag(int64_t s) const { return reinterpret_cast<uint32_t *>(slot(s) + 24); }
+    __device__ __forceinline__ uint32_t *rec(int64_t s) const { return reinterpret_cast<uint32_t *>(slot(s) + 28); }
 };
 
 struct KeyBatch {
@@ -260,22 +250,26 @@ __device__ __forceinline__ bool tail_matches(const uint8_t *rec, const KeyRef &k
     return true;
 }
 
-// slot (b, j) carries the key's tag: does it hold the key?  *val = its value if so.
+// slot s carries the key's tag: does it hold the key?  *val = its value if so.
 template <bool STRONG>
-__device__ __forceinline__ bool slot_holds(const KvTable &t, int64_t b, int j, const KeyRef &k, const uint32_t pw[4],
+__device__ __forceinline__ bool slot_holds(const KvTable &t, int64_t s, const KeyRef &k, const uint32_t pw[4],
                                            int64_t *val) {
-    const uint64_t lv = ld8<STRONG>(t.lv(b, j));
-    const uint4 pre = ld4<STRONG>(t.prefix(b, j));
+    const uint64_t lv = ld8<STRONG>(t.lv(s));
+    const uint4 pre = ld4<STRONG>(t.prefix(s));
     if ((int64_t)(lv & 0xffffffull) != k.len || pre.x != pw[0] || pre.y != pw[1] || pre.z != pw[2] || pre.w != pw[3])
         return false;
-    if (k.len > KV_INLINE &&
-        !tail_matches<STRONG>(t.arena + ((int64_t)ld4b<STRONG>(t.rec(b, j)) << 5), k))
+    if (k.len > KV_INLINE && !tail_matches<STRONG>(t.arena + ((int64_t)ld4b<STRONG>(t.rec(s)) << 5), k))
         return false;
     *val = (int64_t)(lv >> 24);
     return true;
 }
 
-// ---- get: one thread per key -------------------------------------------------
+// the whole slot in one 256-bit load (one sector)
+__device__ __forceinline__ void ld_slot(const uint8_t *p, uint64_t &w0, uint64_t &w1, uint64_t &w2, uint64_t &w3) {
+    asm("ld.global.cg.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(w0), "=l"(w1), "=l"(w2), "=l"(w3) : "l"(p));
+}
+
+// ---- get: one thread per key, one 32-byte slot per probe step ----------------
 __global__ void __launch_bounds__(KV_THREADS) kv_get_kernel(KvTable t, KeyBatch kb, int rank, int world,
                                                              int64_t *__restrict__ out_vals,
                                                              uint8_t *__restrict__ out_hit) {
@@ -287,26 +281,19 @@ __global__ void __launch_bounds__(KV_THREADS) kv_get_kernel(KvTable t, KeyBatch 
     hash_key(k, t.weak, tag, hb, pw);
     int64_t val = -1;
     if (world <= 1 || owner_of(tag, world) == rank) {
-        int64_t b = (int64_t)(hb & (uint32_t)(t.nb - 1));
-        for (int64_t p = 0; p < t.nb; ++p) {
-            const uint4 tg = ld4<false>(t.tag(b, 0));
-            const uint32_t tv[4] = {tg.x, tg.y, tg.z, tg.w};
-            bool done = false;
-#pragma unroll
-            for (int j = 0; j < KV_BUCKET; ++j) {
-                if (done) break;
-                if (tv[j] == tag) {
-                    int64_t v;
-                    if (slot_holds<false>(t, b, j, k, pw, &v)) {
-                        val = v;
-                        done = true;
-                    }
-                } else if (tv[j] == TAG_EMPTY) {
-                    done = true;
-                }
+        const uint64_t k0 = ((uint64_t)pw[1] << 32) | pw[0], k1 = ((uint64_t)pw[3] << 32) | pw[2];
+        int64_t s = (int64_t)(hb & (uint32_t)(t.ns - 1));
+        for (int64_t p = 0; p < t.ns; ++p) {
+            uint64_t w0, w1, w2, w3;
+            ld_slot(t.slot(s), w0, w1, w2, w3);
+            const uint32_t st = (uint32_t)w3;
+            if (st == TAG_EMPTY) break;
+            if (st == tag && w0 == k0 && w1 == k1 && (int64_t)(w2 & 0xffffffull) == k.len &&
+                (k.len <= KV_INLINE || tail_matches<false>(t.arena + ((int64_t)(uint32_t)(w3 >> 32) << 5), k))) {
+                val = (int64_t)(w2 >> 24);
+                break;
             }
-            if (done) break;
-            b = (b + 1) & (t.nb - 1);
+            s = (s + 1) & (t.ns - 1);
         }
     }
     out_vals[i] = val;
@@ -321,13 +308,13 @@ __device__ void write_record(uint8_t *rec, const KeyRef &k) {
 }
 
 // fill a claimed slot and publish its tag (the slot's other fields become visible first)
-__device__ __forceinline__ void publish(const KvTable &t, int64_t b, int j, uint32_t tag, uint32_t rec, uint64_t lv,
+__device__ __forceinline__ void publish(const KvTable &t, int64_t s, uint32_t tag, uint32_t rec, uint64_t lv,
                                         uint4 pre) {
-    *t.rec(b, j) = rec;
-    *t.lv(b, j) = lv;
-    *t.prefix(b, j) = pre;
+    *t.rec(s) = rec;
+    *t.lv(s) = lv;
+    *t.prefix(s) = pre;
     __threadfence();
-    atomicExch(t.tag(b, j), tag);
+    atomicExch(t.tag(s), tag);
 }
 
 // ---- put (upsert) / erase: one thread per key --------------------------------
@@ -345,53 +332,51 @@ __global__ void __launch_bounds__(KV_THREADS) kv_update_kernel(KvTable t, KeyBat
     hash_key(k, t.weak, tag, hb, pw);
     if (world > 1 && owner_of(tag, world) != rank) return;
     const int64_t v = ERASE ? -1 : in_vals[i];
-    int64_t b = (int64_t)(hb & (uint32_t)(t.nb - 1));
-    for (int64_t p = 0; p < t.nb; ++p) {
-        for (int j = 0; j < KV_BUCKET; ++j) {
-            uint32_t cur = ld4b<true>(t.tag(b, j));
-            for (;;) {  // re-examines slot j after a lost CAS / a pending publication
-                if (cur == TAG_BUSY) {
-                    do {
-                        __nanosleep(32);
-                        cur = ld4b<true>(t.tag(b, j));
-                    } while (cur == TAG_BUSY);
-                    continue;
-                }
-                if (cur == tag) {
-                    __threadfence();  // pairs with publish(): the slot's fields are visible
-                    int64_t old;
-                    if (slot_holds<true>(t, b, j, k, pw, &old)) {
-                        if (ERASE) {
-                            if (atomicCAS(t.tag(b, j), tag, TAG_TOMB) == tag) {
-                                atomicAdd(&t.counts[0], (unsigned long long)-1ll);
-                                atomicAdd(&t.counts[1], 1ull);
-                                atomicAdd(&t.counts[3], (unsigned long long)rec_bytes(k.len));
-                            }
-                        } else {
-                            atomicMax(t.lv(b, j), (unsigned long long)pack_lv(k.len, v));
-                        }
-                        return;
-                    }
-                    break;  // same tag, another key
-                }
-                if (cur != TAG_EMPTY) break;  // another key or a tombstone: next slot
-                if (ERASE) return;            // first empty slot: the key is absent
-                const uint32_t got = atomicCAS(t.tag(b, j), TAG_EMPTY, TAG_BUSY);
-                if (got != TAG_EMPTY) {  // lost the race: look at what was claimed there
-                    cur = got;
-                    continue;
-                }
-                int64_t rec = 0;
-                if (k.len > KV_INLINE) {
-                    rec = (int64_t)atomicAdd(&t.counts[2], (unsigned long long)rec_bytes(k.len));
-                    write_record(t.arena + rec, k);
-                }
-                publish(t, b, j, tag, (uint32_t)(rec >> 5), pack_lv(k.len, v), make_uint4(pw[0], pw[1], pw[2], pw[3]));
-                atomicAdd(&t.counts[0], 1ull);
-                return;
+    int64_t s = (int64_t)(hb & (uint32_t)(t.ns - 1));
+    for (int64_t p = 0; p < t.ns; ++p) {
+        uint32_t cur = ld4b<true>(t.tag(s));
+        for (;;) {  // re-examines slot s after a lost CAS / a pending publication
+            if (cur == TAG_BUSY) {
+                do {
+                    __nanosleep(32);
+                    cur = ld4b<true>(t.tag(s));
+                } while (cur == TAG_BUSY);
+                continue;
             }
+            if (cur == tag) {
+                __threadfence();  // pairs with publish(): the slot's fields are visible
+                int64_t old;
+                if (slot_holds<true>(t, s, k, pw, &old)) {
+                    if (ERASE) {
+                        if (atomicCAS(t.tag(s), tag, TAG_TOMB) == tag) {
+                            atomicAdd(&t.counts[0], (unsigned long long)-1ll);
+                            atomicAdd(&t.counts[1], 1ull);
+                            atomicAdd(&t.counts[3], (unsigned long long)rec_bytes(k.len));
+                        }
+                    } else {
+                        atomicMax(t.lv(s), (unsigned long long)pack_lv(k.len, v));
+                    }
+                    return;
+                }
+                break;  // same tag, another key
+            }
+            if (cur != TAG_EMPTY) break;  // another key or a tombstone: next slot
+            if (ERASE) return;            // first empty slot: the key is absent
+            const uint32_t got = atomicCAS(t.tag(s), TAG_EMPTY, TAG_BUSY);
+            if (got != TAG_EMPTY) {  // lost the race: look at what was claimed there
+                cur = got;
+                continue;
+            }
+            int64_t rec = 0;
+            if (k.len > KV_INLINE) {
+                rec = (int64_t)atomicAdd(&t.counts[2], (unsigned long long)rec_bytes(k.len));
+                write_record(t.arena + rec, k);
+            }
+            publish(t, s, tag, (uint32_t)(rec >> 5), pack_lv(k.len, v), make_uint4(pw[0], pw[1], pw[2], pw[3]));
+            atomicAdd(&t.counts[0], 1ull);
+            return;
         }
-        b = (b + 1) & (t.nb - 1);
+        s = (s + 1) & (t.ns - 1);
     }
 }
 
@@ -415,23 +400,19 @@ __device__ __forceinline__ bool live_tag(uint32_t tag) { return (tag & 0x8000000
 
 __global__ void kv_export_kernel(KvTable t, int64_t nslots, int64_t *val_out, int64_t max, unsigned long long *cursor) {
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nslots; s += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t b = s / KV_BUCKET;
-        const int j = (int)(s % KV_BUCKET);
-        if (live_tag(*t.tag(b, j))) {
+        if (live_tag(*t.tag(s))) {
             unsigned long long p = atomicAdd(cursor, 1ull);
-            if ((int64_t)p < max) val_out[p] = (int64_t)(*t.lv(b, j) >> 24);
+            if ((int64_t)p < max) val_out[p] = (int64_t)(*t.lv(s) >> 24);
         }
     }
 }
 
 __global__ void kv_remap_kernel(KvTable t, int64_t nslots, const int64_t *__restrict__ map, int64_t nmap) {
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nslots; s += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t b = s / KV_BUCKET;
-        const int j = (int)(s % KV_BUCKET);
-        if (live_tag(*t.tag(b, j))) {
-            const uint64_t lv = *t.lv(b, j);
+        if (live_tag(*t.tag(s))) {
+            const uint64_t lv = *t.lv(s);
             const int64_t v = (int64_t)(lv >> 24);
-            if (v >= 0 && v < nmap) *t.lv(b, j) = pack_lv((int64_t)(lv & 0xffffffull), map[v]);
+            if (v >= 0 && v < nmap) *t.lv(s) = pack_lv((int64_t)(lv & 0xffffffull), map[v]);
         }
     }
 }
@@ -440,16 +421,14 @@ __global__ void kv_remap_kernel(KvTable t, int64_t nslots, const int64_t *__rest
 // (no duplicates exist); long keys' records move into a fresh, compacted arena
 __global__ void kv_rebuild_kernel(KvTable o, int64_t old_slots, KvTable t) {
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < old_slots; s += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t ob = s / KV_BUCKET;
-        const int oj = (int)(s % KV_BUCKET);
-        if (!live_tag(*o.tag(ob, oj))) continue;
-        const uint64_t lv = *o.lv(ob, oj);
-        const uint4 pre = *o.prefix(ob, oj);
+        if (!live_tag(*o.tag(s))) continue;
+        const uint64_t lv = *o.lv(s);
+        const uint4 pre = *o.prefix(s);
         const int64_t len = (int64_t)(lv & 0xffffffull);
         int64_t rec = 0;
         uint32_t tag, hb, pw[4];
         if (len > KV_INLINE) {
-            const uint8_t *src = o.arena + ((int64_t)*o.rec(ob, oj) << 5);
+            const uint8_t *src = o.arena + ((int64_t)*o.rec(s) << 5);
             const int64_t rb = rec_bytes(len);
             rec = (int64_t)atomicAdd(&t.counts[2], (unsigned long long)rb);
             for (int64_t x = 0; x < rb; x += 8)
@@ -459,29 +438,29 @@ __global__ void kv_rebuild_kernel(KvTable o, int64_t old_slots, KvTable t) {
             hash_inline((uint64_t)pre.x | ((uint64_t)pre.y << 32), (uint64_t)pre.z | ((uint64_t)pre.w << 32), len,
                         t.weak, tag, hb);
         }
-        int64_t b = (int64_t)(hb & (uint32_t)(t.nb - 1));
-        bool done = false;
-        for (int64_t p = 0; p < t.nb && !done; ++p) {
-            for (int j = 0; j < KV_BUCKET && !done; ++j) {
-                if (atomicCAS(t.tag(b, j), TAG_EMPTY, TAG_BUSY) == TAG_EMPTY) {
-                    publish(t, b, j, tag, (uint32_t)(rec >> 5), lv, pre);
-                    atomicAdd(&t.counts[0], 1ull);
-                    done = true;
-                }
+        int64_t q = (int64_t)(hb & (uint32_t)(t.ns - 1));
+        for (int64_t p = 0; p < t.ns; ++p) {
+            if (atomicCAS(t.tag(q), TAG_EMPTY, TAG_BUSY) == TAG_EMPTY) {
+                publish(t, q, tag, (uint32_t)(rec >> 5), lv, pre);
+                atomicAdd(&t.counts[0], 1ull);
+                break;
             }
-            b = (b + 1) & (t.nb - 1);
+            q = (q + 1) & (t.ns - 1);
         }
     }
 }
 
+// sizing: at most 3/16 full when built for `keys` (100M keys -> 2^29 slots, 17 GB); a put
+// that would pass 3/8 (live + tombstones) rebuilds at twice the size
 static int64_t slots_for(int64_t keys) {
     int64_t s = 1024;
-    while (s < 2 * keys) s *= 2;  // load factor <= 0.5
+    while (3 * s < 16 * keys) s *= 2;
     return s;
 }
+static bool over_load(int64_t used, int64_t nslots) { return 8 * used > 3 * nslots; }
 
 static KvTable table_of(pr_kv *h) {
-    return KvTable{h->lines, h->nslots / KV_BUCKET, h->arena, h->d_count, (h->flags & PR_KV_WEAK_HASH) ? 1 : 0};
+    return KvTable{h->lines, h->nslots, h->arena, h->d_count, (h->flags & PR_KV_WEAK_HASH) ? 1 : 0};
 }
 
 static int read_counts(pr_kv *h, unsigned long long c[4], cudaStream_t st) {
@@ -574,13 +553,13 @@ static int put_impl(pr_kv *h, const uint8_t *d_bytes, const int64_t *d_off, int6
     if (n == 0) return PR_OK;
     cudaStream_t st = as_stream(stream);
     const int64_t rec_need = n * 31 + nbytes;  // >= sum of rec_bytes over the batch
-    if (2 * (h->upper + n) > h->nslots || h->arena_upper + rec_need > h->arena_cap) {
+    if (over_load(h->upper + n, h->nslots) || h->arena_upper + rec_need > h->arena_cap) {
         unsigned long long c[4];
         rc = read_counts(h, c, st);
         if (rc) return rc;
         h->upper = (int64_t)(c[0] + c[1]);
         h->arena_upper = (int64_t)c[2];
-        const bool slots_short = 2 * (h->upper + n) > h->nslots;
+        const bool slots_short = over_load(h->upper + n, h->nslots);
         const bool arena_short = h->arena_upper + rec_need > h->arena_cap;
         if (slots_short) {
             rc = rebuild(h, (int64_t)c[0] + n, (int64_t)(c[2] - c[3]) - KV_ARENA_BASE + rec_need, st);

@@ -2,10 +2,10 @@
 
 Rank r owns the keys whose hash maps to r: ``owner = (tag & 0x7fffffff) % world`` where
 tag is the key's 32-bit tag hash (``owner_host`` / device ``pr_kv_owner``).  The table's
-home bucket comes from the OTHER, independent hash chain, so the ownership bits and the
-bucket bits are disjoint: every bucket of a rank's table is a home bucket
-for its keys (round 1 took both from the same low bits, so at world 8 only 1/8 of a
-rank's buckets could be home buckets).
+home slot comes from the OTHER, independent hash chain, so the ownership bits and the
+slot bits are disjoint: every slot of a rank's table is a home slot for its keys
+(round 1 took both from the same low bits, so at world 8 only 1/8 of a rank's buckets
+could be home buckets).
 
 A put inserts only the keys a rank owns; a lookup runs ``pr_kv_get_text_owned`` on every
 rank over the whole (broadcast) batch, which hashes each key once and probes only the

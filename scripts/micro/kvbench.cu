@@ -1,4 +1,7 @@
-// Standalone harness for KV probe kernel variants (includes the library's kv.cu).
+// Standalone harness for the KV probe kernel (includes the library's kv.cu) and two
+// diagnostics: the front half alone (offsets, key words, hash) and + the home-slot load.
+// Round-2 results of the 128-byte bucket-line layout and its variants are in
+// profiles/r02_kv_layout_experiments.txt.
 // Builds a 100M-key table of "query-%09d" keys through pr_kv_put_text, then times
 // lookups: B=65536 batches on S concurrent streams (graph-free, back to back) and one
 // 4M-key batch, for each variant.  Parity is checked for every variant.
@@ -23,55 +26,23 @@ void count_launch() {}
 int sm_count() { return 148; }
 
 
-// K keys per thread, interleaved (more independent probes in flight per thread)
-template <int K>
-__global__ void __launch_bounds__(KV_THREADS) get_multi(KvTable t, KeyBatch kb, int64_t *out_vals, uint8_t *out_hit) {
-    const int64_t base = blockIdx.x * (int64_t)blockDim.x * K + threadIdx.x;
-    int64_t a[K], len[K];
-    uint32_t tag[K], hb[K], pw[K][4];
-    bool have[K];
-#pragma unroll
-    for (int q = 0; q < K; ++q) {
-        const int64_t i = base + q * blockDim.x;
-        have[q] = i < kb.n;
-        a[q] = have[q] ? __ldg(kb.off + i) : 0;
-        len[q] = have[q] ? __ldg(kb.off + i + 1) - a[q] : 0;
+// diagnostics (wrong results by design): the front half alone (offsets, key words, hash)
+// and the front half + the tag-vector load (no slot body)
+template <int TAGS>
+__global__ void __launch_bounds__(KV_THREADS) get_diag(KvTable t, KeyBatch kb, int64_t *out_vals, uint8_t *out_hit) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= kb.n) return;
+    const int64_t a = __ldg(kb.off + i);
+    const KeyRef k(kb.bytes + a, __ldg(kb.off + i + 1) - a);
+    uint32_t tag, hb, pw[4];
+    hash_key(k, t.weak, tag, hb, pw);
+    int64_t v = tag ^ pw[0];
+    if (TAGS) {
+        const uint4 tg = ld4<false>(t.slot((int64_t)(hb & (uint32_t)(t.ns - 1))));
+        v ^= tg.x ^ tg.y ^ tg.z ^ tg.w;
     }
-#pragma unroll
-    for (int q = 0; q < K; ++q) hash_key(KeyRef(kb.bytes + a[q], len[q]), t.weak, tag[q], hb[q], pw[q]);
-    uint4 tg[K];
-    int64_t b[K];
-#pragma unroll
-    for (int q = 0; q < K; ++q) {
-        b[q] = (int64_t)(hb[q] & (uint32_t)(t.nb - 1));
-        tg[q] = have[q] ? ld4<false>(t.tag(b[q], 0)) : make_uint4(0, 0, 0, 0);
-    }
-#pragma unroll
-    for (int q = 0; q < K; ++q) {
-        if (!have[q]) continue;
-        const KeyRef k(kb.bytes + a[q], len[q]);
-        int64_t val = -1;
-        int64_t bb = b[q];
-        uint4 cur = tg[q];
-        for (int64_t p = 0; p < t.nb; ++p) {
-            const uint32_t tv[4] = {cur.x, cur.y, cur.z, cur.w};
-            bool done = false;
-            for (int j = 0; j < KV_BUCKET && !done; ++j) {
-                if (tv[j] == tag[q]) {
-                    int64_t v;
-                    if (slot_holds<false>(t, bb, j, k, pw[q], &v)) { val = v; done = true; }
-                } else if (tv[j] == TAG_EMPTY) {
-                    done = true;
-                }
-            }
-            if (done) break;
-            bb = (bb + 1) & (t.nb - 1);
-            cur = ld4<false>(t.tag(bb, 0));
-        }
-        const int64_t i = base + q * blockDim.x;
-        out_vals[i] = val;
-        out_hit[i] = val >= 0;
-    }
+    out_vals[i] = v;
+    out_hit[i] = v & 1;
 }
 }  // namespace pr
 
@@ -140,11 +111,11 @@ int main(int argc, char **argv) {
         KeyBatch kb{bb[j], bo[j], m};
         const unsigned g = (unsigned)((m + KV_THREADS - 1) / KV_THREADS);
         if (v == 0) kv_get_kernel<<<g, KV_THREADS, 0, s>>>(t, kb, 0, 1, bv[j], bh[j]);
-        if (v == 2) get_multi<2><<<(unsigned)((m + 2 * KV_THREADS - 1) / (2 * KV_THREADS)), KV_THREADS, 0, s>>>(t, kb, bv[j], bh[j]);
-        if (v == 4) get_multi<4><<<(unsigned)((m + 4 * KV_THREADS - 1) / (4 * KV_THREADS)), KV_THREADS, 0, s>>>(t, kb, bv[j], bh[j]);
+        if (v == 11) get_diag<0><<<g, KV_THREADS, 0, s>>>(t, kb, bv[j], bh[j]);
+        if (v == 12) get_diag<1><<<g, KV_THREADS, 0, s>>>(t, kb, bv[j], bh[j]);
     };
-    for (int v : {0, 2, 4}) {
-        for (int ns : {1, 4, 8}) {
+    for (int v : {0, 11, 12}) {
+        for (int ns : {1, 8}) {
             for (int rep = 0; rep < 2; ++rep) {
                 cudaDeviceSynchronize();
                 cudaEventRecord(e0, st[0]);
