@@ -26,6 +26,57 @@ void count_launch() {}
 int sm_count() { return 148; }
 
 
+// software-pipelined grid-stride loop: key j's slot load is in flight while key j+1's
+// offsets / key words load and hash
+struct FH {
+    int64_t len, a;
+    uint32_t tag, hb;
+    uint64_t k0, k1;
+};
+__device__ __forceinline__ FH front(const KvTable &t, const KeyBatch &kb, int64_t i) {
+    FH f;
+    f.a = __ldg(kb.off + i);
+    f.len = __ldg(kb.off + i + 1) - f.a;
+    const KeyRef k(kb.bytes + f.a, f.len);
+    uint32_t pw[4];
+    hash_key(k, t.weak, f.tag, f.hb, pw);
+    f.k0 = ((uint64_t)pw[1] << 32) | pw[0];
+    f.k1 = ((uint64_t)pw[3] << 32) | pw[2];
+    return f;
+}
+__global__ void __launch_bounds__(KV_THREADS) get_pipe(KvTable t, KeyBatch kb, int64_t *out_vals, uint8_t *out_hit) {
+    const int64_t T = (int64_t)gridDim.x * blockDim.x;
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= kb.n) return;
+    FH f = front(t, kb, i);
+    while (true) {
+        int64_t s = (int64_t)(f.hb & (uint32_t)(t.ns - 1));
+        uint64_t w0, w1, w2, w3;
+        ld_slot(t.slot(s), w0, w1, w2, w3);
+        const int64_t i2 = i + T;
+        FH g;
+        if (i2 < kb.n) g = front(t, kb, i2);
+        int64_t val = -1;
+        for (int64_t p = 0; p < t.ns; ++p) {
+            const uint32_t st = (uint32_t)w3;
+            if (st == TAG_EMPTY) break;
+            if (st == f.tag && w0 == f.k0 && w1 == f.k1 && (int64_t)(w2 & 0xffffffull) == f.len &&
+                (f.len <= KV_INLINE ||
+                 tail_matches<false>(t.arena + ((int64_t)(uint32_t)(w3 >> 32) << 5), KeyRef(kb.bytes + f.a, f.len)))) {
+                val = (int64_t)(w2 >> 24);
+                break;
+            }
+            s = (s + 1) & (t.ns - 1);
+            ld_slot(t.slot(s), w0, w1, w2, w3);
+        }
+        out_vals[i] = val;
+        out_hit[i] = val >= 0;
+        if (i2 >= kb.n) break;
+        i = i2;
+        f = g;
+    }
+}
+
 // diagnostics (wrong results by design): the front half alone (offsets, key words, hash)
 // and the front half + the tag-vector load (no slot body)
 template <int TAGS>
@@ -111,10 +162,13 @@ int main(int argc, char **argv) {
         KeyBatch kb{bb[j], bo[j], m};
         const unsigned g = (unsigned)((m + KV_THREADS - 1) / KV_THREADS);
         if (v == 0) kv_get_kernel<<<g, KV_THREADS, 0, s>>>(t, kb, 0, 1, bv[j], bh[j]);
+        if (v == 30) get_pipe<<<std::min<unsigned>(g, 148 * 16), KV_THREADS, 0, s>>>(t, kb, bv[j], bh[j]);
+        if (v == 31) get_pipe<<<std::min<unsigned>(g, 148 * 8), KV_THREADS, 0, s>>>(t, kb, bv[j], bh[j]);
+        if (v == 32) get_pipe<<<(g + 1) / 2, KV_THREADS, 0, s>>>(t, kb, bv[j], bh[j]);
         if (v == 11) get_diag<0><<<g, KV_THREADS, 0, s>>>(t, kb, bv[j], bh[j]);
         if (v == 12) get_diag<1><<<g, KV_THREADS, 0, s>>>(t, kb, bv[j], bh[j]);
     };
-    for (int v : {0, 11, 12}) {
+    for (int v : {0, 30, 31, 32}) {
         for (int ns : {1, 8}) {
             for (int rep = 0; rep < 2; ++rep) {
                 cudaDeviceSynchronize();
