@@ -546,6 +546,31 @@ def main():
 
             configs["c5_routed_sharded"] = {"error": f"{type(exc).__name__}: {exc}",
                                             "trace": traceback.format_exc()[-1500:]}
+        if os.environ.get("BENCH_C5_REPLICAS", "1") == "1":
+            # the other N-GPU layout: sessions are independent, so rank r routes
+            # sessions r, r+N, ... over its OWN full knowledge base (a 72 GB replica) with no
+            # collective at all; throughput = all ranks' routed queries / the slowest rank
+            try:
+                del idx, sh
+                torch.cuda.empty_cache()
+                full = build_shard(a.n, a.dim, 0, a.n)
+                r5 = C.c5_routed(full, a.n, n_sessions=a.c5_sessions, queries_per_session=a.c5_queries,
+                                 session_ids=range(rank, a.c5_sessions, world),
+                                 parity_queries=200 if rank == 0 else 0, l5_oracle_queries=0)
+                ms_max = max_over_ranks(r5["ms_total"])
+                total = sum_over_ranks(float(r5["queries"]))
+                r5["workload"] = r5["workload"].replace("(configs[4], 1 GPU)",
+                                                        f"(configs[4], sessions over {world} GPUs, KB replicated)")
+                r5.update(value=total / (ms_max / 1e3), ms_total=ms_max, queries=int(total),
+                          timing="max over ranks", knowledge_base=f"a full replica on each of the {world} GPUs",
+                          sessions=f"rank r routes sessions r, r+{world}, ... of {a.c5_sessions}")
+                configs["c5_routed_replicas"] = r5
+                del full
+            except Exception as exc:  # noqa: BLE001 - recorded, the headline stands
+                import traceback
+
+                configs["c5_routed_replicas"] = {"error": f"{type(exc).__name__}: {exc}",
+                                                 "trace": traceback.format_exc()[-1500:]}
     if rank == 0 and world == 1 and a.configs:
         import traceback
 

@@ -349,7 +349,8 @@ _LAST_BATCH_WALL: list = []  # (worker, session, batch, host wall ms) of every c
 
 
 def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_session=20_000, batch=4096,
-              seed=0, parity_queries=1000, profile=False, workers=1, l5_oracle_queries=8, shard=None):
+              seed=0, parity_queries=1000, profile=False, workers=1, l5_oracle_queries=8, shard=None,
+              session_ids=None):
     """Routed replay over the bench's 10M x 1024 store turned into a knowledge base:
     rows [0, n_qa) hold HashEmbedder(context) of the QA pool, the rest stay dense
     distractors.
@@ -357,7 +358,10 @@ def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_se
     ``workers`` > 1: that many routers (each its own KV / semantic cache / AKM, one
     shared knowledge base) replay the sessions concurrently from as many threads —
     sessions are independent, and one worker's host-side Python then
-    overlaps another's device scans on the shared GPU."""
+    overlaps another's device scans on the shared GPU.
+
+    ``session_ids``: replay only these of the ``n_sessions`` sessions (multi-GPU session
+    replicas: rank r of N routes sessions r, r+N, ... over its own full knowledge base)."""
     import threading
 
     import torch
@@ -401,7 +405,7 @@ def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_se
         r.latency_model = LatencyDraws(0.25)
         return r
 
-    workers = max(1, min(int(workers), n_sessions))
+    workers = max(1, min(int(workers), n_sessions if session_ids is None else max(1, len(list(session_ids)))))
     routers = [make_router() for _ in range(workers)]
     # warm-up: one whole session of an unrelated seed per router, untimed (first-launch
     # module loading; the stores and search scratch grow to their per-session size, and
@@ -442,8 +446,10 @@ def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_se
         except BaseException as exc:  # noqa: BLE001 - re-raised on the main thread
             errors.append(exc)
 
+    mine_s = list(range(n_sessions)) if session_ids is None else [int(x) for x in session_ids]
+
     def _replay_sessions(w, router, tally):
-        for s in range(w, n_sessions, workers):
+        for s in mine_s[w::workers]:
             router.reset_session()
             router.latency_model.reseed([seed, s, 1])
             qs = session_queries[s]
@@ -556,6 +562,7 @@ def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_se
                     f"{batch} (configs[4], {'1 GPU' if shard is None else 'KB row-sharded over all ranks'}), "
                     f"{workers} concurrent session worker(s)",
         "value": total / (ms / 1e3), "unit": "routed queries/s", "ms_total": ms, "workers": workers,
+        "queries": total, "sessions": mine_s,
         "knowledge_base": ("one GPU" if shard is None else
                            f"row-sharded: this rank holds rows [{int(shard)}, {int(shard) + store.n_local}); local "
                            "list scan + one all-gather merge per span, seed/AKM rows gathered from their owners"),
