@@ -20,3 +20,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:tc8_
     -o gpurun_out/tc8_scan_${R} python bench.py --steps 1 --warmup 3 --no-cpu-baseline --configs "" \
     > gpurun_out/ncu_full_${R}.log 2>&1
 tail -3 gpurun_out/ncu_full_${R}.log
+# the fixed-KV probe (C3 kernel): launches at B=65536 and one 4M-key batch over a 100M-key table
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:kv_get -s 3 -c 2 \
+    -o gpurun_out/kv_get_${R} python scripts/probe_kv2.py > gpurun_out/ncu_kv_${R}.log 2>&1
+tail -3 gpurun_out/ncu_kv_${R}.log
