@@ -1219,6 +1219,187 @@ __global__ void __launch_bounds__(W8_WARPS * 32) tc8_post_kernel(I8PostArgs a) {
     }
 }
 
+// The same post-processing with ONE CTA PER QUERY (the default): the warp-per-query kernel
+// above streams each candidate row through one lane pair with ~16 rows in flight per
+// query, so a query with many appended rows serialised ~16 DRAM round trips per batch of
+// 16 rows and set the kernel's tail (1.1 ms of a 34.5-ms C4 step).  Here 256 threads
+// select the `take` best appended rows by (u, row) with block-wide reductions, score them,
+// then filter EVERY appended row against the resulting exact bound L at once and score the
+// survivors P8_ROWS at a time (two threads per row: numpy's two einsum lanes), with the
+// rows' lines prefetched into L2 as soon as they are selected.  Same rows in, same exact
+// top-k out: any row with u < L has exact <= u < L <= e_k (strictly below the final k-th,
+// so not even a tie), whatever order the survivors are scored in.
+constexpr int P8_THREADS = 256;
+constexpr int P8_ROWS = P8_THREADS / 2;  // rows scored per round
+constexpr int P8_LIST = 2048;            // survivors buffered per pass over the appended rows
+
+__device__ __forceinline__ void prefetch_row_l2(const float *x, int dp8, int t, int nthreads) {
+    // 128-byte lines of one row, spread over the calling threads
+    const char *p = reinterpret_cast<const char *>(x);
+    for (int o = t * 128; o < dp8 * 4; o += nthreads * 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + o));
+}
+
+__global__ void __launch_bounds__(P8_THREADS) tc8_post_cta_kernel(I8PostArgs a) {
+    extern __shared__ __align__(16) float qs[];  // [dp8 + 8]
+    __shared__ double ts[TC_KP];
+    __shared__ int32_t tr[TC_KP];
+    __shared__ int32_t list[P8_LIST];
+    __shared__ double ex[P8_ROWS];
+    __shared__ uint64_t red[P8_THREADS / 32];
+    __shared__ int s_n, s_nl, s_scored;
+    __shared__ float s_L;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t nq_live = live_nq(a.nq_dev, a.nq);
+    for (int64_t q = blockIdx.x; q < nq_live; q += gridDim.x) {
+        const int take = (int)(a.row_limit ? min(a.take, max((int64_t)0, a.row_limit[q])) : a.take);
+        const int cnt = a.acount[q];
+        if (tid == 0) atomicAdd(&a.counters[3], cnt);
+        if (take > 0 && cnt > a.cap) {
+            if (tid == 0) a.fallback[atomicAdd(&a.counters[0], 1)] = (int32_t)q;
+            continue;  // uniform: every thread read the same cnt
+        }
+        const float *qv = a.qp + q * (int64_t)a.dp8;
+        if (take > 0) {
+            for (int j = tid; j < a.dp8; j += P8_THREADS) qs[j] = qv[j];
+            if (tid == 0) {
+                const int n0 = a.seed_n ? min(a.seed_n[q], take) : 0;
+                for (int j = 0; j < n0; ++j) {
+                    ts[j] = a.seed_s[q * TC_KP + j];
+                    tr[j] = a.seed_rows[q * TC_KP + j];
+                }
+                s_n = n0;
+                s_nl = 0;
+                s_scored = 0;
+            }
+            __syncthreads();
+            const uint2 *e = a.abuf + q * (int64_t)a.cap;
+            // (1) the take appended rows with the largest (u, row) keys (not already seeds)
+            uint64_t lastk = ~0ull;
+            for (int j = 0; j < take; ++j) {
+                uint64_t best = 0;
+                for (int i = tid; i < cnt; i += P8_THREADS) {
+                    const uint2 v = e[i];
+                    const uint64_t key = cand_key(__uint_as_float(v.y), v.x);
+                    if (key < lastk && key > best) best = key;
+                }
+                for (int o = 16; o; o >>= 1) {
+                    const uint64_t ob = __shfl_xor_sync(0xffffffffu, best, o);
+                    best = ob > best ? ob : best;
+                }
+                if (lane == 0) red[warp] = best;
+                __syncthreads();
+                best = red[0];
+                for (int w = 1; w < P8_THREADS / 32; ++w) best = red[w] > best ? red[w] : best;
+                __syncthreads();
+                if (best == 0) break;
+                lastk = best;
+                if (tid == 0) {
+                    const int32_t row = (int32_t)key_row(best);
+                    bool dup = false;
+                    for (int t = 0; t < s_n; ++t) dup |= (tr[t] == row);
+                    if (!dup) list[s_nl++] = row;
+                }
+            }
+            __syncthreads();
+            int nl = s_nl;
+            // (2) score the buffered rows P8_ROWS at a time, insert, tighten L; (3) refill the
+            // buffer with every appended row still able to reach the top-k, repeat
+            int next = 0;  // next appended entry to filter
+            bool filtered_all = false;
+            for (;;) {
+                for (int b0 = 0; b0 < nl; b0 += P8_ROWS) {
+                    const int nb = min(P8_ROWS, nl - b0);
+                    const int r = tid >> 1, ch = tid & 1;
+                    double acc = 0.0;
+                    if (r < nb) acc = einsum_chain(a.x32 + (int64_t)list[b0 + r] * a.dp8, qs, a.d, ch);
+                    const double other = __shfl_xor_sync(0xffffffffu, acc, 1);
+                    if (ch == 0 && r < nb) ex[r] = 0.0 + (acc + other);
+                    __syncthreads();
+                    if (tid == 0) {
+                        int n = s_n;
+                        for (int j = 0; j < nb; ++j) top_insert(ts, tr, n, take, ex[j], list[b0 + j]);
+                        s_n = n;
+                        s_scored += nb;
+                        s_L = (n == take) ? __double2float_rd(ts[take - 1]) : -INFINITY;
+                    }
+                    __syncthreads();
+                }
+                if (filtered_all) break;
+                // refill: appended rows with u >= L that are not in the list yet
+                if (tid == 0) s_nl = 0;
+                __syncthreads();
+                const float L = s_L;
+                const int n = s_n;
+                int i = next + tid;
+                for (; next < cnt; next += P8_THREADS, i = next + tid) {
+                    bool pass = false;
+                    int32_t row = -1;
+                    if (i < cnt) {
+                        const uint2 v = e[i];
+                        row = (int32_t)v.x;
+                        pass = __uint_as_float(v.y) >= L;
+                        for (int j = 0; j < n && pass; ++j) pass = (tr[j] != row);
+                    }
+                    const unsigned m = __ballot_sync(0xffffffffu, pass);
+                    int base = 0;
+                    if (lane == 0 && m) base = atomicAdd(&s_nl, __popc(m));
+                    base = __shfl_sync(0xffffffffu, base, 0);
+                    if (pass) {
+                        const int pos = base + __popc(m & ((1u << lane) - 1));
+                        list[pos] = row;
+                        prefetch_row_l2(a.x32 + (int64_t)row * a.dp8, a.dp8, 0, 1);
+                    }
+                    __syncthreads();
+                    if (s_nl > P8_LIST - P8_THREADS) {  // buffer nearly full: score, then continue
+                        next += P8_THREADS;
+                        break;
+                    }
+                    __syncthreads();
+                }
+                nl = s_nl;
+                if (next >= cnt) filtered_all = true;
+                __syncthreads();
+                if (nl == 0 && filtered_all) break;
+            }
+            if (tid == 0) atomicAdd(&a.counters[1], s_scored);
+        } else if (tid == 0) {
+            s_n = 0;
+        }
+        __syncthreads();
+        // outputs (warp 0): self-snap (element-wise equal stored row, index.py:180-181) + clamp (:185)
+        if (warp == 0) {
+            const int n = s_n;
+            for (int j = 0; j < a.k; ++j) {
+                const int64_t o = q * a.k + j;
+                if (j >= n) {
+                    if (lane == 0) {
+                        a.rows[o] = -1;
+                        if (a.raw) a.raw[o] = 0.0;
+                        if (a.rep) a.rep[o] = 0.0;
+                    }
+                    continue;
+                }
+                const double bs = ts[j];
+                const int64_t br = tr[j];
+                double rep = bs;
+                if (bs > 1.0 - 1e-6) {
+                    const float *x = a.x32 + br * (int64_t)a.dp8;
+                    int bad = 0;
+                    for (int t = lane; t < a.d; t += 32) bad |= !(x[t] == qv[t]);
+                    if (!__any_sync(0xffffffffu, bad)) rep = 1.0;
+                }
+                if (lane == 0) {
+                    a.rows[o] = br;
+                    if (a.raw) a.raw[o] = bs;
+                    if (a.rep) a.rep[o] = fmax(-1.0, fmin(1.0, rep));
+                }
+            }
+            if (lane == 0) a.count[q] = n;
+        }
+        __syncthreads();
+    }
+}
+
 // ---------------------------------------------------------------------------
 // host side
 
@@ -1493,8 +1674,14 @@ int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats)
     // 3) exact rescoring of the complete candidate set
     I8PostArgs pa{acount, abuf, cap, s.nq, s.k, std::min<int64_t>(s.k, s.n), s.row_limit, s.x32, s.dp8, s.d, s.qp,
                   seed_rows, seed_s, seed_n, s.rows, s.raw, s.rep, s.count, s.counters, s.fallback_list, s.nq_dev};
+    const char *post_env = getenv("PR_I8_POST");  // "warp": the warp-per-query kernel (A/B knob)
     ::pr::count_launch();
-    tc8_post_kernel<<<wgrid, W8_WARPS * 32, wsmem, st>>>(pa);
+    if (post_env && post_env[0] == 'w') {
+        tc8_post_kernel<<<wgrid, W8_WARPS * 32, wsmem, st>>>(pa);
+    } else {
+        const unsigned pgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(s.nq, (int64_t)sm_count() * 8));
+        tc8_post_cta_kernel<<<pgrid, P8_THREADS, (size_t)(s.dp8 + 8) * sizeof(float), st>>>(pa);
+    }
     PR_LAUNCH_CHECK();
     stats->nsplit = nsplit;
     return PR_OK;
