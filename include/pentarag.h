@@ -115,6 +115,16 @@ int pr_index_search(pr_index *h, const float *d_q, int64_t nq, int k, uint32_t m
  * query j sees exactly the rows written back by queries i < j. */
 int pr_index_search_ex(pr_index *h, const float *d_q, int64_t nq, int k, uint32_t mode, const int64_t *d_row_limit,
                        int64_t *d_rows, double *d_raw, double *d_reported, int32_t *d_count, void *stream);
+/* As pr_index_search_ex for callers that only act on scores >= floor (the semantic-cache and
+ * adaptive-memory thresholds, caches.py:140, knowledge.py:203-205): every result whose exact
+ * score is >= min(floor, 1 - 1e-6) is exact and in its exact rank among such rows (self-snap and
+ * clamp as pr_index_search); rows below that may be missing or out of order, and d_count
+ * counts the rows reported.  A caller deciding `count > 0 && reported[0] >= floor` gets
+ * exactly the full search's decision and, on a hit, its row and score.  The int8 scan then
+ * starts from the floor as its bound (no pilot), so a threshold lookup is one scan. */
+int pr_index_search_floor(pr_index *h, const float *d_q, int64_t nq, int k, uint32_t mode, const int64_t *d_row_limit,
+                          double floor, int64_t *d_rows, double *d_raw, double *d_reported, int32_t *d_count,
+                          void *stream);
 /* The miss-list hand-off of the on-device cascade: search the queries a device-side
  * compaction selected, without reading the list back.  Listed position i searches
  * d_q[d_list[i]] (d_q is [*, dim] fp32) for i < *d_nlist (DEVICE int32); outputs are

@@ -72,6 +72,7 @@ SIGNATURES = {
     "pr_index_append_from": (c_int, [c_vp, c_vp, c_vp, c_i64, c_vp]),
     "pr_index_search": (c_int, [c_vp, c_vp, c_i64, c_int, c_u32, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "pr_index_search_ex": (c_int, [c_vp, c_vp, c_i64, c_int, c_u32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "pr_index_search_floor": (c_int, [c_vp, c_vp, c_i64, c_int, c_u32, c_vp, c_dbl, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "pr_index_search_list": (c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_int, c_u32, c_vp, c_vp, c_vp, c_vp,
                                      c_vp, c_vp]),
     "pr_cascade_gate": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_dbl, c_vp, c_int, c_int, c_int, c_vp, c_vp, c_vp,

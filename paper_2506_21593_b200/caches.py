@@ -277,9 +277,12 @@ class SemanticCache:
 
     def lookup_batch(self, queries, *, mode: int = MODE_AUTO, account: bool = True):
         """Batched lookup over a [B, dim] tensor.  Returns device tensors
-        (hit bool [B], row int64 [B], score float64 [B])."""
+        (hit bool [B], row int64 [B], score float64 [B]); row and score are those of
+        the exact top-1 for a hit (a miss may carry row -1).  The search only has to
+        be exact at or above the threshold (``search_batch(floor=...)``), so the scan
+        starts from the threshold as its bound."""
         index = self._index
-        res = index.search_batch(queries, 1, mode=mode)
+        res = index.search_batch(queries, 1, mode=mode, floor=float(self.threshold))
         hit = (res.count > 0) & (res.scores[:, 0] >= self.threshold)
         if account:
             nh = int(hit.sum().item())

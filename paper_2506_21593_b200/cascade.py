@@ -12,7 +12,9 @@ DEVICE stage (``_launch``, enqueued on the router's CUDA stream, no host read-ba
   the window's first-occurrence map is host-side (texts only), uploaded as a mask.
 * L2 (semantic cache, caches.py:131-145): the first occurrence of every text new to the
   cache is appended up front (that is what write-back will do), and ONE row-limited top-1
-  search lets query j see exactly the rows written by queries before it.
+  search lets query j see exactly the rows written by queries before it.  The router only
+  acts on a top-1 at or above the threshold, so the L2 and L4 searches are threshold
+  searches (``floor``: exact at and above it, the int8 scan starts from it).
 * L3 (memory recall, generation.py:203-224), when the backend is the stub LLM over a
   ``DeviceKnowledgeTable``: one probe of the recall hash table + the confidence gate
   (``pr_recall_gate``).  The table never changes while routing, so no window is needed.
@@ -336,7 +338,8 @@ def _launch(router, queries, vectors, start: int, end: int, mode: int, prev: "_S
         l3_val, l3_d = sp.recall.gate_device(arena[0], arena[1], B, cfg.recall_threshold)
     r2 = None
     if L2 in pos:
-        r2 = sc_index.search_batch(Vd, 1, mode=mode, validate=False, row_limit=sc_limit, count=False)
+        r2 = sc_index.search_batch(Vd, 1, mode=mode, validate=False, row_limit=sc_limit, count=False,
+                                 floor=float(sc.threshold))
     vec_pos = min(pos.get(L4, 99), pos.get(L5, 99))
     l1_d = torch.empty(B, dtype=u8, device=dev)
     l2_d = torch.empty(B, dtype=u8, device=dev)
@@ -375,7 +378,7 @@ def _launch(router, queries, vectors, start: int, end: int, mode: int, prev: "_S
     if L4 in pos:
         thr = akm.threshold
         if len(akm.index):
-            ra = akm.index.search_batch(Vd, 1, mode=mode, validate=False, count=False)
+            ra = akm.index.search_batch(Vd, 1, mode=mode, validate=False, count=False, floor=float(thr))
             l4 |= (ra.count > 0) & (ra.scores[:, 0] >= thr)
         scr = _scratch(router, kbi.dim)
         prev_b = prev.B if prev is not None else 0
@@ -393,7 +396,7 @@ def _launch(router, queries, vectors, start: int, end: int, mode: int, prev: "_S
         store = scr.store(out_max)
         store.append_anonymous_from(kbi, out_rows)
         lim = torch.where(slot >= 0, before[slot.clamp(min=0).long()], torch.zeros_like(before))
-        rs = store.search_batch(Vd, 1, mode=mode, validate=False, row_limit=lim, count=False)
+        rs = store.search_batch(Vd, 1, mode=mode, validate=False, row_limit=lim, count=False, floor=float(thr))
         l4 |= (rs.count > 0) & (rs.scores[:, 0] >= thr)
         l4 &= slot >= 0
 

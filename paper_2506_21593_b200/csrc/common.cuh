@@ -93,6 +93,43 @@ __device__ __forceinline__ double einsum_dot_f32(const float *__restrict__ x, co
     return 0.0 + (a0 + a1);
 }
 
+// One of einsum_dot_f32's two fp64 lanes (ch 0: elements 6,4,2,0 of every block of 8;
+// ch 1: 7,5,3,1; tail two at a time) over operands in ANY memory space (shared staging):
+// lane pair (ch 0, ch 1) + `0.0 + (a0 + a1)` reproduces einsum_dot_f32 bit for bit.
+__device__ __forceinline__ double einsum_lane(const float *x, const float *q, int d, int ch) {
+    double a = 0.0;
+    int j = 0;
+#pragma unroll 4
+    for (; j + 8 <= d; j += 8) {
+        const float4 xa = *reinterpret_cast<const float4 *>(x + j);
+        const float4 xb = *reinterpret_cast<const float4 *>(x + j + 4);
+        const float4 qa = *reinterpret_cast<const float4 *>(q + j);
+        const float4 qb = *reinterpret_cast<const float4 *>(q + j + 4);
+        a = fma((double)(ch ? xb.w : xb.z), (double)(ch ? qb.w : qb.z), a);
+        a = fma((double)(ch ? xb.y : xb.x), (double)(ch ? qb.y : qb.x), a);
+        a = fma((double)(ch ? xa.w : xa.z), (double)(ch ? qa.w : qa.z), a);
+        a = fma((double)(ch ? xa.y : xa.x), (double)(ch ? qa.y : qa.x), a);
+    }
+    for (; j < d; j += 2) a = fma((double)x[j + ch], (double)q[j + ch], a);
+    return a;
+}
+
+// Exact einsum-order score of one stored row by a whole warp: the row is staged in shared
+// memory with coalesced 16-byte loads (one DRAM round trip instead of a per-thread stream of
+// 256 dependent-latency loads), then lanes 0/1 run the two fp64 chains.  Returns the score
+// in lane 0.  xs: this warp's [dp8] staging buffer; qs: the query (shared or global).
+__device__ __forceinline__ double warp_einsum_dot(const float *__restrict__ x, float *xs, const float *qs, int dp8,
+                                                  int d) {
+    const int lane = threadIdx.x & 31;
+    for (int j = lane * 4; j < dp8; j += 128)
+        *reinterpret_cast<float4 *>(xs + j) = __ldg(reinterpret_cast<const float4 *>(x + j));
+    __syncwarp();
+    const double acc = lane < 2 ? einsum_lane(xs, qs, d, lane) : 0.0;
+    const double other = __shfl_xor_sync(0xffffffffu, acc, 1);
+    __syncwarp();
+    return 0.0 + (acc + other);
+}
+
 // (score desc, row asc) total order used everywhere results are ranked
 // (index.py:176 lexsort((arange(n), -scores))).
 __device__ __forceinline__ bool ranks_before(double sa, int64_t ra, double sb, int64_t rb) {

@@ -927,16 +927,16 @@ struct QueryList {
 
 static int search_impl(pr_index *h, const float *d_q, int64_t nq, int k, uint32_t mode, const int64_t *d_row_limit,
                        int64_t *d_rows, double *d_raw, double *d_reported, int32_t *d_count, void *stream,
-                       const QueryList &ql);
+                       const QueryList &ql, double floor);
 
 static int search_entry(pr_index *h, const float *d_q, int64_t nq, int k, uint32_t mode, const int64_t *d_row_limit,
                         int64_t *d_rows, double *d_raw, double *d_reported, int32_t *d_count, void *stream,
-                        const QueryList &ql) {
+                        const QueryList &ql, double floor = -INFINITY) {
     if (!h) PR_FAIL(PR_ERR_BAD_ARG, "null handle");
     cudaStream_t st = as_stream(stream);
     if (!h->scratch_ev) PR_CUDA(cudaEventCreateWithFlags(&h->scratch_ev, cudaEventDisableTiming));
     if (h->scratch_ev_used && h->last_stream != st) PR_CUDA(cudaStreamWaitEvent(st, h->scratch_ev, 0));
-    const int rc = search_impl(h, d_q, nq, k, mode, d_row_limit, d_rows, d_raw, d_reported, d_count, stream, ql);
+    const int rc = search_impl(h, d_q, nq, k, mode, d_row_limit, d_rows, d_raw, d_reported, d_count, stream, ql, floor);
     if (rc == PR_OK) {
         PR_CUDA(cudaEventRecord(h->scratch_ev, st));
         h->scratch_ev_used = true;
@@ -957,9 +957,17 @@ int pr_index_search_ex(pr_index *h, const float *d_q, int64_t nq, int k, uint32_
     return search_entry(h, d_q, nq, k, mode, d_row_limit, d_rows, d_raw, d_reported, d_count, stream, QueryList{});
 }
 
+int pr_index_search_floor(pr_index *h, const float *d_q, int64_t nq, int k, uint32_t mode, const int64_t *d_row_limit,
+                          double floor, int64_t *d_rows, double *d_raw, double *d_reported, int32_t *d_count,
+                          void *stream) {
+    if (floor != floor) PR_FAIL(PR_ERR_BAD_ARG, "floor is NaN");
+    return search_entry(h, d_q, nq, k, mode, d_row_limit, d_rows, d_raw, d_reported, d_count, stream, QueryList{},
+                        floor);
+}
+
 static int search_impl(pr_index *h, const float *d_q, int64_t nq, int k, uint32_t mode, const int64_t *d_row_limit,
                        int64_t *d_rows, double *d_raw, double *d_reported, int32_t *d_count, void *stream,
-                       const QueryList &ql) {
+                       const QueryList &ql, double floor) {
     if (!h) PR_FAIL(PR_ERR_BAD_ARG, "null handle");
     if (k < 1) PR_FAIL(PR_ERR_BAD_ARG, "k must be >= 1");  // index.py:161-162
     if (nq < 0 || nq > INT32_MAX / 2) PR_FAIL(PR_ERR_BAD_ARG, "bad query count");
@@ -990,7 +998,10 @@ static int search_impl(pr_index *h, const float *d_q, int64_t nq, int k, uint32_
     // amortise the start: below ~512k rows the fp16 scan is faster (40k x 1024, 2048
     // queries, k=10: 0.42 ms fp16 vs 3.5 ms int8; 10M rows: int8 1.6x faster).
     const bool tc_pays = mode == PR_SEARCH_AUTO && tensor_ok && pr::tc_worthwhile(h->count, ql.list ? ql.hint : nq);
-    const bool i8_pays = tc_pays && h->count >= ((int64_t)1 << 19);
+    // with a floor the int8 scan starts from a known bound (no cold start, no pilot): it
+    // pays at every size a tensor-core scan does
+    const bool has_floor = floor > -INFINITY;
+    const bool i8_pays = tc_pays && (h->count >= ((int64_t)1 << 19) || has_floor);
     const bool use_i8 = (mode == PR_SEARCH_TENSOR_I8 || i8_pays) && tensor_ok && pr::tc8_eligible(h->dim);
     bool use_tc = !use_i8 && tensor_ok && (mode == PR_SEARCH_TENSOR || mode == PR_SEARCH_TENSOR_I8 || tc_pays);
 
@@ -1039,6 +1050,7 @@ static int search_impl(pr_index *h, const float *d_q, int64_t nq, int k, uint32_
         ts.row_limit = d_row_limit;
         ts.nq_dev = ql.nlist;
         ts.nq_hint = ql.hint;
+        ts.floor = floor;
         rc = timing_pair(h, &ts.ev_begin, &ts.ev_end);
         if (rc) return rc;
         rc = pr::tc8_search(ts, cv, st, &h->stats);

@@ -309,6 +309,7 @@ __device__ __forceinline__ void defer_query(const RescoreArgs &a, int64_t q, dou
 }
 
 __global__ void __launch_bounds__(RS_THREADS) tc_rescore_kernel(RescoreArgs a) {
+    extern __shared__ __align__(16) float rs_dyn[];  // [1 + RS_THREADS / 32][dp8]: query + per-warp row
     __shared__ int64_t r_row[RS_MAX];
     __shared__ double r_apx[RS_MAX];
     __shared__ double r_ex[RS_MAX];
@@ -377,8 +378,19 @@ __global__ void __launch_bounds__(RS_THREADS) tc_rescore_kernel(RescoreArgs a) {
             continue;
         }
         const float *qv = a.qp + q * (int64_t)a.dp8;
-        for (int e = threadIdx.x; e < nr; e += RS_THREADS)
-            r_ex[e] = einsum_dot_f32(a.x32 + r_row[e] * (int64_t)a.dp8, qv, a.d);
+        {
+            // one warp per candidate row, staged through shared memory (warp_einsum_dot):
+            // a thread streaming its own 4-KB row set this kernel's time
+            float *qs = rs_dyn;
+            float *xs = rs_dyn + a.dp8 * (1 + (threadIdx.x >> 5));
+            for (int j = threadIdx.x * 4; j < a.dp8; j += RS_THREADS * 4)
+                *reinterpret_cast<float4 *>(qs + j) = __ldg(reinterpret_cast<const float4 *>(qv + j));
+            __syncthreads();
+            for (int e = threadIdx.x >> 5; e < nr; e += RS_THREADS / 32) {
+                const double ex = warp_einsum_dot(a.x32 + r_row[e] * (int64_t)a.dp8, xs, qs, a.dp8, a.d);
+                if ((threadIdx.x & 31) == 0) r_ex[e] = ex;
+            }
+        }
         if (threadIdx.x == 0) atomicAdd(&a.counters[1], nr);
         __syncthreads();
         // exact top-take of R, certificate, outputs
@@ -737,7 +749,13 @@ int tc_search(TcSearch &s, Carve &cv, cudaStream_t st, pr_search_stats *stats) {
                    clist, cthr};
     int rgrid = (int)std::min<int64_t>(s.nq, (int64_t)sm_count() * 16);
     ::pr::count_launch();
-    tc_rescore_kernel<<<rgrid, RS_THREADS, 0, st>>>(ra);
+    const size_t rs_smem = (size_t)(1 + RS_THREADS / 32) * s.dp8 * sizeof(float);
+    static bool rs_attr = false;
+    if (!rs_attr) {
+        PR_CUDA(cudaFuncSetAttribute(tc_rescore_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+        rs_attr = true;
+    }
+    tc_rescore_kernel<<<rgrid, RS_THREADS, rs_smem, st>>>(ra);
     PR_LAUNCH_CHECK();
 
     // collect pass for certificate failures (device-sized list; tiles past it exit at once)

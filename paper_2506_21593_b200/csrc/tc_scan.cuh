@@ -76,6 +76,9 @@ struct Tc8Search {
     // skipped by every kernel; the grid is shaped for nq_hint queries (host estimate)
     const int32_t *nq_dev = nullptr;
     int64_t nq_hint = 0;
+    // pr_index_search_floor: rows whose exact score is below the floor need not be found
+    // (-inf = a plain search); the scan's bound starts at the floor and the pilot is skipped
+    double floor = -INFINITY;
 };
 int i8_quantize_rows(const float *src, int64_t n, int d, const int64_t *rows, int64_t row0, int dp128, I8Rows &m,
                      cudaStream_t st);

@@ -1606,12 +1606,21 @@ int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats)
         attr = true;
     }
     const char *ceil_env = getenv("PR_I8_CEILING");  // 1: no row can pass (results invalid): fast-path timing
-    const float floor_thr = (ceil_env && ceil_env[0] == '1') ? INFINITY : -INFINITY;
+    // a caller's floor (pr_index_search_floor) as the scan's first bound: rows with u < floor
+    // have exact < floor.  Snapped self-matches (raw > 1 - 1e-6, reported 1.0) must survive a
+    // floor up to 1, and the bound is an fp32 value rounded DOWN.
+    float floor_thr = -INFINITY;
+    if (s.floor > -INFINITY) {
+        const double fe = std::min(s.floor, 1.0 - 1e-6) - 1e-6;
+        floor_thr = (float)fe;
+        if ((double)floor_thr > fe) floor_thr = std::nextafter(floor_thr, -INFINITY);
+    }
+    if (ceil_env && ceil_env[0] == '1') floor_thr = INFINITY;
     const unsigned wgrid = (unsigned)std::max<int64_t>(
         1, std::min<int64_t>(ceil_div<int64_t>(s.nq, W8_WARPS), (int64_t)sm_count() * 8));
 
     // 1) pilot over a tile subsample -> exact seeds and a first bound per query
-    const int psplit = pilot_splits(qtiles_hint, ntiles);
+    const int psplit = s.floor > -INFINITY ? 0 : pilot_splits(qtiles_hint, ntiles);
     int32_t *seed_rows = nullptr, *seed_n = nullptr;
     double *seed_s = nullptr;
     if (psplit > 0) {

@@ -335,12 +335,17 @@ class FlatIndex:
 
     # -- search ----------------------------------------------------------------
     def search_batch(self, queries, k: int, *, mode: int = MODE_AUTO, validate: bool = True,
-                     out: BatchResult | None = None, row_limit=None, count: bool = True) -> BatchResult:
+                     out: BatchResult | None = None, row_limit=None, count: bool = True,
+                     floor: float | None = None) -> BatchResult:
         """Batched FlatIndex.search.  ``queries``: [B, dim] float32 (torch
         tensor on any device, or numpy).  Returns device tensors; counts
         ``search_count`` once per query like B sequential calls (unless
         ``count=False``).  ``row_limit`` (int64 [B]) restricts query b to rows
-        [0, row_limit[b]) — the store as it was earlier in a sequential stream."""
+        [0, row_limit[b]) — the store as it was earlier in a sequential stream.
+        ``floor``: the caller only acts on scores >= floor (a cache threshold):
+        results at or above it are exact, rows below it may be missing
+        (``pr_index_search_floor``) — ``count > 0 and scores[:, 0] >= floor``
+        is then exactly the full search's threshold decision."""
         if k < 1:
             raise ValueError("k must be >= 1")
         torch = _torch()
@@ -369,10 +374,16 @@ class FlatIndex:
             if count:
                 self.search_count += B
             if B:
-                rc = self._L.pr_index_search_ex(
-                    self._h, _lib.ptr(q), B, k, mode, _lib.ptr(lim), _lib.ptr(out.rows), _lib.ptr(out.raw),
-                    _lib.ptr(out.scores), _lib.ptr(out.count), _lib.stream_ptr(),
-                )
+                if floor is None:
+                    rc = self._L.pr_index_search_ex(
+                        self._h, _lib.ptr(q), B, k, mode, _lib.ptr(lim), _lib.ptr(out.rows), _lib.ptr(out.raw),
+                        _lib.ptr(out.scores), _lib.ptr(out.count), _lib.stream_ptr(),
+                    )
+                else:
+                    rc = self._L.pr_index_search_floor(
+                        self._h, _lib.ptr(q), B, k, mode, _lib.ptr(lim), float(floor), _lib.ptr(out.rows),
+                        _lib.ptr(out.raw), _lib.ptr(out.scores), _lib.ptr(out.count), _lib.stream_ptr(),
+                    )
                 _lib.check(rc, "pr_index_search")
         return out
 
