@@ -217,6 +217,10 @@ struct I8ScanParams {
     int32_t *prog;  // [nsplit][qgroups]: tiles loaded + 1 (0 = not started, INT_MAX = done)
     int window;
     const int32_t *nq_dev;  // device query count (nullable): queries >= *nq_dev are skipped
+    // per query, the k largest rounded-down EXACT scores found by ANY CTA's refiner (f2ord
+    // keys, 0 = empty; nullable): their minimum bounds e_k from below like one CTA's refiner
+    // list, but over the union of every split (see gunion_insert)
+    uint32_t *gun;
     // measurement only (PR_I8_VERBOSE): [0] warp-chunks that took the cooperative path,
     // [1] warp-chunks, [2] flagged (query, 8-row group) pairs
     uint32_t *dbg;
@@ -256,6 +260,33 @@ __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t *p) {
     uint32_t v;
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
+}
+
+// Insert a lower bound (f2ord key) into a query's k-slot union list and publish the list's
+// minimum once all k slots are filled.  Every (query, row) pair reaches exactly one refiner
+// once, so the slots always hold k DISTINCT rows' lower bounds: their minimum is a valid
+// lower bound on the true k-th score, and it is the union's k-th largest, not one thread's.
+// Slots only grow (a CAS replaces the current minimum by a larger key), so a minimum read
+// slot by slot is still a minimum over k distinct rows at the end of the read.
+__device__ __forceinline__ void gunion_insert(uint32_t *slots, int k, uint32_t key, uint32_t *lg) {
+    for (;;) {
+        uint32_t mn = 0xFFFFFFFFu;
+        int mi = 0;
+        for (int i = 0; i < k; ++i) {
+            const uint32_t v = ld_relaxed(slots + i);
+            if (v < mn) {
+                mn = v;
+                mi = i;
+            }
+        }
+        if (key <= mn) return;
+        if (atomicCAS(slots + mi, mn, key) == mn) {
+            uint32_t m2 = 0xFFFFFFFFu;
+            for (int i = 0; i < k; ++i) m2 = min(m2, ld_relaxed(slots + i));
+            if (m2 != 0u) atomicMax(lg, m2);
+            return;
+        }
+    }
 }
 
 // index of the n-th (0-based) set bit of m
@@ -795,6 +826,12 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
                         rcnt[ql] = n;
                         // k distinct rows score >= L[k-1]: a valid lower bound on e_k
                         if (n == p.k) atomicMax(p.lg + qg, f2ord(L[p.k - 1]));
+                    }
+                    // ... and the union over every CTA's refiner: each (query, row) is handed to
+                    // one refiner once, so the union list holds distinct rows' exact scores
+                    if (p.gun) {
+                        const uint32_t key = f2ord(exf);
+                        if (key > ld_relaxed(p.lg + qg)) gunion_insert(p.gun + qg * TC_KP, p.k, key, p.lg + qg);
                     }
                 }
                 __syncwarp();
@@ -1545,7 +1582,7 @@ size_t tc8_scratch_bytes(int64_t nq, int dp128, int64_t n) {
     const int ps = pilot_splits(qtiles, ntiles);
     return (size_t)nq_pad * dp128 + (size_t)nq_pad * 16 + (size_t)nq * (4 + 4 + 4 + 4) +
            (size_t)nq * i8_cap(n, nq) * 8 + (size_t)nq * ps * I8_HALVES * TC_KP * 8 + (size_t)nq * TC_KP * 12 +
-           (size_t)qtiles * 4 * 1024 + 65536;
+           (size_t)qtiles * 4 * 1024 + (size_t)nq * TC_KP * 4 + 65536;
 }
 
 int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats) {
@@ -1644,6 +1681,13 @@ int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats)
     I8ScanParams p{s.n, s.dp128 / I8_BLOCK_K, nsplit, tps, (int)ntiles, (int)qtiles, s.k, s.rows8.xs, s.rows8.xe,
                    s.rows8.xt, qmeta, s.row_limit, s.nq, lg, acount, abuf, cap, floor_thr, 0, 1, nullptr, s.x32, s.qp,
                    s.dp8, s.d, 1, nullptr, 0, s.nq_dev};
+    {
+        const char *g_env = getenv("PR_I8_GUNION");  // 0: no union list (A/B knob)
+        if (!(g_env && g_env[0] == '0')) {
+            p.gun = cv.take<uint32_t>((size_t)s.nq * TC_KP);
+            PR_CUDA(cudaMemsetAsync(p.gun, 0, (size_t)s.nq * TC_KP * sizeof(uint32_t), st));
+        }
+    }
     {
         const char *w_env = getenv("PR_I8_WINDOW");  // tiles a pair may run ahead of its split (0 = off)
         p.window = w_env ? atoi(w_env) : 0;  // measured: 48 tiles halves DRAM reads but costs 50 % time
