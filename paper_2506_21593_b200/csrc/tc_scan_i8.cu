@@ -17,7 +17,7 @@
 // L = the k-th largest l over all rows is a lower bound on the true k-th score
 // e_k (k rows score >= L), and so is the exact k-th score of any k distinct
 // rows.  Every row of the true top-k (ties included) has u >= exact >= e_k.
-// 1) A pilot scan over every 32nd 256-row tile keeps per-thread top-k lists of
+// 1) A pilot scan over every 128th 256-row tile keeps per-thread top-k lists of
 //    l; the seed kernel scores the best k of them exactly: seeds + a first
 //    bound per query.  2) The main scan APPENDS every row with u >= the current
 //    bound (the max of the seed bound, the thread's running k-th l, and the
@@ -572,7 +572,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
                 tr[i] = 0xFFFFFFFFu;
             }
             float Lpub = -INFINITY;
-            uint32_t n_coop = 0, n_chunks = 0, n_flag = 0;
+            uint32_t n_coop = 0, n_chunks = 0, n_flag = 0, n_fine = 0;
             for (int i = 0; i < nloc; ++i, ++tix) {
                 const int acc = tix & 1;
                 const uint32_t aphase = (tix >> 1) & 1;
@@ -711,6 +711,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
                             }
                         }
                         if (__any_sync(0xffffffffu, cmask != 0)) {
+                            if (p.dbg) ++n_fine;
                             const float4 *s4 = reinterpret_cast<const float4 *>(ss + c * 32);
 #pragma unroll
                             for (int g = 0; g < 4; ++g) {
@@ -780,6 +781,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
                     atomicAdd(&p.dbg[0], n_coop);
                     atomicAdd(&p.dbg[1], n_chunks);
                     atomicAdd(&p.dbg[2], n_flag);
+                    atomicAdd(&p.dbg[3], n_fine);
                 }
             }
             if (PILOT && valid) {
@@ -1499,11 +1501,14 @@ static int i8_cap(int64_t n, int64_t nq) {
     return (int)cap;
 }
 
-// pilot: every I8_PILOT_STRIDE-th 256-row tile (~3% of the scan) when the store has
-// at least 8 * I8_PILOT_STRIDE tiles
+// pilot: every I8_PILOT_STRIDE-th 256-row tile (~0.8% of the scan) when the store has
+// at least 8 * I8_PILOT_STRIDE tiles.  With the refiners' union bound (gunion_insert) the
+// main scan tightens its own bound quickly, so a sparse pilot is enough: stride 128 vs 32,
+// continuous blocks at 10M x 1024: B=4096 k=5 35.92 vs 36.45 ms; B=2048 k=10 19.90 vs 20.25;
+// B=256 2.90 vs 2.95 (no pilot at all: 38.67 ms)
 static int pilot_stride() {
     const char *e = getenv("PR_I8_PILOT_STRIDE");  // measurement knob (read per search)
-    return e ? std::max(2, atoi(e)) : 32;
+    return e ? std::max(2, atoi(e)) : 128;
 }
 #define I8_PILOT_STRIDE pilot_stride()
 
@@ -1746,8 +1751,11 @@ int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats)
         uint32_t h[4];
         PR_CUDA(cudaMemcpyAsync(h, p.dbg, 16, cudaMemcpyDeviceToHost, st));
         PR_CUDA(cudaStreamSynchronize(st));
-        fprintf(stderr, "tc8_search: cooperative warp-chunks %u of %u (%.4f), flagged groups %u (%.2f per query)\n", h[0],
-                h[1], h[1] ? (double)h[0] / h[1] : 0.0, h[2], (double)h[2] / std::max<int64_t>(1, s.nq));
+        fprintf(stderr,
+                "tc8_search: cooperative warp-chunks %u of %u (%.4f), flagged groups %u (%.2f per query), per-row "
+                "fast-path warp-chunks %u (%.4f)\n",
+                h[0], h[1], h[1] ? (double)h[0] / h[1] : 0.0, h[2], (double)h[2] / std::max<int64_t>(1, s.nq), h[3],
+                h[1] ? (double)h[3] / h[1] : 0.0);
     }
     // 3) exact rescoring of the complete candidate set
     I8PostArgs pa{acount, abuf, cap, s.nq, s.k, std::min<int64_t>(s.k, s.n), s.row_limit, s.x32, s.dp8, s.d, s.qp,
