@@ -1362,6 +1362,9 @@ __global__ void __launch_bounds__(P8_THREADS) tc8_post_cta_kernel(I8PostArgs a) 
                     if (!dup) list[s_nl++] = row;
                 }
             }
+            // the bound before any appended row is scored: the seeds' k-th (phase (1) may have
+            // selected only seeds, and then no scoring round below sets it)
+            if (tid == 0) s_L = (s_n == take) ? __double2float_rd(ts[take - 1]) : -INFINITY;
             __syncthreads();
             int nl = s_nl;
             // (2) score the buffered rows P8_ROWS at a time, insert, tighten L; (3) refill the
