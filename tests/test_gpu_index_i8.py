@@ -183,10 +183,15 @@ def test_i8_unnormalised_rows(gpu, rng):
 
 
 @pytest.mark.parametrize("k", [1, 5, 16])
-def test_i8_pilot_path(gpu, rng, k):
-    """Stores of >= 65536 rows run the 1/32-tile pilot first: its exact seeds
-    and lower bounds must not change any result (incl. ties and row limits)."""
+@pytest.mark.parametrize("stride", ["8", "2"])
+def test_i8_pilot_path(gpu, rng, k, stride, monkeypatch):
+    """The pilot (every stride-th tile; the default 128 needs >= 1024 tiles, so the
+    stride is forced here) must not change any result (incl. ties and row limits).
+    Stride 2 makes the pilot's seeds the true top-k for most queries: the post
+    kernel's first phase then selects only seed rows."""
     import torch
+
+    monkeypatch.setenv("PR_I8_PILOT_STRIDE", stride)
 
     from oracle import flat_index as F
     from paper_2506_21593_b200 import FlatIndex
@@ -260,11 +265,14 @@ def test_i8_tiny_stores_and_odd_batches(gpu, rng, n, nq):
 
 
 @pytest.mark.parametrize("env", [{}, {"PR_I8_ARES": "0"}, {"PR_I8_CG": "1"}, {"PR_I8_REFINE": "0"},
-                                 {"PR_I8_PILOT_STRIDE": "4"}, {"PR_I8_MC": "2"}, {"PR_I8_MC": "4"}])
+                                 {"PR_I8_PILOT_STRIDE": "4"}, {"PR_I8_PILOT_STRIDE": "2"}, {"PR_I8_MC": "2"},
+                                 {"PR_I8_MC": "4"}, {"PR_I8_GUNION": "0"}, {"PR_I8_FAST": "1"},
+                                 {"PR_I8_POST": "warp"}])
 def test_i8_kernel_variants(gpu, rng, env, monkeypatch):
     """The scan variants behind the per-call knobs (streamed vs resident query tile,
-    single-CTA vs 2-CTA MMA, refiner off, a denser pilot, 1 (default) / 2 / 4 CTA pairs per
-    multicast cluster) all give the oracle's answer."""
+    single-CTA vs 2-CTA MMA, refiner off, denser pilots, 1 (default) / 2 / 4 CTA pairs per
+    multicast cluster, no refiner union bound, the single-level fast path, the
+    warp-per-query post kernel) all give the oracle's answer."""
     from paper_2506_21593_b200 import FlatIndex
 
     for key, val in env.items():
