@@ -306,7 +306,17 @@ def c3_kv(hbm_gbs: float, n_keys=100_000_000, batch=65536, n_batches=32, steps=5
         "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm_gbs, "unit": "GB/s", "frac": gbs / hbm_gbs,
                      "bytes_per_lookup": 56,
                      "note": "algorithmic 56 B per lookup (16-B key + one 32-B table sector + 8-B value, SURVEY "
-                             "§8d); the kernel also confirms every tag match against the stored key bytes"},
+                             "§8d); the kernel also confirms every tag match against the stored key bytes",
+                     # what the DRAM actually charges: one random 128-B line per lookup (+ key, offsets,
+                     # outputs) — ncu 156 B read + 9 B written per lookup (profiles/r02c_kv_get_ncu_summary.txt);
+                     # the random-line ceiling of this part is ~45.3 G lines/s (scripts/micro/randline.cu,
+                     # profiles/r02_kv_layout_experiments.txt)
+                     "physical": {"dram_bytes_per_lookup": 165, "achieved_GBps": per_s * 165 / 1e9,
+                                  "frac_of_hbm": per_s * 165 / 1e9 / hbm_gbs,
+                                  "random_line_ceiling_per_s": 45.3e9,
+                                  "frac_of_random_line_ceiling": per_s / 45.3e9,
+                                  "source": "ncu dram bytes per lookup (r02c capture) and the randline micro; "
+                                            "constants, not measured in this run"}},
         "large_batch": {"batch": int(big_ids.size), "value": big_per_s, "unit": "lookups/s",
                         "algorithmic_GBps": big_per_s * 56 / 1e9, "frac_of_hbm": big_per_s * 56 / 1e9 / hbm_gbs},
         "parity": {"lookups_checked": n_batches * batch + int(big_ids.size), "mismatches": bad},
