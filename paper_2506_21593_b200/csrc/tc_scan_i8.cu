@@ -30,6 +30,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <vector>
 #include <cmath>
 #include <climits>
 #include <cstdio>
@@ -1292,7 +1293,28 @@ __global__ void __launch_bounds__(W8_WARPS * 32) tc8_post_kernel(I8PostArgs a) {
 // top-k out: any row with u < L has exact <= u < L <= e_k (strictly below the final k-th,
 // so not even a tie), whatever order the survivors are scored in.
 constexpr int P8_THREADS = 256;
-constexpr int P8_ROWS = P8_THREADS / 2;  // rows scored per round
+constexpr int P8_ROWS = P8_THREADS / 2;  // rows scored per round (a thread pair per row)
+
+// einsum_chain with the query already in fp64 (converted once per query): the fp64 pipe runs
+// the dependent DFMA chain (24-cycle latency on B200, scripts/micro/dfma.cu) and every
+// F2F.F64.F32 conversion, so converting the query once halves the conversions.  Bit-identical:
+// (double)q is exact, so fma((double)x, qd, a) == fma((double)x, (double)q, a).
+__device__ __forceinline__ double einsum_chain_qd(const float *__restrict__ x, const double *__restrict__ qd, int d,
+                                                  int ch) {
+    double a = 0.0;
+    int j = 0;
+#pragma unroll 8
+    for (; j + 8 <= d; j += 8) {
+        const float4 xa = __ldg(reinterpret_cast<const float4 *>(x + j));
+        const float4 xb = __ldg(reinterpret_cast<const float4 *>(x + j + 4));
+        a = fma((double)(ch ? xb.w : xb.z), qd[j + 6 + ch], a);
+        a = fma((double)(ch ? xb.y : xb.x), qd[j + 4 + ch], a);
+        a = fma((double)(ch ? xa.w : xa.z), qd[j + 2 + ch], a);
+        a = fma((double)(ch ? xa.y : xa.x), qd[j + ch], a);
+    }
+    for (; j < d; j += 2) a = fma((double)x[j + ch], qd[j + ch], a);
+    return a;
+}
 constexpr int P8_LIST = 2048;            // survivors buffered per pass over the appended rows
 
 __device__ __forceinline__ void prefetch_row_l2(const float *x, int dp8, int t, int nthreads) {
@@ -1302,13 +1324,15 @@ __device__ __forceinline__ void prefetch_row_l2(const float *x, int dp8, int t, 
 }
 
 __global__ void __launch_bounds__(P8_THREADS) tc8_post_cta_kernel(I8PostArgs a) {
-    extern __shared__ __align__(16) float qs[];  // [dp8 + 8]
+    extern __shared__ __align__(16) double qd[];  // [dp8] the query in fp64
     __shared__ double ts[TC_KP];
     __shared__ int32_t tr[TC_KP];
     __shared__ int32_t list[P8_LIST];
     __shared__ double ex[P8_ROWS];
+    __shared__ int32_t ins[P8_ROWS];
+    __shared__ uint64_t keys[P8_THREADS];
     __shared__ uint64_t red[P8_THREADS / 32];
-    __shared__ int s_n, s_nl, s_scored;
+    __shared__ int s_n, s_nl, s_scored, s_nins;
     __shared__ float s_L;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t nq_live = live_nq(a.nq_dev, a.nq);
@@ -1322,7 +1346,7 @@ __global__ void __launch_bounds__(P8_THREADS) tc8_post_cta_kernel(I8PostArgs a) 
         }
         const float *qv = a.qp + q * (int64_t)a.dp8;
         if (take > 0) {
-            for (int j = tid; j < a.dp8; j += P8_THREADS) qs[j] = qv[j];
+            for (int j = tid; j < a.dp8; j += P8_THREADS) qd[j] = (double)qv[j];
             if (tid == 0) {
                 const int n0 = a.seed_n ? min(a.seed_n[q], take) : 0;
                 for (int j = 0; j < n0; ++j) {
@@ -1335,32 +1359,52 @@ __global__ void __launch_bounds__(P8_THREADS) tc8_post_cta_kernel(I8PostArgs a) 
             }
             __syncthreads();
             const uint2 *e = a.abuf + q * (int64_t)a.cap;
-            // (1) the take appended rows with the largest (u, row) keys (not already seeds)
-            uint64_t lastk = ~0ull;
-            for (int j = 0; j < take; ++j) {
+            // (1) promising rows to score first, in ONE pass over the appended list: every
+            // thread's largest (u, row) key, then the `take` largest of those 256 (warp 0).
+            // Any rows would do for correctness (the refill below filters against the exact
+            // bound they yield); the largest u give a tight bound early.
+            {
                 uint64_t best = 0;
+#pragma unroll 4
                 for (int i = tid; i < cnt; i += P8_THREADS) {
                     const uint2 v = e[i];
                     const uint64_t key = cand_key(__uint_as_float(v.y), v.x);
-                    if (key < lastk && key > best) best = key;
+                    best = key > best ? key : best;
                 }
-                for (int o = 16; o; o >>= 1) {
-                    const uint64_t ob = __shfl_xor_sync(0xffffffffu, best, o);
-                    best = ob > best ? ob : best;
-                }
-                if (lane == 0) red[warp] = best;
+                keys[tid] = best;
                 __syncthreads();
-                best = red[0];
-                for (int w = 1; w < P8_THREADS / 32; ++w) best = red[w] > best ? red[w] : best;
-                __syncthreads();
-                if (best == 0) break;
-                lastk = best;
-                if (tid == 0) {
-                    const int32_t row = (int32_t)key_row(best);
-                    bool dup = false;
-                    for (int t = 0; t < s_n; ++t) dup |= (tr[t] == row);
-                    if (!dup) list[s_nl++] = row;
+                if (warp == 0) {
+                    uint64_t kl[P8_THREADS / 32];
+#pragma unroll
+                    for (int x = 0; x < P8_THREADS / 32; ++x) kl[x] = keys[lane * (P8_THREADS / 32) + x];
+                    for (int j = 0; j < take; ++j) {
+                        uint64_t m = 0;
+                        int mx = 0;
+#pragma unroll
+                        for (int x = 0; x < P8_THREADS / 32; ++x)
+                            if (kl[x] > m) {
+                                m = kl[x];
+                                mx = x;
+                            }
+                        uint64_t wm = m;
+                        for (int o = 16; o; o >>= 1) {
+                            const uint64_t ob = __shfl_xor_sync(0xffffffffu, wm, o);
+                            wm = ob > wm ? ob : wm;
+                        }
+                        if (wm == 0) break;
+                        if (m == wm) {  // keys are unique (rows are): exactly one lane owns it
+#pragma unroll
+                            for (int x = 0; x < P8_THREADS / 32; ++x)
+                                if (x == mx) kl[x] = 0;
+                            const int32_t row = (int32_t)key_row(wm);
+                            bool dup = false;
+                            for (int t = 0; t < s_n; ++t) dup |= (tr[t] == row);
+                            if (!dup) list[s_nl++] = row;
+                        }
+                        __syncwarp();
+                    }
                 }
+                __syncthreads();
             }
             // the bound before any appended row is scored: the seeds' k-th (phase (1) may have
             // selected only seeds, and then no scoring round below sets it)
@@ -1376,13 +1420,26 @@ __global__ void __launch_bounds__(P8_THREADS) tc8_post_cta_kernel(I8PostArgs a) 
                     const int nb = min(P8_ROWS, nl - b0);
                     const int r = tid >> 1, ch = tid & 1;
                     double acc = 0.0;
-                    if (r < nb) acc = einsum_chain(a.x32 + (int64_t)list[b0 + r] * a.dp8, qs, a.d, ch);
+                    if (r < nb) acc = einsum_chain_qd(a.x32 + (int64_t)list[b0 + r] * a.dp8, qd, a.d, ch);
                     const double other = __shfl_xor_sync(0xffffffffu, acc, 1);
-                    if (ch == 0 && r < nb) ex[r] = 0.0 + (acc + other);
+                    // only rows that rank before the current k-th can enter the list (the k-th only
+                    // rises while they are inserted, so this pre-filter never drops one that would
+                    // stay): thread 0 inserts those few instead of walking all nb scored rows
+                    if (tid == 0) s_nins = 0;
+                    __syncthreads();
+                    if (ch == 0 && r < nb) {
+                        const double sc = 0.0 + (acc + other);
+                        const int n0 = s_n;
+                        if (n0 < take || ranks_before(sc, list[b0 + r], ts[take - 1], tr[take - 1])) {
+                            const int slot = atomicAdd(&s_nins, 1);
+                            ex[slot] = sc;
+                            ins[slot] = list[b0 + r];
+                        }
+                    }
                     __syncthreads();
                     if (tid == 0) {
                         int n = s_n;
-                        for (int j = 0; j < nb; ++j) top_insert(ts, tr, n, take, ex[j], list[b0 + j]);
+                        for (int j = 0; j < s_nins; ++j) top_insert(ts, tr, n, take, ex[j], ins[j]);
                         s_n = n;
                         s_scored += nb;
                         s_L = (n == take) ? __double2float_rd(ts[take - 1]) : -INFINITY;
@@ -1395,28 +1452,32 @@ __global__ void __launch_bounds__(P8_THREADS) tc8_post_cta_kernel(I8PostArgs a) 
                 __syncthreads();
                 const float L = s_L;
                 const int n = s_n;
-                int i = next + tid;
-                for (; next < cnt; next += P8_THREADS, i = next + tid) {
-                    bool pass = false;
-                    int32_t row = -1;
-                    if (i < cnt) {
-                        const uint2 v = e[i];
-                        row = (int32_t)v.x;
-                        pass = __uint_as_float(v.y) >= L;
-                        for (int j = 0; j < n && pass; ++j) pass = (tr[j] != row);
+                constexpr int P8_U = 4;  // entries per thread per pass: loads in flight together
+                for (; next < cnt; next += P8_U * P8_THREADS) {
+                    uint2 v[P8_U];
+#pragma unroll
+                    for (int u = 0; u < P8_U; ++u) {
+                        const int i = next + u * P8_THREADS + tid;
+                        v[u] = i < cnt ? e[i] : make_uint2(0u, 0u);
                     }
-                    const unsigned m = __ballot_sync(0xffffffffu, pass);
-                    int base = 0;
-                    if (lane == 0 && m) base = atomicAdd(&s_nl, __popc(m));
-                    base = __shfl_sync(0xffffffffu, base, 0);
-                    if (pass) {
-                        const int pos = base + __popc(m & ((1u << lane) - 1));
-                        list[pos] = row;
-                        prefetch_row_l2(a.x32 + (int64_t)row * a.dp8, a.dp8, 0, 1);
+#pragma unroll
+                    for (int u = 0; u < P8_U; ++u) {
+                        const int32_t row = (int32_t)v[u].x;
+                        bool pass = next + u * P8_THREADS + tid < cnt && __uint_as_float(v[u].y) >= L;
+                        for (int j = 0; j < n && pass; ++j) pass = (tr[j] != row);
+                        const unsigned m = __ballot_sync(0xffffffffu, pass);
+                        int base = 0;
+                        if (lane == 0 && m) base = atomicAdd(&s_nl, __popc(m));
+                        base = __shfl_sync(0xffffffffu, base, 0);
+                        if (pass) {
+                            const int pos = base + __popc(m & ((1u << lane) - 1));
+                            list[pos] = row;
+                            prefetch_row_l2(a.x32 + (int64_t)row * a.dp8, a.dp8, 0, 1);
+                        }
                     }
                     __syncthreads();
-                    if (s_nl > P8_LIST - P8_THREADS) {  // buffer nearly full: score, then continue
-                        next += P8_THREADS;
+                    if (s_nl > P8_LIST - P8_U * P8_THREADS) {  // buffer nearly full: score, then continue
+                        next += P8_U * P8_THREADS;
                         break;
                     }
                     __syncthreads();
@@ -1759,6 +1820,16 @@ int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats)
                 "fast-path warp-chunks %u (%.4f)\n",
                 h[0], h[1], h[1] ? (double)h[0] / h[1] : 0.0, h[2], (double)h[2] / std::max<int64_t>(1, s.nq), h[3],
                 h[1] ? (double)h[3] / h[1] : 0.0);
+        std::vector<int32_t> ac((size_t)s.nq);
+        PR_CUDA(cudaMemcpyAsync(ac.data(), acount, (size_t)s.nq * 4, cudaMemcpyDeviceToHost, st));
+        PR_CUDA(cudaStreamSynchronize(st));
+        std::vector<int32_t> srt(ac);
+        std::sort(srt.begin(), srt.end());
+        const size_t m = srt.size();
+        if (m)
+            fprintf(stderr, "tc8_search: appended per query: median %d p90 %d p99 %d max %d (query %lld)\n", srt[m / 2],
+                    srt[m * 9 / 10], srt[m * 99 / 100], srt[m - 1],
+                    (long long)(std::max_element(ac.begin(), ac.end()) - ac.begin()));
     }
     // 3) exact rescoring of the complete candidate set
     I8PostArgs pa{acount, abuf, cap, s.nq, s.k, std::min<int64_t>(s.k, s.n), s.row_limit, s.x32, s.dp8, s.d, s.qp,
@@ -1769,7 +1840,13 @@ int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats)
         tc8_post_kernel<<<wgrid, W8_WARPS * 32, wsmem, st>>>(pa);
     } else {
         const unsigned pgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(s.nq, (int64_t)sm_count() * 8));
-        tc8_post_cta_kernel<<<pgrid, P8_THREADS, (size_t)(s.dp8 + 8) * sizeof(float), st>>>(pa);
+        const size_t psmem = (size_t)s.dp8 * sizeof(double);
+        static bool p8_attr = false;
+        if (!p8_attr) {
+            PR_CUDA(cudaFuncSetAttribute(tc8_post_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+            p8_attr = true;
+        }
+        tc8_post_cta_kernel<<<pgrid, P8_THREADS, psmem, st>>>(pa);
     }
     PR_LAUNCH_CHECK();
     stats->nsplit = nsplit;
