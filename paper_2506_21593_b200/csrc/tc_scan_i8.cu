@@ -1578,7 +1578,14 @@ static int pilot_stride() {
 
 static int pilot_splits(int64_t qtiles, int64_t ntiles) {
     if (ntiles < 8 * (int64_t)I8_PILOT_STRIDE) return 0;
-    return choose_nsplit_waves(qtiles, ceil_div<int64_t>(ntiles, I8_PILOT_STRIDE));
+    const int64_t ptiles = ceil_div<int64_t>(ntiles, I8_PILOT_STRIDE);
+    const char *e = getenv("PR_I8_PSPLIT");  // measurement knob: pilot row splits
+    if (e && atoi(e) > 0) return (int)std::min<int64_t>(ptiles, atoi(e));
+    // ONE wave: each pilot item pays a cold start (its first tile floods the cooperative path
+    // before its lists fill), so fewer, longer items win — measured at 10M x 1024 (pilot ms,
+    // ncu): B = 4096: 4 splits 0.66 vs 9 (two waves) 0.74; B = 2048: 2/3/4/6 splits 0.93 /
+    // 0.74 / 0.65 / 0.54 vs 18 (two waves) 0.94
+    return (int)std::max<int64_t>(1, std::min<int64_t>(ptiles, (int64_t)sm_count() / std::max<int64_t>(1, qtiles)));
 }
 
 bool tc8_eligible(int d) { return d <= 2048; }
