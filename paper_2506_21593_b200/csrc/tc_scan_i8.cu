@@ -1118,6 +1118,7 @@ __global__ void __launch_bounds__(W8_WARPS * 32) tc8_seed_kernel(I8SeedArgs a) {
 }
 
 struct I8PostArgs {
+    unsigned long long *clk;  // measurement only (PR_I8_VERBOSE): per-phase cycles, rounds, passes
     const int32_t *acount;
     const uint2 *abuf;
     int cap;
@@ -1339,6 +1340,8 @@ __global__ void __launch_bounds__(P8_THREADS) tc8_post_cta_kernel(I8PostArgs a) 
     for (int64_t q = blockIdx.x; q < nq_live; q += gridDim.x) {
         const int take = (int)(a.row_limit ? min(a.take, max((int64_t)0, a.row_limit[q])) : a.take);
         const int cnt = a.acount[q];
+        long long c0 = a.clk ? clock64() : 0, c1 = c0, c2 = c0;
+        int rounds = 0, passes = 0;
         if (tid == 0) atomicAdd(&a.counters[3], cnt);
         if (take > 0 && cnt > a.cap) {
             if (tid == 0) a.fallback[atomicAdd(&a.counters[0], 1)] = (int32_t)q;
@@ -1411,12 +1414,14 @@ __global__ void __launch_bounds__(P8_THREADS) tc8_post_cta_kernel(I8PostArgs a) 
             if (tid == 0) s_L = (s_n == take) ? __double2float_rd(ts[take - 1]) : -INFINITY;
             __syncthreads();
             int nl = s_nl;
+            if (a.clk) c1 = clock64();
             // (2) score the buffered rows P8_ROWS at a time, insert, tighten L; (3) refill the
             // buffer with every appended row still able to reach the top-k, repeat
             int next = 0;  // next appended entry to filter
             bool filtered_all = false;
             for (;;) {
                 for (int b0 = 0; b0 < nl; b0 += P8_ROWS) {
+                    ++rounds;
                     const int nb = min(P8_ROWS, nl - b0);
                     const int r = tid >> 1, ch = tid & 1;
                     double acc = 0.0;
@@ -1454,6 +1459,7 @@ __global__ void __launch_bounds__(P8_THREADS) tc8_post_cta_kernel(I8PostArgs a) 
                 const int n = s_n;
                 constexpr int P8_U = 4;  // entries per thread per pass: loads in flight together
                 for (; next < cnt; next += P8_U * P8_THREADS) {
+                    ++passes;
                     uint2 v[P8_U];
 #pragma unroll
                     for (int u = 0; u < P8_U; ++u) {
@@ -1488,6 +1494,7 @@ __global__ void __launch_bounds__(P8_THREADS) tc8_post_cta_kernel(I8PostArgs a) 
                 if (nl == 0 && filtered_all) break;
             }
             if (tid == 0) atomicAdd(&a.counters[1], s_scored);
+            if (a.clk) c2 = clock64();
         } else if (tid == 0) {
             s_n = 0;
         }
@@ -1521,6 +1528,15 @@ __global__ void __launch_bounds__(P8_THREADS) tc8_post_cta_kernel(I8PostArgs a) 
                 }
             }
             if (lane == 0) a.count[q] = n;
+        }
+        if (a.clk && tid == 0) {
+            const long long c3 = clock64();
+            atomicAdd(&a.clk[0], (unsigned long long)(c1 - c0));
+            atomicAdd(&a.clk[1], (unsigned long long)(c2 - c1));
+            atomicAdd(&a.clk[2], (unsigned long long)(c3 - c2));
+            atomicAdd(&a.clk[3], (unsigned long long)rounds);
+            atomicAdd(&a.clk[4], (unsigned long long)passes);
+            atomicAdd(&a.clk[5], 1ull);
         }
         __syncthreads();
     }
@@ -1839,7 +1855,12 @@ int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats)
                     (long long)(std::max_element(ac.begin(), ac.end()) - ac.begin()));
     }
     // 3) exact rescoring of the complete candidate set
-    I8PostArgs pa{acount, abuf, cap, s.nq, s.k, std::min<int64_t>(s.k, s.n), s.row_limit, s.x32, s.dp8, s.d, s.qp,
+    unsigned long long *pclk = nullptr;
+    if (verbose) {
+        pclk = cv.take<unsigned long long>(8);
+        PR_CUDA(cudaMemsetAsync(pclk, 0, 64, st));
+    }
+    I8PostArgs pa{pclk, acount, abuf, cap, s.nq, s.k, std::min<int64_t>(s.k, s.n), s.row_limit, s.x32, s.dp8, s.d, s.qp,
                   seed_rows, seed_s, seed_n, s.rows, s.raw, s.rep, s.count, s.counters, s.fallback_list, s.nq_dev};
     const char *post_env = getenv("PR_I8_POST");  // "warp": the warp-per-query kernel (A/B knob)
     ::pr::count_launch();
@@ -1856,6 +1877,14 @@ int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats)
         tc8_post_cta_kernel<<<pgrid, P8_THREADS, psmem, st>>>(pa);
     }
     PR_LAUNCH_CHECK();
+    if (pclk) {  // measurement only: synchronises
+        unsigned long long h[8];
+        PR_CUDA(cudaMemcpyAsync(h, pclk, 64, cudaMemcpyDeviceToHost, st));
+        PR_CUDA(cudaStreamSynchronize(st));
+        const double nq = (double)std::max<unsigned long long>(1, h[5]);
+        fprintf(stderr, "tc8_post: per query: select %.0f cycles, score+refill %.0f cycles (%.2f rounds, %.2f passes), "
+                        "outputs %.0f cycles\n", h[0] / nq, h[1] / nq, h[3] / nq, h[4] / nq, h[2] / nq);
+    }
     stats->nsplit = nsplit;
     return PR_OK;
 }
