@@ -109,9 +109,13 @@ def route_batch(router, queries, vectors=None, *, mode: int = MODE_AUTO, materia
             return exc
 
     pending = None
-    hold = isinstance(kv, FixedKVCache)
-    if hold:
-        kv._compact_hold += 1  # KV values read by a launched span stay valid until its host stage
+    # KV values (write sequence numbers = arena indices) read by a launched span stay valid
+    # until its host stage: no arena compaction of the fixed-KV cache, nor of a device recall
+    # table (an add from another thread could otherwise compact it between probe and decision)
+    held = [c for c in (kv, getattr(getattr(router.backend, "knowledge", None), "_kv", None))
+            if isinstance(c, FixedKVCache)]
+    for c in held:
+        c._compact_hold += 1
     try:
         while i < n:
             if not batchable(router):
@@ -158,11 +162,11 @@ def route_batch(router, queries, vectors=None, *, mode: int = MODE_AUTO, materia
     finally:
         if pending is not None:
             _discard(router, pending)
-        if hold:
-            kv._compact_hold -= 1
-            if not kv._compact_hold:
-                with kv._lock:
-                    kv._maybe_compact()
+        for c in held:
+            c._compact_hold -= 1
+            if not c._compact_hold:
+                with c._lock:
+                    c._maybe_compact()
     router.last_batch_stats = stats
     rb = RoutedBatch(segs)
     return rb.results() if materialize else rb

@@ -124,7 +124,7 @@ class DeviceKnowledgeTable:
         if not questions:
             return
         self._kv.put_entries(list(questions), [RecallEntry(a, c) for a, c in zip(answers, confs)])
-        self._conf_d = None
+        self._conf_d = None  # rebuilt from the (possibly compacted) arena on the next gate
 
     def lookup(self, question: str) -> tuple[str, float] | None:
         from .textarena import to_device
