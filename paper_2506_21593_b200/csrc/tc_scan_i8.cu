@@ -1119,6 +1119,7 @@ __global__ void __launch_bounds__(W8_WARPS * 32) tc8_seed_kernel(I8SeedArgs a) {
 
 struct I8PostArgs {
     unsigned long long *clk;  // measurement only (PR_I8_VERBOSE): per-phase cycles, rounds, passes
+    int pf;                   // ring-prefetched chains (PR_I8_POSTPF=0: the plain loop; A/B knob)
     const int32_t *acount;
     const uint2 *abuf;
     int cap;
@@ -1324,7 +1325,40 @@ __device__ __forceinline__ void prefetch_row_l2(const float *x, int dp8, int t, 
     for (int o = t * 128; o < dp8 * 4; o += nthreads * 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + o));
 }
 
-__global__ void __launch_bounds__(P8_THREADS) tc8_post_cta_kernel(I8PostArgs a) {
+// The chain with the row streamed through a ring of P8_G blocks of 8 elements: each block's
+// slot is refilled with the block P8_G ahead right after it is consumed (static register
+// indices: the inner loop is unrolled over the ring), so P8_G blocks stay in flight instead of
+// one memory round trip per block.  d must be a multiple of 8 P8_G (else the plain loop).
+constexpr int P8_G = 4;
+__device__ __forceinline__ double einsum_chain_qd_pf(const float *__restrict__ x, const double *__restrict__ qd, int d,
+                                                     int ch) {
+    const float4 *xp = reinterpret_cast<const float4 *>(x);
+    const int nblk = d >> 3;
+    float4 ring[2 * P8_G];
+#pragma unroll
+    for (int u = 0; u < 2 * P8_G; ++u) ring[u] = __ldg(xp + u);
+    double a = 0.0;
+#pragma unroll 1
+    for (int b0 = 0; b0 < nblk; b0 += P8_G) {
+#pragma unroll
+        for (int u = 0; u < P8_G; ++u) {
+            const float4 xa = ring[2 * u], xb = ring[2 * u + 1];
+            const int nb = b0 + u + P8_G;
+            if (nb < nblk) {
+                ring[2 * u] = __ldg(xp + 2 * nb);
+                ring[2 * u + 1] = __ldg(xp + 2 * nb + 1);
+            }
+            const double *q = qd + (b0 + u) * 8;
+            a = fma((double)(ch ? xb.w : xb.z), q[6 + ch], a);
+            a = fma((double)(ch ? xb.y : xb.x), q[4 + ch], a);
+            a = fma((double)(ch ? xa.w : xa.z), q[2 + ch], a);
+            a = fma((double)(ch ? xa.y : xa.x), q[ch], a);
+        }
+    }
+    return a;
+}
+
+__global__ void __launch_bounds__(P8_THREADS, 4) tc8_post_cta_kernel(I8PostArgs a) {
     extern __shared__ __align__(16) double qd[];  // [dp8] the query in fp64
     __shared__ double ts[TC_KP];
     __shared__ int32_t tr[TC_KP];
@@ -1425,7 +1459,11 @@ __global__ void __launch_bounds__(P8_THREADS) tc8_post_cta_kernel(I8PostArgs a) 
                     const int nb = min(P8_ROWS, nl - b0);
                     const int r = tid >> 1, ch = tid & 1;
                     double acc = 0.0;
-                    if (r < nb) acc = einsum_chain_qd(a.x32 + (int64_t)list[b0 + r] * a.dp8, qd, a.d, ch);
+                    if (r < nb) {
+                        const float *xr = a.x32 + (int64_t)list[b0 + r] * a.dp8;
+                        acc = (a.d % (8 * P8_G) == 0 && a.pf) ? einsum_chain_qd_pf(xr, qd, a.d, ch)
+                                                              : einsum_chain_qd(xr, qd, a.d, ch);
+                    }
                     const double other = __shfl_xor_sync(0xffffffffu, acc, 1);
                     // only rows that rank before the current k-th can enter the list (the k-th only
                     // rises while they are inserted, so this pre-filter never drops one that would
@@ -1860,14 +1898,17 @@ int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats)
         pclk = cv.take<unsigned long long>(8);
         PR_CUDA(cudaMemsetAsync(pclk, 0, 64, st));
     }
-    I8PostArgs pa{pclk, acount, abuf, cap, s.nq, s.k, std::min<int64_t>(s.k, s.n), s.row_limit, s.x32, s.dp8, s.d, s.qp,
+    const char *pf_env = getenv("PR_I8_POSTPF");
+    I8PostArgs pa{pclk, !(pf_env && pf_env[0] == '0'), acount, abuf, cap, s.nq, s.k, std::min<int64_t>(s.k, s.n), s.row_limit, s.x32, s.dp8, s.d, s.qp,
                   seed_rows, seed_s, seed_n, s.rows, s.raw, s.rep, s.count, s.counters, s.fallback_list, s.nq_dev};
     const char *post_env = getenv("PR_I8_POST");  // "warp": the warp-per-query kernel (A/B knob)
     ::pr::count_launch();
     if (post_env && post_env[0] == 'w') {
         tc8_post_kernel<<<wgrid, W8_WARPS * 32, wsmem, st>>>(pa);
     } else {
-        const unsigned pgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(s.nq, (int64_t)sm_count() * 8));
+        const char *pg_env = getenv("PR_I8_POSTGRID");  // measurement knob: post CTAs per SM
+        const int per_sm = pg_env && atoi(pg_env) > 0 ? atoi(pg_env) : 8;
+        const unsigned pgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(s.nq, (int64_t)sm_count() * per_sm));
         const size_t psmem = (size_t)s.dp8 * sizeof(double);
         static bool p8_attr = false;
         if (!p8_attr) {
