@@ -656,6 +656,12 @@ def c1_routed(reference: bool = True, procs: int = 9, batch: int = 4096, reps: i
     simulate_batched(router, questions, n_sessions=2, n_queries=n_q, seed=cfg["seed"] + 1000, batch=batch)  # warm-up
     times, logs = [], None
     for _ in range(reps):
+        # the previous run's router (its stores hold device tables; reference cycles keep it
+        # alive) is collected HERE, not by a GC pass inside the next timed run — destroying
+        # a store synchronises the device and frees memory (two of three runs used to take 2x)
+        del router
+        gc.collect()
+        torch.cuda.synchronize()
         router = CascadeRouter(embedder=emb, backend=StubBackend(), knowledge_base=kb)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
