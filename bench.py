@@ -584,11 +584,46 @@ def main():
                           sessions=f"rank r routes sessions r, r+{world}, ... of {a.c5_sessions}")
                 configs["c5_routed_replicas"] = r5
                 del full
+                import gc
+
+                gc.collect()  # the replica's routers / payload views sit in reference cycles
+                torch.cuda.empty_cache()
             except Exception as exc:  # noqa: BLE001 - recorded, the headline stands
                 import traceback
 
                 configs["c5_routed_replicas"] = {"error": f"{type(exc).__name__}: {exc}",
                                                  "trace": traceback.format_exc()[-1500:]}
+        gsz = int(os.environ.get("BENCH_C5_GROUP", "2"))
+        if 1 < gsz < world and world % gsz == 0:
+            # the hybrid layout: groups of `gsz` ranks, each group row-shards its own copy of the
+            # KB over its ranks (one all-gather per span inside the group) and routes sessions
+            # g, g + N/gsz, ...: the L5 scan splits gsz ways and the per-span host work is spread
+            # over N/gsz groups
+            try:
+                groups = [dist.new_group(list(range(g * gsz, (g + 1) * gsz))) for g in range(world // gsz)]
+                gi, rg = rank // gsz, rank % gsz
+                glo, ghi = shard_range(a.n, rg, gsz)
+                torch.cuda.empty_cache()
+                part = build_shard(a.n, a.dim, glo, ghi)
+                r5 = C.c5_routed(part, a.n, n_sessions=a.c5_sessions, queries_per_session=a.c5_queries, shard=glo,
+                                 group=groups[gi], session_ids=range(gi, a.c5_sessions, world // gsz))
+                ms_max = max_over_ranks(r5["ms_total"])
+                total = sum_over_ranks(float(r5["queries"]) if rg == 0 else 0.0)
+                r5["workload"] = r5["workload"].replace("KB row-sharded over all ranks",
+                                                        f"{world // gsz} groups of {gsz} GPUs, each with its own KB "
+                                                        "row-sharded over the group, sessions spread over the groups")
+                r5.update(value=total / (ms_max / 1e3), ms_total=ms_max, queries=int(total), timing="max over ranks",
+                          sessions=f"group g of {world // gsz} routes sessions g, g+{world // gsz}, ... of "
+                                   f"{a.c5_sessions}")
+                configs["c5_routed_groups"] = r5
+                del part
+            except Exception as exc:  # noqa: BLE001 - recorded, the headline stands
+                import traceback
+
+                configs["c5_routed_groups"] = {"error": f"{type(exc).__name__}: {exc}",
+                                               "trace": traceback.format_exc()[-1500:]}
+                print(f"rank {rank}: c5_routed_groups failed: {traceback.format_exc()[-1500:]}", file=sys.stderr,
+                      flush=True)
     if rank == 0 and world == 1 and a.configs:
         import traceback
 

@@ -361,7 +361,7 @@ _LAST_BATCH_WALL: list = []  # (worker, session, batch, host wall ms) of every c
 
 def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_session=20_000, batch=4096,
               seed=0, parity_queries=1000, profile=False, workers=1, l5_oracle_queries=8, shard=None,
-              session_ids=None):
+              session_ids=None, group=None):
     """Routed replay over the bench's 10M x 1024 store turned into a knowledge base:
     rows [0, n_qa) hold HashEmbedder(context) of the QA pool, the rest stay dense
     distractors.
@@ -372,7 +372,9 @@ def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_se
     overlaps another's device scans on the shared GPU.
 
     ``session_ids``: replay only these of the ``n_sessions`` sessions (multi-GPU session
-    replicas: rank r of N routes sessions r, r+N, ... over its own full knowledge base)."""
+    replicas: rank r of N routes sessions r, r+N, ... over its own full knowledge base).
+    ``group``: the process group a row-sharded knowledge base (``shard``) spans (default: all
+    ranks) — the hybrid layout: groups of ranks, each with its own sharded KB and sessions."""
     import threading
 
     import torch
@@ -399,7 +401,7 @@ def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_se
         a, b = row0, min(row0 + len(store), n_qa)
         if a < b:
             store._update_rows(np.arange(a, b, dtype=np.int64) - row0, ctx[a:b])
-        store = ShardedRowIndex.wrap(store, [str(i) for i in range(n_store)], None, row0)
+        store = ShardedRowIndex.wrap(store, [str(i) for i in range(n_store)], None, row0, group=group)
         parity_queries = min(parity_queries, 200)
         l5_oracle_queries = 0
         workers = 1
