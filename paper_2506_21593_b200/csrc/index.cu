@@ -997,7 +997,12 @@ static int search_impl(pr_index *h, const float *d_q, int64_t nq, int k, uint32_
     // The int8 scan's per-(query, split) bounds start cold, so it needs long row splits to
     // amortise the start: below ~512k rows the fp16 scan is faster (40k x 1024, 2048
     // queries, k=10: 0.42 ms fp16 vs 3.5 ms int8; 10M rows: int8 1.6x faster).
-    const bool tc_pays = mode == PR_SEARCH_AUTO && tensor_ok && pr::tc_worthwhile(h->count, ql.list ? ql.hint : nq);
+    // a listed search decides with the list's CAPACITY, not the host's estimate of its live
+    // count: the estimate comes from the previous span and can be tiny (a span the caches
+    // answered), and the exact scan's cost grows with the live count — a 2M-row knowledge
+    // base once scanned a 2,000-query list in fp64 for 1.5 s (the tensor path's cost for a
+    // short list is bounded: its grid is still shaped by the estimate)
+    const bool tc_pays = mode == PR_SEARCH_AUTO && tensor_ok && pr::tc_worthwhile(h->count, nq);
     // with a floor the int8 scan starts from a known bound (no cold start, no pilot): it
     // pays at every size a tensor-core scan does
     const bool has_floor = floor > -INFINITY;
