@@ -86,20 +86,25 @@ def search_stream(index, host_batches: Iterable, k: int, *, mode: int = MODE_AUT
     cur = next(it, None)
     if cur is None:
         return
-    i = 0
-    upload(0, cur)
-    pending = None  # index of the batch whose results are on their way to the host
-    while cur is not None:
-        nxt = next(it, None)
-        scan(i, cur.shape[0])
-        if nxt is not None:
-            upload(i + 1, nxt)  # overlaps scan i
-        download(i, cur.shape[0])  # overlaps scan i + 1
-        if pending is not None:
-            ev_d2h[pending & 1].synchronize()
-            yield hres[pending & 1]
-        pending = i
-        cur = nxt
-        i += 1
-    ev_d2h[pending & 1].synchronize()
-    yield hres[pending & 1]
+    try:
+        i = 0
+        upload(0, cur)
+        pending = None  # index of the batch whose results are on their way to the host
+        while cur is not None:
+            nxt = next(it, None)
+            scan(i, cur.shape[0])
+            if nxt is not None:
+                upload(i + 1, nxt)  # overlaps scan i
+            download(i, cur.shape[0])  # overlaps scan i + 1
+            if pending is not None:
+                ev_d2h[pending & 1].synchronize()
+                yield hres[pending & 1]
+            pending = i
+            cur = nxt
+            i += 1
+        ev_d2h[pending & 1].synchronize()
+        yield hres[pending & 1]
+    finally:
+        # a consumer that stops early (or an exception) must not free buffers the copy
+        # stream still reads or writes
+        copy.synchronize()

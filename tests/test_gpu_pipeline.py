@@ -39,3 +39,9 @@ def test_search_stream_equals_search_batch(gpu, rng, sharded):
         assert (g[1].view(np.int64) == w[1].view(np.int64)).all(), f"batch {b} score bits"
         np.testing.assert_array_equal(g[2], w[2], err_msg=f"batch {b} counts")
     assert list(search_stream(index, [], k)) == []
+    # a consumer that stops after the first batch: the generator's cleanup waits for the
+    # copy stream, and a fresh stream afterwards still gives the right answers
+    first = next(iter(search_stream(index, batches, k)))
+    np.testing.assert_array_equal(first[0].numpy(), want[0][0])
+    again = [t[0].numpy().copy() for t in search_stream(index, batches[:2], k)]
+    np.testing.assert_array_equal(again[1], want[1][0])
