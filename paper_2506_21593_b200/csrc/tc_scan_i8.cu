@@ -1619,20 +1619,23 @@ static int i8_cap(int64_t n, int64_t nq) {
     return (int)cap;
 }
 
-// pilot: every I8_PILOT_STRIDE-th 256-row tile (~0.8% of the scan) when the store has
-// at least 8 * I8_PILOT_STRIDE tiles.  With the refiners' union bound (gunion_insert) the
-// main scan tightens its own bound quickly, so a sparse pilot is enough: stride 128 vs 32,
-// continuous blocks at 10M x 1024: B=4096 k=5 35.92 vs 36.45 ms; B=2048 k=10 19.90 vs 20.25;
-// B=256 2.90 vs 2.95 (no pilot at all: 38.67 ms)
-static int pilot_stride() {
+// pilot: every stride-th 256-row tile, the stride chosen so the pilot samples ~160 tiles
+// (clamped to [16, 128]), when the store has at least 8 strides of tiles.  With the refiners'
+// union bound (gunion_insert) the main scan tightens its own bound, so a sparse pilot is
+// enough on a large store — continuous blocks, top-5, B = 4096: 10M rows: stride 128 vs 32,
+// 35.92 vs 36.45 ms (no pilot 38.67); 2.5M rows: 128 / 64 / 32 all 9.92-9.99 ms — while a short
+// store wants a denser one — 1.25M rows (one of 8 row shards): 128 / 64 / 32 / 24 / 16 / 8 ->
+// 6.08 / 5.94 / 5.79 / 5.76 / 5.77 / 5.96 ms
+static int pilot_stride(int64_t ntiles) {
     const char *e = getenv("PR_I8_PILOT_STRIDE");  // measurement knob (read per search)
-    return e ? std::max(2, atoi(e)) : 128;
+    if (e) return std::max(2, atoi(e));
+    return (int)std::min<int64_t>(128, std::max<int64_t>(16, ntiles / 160));
 }
-#define I8_PILOT_STRIDE pilot_stride()
 
 static int pilot_splits(int64_t qtiles, int64_t ntiles) {
-    if (ntiles < 8 * (int64_t)I8_PILOT_STRIDE) return 0;
-    const int64_t ptiles = ceil_div<int64_t>(ntiles, I8_PILOT_STRIDE);
+    const int stride = pilot_stride(ntiles);
+    if (ntiles < 8 * (int64_t)stride) return 0;
+    const int64_t ptiles = ceil_div<int64_t>(ntiles, stride);
     const char *e = getenv("PR_I8_PSPLIT");  // measurement knob: pilot row splits
     if (e && atoi(e) > 0) return (int)std::min<int64_t>(ptiles, atoi(e));
     // ONE wave: each pilot item pays a cold start (its first tile floods the cooperative path
@@ -1814,14 +1817,15 @@ int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats)
     int32_t *seed_rows = nullptr, *seed_n = nullptr;
     double *seed_s = nullptr;
     if (psplit > 0) {
-        const int64_t ptiles = ceil_div<int64_t>(ntiles, I8_PILOT_STRIDE);
+        const int pstride = pilot_stride(ntiles);
+        const int64_t ptiles = ceil_div<int64_t>(ntiles, pstride);
         uint64_t *pcand = cv.take<uint64_t>((size_t)s.nq * psplit * I8_HALVES * TC_KP);
         seed_rows = cv.take<int32_t>((size_t)s.nq * TC_KP);
         seed_s = cv.take<double>((size_t)s.nq * TC_KP);
         seed_n = cv.take<int32_t>((size_t)s.nq);
         I8ScanParams pp{s.n, s.dp128 / I8_BLOCK_K, psplit, (int)ceil_div<int64_t>(ptiles, psplit), (int)ptiles,
                         (int)qtiles, s.k, s.rows8.xs, s.rows8.xe, s.rows8.xt, qmeta, s.row_limit, s.nq, lg, acount,
-                        abuf, cap, floor_thr, 0, I8_PILOT_STRIDE, pcand, s.x32, s.qp, s.dp8, s.d, 0, nullptr, 0, s.nq_dev};
+                        abuf, cap, floor_thr, 0, pstride, pcand, s.x32, s.qp, s.dp8, s.d, 0, nullptr, 0, s.nq_dev};
         rc = launch_scan8_cg<true>(cg, ares, (s.nq_dev ? qtiles_hint : qtiles) * psplit, qmap.map, xmap,
                                    pp, st);
         if (rc) return rc;
