@@ -1139,6 +1139,10 @@ struct I8PostArgs {
     int32_t *counters;  // [0] fallback, [1] rescored rows, [3] appended rows
     int32_t *fallback;
     const int32_t *nq_dev;
+    // the scan's published lower bounds on e_k (f2ord; nullable): a valid filter for the
+    // appended rows from the start, so the post kernel needs ONE scoring round, not two
+    // (PR_I8_POSTLG=0 restores the first round over the largest-u rows; A/B knob)
+    const uint32_t *lg;
 };
 
 __global__ void __launch_bounds__(W8_WARPS * 32) tc8_post_kernel(I8PostArgs a) {
@@ -1396,11 +1400,15 @@ __global__ void __launch_bounds__(P8_THREADS, 4) tc8_post_cta_kernel(I8PostArgs 
             }
             __syncthreads();
             const uint2 *e = a.abuf + q * (int64_t)a.cap;
+            // the scan published a lower bound on e_k for this query (k distinct rows' exact
+            // scores, rounded down): every row that can reach the top-k has u >= it, so the
+            // refill below can filter with it at once — no first round of scoring
+            const float Lscan = a.lg ? ord2f(__ldg(a.lg + q)) : -INFINITY;
             // (1) promising rows to score first, in ONE pass over the appended list: every
             // thread's largest (u, row) key, then the `take` largest of those 256 (warp 0).
             // Any rows would do for correctness (the refill below filters against the exact
             // bound they yield); the largest u give a tight bound early.
-            {
+            if (Lscan == -INFINITY) {
                 uint64_t best = 0;
 #pragma unroll 4
                 for (int i = tid; i < cnt; i += P8_THREADS) {
@@ -1445,7 +1453,7 @@ __global__ void __launch_bounds__(P8_THREADS, 4) tc8_post_cta_kernel(I8PostArgs 
             }
             // the bound before any appended row is scored: the seeds' k-th (phase (1) may have
             // selected only seeds, and then no scoring round below sets it)
-            if (tid == 0) s_L = (s_n == take) ? __double2float_rd(ts[take - 1]) : -INFINITY;
+            if (tid == 0) s_L = fmaxf(Lscan, (s_n == take) ? __double2float_rd(ts[take - 1]) : -INFINITY);
             __syncthreads();
             int nl = s_nl;
             if (a.clk) c1 = clock64();
@@ -1485,7 +1493,7 @@ __global__ void __launch_bounds__(P8_THREADS, 4) tc8_post_cta_kernel(I8PostArgs 
                         for (int j = 0; j < s_nins; ++j) top_insert(ts, tr, n, take, ex[j], ins[j]);
                         s_n = n;
                         s_scored += nb;
-                        s_L = (n == take) ? __double2float_rd(ts[take - 1]) : -INFINITY;
+                        s_L = fmaxf(Lscan, (n == take) ? __double2float_rd(ts[take - 1]) : -INFINITY);
                     }
                     __syncthreads();
                 }
@@ -1904,7 +1912,10 @@ int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats)
     }
     const char *pf_env = getenv("PR_I8_POSTPF");
     I8PostArgs pa{pclk, !(pf_env && pf_env[0] == '0'), acount, abuf, cap, s.nq, s.k, std::min<int64_t>(s.k, s.n), s.row_limit, s.x32, s.dp8, s.d, s.qp,
-                  seed_rows, seed_s, seed_n, s.rows, s.raw, s.rep, s.count, s.counters, s.fallback_list, s.nq_dev};
+                  seed_rows, seed_s, seed_n, s.rows, s.raw, s.rep, s.count, s.counters, s.fallback_list, s.nq_dev,
+                  nullptr};
+    const char *plg_env = getenv("PR_I8_POSTLG");
+    if (!(plg_env && plg_env[0] == '0')) pa.lg = lg;
     const char *post_env = getenv("PR_I8_POST");  // "warp": the warp-per-query kernel (A/B knob)
     ::pr::count_launch();
     if (post_env && post_env[0] == 'w') {
