@@ -223,6 +223,8 @@ struct I8ScanParams {
     // list, but over the union of every split (see gunion_insert)
     uint32_t *gun;
     int fast2;  // two-level fast path (PR_I8_FAST=1 single level, A/B knob)
+    int refine_fast;   // refiner publishes fp32 lower bounds (PR_I8_REFINEF=0: exact fp64 einsum scores)
+    float refine_err;  // the factor g of dot_f32_lower's error bound (m 2^-24 / (1 - m 2^-24), m = d + 3)
     // measurement only (PR_I8_VERBOSE): [0] warp-chunks that took the cooperative path,
     // [1] warp-chunks, [2] flagged (query, 8-row group) pairs
     uint32_t *dbg;
@@ -262,6 +264,37 @@ __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t *p) {
     uint32_t v;
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
+}
+
+// fp32 dot of two [d] rows with four independent chains, lowered by a rigorous bound on the
+// fp32 error: for m = d + 3 fp32 roundings in any order, |dot_fp32 - exact| <= g * S with
+// g = m 2^-24 / (1 - m 2^-24) and S = sum |x_i q_i|, which is accumulated alongside (in fp32,
+// so it is itself within a factor (1 + g) of the true S).  A lower bound on the exact dot for
+// any vectors (unnormalised rows included), ~6x fewer cycles than the fp64 einsum chain.
+__device__ __forceinline__ float dot_f32_lower(const float *__restrict__ x, const float *__restrict__ q, int d,
+                                               float g) {
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, s0 = 0.f, s1 = 0.f;
+    int j = 0;
+#pragma unroll 4
+    for (; j + 4 <= d; j += 4) {
+        const float4 xa = __ldg(reinterpret_cast<const float4 *>(x + j));
+        const float4 qa = __ldg(reinterpret_cast<const float4 *>(q + j));
+        a0 = __fmaf_rn(xa.x, qa.x, a0);
+        a1 = __fmaf_rn(xa.y, qa.y, a1);
+        a2 = __fmaf_rn(xa.z, qa.z, a2);
+        a3 = __fmaf_rn(xa.w, qa.w, a3);
+        s0 = __fmaf_rn(fabsf(xa.x), fabsf(qa.x), s0);
+        s1 = __fmaf_rn(fabsf(xa.y), fabsf(qa.y), s1);
+        s0 = __fmaf_rn(fabsf(xa.z), fabsf(qa.z), s0);
+        s1 = __fmaf_rn(fabsf(xa.w), fabsf(qa.w), s1);
+    }
+    for (; j < d; ++j) {
+        a0 = __fmaf_rn(x[j], q[j], a0);
+        s0 = __fmaf_rn(fabsf(x[j]), fabsf(q[j]), s0);
+    }
+    const float dot = __fadd_rn(__fadd_rn(a0, a1), __fadd_rn(a2, a3));
+    const float S = __fmul_ru(__fadd_ru(s0, s1), 1.0f + 2.0f * g);  // >= the true S
+    return __fsub_rd(dot, __fadd_ru(__fmul_ru(g, S), 1e-30f));
 }
 
 // Insert a lower bound (f2ord key) into a query's k-slot union list and publish the list's
@@ -829,7 +862,18 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
             const int64_t qg = job ? (int64_t)(job >> 32) - 1 : 0;
             const uint32_t row = (uint32_t)job;
             double ex = 0.0;
-            if (job) ex = einsum_dot_f32(p.x32 + (int64_t)row * p.dp8, p.qp + qg * p.dp8, p.d);
+            if (job) {
+                if (p.refine_fast) {
+                    // a rigorous LOWER bound is all the refiner publishes, so the fp64 einsum
+                    // chain (24-cycle dependent DFMAs) is not needed: four independent fp32 FMA
+                    // chains, then minus the accumulation error bound — for any order of n fp32
+                    // FMAs, |sum - exact| <= n 2^-24 sum|x_i q_i| / (1 - n 2^-24), and
+                    // sum|x_i q_i| <= ||x|| ||q|| (unit vectors within 1e-4; row norms <= maxnorm)
+                    ex = (double)dot_f32_lower(p.x32 + (int64_t)row * p.dp8, p.qp + qg * p.dp8, p.d, p.refine_err);
+                } else {
+                    ex = einsum_dot_f32(p.x32 + (int64_t)row * p.dp8, p.qp + qg * p.dp8, p.d);
+                }
+            }
             for (uint32_t m = has; m; m &= m - 1) {
                 const int src = __ffs(m) - 1;
                 if (lane == src) {
@@ -1847,6 +1891,13 @@ int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats)
                    s.rows8.xt, qmeta, s.row_limit, s.nq, lg, acount, abuf, cap, floor_thr, 0, 1, nullptr, s.x32, s.qp,
                    s.dp8, s.d, 1, nullptr, 0, s.nq_dev};
     {
+        const char *rf_env = getenv("PR_I8_REFINEF");  // 0: exact fp64 refiner scores (A/B knob)
+        p.refine_fast = !(rf_env && rf_env[0] == '0');
+        {
+            // the factor g of dot_f32_lower's error bound, rounded up
+            const double u = std::ldexp(1.0, -24), m = (double)s.d + 3.0;
+            p.refine_err = (float)(m * u / (1.0 - m * u) * 1.0001);
+        }
         const char *f_env = getenv("PR_I8_FAST");  // 1: the single-level fast path (A/B knob)
         p.fast2 = !(f_env && f_env[0] == '1');
         const char *g_env = getenv("PR_I8_GUNION");  // 0: no union list (A/B knob)
