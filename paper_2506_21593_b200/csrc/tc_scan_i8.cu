@@ -1187,6 +1187,11 @@ struct I8PostArgs {
     // appended rows from the start, so the post kernel needs ONE scoring round, not two
     // (PR_I8_POSTLG=0 restores the first round over the largest-u rows; A/B knob)
     const uint32_t *lg;
+    // prefetch each refilled row into L2 (PR_I8_POSTL2=1; A/B knob).  Off: at 10M x 1024, B = 4096
+    // the prefetches cost more than they hide (score+refill 132k -> 96k cycles per query; the
+    // ring chain's own loads keep enough in flight).  A lane pair splitting each block's loads
+    // (twice the blocks in flight in the same registers, two shuffles per block) was slower still.
+    int l2pf = 0;
 };
 
 __global__ void __launch_bounds__(W8_WARPS * 32) tc8_post_kernel(I8PostArgs a) {
@@ -1338,9 +1343,8 @@ __global__ void __launch_bounds__(W8_WARPS * 32) tc8_post_kernel(I8PostArgs a) {
 // 16 rows and set the kernel's tail (1.1 ms of a 34.5-ms C4 step).  Here 256 threads
 // select the `take` best appended rows by (u, row) with block-wide reductions, score them,
 // then filter EVERY appended row against the resulting exact bound L at once and score the
-// survivors P8_ROWS at a time (two threads per row: numpy's two einsum lanes), with the
-// rows' lines prefetched into L2 as soon as they are selected.  Same rows in, same exact
-// top-k out: any row with u < L has exact <= u < L <= e_k (strictly below the final k-th,
+// survivors P8_ROWS at a time (two threads per row: numpy's two einsum lanes).  Same rows in,
+// same exact top-k out: any row with u < L has exact <= u < L <= e_k (strictly below the final k-th,
 // so not even a tie), whatever order the survivors are scored in.
 constexpr int P8_THREADS = 256;
 constexpr int P8_ROWS = P8_THREADS / 2;  // rows scored per round (a thread pair per row)
@@ -1513,8 +1517,10 @@ __global__ void __launch_bounds__(P8_THREADS, 4) tc8_post_cta_kernel(I8PostArgs 
                     double acc = 0.0;
                     if (r < nb) {
                         const float *xr = a.x32 + (int64_t)list[b0 + r] * a.dp8;
-                        acc = (a.d % (8 * P8_G) == 0 && a.pf) ? einsum_chain_qd_pf(xr, qd, a.d, ch)
-                                                              : einsum_chain_qd(xr, qd, a.d, ch);
+                        if (a.pf && a.d % (8 * P8_G) == 0)
+                            acc = einsum_chain_qd_pf(xr, qd, a.d, ch);
+                        else
+                            acc = einsum_chain_qd(xr, qd, a.d, ch);
                     }
                     const double other = __shfl_xor_sync(0xffffffffu, acc, 1);
                     // only rows that rank before the current k-th can enter the list (the k-th only
@@ -1568,7 +1574,7 @@ __global__ void __launch_bounds__(P8_THREADS, 4) tc8_post_cta_kernel(I8PostArgs 
                         if (pass) {
                             const int pos = base + __popc(m & ((1u << lane) - 1));
                             list[pos] = row;
-                            prefetch_row_l2(a.x32 + (int64_t)row * a.dp8, a.dp8, 0, 1);
+                            if (a.l2pf) prefetch_row_l2(a.x32 + (int64_t)row * a.dp8, a.dp8, 0, 1);
                         }
                     }
                     __syncthreads();
@@ -1965,6 +1971,8 @@ int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats)
     I8PostArgs pa{pclk, !(pf_env && pf_env[0] == '0'), acount, abuf, cap, s.nq, s.k, std::min<int64_t>(s.k, s.n), s.row_limit, s.x32, s.dp8, s.d, s.qp,
                   seed_rows, seed_s, seed_n, s.rows, s.raw, s.rep, s.count, s.counters, s.fallback_list, s.nq_dev,
                   nullptr};
+    const char *pl2_env = getenv("PR_I8_POSTL2");
+    if (pl2_env && pl2_env[0] == '1') pa.l2pf = 1;
     const char *plg_env = getenv("PR_I8_POSTLG");
     if (!(plg_env && plg_env[0] == '0')) pa.lg = lg;
     const char *post_env = getenv("PR_I8_POST");  // "warp": the warp-per-query kernel (A/B knob)
