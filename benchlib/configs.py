@@ -11,6 +11,7 @@ device-timed with CUDA events and comes with its own parity check.
 from __future__ import annotations
 
 import gc
+import os
 import time
 
 import numpy as np
@@ -495,6 +496,10 @@ def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_se
             gc_ms[1] = max(gc_ms[1], dt)
 
     gc.callbacks.append(_gc_timer)
+    gc_stats0 = gc.get_stats()
+    gc_off = os.environ.get("C5_GC_DISABLE") == "1"  # measurement knob: no cyclic GC while timed
+    if gc_off:
+        gc.disable()
     e0, e1 = _events()
     torch.cuda.synchronize()
     e0.record()
@@ -513,7 +518,10 @@ def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_se
     torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
+    if gc_off:
+        gc.enable()
     gc.callbacks.remove(_gc_timer)
+    gc_counts = [b["collections"] - a["collections"] for a, b in zip(gc_stats0, gc.get_stats())]
     walls = np.array([b[3] for b in _LAST_BATCH_WALL]) if _LAST_BATCH_WALL else np.zeros(1)
     if errors:
         raise errors[0]
@@ -583,7 +591,8 @@ def c5_routed(store, n_store: int, *, n_qa=120_000, n_sessions=2, queries_per_se
         "spans": sum(t.get("spans", 0) for t in tallies), "spans_pipelined": sum(t.get("pipelined", 0) for t in tallies),
         "span_wall_ms_mean_per_session": {"n": int(walls.size), "median": float(np.median(walls)), "p90": float(np.percentile(walls, 90)),
                           "max": float(walls.max()), "sum": float(walls.sum())},
-        "gc_ms_in_timed_region": {"total": gc_ms[0], "longest": gc_ms[1]},
+        "gc_ms_in_timed_region": {"total": gc_ms[0], "longest": gc_ms[1], "collections_per_generation": gc_counts,
+                                  "disabled": gc_off},
         "stage_seconds": getattr(router, "batch_profile", None),
         "query_vectors": "device HashEmbedder (pr_hash_embed) inside the timed region, from raw query texts",
         "prep_seconds": prep_s,
