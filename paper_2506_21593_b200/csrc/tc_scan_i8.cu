@@ -223,6 +223,7 @@ struct I8ScanParams {
     // list, but over the union of every split (see gunion_insert)
     uint32_t *gun;
     int fast2;  // two-level fast path (PR_I8_FAST=1 single level, A/B knob)
+    int gskip;  // level (2) skips groups no lane passed (1) for (PR_I8_GSKIP=0: every group; A/B knob)
     int refine_fast;   // refiner publishes fp32 lower bounds (PR_I8_REFINEF=0: exact fp64 einsum scores)
     float refine_err;  // the factor g of dot_f32_lower's error bound (m 2^-24 / (1 - m 2^-24), m = d + 3)
     // measurement only (PR_I8_VERBOSE): [0] warp-chunks that took the cooperative path,
@@ -749,6 +750,8 @@ __global__ void __launch_bounds__(I8_THREADS, 1)
                             const float4 *s4 = reinterpret_cast<const float4 *>(ss + c * 32);
 #pragma unroll
                             for (int g = 0; g < 4; ++g) {
+                                // a group no lane passed (1) for: skip it warp-uniformly
+                                if (p.gskip && !__any_sync(0xffffffffu, (cmask >> g) & 1u)) continue;
                                 const float4 sa = s4[2 * g], sb = s4[2 * g + 1];
                                 float m0 = fmaxf(__fmul_rn(i2f_exact(v[8 * g + 0]), sa.x),
                                                  __fmul_rn(i2f_exact(v[8 * g + 1]), sa.y));
@@ -1906,6 +1909,8 @@ int tc8_search(Tc8Search &s, Carve &cv, cudaStream_t st, pr_search_stats *stats)
         }
         const char *f_env = getenv("PR_I8_FAST");  // 1: the single-level fast path (A/B knob)
         p.fast2 = !(f_env && f_env[0] == '1');
+        const char *gs_env = getenv("PR_I8_GSKIP");
+        p.gskip = !(gs_env && gs_env[0] == '0');
         const char *g_env = getenv("PR_I8_GUNION");  // 0: no union list (A/B knob)
         if (!(g_env && g_env[0] == '0')) {
             p.gun = cv.take<uint32_t>((size_t)s.nq * TC_KP);
