@@ -51,6 +51,8 @@ settle thread.
 from __future__ import annotations
 
 import time
+from collections import deque
+from itertools import repeat
 
 import numpy as np
 
@@ -59,7 +61,7 @@ from .caches import FixedKVCache, SemanticCache
 from .errors import CascadeError
 from .index import MODE_AUTO, FlatIndex
 from .knowledge import AdaptiveKnowledgeMemory
-from .ledger import BatchLedger, CtxRows, LedgerEntry, entry_text_conf
+from .ledger import BatchLedger, CtxRows, entries_of, entry_text_conf
 from .records import LayerTag
 from .router import LayerProbe
 from .textarena import to_device
@@ -276,7 +278,7 @@ class _Span:
 
     __slots__ = ("start", "end", "size", "B", "qs", "texts", "arena", "n_pre_sc", "new_js", "prev_last",
                  "prev", "host", "event", "kb_rows_d", "kb_cnt_d", "nlist_d", "t_start", "entries", "recall",
-                 "l3", "l3_val")
+                 "l3", "l3_val", "first", "first_of")
 
 
 def _launch(router, queries, vectors, start: int, end: int, mode: int, prev: "_Span | None") -> _Span:
@@ -305,14 +307,15 @@ def _launch(router, queries, vectors, start: int, end: int, mode: int, prev: "_S
 
     # ---- window dedupe (host, texts only): an earlier write of the same text in this span
     # or in the previous one (that span is written back before this span's queries route)
-    first_of = {t: j for j, t in zip(range(B - 1, -1, -1), reversed(texts))}  # earliest index wins
+    first_of = dict(zip(reversed(texts), range(B - 1, -1, -1)))  # earliest index wins (inserted last)
     first = np.fromiter(map(first_of.__getitem__, texts), dtype=np.int64, count=B)
+    sp.first, sp.first_of = first, first_of
     ar = np.arange(B)
     rep = first < ar
     sp.prev_last = None
     sp.prev = prev
     if prev is not None:
-        prev_last = {t: j for j, t in enumerate(prev.texts)}  # latest writer in the previous span
+        prev_last = dict(zip(prev.texts, range(prev.B)))  # latest writer in the previous span
         sp.prev_last = prev_last
         rep |= np.fromiter(map(prev_last.__contains__, texts), dtype=bool, count=B)
 
@@ -321,11 +324,13 @@ def _launch(router, queries, vectors, start: int, end: int, mode: int, prev: "_S
     sp.n_pre_sc = n_pre_sc = len(sc_index)
     with sc_index._lock:
         sc_rows = sc_index._row_by_id
-        new_js = np.array([j for j in np.flatnonzero(first == ar).tolist() if texts[j] not in sc_rows],
-                          dtype=np.int64)
+        f_js = np.flatnonzero(first == ar)
+        known = np.fromiter(map(sc_rows.__contains__, map(texts.__getitem__, f_js.tolist())), dtype=bool,
+                            count=f_js.size)
+        new_js = f_js[~known]
     sp.new_js = new_js
     if new_js.size:
-        sc_index.extend_arrays([texts[j] for j in new_js], Vd[_lib.h2d(new_js)],
+        sc_index.extend_arrays(list(map(texts.__getitem__, new_js.tolist())), Vd[_lib.h2d(new_js)],
                                payloads=[None] * int(new_js.size), validate=False)
     sc_limit = n_pre_sc + np.searchsorted(new_js, ar, side="left")  # rows written by queries i < j
     prof.mark("L.dedupe+sc_extend")
@@ -453,7 +458,7 @@ def _finish(router, sp: _Span, *, more_follow: bool):
     # host work that needs no device result: the ledger shell and the span's cache entries
     ledger = BatchLedger.__new__(BatchLedger)
     now = time.monotonic_ns()
-    entries = sp.entries = [LedgerEntry(t, ledger, j, now) for j, t in enumerate(texts)]
+    entries = sp.entries = entries_of(texts, ledger, now)
     prof.mark("prep")
     l1, l2, slot, l4_unsure, sc_row, kv_val, kb_rows, kb_cnt, nlist = _unpack(sp, cfg.akm_seed_k)
     router._cascade_nlist_hint = max(1, nlist)
@@ -478,26 +483,7 @@ def _finish(router, sp: _Span, *, more_follow: bool):
     sv = serving
     hit_js = np.flatnonzero((sv == v1) | (sv == v2))
     if hit_js.size:
-        sc_ids = sc_index._ids
-        kv_entry, sc_payload = kv.entry_at, sc_index.payload_at
-        prev_last = sp.prev_last
-        prev_entries = sp.prev.entries if sp.prev is not None else None
-        latest: dict[str, int] = {}
-        nxt = 0
-        hl = hit_js.tolist()
-        for j in hl:
-            latest.update(zip(texts[nxt:j], range(nxt, j)))  # writers since the previous hit
-            nxt = j
-            key = texts[j] if sv[j] == v1 else sc_ids[int(sc_row[j])]  # the serving layer's key
-            i = latest.get(key, -1)
-            if i >= 0:  # an earlier query of this span wrote the key
-                text[j], conf_l[j] = text[i], conf_l[i]
-            elif prev_last is not None and key in prev_last:  # the previous span wrote it last
-                text[j], conf_l[j] = entry_text_conf(prev_entries[prev_last[key]])
-            elif sv[j] == v1:
-                text[j], conf_l[j] = entry_text_conf(kv_entry(int(kv_val[j])))
-            else:
-                text[j], conf_l[j] = entry_text_conf(sc_payload(int(sc_row[j])))
+        _serve_hits(router, sp, hit_js, sv == v1, sc_row, kv_val, text, conf_l)
     conf = np.asarray(conf_l, dtype=np.float64)
     ctx_rows = CtxRows(kb_rows, slot[:p], kb_cnt, cfg.retrieval_k, sv == v5)
     probe_prefix = {}
@@ -508,6 +494,60 @@ def _finish(router, sp: _Span, *, more_follow: bool):
     _writeback(router, sp, p, entries, ledger, serving, slot, kb_rows, kb_cnt, more_follow, prof)
     sp.prev = sp.prev_last = None  # the previous span is no longer read: no chain of spans stays alive
     return p, ledger
+
+
+def _serve_hits(router, sp, hit_js, is_l1, sc_row, kv_val, text, conf_l):
+    """Answers of the span's L1 / L2 hits, in order: a hit serves a copy of the latest
+    answer written for its key (router.py:333-337 writes every routed query back) — by
+    an earlier query of this span, else by the previous span, else the stored entry.
+
+    The in-span writer of hit j is the last i < j whose text is the key: with each text
+    numbered by its first occurrence in the span (``sp.first``), that is one
+    searchsorted over the sorted (text number, position) pairs instead of a dict
+    replayed query by query."""
+    texts = sp.texts
+    B = len(texts)
+    first = sp.first
+    n = hit_js.size
+    h1 = is_l1[hit_js]
+    keys = [None] * n
+    kid = np.full(n, -1, dtype=np.int64)
+    t1 = np.flatnonzero(h1)
+    if t1.size:
+        kid[t1] = first[hit_js[t1]]
+        for t, j in zip(t1.tolist(), hit_js[t1].tolist()):
+            keys[t] = texts[j]
+    t2 = np.flatnonzero(~h1)
+    if t2.size:
+        sc_ids = router.semantic_cache.index._ids
+        k2 = [sc_ids[r] for r in sc_row[hit_js[t2]].tolist()]
+        fo = sp.first_of.get
+        kid[t2] = np.fromiter(map(fo, k2, repeat(-1)), dtype=np.int64, count=t2.size)
+        for t, k in zip(t2.tolist(), k2):
+            keys[t] = k
+    w = B + 1
+    pairs = np.sort(first * w + np.arange(B))
+    at = np.searchsorted(pairs, kid * w + hit_js, side="left") - 1
+    cand = pairs[np.maximum(at, 0)]
+    src = np.where((kid >= 0) & (at >= 0) & (cand // w == kid), cand % w, -1)
+    # written before this span: from the previous span's entries or the stores
+    prev_last = sp.prev_last
+    prev_entries = sp.prev.entries if sp.prev is not None else None
+    kv_entry, sc_payload = router.kv_cache.entry_at, router.semantic_cache.index.payload_at
+    ext = np.flatnonzero(src < 0)
+    for t, j, l1 in zip(ext.tolist(), hit_js[ext].tolist(), h1[ext].tolist()):
+        key = keys[t]
+        if prev_last is not None and key in prev_last:
+            text[j], conf_l[j] = entry_text_conf(prev_entries[prev_last[key]])
+        elif l1:
+            text[j], conf_l[j] = entry_text_conf(kv_entry(int(kv_val[j])))
+        else:
+            text[j], conf_l[j] = entry_text_conf(sc_payload(int(sc_row[j])))
+    # written earlier in this span: copies, in order (a writer may itself be a hit)
+    ins = np.flatnonzero(src >= 0)
+    for j, i in zip(hit_js[ins].tolist(), src[ins].tolist()):
+        text[j] = text[i]
+        conf_l[j] = conf_l[i]
 
 
 def _decide(router, sp, l1, l2, slot, l4_unsure, kb_rows, kb_cnt, prof):
@@ -620,8 +660,8 @@ def _writeback(router, sp, p, entries, ledger, serving, slot, kb_rows, kb_cnt, m
             sc_index.truncate(sp.n_pre_sc + n_new_kept)
     with sc._lock, sc_index._lock:
         payloads, rowmap = sc_index._payloads, sc_index._row_by_id
-        for t, e in zip(texts[:p], entries):
-            payloads[rowmap[t]] = e  # in order: the last write of a text wins
+        # in order (the last write of a text wins), the loop run by map in C
+        deque(map(payloads.__setitem__, map(rowmap.__getitem__, texts[:p]), entries), maxlen=0)
         seq = sc._seq
         sc._recency.update(zip(texts[:p], range(seq + 1, seq + p + 1)))
         sc._seq = seq + p

@@ -12,6 +12,9 @@ identical to what sequential ``route`` would have produced.
 """
 from __future__ import annotations
 
+from functools import partial
+from itertools import count, repeat
+from operator import itemgetter
 from typing import Sequence
 
 import numpy as np
@@ -94,23 +97,38 @@ class BatchLedger:
         return {LayerTag(int(v)): int(c) for v, c in zip(vals, cnt)}
 
 
-class LedgerEntry:
-    """A cache entry written by a routed batch; ``answer`` is built on first use."""
+class LedgerEntry(tuple):
+    """A cache entry written by a routed batch; ``answer`` is built on first use.
 
-    __slots__ = ("query_text", "created_at_ns", "_ledger", "_j")
+    A tuple ``(query_text, ledger, j, created_at_ns)``: a span builds one per query, and
+    ``entries_of`` makes them without running Python per entry (a class with ``__init__``
+    cost ~0.3 us each, 1.2 ms per 4096-query span)."""
 
-    def __init__(self, query_text: str, ledger: BatchLedger, j: int, created_at_ns: int):
-        self.query_text = query_text
-        self.created_at_ns = created_at_ns
-        self._ledger = ledger
-        self._j = j
+    __slots__ = ()
+
+    def __new__(cls, query_text: str, ledger: BatchLedger, j: int, created_at_ns: int):
+        return tuple.__new__(cls, (query_text, ledger, j, created_at_ns))
+
+    query_text = property(itemgetter(0))
+    _ledger = property(itemgetter(1))
+    _j = property(itemgetter(2))
+    created_at_ns = property(itemgetter(3))
 
     @property
     def answer(self) -> AnswerRecord:
-        return self._ledger.answer(self._j)
+        return self[1].answer(self[2])
 
     def text_conf(self) -> tuple[str, float]:
-        return self._ledger.text[self._j], float(self._ledger.conf[self._j])
+        lg, j = self[1], self[2]
+        return lg.text[j], float(lg.conf[j])
+
+
+_make_entry = partial(tuple.__new__, LedgerEntry)
+
+
+def entries_of(texts: Sequence[str], ledger: BatchLedger, created_at_ns: int) -> list:
+    """``[LedgerEntry(t, ledger, j, created_at_ns) for j, t in enumerate(texts)]``, built in C."""
+    return list(map(_make_entry, zip(texts, repeat(ledger), count(), repeat(created_at_ns))))
 
 
 def entry_text_conf(entry) -> tuple[str, float]:

@@ -40,5 +40,5 @@ if os.environ.get("C5_CPROFILE", "1") == "1":
     pr.disable()
     print("cprofile run", round(r["value"]))
     s = io.StringIO()
-    pstats.Stats(pr, stream=s).sort_stats("tottime").print_stats(40)
-    print(s.getvalue()[:9000])
+    pstats.Stats(pr, stream=s).sort_stats("tottime").print_stats("paper_2506|_lib|pinned|ledger", 45)
+    print(s.getvalue()[:12000])
