@@ -53,15 +53,16 @@ from __future__ import annotations
 import time
 from collections import deque
 from itertools import repeat
+from operator import attrgetter, getitem, is_, itemgetter
 
 import numpy as np
 
 from . import _lib, generation, pinned
 from .caches import FixedKVCache, SemanticCache
 from .errors import CascadeError
-from .index import MODE_AUTO, FlatIndex
+from .index import _DEFERRED, MODE_AUTO, FlatIndex
 from .knowledge import AdaptiveKnowledgeMemory
-from .ledger import BatchLedger, CtxRows, entries_of, entry_text_conf
+from .ledger import BatchLedger, CtxRows, LedgerEntry, entries_of, entry_text_conf
 from .records import LayerTag
 from .router import LayerProbe
 from .textarena import to_device
@@ -319,6 +320,7 @@ def _launch(router, queries, vectors, start: int, end: int, mode: int, prev: "_S
         sp.prev_last = prev_last
         rep |= np.fromiter(map(prev_last.__contains__, texts), dtype=bool, count=B)
 
+    prof.mark("L.dedupe")
     # ---- L2 rows write-back will create: first occurrences of texts new to the cache
     sc_index = sc.index
     sp.n_pre_sc = n_pre_sc = len(sc_index)
@@ -329,11 +331,12 @@ def _launch(router, queries, vectors, start: int, end: int, mode: int, prev: "_S
                             count=f_js.size)
         new_js = f_js[~known]
     sp.new_js = new_js
+    prof.mark("L.new_js")
     if new_js.size:
         sc_index.extend_arrays(list(map(texts.__getitem__, new_js.tolist())), Vd[_lib.h2d(new_js)],
                                payloads=[None] * int(new_js.size), validate=False)
     sc_limit = n_pre_sc + np.searchsorted(new_js, ar, side="left")  # rows written by queries i < j
-    prof.mark("L.dedupe+sc_extend")
+    prof.mark("L.sc_extend")
 
     # ---- L1 probe, L2 top-1, gate + miss-list compaction: all on the device
     u8, i64 = torch.uint8, torch.int64
@@ -484,13 +487,14 @@ def _finish(router, sp: _Span, *, more_follow: bool):
     hit_js = np.flatnonzero((sv == v1) | (sv == v2))
     if hit_js.size:
         _serve_hits(router, sp, hit_js, sv == v1, sc_row, kv_val, text, conf_l)
+    prof.mark("hits")
     conf = np.asarray(conf_l, dtype=np.float64)
     ctx_rows = CtxRows(kb_rows, slot[:p], kb_cnt, cfg.retrieval_k, sv == v5)
     probe_prefix = {}
     for L in order:
         probe_prefix[L] = tuple(_PROBE[M, "rejected" if M is L3 else "miss"] for M in order[: pos[L]])
     ledger.__init__(qs[:p], serving, lat, text, conf, ctx_rows, router.knowledge_base.index, probe_prefix)
-    prof.mark("materialise")
+    prof.mark("ledger")
     _writeback(router, sp, p, entries, ledger, serving, slot, kb_rows, kb_cnt, more_follow, prof)
     sp.prev = sp.prev_last = None  # the previous span is no longer read: no chain of spans stays alive
     return p, ledger
@@ -504,50 +508,70 @@ def _serve_hits(router, sp, hit_js, is_l1, sc_row, kv_val, text, conf_l):
     The in-span writer of hit j is the last i < j whose text is the key: with each text
     numbered by its first occurrence in the span (``sp.first``), that is one
     searchsorted over the sorted (text number, position) pairs instead of a dict
-    replayed query by query."""
+    replayed query by query.  The per-hit gathers below run as ``map`` passes (the
+    loop in C; ~2,000 hits per 4096-query span)."""
     texts = sp.texts
     B = len(texts)
-    first = sp.first
     n = hit_js.size
     h1 = is_l1[hit_js]
-    keys = [None] * n
+    keys = [None] * n  # the serving layer's key of each hit
     kid = np.full(n, -1, dtype=np.int64)
     t1 = np.flatnonzero(h1)
     if t1.size:
-        kid[t1] = first[hit_js[t1]]
-        for t, j in zip(t1.tolist(), hit_js[t1].tolist()):
-            keys[t] = texts[j]
+        kid[t1] = sp.first[hit_js[t1]]
+        _put(keys, t1.tolist(), map(texts.__getitem__, hit_js[t1].tolist()))
     t2 = np.flatnonzero(~h1)
     if t2.size:
-        sc_ids = router.semantic_cache.index._ids
-        k2 = [sc_ids[r] for r in sc_row[hit_js[t2]].tolist()]
-        fo = sp.first_of.get
-        kid[t2] = np.fromiter(map(fo, k2, repeat(-1)), dtype=np.int64, count=t2.size)
-        for t, k in zip(t2.tolist(), k2):
-            keys[t] = k
+        k2 = list(map(router.semantic_cache.index._ids.__getitem__, sc_row[hit_js[t2]].tolist()))
+        kid[t2] = np.fromiter(map(sp.first_of.get, k2, repeat(-1)), dtype=np.int64, count=t2.size)
+        _put(keys, t2.tolist(), k2)
     w = B + 1
-    pairs = np.sort(first * w + np.arange(B))
+    pairs = np.sort(sp.first * w + np.arange(B))
     at = np.searchsorted(pairs, kid * w + hit_js, side="left") - 1
     cand = pairs[np.maximum(at, 0)]
     src = np.where((kid >= 0) & (at >= 0) & (cand // w == kid), cand % w, -1)
-    # written before this span: from the previous span's entries or the stores
-    prev_last = sp.prev_last
-    prev_entries = sp.prev.entries if sp.prev is not None else None
-    kv_entry, sc_payload = router.kv_cache.entry_at, router.semantic_cache.index.payload_at
+    # written before this span: by the previous span (its entries), else the stored entry
     ext = np.flatnonzero(src < 0)
-    for t, j, l1 in zip(ext.tolist(), hit_js[ext].tolist(), h1[ext].tolist()):
-        key = keys[t]
-        if prev_last is not None and key in prev_last:
-            text[j], conf_l[j] = entry_text_conf(prev_entries[prev_last[key]])
-        elif l1:
-            text[j], conf_l[j] = entry_text_conf(kv_entry(int(kv_val[j])))
+    m = ext.size
+    if m:
+        ej = hit_js[ext]
+        keys_e = list(map(keys.__getitem__, ext.tolist()))
+        ents = [None] * m
+        pidx = np.full(m, -1, dtype=np.int64)
+        if sp.prev_last is not None:
+            pidx = np.fromiter(map(sp.prev_last.get, keys_e, repeat(-1)), dtype=np.int64, count=m)
+            inprev = np.flatnonzero(pidx >= 0)
+            _put(ents, inprev.tolist(), map(sp.prev.entries.__getitem__, pidx[inprev].tolist()))
+        stored = pidx < 0
+        s1 = np.flatnonzero(stored & h1[ext])
+        _put(ents, s1.tolist(), map(router.kv_cache.entry_at, kv_val[ej[s1]].tolist()))
+        s2 = np.flatnonzero(stored & ~h1[ext])
+        _put(ents, s2.tolist(), map(router.semantic_cache.index.payload_at, sc_row[ej[s2]].tolist()))
+        ejl = ej.tolist()
+        if set(map(type, ents)) == {LedgerEntry}:
+            # (ledger.text[j], ledger.conf[j]) of every entry, without a Python call each
+            lgs, js = list(map(_ENT_LEDGER, ents)), list(map(_ENT_J, ents))
+            _put(text, ejl, map(getitem, map(_TEXT, lgs), js))
+            _put(conf_l, ejl, map(float, map(getitem, map(_CONF, lgs), js)))
         else:
-            text[j], conf_l[j] = entry_text_conf(sc_payload(int(sc_row[j])))
-    # written earlier in this span: copies, in order (a writer may itself be a hit)
+            for j, e in zip(ejl, ents):
+                text[j], conf_l[j] = entry_text_conf(e)
+    # written earlier in this span: copies in order (a writer may itself be a hit; map
+    # reads text[i] only after every earlier assignment ran)
     ins = np.flatnonzero(src >= 0)
-    for j, i in zip(hit_js[ins].tolist(), src[ins].tolist()):
-        text[j] = text[i]
-        conf_l[j] = conf_l[i]
+    if ins.size:
+        jl, il = hit_js[ins].tolist(), src[ins].tolist()
+        _put(text, jl, map(text.__getitem__, il))
+        _put(conf_l, jl, map(conf_l.__getitem__, il))
+
+
+_ENT_LEDGER, _ENT_J = itemgetter(1), itemgetter(2)
+_TEXT, _CONF, _ANSWER = attrgetter("text"), attrgetter("conf"), attrgetter("answer")
+
+
+def _put(lst: list, idx, vals) -> None:
+    """lst[i] = v for the pairs in order (consumed lazily: one pass in C)."""
+    deque(map(lst.__setitem__, idx, vals), maxlen=0)
 
 
 def _decide(router, sp, l1, l2, slot, l4_unsure, kb_rows, kb_cnt, prof):
@@ -627,18 +651,27 @@ def _decide(router, sp, l1, l2, slot, l4_unsure, kb_rows, kb_cnt, prof):
     if l5_js:
         l5_slots = slot[l5_js]
         if stub:
-            payload_at, first_sentence = kb.index.payload_at, generation.first_sentence
-            cc = backend.context_confidence
-            for j, r in zip(l5_js, kb_rows[l5_slots, 0].tolist()):
-                top = payload_at(r)
-                text[j] = top.answer if top.answer else first_sentence(top.text)
-                conf_l[j] = cc
+            # top passage of each query, its answer, else its first sentence: map passes
+            # (the loop in C) over the ~2,000 retrieval answers of a 4096-query span
+            kbi = kb.index
+            rows = kb_rows[l5_slots, 0].tolist()
+            pl = getattr(kbi, "_payloads", None)
+            tops = list(map(pl.__getitem__, rows)) if pl is not None else None
+            if tops is None or any(map(is_, tops, repeat(_DEFERRED))):
+                tops = list(map(kbi.payload_at, rows))
+            ans = list(map(_ANSWER, tops))
+            if not all(ans):
+                first_sentence = generation.first_sentence
+                ans = [a if a else first_sentence(t.text) for a, t in zip(ans, tops)]
+            _put(text, l5_js, ans)
+            _put(conf_l, l5_js, repeat(backend.context_confidence, len(l5_js)))
             backend.context_calls += len(l5_js)
         else:
             for j, s5 in zip(l5_js, l5_slots.tolist()):
                 passages = [kb.index.payload_at(int(r)) for r in kb_rows[s5, : min(k_ctx, int(kb_cnt[s5]))]]
                 a = generation.generate_with_context(backend, qs[j], passages, L5)
                 text[j], conf_l[j] = a.text, a.confidence
+    prof.mark("answers")
     return p, serving, lat, text, conf_l, recalled
 
 
@@ -662,6 +695,7 @@ def _writeback(router, sp, p, entries, ledger, serving, slot, kb_rows, kb_cnt, m
         payloads, rowmap = sc_index._payloads, sc_index._row_by_id
         # in order (the last write of a text wins), the loop run by map in C
         deque(map(payloads.__setitem__, map(rowmap.__getitem__, texts[:p]), entries), maxlen=0)
+        prof.mark("wb.sc_payloads")
         seq = sc._seq
         sc._recency.update(zip(texts[:p], range(seq + 1, seq + p + 1)))
         sc._seq = seq + p

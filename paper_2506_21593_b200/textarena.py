@@ -33,6 +33,7 @@ class DeviceTexts(tuple):
         t.host_off = host_off
         t.n = len(host_off) - 1
         t.nbytes = int(host_off[-1])
+        t.ascii = None  # True when every text is ASCII (one byte per character), if known
         return t
 
     def nbytes_of(self, n: int) -> int:
@@ -44,4 +45,7 @@ def to_device(texts: Sequence[str]) -> DeviceTexts:
     from ._lib import h2d
 
     data, off = encode_texts(texts)
-    return DeviceTexts(h2d(data), h2d(off), off)
+    t = DeviceTexts(h2d(data), h2d(off), off)
+    # UTF-8 spends >= 2 bytes on every non-ASCII character (and surrogatepass 3 on a surrogate)
+    t.ascii = sum(map(len, texts)) == t.nbytes
+    return t

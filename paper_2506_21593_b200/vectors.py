@@ -164,7 +164,11 @@ class HashEmbedder:
         L = _lib.load()
         _lib.check(L.pr_hash_embed(_lib.ptr(d_data), _lib.ptr(d_off), n, self.dim, int.from_bytes(self._key, "big"),
                                    _lib.ptr(out), _lib.ptr(flag), _lib.stream_ptr()), "hash_embed")
-        host = [i for i, t in enumerate(texts) if not (t and t.isascii() and len(t) <= 512)]
+        if getattr(arena, "ascii", None):  # all ASCII: a text's byte count is its length
+            lens = np.diff(arena.host_off)
+            host = np.flatnonzero((lens == 0) | (lens > 512)).tolist()
+        else:
+            host = [i for i, t in enumerate(texts) if not (t and t.isascii() and len(t) <= 512)]
         if host:
             rows = np.stack([self.embed_array(texts[i]) for i in host])
             out[torch.tensor(host, device="cuda")] = torch.from_numpy(rows).cuda()
