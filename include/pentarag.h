@@ -246,6 +246,62 @@ int pr_cascade_seeds(const int64_t *d_prev_rows, const int32_t *d_prev_cnt, cons
                      const int64_t *d_rows, const int32_t *d_cnt, const int32_t *d_n, int seed_k, int32_t *d_mark,
                      int64_t *d_out_rows, int64_t out_max, int32_t *d_nout, int64_t *d_before, void *stream);
 
+/* One span of the on-device cascade in ONE call (SURVEY §8(b) pr_cascade_route; router.py:227-273
+ * _probe and :275-364 route for B queries): the L1 probe (pr_kv_get_text), the L2 top-1
+ * threshold search over the rows each query may see (pr_index_search_floor, d_sc_limit),
+ * pr_cascade_gate, the knowledge-base scan of the compacted miss list (pr_index_search_list),
+ * the L4 guard (pr_cascade_seeds; the seeds appended to the scratch store `guard` with
+ * pr_index_append_from; top-1 threshold searches over it, row-limited per listed query, and
+ * over the adaptive memory), then ONE packed int64 record for the host's single read-back:
+ *   d_packed[9B + 1 + B*seed_k] = l1[B] l2[B] slot[B] l4[B] sc_row[B] kv_val[B] kb_cnt[B]
+ *                                  l3[B] l3_val[B] nlist kb_rows[B*seed_k]
+ * (-1 in the columns of a layer not probed; kb_rows past nlist undefined).  The caller holds
+ * the stores' locks, clears `guard` first, and keeps d_kb_rows / d_kb_cnt / d_nlist alive
+ * for the next span (its d_prev_*).  d_scratch: pr_cascade_route_scratch(B, seed_k, prev_B)
+ * bytes, free again once the stream has passed this call. */
+typedef struct pr_cascade_span {
+    int64_t B;
+    const float *d_vec; /* [B, dim] fp32 query vectors */
+    uint32_t mode;      /* PR_SEARCH_* for every search of the span */
+    /* L1: kv NULL = not probed; keys are the UTF-8 arena of the span's texts */
+    pr_kv *kv;
+    const uint8_t *d_text;
+    const int64_t *d_text_off;
+    const uint8_t *d_rep; /* [B] an earlier in-window write of the same text (required) */
+    /* L3 decided on the device (pr_recall_gate): NULL = none */
+    const uint8_t *d_l3_hit;
+    const int64_t *d_l3_val;
+    /* L2: sc NULL = not probed */
+    pr_index *sc;
+    const int64_t *d_sc_limit; /* [B] rows of the semantic cache query j sees */
+    double sc_threshold;
+    int l1_blocks, l2_blocks, l3_blocks; /* fast layers probed before the vector layers */
+    /* L5: the knowledge base, seeds per listed query, expected list length */
+    pr_index *kb;
+    int seed_k;
+    int64_t nlist_hint;
+    int64_t *d_kb_rows; /* [B, seed_k] */
+    double *d_kb_raw;   /* [B, seed_k] */
+    double *d_kb_rep;   /* [B, seed_k] */
+    int32_t *d_kb_cnt;  /* [B] */
+    int32_t *d_nlist;   /* [1] */
+    int32_t *d_slot;    /* [B] list position of query j or -1 */
+    /* L4: probe_l4 0 = not probed; akm_rows 0 = empty adaptive memory */
+    int probe_l4;
+    pr_index *akm;
+    int64_t akm_rows;
+    double akm_threshold;
+    pr_index *guard; /* scratch store, cleared by the caller */
+    int32_t *d_mark; /* pr_cascade_mark_init'ed, knowledge-base rows long */
+    const int64_t *d_prev_rows;
+    const int32_t *d_prev_cnt;
+    const int32_t *d_prev_n;
+    int64_t prev_B;
+    int64_t *d_packed; /* [9B + 1 + B*seed_k] */
+} pr_cascade_span;
+int64_t pr_cascade_route_scratch(int64_t B, int seed_k, int64_t prev_B);
+int pr_cascade_route(const pr_cascade_span *s, void *d_scratch, int64_t scratch_bytes, void *stream);
+
 /* ---- device HashEmbedder: embedding.py:117-160 ------------
  * Texts are a UTF-8 arena + offsets as for pr_fingerprint; d_out is fp32
  * [n, dim], bit-identical to HashEmbedder(seed).embed(text).values for every

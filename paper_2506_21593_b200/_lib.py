@@ -107,7 +107,28 @@ SIGNATURES = {
     "pr_l2_fetch_granularity": (c_int, [c_int, c_vp]),
     "pr_hash_embed": (c_int, [c_vp, c_vp, c_i64, c_int, ctypes.c_uint64, c_vp, c_vp, c_vp]),
     "pr_blake2b64_host": (ctypes.c_uint64, [ctypes.c_uint64, ctypes.c_char_p, c_vp, c_i64]),
+    "pr_cascade_route_scratch": (c_i64, [c_i64, c_int, c_i64]),
+    "pr_cascade_route": (c_int, [c_vp, c_vp, c_i64, c_vp]),
 }
+
+
+class CascadeSpan(ctypes.Structure):
+    """pr_cascade_span (include/pentarag.h): one span of the on-device cascade."""
+
+    _fields_ = [
+        ("B", c_i64), ("d_vec", c_vp), ("mode", c_u32),
+        ("kv", c_vp), ("d_text", c_vp), ("d_text_off", c_vp), ("d_rep", c_vp),
+        ("d_l3_hit", c_vp), ("d_l3_val", c_vp),
+        ("sc", c_vp), ("d_sc_limit", c_vp), ("sc_threshold", c_dbl),
+        ("l1_blocks", c_int), ("l2_blocks", c_int), ("l3_blocks", c_int),
+        ("kb", c_vp), ("seed_k", c_int), ("nlist_hint", c_i64),
+        ("d_kb_rows", c_vp), ("d_kb_raw", c_vp), ("d_kb_rep", c_vp), ("d_kb_cnt", c_vp), ("d_nlist", c_vp),
+        ("d_slot", c_vp),
+        ("probe_l4", c_int), ("akm", c_vp), ("akm_rows", c_i64), ("akm_threshold", c_dbl),
+        ("guard", c_vp), ("d_mark", c_vp),
+        ("d_prev_rows", c_vp), ("d_prev_cnt", c_vp), ("d_prev_n", c_vp), ("prev_B", c_i64),
+        ("d_packed", c_vp),
+    ]
 
 
 def load(path: str = LIB_PATH):

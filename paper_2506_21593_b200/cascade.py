@@ -50,6 +50,8 @@ settle thread.
 """
 from __future__ import annotations
 
+import ctypes
+import os
 import time
 from collections import deque
 from itertools import repeat
@@ -338,6 +340,8 @@ def _launch(router, queries, vectors, start: int, end: int, mode: int, prev: "_S
     sc_limit = n_pre_sc + np.searchsorted(new_js, ar, side="left")  # rows written by queries i < j
     prof.mark("L.sc_extend")
 
+    if _ROUTE_C and not getattr(kb.index, "sharded", False):
+        return _launch_c(router, sp, Vd, arena, rep, sc_limit, mode, prev, pos, prof)
     # ---- L1 probe, L2 top-1, gate + miss-list compaction: all on the device
     u8, i64 = torch.uint8, torch.int64
     kv_hit = kv_val = None
@@ -423,6 +427,91 @@ def _launch(router, queries, vectors, start: int, end: int, mode: int, prev: "_S
             (l3_val if l3_val is not None else none),
             nlist.to(i64)]
     packed = torch.cat([c.reshape(-1) for c in cols] + [kb_rows.reshape(-1)])
+    sp.host, sp.event = pinned.ring().d2h(packed)
+    prof.mark("L.pack")
+    prof.merge_into(router)
+    return sp
+
+
+# PR_CASCADE_ROUTE=0: the span's device stage as separate calls from Python (A/B knob; a
+# row-sharded knowledge base always takes that path: its scan ends in a collective)
+_ROUTE_C = os.environ.get("PR_CASCADE_ROUTE", "1") != "0"
+
+
+def _hv(h):
+    return h.value if isinstance(h, ctypes.c_void_p) else h
+
+
+def _launch_c(router, sp, Vd, arena, rep, sc_limit, mode, prev, pos, prof) -> _Span:
+    """The span's device stage as ONE pr_cascade_route call (include/pentarag.h): L1 probe,
+    L2 threshold top-1, gate + miss list, knowledge-base list scan, L4 guard, packed result."""
+    import torch
+
+    L = _lib.load()
+    cfg = router.config
+    kv, sc, akm, kb = router.kv_cache, router.semantic_cache, router.adaptive_memory, router.knowledge_base
+    B, sk, kbi = sp.B, cfg.akm_seed_k, kb.index
+    s = _lib.stream_ptr()
+    dev, i64 = "cuda", torch.int64
+    vec_pos = min(pos.get(L4, 99), pos.get(L5, 99))
+    d = _lib.CascadeSpan()
+    d.B, d.d_vec, d.mode = B, _lib.ptr(Vd), mode
+    rep_d = _lib.h2d(rep.astype(np.uint8))
+    d.d_rep = _lib.ptr(rep_d)
+    if L1 in pos:
+        d.kv, d.d_text, d.d_text_off = _hv(kv._h), _lib.ptr(arena[0]), _lib.ptr(arena[1])
+    sp.recall = _device_recall(router) if L3 in pos else None
+    l3_val = l3_d = None
+    if sp.recall is not None:
+        l3_val, l3_d = sp.recall.gate_device(arena[0], arena[1], B, cfg.recall_threshold)
+        d.d_l3_hit, d.d_l3_val = _lib.ptr(l3_d), _lib.ptr(l3_val)
+    lim_d = None
+    if L2 in pos:
+        lim_d = _lib.h2d(sc_limit, i64)
+        d.sc, d.d_sc_limit, d.sc_threshold = _hv(sc.index.handle), _lib.ptr(lim_d), float(sc.threshold)
+    d.l1_blocks = int(L1 in pos and pos[L1] < vec_pos)
+    d.l2_blocks = int(L2 in pos and pos[L2] < vec_pos)
+    d.l3_blocks = int(L3 in pos and pos[L3] < vec_pos)
+    kb_rows = torch.empty((B, sk), dtype=i64, device=dev)
+    kb_raw = torch.empty((B, sk), dtype=torch.float64, device=dev)
+    kb_rep = torch.empty((B, sk), dtype=torch.float64, device=dev)
+    kb_cnt = torch.empty(B, dtype=torch.int32, device=dev)
+    nlist = torch.empty(1, dtype=torch.int32, device=dev)
+    slot = torch.empty(B, dtype=torch.int32, device=dev)
+    packed = torch.empty(9 * B + 1 + B * sk, dtype=i64, device=dev)
+    d.kb, d.seed_k = _hv(kbi.handle), sk
+    d.nlist_hint = int(min(B, max(1, getattr(router, "_cascade_nlist_hint", B // 2 + 1))))
+    d.d_kb_rows, d.d_kb_raw, d.d_kb_rep = _lib.ptr(kb_rows), _lib.ptr(kb_raw), _lib.ptr(kb_rep)
+    d.d_kb_cnt, d.d_nlist, d.d_slot, d.d_packed = _lib.ptr(kb_cnt), _lib.ptr(nlist), _lib.ptr(slot), _lib.ptr(packed)
+    locks = [sc.index._lock]
+    if L4 in pos:
+        scr = _scratch(router, kbi.dim)
+        prev_b = prev.B if prev is not None else 0
+        guard = scr.store((prev_b + B) * sk)
+        d.probe_l4, d.akm_rows, d.akm_threshold = 1, len(akm.index), float(akm.threshold)
+        d.akm, d.guard, d.d_mark = _hv(akm.index.handle), _hv(guard.handle), _lib.ptr(scr.marks(len(kbi)))
+        if prev is not None:
+            d.d_prev_rows, d.d_prev_cnt, d.d_prev_n = (_lib.ptr(prev.kb_rows_d), _lib.ptr(prev.kb_cnt_d),
+                                                       _lib.ptr(prev.nlist_d))
+            d.prev_B = prev.B
+        locks.append(akm.index._lock)
+        prev_for_scratch = prev_b
+    else:
+        prev_for_scratch = 0
+    locks.append(kbi._lock)  # last: the knowledge base may be shared by concurrent routers
+    need = int(L.pr_cascade_route_scratch(B, sk, prev_for_scratch))
+    buf = getattr(router, "_cascade_route_buf", None)
+    if buf is None or buf.numel() < need:
+        buf = router._cascade_route_buf = torch.empty(need + need // 4, dtype=torch.uint8, device=dev)
+    for lk in locks:
+        lk.acquire()
+    try:
+        _lib.check(L.pr_cascade_route(ctypes.byref(d), _lib.ptr(buf), buf.numel(), s), "cascade_route")
+    finally:
+        for lk in reversed(locks):
+            lk.release()
+    sp.kb_rows_d, sp.kb_cnt_d, sp.nlist_d = kb_rows, kb_cnt, nlist
+    prof.mark("L.route")
     sp.host, sp.event = pinned.ring().d2h(packed)
     prof.mark("L.pack")
     prof.merge_into(router)

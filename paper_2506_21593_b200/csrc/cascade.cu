@@ -173,6 +173,75 @@ __global__ void __launch_bounds__(CG_THREADS) cascade_seeds_kernel(SeedArgs a) {
     if (threadIdx.x == 0) *a.nout = base;
 }
 
+// L4 guard row limit of query j: the deduplicated seeds visible to its list position
+__global__ void guard_limit_kernel(int64_t B, const int32_t *slot, const int64_t *before, int64_t *lim) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < B; j += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t s = slot[j];
+        lim[j] = s >= 0 ? before[s] : 0;
+    }
+}
+
+struct PackArgs {
+    int64_t B;
+    int seed_k;
+    const uint8_t *l1, *l2;
+    const int32_t *slot;
+    const int64_t *sc_rows;  // [B] top-1 rows of L2 (NULL: not probed)
+    const int64_t *kv_val;   // NULL: not probed
+    const int32_t *kb_cnt;
+    const uint8_t *l3;
+    const int64_t *l3_val;
+    const int32_t *nlist;
+    const int64_t *kb_rows;
+    int probe_l4;
+    double thr;
+    const int32_t *a_cnt;  // adaptive memory top-1 (NULL: empty)
+    const double *a_rep;
+    const int32_t *g_cnt;  // guard top-1
+    const double *g_rep;
+    int64_t *out;
+};
+
+// the span's packed read-back, and l4[j] = listed && (AKM top-1 >= thr || guard top-1 >= thr)
+__global__ void cascade_pack_kernel(PackArgs a) {
+    const int64_t B = a.B, nr = B * a.seed_k;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < B + nr; t += (int64_t)gridDim.x * blockDim.x) {
+        if (t >= B) {
+            a.out[9 * B + 1 + (t - B)] = a.kb_rows[t - B];
+            continue;
+        }
+        const int64_t j = t;
+        const int32_t s = a.slot[j];
+        bool l4 = false;
+        if (a.probe_l4 && s >= 0) {
+            l4 = (a.a_cnt && a.a_cnt[j] > 0 && a.a_rep[j] >= a.thr) || (a.g_cnt[j] > 0 && a.g_rep[j] >= a.thr);
+        }
+        int64_t *o = a.out;
+        o[j] = a.l1[j];
+        o[B + j] = a.l2[j];
+        o[2 * B + j] = s;
+        o[3 * B + j] = l4;
+        o[4 * B + j] = a.sc_rows ? a.sc_rows[j] : -1;
+        o[5 * B + j] = a.kv_val ? a.kv_val[j] : -1;
+        o[6 * B + j] = a.kb_cnt[j];
+        o[7 * B + j] = a.l3 ? (int64_t)a.l3[j] : -1;
+        o[8 * B + j] = a.l3_val ? a.l3_val[j] : -1;
+        if (j == 0) o[9 * B] = *a.nlist;
+    }
+}
+
+// carve of the composite call's scratch (256-byte aligned pieces)
+struct RouteCarve {
+    char *p;
+    int64_t used = 0;
+    template <class T>
+    T *take(int64_t n) {
+        T *r = reinterpret_cast<T *>(p ? p + used : nullptr);
+        used += ((int64_t)sizeof(T) * std::max<int64_t>(n, 1) + 255) & ~(int64_t)255;
+        return r;
+    }
+};
+
 }  // namespace pr
 
 using namespace pr;
@@ -224,6 +293,86 @@ int pr_cascade_seeds(const int64_t *d_prev_rows, const int32_t *d_prev_cnt, cons
                d_before};
     ::pr::count_launch();
     cascade_seeds_kernel<<<1, CG_THREADS, 0, as_stream(stream)>>>(a);
+    PR_LAUNCH_CHECK();
+    return PR_OK;
+}
+
+int64_t pr_cascade_route_scratch(int64_t B, int seed_k, int64_t prev_B) {
+    if (B < 0 || seed_k < 1 || prev_B < 0) return -1;
+    RouteCarve c{nullptr};
+    c.take<uint8_t>(B), c.take<int64_t>(B);                    // kv hit / value
+    c.take<uint8_t>(B), c.take<uint8_t>(B), c.take<int32_t>(B);  // l1, l2, list
+    for (int r = 0; r < 3; ++r) c.take<int64_t>(B), c.take<double>(B), c.take<double>(B), c.take<int32_t>(B);
+    c.take<int64_t>((prev_B + B) * seed_k), c.take<int32_t>(1), c.take<int64_t>(B), c.take<int64_t>(B);
+    return c.used;
+}
+
+int pr_cascade_route(const pr_cascade_span *s, void *d_scratch, int64_t scratch_bytes, void *stream) {
+    if (!s || s->B < 0 || s->seed_k < 1 || !s->kb || !s->d_rep || !s->d_kb_rows || !s->d_kb_raw || !s->d_kb_rep ||
+        !s->d_kb_cnt || !s->d_nlist || !s->d_slot || !s->d_packed || (s->B > 0 && !s->d_vec) ||
+        (s->kv && (!s->d_text || !s->d_text_off)) || (s->sc && !s->d_sc_limit) ||
+        (s->probe_l4 && (!s->guard || !s->d_mark || (s->akm_rows > 0 && !s->akm))) ||
+        (s->d_prev_rows && (!s->d_prev_cnt || !s->d_prev_n)))
+        PR_FAIL(PR_ERR_BAD_ARG, "bad cascade_route");
+    const int64_t B = s->B;
+    const int sk = s->seed_k;
+    const int64_t prev_B = s->d_prev_rows ? s->prev_B : 0;
+    const int64_t need = pr_cascade_route_scratch(B, sk, prev_B);
+    if (!d_scratch || scratch_bytes < need) PR_FAIL(PR_ERR_BAD_ARG, "cascade_route scratch too small");
+    cudaStream_t st = as_stream(stream);
+    RouteCarve c{static_cast<char *>(d_scratch)};
+    uint8_t *kv_hit = c.take<uint8_t>(B);
+    int64_t *kv_val = c.take<int64_t>(B);
+    uint8_t *l1 = c.take<uint8_t>(B), *l2 = c.take<uint8_t>(B);
+    int32_t *lst = c.take<int32_t>(B);
+    int64_t *rows[3];
+    double *raw[3], *rep[3];
+    int32_t *cnt[3];  // 0: semantic cache, 1: adaptive memory, 2: guard
+    for (int r = 0; r < 3; ++r)
+        rows[r] = c.take<int64_t>(B), raw[r] = c.take<double>(B), rep[r] = c.take<double>(B), cnt[r] = c.take<int32_t>(B);
+    const int64_t out_max = (prev_B + B) * sk;
+    int64_t *out_rows = c.take<int64_t>(out_max);
+    int32_t *nout = c.take<int32_t>(1);
+    int64_t *before = c.take<int64_t>(B), *lim = c.take<int64_t>(B);
+    int rc;
+    if (B == 0) return PR_OK;
+    // L1, L2: the fast layers' probes
+    if (s->kv && (rc = pr_kv_get_text(s->kv, s->d_text, s->d_text_off, B, kv_val, kv_hit, stream)) != PR_OK) return rc;
+    if (s->sc && (rc = pr_index_search_floor(s->sc, s->d_vec, B, 1, s->mode, s->d_sc_limit, s->sc_threshold, rows[0],
+                                             raw[0], rep[0], cnt[0], stream)) != PR_OK)
+        return rc;
+    // gate + the compacted miss list, then the knowledge-base scan of the listed queries
+    if ((rc = pr_cascade_gate(B, s->kv ? kv_hit : nullptr, s->d_rep, s->sc ? cnt[0] : nullptr, s->sc ? rep[0] : nullptr,
+                              s->sc_threshold, s->d_l3_hit, s->l1_blocks, s->l2_blocks, s->l3_blocks, l1, l2, lst,
+                              s->d_nlist, s->d_slot, stream)) != PR_OK)
+        return rc;
+    const int64_t hint = std::min<int64_t>(B, std::max<int64_t>(1, s->nlist_hint));
+    if ((rc = pr_index_search_list(s->kb, s->d_vec, lst, s->d_nlist, B, hint, sk, s->mode, nullptr, s->d_kb_rows,
+                                   s->d_kb_raw, s->d_kb_rep, s->d_kb_cnt, stream)) != PR_OK)
+        return rc;
+    // L4 guard: the adaptive memory as it is, and the seeds settled before each listed query
+    const bool akm_on = s->probe_l4 && s->akm_rows > 0;
+    if (s->probe_l4) {
+        if (akm_on && (rc = pr_index_search_floor(s->akm, s->d_vec, B, 1, s->mode, nullptr, s->akm_threshold, rows[1],
+                                                  raw[1], rep[1], cnt[1], stream)) != PR_OK)
+            return rc;
+        if ((rc = pr_cascade_seeds(s->d_prev_rows, s->d_prev_cnt, s->d_prev_n, s->d_kb_rows, s->d_kb_cnt, s->d_nlist, sk,
+                                   s->d_mark, out_rows, out_max, nout, before, stream)) != PR_OK)
+            return rc;
+        if ((rc = pr_index_append_from(s->guard, s->kb, out_rows, out_max, stream)) != PR_OK) return rc;
+        ::pr::count_launch();
+        guard_limit_kernel<<<(unsigned)std::min<int64_t>((B + 255) / 256, 148 * 4), 256, 0, st>>>(B, s->d_slot, before,
+                                                                                                 lim);
+        PR_LAUNCH_CHECK();
+        if ((rc = pr_index_search_floor(s->guard, s->d_vec, B, 1, s->mode, lim, s->akm_threshold, rows[2], raw[2],
+                                        rep[2], cnt[2], stream)) != PR_OK)
+            return rc;
+    }
+    PackArgs a{B, sk, l1, l2, s->d_slot, s->sc ? rows[0] : nullptr, s->kv ? kv_val : nullptr, s->d_kb_cnt,
+               s->d_l3_hit, s->d_l3_val, s->d_nlist, s->d_kb_rows, s->probe_l4, s->akm_threshold,
+               akm_on ? cnt[1] : nullptr, akm_on ? rep[1] : nullptr, cnt[2], rep[2], s->d_packed};
+    ::pr::count_launch();
+    cascade_pack_kernel<<<(unsigned)std::min<int64_t>((B * (1 + sk) + 255) / 256, 148 * 8), 256, 0, st>>>(a);
     PR_LAUNCH_CHECK();
     return PR_OK;
 }

@@ -116,3 +116,22 @@ def test_search_modes_match_header():
     modes = dict((m, int(v)) for m, v in re.findall(r"#define (PR_SEARCH_\w+) (\d+)", text))
     assert modes == {k: getattr(_lib, k) for k in modes}
     assert set(modes) == {"PR_SEARCH_AUTO", "PR_SEARCH_EXACT", "PR_SEARCH_TENSOR", "PR_SEARCH_TENSOR_I8"}
+
+
+def test_cascade_span_layout_matches_header(tmp_path):
+    """ctypes CascadeSpan has pr_cascade_span's size and field offsets (gcc on the header)."""
+    import subprocess
+
+    from paper_2506_21593_b200 import _lib
+
+    names = [n for n, _ in _lib.CascadeSpan._fields_]
+    src = tmp_path / "off.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "pentarag.h"\nint main(void){\n'
+                   '  printf("%zu\\n", sizeof(pr_cascade_span));\n'
+                   + "".join(f'  printf("%zu\\n", offsetof(pr_cascade_span, {n}));\n' for n in names) + "  return 0;\n}\n")
+    exe = tmp_path / "off"
+    inc = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include")
+    subprocess.run(["gcc", "-I", inc, str(src), "-o", str(exe)], check=True)
+    got = [int(x) for x in subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split()]
+    want = [ctypes.sizeof(_lib.CascadeSpan)] + [getattr(_lib.CascadeSpan, n).offset for n in names]
+    assert got == want
