@@ -92,17 +92,21 @@ def test_route_batch_matches_reference_simulation(gpu):
             assert [pid for pid, _ in ev.supporting_passages] == [p["id"] for p in r["supporting_passages"]], i
 
 
+@pytest.mark.parametrize("one_call", [True, False], ids=["pr_cascade_route", "python_orchestration"])
 @pytest.mark.parametrize("span", [4096, 29])
 @pytest.mark.parametrize("variant", ["default", "permuted", "disabled", "recall", "device_recall",
                                      "device_recall_first"])
-def test_route_batch_equals_sequential_random(gpu, variant, span):
-    """device_recall*: the batched router's recall table is a DeviceKnowledgeTable (L3
+def test_route_batch_equals_sequential_random(gpu, variant, span, one_call, monkeypatch):
+    """Both device-stage orchestrations of a span (the one-call pr_cascade_route and the
+    same calls issued one by one from Python) against sequential route().
+    device_recall*: the batched router's recall table is a DeviceKnowledgeTable (L3
     decided on the device, pr_recall_gate), the sequential twin's the host
     StubKnowledgeTable with the same adds — low confidences, empty answers, overwrites,
     an inclusive threshold boundary, and L3 probed first."""
     from paper_2506_21593_b200 import (DeviceKnowledgeTable, LayerTag, RouterConfig, StubBackend, StubKnowledgeTable,
-                                       validate_query)
+                                       cascade, validate_query)
 
+    monkeypatch.setattr(cascade, "_ROUTE_C", one_call)
     gold = _golden("simulation.json")
     corpus, questions = gold["corpus"][:150], gold["questions"]
     kw = {}
